@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""bench.py -- one JSON line: the hot path of arXiv 2006.08861 on B200.
+
+A step = one pass of the whole hot path: tau seeding, coarse+fine
+scan with per-CTA top-N, per-rank merge, cross-rank all-gather + merge (N > 1),
+candidate assembly and Algorithm 2 over one batch of query frames.
+
+Workload (default C4, BASELINE.json configs[3]): a 100M-entry synthetic
+city-scale database (seeded generator G), sharded in equal
+contiguous slices over the ranks (strong scaling: total work fixed), 1,024
+query frames at random test positions, N = 15, each frame a bundle (M = 1)
+aggregated by Algorithm 2 (TopC 10, 3 m, 20 %).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--batch B]
+  python bench.py --impl reference ...   # the CPU oracle as the reference arm
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "queries/sec and DB feature-shift comparisons/sec vs HBM roofline, 1/2/4/8 B200"
+QSEED = 4242
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="omniloc", choices=["omniloc", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--batch", type=int, default=0, help="query frames per step (0 = config)")
+    ap.add_argument("--coarse-k", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--small-batch", type=int, default=8, help="extra HBM-regime line (0 = off)")
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def _dist_init(n_gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# =========================================================================== omniloc arm
+def run_omniloc(a):
+    import torch
+    import synthgen
+    import paper_2006_08861_b200 as ol
+
+    rank, world, local = _dist_init(a.gpus)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg = synthgen.CONFIGS[a.config]
+    spec = cfg.spec
+    n_total = spec.n_entries
+    assert len(cfg.subspace_sizes) == 1, "bench drives single-subspace configs (C3/C4/C5)"
+    B = a.batch or cfg.n_queries
+
+    # this rank's shard, generated straight into HBM (counter-based generator)
+    t0 = time.time()
+    b0, cnt = ol.shard_range(n_total, rank, world)
+    F, C = synthgen.db_device(spec, b0, cnt, dev)
+    qpts = synthgen.query_points(spec, QSEED, B)
+    Qd, _ = synthgen.render_device(spec, qpts, dev)
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        group = dist.group.WORLD
+    eng = ol.Engine(local, coarse_k=a.coarse_k, process_group=group)
+    t0 = time.time()
+    eng.upload(F, C, [n_total], spec.grid())
+    torch.cuda.synchronize()
+    upload_s = time.time() - t0
+    if a.no_cpu or rank != 0 or world > 1:
+        del F, C
+        F = C = None
+    torch.cuda.empty_cache()
+
+    params = ol.Params(N=cfg.N)
+    Q3 = Qd.view(B, 1, 64)
+
+    def step():
+        eng.query(Q3, params=params, aggregate=True)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    kernels_per_step = eng.stat("kernels")
+    survivors = eng.stat("survivors")
+    eng.set_option("time_kernels", 1)
+
+    stream = torch.cuda.current_stream(dev)
+    clocks = Clocks(local)
+    _barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    _barrier(world)
+    clk = clocks.stop()
+    ms = _max_over_ranks(e0.elapsed_time(e1), world) / a.steps
+    scan_ns = eng.stat("time_scan_ns") / a.steps
+    seed_ns = eng.stat("time_seed_ns") / a.steps
+    merge_ns = eng.stat("time_merge_ns") / a.steps
+    final_ns = eng.stat("time_final_ns") / a.steps
+    eng.set_option("time_kernels", 0)
+    qps = B / (ms / 1e3)
+    cps = qps * n_total
+
+    # ------------------------------------------------ roofline of the dominant kernel (scan)
+    peaks = _peaks()
+    kc = a.coarse_k if a.coarse_k else 64
+    rows_local = cnt
+    pairs = B * rows_local
+    scan_s = scan_ns / 1e9
+    # FP32 issue ceiling: 148 SMs x 128 lanes x SM clock; 2*kc lane
+    # instructions (FSUB + FFMA per coefficient) per pair are algorithmically required
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    alu_peak = 148 * 128 * sm_max * 1e6 / 1e12          # T lane-instr/s
+    achieved_alu = pairs * 2 * kc / scan_s / 1e12 if scan_s > 0 else None
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    alg_bytes = rows_local * kc * 4 + survivors / max(a.warmup, 1) * 0   # coarse plane once
+    achieved_gbs = alg_bytes / scan_s / 1e9 if scan_s > 0 else None
+    roofline = {"kernel": f"scan_kernel<{kc}>", "bound": "alu", "achieved": achieved_alu,
+                "peak": alu_peak, "unit": "T lane-instr/s",
+                "frac": achieved_alu / alu_peak if achieved_alu else None,
+                "traffic": None,
+                "peak_source": f"148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+                "per_launch": {"pairs": pairs, "lane_instr": pairs * 2 * kc, "algorithmic_bytes": alg_bytes,
+                               "avg_ms": scan_s * 1e3, "hbm_gbs": achieved_gbs,
+                               "hbm_frac": achieved_gbs / hbm_peak if achieved_gbs else None},
+                "step_share": scan_ns / (ms * 1e6)}
+
+    out = {"metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded generator G, DESIGN.md §4)",
+           "config": {"workload": a.config, "db_entries": n_total, "query_frames": B, "M": 1, "N": cfg.N,
+                      "aggregate": True, "top_c": 10, "toler_per": 0.2, "radius_m": 3.0,
+                      "coarse_k": a.coarse_k, "parallelism": f"db-shard{world}",
+                      "l2": "inputs larger than L2 (coarse plane %.1f GB/rank)" % (rows_local * kc * 4 / 1e9)},
+           "comparisons_per_sec": cps,
+           "stages_ms": {"tau_seed": seed_ns / 1e6, "scan": scan_ns / 1e6, "merge": merge_ns / 1e6,
+                         "finalize": final_ns / 1e6},
+           "survivor_frac": survivors / max(pairs, 1),
+           "gpu_launches": kernels_per_step * a.steps,
+           "roofline": roofline, "clocks": clk,
+           "setup_s": {"generate": gen_s, "upload": upload_s}}
+
+    # ------------------------------------------------ small-batch (HBM regime) line
+    if a.small_batch and world == 1:
+        b2 = a.small_batch
+        Qs = Qd[:b2].view(b2, 1, 64)
+        for _ in range(3):
+            eng.query(Qs, params=params, aggregate=True)
+        torch.cuda.synchronize()
+        eng.set_option("time_kernels", 1)
+        reps = 20
+        e0.record(stream)
+        for _ in range(reps):
+            eng.query(Qs, params=params, aggregate=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        sms = e0.elapsed_time(e1) / reps
+        sscan = eng.stat("time_scan_ns") / reps / 1e9
+        for k in ("seed", "merge", "final"):
+            eng.stat(f"time_{k}_ns")
+        eng.set_option("time_kernels", 0)
+        gbs = rows_local * kc * 4 / sscan / 1e9
+        out["small_batch"] = {"query_frames": b2, "ms_per_step": sms, "queries_per_s": b2 / (sms / 1e3),
+                              "scan_ms": sscan * 1e3, "scan_hbm_gbs": gbs, "hbm_peak_gbs": hbm_peak,
+                              "hbm_frac": gbs / hbm_peak}
+
+    # ------------------------------------------------ e2e through the public API, host buffers
+    if not a.no_e2e:
+        Qh = Qd.cpu().pin_memory()
+        Q3h = Qh.view(B, 1, 64)
+        ncand = None
+        eng.query(Q3h.numpy(), params=params, aggregate=True)
+        ncand = eng.candidate_count()
+        res = torch.empty(ncand * 32, dtype=torch.uint8).pin_memory()
+        torch.cuda.synchronize()
+        _barrier(world)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(a.steps):
+            eng.query(Q3h.numpy(), params=params, aggregate=True)   # H2D inside (pinned host)
+            eng.topk_into(res)                                        # D2H of the result
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / a.steps * 1e3
+        ems = _max_over_ranks(max(e0.elapsed_time(e1) / a.steps, wall), world)
+        out["e2e"] = {"value": B / (ems / 1e3), "unit": "queries/s", "ms_per_step": ems,
+                      "h2d_bytes_per_step": B * 64 * 4, "d2h_bytes_per_step": ncand * 32}
+
+    # ------------------------------------------------ CPU oracle baseline (rank 0, N = 1)
+    if rank == 0 and world == 1 and not a.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(F, C, Qd, cfg, n_total)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def cpu_baseline(F, C, Qd, cfg, n_total, budget_s: float = 15.0):
+    """The oracle as it stands, on the host cores, on a bounded sample of the same
+    workload: the first S rows of the DB and the first q query frames; the rate is
+    scaled to queries/s over the full DB (comparisons/s / n_total)."""
+    import oracle
+    S = min(F.shape[0], 2_000_000)
+    Fh = F[:S].cpu().numpy()
+    Ch = C[:S].cpu().numpy()
+    Qh = Qd.cpu().numpy()
+    oracle.lib()
+    t0 = time.perf_counter()
+    oracle.retrieve([S], Fh, Ch, Qh[:1, None, :], cfg.N)
+    t1 = time.perf_counter() - t0
+    nq = int(max(1, min(Qh.shape[0], budget_s / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    oracle.retrieve([S], Fh, Ch, Qh[:nq, None, :], cfg.N)
+    dt = time.perf_counter() - t0
+    cps = nq * S / dt
+    return {"value": cps / n_total, "unit": "queries/s", "cores": _cores(), "kind": "oracle",
+            "comparisons_per_sec": cps,
+            "sample": f"{nq} query frames x first {S:,} of {n_total:,} DB rows (full-DB rate = "
+                      f"comparisons/s / {n_total:,}); acc chain + sort-all top-{cfg.N}, OpenMP over rows",
+            "seconds": dt}
+
+
+# =========================================================================== reference arm
+def run_reference(a):
+    """The CPU oracle as the reference arm (tier rule): the same workload, metric
+    and unit; each step one query frame against a bounded DB sample on the host
+    cores, rate scaled to the full DB."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synthgen
+    import oracle
+    cfg = synthgen.CONFIGS[a.config]
+    spec = cfg.spec
+    n_total = spec.n_entries
+    S = min(n_total, 500_000)
+    F, C = synthgen.db_host(spec, 0, S)
+    B = a.batch or cfg.n_queries
+    Q = synthgen.render_host(spec, synthgen.query_points(spec, QSEED, min(B, a.steps + a.warmup)))["desc"]
+    oracle.lib()
+    for i in range(a.warmup):
+        oracle.retrieve([S], F, C, Q[i % len(Q)][None, None, :], cfg.N)
+    t0 = time.perf_counter()
+    for i in range(a.steps):
+        oracle.retrieve([S], F, C, Q[(a.warmup + i) % len(Q)][None, None, :], cfg.N)
+    dt = (time.perf_counter() - t0) / a.steps
+    qps = (S / dt) / n_total
+    out = {"impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world,
+           "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (seeded generator G, DESIGN.md §4)",
+           "config": {"workload": a.config, "db_entries": n_total, "query_frames": B, "N": cfg.N},
+           "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": _cores(), "kind": "oracle",
+                            "sample": f"1 query frame per step x first {S:,} of {n_total:,} DB rows "
+                                      f"(rate scaled by {S:,}/{n_total:,})"},
+           "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_omniloc(args)

@@ -1,0 +1,253 @@
+/*
+ * omniloc.h -- C-ABI of the B200-native hot path of arXiv 2006.08861
+ * ("GPU-accelerated Hierarchical Panoramic Image Feature Retrieval for Indoor
+ * Localization", Hu, Zhu, Zhang, ICMR'16).
+ *
+ * The library retrieves, for every query frame and every database subspace,
+ * the N database descriptors nearest in Euclidean distance (P:139, P:157,
+ * P:162; Algorithm 1) and fuses each M-frame bundle's candidates into
+ * one floor-plan tile with the 2-D multi-frame aggregation (
+ * Algorithm 2).  Everything runs in hand-written sm_100a kernels; there is no
+ * CPU fallback.  The database may be sharded over ranks (one process per GPU);
+ * ranks then exchange their per-rank top-N (see ol_payload / ol_finalize).
+ *
+ * Citation key: P:n = PAPER.md line n; S:n = SPEC.md line n; R<k> = DESIGN.md
+ * reading k.
+ *
+ * Conventions for every entry point:
+ *   - returns ol_status: OL_OK (0) or a negative OL_ERR_* code; no exception
+ *     ever crosses the ABI.  ol_last_error(ctx) gives a one-line message.
+ *   - "device" pointers are CUDA global-memory pointers on the context's
+ *     device; "host" pointers are ordinary (pageable or pinned) memory.
+ *   - all device work is ordered on the context's stream (borrowed from the
+ *     caller or owned by the library); calls are not thread-safe per context.
+ *
+ * Numeric contract (R3): descriptors and queries are fp32.  For a query q and
+ * a database row f the library computes acc = squared distance by the fixed
+ * chain  acc = +0;  for k = 0..K-1: d = RN32(q_k - f_k); acc = fma32(d, d, acc),
+ * reports dist = RN32(sqrt(acc)), and ranks by (acc, frame index).  Results are
+ * bit-identical to a sequential scan for any launch shape, shard count or
+ * pruning threshold (the coarse/fine hierarchy, R2, is exact).
+ */
+#ifndef OMNILOC_H
+#define OMNILOC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define OL_API __attribute__((visibility("default")))
+#else
+#define OL_API
+#endif
+
+typedef int32_t ol_status;
+
+#define OL_OK                       0
+#define OL_ERR_INVALID_ARGUMENT    (-1)  /* a parameter outside its documented range   */
+#define OL_ERR_DIMENSION_MISMATCH  (-2)  /* K != 64                              */
+#define OL_ERR_NONFINITE           (-3)  /* NaN/Inf in features or frames        */
+#define OL_ERR_OUT_OF_RANGE        (-4)  /* tile outside the grid, m>=n  */
+#define OL_ERR_OOM                 (-5)  /* cudaMalloc failed                           */
+#define OL_ERR_CUDA                (-6)  /* any other CUDA runtime error                */
+#define OL_ERR_NOT_READY           (-7)  /* query before upload / get before query      */
+#define OL_ERR_EMPTY               (-8)  /* a bundle with no candidates, or no
+                                            estimates because aggregation was off      */
+
+#define OL_K 64           /* descriptor length: |DFT| bins 1..64       */
+#define OL_MAX_N 128      /* largest supported top-N per (frame, subspace)          */
+#define OL_MAX_TOP_C 64   /* largest supported TopC (P:197 uses 10)                 */
+#define OL_MAX_M 64       /* largest bundle                                 */
+
+typedef struct ol_ctx ol_ctx;
+
+/* Context configuration (ol_create). */
+typedef struct {
+    int32_t device;        /* CUDA device ordinal                                   */
+    int32_t rank, world;   /* this process's shard index and the shard count (>=1)  */
+    void *cuda_stream;     /* cudaStream_t to borrow (e.g. torch's current stream);
+                              NULL -> the library creates and owns one             */
+    uint32_t K;            /* must be OL_K                                           */
+    uint32_t coarse_k;     /* prefix length of the coarse pass (R2): 0 or 64 = one
+                              pass over full rows; 8, 16 or 32 = exact coarse/fine  */
+} ol_config;
+
+/* Database to upload (ol_upload_db).  The database is n_subspaces independent
+ * subspaces ("each floor data is counted as one subspace"; "the n_i
+ * subspace has |n_i| modeled frames").  This rank holds, for every subspace i,
+ * the contiguous slice of frames [shard_begin[i], shard_begin[i]+shard_count[i])
+ * of its global_sizes[i] frames; features/coords hold those slices back to back
+ * in subspace order.  Frame indices in results are global within a subspace. */
+typedef struct {
+    uint32_t n_subspaces;
+    const uint64_t *global_sizes;  /* [n_subspaces] |n_i| >= 1 (host)               */
+    const uint64_t *shard_begin;   /* [n_subspaces] (host); NULL together with
+                                      shard_count -> the library takes the equal
+                                      contiguous slice r of world (ol_shard_range) */
+    const uint64_t *shard_count;   /* [n_subspaces] (host) or NULL                  */
+    const float *features;         /* [sum shard_count][K] fp32 row-major           */
+    const int32_t *coords;         /* [sum shard_count][2] (x, y) 30 cm tiles*/
+    int32_t grid_w, grid_h;        /* tile grid; every coord must satisfy
+                                      0 <= x < grid_w, 0 <= y < grid_h     */
+    int32_t on_device;             /* 1: features/coords are device pointers         */
+} ol_db_desc;
+
+/* Retrieval + aggregation parameters. */
+typedef struct {
+    uint32_t N;          /* top-N per (query frame, subspace), 1..OL_MAX_N (15) */
+    uint32_t top_c;      /* TopC tiles scanned, 1..OL_MAX_TOP_C (10)             */
+    double toler_per;    /* acceptance fraction in (0, 1] (0.2)                  */
+    double radius_m;     /* tolerance-circle radius in metres, > 0 (3)           */
+    double tile_m;       /* tile edge in metres, > 0 (0.30)                      */
+} ol_params;
+
+/* One retrieval hit. 32 bytes. */
+typedef struct {
+    uint32_t subspace;     /* subspace index i (0-based)                             */
+    uint32_t frame;        /* global frame index t within subspace i (0-based)      */
+    uint32_t bundle;       /* bundle index                                           */
+    uint32_t query_frame;  /* frame index within the bundle, 0..M-1                 */
+    float dist2;           /* acc, the fp32 squared distance (R3)                    */
+    float dist;            /* RN32(sqrt(acc))                                        */
+    int32_t x, y;          /* the frame's floor tile (geo-referenced table)  */
+} ol_candidate;
+
+typedef struct {
+    int32_t x, y;
+    uint32_t count;        /* candidates binned in this tile (Alg. 2 step 2)         */
+    uint32_t circle;       /* candidates within the tolerance circle         */
+} ol_ranked_tile;
+
+/* Aggregated location of one bundle (Algorithm 2). */
+typedef struct {
+    int32_t x, y;              /* FinalPosition tile                                  */
+    double x_m, y_m;           /* tile_m * (x, y): tile centre in metres      */
+    double confidence;         /* circle / total (binary64 division)                  */
+    uint32_t low_confidence;   /* 1 if no ranked tile passed (fallback) */
+    uint32_t n_ranked;         /* min(top_c, distinct tiles)                          */
+    uint32_t total;            /* candidates in the bundle                            */
+    uint32_t _pad;
+    ol_ranked_tile ranked[OL_MAX_TOP_C];
+} ol_estimate;
+
+/* ---- lifetime ------------------------------------------------------------ */
+
+/* Create a context on cfg->device.  Errors: INVALID_ARGUMENT (world < 1, rank
+ * outside [0, world), coarse_k not in {0, 8, 16, 32, 64}), DIMENSION_MISMATCH
+ * (K != 64), CUDA.  On error *out is NULL and ol_last_error(NULL) explains. */
+OL_API ol_status ol_create(const ol_config *cfg, ol_ctx **out);
+
+/* Free all device/host resources of the context (NULL is a no-op). */
+OL_API void ol_destroy(ol_ctx *ctx);
+
+/* Replace the stream all later calls are ordered on (NULL -> a library-owned
+ * stream).  The previous owned stream, if any, is synchronised and destroyed. */
+OL_API ol_status ol_set_stream(ol_ctx *ctx, void *cuda_stream);
+
+/* Last error message of ctx (or of the calling thread if ctx is NULL). Never NULL. */
+OL_API const char *ol_last_error(const ol_ctx *ctx);
+
+/* The contiguous slice [begin, begin+count) of a subspace of `global_size`
+ * frames owned by `rank` of `world`: begin = floor(rank*size/world).  Pure host
+ * function.  Errors: INVALID_ARGUMENT (world < 1 or rank >= world). */
+OL_API ol_status ol_shard_range(uint64_t global_size, int32_t rank, int32_t world, uint64_t *begin,
+                         uint64_t *count);
+
+/* ---- database ------------------------------------------------------------ */
+
+/* Copy (and re-lay out) the database into device memory owned by the context;
+ * replaces any previous database.  Synchronous.  Errors: INVALID_ARGUMENT
+ * (n_subspaces = 0, a size 0, shard outside its subspace, grid <= 0),
+ * NONFINITE, OUT_OF_RANGE (coord outside the grid), OOM, CUDA. */
+OL_API ol_status ol_upload_db(ol_ctx *ctx, const ol_db_desc *db);
+
+/* ---- query --------------------------------------------------------------- */
+
+/* Retrieve the top-N of every (bundle, frame, subspace) (Alg. 1) and,
+ * if `aggregate`, fuse every bundle (Alg. 2).  frames: [n_bundles][M][K] fp32,
+ * host or device (on_device).  Asynchronous on the context stream: a host
+ * `frames` buffer is read before return; results stay valid until the next
+ * ol_query.  With world > 1 this call produces only this rank's top-N (the
+ * "payload"); the caller all-gathers payloads and calls ol_finalize.
+ * Errors: NOT_READY (no database), INVALID_ARGUMENT (n_bundles = 0, M even or
+ * 0 or > OL_MAX_M, N = 0 or > OL_MAX_N, top_c = 0 or > OL_MAX_TOP_C,
+ * toler_per outside (0, 1], radius_m <= 0, tile_m <= 0, a bundle with more than
+ * 8192 candidates when aggregating), NONFINITE (host frames; device frames
+ * are checked on the device and reported by the next ol_get_*), OOM, CUDA. */
+OL_API ol_status ol_query(ol_ctx *ctx, uint32_t n_bundles, uint32_t M, const float *frames,
+                   int32_t on_device, const ol_params *p, int32_t aggregate);
+
+/* This rank's per-(frame, subspace) top-N as 16-byte records
+ * {u32 acc_bits, u32 frame, i32 x, i32 y} in [frame][subspace][N] order, padded
+ * with acc_bits = frame = 0xFFFFFFFF.  *dev_ptr is owned by the context. */
+OL_API ol_status ol_payload(ol_ctx *ctx, const void **dev_ptr, uint64_t *bytes);
+
+/* Copy this rank's payload (ol_payload) to `dst` (device memory, at least the
+ * payload's bytes), stream-ordered; e.g. into a buffer the caller all-gathers. */
+OL_API ol_status ol_payload_copy(ol_ctx *ctx, void *dst);
+
+/* Merge `world` payloads gathered back to back at `gathered` (device, world *
+ * payload bytes, rank order) into the global top-N, then build candidates and
+ * (if requested in ol_query) estimates.  Identical on every rank.  Errors:
+ * NOT_READY (no preceding ol_query), INVALID_ARGUMENT (world mismatch), CUDA. */
+OL_API ol_status ol_finalize(ol_ctx *ctx, const void *gathered, int32_t world);
+
+/* ---- results ------------------------------------------------------------- */
+
+/* Number of candidates of the last query: n_bundles * M * sum_i min(N, |n_i|). */
+OL_API ol_status ol_candidate_count(const ol_ctx *ctx, uint64_t *count);
+
+/* Copy the candidates to a caller-owned host buffer in (bundle, frame, subspace,
+ * rank) order.  Synchronises the stream.  Errors: INVALID_ARGUMENT
+ * (capacity too small), NOT_READY, NONFINITE (device frames held NaN/Inf), CUDA. */
+OL_API ol_status ol_get_topk(ol_ctx *ctx, ol_candidate *out, uint64_t capacity, uint64_t *written);
+
+/* Device pointer to the same candidate array (owned by the context; valid until
+ * the next ol_query).  Does not synchronise. */
+OL_API ol_status ol_topk_device(ol_ctx *ctx, const ol_candidate **dev_ptr, uint64_t *count);
+
+/* Copy the n_bundles estimates to a caller-owned host buffer.  Synchronises.
+ * Errors: EMPTY (aggregation was not requested), INVALID_ARGUMENT (capacity),
+ * NOT_READY, CUDA. */
+OL_API ol_status ol_get_estimates(ol_ctx *ctx, ol_estimate *out, uint32_t capacity);
+
+/* ---- standalone pieces --------------------------------------------------- */
+
+/* Algorithm 2 alone on caller-provided candidate tiles: bundle b owns
+ * xy[offsets[b] .. offsets[b+1]) (pairs of int32).  offsets/xy host or device
+ * (on_device); out is a host array of n_bundles.  Synchronous.  Errors: EMPTY
+ * (a bundle with zero candidates), INVALID_ARGUMENT (parameters as in
+ * ol_query; a bundle with more than 8192 candidates), CUDA. */
+OL_API ol_status ol_aggregate(ol_ctx *ctx, uint32_t n_bundles, const uint32_t *offsets,
+                       const int32_t *xy, int32_t on_device, const ol_params *p,
+                       ol_estimate *out);
+
+/* selectNearbyFrames (Alg. 1 step 2; window shape P:139): the window
+ * of frames around m, of length min(M, n_frames), shifted to stay inside the
+ * sequence.  Pure host function.  Errors: INVALID_ARGUMENT (M even or 0),
+ * OUT_OF_RANGE (m >= n_frames). */
+OL_API ol_status ol_select_window(uint32_t n_frames, uint32_t m, uint32_t M, uint32_t *first,
+                           uint32_t *len);
+
+/* ---- tuning / introspection (never changes results) ---------------------- */
+
+/* Launch-shape knobs for schedule-independence tests and tuning:
+ *   "chunk"      entries per work item (0 = automatic)
+ *   "qtile"      query frames per CTA tile (0 = automatic)
+ *   "tau_seed"   1 (default) / 0: seed pruning thresholds from a sample
+ *   "ctas"       cap on resident CTAs (0 = automatic)
+ * Errors: INVALID_ARGUMENT (unknown key or value). */
+OL_API ol_status ol_set_option(ol_ctx *ctx, const char *key, int64_t value);
+
+/* Read statistics of the last query: "survivors" (pairs that passed the coarse
+ * bound), "pairs" (pairs scanned), "kernels" (kernel launches of the last
+ * ol_query + ol_finalize).  Synchronises. */
+OL_API ol_status ol_get_stat(ol_ctx *ctx, const char *key, int64_t *value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OMNILOC_H */

@@ -1,0 +1,343 @@
+"""omniloc -- B200-native hot path of arXiv 2006.08861 (Hu, Zhu, Zhang, ICMR'16).
+
+Thin Python binding over the C-ABI in ``include/omniloc.h`` (``libomniloc.so``):
+argument marshalling only.  Every step of the path -- distance chain, coarse
+pruning, fine completion, top-N selection, merges and Algorithm 2 -- runs in the
+library's sm_100a kernels.  PyTorch provides device memory, the CUDA stream and
+(for sharded databases) the ``torch.distributed`` all-gather of the per-rank
+top-N payloads.  There is no CPU fallback: if the library or a GPU is missing,
+``Engine`` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = ["Engine", "OmnilocError", "lib", "select_window", "shard_range", "CANDIDATE_DTYPE",
+           "ESTIMATE_DTYPE", "PAYLOAD_RECORD_BYTES", "build"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libomniloc.so")
+
+OL_OK, OL_ERR_INVALID_ARGUMENT, OL_ERR_DIMENSION_MISMATCH, OL_ERR_NONFINITE = 0, -1, -2, -3
+OL_ERR_OUT_OF_RANGE, OL_ERR_OOM, OL_ERR_CUDA, OL_ERR_NOT_READY, OL_ERR_EMPTY = -4, -5, -6, -7, -8
+K = 64
+MAX_TOP_C = 64
+PAYLOAD_RECORD_BYTES = 16
+
+_NAMES = {0: "OK", -1: "INVALID_ARGUMENT", -2: "DIMENSION_MISMATCH", -3: "NONFINITE",
+          -4: "OUT_OF_RANGE", -5: "OOM", -6: "CUDA", -7: "NOT_READY", -8: "EMPTY"}
+
+
+class OmnilocError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"OL_ERR_{_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class ol_config(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("cuda_stream", ctypes.c_void_p), ("K", ctypes.c_uint32), ("coarse_k", ctypes.c_uint32)]
+
+
+class ol_db_desc(ctypes.Structure):
+    _fields_ = [("n_subspaces", ctypes.c_uint32), ("global_sizes", ctypes.c_void_p),
+                ("shard_begin", ctypes.c_void_p), ("shard_count", ctypes.c_void_p),
+                ("features", ctypes.c_void_p), ("coords", ctypes.c_void_p),
+                ("grid_w", ctypes.c_int32), ("grid_h", ctypes.c_int32), ("on_device", ctypes.c_int32)]
+
+
+class ol_params(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_uint32), ("top_c", ctypes.c_uint32), ("toler_per", ctypes.c_double),
+                ("radius_m", ctypes.c_double), ("tile_m", ctypes.c_double)]
+
+
+CANDIDATE_DTYPE = np.dtype([("subspace", np.uint32), ("frame", np.uint32), ("bundle", np.uint32),
+                            ("query_frame", np.uint32), ("dist2", np.float32), ("dist", np.float32),
+                            ("x", np.int32), ("y", np.int32)])
+RANKED_DTYPE = np.dtype([("x", np.int32), ("y", np.int32), ("count", np.uint32), ("circle", np.uint32)])
+ESTIMATE_DTYPE = np.dtype([("x", np.int32), ("y", np.int32), ("x_m", np.float64), ("y_m", np.float64),
+                           ("confidence", np.float64), ("low_confidence", np.uint32),
+                           ("n_ranked", np.uint32), ("total", np.uint32), ("_pad", np.uint32),
+                           ("ranked", RANKED_DTYPE, (MAX_TOP_C,))])
+assert CANDIDATE_DTYPE.itemsize == 32 and ESTIMATE_DTYPE.itemsize == 48 + 16 * MAX_TOP_C
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    from . import _build
+    return _build.build(force=force)
+
+
+def lib():
+    """Load libomniloc.so (raises if it was never built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run paper_2006_08861_b200.build() "
+                              "(or __graft_entry__.build()) first; there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        P, u32, u64, i32, i64 = (ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32,
+                                 ctypes.c_int64)
+        sig = {
+            "ol_create": ([ctypes.POINTER(ol_config), ctypes.POINTER(P)], i32),
+            "ol_destroy": ([P], None),
+            "ol_last_error": ([P], ctypes.c_char_p),
+            "ol_set_stream": ([P, P], i32),
+            "ol_shard_range": ([u64, i32, i32, ctypes.POINTER(u64), ctypes.POINTER(u64)], i32),
+            "ol_upload_db": ([P, ctypes.POINTER(ol_db_desc)], i32),
+            "ol_query": ([P, u32, u32, P, i32, ctypes.POINTER(ol_params), i32], i32),
+            "ol_payload": ([P, ctypes.POINTER(P), ctypes.POINTER(u64)], i32),
+            "ol_payload_copy": ([P, P], i32),
+            "ol_finalize": ([P, P, i32], i32),
+            "ol_candidate_count": ([P, ctypes.POINTER(u64)], i32),
+            "ol_get_topk": ([P, P, u64, ctypes.POINTER(u64)], i32),
+            "ol_topk_device": ([P, ctypes.POINTER(P), ctypes.POINTER(u64)], i32),
+            "ol_get_estimates": ([P, P, u32], i32),
+            "ol_aggregate": ([P, u32, P, P, i32, ctypes.POINTER(ol_params), P], i32),
+            "ol_select_window": ([u32, u32, u32, ctypes.POINTER(u32), ctypes.POINTER(u32)], i32),
+            "ol_set_option": ([P, ctypes.c_char_p, i64], i32),
+            "ol_get_stat": ([P, ctypes.c_char_p, ctypes.POINTER(i64)], i32),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(status: int, ctx=None):
+    if status != OL_OK:
+        raise OmnilocError(status, lib().ol_last_error(ctx).decode())
+
+
+def select_window(n_frames: int, m: int, M: int):
+    """selectNearbyFrames (Alg. 1): -> (first, length)."""
+    f = ctypes.c_uint32(); n = ctypes.c_uint32()
+    _check(lib().ol_select_window(n_frames, m, M, ctypes.byref(f), ctypes.byref(n)))
+    return f.value, n.value
+
+
+def shard_range(n: int, rank: int, world: int):
+    b = ctypes.c_uint64(); c = ctypes.c_uint64()
+    _check(lib().ol_shard_range(n, rank, world, ctypes.byref(b), ctypes.byref(c)))
+    return b.value, c.value
+
+
+def _ptr(x):
+    """(pointer, on_device) of a contiguous torch tensor or numpy array."""
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"]
+        return x.ctypes.data, 0
+    assert x.is_contiguous()
+    return x.data_ptr(), int(x.is_cuda)
+
+
+@dataclass
+class Params:
+    N: int = 15
+    top_c: int = 10
+    toler_per: float = 0.2
+    radius_m: float = 3.0
+    tile_m: float = 0.3
+
+    def c(self) -> ol_params:
+        return ol_params(self.N, self.top_c, self.toler_per, self.radius_m, self.tile_m)
+
+
+class Engine:
+    """One context on one GPU: upload a (sharded) feature database, query bundles.
+
+    ``process_group``: a torch.distributed group whose ranks each hold one shard;
+    the per-rank top-N payloads are all-gathered through it (NCCL on GPUs).
+    """
+
+    def __init__(self, device: int = 0, coarse_k: int = 16, process_group=None, rank: int | None = None,
+                 world: int | None = None, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("omniloc needs a CUDA device (no CPU fallback)")
+        self._torch = torch
+        self.device = torch.device("cuda", device)
+        self.group = process_group
+        if process_group is not None:
+            import torch.distributed as dist
+            rank = dist.get_rank(process_group)
+            world = dist.get_world_size(process_group)
+        self.rank = 0 if rank is None else rank
+        self.world = 1 if world is None else world
+        self._stream = stream
+        L = lib()
+        cfg = ol_config(device, self.rank, self.world, self._stream_ptr(), K, coarse_k)
+        h = ctypes.c_void_p()
+        _check(L.ol_create(ctypes.byref(cfg), ctypes.byref(h)))
+        self._h = h
+        self.params = Params()
+        self._gather_buf = None
+        self._payload_buf = None
+
+    def _stream_ptr(self):
+        if self._stream is not None:
+            return self._stream.cuda_stream
+        return self._torch.cuda.current_stream(self.device).cuda_stream
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ol_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, status):
+        if status != OL_OK:
+            raise OmnilocError(status, lib().ol_last_error(self._h).decode())
+
+    def sync_stream(self):
+        self._ck(lib().ol_set_stream(self._h, ctypes.c_void_p(self._stream_ptr())))
+
+    # ---------------------------------------------------------------- database
+    def upload(self, features, coords, subspace_sizes, grid, shard_begin=None, shard_count=None):
+        """features [rows][64] f32, coords [rows][2] i32 (this rank's rows, subspace order);
+        subspace_sizes: global |n_i|; grid: (grid_w, grid_h)."""
+        self.sync_stream()
+        sizes = np.ascontiguousarray(subspace_sizes, np.uint64)
+        fp, fdev = _ptr(features)
+        cp, cdev = _ptr(coords)
+        if fdev != cdev:
+            raise ValueError("features and coords must both be host or both device")
+        sb = sc = None
+        if shard_begin is not None:
+            sb = np.ascontiguousarray(shard_begin, np.uint64)
+            sc = np.ascontiguousarray(shard_count, np.uint64)
+        desc = ol_db_desc(len(sizes), sizes.ctypes.data, sb.ctypes.data if sb is not None else None,
+                          sc.ctypes.data if sc is not None else None, fp, cp, int(grid[0]), int(grid[1]),
+                          fdev)
+        self._ck(lib().ol_upload_db(self._h, ctypes.byref(desc)))
+        self.sizes = sizes
+
+    # ---------------------------------------------------------------- query
+    def query(self, frames, N: int | None = None, aggregate: bool = True, params: Params | None = None,
+              M: int | None = None, exchange: bool = True):
+        """frames [B][M][64] (or [B][64] for M=1) f32, host (numpy / pinned torch) or device.
+        Runs Alg. 1 + Alg. 2; results via topk() / estimates().  With world > 1 and
+        ``exchange`` the per-rank payloads are all-gathered over the process group
+        and merged; with ``exchange=False`` the caller gathers (payload() /
+        finalize_gathered())."""
+        p = params or self.params
+        if N is not None:
+            p = Params(N, p.top_c, p.toler_per, p.radius_m, p.tile_m)
+        shape = tuple(frames.shape)
+        if len(shape) == 2:
+            B, Mq = shape[0], 1
+        else:
+            B, Mq = shape[0], shape[1]
+        if M is not None:
+            Mq = M
+        self.sync_stream()
+        fp, fdev = _ptr(frames)
+        pc = p.c()
+        self._ck(lib().ol_query(self._h, B, Mq, ctypes.c_void_p(fp), fdev, ctypes.byref(pc),
+                                1 if aggregate else 0))
+        if self.world > 1 and exchange:
+            self._exchange_and_finalize()
+        self._last = (B, Mq, p, aggregate)
+
+    def _exchange_and_finalize(self):
+        """Cross-GPU merge: all-gather the per-rank top-N payloads
+        through torch.distributed (NCCL over NVLink on GPUs), merge in-library."""
+        torch = self._torch
+        ptr = ctypes.c_void_p(); nbytes = ctypes.c_uint64()
+        self._ck(lib().ol_payload(self._h, ctypes.byref(ptr), ctypes.byref(nbytes)))
+        n = nbytes.value
+        if self._payload_buf is None or self._payload_buf.numel() < n:
+            self._payload_buf = torch.empty(n, dtype=torch.uint8, device=self.device)
+            self._gather_buf = torch.empty(n * self.world, dtype=torch.uint8, device=self.device)
+        src = self._payload_buf[:n]
+        dst = self._gather_buf[: n * self.world]
+        self._ck(lib().ol_payload_copy(self._h, ctypes.c_void_p(src.data_ptr())))
+        exchange_payloads(src, dst, self.group)
+        self._ck(lib().ol_finalize(self._h, ctypes.c_void_p(dst.data_ptr()), self.world))
+
+    def finalize_gathered(self, gathered):
+        """Finalize with payloads gathered by the caller (device tensor, rank order)."""
+        self._ck(lib().ol_finalize(self._h, ctypes.c_void_p(gathered.data_ptr()), self.world))
+
+    def payload(self):
+        """This rank's payload as a new device uint8 tensor."""
+        ptr = ctypes.c_void_p(); nbytes = ctypes.c_uint64()
+        self._ck(lib().ol_payload(self._h, ctypes.byref(ptr), ctypes.byref(nbytes)))
+        t = self._torch.empty(nbytes.value, dtype=self._torch.uint8, device=self.device)
+        self._ck(lib().ol_payload_copy(self._h, ctypes.c_void_p(t.data_ptr())))
+        return t
+
+    # ---------------------------------------------------------------- results
+    def candidate_count(self) -> int:
+        n = ctypes.c_uint64()
+        self._ck(lib().ol_candidate_count(self._h, ctypes.byref(n)))
+        return n.value
+
+    def topk(self, out: np.ndarray | None = None) -> np.ndarray:
+        n = self.candidate_count()
+        if out is None:
+            out = np.empty(n, CANDIDATE_DTYPE)
+        w = ctypes.c_uint64()
+        self._ck(lib().ol_get_topk(self._h, ctypes.c_void_p(out.ctypes.data), out.shape[0], ctypes.byref(w)))
+        return out[: w.value]
+
+    def topk_into(self, pinned) -> int:
+        """D2H of the candidates into a (pinned) torch uint8 host tensor; returns bytes."""
+        n = self.candidate_count()
+        w = ctypes.c_uint64()
+        self._ck(lib().ol_get_topk(self._h, ctypes.c_void_p(pinned.data_ptr()),
+                                   pinned.numel() // CANDIDATE_DTYPE.itemsize, ctypes.byref(w)))
+        return n * CANDIDATE_DTYPE.itemsize
+
+    def topk_device(self):
+        """(device pointer, count) of the candidate array (owned by the engine)."""
+        p = ctypes.c_void_p(); n = ctypes.c_uint64()
+        self._ck(lib().ol_topk_device(self._h, ctypes.byref(p), ctypes.byref(n)))
+        return p.value, n.value
+
+    def estimates(self) -> np.ndarray:
+        B = self._last[0]
+        out = np.empty(B, ESTIMATE_DTYPE)
+        self._ck(lib().ol_get_estimates(self._h, ctypes.c_void_p(out.ctypes.data), B))
+        return out
+
+    def aggregate(self, xy, offsets, params: Params | None = None) -> np.ndarray:
+        """Algorithm 2 alone: bundle b owns xy[offsets[b]:offsets[b+1]]."""
+        p = (params or self.params).c()
+        xy = np.ascontiguousarray(xy, np.int32).reshape(-1, 2)
+        off = np.ascontiguousarray(offsets, np.uint32)
+        nb = off.shape[0] - 1
+        out = np.empty(nb, ESTIMATE_DTYPE)
+        self.sync_stream()
+        self._ck(lib().ol_aggregate(self._h, nb, ctypes.c_void_p(off.ctypes.data),
+                                    ctypes.c_void_p(xy.ctypes.data), 0, ctypes.byref(p),
+                                    ctypes.c_void_p(out.ctypes.data)))
+        return out
+
+    def set_option(self, key: str, value: int):
+        self._ck(lib().ol_set_option(self._h, key.encode(), int(value)))
+
+    def stat(self, key: str) -> int:
+        v = ctypes.c_int64()
+        self._ck(lib().ol_get_stat(self._h, key.encode(), ctypes.byref(v)))
+        return v.value
+
+
+def exchange_payloads(src, dst, group=None):
+    """All-gather equal-size uint8 payload tensors in rank order (NCCL on CUDA
+    tensors, gloo on CPU tensors).  The only collective of the path (§8e)."""
+    import torch.distributed as dist
+    dist.all_gather_into_tensor(dst, src, group=group)
+    return dst

@@ -1,0 +1,187 @@
+// aggregate.cu -- Algorithm 2, 2-D multi-frame candidate aggregation
+// on sm_100a (kernel NK5).  One CTA per bundle, all in shared memory:
+//   1. 2-D binning (Alg. 2 steps 2-3): sort the candidates' tile keys (y, x);
+//      runs of equal keys are the non-zero tiles of locationDistriArray and
+//      their lengths the counts (a sparse histogram: only occupied tiles exist);
+//   2. rankLocationDistribution / findTopDensityArea (steps 5-6): sort the
+//      occupied tiles by (count desc, y asc, x asc) (R7) and keep TopC;
+//   3. the tolerance circle of each ranked tile (step 7-8): the sum of
+//      the counts of the occupied tiles whose centre lies within radius_m
+//      (dx^2 + dy^2 <= (radius_m / tile_m)^2, inclusive, R11);
+//   4. the first ranked tile whose circle > toler_per * total (strict)
+//      wins; if none does, the ranked tile with the largest circle (earliest
+//      rank on ties) flagged low-confidence (R12).
+#include "ol_internal.h"
+
+namespace ol {
+
+constexpr int kAggThreads = 512;
+
+__device__ void bitonic_sort_u64(u64 *v, uint32_t P) {
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t t = threadIdx.x; t < P; t += blockDim.x) {
+                uint32_t o = t ^ j;
+                if (o > t) {
+                    bool up = (t & k) == 0;
+                    u64 x = v[t], y = v[o];
+                    if ((x > y) == up) { v[t] = y; v[o] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// exclusive block scan of one value per thread; returns the thread's offset, *total
+__device__ uint32_t block_excl_scan(uint32_t v, uint32_t *scratch, uint32_t *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) scratch[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < (int)(blockDim.x / 32) ? scratch[lane] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        scratch[lane] = w;  // inclusive prefix over warps
+    }
+    __syncthreads();
+    uint32_t res = x - v + (warp > 0 ? scratch[warp - 1] : 0);
+    *total = scratch[blockDim.x / 32 - 1];
+    __syncthreads();
+    return res;
+}
+
+__global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ uint32_t scratch[32];
+    __shared__ uint32_t circ[OL_MAX_TOP_C];
+    __shared__ uint32_t red[kAggThreads / 32];
+    const uint32_t b = blockIdx.x;
+    uint32_t begin, total;
+    if (a.cand) { begin = b * a.per_bundle; total = a.per_bundle; }
+    else { begin = a.offsets[b]; total = a.offsets[b + 1] - begin; }
+    ol_estimate *out = a.out + b;
+    if (total == 0 || total > (uint32_t)kAggMax) {
+        if (threadIdx.x == 0) { *a.err_empty = total == 0 ? 1 : 2; out->total = total; }
+        return;
+    }
+    uint32_t P = 1;
+    while (P < total) P <<= 1;
+    u64 *keys = reinterpret_cast<u64 *>(smem);          // [P]  sorted candidate tiles
+    u64 *dtile = keys + kAggMax;                        // [P]  occupied tiles
+    uint32_t *dcount = reinterpret_cast<uint32_t *>(dtile + kAggMax);  // [P]
+    for (uint32_t t = threadIdx.x; t < P; t += blockDim.x) {
+        u64 k = kPadKey;
+        if (t < total) {
+            int32_t x, y;
+            if (a.cand) { x = a.cand[begin + t].x; y = a.cand[begin + t].y; }
+            else { x = a.xy[2 * (size_t)(begin + t)]; y = a.xy[2 * (size_t)(begin + t) + 1]; }
+            k = ((u64)(uint32_t)y << 32) | (uint32_t)x;
+        }
+        keys[t] = k;
+    }
+    __syncthreads();
+    // step 1: binning by sort
+    bitonic_sort_u64(keys, P);
+    const uint32_t per = (P + blockDim.x - 1) / blockDim.x;
+    const uint32_t lo = threadIdx.x * per, hi = min(lo + per, total);
+    uint32_t mine = 0;
+    for (uint32_t t = lo; t < hi; ++t) mine += (t == 0 || keys[t] != keys[t - 1]);
+    uint32_t nd;
+    uint32_t pos = block_excl_scan(mine, scratch, &nd);
+    uint32_t *first = reinterpret_cast<uint32_t *>(dcount);  // temporarily: run starts
+    for (uint32_t t = lo; t < hi; ++t)
+        if (t == 0 || keys[t] != keys[t - 1]) { dtile[pos] = keys[t]; first[pos] = t; ++pos; }
+    __syncthreads();
+    uint32_t cnt[16];  // per <= kAggMax / kAggThreads
+    const uint32_t dper = (nd + blockDim.x - 1) / blockDim.x;
+    for (uint32_t j = 0; j < dper; ++j) {
+        uint32_t d = threadIdx.x * dper + j;
+        cnt[j] = d < nd ? ((d + 1 < nd ? first[d + 1] : total) - first[d]) : 0;
+    }
+    __syncthreads();
+    for (uint32_t j = 0; j < dper; ++j) {
+        uint32_t d = threadIdx.x * dper + j;
+        if (d < nd) dcount[d] = cnt[j];
+    }
+    __syncthreads();
+    // step 2: rank occupied tiles (count desc; ties by (y, x) = position in dtile)
+    uint32_t PD = 1;
+    while (PD < nd) PD <<= 1;
+    for (uint32_t d = threadIdx.x; d < PD; d += blockDim.x)
+        keys[d] = d < nd ? (((u64)(0xFFFFFFFFu - dcount[d]) << 32) | d) : kPadKey;
+    __syncthreads();
+    bitonic_sort_u64(keys, PD);
+    const uint32_t nr = min(a.top_c, nd);
+    // step 3: tolerance circles
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint32_t r = 0; r < nr; ++r) {
+        const u64 c = dtile[(uint32_t)keys[r]];
+        const int64_t cx = (int32_t)(uint32_t)c, cy = (int32_t)(uint32_t)(c >> 32);
+        uint32_t s = 0;
+        for (uint32_t d = threadIdx.x; d < nd; d += blockDim.x) {
+            const u64 t = dtile[d];
+            const int64_t dx = (int64_t)(int32_t)(uint32_t)t - cx;
+            const int64_t dy = (int64_t)(int32_t)(uint32_t)(t >> 32) - cy;
+            if ((double)(dx * dx + dy * dy) <= a.r2) s += dcount[d];
+        }
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) red[warp] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+            for (int w = 0; w < kAggThreads / 32; ++w) tot += red[w];
+            circ[r] = tot;
+        }
+        __syncthreads();
+    }
+    // step 4: decision
+    if (threadIdx.x == 0) {
+        const double thresh = a.toler_per * (double)total;
+        int chosen = -1, best = 0;
+        for (uint32_t r = 0; r < nr; ++r) {
+            if (chosen < 0 && (double)circ[r] > thresh) chosen = (int)r;
+            if (circ[r] > circ[best]) best = (int)r;
+        }
+        uint32_t low = 0;
+        if (chosen < 0) { chosen = best; low = 1; }
+        const u64 c = dtile[(uint32_t)keys[chosen]];
+        out->x = (int32_t)(uint32_t)c;
+        out->y = (int32_t)(uint32_t)(c >> 32);
+        out->x_m = a.tile_m * (double)out->x;
+        out->y_m = a.tile_m * (double)out->y;
+        out->confidence = (double)circ[chosen] / (double)total;
+        out->low_confidence = low;
+        out->n_ranked = nr;
+        out->total = total;
+        out->_pad = 0;
+    }
+    for (uint32_t r = threadIdx.x; r < OL_MAX_TOP_C; r += blockDim.x) {
+        ol_ranked_tile rt = {0, 0, 0, 0};
+        if (r < nr) {
+            const uint32_t d = (uint32_t)keys[r];
+            const u64 c = dtile[d];
+            rt.x = (int32_t)(uint32_t)c;
+            rt.y = (int32_t)(uint32_t)(c >> 32);
+            rt.count = dcount[d];
+            rt.circle = circ[r];
+        }
+        out->ranked[r] = rt;
+    }
+}
+
+cudaError_t launch_aggregate(const AggArgs &a, cudaStream_t s) {
+    const size_t smem = sizeof(u64) * kAggMax * 2 + sizeof(uint32_t) * kAggMax;
+    cudaFuncSetAttribute(aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    aggregate_kernel<<<a.n_bundles, kAggThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace ol

@@ -1,0 +1,143 @@
+// merge.cu -- the top-N merges (NK4) and candidate assembly.
+//
+//  merge_chunks: the N smallest keys of every (query frame, subspace) over the
+//    per-work-item lists the scan wrote; attaches the geo-referenced tile of
+//    each winner ("mapped to their actual floor plan 2D coordinates by
+//    checking the geo-referenced mapping table") -> this rank's payload.
+//  merge_ranks: the N smallest of the W gathered payloads (cross-GPU merge).
+//  candidates: records -> ol_candidate rows in (bundle, frame, subspace, rank)
+//    order, dist = RN32(sqrt(acc)) (R3).
+// Keys (acc bits << 32 | frame) are unique within a subspace apart from the
+// all-ones pad, so "N rounds of extract-the-minimum" is the exact top-N.
+#include "ol_internal.h"
+
+namespace ol {
+
+__device__ __forceinline__ u64 warp_min_u64(u64 v) {
+    for (int o = 16; o; o >>= 1) {
+        u64 w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+constexpr int kMergeThreads = 256;
+
+// One warp per (query, subspace).
+__global__ void __launch_bounds__(kMergeThreads) merge_chunks_kernel(MergeArgs a) {
+    const uint32_t gw = (blockIdx.x * kMergeThreads + threadIdx.x) / 32;
+    const int lane = threadIdx.x & 31;
+    if (gw >= a.nq * a.n_sub) return;
+    const uint32_t q = gw / a.n_sub, i = gw % a.n_sub;
+    const SubInfo si = a.subs[i];
+    const uint32_t nk = (si.chunk_end - si.chunk_begin) * a.N;
+    const u64 *src = a.partial + ((size_t)q * a.n_items + si.chunk_begin) * a.N;
+    uint4 *dst = a.records + ((size_t)q * a.n_sub + i) * a.N;
+    u64 last = 0;
+    bool have_last = false;
+    for (uint32_t r = 0; r < a.N; ++r) {
+        u64 best = kPadKey;
+        for (uint32_t t = lane; t < nk; t += 32) {
+            u64 v = src[t];
+            if ((!have_last || v > last) && v < best) best = v;
+        }
+        best = warp_min_u64(best);
+        if (lane == 0) {
+            uint4 rec;
+            if (best == kPadKey) {
+                rec = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u);
+            } else {
+                const uint32_t frame = (uint32_t)best;
+                const uint64_t row = si.row_begin + (frame - si.shard_begin);
+                rec = make_uint4((uint32_t)(best >> 32), frame, (uint32_t)a.coords[2 * row],
+                                 (uint32_t)a.coords[2 * row + 1]);
+            }
+            dst[r] = rec;
+        }
+        if (best == kPadKey) {  // the rest are pads too
+            for (uint32_t rr = r + 1 + lane; rr < a.N; rr += 32)
+                dst[rr] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u);
+            break;
+        }
+        last = best;
+        have_last = true;
+    }
+}
+
+cudaError_t launch_merge_chunks(const MergeArgs &a, cudaStream_t s) {
+    uint64_t warps = (uint64_t)a.nq * a.n_sub;
+    uint64_t blocks = (warps * 32 + kMergeThreads - 1) / kMergeThreads;
+    merge_chunks_kernel<<<(unsigned)blocks, kMergeThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+// One warp per (query, subspace): the N smallest of world sorted lists.
+__global__ void __launch_bounds__(kMergeThreads) merge_ranks_kernel(RankMergeArgs a) {
+    const uint32_t gw = (blockIdx.x * kMergeThreads + threadIdx.x) / 32;
+    const int lane = threadIdx.x & 31;
+    if (gw >= a.nq * a.n_sub) return;
+    const size_t per_rank = (size_t)a.nq * a.n_sub * a.N;
+    const size_t base = (size_t)gw * a.N;
+    const uint32_t nk = a.world * a.N;
+    u64 last = 0;
+    bool have_last = false;
+    for (uint32_t r = 0; r < a.N; ++r) {
+        u64 best = kPadKey;
+        uint32_t bt = 0xFFFFFFFFu;
+        for (uint32_t t = lane; t < nk; t += 32) {
+            const uint4 rec = a.gathered[(t / a.N) * per_rank + base + (t % a.N)];
+            const u64 v = ((u64)rec.x << 32) | rec.y;
+            if ((!have_last || v > last) && v < best) { best = v; bt = t; }
+        }
+        const u64 wbest = warp_min_u64(best);
+        // the lane that holds the winner writes it (carries x, y)
+        const unsigned owner = __ballot_sync(0xffffffffu, best == wbest && bt != 0xFFFFFFFFu);
+        if (wbest == kPadKey) {
+            for (uint32_t rr = r + lane; rr < a.N; rr += 32)
+                a.records[base + rr] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u);
+            break;
+        }
+        if (lane == __ffs(owner) - 1)
+            a.records[base + r] = a.gathered[(bt / a.N) * per_rank + base + (bt % a.N)];
+        last = wbest;
+        have_last = true;
+    }
+}
+
+cudaError_t launch_merge_ranks(const RankMergeArgs &a, cudaStream_t s) {
+    uint64_t warps = (uint64_t)a.nq * a.n_sub;
+    uint64_t blocks = (warps * 32 + kMergeThreads - 1) / kMergeThreads;
+    merge_ranks_kernel<<<(unsigned)blocks, kMergeThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+__global__ void candidates_kernel(CandArgs a) {
+    const uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t total = (uint64_t)a.nq * a.n_sub * a.N;
+    if (t >= total) return;
+    const uint32_t r = (uint32_t)(t % a.N);
+    const uint32_t i = (uint32_t)((t / a.N) % a.n_sub);
+    const uint32_t q = (uint32_t)(t / ((uint64_t)a.N * a.n_sub));
+    const uint32_t c = a.sub_prefix[i + 1] - a.sub_prefix[i];
+    if (r >= c) return;
+    const uint4 rec = a.records[t];
+    const float acc = __uint_as_float(rec.x);
+    ol_candidate o;
+    o.subspace = i;
+    o.frame = rec.y;
+    o.bundle = q / a.M;
+    o.query_frame = q % a.M;
+    o.dist2 = acc;
+    o.dist = __fsqrt_rn(acc);
+    o.x = (int32_t)rec.z;
+    o.y = (int32_t)rec.w;
+    a.out[(uint64_t)q * a.sub_prefix[a.n_sub] + a.sub_prefix[i] + r] = o;
+}
+
+cudaError_t launch_candidates(const CandArgs &a, cudaStream_t s) {
+    uint64_t total = (uint64_t)a.nq * a.n_sub * a.N;
+    candidates_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace ol

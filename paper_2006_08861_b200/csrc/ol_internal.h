@@ -1,0 +1,103 @@
+// ol_internal.h -- shared declarations of the omniloc runtime and its kernels.
+// Product code only (no oracle, no generator).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/omniloc.h"
+
+namespace ol {
+
+typedef unsigned long long u64;
+
+constexpr int kK = OL_K;
+constexpr int kScanThreads = 256;
+constexpr int kScanWarps = kScanThreads / 32;
+constexpr int kMaxQT = 64;            // query frames per scan CTA
+constexpr int kAggMax = 8192;         // candidates per bundle in the aggregation kernel
+constexpr u64 kPadKey = ~0ull;
+constexpr uint32_t kInfBits = 0x7F800000u;  // +inf: "no threshold yet"
+
+// One scan work item: a contiguous run of rows of one subspace.
+struct WorkItem {
+    uint32_t sub;          // subspace
+    uint32_t count;        // rows in this chunk
+    uint64_t row_begin;    // first row in the device planes
+    uint32_t frame_begin;  // global frame index (within the subspace) of that row
+    uint32_t _pad;
+};
+
+struct SubInfo {
+    uint64_t row_begin;    // first local row of the subspace in the device planes
+    uint64_t count;        // local rows (this rank's shard)
+    uint32_t shard_begin;  // global frame index of the first local row
+    uint32_t global_size;  // |n_i|
+    uint32_t chunk_begin;  // first work item of the subspace
+    uint32_t chunk_end;
+};
+
+struct ScanArgs {
+    const float *coarse;         // [rows][kc]
+    const float *fine;           // [rows][K - kc] (null when kc == K)
+    const float *queries;        // [nq][K]
+    const WorkItem *items;
+    const uint32_t *tau0;        // [nq][n_sub] acc bits, or null
+    u64 *partial;                // [nq][n_items][N]
+    unsigned long long *stat_survivors;  // may be null
+    uint32_t nq, n_items, n_qtiles, qt, n_sub, N;
+};
+
+struct SeedArgs {
+    const float *coarse, *fine, *queries;
+    const SubInfo *subs;
+    uint32_t *tau0;              // [nq][n_sub]
+    uint32_t nq, n_sub, N, samples, kc;
+};
+
+struct MergeArgs {
+    const u64 *partial;          // [nq][n_items][N]
+    const SubInfo *subs;
+    const int32_t *coords;       // [rows][2]
+    uint4 *records;              // [nq][n_sub][N]
+    uint32_t nq, n_items, n_sub, N;
+};
+
+struct RankMergeArgs {
+    const uint4 *gathered;       // [world][nq][n_sub][N]
+    uint4 *records;              // [nq][n_sub][N]
+    uint32_t nq, n_sub, N, world;
+};
+
+struct CandArgs {
+    const uint4 *records;        // [nq][n_sub][N]
+    const uint32_t *sub_prefix;  // [n_sub+1] prefix of min(N, |n_i|)
+    ol_candidate *out;
+    uint32_t nq, n_sub, N, M;
+};
+
+struct AggArgs {
+    const ol_candidate *cand;    // if non-null: bundle b = cand[b*per .. (b+1)*per)
+    uint32_t per_bundle;
+    const uint32_t *offsets;     // else: xy pairs with offsets
+    const int32_t *xy;
+    ol_estimate *out;            // device
+    int *err_empty;              // device flag
+    uint32_t n_bundles, top_c;
+    double toler_per, r2, tile_m;
+};
+
+// launchers (return cudaGetLastError())
+cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s);
+cudaError_t launch_scan(int kc, const ScanArgs &a, size_t smem, int grid, cudaStream_t s);
+size_t scan_smem_bytes(uint32_t qt, uint32_t N);
+cudaError_t launch_merge_chunks(const MergeArgs &a, cudaStream_t s);
+cudaError_t launch_merge_ranks(const RankMergeArgs &a, cudaStream_t s);
+cudaError_t launch_candidates(const CandArgs &a, cudaStream_t s);
+cudaError_t launch_aggregate(const AggArgs &a, cudaStream_t s);
+cudaError_t launch_check_finite(const float *p, uint64_t n, int *flag, cudaStream_t s);
+cudaError_t launch_relayout(const float *src, uint64_t rows, int kc, float *coarse, float *fine,
+                            cudaStream_t s);
+cudaError_t launch_check_coords(const int32_t *xy, uint64_t rows, int32_t gw, int32_t gh,
+                                int *flag, cudaStream_t s);
+
+}  // namespace ol

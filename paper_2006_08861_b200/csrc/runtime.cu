@@ -1,0 +1,679 @@
+// runtime.cu -- the omniloc C-ABI (include/omniloc.h): context, database layout
+// in HBM, work decomposition, launch sequence and result retrieval.
+//
+// Launch sequence of one ol_query:
+//   [check_finite]  device frames only
+//   tau_seed        NK3  thresholds from a row sample         (one CTA / (frame, subspace))
+//   scan<kc>        NK2  coarse prefix + fine completion + CTA top-N (the hot loop)
+//   merge_chunks    NK4  per-rank top-N per (frame, subspace) + tiles -> payload
+//   -- world == 1: finalize immediately; world > 1: caller all-gathers payloads --
+//   merge_ranks     NK4' N smallest of the W gathered payloads   (world > 1 only)
+//   candidates           records -> ol_candidate rows, SPEC order
+//   aggregate       NK5  Algorithm 2 per bundle                  (if requested)
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ol_internal.h"
+
+using namespace ol;
+
+static thread_local std::string g_thread_err = "no error";
+
+struct ol_ctx {
+    int device = 0, rank = 0, world = 1, kc = 16;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err = "no error";
+    // database
+    bool db_ready = false;
+    uint32_t n_sub = 0;
+    uint64_t rows = 0;
+    int32_t grid_w = 0, grid_h = 0;
+    std::vector<SubInfo> subs;
+    SubInfo *subs_d = nullptr;
+    float *coarse = nullptr, *fine = nullptr;
+    int32_t *coords = nullptr;
+    // work items (cached per chunk size)
+    std::vector<WorkItem> items;
+    WorkItem *items_d = nullptr;
+    size_t items_cap = 0;
+    uint64_t items_chunk = 0;
+    // per-query buffers
+    float *q_d = nullptr; size_t q_cap = 0;
+    uint32_t *tau0_d = nullptr; size_t tau_cap = 0;
+    u64 *partial_d = nullptr; size_t partial_cap = 0;
+    uint4 *payload_d = nullptr; size_t payload_cap = 0;
+    uint4 *final_d = nullptr; size_t final_cap = 0;
+    ol_candidate *cand_d = nullptr; size_t cand_cap = 0;
+    ol_estimate *est_d = nullptr; size_t est_cap = 0;
+    uint32_t *prefix_d = nullptr; size_t prefix_cap = 0;
+    uint32_t prefix_N = 0;  // N the device prefix was built for (0 = none)
+    uint32_t *agg_off_d = nullptr; size_t agg_off_cap = 0;
+    int32_t *agg_xy_d = nullptr; size_t agg_xy_cap = 0;
+    int *flags_d = nullptr;                // [0] nonfinite frames, [1] aggregation error
+    unsigned long long *stat_d = nullptr;  // [0] survivors
+    // last query
+    bool q_ready = false, finalized = false;
+    uint32_t nb = 0, M = 0, N = 0, nq = 0, qt = 0;
+    int aggregate = 0;
+    ol_params params{};
+    uint64_t n_cand = 0, per_bundle = 0, pairs = 0;
+    int launches = 0;
+    // options
+    int64_t opt_chunk = 0, opt_qtile = 0, opt_tau_seed = 1, opt_ctas = 0, opt_time = 0;
+    // per-kernel-class CUDA-event timing (option "time_kernels"): pairs recorded on
+    // the context stream around each launch; summed and released by ol_get_stat
+    enum { T_SEED, T_SCAN, T_MERGE, T_FINAL, T_COUNT };
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[T_COUNT];
+    std::vector<cudaEvent_t> ev_pool;
+};
+
+static cudaEvent_t take_event(ol_ctx *c) {
+    if (!c->ev_pool.empty()) { cudaEvent_t e = c->ev_pool.back(); c->ev_pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct TimeScope {  // records an event pair around a launch when timing is on
+    ol_ctx *c; int cls; cudaEvent_t a = nullptr;
+    TimeScope(ol_ctx *c_, int cls_) : c(c_), cls(cls_) {
+        if (c->opt_time) { a = take_event(c); cudaEventRecord(a, c->stream); }
+    }
+    ~TimeScope() {
+        if (a) { cudaEvent_t b = take_event(c); cudaEventRecord(b, c->stream); c->ev[cls].push_back({a, b}); }
+    }
+};
+
+// ---------------------------------------------------------------- helpers
+static ol_status fail(ol_ctx *c, ol_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    g_thread_err = buf;
+    return s;
+}
+
+#define OL_CUDA(c, call)                                                                   \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail((c), e_ == cudaErrorMemoryAllocation ? OL_ERR_OOM : OL_ERR_CUDA,    \
+                        "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    } while (0)
+
+#define OL_LAUNCH(c, call)  \
+    do {                    \
+        OL_CUDA(c, call);   \
+        ++(c)->launches;    \
+    } while (0)
+
+template <typename T>
+static cudaError_t grow(T **p, size_t *cap, size_t n) {
+    if (n <= *cap && *p) return cudaSuccess;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    size_t want = n < 1 ? 1 : n;
+    cudaError_t e = cudaMalloc((void **)p, want * sizeof(T));
+    if (e == cudaSuccess) *cap = want;
+    return e;
+}
+
+static ol_status check_params(ol_ctx *c, const ol_params *p, bool need_agg) {
+    if (!p) return fail(c, OL_ERR_INVALID_ARGUMENT, "params is NULL");
+    if (p->N == 0 || p->N > OL_MAX_N)
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "N=%u outside 1..%d", p->N, OL_MAX_N);
+    if (need_agg) {
+        if (p->top_c == 0 || p->top_c > OL_MAX_TOP_C)
+            return fail(c, OL_ERR_INVALID_ARGUMENT, "top_c=%u outside 1..%d", p->top_c, OL_MAX_TOP_C);
+        if (!(p->toler_per > 0.0 && p->toler_per <= 1.0))
+            return fail(c, OL_ERR_INVALID_ARGUMENT, "toler_per=%g outside (0,1]", p->toler_per);
+        if (!(p->radius_m > 0.0) || !std::isfinite(p->radius_m))
+            return fail(c, OL_ERR_INVALID_ARGUMENT, "radius_m=%g must be > 0", p->radius_m);
+        if (!(p->tile_m > 0.0) || !std::isfinite(p->tile_m))
+            return fail(c, OL_ERR_INVALID_ARGUMENT, "tile_m=%g must be > 0", p->tile_m);
+    }
+    return OL_OK;
+}
+
+static void free_db(ol_ctx *c) {
+    cudaFree(c->coarse); cudaFree(c->fine); cudaFree(c->coords); cudaFree(c->subs_d);
+    c->coarse = c->fine = nullptr; c->coords = nullptr; c->subs_d = nullptr;
+    c->db_ready = false;
+    c->items.clear();
+    c->items_chunk = 0;
+}
+
+extern "C" {
+
+// ---------------------------------------------------------------- lifetime
+ol_status ol_create(const ol_config *cfg, ol_ctx **out) {
+    if (!out) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (!cfg) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "cfg is NULL");
+    if (cfg->K != OL_K) return fail(nullptr, OL_ERR_DIMENSION_MISMATCH, "K=%u, library needs %d", cfg->K, OL_K);
+    if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world)
+        return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "rank=%d world=%d", cfg->rank, cfg->world);
+    int kc = cfg->coarse_k == 0 ? OL_K : (int)cfg->coarse_k;
+    if (kc != 8 && kc != 16 && kc != 32 && kc != 64)
+        return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "coarse_k=%u not in {0,8,16,32,64}", cfg->coarse_k);
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(nullptr, OL_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+    if (cfg->device < 0 || cfg->device >= ndev)
+        return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "device %d of %d", cfg->device, ndev);
+    ol_ctx *c = new ol_ctx();
+    c->device = cfg->device; c->rank = cfg->rank; c->world = cfg->world; c->kc = kc;
+    e = cudaSetDevice(c->device);
+    if (e == cudaSuccess) {
+        if (cfg->cuda_stream) c->stream = (cudaStream_t)cfg->cuda_stream;
+        else { e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking); c->own_stream = true; }
+    }
+    if (e == cudaSuccess) e = cudaMalloc((void **)&c->flags_d, 4 * sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc((void **)&c->stat_d, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(c->flags_d, 0, 4 * sizeof(int));
+    if (e != cudaSuccess) {
+        fail(nullptr, OL_ERR_CUDA, "ol_create: %s", cudaGetErrorString(e));
+        ol_destroy(c);
+        return OL_ERR_CUDA;
+    }
+    *out = c;
+    return OL_OK;
+}
+
+void ol_destroy(ol_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    free_db(c);
+    cudaFree(c->items_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
+    cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
+    cudaFree(c->prefix_d); cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
+    cudaFree(c->flags_d); cudaFree(c->stat_d);
+    for (auto &v : c->ev)
+        for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char *ol_last_error(const ol_ctx *c) { return c ? c->err.c_str() : g_thread_err.c_str(); }
+
+ol_status ol_set_stream(ol_ctx *c, void *stream) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (c->own_stream && c->stream) { cudaStreamSynchronize(c->stream); cudaStreamDestroy(c->stream); }
+    c->own_stream = false;
+    c->stream = (cudaStream_t)stream;
+    if (!stream) {
+        cudaSetDevice(c->device);
+        OL_CUDA(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    return OL_OK;
+}
+
+ol_status ol_shard_range(uint64_t n, int32_t rank, int32_t world, uint64_t *begin,
+                         uint64_t *count) {
+    if (world < 1 || rank < 0 || rank >= world || !begin || !count)
+        return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "rank=%d world=%d", rank, world);
+    // floor(r * n / w) without overflow for n < 2^63, w < 2^31
+    uint64_t b = (n / world) * rank + (n % world) * rank / world;
+    uint64_t e = (n / world) * (rank + 1) + (n % world) * (rank + 1) / world;
+    *begin = b;
+    *count = e - b;
+    return OL_OK;
+}
+
+ol_status ol_select_window(uint32_t n_frames, uint32_t m, uint32_t M, uint32_t *first,
+                           uint32_t *len) {
+    if (M == 0 || M % 2 == 0) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "M=%u must be odd", M);
+    if (m >= n_frames) return fail(nullptr, OL_ERR_OUT_OF_RANGE, "m=%u >= n_frames=%u", m, n_frames);
+    if (!first || !len) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "NULL output");
+    const uint32_t L = M < n_frames ? M : n_frames;
+    const uint32_t h = (M - 1) / 2;
+    uint32_t f = m > h ? m - h : 0;          // centred window, clipped at the start ...
+    if (f > n_frames - L) f = n_frames - L;  // ... and shifted back from the end
+    *first = f;
+    *len = L;
+    return OL_OK;
+}
+
+// ---------------------------------------------------------------- database
+ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!db || db->n_subspaces == 0 || !db->global_sizes || !db->features || !db->coords)
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "database descriptor incomplete");
+    if ((db->shard_begin == nullptr) != (db->shard_count == nullptr))
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "shard_begin and shard_count must both be set or NULL");
+    if (db->grid_w <= 0 || db->grid_h <= 0)
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "grid %dx%d", db->grid_w, db->grid_h);
+    OL_CUDA(c, cudaSetDevice(c->device));
+    const uint32_t ns = db->n_subspaces;
+    std::vector<SubInfo> subs(ns);
+    uint64_t rows = 0;
+    for (uint32_t i = 0; i < ns; ++i) {
+        const uint64_t gs = db->global_sizes[i];
+        if (gs == 0 || gs > 0xFFFFFFFEull)
+            return fail(c, OL_ERR_INVALID_ARGUMENT, "subspace %u size %llu outside 1..2^32-2", i,
+                        (unsigned long long)gs);
+        uint64_t b, n;
+        if (db->shard_begin) { b = db->shard_begin[i]; n = db->shard_count[i]; }
+        else ol_shard_range(gs, c->rank, c->world, &b, &n);
+        if (b + n > gs)
+            return fail(c, OL_ERR_INVALID_ARGUMENT, "shard [%llu,+%llu) outside subspace %u of %llu",
+                        (unsigned long long)b, (unsigned long long)n, i, (unsigned long long)gs);
+        subs[i].row_begin = rows;
+        subs[i].count = n;
+        subs[i].shard_begin = (uint32_t)b;
+        subs[i].global_size = (uint32_t)gs;
+        rows += n;
+    }
+    // validate inputs (S:32 finite values; S:102 coords inside the grid)
+    if (!db->on_device) {
+        for (uint64_t t = 0; t < rows * OL_K; ++t)
+            if (!std::isfinite(db->features[t]))
+                return fail(c, OL_ERR_NONFINITE, "feature value %llu is not finite", (unsigned long long)t);
+        for (uint64_t t = 0; t < rows; ++t) {
+            int32_t x = db->coords[2 * t], y = db->coords[2 * t + 1];
+            if (x < 0 || x >= db->grid_w || y < 0 || y >= db->grid_h)
+                return fail(c, OL_ERR_OUT_OF_RANGE, "coord (%d,%d) of row %llu outside %dx%d grid", x, y,
+                            (unsigned long long)t, db->grid_w, db->grid_h);
+        }
+    }
+    free_db(c);
+    const int kc = c->kc;
+    OL_CUDA(c, cudaMalloc((void **)&c->coarse, sizeof(float) * (rows ? rows : 1) * kc));
+    if (kc < OL_K) OL_CUDA(c, cudaMalloc((void **)&c->fine, sizeof(float) * (rows ? rows : 1) * (OL_K - kc)));
+    OL_CUDA(c, cudaMalloc((void **)&c->coords, sizeof(int32_t) * 2 * (rows ? rows : 1)));
+    OL_CUDA(c, cudaMalloc((void **)&c->subs_d, sizeof(SubInfo) * ns));
+    const float *src = db->features;
+    float *tmp = nullptr;
+    if (rows) {
+        if (db->on_device) {
+            OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 2 * sizeof(int), c->stream));
+            OL_CUDA(c, launch_check_finite(db->features, rows * OL_K, c->flags_d, c->stream));
+            OL_CUDA(c, launch_check_coords(db->coords, rows, db->grid_w, db->grid_h, c->flags_d + 1,
+                                           c->stream));
+            int fl[2];
+            OL_CUDA(c, cudaMemcpyAsync(fl, c->flags_d, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
+            OL_CUDA(c, cudaStreamSynchronize(c->stream));
+            OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 2 * sizeof(int), c->stream));
+            if (fl[0]) { free_db(c); return fail(c, OL_ERR_NONFINITE, "device features hold NaN/Inf"); }
+            if (fl[1]) { free_db(c); return fail(c, OL_ERR_OUT_OF_RANGE, "device coords outside the grid"); }
+            OL_CUDA(c, cudaMemcpyAsync(c->coords, db->coords, sizeof(int32_t) * 2 * rows,
+                                       cudaMemcpyDeviceToDevice, c->stream));
+        } else {
+            OL_CUDA(c, cudaMalloc((void **)&tmp, sizeof(float) * rows * OL_K));
+            OL_CUDA(c, cudaMemcpyAsync(tmp, db->features, sizeof(float) * rows * OL_K,
+                                       cudaMemcpyHostToDevice, c->stream));
+            OL_CUDA(c, cudaMemcpyAsync(c->coords, db->coords, sizeof(int32_t) * 2 * rows,
+                                       cudaMemcpyHostToDevice, c->stream));
+            src = tmp;
+        }
+        OL_CUDA(c, launch_relayout(src, rows, kc, c->coarse, c->fine, c->stream));
+    }
+    OL_CUDA(c, cudaMemcpyAsync(c->subs_d, subs.data(), sizeof(SubInfo) * ns, cudaMemcpyHostToDevice,
+                               c->stream));
+    OL_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (tmp) cudaFree(tmp);
+    c->subs = subs;
+    c->n_sub = ns;
+    c->rows = rows;
+    c->grid_w = db->grid_w;
+    c->grid_h = db->grid_h;
+    c->db_ready = true;
+    c->q_ready = false;
+    c->prefix_N = 0;
+    return OL_OK;
+}
+
+// ---------------------------------------------------------------- work decomposition
+static ol_status build_items(ol_ctx *c, uint64_t chunk) {
+    if (chunk == c->items_chunk && !c->items.empty()) return OL_OK;
+    std::vector<WorkItem> items;
+    for (uint32_t i = 0; i < c->n_sub; ++i) {
+        SubInfo &s = c->subs[i];
+        s.chunk_begin = (uint32_t)items.size();
+        for (uint64_t o = 0; o < s.count; o += chunk) {
+            WorkItem w;
+            w.sub = i;
+            w.count = (uint32_t)((s.count - o) < chunk ? (s.count - o) : chunk);
+            w.row_begin = s.row_begin + o;
+            w.frame_begin = (uint32_t)(s.shard_begin + o);
+            w._pad = 0;
+            items.push_back(w);
+        }
+        s.chunk_end = (uint32_t)items.size();
+    }
+    OL_CUDA(c, grow(&c->items_d, &c->items_cap, items.size()));
+    if (!items.empty())
+        OL_CUDA(c, cudaMemcpyAsync(c->items_d, items.data(), sizeof(WorkItem) * items.size(),
+                                   cudaMemcpyHostToDevice, c->stream));
+    OL_CUDA(c, cudaMemcpyAsync(c->subs_d, c->subs.data(), sizeof(SubInfo) * c->n_sub,
+                               cudaMemcpyHostToDevice, c->stream));
+    OL_CUDA(c, cudaStreamSynchronize(c->stream));  // host vectors are pageable and reused
+    c->items.swap(items);
+    c->items_chunk = chunk;
+    return OL_OK;
+}
+
+static ol_status finalize_impl(ol_ctx *c, const uint4 *gathered, int world);
+
+// ---------------------------------------------------------------- query
+ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int32_t on_device,
+                   const ol_params *p, int32_t aggregate) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->db_ready) return fail(c, OL_ERR_NOT_READY, "no database uploaded");
+    ol_status st = check_params(c, p, aggregate != 0);
+    if (st) return st;
+    if (nb == 0) return fail(c, OL_ERR_INVALID_ARGUMENT, "n_bundles = 0");
+    if (M == 0 || M % 2 == 0 || M > OL_MAX_M)
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "M=%u must be odd and <= %d", M, OL_MAX_M);
+    if (!frames) return fail(c, OL_ERR_INVALID_ARGUMENT, "frames is NULL");
+    const uint64_t nq64 = (uint64_t)nb * M;
+    if (nq64 > (1u << 24)) return fail(c, OL_ERR_INVALID_ARGUMENT, "too many query frames");
+    const uint32_t nq = (uint32_t)nq64, N = p->N;
+    uint64_t per_q = 0;
+    for (uint32_t i = 0; i < c->n_sub; ++i) per_q += c->subs[i].global_size < N ? c->subs[i].global_size : N;
+    if (aggregate && per_q * M > (uint64_t)kAggMax)
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "bundle of %llu candidates exceeds %d",
+                    (unsigned long long)(per_q * M), kAggMax);
+    OL_CUDA(c, cudaSetDevice(c->device));
+    c->launches = 0;
+    c->q_ready = c->finalized = false;
+
+    // query tile and chunk size (launch shape only; results never depend on them)
+    uint32_t qt = c->opt_qtile > 0 ? (uint32_t)c->opt_qtile : kMaxQT;
+    while (qt > 8 && scan_smem_bytes(qt, N) > 150 * 1024) qt -= 8;
+    if (qt > kMaxQT) qt = kMaxQT;
+    if (qt > nq) qt = nq;
+    const uint32_t n_qtiles = (nq + qt - 1) / qt;
+    uint64_t chunk = (uint64_t)c->opt_chunk;
+    if (chunk == 0) {
+        const uint64_t target = 148ull * 8;
+        chunk = (c->rows * n_qtiles + target - 1) / target;
+        chunk = ((chunk + 255) / 256) * 256;
+        if (chunk < 1024) chunk = 1024;
+    }
+    if (chunk > 0xFFFFFFFFull) chunk = 0xFFFFFFFFull;
+    st = build_items(c, chunk);
+    if (st) return st;
+    const uint32_t n_items = (uint32_t)c->items.size();
+
+    // buffers
+    OL_CUDA(c, grow(&c->tau0_d, &c->tau_cap, (size_t)nq * c->n_sub));
+    OL_CUDA(c, grow(&c->partial_d, &c->partial_cap, (size_t)nq * (n_items ? n_items : 1) * N));
+    OL_CUDA(c, grow(&c->payload_d, &c->payload_cap, (size_t)nq * c->n_sub * N));
+    const float *q = frames;
+    if (!on_device) {
+        for (uint64_t t = 0; t < nq64 * OL_K; ++t)
+            if (!std::isfinite(frames[t]))
+                return fail(c, OL_ERR_NONFINITE, "frame value %llu is not finite", (unsigned long long)t);
+        OL_CUDA(c, grow(&c->q_d, &c->q_cap, (size_t)nq * OL_K));
+        OL_CUDA(c, cudaMemcpyAsync(c->q_d, frames, sizeof(float) * nq * OL_K, cudaMemcpyHostToDevice,
+                                   c->stream));
+        q = c->q_d;
+    }
+    OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 2 * sizeof(int), c->stream));
+    OL_CUDA(c, cudaMemsetAsync(c->stat_d, 0, sizeof(unsigned long long), c->stream));
+    if (on_device) OL_LAUNCH(c, launch_check_finite(q, nq64 * OL_K, c->flags_d, c->stream));
+
+    const bool seed = c->opt_tau_seed != 0;
+    if (seed) {
+        SeedArgs sa;
+        sa.coarse = c->coarse; sa.fine = c->fine; sa.queries = q; sa.subs = c->subs_d;
+        sa.tau0 = c->tau0_d; sa.nq = nq; sa.n_sub = c->n_sub; sa.N = N; sa.kc = (uint32_t)c->kc;
+        // a sample of count/8 rows (at most 4096) per subspace; below N rows: no seed
+        uint32_t S = 4096;
+        for (auto &s : c->subs) { uint64_t v = s.count / 8; if (v < S) S = (uint32_t)v; }
+        sa.samples = S < 1 ? 1 : S;
+        TimeScope ts(c, ol_ctx::T_SEED);
+        OL_LAUNCH(c, launch_tau_seed(sa, c->stream));
+    }
+    if (n_items) {
+        ScanArgs a;
+        a.coarse = c->coarse; a.fine = c->fine; a.queries = q; a.items = c->items_d;
+        a.tau0 = seed ? c->tau0_d : nullptr; a.partial = c->partial_d; a.stat_survivors = c->stat_d;
+        a.nq = nq; a.n_items = n_items; a.n_qtiles = n_qtiles; a.qt = qt; a.n_sub = c->n_sub; a.N = N;
+        TimeScope ts(c, ol_ctx::T_SCAN);
+        OL_LAUNCH(c, launch_scan(c->kc, a, scan_smem_bytes(qt, N), (int)(n_items * n_qtiles), c->stream));
+    }
+    MergeArgs ma;
+    ma.partial = c->partial_d; ma.subs = c->subs_d; ma.coords = c->coords; ma.records = c->payload_d;
+    ma.nq = nq; ma.n_items = n_items; ma.n_sub = c->n_sub; ma.N = N;
+    {
+        TimeScope ts(c, ol_ctx::T_MERGE);
+        OL_LAUNCH(c, launch_merge_chunks(ma, c->stream));
+    }
+
+    c->nb = nb; c->M = M; c->N = N; c->nq = nq; c->qt = qt; c->aggregate = aggregate; c->params = *p;
+    c->per_bundle = per_q * M;
+    c->n_cand = per_q * nq;
+    c->pairs = (uint64_t)nq * c->rows;
+    c->q_ready = true;
+    if (c->world == 1) return finalize_impl(c, c->payload_d, 1);
+    return OL_OK;
+}
+
+ol_status ol_payload(ol_ctx *c, const void **dev_ptr, uint64_t *bytes) {
+    if (!c || !dev_ptr || !bytes) return fail(c, OL_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!c->q_ready) return fail(c, OL_ERR_NOT_READY, "no query");
+    *dev_ptr = c->payload_d;
+    *bytes = (uint64_t)c->nq * c->n_sub * c->N * sizeof(uint4);
+    return OL_OK;
+}
+
+ol_status ol_payload_copy(ol_ctx *c, void *dst) {
+    if (!c || !dst) return fail(c, OL_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!c->q_ready) return fail(c, OL_ERR_NOT_READY, "no query");
+    OL_CUDA(c, cudaSetDevice(c->device));
+    OL_CUDA(c, cudaMemcpyAsync(dst, c->payload_d, (size_t)c->nq * c->n_sub * c->N * sizeof(uint4),
+                               cudaMemcpyDeviceToDevice, c->stream));
+    return OL_OK;
+}
+
+static ol_status finalize_impl(ol_ctx *c, const uint4 *gathered, int world) {
+    TimeScope ts(c, ol_ctx::T_FINAL);
+    const uint32_t nq = c->nq, N = c->N, ns = c->n_sub;
+    const uint4 *rec = gathered;
+    if (world > 1 || gathered != c->payload_d) {
+        OL_CUDA(c, grow(&c->final_d, &c->final_cap, (size_t)nq * ns * N));
+        RankMergeArgs ra;
+        ra.gathered = gathered; ra.records = c->final_d; ra.nq = nq; ra.n_sub = ns; ra.N = N;
+        ra.world = (uint32_t)world;
+        OL_LAUNCH(c, launch_merge_ranks(ra, c->stream));
+        rec = c->final_d;
+    }
+    if (c->prefix_N != N) {
+        std::vector<uint32_t> prefix(ns + 1, 0);
+        for (uint32_t i = 0; i < ns; ++i)
+            prefix[i + 1] = prefix[i] + (c->subs[i].global_size < N ? c->subs[i].global_size : N);
+        OL_CUDA(c, grow(&c->prefix_d, &c->prefix_cap, ns + 1));
+        OL_CUDA(c, cudaMemcpyAsync(c->prefix_d, prefix.data(), sizeof(uint32_t) * (ns + 1),
+                                   cudaMemcpyHostToDevice, c->stream));
+        OL_CUDA(c, cudaStreamSynchronize(c->stream));
+        c->prefix_N = N;
+    }
+    OL_CUDA(c, grow(&c->cand_d, &c->cand_cap, c->n_cand));
+    CandArgs ca;
+    ca.records = rec; ca.sub_prefix = c->prefix_d; ca.out = c->cand_d; ca.nq = nq; ca.n_sub = ns;
+    ca.N = N; ca.M = c->M;
+    OL_LAUNCH(c, launch_candidates(ca, c->stream));
+    if (c->aggregate) {
+        OL_CUDA(c, grow(&c->est_d, &c->est_cap, c->nb));
+        AggArgs ag;
+        ag.cand = c->cand_d; ag.per_bundle = (uint32_t)c->per_bundle; ag.offsets = nullptr;
+        ag.xy = nullptr; ag.out = c->est_d; ag.err_empty = c->flags_d + 1; ag.n_bundles = c->nb;
+        ag.top_c = c->params.top_c; ag.toler_per = c->params.toler_per;
+        const double r = c->params.radius_m / c->params.tile_m;
+        ag.r2 = r * r; ag.tile_m = c->params.tile_m;
+        OL_LAUNCH(c, launch_aggregate(ag, c->stream));
+    }
+    c->finalized = true;
+    return OL_OK;
+}
+
+ol_status ol_finalize(ol_ctx *c, const void *gathered, int32_t world) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->q_ready) return fail(c, OL_ERR_NOT_READY, "no query to finalize");
+    if (world != c->world || !gathered)
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "world %d != context world %d", world, c->world);
+    OL_CUDA(c, cudaSetDevice(c->device));
+    return finalize_impl(c, (const uint4 *)gathered, world);
+}
+
+// ---------------------------------------------------------------- results
+static ol_status check_flags(ol_ctx *c) {
+    int fl[2];
+    OL_CUDA(c, cudaMemcpyAsync(fl, c->flags_d, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
+    OL_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (fl[0]) return fail(c, OL_ERR_NONFINITE, "query frames hold NaN/Inf");
+    if (fl[1] == 1) return fail(c, OL_ERR_EMPTY, "a bundle has no candidates");
+    if (fl[1] == 2) return fail(c, OL_ERR_INVALID_ARGUMENT, "a bundle exceeds %d candidates", kAggMax);
+    return OL_OK;
+}
+
+ol_status ol_candidate_count(const ol_ctx *c, uint64_t *count) {
+    if (!c || !count) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!c->finalized) return fail(const_cast<ol_ctx *>(c), OL_ERR_NOT_READY, "no finalized query");
+    *count = c->n_cand;
+    return OL_OK;
+}
+
+ol_status ol_get_topk(ol_ctx *c, ol_candidate *out, uint64_t capacity, uint64_t *written) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->finalized) return fail(c, OL_ERR_NOT_READY, "no finalized query");
+    if (!out || capacity < c->n_cand)
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "capacity %llu < %llu candidates",
+                    (unsigned long long)capacity, (unsigned long long)c->n_cand);
+    OL_CUDA(c, cudaSetDevice(c->device));
+    OL_CUDA(c, cudaMemcpyAsync(out, c->cand_d, sizeof(ol_candidate) * c->n_cand, cudaMemcpyDeviceToHost,
+                               c->stream));
+    ol_status st = check_flags(c);
+    if (st) return st;
+    if (written) *written = c->n_cand;
+    return OL_OK;
+}
+
+ol_status ol_topk_device(ol_ctx *c, const ol_candidate **dev_ptr, uint64_t *count) {
+    if (!c || !dev_ptr || !count) return fail(c, OL_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!c->finalized) return fail(c, OL_ERR_NOT_READY, "no finalized query");
+    *dev_ptr = c->cand_d;
+    *count = c->n_cand;
+    return OL_OK;
+}
+
+ol_status ol_get_estimates(ol_ctx *c, ol_estimate *out, uint32_t capacity) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->finalized) return fail(c, OL_ERR_NOT_READY, "no finalized query");
+    if (!c->aggregate) return fail(c, OL_ERR_EMPTY, "aggregation was not requested");
+    if (!out || capacity < c->nb)
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "capacity %u < %u bundles", capacity, c->nb);
+    OL_CUDA(c, cudaSetDevice(c->device));
+    OL_CUDA(c, cudaMemcpyAsync(out, c->est_d, sizeof(ol_estimate) * c->nb, cudaMemcpyDeviceToHost,
+                               c->stream));
+    return check_flags(c);
+}
+
+ol_status ol_aggregate(ol_ctx *c, uint32_t nb, const uint32_t *offsets, const int32_t *xy,
+                       int32_t on_device, const ol_params *p, ol_estimate *out) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    ol_status st = check_params(c, p, true);
+    if (st) return st;
+    if (nb == 0 || !offsets || !xy || !out) return fail(c, OL_ERR_INVALID_ARGUMENT, "empty/NULL input");
+    OL_CUDA(c, cudaSetDevice(c->device));
+    const uint32_t *off_d = offsets;
+    const int32_t *xy_d = xy;
+    if (!on_device) {
+        for (uint32_t b = 0; b < nb; ++b) {
+            if (offsets[b + 1] < offsets[b]) return fail(c, OL_ERR_INVALID_ARGUMENT, "offsets decrease");
+            if (offsets[b + 1] == offsets[b]) return fail(c, OL_ERR_EMPTY, "bundle %u has no candidates", b);
+            if (offsets[b + 1] - offsets[b] > (uint32_t)kAggMax)
+                return fail(c, OL_ERR_INVALID_ARGUMENT, "bundle %u exceeds %d candidates", b, kAggMax);
+        }
+        const uint64_t tot = offsets[nb];
+        OL_CUDA(c, grow(&c->agg_off_d, &c->agg_off_cap, nb + 1));
+        OL_CUDA(c, grow(&c->agg_xy_d, &c->agg_xy_cap, 2 * (tot ? tot : 1)));
+        OL_CUDA(c, cudaMemcpyAsync(c->agg_off_d, offsets, sizeof(uint32_t) * (nb + 1),
+                                   cudaMemcpyHostToDevice, c->stream));
+        OL_CUDA(c, cudaMemcpyAsync(c->agg_xy_d, xy, sizeof(int32_t) * 2 * tot, cudaMemcpyHostToDevice,
+                                   c->stream));
+        off_d = c->agg_off_d;
+        xy_d = c->agg_xy_d;
+    }
+    OL_CUDA(c, grow(&c->est_d, &c->est_cap, nb));
+    OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 2 * sizeof(int), c->stream));
+    AggArgs ag;
+    ag.cand = nullptr; ag.per_bundle = 0; ag.offsets = off_d; ag.xy = xy_d; ag.out = c->est_d;
+    ag.err_empty = c->flags_d + 1; ag.n_bundles = nb; ag.top_c = p->top_c; ag.toler_per = p->toler_per;
+    const double r = p->radius_m / p->tile_m;
+    ag.r2 = r * r; ag.tile_m = p->tile_m;
+    OL_CUDA(c, launch_aggregate(ag, c->stream));
+    OL_CUDA(c, cudaMemcpyAsync(out, c->est_d, sizeof(ol_estimate) * nb, cudaMemcpyDeviceToHost, c->stream));
+    st = check_flags(c);
+    c->finalized = false;  // est_d now holds these estimates, not the last query's
+    return st;
+}
+
+// ---------------------------------------------------------------- options / stats
+ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
+    if (!c || !key) return fail(c, OL_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!strcmp(key, "chunk")) { if (v < 0) goto bad; c->opt_chunk = v; }
+    else if (!strcmp(key, "qtile")) { if (v < 0 || v > kMaxQT) goto bad; c->opt_qtile = v; }
+    else if (!strcmp(key, "tau_seed")) { if (v != 0 && v != 1) goto bad; c->opt_tau_seed = v; }
+    else if (!strcmp(key, "ctas")) { if (v < 0) goto bad; c->opt_ctas = v; }
+    else if (!strcmp(key, "time_kernels")) { if (v != 0 && v != 1) goto bad; c->opt_time = v; }
+    else return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown option '%s'", key);
+    return OL_OK;
+bad:
+    return fail(c, OL_ERR_INVALID_ARGUMENT, "bad value %lld for '%s'", (long long)v, key);
+}
+
+ol_status ol_get_stat(ol_ctx *c, const char *key, int64_t *value) {
+    if (!c || !key || !value) return fail(c, OL_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!strcmp(key, "survivors")) {
+        unsigned long long v = 0;
+        OL_CUDA(c, cudaMemcpyAsync(&v, c->stat_d, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+        OL_CUDA(c, cudaStreamSynchronize(c->stream));
+        *value = (int64_t)v;
+    } else if (!strcmp(key, "pairs")) *value = (int64_t)c->pairs;
+    else if (!strcmp(key, "kernels")) *value = c->launches;
+    else if (!strcmp(key, "qtile")) *value = c->qt;
+    else if (!strcmp(key, "chunk")) *value = (int64_t)c->items_chunk;
+    else if (!strcmp(key, "items")) *value = (int64_t)c->items.size();
+    else if (!strncmp(key, "time_", 5)) {
+        // time_seed_ns / time_scan_ns / time_merge_ns / time_final_ns: summed over the
+        // launches since the last read (then released); time_*_n: how many launches
+        static const char *names[] = {"seed", "scan", "merge", "final"};
+        int cls = -1;
+        for (int k = 0; k < 4; ++k)
+            if (!strncmp(key + 5, names[k], strlen(names[k]))) cls = k;
+        if (cls < 0) return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown stat '%s'", key);
+        const bool count = strstr(key, "_n") && key[strlen(key) - 1] == 'n' && key[strlen(key) - 2] == '_';
+        if (count) { *value = (int64_t)c->ev[cls].size(); return OL_OK; }
+        OL_CUDA(c, cudaStreamSynchronize(c->stream));
+        double ns = 0;
+        for (auto &p : c->ev[cls]) {
+            float ms = 0;
+            OL_CUDA(c, cudaEventElapsedTime(&ms, p.first, p.second));
+            ns += ms * 1e6;
+            c->ev_pool.push_back(p.first);
+            c->ev_pool.push_back(p.second);
+        }
+        c->ev[cls].clear();
+        *value = (int64_t)ns;
+    }
+    else return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown stat '%s'", key);
+    return OL_OK;
+}
+
+}  // extern "C"

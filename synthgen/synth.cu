@@ -156,9 +156,8 @@ void render_host(const syn_spec &s, const syn_point &p, double *prof, float *des
     double n2 = 0;
     for (int k = 1; k <= s.K; ++k) {
         double re = 0, im = 0;
-        for (int w = 0; w < s.W; ++w) {
-            int r = (int)(((int64_t)k * w) % s.W);
-            re += prof[w] * cosT[r];
+        for (int w = 0, r = 0; w < s.W; ++w, r = (r + k >= s.W) ? r + k - s.W : r + k) {
+            re += prof[w] * cosT[r];   // r = (k * w) mod W
             im -= prof[w] * sinT[r];
         }
         m[k - 1] = sqrt(re * re + im * im);
@@ -203,9 +202,8 @@ __global__ void render_kernel(syn_spec s, int64_t n, int mode, int64_t e_begin,
         int nb = 0;
         for (int k = lane + 1; k <= s.K; k += 32, ++nb) {
             double re = 0, im = 0;
-            for (int w = 0; w < s.W; ++w) {
-                int r = (int)(((int64_t)k * w) % s.W);
-                re += prof[w] * cosT[r];
+            for (int w = 0, r = 0; w < s.W; ++w, r = (r + k >= s.W) ? r + k - s.W : r + k) {
+                re += prof[w] * cosT[r];   // r = (k * w) mod W
                 im -= prof[w] * sinT[r];
             }
             mk[nb] = sqrt(re * re + im * im);

