@@ -20,7 +20,7 @@
  *   - "device" pointers are CUDA global-memory pointers on the context's
  *     device; "host" pointers are ordinary (pageable or pinned) memory.
  *   - all device work is ordered on the context's stream (borrowed from the
- *     caller or owned by the library); calls are not thread-safe per context.
+ *     caller); calls are not thread-safe per context.
  *
  * Numeric contract (R3): descriptors and queries are fp32.  For a query q and
  * a database row f the library computes acc = squared distance by the fixed
@@ -69,7 +69,8 @@ typedef struct {
     int32_t device;        /* CUDA device ordinal                                   */
     int32_t rank, world;   /* this process's shard index and the shard count (>=1)  */
     void *cuda_stream;     /* cudaStream_t to borrow (e.g. torch's current stream);
-                              NULL -> the library creates and owns one             */
+                              NULL = the CUDA legacy default stream.  The library
+                              never creates or destroys streams.               */
     uint32_t K;            /* must be OL_K                                           */
     uint32_t coarse_k;     /* prefix length of the coarse pass (R2): 0 or 64 = one
                               pass over full rows; 8, 16 or 32 = exact coarse/fine  */
@@ -143,8 +144,8 @@ OL_API ol_status ol_create(const ol_config *cfg, ol_ctx **out);
 /* Free all device/host resources of the context (NULL is a no-op). */
 OL_API void ol_destroy(ol_ctx *ctx);
 
-/* Replace the stream all later calls are ordered on (NULL -> a library-owned
- * stream).  The previous owned stream, if any, is synchronised and destroyed. */
+/* Replace the stream all later calls are ordered on (borrowed; NULL = the
+ * legacy default stream). */
 OL_API ol_status ol_set_stream(ol_ctx *ctx, void *cuda_stream);
 
 /* Last error message of ctx (or of the calling thread if ctx is NULL). Never NULL. */

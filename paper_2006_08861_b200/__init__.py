@@ -202,7 +202,11 @@ class Engine:
             raise OmnilocError(status, lib().ol_last_error(self._h).decode())
 
     def sync_stream(self):
-        self._ck(lib().ol_set_stream(self._h, ctypes.c_void_p(self._stream_ptr())))
+        """Order the library's work on torch's current stream (or the given one)."""
+        s = self._stream_ptr()
+        if s != getattr(self, "_bound_stream", None):
+            self._ck(lib().ol_set_stream(self._h, ctypes.c_void_p(s)))
+            self._bound_stream = s
 
     # ---------------------------------------------------------------- database
     def upload(self, features, coords, subspace_sizes, grid, shard_begin=None, shard_count=None):

@@ -25,8 +25,7 @@ static thread_local std::string g_thread_err = "no error";
 
 struct ol_ctx {
     int device = 0, rank = 0, world = 1, kc = 16;
-    cudaStream_t stream = nullptr;
-    bool own_stream = false;
+    cudaStream_t stream = nullptr;  // borrowed (NULL = legacy default stream)
     std::string err = "no error";
     // database
     bool db_ready = false;
@@ -175,8 +174,7 @@ ol_status ol_create(const ol_config *cfg, ol_ctx **out) {
     c->device = cfg->device; c->rank = cfg->rank; c->world = cfg->world; c->kc = kc;
     e = cudaSetDevice(c->device);
     if (e == cudaSuccess) {
-        if (cfg->cuda_stream) c->stream = (cudaStream_t)cfg->cuda_stream;
-        else { e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking); c->own_stream = true; }
+        c->stream = (cudaStream_t)cfg->cuda_stream;  // borrowed; NULL = legacy default stream
     }
     if (e == cudaSuccess) e = cudaMalloc((void **)&c->flags_d, 4 * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc((void **)&c->stat_d, 4 * sizeof(unsigned long long));
@@ -193,7 +191,7 @@ ol_status ol_create(const ol_config *cfg, ol_ctx **out) {
 void ol_destroy(ol_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
-    if (c->stream) cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(c->stream);
     free_db(c);
     cudaFree(c->items_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
@@ -202,7 +200,6 @@ void ol_destroy(ol_ctx *c) {
     for (auto &v : c->ev)
         for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
-    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
 
@@ -210,14 +207,7 @@ const char *ol_last_error(const ol_ctx *c) { return c ? c->err.c_str() : g_threa
 
 ol_status ol_set_stream(ol_ctx *c, void *stream) {
     if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
-    if (c->own_stream && c->stream) { cudaStreamSynchronize(c->stream); cudaStreamDestroy(c->stream); }
-    c->own_stream = false;
     c->stream = (cudaStream_t)stream;
-    if (!stream) {
-        cudaSetDevice(c->device);
-        OL_CUDA(c, cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-        c->own_stream = true;
-    }
     return OL_OK;
 }
 
