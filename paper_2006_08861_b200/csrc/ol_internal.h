@@ -2,6 +2,7 @@
 // Product code only (no oracle, no generator).
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/omniloc.h"
@@ -86,7 +87,32 @@ struct AggArgs {
     double toler_per, r2, tile_m;
 };
 
+struct TcScanArgs {
+    const WorkItem *items;
+    const float2 *qmeta;          // [nq] (RD ||q||^2, RU ||q - fp16(q)||)
+    const float2 *rmeta;          // [rows] (RD ||f||^2, RU ||f - fp16(f)||)
+    const uint32_t *nq_max;       // bits of the batch norm bound
+    const uint32_t *force_all;    // nonzero: a frame left the fp16 range -> score every pair
+    float nf_max;                 // database norm bound
+    uint32_t *g_tau;              // [nq][n_sub] acc bits: seeded, then shared running minimum
+    const float *queries;         // fp32 [nq][K]
+    const float *coarse, *fine;   // fp32 planes (exact re-scoring)
+    u64 *partial;                 // [nq][n_items][N]
+    unsigned long long *stat_survivors;
+    uint32_t nq, n_items, n_qblocks, qb, qb_mma, n_sub, N, kc;
+};
+
 // launchers (return cudaGetLastError())
+cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, uint64_t rows, void *plane,
+                                float2 *rmeta, uint32_t *nf_max, uint32_t *maxabs, cudaStream_t s);
+cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float2 *qmeta,
+                                   uint32_t *nq_max, uint32_t *force_all, cudaStream_t s);
+cudaError_t launch_fill_u32(uint32_t *p, uint64_t n, uint32_t v, cudaStream_t s);
+bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows);
+cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q, const TcScanArgs &a, int grid,
+                          cudaStream_t s);
+size_t tc_smem_bytes(uint32_t qb, uint32_t N);
+uint32_t tc_max_qb(uint32_t N);
 cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s);
 cudaError_t launch_scan(int kc, const ScanArgs &a, size_t smem, int grid, cudaStream_t s);
 size_t scan_smem_bytes(uint32_t qt, uint32_t N);

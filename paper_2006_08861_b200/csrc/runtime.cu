@@ -36,6 +36,16 @@ struct ol_ctx {
     SubInfo *subs_d = nullptr;
     float *coarse = nullptr, *fine = nullptr;
     int32_t *coords = nullptr;
+    // tensor-core filter operands (tcscan.cu): fp16 rows + per-row bound terms
+    void *plane16 = nullptr;
+    float2 *rmeta = nullptr;
+    uint32_t *tcstat_d = nullptr;  // [0] database norm bound bits, [1] max |f| bits
+    bool tc_ok = false;
+    float nf_max = 0.f;
+    CUtensorMap map_rows;
+    void *q16 = nullptr; size_t q16_cap = 0;
+    float2 *qmeta = nullptr; size_t qmeta_cap = 0;
+    bool used_tc = false;
     // work items (cached per chunk size)
     std::vector<WorkItem> items;
     WorkItem *items_d = nullptr;
@@ -64,6 +74,8 @@ struct ol_ctx {
     int launches = 0;
     // options
     int64_t opt_chunk = 0, opt_qtile = 0, opt_tau_seed = 1, opt_ctas = 0, opt_time = 0;
+    int64_t opt_tc = -1;         // tensor-core filter: -1 auto (>= 32 frames), 0 off, 1 always
+    int64_t opt_tc_min_frames = 32;
     // per-kernel-class CUDA-event timing (option "time_kernels"): pairs recorded on
     // the context stream around each launch; summed and released by ol_get_stat
     enum { T_SEED, T_SCAN, T_MERGE, T_FINAL, T_COUNT };
@@ -145,7 +157,9 @@ static ol_status check_params(ol_ctx *c, const ol_params *p, bool need_agg) {
 
 static void free_db(ol_ctx *c) {
     cudaFree(c->coarse); cudaFree(c->fine); cudaFree(c->coords); cudaFree(c->subs_d);
+    cudaFree(c->plane16); cudaFree(c->rmeta);
     c->coarse = c->fine = nullptr; c->coords = nullptr; c->subs_d = nullptr;
+    c->plane16 = nullptr; c->rmeta = nullptr; c->tc_ok = false;
     c->db_ready = false;
     c->items.clear();
     c->items_chunk = 0;
@@ -178,6 +192,7 @@ ol_status ol_create(const ol_config *cfg, ol_ctx **out) {
     }
     if (e == cudaSuccess) e = cudaMalloc((void **)&c->flags_d, 4 * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc((void **)&c->stat_d, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc((void **)&c->tcstat_d, 4 * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(c->flags_d, 0, 4 * sizeof(int));
     if (e != cudaSuccess) {
         fail(nullptr, OL_ERR_CUDA, "ol_create: %s", cudaGetErrorString(e));
@@ -196,7 +211,8 @@ void ol_destroy(ol_ctx *c) {
     cudaFree(c->items_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
     cudaFree(c->prefix_d); cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
-    cudaFree(c->flags_d); cudaFree(c->stat_d);
+    cudaFree(c->flags_d); cudaFree(c->stat_d); cudaFree(c->tcstat_d);
+    cudaFree(c->q16); cudaFree(c->qmeta);
     for (auto &v : c->ev)
         for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -310,11 +326,27 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
             src = tmp;
         }
         OL_CUDA(c, launch_relayout(src, rows, kc, c->coarse, c->fine, c->stream));
+        if (c->opt_tc != 0) {
+            OL_CUDA(c, cudaMalloc(&c->plane16, sizeof(uint16_t) * rows * OL_K));
+            OL_CUDA(c, cudaMalloc((void **)&c->rmeta, sizeof(float2) * rows));
+            OL_CUDA(c, cudaMemsetAsync(c->tcstat_d, 0, 4 * sizeof(uint32_t), c->stream));
+            OL_CUDA(c, launch_tc_prep_rows(c->coarse, c->fine, kc, rows, c->plane16, c->rmeta, c->tcstat_d,
+                                           c->tcstat_d + 1, c->stream));
+        }
     }
     OL_CUDA(c, cudaMemcpyAsync(c->subs_d, subs.data(), sizeof(SubInfo) * ns, cudaMemcpyHostToDevice,
                                c->stream));
     OL_CUDA(c, cudaStreamSynchronize(c->stream));
     if (tmp) cudaFree(tmp);
+    if (c->plane16 && rows) {
+        uint32_t st[2];
+        OL_CUDA(c, cudaMemcpy(st, c->tcstat_d, sizeof(st), cudaMemcpyDeviceToHost));
+        const float nf = *reinterpret_cast<float *>(&st[0]), amax = *reinterpret_cast<float *>(&st[1]);
+        c->nf_max = nf;
+        // fp16 operands need |f| well inside the fp16 range, and the row count fits a TMA coordinate
+        c->tc_ok = std::isfinite(nf) && amax < 65000.f && rows < (1ull << 31) &&
+                   make_tc_map(&c->map_rows, c->plane16, rows, 128);
+    }
     c->subs = subs;
     c->n_sub = ns;
     c->rows = rows;
@@ -381,14 +413,29 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     c->launches = 0;
     c->q_ready = c->finalized = false;
 
-    // query tile and chunk size (launch shape only; results never depend on them)
+    // launch shape (results never depend on it): tensor-core filter or CUDA-core
+    // scan, query tile, chunk size
+    const bool use_tc = c->tc_ok && (c->opt_tc == 1 || (c->opt_tc == -1 && nq >= (uint32_t)c->opt_tc_min_frames));
+    uint32_t tc_qb = 0;
     uint32_t qt = c->opt_qtile > 0 ? (uint32_t)c->opt_qtile : kMaxQT;
     while (qt > 8 && scan_smem_bytes(qt, N) > 150 * 1024) qt -= 8;
     if (qt > kMaxQT) qt = kMaxQT;
     if (qt > nq) qt = nq;
-    const uint32_t n_qtiles = (nq + qt - 1) / qt;
+    uint32_t n_qtiles = (nq + qt - 1) / qt;
     uint64_t chunk = (uint64_t)c->opt_chunk;
-    if (chunk == 0) {
+    if (use_tc) {
+        tc_qb = tc_max_qb(N);
+        const uint32_t nq16 = (nq + 15) / 16 * 16;
+        if (tc_qb > nq16) tc_qb = nq16;
+        n_qtiles = (nq + tc_qb - 1) / tc_qb;
+        if (chunk == 0) {
+            const uint64_t target = 148ull * 4;
+            chunk = (c->rows * n_qtiles + target - 1) / target;
+            if (chunk < 4096) chunk = 4096;
+        }
+        chunk = (chunk + 127) / 128 * 128;
+        if (chunk > (1ull << 24) - 128) chunk = (1ull << 24) - 128;
+    } else if (chunk == 0) {
         const uint64_t target = 148ull * 8;
         chunk = (c->rows * n_qtiles + target - 1) / target;
         chunk = ((chunk + 255) / 256) * 256;
@@ -429,7 +476,28 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         TimeScope ts(c, ol_ctx::T_SEED);
         OL_LAUNCH(c, launch_tau_seed(sa, c->stream));
     }
-    if (n_items) {
+    c->used_tc = false;
+    if (n_items && use_tc) {
+        const uint32_t qb = tc_qb, n_qblocks = (nq + qb - 1) / qb, nq_pad = n_qblocks * qb;
+        OL_CUDA(c, grow((uint16_t **)&c->q16, &c->q16_cap, (size_t)nq_pad * OL_K));
+        OL_CUDA(c, grow(&c->qmeta, &c->qmeta_cap, nq));
+        OL_CUDA(c, cudaMemsetAsync(c->tcstat_d + 2, 0, 2 * sizeof(uint32_t), c->stream));
+        OL_LAUNCH(c, launch_tc_prep_queries(q, nq, nq_pad, c->q16, c->qmeta, c->tcstat_d + 2, c->tcstat_d + 3,
+                                            c->stream));
+        if (!seed) OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
+        CUtensorMap map_q;
+        if (!make_tc_map(&map_q, c->q16, nq_pad, qb)) return fail(c, OL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+        TcScanArgs a;
+        a.items = c->items_d; a.qmeta = c->qmeta; a.rmeta = c->rmeta; a.nq_max = c->tcstat_d + 2;
+        a.force_all = c->tcstat_d + 3;
+        a.nf_max = c->nf_max; a.g_tau = c->tau0_d; a.queries = q; a.coarse = c->coarse; a.fine = c->fine;
+        a.partial = c->partial_d; a.stat_survivors = c->stat_d;
+        a.nq = nq; a.n_items = n_items; a.n_qblocks = n_qblocks; a.qb = qb; a.qb_mma = qb; a.n_sub = c->n_sub;
+        a.N = N; a.kc = (uint32_t)c->kc;
+        TimeScope ts(c, ol_ctx::T_SCAN);
+        OL_LAUNCH(c, launch_tcscan(c->map_rows, map_q, a, (int)(n_items * n_qblocks), c->stream));
+        c->used_tc = true;
+    } else if (n_items) {
         ScanArgs a;
         a.coarse = c->coarse; a.fine = c->fine; a.queries = q; a.items = c->items_d;
         a.tau0 = seed ? c->tau0_d : nullptr; a.partial = c->partial_d; a.stat_survivors = c->stat_d;
@@ -622,6 +690,8 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "tau_seed")) { if (v != 0 && v != 1) goto bad; c->opt_tau_seed = v; }
     else if (!strcmp(key, "ctas")) { if (v < 0) goto bad; c->opt_ctas = v; }
     else if (!strcmp(key, "time_kernels")) { if (v != 0 && v != 1) goto bad; c->opt_time = v; }
+    else if (!strcmp(key, "tc")) { if (v < -1 || v > 1) goto bad; c->opt_tc = v; }
+    else if (!strcmp(key, "tc_min_frames")) { if (v < 1) goto bad; c->opt_tc_min_frames = v; }
     else return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown option '%s'", key);
     return OL_OK;
 bad:
@@ -640,6 +710,8 @@ ol_status ol_get_stat(ol_ctx *c, const char *key, int64_t *value) {
     else if (!strcmp(key, "qtile")) *value = c->qt;
     else if (!strcmp(key, "chunk")) *value = (int64_t)c->items_chunk;
     else if (!strcmp(key, "items")) *value = (int64_t)c->items.size();
+    else if (!strcmp(key, "used_tc")) *value = c->used_tc ? 1 : 0;
+    else if (!strcmp(key, "tc_ok")) *value = c->tc_ok ? 1 : 0;
     else if (!strncmp(key, "time_", 5)) {
         // time_seed_ns / time_scan_ns / time_merge_ns / time_final_ns: summed over the
         // launches since the last read (then released); time_*_n: how many launches

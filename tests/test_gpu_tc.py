@@ -1,0 +1,104 @@
+"""GPU parity of the tensor-core certified filter (tcscan, NEXT-2): forced on and
+off, bit-exact against the oracle on paper-shaped data, flat spectra, negative
+and degenerate vectors, many subspaces, large N (smaller query blocks), values
+outside the fp16 range (the library must fall back to the CUDA-core scan), and
+without threshold seeding (every pair survives until the lists fill)."""
+import numpy as np
+import pytest
+
+import oracle
+import synthgen
+import paper_2006_08861_b200 as ol
+from gpu_helpers import assert_candidates_equal, assert_estimates_equal
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(F, C, sizes, Q, N, tc, grid=(4096, 4096), agg=True, **opts):
+    e = ol.Engine(0, coarse_k=16)
+    e.set_option("tc", tc)
+    for k, v in opts.items():
+        e.set_option(k, v)
+    e.upload(F, C, sizes, grid)
+    e.query(Q, N=N, aggregate=agg)
+    return e
+
+
+@pytest.mark.parametrize("N", [1, 15, 64, 128])
+def test_tc_paper_shaped(N):
+    spec = synthgen.Spec(seed=31, n_floors=2, paths=5, frames_per_path=1200)
+    F, C = synthgen.db_host(spec)
+    Q = synthgen.render_host(spec, synthgen.query_points(spec, 9, 300))["desc"][:, None, :]
+    ref = oracle.retrieve([F.shape[0]], F, C, Q, N)
+    for tc in (1, 0):
+        e = _run(F, C, [F.shape[0]], Q, N, tc, spec.grid())
+        assert e.stat("used_tc") == tc
+        assert_candidates_equal(e.topk(), ref, f"N={N} tc={tc}")
+        if tc and N <= 15:
+            assert e.stat("survivors") < 0.02 * e.stat("pairs")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_tc_adversarial(seed):
+    rng = np.random.default_rng(500 + seed)
+    sizes = [int(x) for x in rng.integers(50, 3000, int(rng.integers(1, 4)))]
+    rows = sum(sizes)
+    kind = seed % 4
+    if kind == 0:
+        F = synthgen.gflat(rows, seed=seed, dup_frac=0.05)
+    elif kind == 1:
+        F = (rng.standard_normal((rows, 64)) * 3).astype(np.float32)      # signed, non-unit
+    elif kind == 2:
+        F = rng.random((rows, 64)).astype(np.float32)
+        F[rng.integers(0, rows, rows // 10)] = 0.0                        # degenerate rows
+    else:
+        F = (rng.random((rows, 64)) * 1e-3).astype(np.float32)             # fp16 subnormal range
+    C = rng.integers(0, 500, (rows, 2)).astype(np.int32)
+    M = int(rng.choice([1, 3, 5]))
+    B = int(rng.integers(8, 80))
+    Q = F[rng.integers(0, rows, B * M)].reshape(B, M, 64).copy()
+    Q += (rng.standard_normal(Q.shape) * 1e-4).astype(np.float32)
+    Q[0, 0] = 0.0
+    N = int(rng.choice([5, 15, 33]))
+    ref = oracle.retrieve(sizes, F, C, Q, N)
+    opts = {"tau_seed": 0} if seed % 3 == 0 else {}
+    e = _run(F, C, sizes, Q, N, 1, **opts)
+    assert e.stat("used_tc") == 1
+    assert_candidates_equal(e.topk(), ref, f"seed {seed}")
+    assert_estimates_equal(e.estimates(), ref, ctx=f"seed {seed}")
+
+
+def test_tc_out_of_fp16_range_falls_back():
+    rng = np.random.default_rng(9)
+    F = rng.random((3000, 64)).astype(np.float32)
+    F[17, 3] = 1e6
+    C = rng.integers(0, 100, (3000, 2)).astype(np.int32)
+    Q = F[:40][:, None, :].copy()
+    ref = oracle.retrieve([3000], F, C, Q, 15)
+    e = _run(F, C, [3000], Q, 15, 1)
+    assert e.stat("tc_ok") == 0 and e.stat("used_tc") == 0
+    assert_candidates_equal(e.topk(), ref, "fallback")
+    # a query out of range: still the TC kernel, every pair re-scored exactly
+    Q2 = Q.copy()
+    Q2[3, 0, 5] = 7e4
+    F2 = F.copy(); F2[17, 3] = 0.5
+    ref2 = oracle.retrieve([3000], F2, C, Q2, 15)
+    e2 = _run(F2, C, [3000], Q2, 15, 1)
+    assert e2.stat("used_tc") == 1
+    assert_candidates_equal(e2.topk(), ref2, "query out of range")
+
+
+def test_tc_schedule_invariance():
+    spec = synthgen.Spec(seed=33, n_floors=1, paths=5, frames_per_path=2000)
+    F, C = synthgen.db_host(spec)
+    Q = synthgen.render_host(spec, synthgen.query_points(spec, 5, 600))["desc"][:, None, :]
+    outs = set()
+    for opts in ({}, {"chunk": 4096}, {"chunk": 128}, {"tau_seed": 0, "chunk": 2048}, {"tc": 0}):
+        e = ol.Engine(0)
+        e.set_option("tc", 1)
+        for k, v in opts.items():
+            e.set_option(k, v)
+        e.upload(F, C, [F.shape[0]], spec.grid())
+        e.query(Q, N=15)
+        outs.add(e.topk().tobytes() + e.estimates().tobytes())
+    assert len(outs) == 1
