@@ -209,23 +209,36 @@ def run_omniloc(a):
     rows_local = cnt
     pairs = B * rows_local
     scan_s = scan_ns / 1e9
-    # FP32 issue ceiling: 148 SMs x 128 lanes x SM clock; 2*kc lane
-    # instructions (FSUB + FFMA per coefficient) per pair are algorithmically required
+    used_tc = bool(eng.stat("used_tc"))
     sm_max = peaks.get("sm_max_mhz", 1965.0)
-    alu_peak = 148 * 128 * sm_max * 1e6 / 1e12          # T lane-instr/s
-    achieved_alu = pairs * 2 * kc / scan_s / 1e12 if scan_s > 0 else None
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    alg_bytes = rows_local * kc * 4 + survivors / max(a.warmup, 1) * 0   # coarse plane once
-    achieved_gbs = alg_bytes / scan_s / 1e9 if scan_s > 0 else None
-    roofline = {"kernel": f"scan_kernel<{kc}>", "bound": "alu", "achieved": achieved_alu,
-                "peak": alu_peak, "unit": "T lane-instr/s",
-                "frac": achieved_alu / alu_peak if achieved_alu else None,
-                "traffic": None,
-                "peak_source": f"148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
-                "per_launch": {"pairs": pairs, "lane_instr": pairs * 2 * kc, "algorithmic_bytes": alg_bytes,
-                               "avg_ms": scan_s * 1e3, "hbm_gbs": achieved_gbs,
-                               "hbm_frac": achieved_gbs / hbm_peak if achieved_gbs else None},
-                "step_share": scan_ns / (ms * 1e6)}
+    if used_tc:
+        # tensor-core certified filter: 2 x 64 fp16 MMA flops per (query, row) pair; peak =
+        # measured dense bf16 burst (fp16 and bf16 have the same nominal tensor rate)
+        flops = 2.0 * 64 * pairs
+        tc_peak = peaks.get("bf16_tflops", 1590.0)
+        achieved = flops / scan_s / 1e12 if scan_s > 0 else None
+        alg_bytes = rows_local * (64 * 2 + 8)          # fp16 row + 8 B bound terms, once
+        roofline = {"kernel": "tcscan_kernel", "bound": "tensor", "achieved": achieved, "peak": tc_peak,
+                    "unit": "TFLOP/s", "frac": achieved / tc_peak if achieved else None, "traffic": None,
+                    "peak_source": "MEASURED_PEAKS bf16_tflops (burst, of measured; fp16 = bf16 nominal rate); "
+                                   f"sustained {peaks.get('bf16_tflops_sustained')}",
+                    "per_launch": {"pairs": pairs, "mma_flops": flops, "algorithmic_bytes": alg_bytes,
+                                   "avg_ms": scan_s * 1e3,
+                                   "hbm_gbs": alg_bytes / scan_s / 1e9 if scan_s > 0 else None,
+                                   "exact_rescored_pairs": survivors}}
+    else:
+        # CUDA-core scan: FP32 issue ceiling 148 SMs x 128 lanes x SM clock; 2*kc lane
+        # instructions (FSUB + FFMA per coefficient) per pair are algorithmically required
+        alu_peak = 148 * 128 * sm_max * 1e6 / 1e12
+        achieved = pairs * 2 * kc / scan_s / 1e12 if scan_s > 0 else None
+        alg_bytes = rows_local * kc * 4
+        roofline = {"kernel": f"scan_kernel<{kc}>", "bound": "alu", "achieved": achieved, "peak": alu_peak,
+                    "unit": "T lane-instr/s", "frac": achieved / alu_peak if achieved else None, "traffic": None,
+                    "peak_source": f"148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+                    "per_launch": {"pairs": pairs, "lane_instr": pairs * 2 * kc, "algorithmic_bytes": alg_bytes,
+                                   "avg_ms": scan_s * 1e3}}
+    roofline["step_share"] = scan_ns / (ms * 1e6)
 
     out = {"metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -237,7 +250,7 @@ def run_omniloc(a):
            "comparisons_per_sec": cps,
            "stages_ms": {"tau_seed": seed_ns / 1e6, "scan": scan_ns / 1e6, "merge": merge_ns / 1e6,
                          "finalize": final_ns / 1e6},
-           "survivor_frac": survivors / max(pairs, 1),
+           "survivor_frac": survivors / max(pairs, 1), "scan_path": "tensor-core filter" if used_tc else "cuda-core",
            "gpu_launches": kernels_per_step * a.steps,
            "roofline": roofline, "clocks": clk,
            "setup_s": {"generate": gen_s, "upload": upload_s}}

@@ -99,7 +99,11 @@ struct TcScanArgs {
     const float *coarse, *fine;   // fp32 planes (exact re-scoring)
     u64 *partial;                 // [nq][n_items][N]
     unsigned long long *stat_survivors;
+    unsigned long long *stat_flagged;   // (row, 32-column chunk) groups that took the cold path
     uint32_t nq, n_items, n_qblocks, qb, qb_mma, n_sub, N, kc;
+    uint32_t dbg;                 // profiling only: 1 skip epilogue math, 2 skip MMA, 4 skip cold
+                                  // path (wrong results); 8 per-role clock64 accounting -> prof
+    unsigned long long *prof;     // [16] cycle counters (dbg & 8)
 };
 
 // launchers (return cudaGetLastError())

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -65,6 +66,7 @@ struct ol_ctx {
     int32_t *agg_xy_d = nullptr; size_t agg_xy_cap = 0;
     int *flags_d = nullptr;                // [0] nonfinite frames, [1] aggregation error
     unsigned long long *stat_d = nullptr;  // [0] survivors
+    unsigned long long *prof_d = nullptr;  // [16] tcscan per-role cycle counters (tc_debug & 8)
     // last query
     bool q_ready = false, finalized = false;
     uint32_t nb = 0, M = 0, N = 0, nq = 0, qt = 0;
@@ -76,6 +78,7 @@ struct ol_ctx {
     int64_t opt_chunk = 0, opt_qtile = 0, opt_tau_seed = 1, opt_ctas = 0, opt_time = 0;
     int64_t opt_tc = -1;         // tensor-core filter: -1 auto (>= 32 frames), 0 off, 1 always
     int64_t opt_tc_min_frames = 32;
+    int64_t opt_tc_debug = 0;    // profiling experiments only (results invalid when nonzero)
     // per-kernel-class CUDA-event timing (option "time_kernels"): pairs recorded on
     // the context stream around each launch; summed and released by ol_get_stat
     enum { T_SEED, T_SCAN, T_MERGE, T_FINAL, T_COUNT };
@@ -193,6 +196,7 @@ ol_status ol_create(const ol_config *cfg, ol_ctx **out) {
     if (e == cudaSuccess) e = cudaMalloc((void **)&c->flags_d, 4 * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc((void **)&c->stat_d, 4 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMalloc((void **)&c->tcstat_d, 4 * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMalloc((void **)&c->prof_d, 1024 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemset(c->flags_d, 0, 4 * sizeof(int));
     if (e != cudaSuccess) {
         fail(nullptr, OL_ERR_CUDA, "ol_create: %s", cudaGetErrorString(e));
@@ -211,7 +215,7 @@ void ol_destroy(ol_ctx *c) {
     cudaFree(c->items_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
     cudaFree(c->prefix_d); cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
-    cudaFree(c->flags_d); cudaFree(c->stat_d); cudaFree(c->tcstat_d);
+    cudaFree(c->flags_d); cudaFree(c->stat_d); cudaFree(c->tcstat_d); cudaFree(c->prof_d);
     cudaFree(c->q16); cudaFree(c->qmeta);
     for (auto &v : c->ev)
         for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
@@ -328,7 +332,8 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
         OL_CUDA(c, launch_relayout(src, rows, kc, c->coarse, c->fine, c->stream));
         if (c->opt_tc != 0) {
             OL_CUDA(c, cudaMalloc(&c->plane16, sizeof(uint16_t) * rows * OL_K));
-            OL_CUDA(c, cudaMalloc((void **)&c->rmeta, sizeof(float2) * rows));
+            OL_CUDA(c, cudaMalloc((void **)&c->rmeta, sizeof(float2) * (rows + 132)));  // + one tile of pad
+            OL_CUDA(c, cudaMemsetAsync(c->rmeta + rows, 0, sizeof(float2) * 132, c->stream));
             OL_CUDA(c, cudaMemsetAsync(c->tcstat_d, 0, 4 * sizeof(uint32_t), c->stream));
             OL_CUDA(c, launch_tc_prep_rows(c->coarse, c->fine, kc, rows, c->plane16, c->rmeta, c->tcstat_d,
                                            c->tcstat_d + 1, c->stream));
@@ -461,7 +466,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         q = c->q_d;
     }
     OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 2 * sizeof(int), c->stream));
-    OL_CUDA(c, cudaMemsetAsync(c->stat_d, 0, sizeof(unsigned long long), c->stream));
+    OL_CUDA(c, cudaMemsetAsync(c->stat_d, 0, 2 * sizeof(unsigned long long), c->stream));
     if (on_device) OL_LAUNCH(c, launch_check_finite(q, nq64 * OL_K, c->flags_d, c->stream));
 
     const bool seed = c->opt_tau_seed != 0;
@@ -491,9 +496,11 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         a.items = c->items_d; a.qmeta = c->qmeta; a.rmeta = c->rmeta; a.nq_max = c->tcstat_d + 2;
         a.force_all = c->tcstat_d + 3;
         a.nf_max = c->nf_max; a.g_tau = c->tau0_d; a.queries = q; a.coarse = c->coarse; a.fine = c->fine;
-        a.partial = c->partial_d; a.stat_survivors = c->stat_d;
+        a.partial = c->partial_d; a.stat_survivors = c->stat_d; a.stat_flagged = c->stat_d + 1;
         a.nq = nq; a.n_items = n_items; a.n_qblocks = n_qblocks; a.qb = qb; a.qb_mma = qb; a.n_sub = c->n_sub;
-        a.N = N; a.kc = (uint32_t)c->kc;
+        a.N = N; a.kc = (uint32_t)c->kc; a.dbg = (uint32_t)c->opt_tc_debug;
+        a.prof = c->prof_d;
+        if (c->opt_tc_debug & 8) OL_CUDA(c, cudaMemsetAsync(c->prof_d, 0, 16 * sizeof(unsigned long long), c->stream));
         TimeScope ts(c, ol_ctx::T_SCAN);
         OL_LAUNCH(c, launch_tcscan(c->map_rows, map_q, a, (int)(n_items * n_qblocks), c->stream));
         c->used_tc = true;
@@ -692,6 +699,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "time_kernels")) { if (v != 0 && v != 1) goto bad; c->opt_time = v; }
     else if (!strcmp(key, "tc")) { if (v < -1 || v > 1) goto bad; c->opt_tc = v; }
     else if (!strcmp(key, "tc_min_frames")) { if (v < 1) goto bad; c->opt_tc_min_frames = v; }
+    else if (!strcmp(key, "tc_debug")) { if (v < 0 || v > 31) goto bad; c->opt_tc_debug = v; }
     else return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown option '%s'", key);
     return OL_OK;
 bad:
@@ -705,6 +713,16 @@ ol_status ol_get_stat(ol_ctx *c, const char *key, int64_t *value) {
         OL_CUDA(c, cudaMemcpyAsync(&v, c->stat_d, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
         OL_CUDA(c, cudaStreamSynchronize(c->stream));
         *value = (int64_t)v;
+    } else if (!strcmp(key, "flagged")) {
+        unsigned long long v = 0;
+        OL_CUDA(c, cudaMemcpyAsync(&v, c->stat_d + 1, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+        OL_CUDA(c, cudaStreamSynchronize(c->stream));
+        *value = (int64_t)v;
+    } else if (!strncmp(key, "prof", 4)) {
+        unsigned long long v[1024];
+        OL_CUDA(c, cudaMemcpyAsync(v, c->prof_d, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+        OL_CUDA(c, cudaStreamSynchronize(c->stream));
+        *value = (int64_t)v[atoi(key + 4)];
     } else if (!strcmp(key, "pairs")) *value = (int64_t)c->pairs;
     else if (!strcmp(key, "kernels")) *value = c->launches;
     else if (!strcmp(key, "qtile")) *value = c->qt;

@@ -25,8 +25,9 @@
 // Warp roles: 0 TMA producer of 128-row fp16 tiles (SW128, 4-stage mbarrier
 // ring); 1 TMEM allocator + single-thread tcgen05.mma issuer (M=128 rows,
 // N=query block, K=64 as 4 x K16) into a double-buffered TMEM accumulator
-// (2 x 256 columns); 2..9 epilogue (tcgen05.ld, threshold test, survivor push);
-// 10..11 exact re-scoring + top-N insertion.
+// (2 x 256 columns); 2..17 epilogue (tcgen05.ld, threshold test, survivor
+// push; 4 warps per TMEM lane quarter, 64 columns each); 18..19 exact
+// re-scoring + top-N insertion.
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
@@ -38,25 +39,25 @@ namespace ol {
 using namespace tc;
 
 constexpr int kTileRows = 128;
-constexpr int kStages = 4;
+constexpr int kStages = 8;
 constexpr int kQB = 256;                 // max query frames per CTA (MMA N)
-constexpr int kEpiWarps = 8;
-constexpr int kExactWarps = 2;
+constexpr int kEpiWarps = 16;
+constexpr int kExactWarps = 1;
 constexpr int kTcThreads = 32 * (2 + kEpiWarps + kExactWarps);
-constexpr int kRing = 2048;              // survivor ring entries (r_local << 8 | q_local)
+constexpr int kRing = 1024;              // survivor ring entries (r_local << 8 | q_local)
 constexpr float kTauInflate = 1.0f + 1.0f / 131072.0f;   // 1 + 2^-17
 
 struct TcSmem {
     alignas(1024) __half b[kQB * kK];                // query block (resident)
     alignas(1024) __half a[kStages][kTileRows * kK];  // row tiles
+    alignas(16) float2 rm[kStages][kTileRows + 2];   // the tiles' (RD ||f||^2, RU e_f), from an
+                                                     // even row (16-B aligned bulk copy)
     uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], qbar;
     uint32_t tmem_base;
     alignas(16) float alpha[kQB];
-    alignas(16) float h[kQB];
-    alignas(16) float T[kQB];
+    alignas(16) float h[kQB];   // h_q = (alpha_q - tau_q (1 + 2^-17)) / 2
     uint32_t tau[kQB];
     int lock[kQB];
-    float gmin_w[kEpiWarps];
     // survivor queue: bounded MPMC ring with per-slot sequence numbers (Vyukov):
     // slot i is free for position p when seq == p, filled when seq == p + 1
     uint32_t seq[kRing], val[kRing];
@@ -72,17 +73,77 @@ __device__ __forceinline__ float chain_step_tc(float acc, float q, float f) {
     return __fmaf_rn(d, d, acc);
 }
 
-// Exact per-row survivor test; enqueue (r_local, column) on the MPMC ring,
-// waiting while the ring is full.
-__device__ __forceinline__ void tc_push(TcSmem &s, float d, uint32_t col, uint32_t qn, float g, uint32_t rl) {
-    if (col < qn && d - (s.h[col] + g) >= 0.f) {
-        const unsigned pos = atomicAdd(&s.prod, 1u);
-        volatile uint32_t *sq = &s.seq[pos % kRing];
-        while (*sq != pos) __nanosleep(64);
-        s.val[pos % kRing] = (rl << 8) | col;
-        __threadfence_block();
-        *sq = pos + 1;
+__device__ __forceinline__ uint32_t lds_u32(const void *p) {  // volatile shared-memory load
+    return *reinterpret_cast<const volatile uint32_t *>(p);
+}
+__device__ __forceinline__ uint64_t lds_u64(const void *p) {
+    return *reinterpret_cast<const volatile uint64_t *>(p);
+}
+__device__ __forceinline__ void sts_u32(void *p, uint32_t v) {  // volatile shared-memory store
+    *reinterpret_cast<volatile uint32_t *>(p) = v;
+}
+
+__device__ __forceinline__ uint64_t pack2(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {  // FADD2: two RN fp32 subtractions
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+__device__ __forceinline__ float h_of(float alpha, uint32_t tau_bits) {
+    return 0.5f * (alpha - __uint_as_float(tau_bits) * kTauInflate);
+}
+
+__device__ __forceinline__ float max3f(float a, float b, float c) {  // FMNMX3
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
+// Threshold test of 32 accumulator columns of one row: x = (D - g) - h per
+// column (two FADD2 per column pair); sets bit `chunk` of flags if any x >= 0.
+__device__ __forceinline__ void tc_test32(const uint32_t (&v)[32], uint64_t gg, const uint64_t *h2,
+                                          uint32_t &flags, int chunk) {
+    uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+        const uint64_t x0 = sub2(sub2(pack2(v[2 * j], v[2 * j + 1]), gg), h2[j]);
+        const uint64_t x1 = sub2(sub2(pack2(v[2 * j + 2], v[2 * j + 3]), gg), h2[j + 1]);
+        const uint32_t m = (uint32_t)x0 & (uint32_t)(x0 >> 32) & (uint32_t)x1 & (uint32_t)(x1 >> 32);
+        if (j & 2) a1 &= m; else a0 &= m;
     }
+    flags |= ((~(a0 & a1)) >> 31) << chunk;
+}
+// Bit mask of the passing columns among 32 (same arithmetic as tc_test32).
+__device__ __forceinline__ uint32_t tc_mask32(const uint32_t (&v)[32], uint64_t gg, const uint64_t *h2) {
+    uint32_t mask = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const uint64_t x = sub2(sub2(pack2(v[2 * j], v[2 * j + 1]), gg), h2[j]);
+        mask |= ((~(uint32_t)x >> 31) << (2 * j)) | ((~(uint32_t)(x >> 32) >> 31) << (2 * j + 1));
+    }
+    return mask;
+}
+
+// Enqueue a survivor (r_local << 8 | column) on the MPMC ring, waiting while
+// the ring is full.
+__device__ __forceinline__ void tc_enqueue(TcSmem &s, uint32_t e) {
+    const unsigned pos = atomicAdd(&s.prod, 1u);
+    uint32_t *sq = &s.seq[pos % kRing];
+    while (lds_u32(sq) != pos) __nanosleep(64);
+    s.val[pos % kRing] = e;
+    __threadfence_block();
+    sts_u32(sq, pos + 1);
+}
+
+// Cold path of the epilogue: the row passed for some of its 64 columns; find them
+// (same arithmetic as the hot test) and enqueue them.  Kept out of line so the
+// hot loop's register allocation does not carry it.
+__device__ __noinline__ void tc_cold(TcSmem &s, const uint32_t *v, float g, uint32_t cb, uint32_t qn,
+                                     uint32_t rl, unsigned long long *stat_flagged) {
+    for (uint32_t j = 0; j < 64; ++j)
+        if (cb + j < qn && __fsub_rn(__uint_as_float(v[j]), s.h[cb + j]) >= g) tc_enqueue(s, (rl << 8) | (cb + j));
+    if (stat_flagged) atomicAdd(stat_flagged, 1ull);
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -104,7 +165,9 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
 
     // ---------------------------------------------------------------- setup
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kStages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 1); }
+        // a stage is free once the MMA consumed its rows AND every epilogue warp read
+        // its bound terms (rm)
+        for (int i = 0; i < kStages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 1 + kEpiWarps); }
         for (int i = 0; i < 2; ++i) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], kEpiWarps); }
         mbar_init(&s.qbar, 1);
         fence_mbar_init();
@@ -124,9 +187,11 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             const float2 m = a.qmeta[q0 + q];  // (RD ||q||^2, RU e_q)
             s.alpha[q] = force_all ? -INFINITY : m.x - 2.f * m.y * nfm - c0 - sigma;
             s.tau[q] = a.g_tau[(size_t)(q0 + q) * a.n_sub + it.sub];
+            s.h[q] = h_of(s.alpha[q], s.tau[q]);
         } else {
-            s.alpha[q] = INFINITY;  // padded query column: h = T = +inf, never passes
+            s.alpha[q] = INFINITY;  // padded query column: h = +inf, never passes
             s.tau[q] = 0;
+            s.h[q] = INFINITY;
         }
         s.lock[q] = 0;
     }
@@ -144,9 +209,11 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             tma_load_2d(s.b, &map_q, &s.qbar, 0, (int)q0);
             for (uint32_t t = 0; t < n_tiles; ++t) {
                 const uint32_t st = t % kStages;
-                if (t >= kStages) mbar_wait(&s.empty[st], ((t / kStages) - 1) & 1);
-                mbar_expect_tx(&s.full[st], sizeof(s.a[0]));
-                tma_load_2d(s.a[st], &map_rows, &s.full[st], 0, (int)(it.row_begin + (uint64_t)t * kTileRows));
+                if (t >= kStages) mbar_wait_sleep(&s.empty[st], ((t / kStages) - 1) & 1);
+                const uint64_t r0 = it.row_begin + (uint64_t)t * kTileRows;
+                mbar_expect_tx(&s.full[st], sizeof(s.a[0]) + sizeof(s.rm[0]));
+                tma_load_2d(s.a[st], &map_rows, &s.full[st], 0, (int)r0);
+                bulk_load(s.rm[st], a.rmeta + (r0 & ~1ull), sizeof(s.rm[0]), &s.full[st]);  // rmeta padded
             }
         }
     } else if (warp == 1) {
@@ -162,7 +229,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 tc_fence_after();
                 const uint32_t a_base = smem_u32(s.a[st]);
 #pragma unroll
-                for (int k = 0; k < kK / 16; ++k)
+                for (int k = 0; k < ((a.dbg & 2) ? 0 : kK / 16); ++k)
                     mma_f16(tmem + buf * kQB, desc_sw128_kmajor(a_base + k * 32),
                             desc_sw128_kmajor(b_base + k * 32), idesc, k > 0 ? 1u : 0u);
                 mma_commit(&s.empty[st]);
@@ -171,99 +238,111 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         }
     } else if (warp < 2 + kEpiWarps) {
         // ------------------------------------------------------------ epilogue
-        const int ew = warp - 2;                  // 0..7
+        // 16 warps: warp -> (TMEM lane quarter, 64 query columns); thread = one row.
+        // Per tile: read the 64 accumulator columns, hand the TMEM buffer back at once,
+        // then on registers: y_c = RN(D_c - h_c) (FADD2) and max over c (FMNMX3); the
+        // row survives for some column iff max_c y_c >= g (cold path, rare).
+        const int ew = warp - 2;                  // 0..15
         const uint32_t quarter = warp & 3;        // TMEM lanes 32*quarter ..
-        const uint32_t half = ew >> 2;            // columns half*128 ..
-        const uint32_t et = ew * 32 + lane;       // 0..255: column owned in the T update
-        const bool my_half = half * 128 < a.qb_mma;
+        const uint32_t part = ew >> 2;            // columns part*64 .. +64
+        const uint32_t ncol = part * 64 < a.qb_mma ? min(64u, a.qb_mma - part * 64) : 0u;
+        const uint32_t r_in_tile = quarter * 32 + lane;
+        const uint32_t rc = ew * 32 + lane;       // threshold column refreshed by this thread
+        uint32_t gt = 0xFFFFFFFFu;                // shared running threshold, loaded one tile ahead
         for (uint32_t t = 0; t < n_tiles; ++t) {
-            const uint32_t buf = t & 1;
-            const uint32_t rl = t * kTileRows + quarter * 32 + lane;   // row within the item
+            const uint32_t buf = t & 1, st = t % kStages;
+            const uint32_t rl = t * kTileRows + r_in_tile;   // row within the item
             const bool valid = rl < it.count;
-            float g = INFINITY;
-            if (valid) {
-                const float2 m = a.rmeta[it.row_begin + rl];  // (RD ||f||^2, RU e_f)
-                g = 0.5f * (m.x - 2.f * nqm * m.y);
-            }
-            float gm = g;
-            for (int o = 16; o; o >>= 1) gm = fminf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
-            if (lane == 0) s.gmin_w[ew] = gm;
-            named_bar(1, 32 * kEpiWarps);
-            {   // thresholds of this tile: T_c = h_c + min_r g_r  (a superset test)
-                float gmin = s.gmin_w[0];
-#pragma unroll
-                for (int w = 1; w < kEpiWarps; ++w) gmin = fminf(gmin, s.gmin_w[w]);
-                float tau_c = __uint_as_float(s.tau[et]);
-                if (et < qn) tau_c = fminf(tau_c, __uint_as_float(a.g_tau[(size_t)(q0 + et) * a.n_sub + it.sub]));
-                const float hc = 0.5f * (s.alpha[et] - tau_c * kTauInflate);
-                s.h[et] = hc;
-                s.T[et] = hc + gmin;
-            }
-            named_bar(1, 32 * kEpiWarps);
-            mbar_wait(&s.tfull[buf], (t >> 1) & 1);
+            const uint32_t gt_prev = gt;   // loaded a tile ago (latency hidden)
+            if (rc < qn) gt = __ldcg(&a.g_tau[(size_t)(q0 + rc) * a.n_sub + it.sub]);
+            mbar_wait(&s.tfull[buf], (t >> 1) & 1);          // MMA t done (its stage landed)
             tc_fence_after();
-            if (my_half) {
-                const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * kQB + half * 128;
-                const uint32_t ncol = min(128u, a.qb_mma - half * 128);
-                for (uint32_t c0 = 0; c0 < ncol; c0 += 64) {
-                    uint32_t v0[32], v1[32];
-                    tmem_ld32(taddr + c0, v0);
-                    tmem_ld32(taddr + c0 + 32, v1);
-                    tmem_ld_wait();
-                    uint32_t andv = 0xFFFFFFFFu;
-                    const float4 *T4 = reinterpret_cast<const float4 *>(s.T + half * 128 + c0);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float4 tt = T4[j];
-                        andv &= __float_as_uint(__uint_as_float(v0[4 * j]) - tt.x) &
-                                __float_as_uint(__uint_as_float(v0[4 * j + 1]) - tt.y) &
-                                __float_as_uint(__uint_as_float(v0[4 * j + 2]) - tt.z) &
-                                __float_as_uint(__uint_as_float(v0[4 * j + 3]) - tt.w);
-                    }
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float4 tt = T4[8 + j];
-                        andv &= __float_as_uint(__uint_as_float(v1[4 * j]) - tt.x) &
-                                __float_as_uint(__uint_as_float(v1[4 * j + 1]) - tt.y) &
-                                __float_as_uint(__uint_as_float(v1[4 * j + 2]) - tt.z) &
-                                __float_as_uint(__uint_as_float(v1[4 * j + 3]) - tt.w);
-                    }
-                    if (valid && !(andv >> 31)) {
-                        // some column passed the superset test: exact per-row test, enqueue
-                        const uint32_t cb = half * 128 + c0;
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) tc_push(s, __uint_as_float(v0[j]), cb + j, qn, g, rl);
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) tc_push(s, __uint_as_float(v1[j]), cb + 32 + j, qn, g, rl);
-                    }
-                }
+            const float2 m = s.rm[st][r_in_tile + (it.row_begin & 1)];   // (RD ||f||^2, RU e_f)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.empty[st]);
+            const float g = valid ? 0.5f * (m.x - 2.f * nqm * m.y) : INFINITY;
+            const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * kQB + part * 64;
+            uint32_t va[32], vb[32];
+            if (ncol) {
+                tmem_ld32(taddr, va);
+                tmem_ld32(taddr + 32, vb);
+                tmem_ld_wait_regs(va);   // orders every use of va and vb after the wait
+                reg_fence(vb);
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.tempty[buf]);
+            if (ncol && !(a.dbg & 1)) {
+                const float4 *H4 = reinterpret_cast<const float4 *>(s.h + part * 64);
+                float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float4 h = H4[j];
+                    const uint64_t y0 = sub2(pack2(va[4 * j], va[4 * j + 1]), pack2(__float_as_uint(h.x), __float_as_uint(h.y)));
+                    const uint64_t y1 = sub2(pack2(va[4 * j + 2], va[4 * j + 3]), pack2(__float_as_uint(h.z), __float_as_uint(h.w)));
+                    mx0 = max3f(mx0, __uint_as_float((uint32_t)y0), __uint_as_float((uint32_t)(y0 >> 32)));
+                    mx1 = max3f(mx1, __uint_as_float((uint32_t)y1), __uint_as_float((uint32_t)(y1 >> 32)));
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float4 h = H4[8 + j];
+                    const uint64_t y0 = sub2(pack2(vb[4 * j], vb[4 * j + 1]), pack2(__float_as_uint(h.x), __float_as_uint(h.y)));
+                    const uint64_t y1 = sub2(pack2(vb[4 * j + 2], vb[4 * j + 3]), pack2(__float_as_uint(h.z), __float_as_uint(h.w)));
+                    mx0 = max3f(mx0, __uint_as_float((uint32_t)y0), __uint_as_float((uint32_t)(y0 >> 32)));
+                    mx1 = max3f(mx1, __uint_as_float((uint32_t)y1), __uint_as_float((uint32_t)(y1 >> 32)));
+                }
+                // cold path (rare): enqueue exactly the passing columns
+                if (!(a.dbg & 4) && fmaxf(mx0, mx1) >= g) {
+                    uint32_t spill[64];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) { spill[j] = va[j]; spill[32 + j] = vb[j]; }
+                    tc_cold(s, spill, g, part * 64, qn, rl, a.stat_flagged);
+                    if (a.dbg & 8) atomicAdd(&a.prof[part * 4 + quarter], 1ull);
+                }
+            }
+            // the threshold loaded a tile ago: tighten this column if another CTA did better
+            if (rc < qn && gt_prev < lds_u32(&s.tau[rc])) {
+                atomicMin(&s.tau[rc], gt_prev);
+                s.h[rc] = h_of(s.alpha[rc], lds_u32(&s.tau[rc]));
+            }
         }
         named_bar(1, 32 * kEpiWarps);
-        if (ew == 0 && lane == 0) {
+        if (warp == 2 && lane == 0) {
             __threadfence_block();
-            *(volatile unsigned *)&s.closed_at = *(volatile unsigned *)&s.prod;
-            *(volatile int *)&s.closed = 1;
+            sts_u32(&s.closed_at, lds_u32(&s.prod));
+            __threadfence_block();
+            sts_u32(&s.closed, 1u);
         }
     } else {
         // ------------------------------------------------------------ exact re-scoring
         while (true) {
             const unsigned p = atomicAdd(&s.cons_res, 1u);
-            volatile uint32_t *sq = &s.seq[p % kRing];
+            uint32_t *sq = &s.seq[p % kRing];
             bool got = false;
+            uint32_t idle = 0, nap = 64;
             while (true) {
-                if (*sq == p + 1) { got = true; break; }
-                if (*(volatile int *)&s.closed && p >= *(volatile unsigned *)&s.closed_at) break;
-                __nanosleep(32);
+                if (lds_u32(sq) == p + 1) { got = true; break; }
+                if (lds_u32(&s.closed) && p >= lds_u32(&s.closed_at)) break;
+                // idle: now and then import the running thresholds other CTAs
+                // published (any value ever held is a valid bound, so races only loosen h)
+                {
+                    const uint32_t qi = (idle++ * (32 * kExactWarps) + (threadIdx.x - 32 * (2 + kEpiWarps))) % kQB;
+                    if (qi < qn) {
+                        const uint32_t gt = __ldcg(&a.g_tau[(size_t)(q0 + qi) * a.n_sub + it.sub]);
+                        if (gt < lds_u32(&s.tau[qi])) {
+                            atomicMin(&s.tau[qi], gt);
+                            s.h[qi] = h_of(s.alpha[qi], lds_u32(&s.tau[qi]));
+                        }
+                    }
+                }
+                __nanosleep(nap);
+                if (nap < 2048) nap <<= 1;
             }
             if (!got) break;
             __threadfence_block();
             const uint32_t e = s.val[p % kRing];
             __threadfence_block();
-            *sq = p + kRing;
+            sts_u32(sq, p + kRing);
             const uint32_t rl = e >> 8, col = e & 0xFF;
             const uint64_t row = it.row_begin + rl;
             const float4 *qv = reinterpret_cast<const float4 *>(a.queries + (size_t)(q0 + col) * kK);
@@ -284,7 +363,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             }
             const u64 key = ((u64)__float_as_uint(acc) << 32) | (u64)(it.frame_begin + rl);
             u64 *L = lists + (size_t)col * N;
-            if (key < *(volatile u64 *)&L[N - 1]) {
+            if (key < lds_u64(&L[N - 1])) {
                 while (atomicCAS(&s.lock[col], 0, 1) != 0) __nanosleep(16);
                 __threadfence_block();
                 if (key < L[N - 1]) {
@@ -294,6 +373,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                     if (L[N - 1] != kPadKey) {
                         const uint32_t tb = (uint32_t)(L[N - 1] >> 32);
                         atomicMin(&s.tau[col], tb);
+                        s.h[col] = h_of(s.alpha[col], lds_u32(&s.tau[col]));
                         atomicMin(&a.g_tau[(size_t)(q0 + col) * a.n_sub + it.sub], tb);
                     }
                 }
@@ -307,6 +387,12 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     // ---------------------------------------------------------------- teardown
     tc_fence_before();
     __syncthreads();
+    if ((a.dbg & 16) && blockIdx.x == 0)
+        for (uint32_t q = threadIdx.x; q < kQB; q += blockDim.x) {
+            a.prof[16 + q] = __float_as_uint(s.h[q]);
+            a.prof[16 + 256 + q] = s.tau[q];
+            a.prof[16 + 512 + q] = __float_as_uint(s.alpha[q]);
+        }
     if (warp == 1) tmem_dealloc<512>(tmem);
     for (uint32_t i = threadIdx.x; i < qn * N; i += blockDim.x) {
         const uint32_t q = i / N, r = i % N;
@@ -459,7 +545,8 @@ cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q,
 }
 
 uint32_t tc_max_qb(uint32_t N) {
-    uint32_t qb = (uint32_t)(65536 / (N * sizeof(u64)));
+    const size_t budget = 227 * 1024 - sizeof(TcSmem) - 1024;   // what the top-N lists may use
+    uint32_t qb = (uint32_t)(budget / (N * sizeof(u64)));
     qb = qb / 16 * 16;
     if (qb > (uint32_t)kQB) qb = kQB;
     if (qb < 16) qb = 16;
