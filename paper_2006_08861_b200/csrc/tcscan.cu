@@ -292,7 +292,8 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                     mx1 = max3f(mx1, __uint_as_float((uint32_t)y1), __uint_as_float((uint32_t)(y1 >> 32)));
                 }
                 // cold path (rare): enqueue exactly the passing columns
-                if (!(a.dbg & 4) && fmaxf(mx0, mx1) >= g) {
+                if (!(a.dbg & 4) && valid && fmaxf(mx0, mx1) >= g) {   // (rows past the item
+                    // end have g = +inf, which still passes while h = -inf: hence `valid`)
                     uint32_t spill[64];
 #pragma unroll
                     for (int j = 0; j < 32; ++j) { spill[j] = va[j]; spill[32 + j] = vb[j]; }

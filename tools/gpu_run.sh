@@ -1,4 +1,4 @@
-CMD="python tools/tc_experiment.py 100000000 0"
-timeout 300 $CMD > gpurun_out/exp_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tcscan -s 3 -c 1 -o gpurun_out/prof_tc3 $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu=$?
-tail -2 gpurun_out/exp_plain.log
+timeout 1500 python -m pytest tests -m "gpu" -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+tail -2 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --steps 20 --warmup 3 > gpurun_out/bench.log 2>&1; echo bench=$?
+tail -1 gpurun_out/bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['stages_ms'], d['survivor_frac'], d['roofline']['frac'], d['e2e']['value'], d['small_batch'])"
