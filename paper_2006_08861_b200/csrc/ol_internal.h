@@ -19,6 +19,14 @@ constexpr int kAggMax = 8192;         // candidates per bundle in the aggregatio
 constexpr u64 kPadKey = ~0ull;
 constexpr uint32_t kInfBits = 0x7F800000u;  // +inf: "no threshold yet"
 
+// Coarse plane layout: tiles of 32 rows; inside a tile, 16-byte columns of 4
+// coefficients, each column 32 rows x 16 B contiguous.  A warp whose lane i owns
+// row (32 t + i) loads 512 contiguous bytes per LDG.128.  Every subspace starts
+// on a tile boundary (rows padded to a multiple of 32).
+__host__ __device__ __forceinline__ uint64_t coarse_off(uint64_t row, uint32_t k, uint32_t kc) {
+    return (((row >> 5) * (kc >> 2) + (k >> 2)) << 7) + ((row & 31) << 2) + (k & 3);
+}
+
 // One scan work item: a contiguous run of rows of one subspace.
 struct WorkItem {
     uint32_t sub;          // subspace
@@ -42,7 +50,7 @@ struct ScanArgs {
     const float *fine;           // [rows][K - kc] (null when kc == K)
     const float *queries;        // [nq][K]
     const WorkItem *items;
-    const uint32_t *tau0;        // [nq][n_sub] acc bits, or null
+    uint32_t *tau0;              // [nq][n_sub] acc bits (seeded; shared running minimum), or null
     u64 *partial;                // [nq][n_items][N]
     unsigned long long *stat_survivors;  // may be null
     uint32_t nq, n_items, n_qtiles, qt, n_sub, N;
@@ -52,7 +60,7 @@ struct SeedArgs {
     const float *coarse, *fine, *queries;
     const SubInfo *subs;
     uint32_t *tau0;              // [nq][n_sub]
-    uint32_t nq, n_sub, N, samples, kc;
+    uint32_t nq, n_sub, N, samples, kc, splits;   // splits: independent samples per (frame, sub)
 };
 
 struct MergeArgs {
@@ -120,13 +128,17 @@ uint32_t tc_max_qb(uint32_t N);
 cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s);
 cudaError_t launch_scan(int kc, const ScanArgs &a, size_t smem, int grid, cudaStream_t s);
 size_t scan_smem_bytes(uint32_t qt, uint32_t N);
+cudaError_t launch_scan2(int kc, const ScanArgs &a, size_t smem, int grid, cudaStream_t s);
+size_t scan2_smem_bytes(uint32_t qt, uint32_t N, int kc);
+cudaError_t launch_scan3(int kc, const ScanArgs &a, size_t smem, int grid, cudaStream_t s);
+size_t scan3_smem_bytes(uint32_t qt, uint32_t N, int kc);
 cudaError_t launch_merge_chunks(const MergeArgs &a, cudaStream_t s);
 cudaError_t launch_merge_ranks(const RankMergeArgs &a, cudaStream_t s);
 cudaError_t launch_candidates(const CandArgs &a, cudaStream_t s);
 cudaError_t launch_aggregate(const AggArgs &a, cudaStream_t s);
 cudaError_t launch_check_finite(const float *p, uint64_t n, int *flag, cudaStream_t s);
-cudaError_t launch_relayout(const float *src, uint64_t rows, int kc, float *coarse, float *fine,
-                            cudaStream_t s);
+cudaError_t launch_relayout(const float *src, uint64_t rows, uint64_t dst_row0, int kc, float *coarse,
+                            float *fine, cudaStream_t s);
 cudaError_t launch_check_coords(const int32_t *xy, uint64_t rows, int32_t gw, int32_t gh,
                                 int *flag, cudaStream_t s);
 

@@ -78,7 +78,8 @@ struct ol_ctx {
     int64_t opt_chunk = 0, opt_qtile = 0, opt_tau_seed = 1, opt_ctas = 0, opt_time = 0;
     int64_t opt_tc = -1;         // tensor-core filter: -1 auto (>= 32 frames), 0 off, 1 always
     int64_t opt_tc_min_frames = 32;
-    int64_t opt_tc_debug = 0;    // profiling experiments only (results invalid when nonzero)
+    int64_t opt_tc_debug = 0;
+    int64_t opt_scan2 = 1;       // small batches (<= 16 frames per tile) use scan2_kernel    // profiling experiments only (results invalid when nonzero)
     // per-kernel-class CUDA-event timing (option "time_kernels"): pairs recorded on
     // the context stream around each launch; summed and released by ol_get_stat
     enum { T_SEED, T_SCAN, T_MERGE, T_FINAL, T_COUNT };
@@ -269,7 +270,8 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
     OL_CUDA(c, cudaSetDevice(c->device));
     const uint32_t ns = db->n_subspaces;
     std::vector<SubInfo> subs(ns);
-    uint64_t rows = 0;
+    std::vector<uint64_t> src_begin(ns);   // row offset of subspace i in the caller's arrays
+    uint64_t rows = 0, rows_pad = 0;       // device rows: each subspace starts on a 32-row tile
     for (uint32_t i = 0; i < ns; ++i) {
         const uint64_t gs = db->global_sizes[i];
         if (gs == 0 || gs > 0xFFFFFFFEull)
@@ -281,11 +283,13 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
         if (b + n > gs)
             return fail(c, OL_ERR_INVALID_ARGUMENT, "shard [%llu,+%llu) outside subspace %u of %llu",
                         (unsigned long long)b, (unsigned long long)n, i, (unsigned long long)gs);
-        subs[i].row_begin = rows;
+        src_begin[i] = rows;
+        subs[i].row_begin = rows_pad;
         subs[i].count = n;
         subs[i].shard_begin = (uint32_t)b;
         subs[i].global_size = (uint32_t)gs;
         rows += n;
+        rows_pad += (n + 31) / 32 * 32;
     }
     // validate inputs (S:32 finite values; S:102 coords inside the grid)
     if (!db->on_device) {
@@ -301,13 +305,20 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
     }
     free_db(c);
     const int kc = c->kc;
-    OL_CUDA(c, cudaMalloc((void **)&c->coarse, sizeof(float) * (rows ? rows : 1) * kc));
-    if (kc < OL_K) OL_CUDA(c, cudaMalloc((void **)&c->fine, sizeof(float) * (rows ? rows : 1) * (OL_K - kc)));
-    OL_CUDA(c, cudaMalloc((void **)&c->coords, sizeof(int32_t) * 2 * (rows ? rows : 1)));
+    const uint64_t R = rows_pad ? rows_pad : 32;
+    OL_CUDA(c, cudaMalloc((void **)&c->coarse, sizeof(float) * R * kc));
+    OL_CUDA(c, cudaMemsetAsync(c->coarse, 0, sizeof(float) * R * kc, c->stream));   // padding rows = 0
+    if (kc < OL_K) {
+        OL_CUDA(c, cudaMalloc((void **)&c->fine, sizeof(float) * R * (OL_K - kc)));
+        OL_CUDA(c, cudaMemsetAsync(c->fine, 0, sizeof(float) * R * (OL_K - kc), c->stream));
+    }
+    OL_CUDA(c, cudaMalloc((void **)&c->coords, sizeof(int32_t) * 2 * R));
+    OL_CUDA(c, cudaMemsetAsync(c->coords, 0, sizeof(int32_t) * 2 * R, c->stream));
     OL_CUDA(c, cudaMalloc((void **)&c->subs_d, sizeof(SubInfo) * ns));
     const float *src = db->features;
     float *tmp = nullptr;
     if (rows) {
+        const cudaMemcpyKind kind = db->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
         if (db->on_device) {
             OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 2 * sizeof(int), c->stream));
             OL_CUDA(c, launch_check_finite(db->features, rows * OL_K, c->flags_d, c->stream));
@@ -319,23 +330,25 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
             OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 2 * sizeof(int), c->stream));
             if (fl[0]) { free_db(c); return fail(c, OL_ERR_NONFINITE, "device features hold NaN/Inf"); }
             if (fl[1]) { free_db(c); return fail(c, OL_ERR_OUT_OF_RANGE, "device coords outside the grid"); }
-            OL_CUDA(c, cudaMemcpyAsync(c->coords, db->coords, sizeof(int32_t) * 2 * rows,
-                                       cudaMemcpyDeviceToDevice, c->stream));
         } else {
             OL_CUDA(c, cudaMalloc((void **)&tmp, sizeof(float) * rows * OL_K));
             OL_CUDA(c, cudaMemcpyAsync(tmp, db->features, sizeof(float) * rows * OL_K,
                                        cudaMemcpyHostToDevice, c->stream));
-            OL_CUDA(c, cudaMemcpyAsync(c->coords, db->coords, sizeof(int32_t) * 2 * rows,
-                                       cudaMemcpyHostToDevice, c->stream));
             src = tmp;
         }
-        OL_CUDA(c, launch_relayout(src, rows, kc, c->coarse, c->fine, c->stream));
+        for (uint32_t i = 0; i < ns; ++i) {   // subspace i -> its tile-aligned device rows
+            if (!subs[i].count) continue;
+            OL_CUDA(c, cudaMemcpyAsync(c->coords + 2 * subs[i].row_begin, db->coords + 2 * src_begin[i],
+                                       sizeof(int32_t) * 2 * subs[i].count, kind, c->stream));
+            OL_CUDA(c, launch_relayout(src + src_begin[i] * OL_K, subs[i].count, subs[i].row_begin, kc, c->coarse,
+                                       c->fine, c->stream));
+        }
         if (c->opt_tc != 0) {
-            OL_CUDA(c, cudaMalloc(&c->plane16, sizeof(uint16_t) * rows * OL_K));
-            OL_CUDA(c, cudaMalloc((void **)&c->rmeta, sizeof(float2) * (rows + 132)));  // + one tile of pad
-            OL_CUDA(c, cudaMemsetAsync(c->rmeta + rows, 0, sizeof(float2) * 132, c->stream));
+            OL_CUDA(c, cudaMalloc(&c->plane16, sizeof(uint16_t) * rows_pad * OL_K));
+            OL_CUDA(c, cudaMalloc((void **)&c->rmeta, sizeof(float2) * (rows_pad + 132)));  // + a tile of pad
+            OL_CUDA(c, cudaMemsetAsync(c->rmeta + rows_pad, 0, sizeof(float2) * 132, c->stream));
             OL_CUDA(c, cudaMemsetAsync(c->tcstat_d, 0, 4 * sizeof(uint32_t), c->stream));
-            OL_CUDA(c, launch_tc_prep_rows(c->coarse, c->fine, kc, rows, c->plane16, c->rmeta, c->tcstat_d,
+            OL_CUDA(c, launch_tc_prep_rows(c->coarse, c->fine, kc, rows_pad, c->plane16, c->rmeta, c->tcstat_d,
                                            c->tcstat_d + 1, c->stream));
         }
     }
@@ -349,8 +362,8 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
         const float nf = *reinterpret_cast<float *>(&st[0]), amax = *reinterpret_cast<float *>(&st[1]);
         c->nf_max = nf;
         // fp16 operands need |f| well inside the fp16 range, and the row count fits a TMA coordinate
-        c->tc_ok = std::isfinite(nf) && amax < 65000.f && rows < (1ull << 31) &&
-                   make_tc_map(&c->map_rows, c->plane16, rows, 128);
+        c->tc_ok = std::isfinite(nf) && amax < 65000.f && rows_pad < (1ull << 31) &&
+                   make_tc_map(&c->map_rows, c->plane16, rows_pad, 128);
     }
     c->subs = subs;
     c->n_sub = ns;
@@ -474,11 +487,18 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         SeedArgs sa;
         sa.coarse = c->coarse; sa.fine = c->fine; sa.queries = q; sa.subs = c->subs_d;
         sa.tau0 = c->tau0_d; sa.nq = nq; sa.n_sub = c->n_sub; sa.N = N; sa.kc = (uint32_t)c->kc;
-        // a sample of count/8 rows (at most 4096) per subspace; below N rows: no seed
+        // splits x (count/8, at most 4096) rows per subspace, about 64k sampled pairs per
+        // row... i.e. more splits for few frames; below N rows per split: no seed (+inf)
         uint32_t S = 4096;
-        for (auto &s : c->subs) { uint64_t v = s.count / 8; if (v < S) S = (uint32_t)v; }
+        uint64_t minc = ~0ull;
+        for (auto &s : c->subs) { uint64_t v = s.count / 8; if (v < S) S = (uint32_t)v; if (s.count < minc) minc = s.count; }
         sa.samples = S < 1 ? 1 : S;
+        uint32_t splits = 1;
+        while (splits < 16 && (uint64_t)nq * c->n_sub * splits < 148 * 2 &&
+               (uint64_t)sa.samples * splits * 2 * 8 <= minc) splits *= 2;
+        sa.splits = splits;
         TimeScope ts(c, ol_ctx::T_SEED);
+        OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
         OL_LAUNCH(c, launch_tau_seed(sa, c->stream));
     }
     c->used_tc = false;
@@ -510,7 +530,12 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         a.tau0 = seed ? c->tau0_d : nullptr; a.partial = c->partial_d; a.stat_survivors = c->stat_d;
         a.nq = nq; a.n_items = n_items; a.n_qtiles = n_qtiles; a.qt = qt; a.n_sub = c->n_sub; a.N = N;
         TimeScope ts(c, ol_ctx::T_SCAN);
-        OL_LAUNCH(c, launch_scan(c->kc, a, scan_smem_bytes(qt, N), (int)(n_items * n_qtiles), c->stream));
+        if (qt <= 16 && c->opt_scan2 == 2 && c->kc < OL_K)   // few frames: TMA-fed row-pair kernel
+            OL_LAUNCH(c, launch_scan3(c->kc, a, scan3_smem_bytes(qt, N, c->kc), (int)(n_items * n_qtiles), c->stream));
+        else if (qt <= 16 && c->opt_scan2)   // few frames: row-pair f32x2 streaming kernel
+            OL_LAUNCH(c, launch_scan2(c->kc, a, scan2_smem_bytes(qt, N, c->kc), (int)(n_items * n_qtiles), c->stream));
+        else
+            OL_LAUNCH(c, launch_scan(c->kc, a, scan_smem_bytes(qt, N), (int)(n_items * n_qtiles), c->stream));
     }
     MergeArgs ma;
     ma.partial = c->partial_d; ma.subs = c->subs_d; ma.coords = c->coords; ma.records = c->payload_d;
@@ -698,6 +723,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "ctas")) { if (v < 0) goto bad; c->opt_ctas = v; }
     else if (!strcmp(key, "time_kernels")) { if (v != 0 && v != 1) goto bad; c->opt_time = v; }
     else if (!strcmp(key, "tc")) { if (v < -1 || v > 1) goto bad; c->opt_tc = v; }
+    else if (!strcmp(key, "scan2")) { if (v < 0 || v > 2) goto bad; c->opt_scan2 = v; }
     else if (!strcmp(key, "tc_min_frames")) { if (v < 1) goto bad; c->opt_tc_min_frames = v; }
     else if (!strcmp(key, "tc_debug")) { if (v < 0 || v > 31) goto bad; c->opt_tc_debug = v; }
     else return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown option '%s'", key);

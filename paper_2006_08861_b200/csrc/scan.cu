@@ -13,6 +13,7 @@
 // is always >= the true N-th distance, so no true top-N pair is ever pruned.
 // kc == K is the one-pass scan (NK1).
 #include "ol_internal.h"
+#include "tc_ptx.cuh"
 
 namespace ol {
 
@@ -63,10 +64,10 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
         const bool valid = e < it.count;
         const uint64_t row = it.row_begin + (valid ? e : 0);
         float f[KC];
-        const float4 *src = reinterpret_cast<const float4 *>(a.coarse + row * KC);
 #pragma unroll
         for (int k = 0; k < KC / 4; ++k) {
-            float4 v = valid ? __ldg(src + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 *src = reinterpret_cast<const float4 *>(a.coarse + coarse_off(row, 4 * k, KC));
+            float4 v = valid ? __ldg(src) : make_float4(0.f, 0.f, 0.f, 0.f);
             f[4 * k] = v.x; f[4 * k + 1] = v.y; f[4 * k + 2] = v.z; f[4 * k + 3] = v.w;
         }
         for (uint32_t q = 0; q < qn; ++q) {
@@ -139,6 +140,394 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- small-batch scan (NK2s)
+// Same contract as scan_kernel, tuned for few query frames (<= kMaxQT2), the
+// HBM-bound regime: each thread owns a PAIR of rows (r, r + 256) whose coarse
+// coefficients it keeps packed as f32x2 pairs, so every chain step is one FADD2
+// + one FFMA2 for two rows (each lane still the exact RN fp32 chain of R3), the
+// next pair's rows are loaded before the current pair is scored (register
+// double buffering), and query coefficients sit duplicated (q, q) in smem so one
+// LDS.128 feeds two steps.
+constexpr int kMaxQT2 = 16;
+
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+    return ((uint64_t)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ uint64_t f2sub(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+template <int KC>
+__device__ __forceinline__ void load_pair(const float *coarse, const WorkItem &it, uint32_t e0, float4 (&v)[2][KC / 4]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t e = e0 + h * kScanThreads;
+        const bool ok = e < it.count;
+        const uint64_t row = it.row_begin + (ok ? e : 0);
+#pragma unroll
+        for (int k = 0; k < KC / 4; ++k)
+            v[h][k] = ok ? __ldg(reinterpret_cast<const float4 *>(coarse + coarse_off(row, 4 * k, KC)))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// Survivors of one query for a thread's row pair: finish the chain from the fine
+// plane and insert into the warp's list (ballot-serialised, see scan_kernel).
+template <int KC>
+__device__ __noinline__ void scan2_survivors(const ScanArgs &a, const WorkItem &it, const float *qs, u64 *lists,
+                                             uint32_t *tau, uint32_t q, uint32_t q0, uint32_t qt, uint32_t N,
+                                             int warp, int lane, uint32_t e0, uint32_t e1, bool s0, bool s1,
+                                             uint64_t acc2, unsigned long long &survivors) {
+    for (int h = 0; h < 2; ++h) {
+        const bool sv = h ? s1 : s0;
+        const uint32_t e = h ? e1 : e0;
+        float acc = __uint_as_float(h ? (uint32_t)(acc2 >> 32) : (uint32_t)acc2);
+        u64 key = kPadKey;
+        if (sv) {
+            ++survivors;
+            if (KC < kK) {  // fine pass: continue the same chain
+                const uint64_t row = it.row_begin + e;
+                const float4 *fr = reinterpret_cast<const float4 *>(a.fine + row * (kK - KC));
+                const float4 *qv = reinterpret_cast<const float4 *>(qs + q * kK);
+#pragma unroll
+                for (int k = 0; k < (kK - KC) / 4; ++k) {
+                    const float4 x = qv[KC / 4 + k], v = __ldg(fr + k);
+                    acc = chain_step(acc, x.x, v.x);
+                    acc = chain_step(acc, x.y, v.y);
+                    acc = chain_step(acc, x.z, v.z);
+                    acc = chain_step(acc, x.w, v.w);
+                }
+            }
+            key = ((u64)__float_as_uint(acc) << 32) | (u64)(it.frame_begin + e);
+        }
+        u64 *L = lists + ((size_t)warp * qt + q) * N;
+        unsigned m = __ballot_sync(0xffffffffu, key < L[N - 1]);
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            if (lane == l) {
+                const u64 nth = list_insert(L, N, key);
+                if (nth != kPadKey) {
+                    const uint32_t tb = (uint32_t)(nth >> 32);
+                    atomicMin(&tau[q], tb);
+                    // publish: any CTA's N-th is a valid bound for all of them
+                    if (a.tau0) atomicMin(&a.tau0[(size_t)(q0 + q) * a.n_sub + it.sub], tb);
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+template <int KC>
+__global__ void __launch_bounds__(kScanThreads) scan2_kernel(ScanArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t qt = a.qt, N = a.N;
+    float *qs = reinterpret_cast<float *>(smem);                           // [qt][K] (fine part)
+    uint64_t *qd = reinterpret_cast<uint64_t *>(qs + kMaxQT2 * kK);        // [qt][KC] (q, q)
+    uint32_t *tau = reinterpret_cast<uint32_t *>(qd + kMaxQT2 * KC);       // [kMaxQT2]
+    u64 *lists = reinterpret_cast<u64 *>(tau + kMaxQT2);                   // [warps][qt][N]
+
+    const uint32_t item_id = blockIdx.x / a.n_qtiles;
+    const uint32_t qtile = blockIdx.x % a.n_qtiles;
+    const WorkItem it = a.items[item_id];
+    const uint32_t q0 = qtile * qt;
+    const uint32_t qn = min(qt, a.nq - q0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    for (uint32_t i = threadIdx.x; i < kMaxQT2 * kK; i += blockDim.x) {
+        const float v = i < qn * kK ? a.queries[(size_t)q0 * kK + i] : 0.f;
+        qs[i] = v;
+        if ((i % kK) < (uint32_t)KC) qd[(i / kK) * KC + (i % kK)] = f2pack(v, v);
+    }
+    for (uint32_t q = threadIdx.x; q < kMaxQT2; q += blockDim.x)
+        tau[q] = (a.tau0 && q < qn) ? a.tau0[(size_t)(q0 + q) * a.n_sub + it.sub] : kInfBits;
+    for (uint32_t i = threadIdx.x; i < kScanWarps * qt * N; i += blockDim.x) lists[i] = kPadKey;
+    __syncthreads();
+
+    unsigned long long survivors = 0;
+    float4 nxt[2][KC / 4];
+    load_pair<KC>(a.coarse, it, threadIdx.x, nxt);
+    for (uint32_t base = 0; base < it.count; base += 2 * kScanThreads) {
+        uint64_t f2[KC];   // (row0[k], row1[k])
+#pragma unroll
+        for (int k = 0; k < KC / 4; ++k) {
+            f2[4 * k] = f2pack(nxt[0][k].x, nxt[1][k].x);
+            f2[4 * k + 1] = f2pack(nxt[0][k].y, nxt[1][k].y);
+            f2[4 * k + 2] = f2pack(nxt[0][k].z, nxt[1][k].z);
+            f2[4 * k + 3] = f2pack(nxt[0][k].w, nxt[1][k].w);
+        }
+        const uint32_t e0 = base + threadIdx.x, e1 = e0 + kScanThreads;
+        const bool v0 = e0 < it.count, v1 = e1 < it.count;
+        // import the thresholds other CTAs published (valid bounds; races only loosen)
+        if (a.tau0 && threadIdx.x < qn && (base & (8 * kScanThreads - 1)) == 0)
+            atomicMin(&tau[threadIdx.x], __ldcg(&a.tau0[(size_t)(q0 + threadIdx.x) * a.n_sub + it.sub]));
+        if (base + 2 * kScanThreads < it.count) load_pair<KC>(a.coarse, it, e0 + 2 * kScanThreads, nxt);
+        // four query chains at a time for instruction-level parallelism (qd/tau are
+        // padded to kMaxQT2 frames, so the tail group reads harmless values)
+        for (uint32_t qb = 0; qb < qn; qb += 4) {
+            uint64_t acc2[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int k = 0; k < KC / 2; ++k) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const ulonglong2 x = reinterpret_cast<const ulonglong2 *>(qd + (qb + u) * KC)[k];
+                    uint64_t d = f2sub(x.x, f2[2 * k]);
+                    acc2[u] = f2fma(d, d, acc2[u]);
+                    d = f2sub(x.y, f2[2 * k + 1]);
+                    acc2[u] = f2fma(d, d, acc2[u]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t q = qb + u;
+                if (q >= qn) break;
+                const uint32_t tq = tau[q];
+                const bool s0 = v0 && (uint32_t)acc2[u] <= tq, s1 = v1 && (uint32_t)(acc2[u] >> 32) <= tq;
+                if (__any_sync(0xffffffffu, s0 || s1))
+                    scan2_survivors<KC>(a, it, qs, lists, tau, q, q0, qt, N, warp, lane, e0, e1, s0, s1, acc2[u],
+                                        survivors);
+            }
+        }
+    }
+    if (a.stat_survivors) {
+        for (int o = 16; o; o >>= 1) survivors += __shfl_xor_sync(0xffffffffu, survivors, o);
+        if (lane == 0 && survivors) atomicAdd(a.stat_survivors, survivors);
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < qn; q += blockDim.x) {
+        int h[kScanWarps];
+#pragma unroll
+        for (int w = 0; w < kScanWarps; ++w) h[w] = 0;
+        u64 *dst = a.partial + ((size_t)(q0 + q) * a.n_items + item_id) * N;
+        for (uint32_t r = 0; r < N; ++r) {
+            u64 best = kPadKey;
+            int bw = 0;
+#pragma unroll
+            for (int w = 0; w < kScanWarps; ++w) {
+                const u64 v = h[w] < (int)N ? lists[((size_t)w * qt + q) * N + h[w]] : kPadKey;
+                if (v < best) { best = v; bw = w; }
+            }
+            dst[r] = best;
+            if (best != kPadKey) ++h[bw];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- small-batch scan, TMA-fed
+// scan2's arithmetic, but the coarse rows reach shared memory through 1-D bulk
+// copies (cp.async.bulk, UBLKCP) issued by a producer warp into a kStages2-deep
+// mbarrier ring, so bytes in flight no longer cost registers; the 8 consumer
+// warps read their row pairs with LDS.128.
+constexpr int kStages2 = 3;
+constexpr int kRows2 = 2 * kScanThreads;   // rows per stage
+
+template <int KC>
+__global__ void __launch_bounds__(kScanThreads + 32) scan3_kernel(ScanArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t qt = a.qt, N = a.N;
+    float *rows = reinterpret_cast<float *>(smem);                         // [kStages2][kRows2][KC]
+    uint64_t *full = reinterpret_cast<uint64_t *>(rows + kStages2 * kRows2 * KC);
+    uint64_t *empty = full + kStages2;
+    float *qs = reinterpret_cast<float *>(empty + kStages2);               // [qt][K]
+    uint64_t *qd = reinterpret_cast<uint64_t *>(qs + kMaxQT2 * kK);        // [qt][KC] (q, q)
+    uint32_t *tau = reinterpret_cast<uint32_t *>(qd + kMaxQT2 * KC);       // [kMaxQT2]
+    u64 *lists = reinterpret_cast<u64 *>(tau + kMaxQT2);                   // [warps][qt][N]
+
+    const uint32_t item_id = blockIdx.x / a.n_qtiles;
+    const uint32_t qtile = blockIdx.x % a.n_qtiles;
+    const WorkItem it = a.items[item_id];
+    const uint32_t q0 = qtile * qt;
+    const uint32_t qn = min(qt, a.nq - q0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t n_stages_total = (it.count + kRows2 - 1) / kRows2;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages2; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], kScanWarps); }
+        tc::fence_mbar_init();
+    }
+    for (uint32_t i = threadIdx.x; i < qn * kK; i += blockDim.x) {
+        const float v = a.queries[(size_t)q0 * kK + i];
+        qs[i] = v;
+        if ((i % kK) < (uint32_t)KC) qd[(i / kK) * KC + (i % kK)] = f2pack(v, v);
+    }
+    for (uint32_t q = threadIdx.x; q < kMaxQT2; q += blockDim.x)
+        tau[q] = (a.tau0 && q < qn) ? a.tau0[(size_t)(q0 + q) * a.n_sub + it.sub] : kInfBits;
+    for (uint32_t i = threadIdx.x; i < kScanWarps * qt * N; i += blockDim.x) lists[i] = kPadKey;
+    __syncthreads();
+
+    if (warp == kScanWarps) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            for (uint32_t t = 0; t < n_stages_total; ++t) {
+                const uint32_t st = t % kStages2;
+                if (t >= kStages2) tc::mbar_wait_sleep(&empty[st], ((t / kStages2) - 1) & 1);
+                // whole 32-row tiles (the plane is padded to tiles, so this stays in bounds)
+                const uint32_t nrows = (min((uint32_t)kRows2, it.count - t * kRows2) + 31) & ~31u;
+                const uint32_t bytes = nrows * KC * sizeof(float);
+                tc::mbar_expect_tx(&full[st], bytes);
+                tc::bulk_load(rows + (size_t)st * kRows2 * KC,
+                              a.coarse + coarse_off(it.row_begin + (uint64_t)t * kRows2, 0, KC), bytes, &full[st]);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ consumers
+        unsigned long long survivors = 0;
+        for (uint32_t t = 0; t < n_stages_total; ++t) {
+            const uint32_t st = t % kStages2, base = t * kRows2;
+            const uint32_t e0 = base + threadIdx.x, e1 = e0 + kScanThreads;
+            const bool v0 = e0 < it.count, v1 = e1 < it.count;
+            if (a.tau0 && threadIdx.x < qn && (t & 7) == 0)   // import published thresholds
+                atomicMin(&tau[threadIdx.x], __ldcg(&a.tau0[(size_t)(q0 + threadIdx.x) * a.n_sub + it.sub]));
+            tc::mbar_wait(&full[st], (t / kStages2) & 1);
+            uint64_t f2[KC];   // (row0[k], row1[k])
+            {
+                const float *sb = rows + (size_t)st * kRows2 * KC;
+#pragma unroll
+                for (int k = 0; k < KC / 4; ++k) {
+                    const float4 x = v0 ? *reinterpret_cast<const float4 *>(sb + coarse_off(threadIdx.x, 4 * k, KC))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float4 y = v1 ? *reinterpret_cast<const float4 *>(sb + coarse_off(threadIdx.x + kScanThreads, 4 * k, KC))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                    f2[4 * k] = f2pack(x.x, y.x); f2[4 * k + 1] = f2pack(x.y, y.y);
+                    f2[4 * k + 2] = f2pack(x.z, y.z); f2[4 * k + 3] = f2pack(x.w, y.w);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&empty[st]);
+            for (uint32_t q = 0; q < qn; ++q) {
+                const ulonglong2 *qq = reinterpret_cast<const ulonglong2 *>(qd + q * KC);
+                uint64_t acc2 = 0;
+#pragma unroll
+                for (int k = 0; k < KC / 2; ++k) {
+                    const ulonglong2 x = qq[k];
+                    uint64_t d = f2sub(x.x, f2[2 * k]);
+                    acc2 = f2fma(d, d, acc2);
+                    d = f2sub(x.y, f2[2 * k + 1]);
+                    acc2 = f2fma(d, d, acc2);
+                }
+                const uint32_t tq = tau[q];
+                const bool s0 = v0 && (uint32_t)acc2 <= tq, s1 = v1 && (uint32_t)(acc2 >> 32) <= tq;
+                if (__any_sync(0xffffffffu, s0 || s1)) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const bool sv = h ? s1 : s0;
+                        const uint32_t e = h ? e1 : e0;
+                        float acc = __uint_as_float(h ? (uint32_t)(acc2 >> 32) : (uint32_t)acc2);
+                        u64 key = kPadKey;
+                        if (sv) {
+                            ++survivors;
+                            if (KC < kK) {
+                                const uint64_t row = it.row_begin + e;
+                                const float4 *fr = reinterpret_cast<const float4 *>(a.fine + row * (kK - KC));
+                                const float4 *qv = reinterpret_cast<const float4 *>(qs + q * kK);
+#pragma unroll
+                                for (int k = 0; k < (kK - KC) / 4; ++k) {
+                                    const float4 x = qv[KC / 4 + k], v = __ldg(fr + k);
+                                    acc = chain_step(acc, x.x, v.x);
+                                    acc = chain_step(acc, x.y, v.y);
+                                    acc = chain_step(acc, x.z, v.z);
+                                    acc = chain_step(acc, x.w, v.w);
+                                }
+                            }
+                            key = ((u64)__float_as_uint(acc) << 32) | (u64)(it.frame_begin + e);
+                        }
+                        u64 *L = lists + ((size_t)warp * qt + q) * N;
+                        unsigned m = __ballot_sync(0xffffffffu, key < L[N - 1]);
+                        while (m) {
+                            const int l = __ffs(m) - 1;
+                            m &= m - 1;
+                            if (lane == l) {
+                                const u64 nth = list_insert(L, N, key);
+                                if (nth != kPadKey) {
+                                    const uint32_t tb = (uint32_t)(nth >> 32);
+                                    atomicMin(&tau[q], tb);
+                                    if (a.tau0) atomicMin(&a.tau0[(size_t)(q0 + q) * a.n_sub + it.sub], tb);
+                                }
+                            }
+                            __syncwarp();
+                        }
+                    }
+                }
+            }
+        }
+        if (a.stat_survivors) {
+            for (int o = 16; o; o >>= 1) survivors += __shfl_xor_sync(0xffffffffu, survivors, o);
+            if (lane == 0 && survivors) atomicAdd(a.stat_survivors, survivors);
+        }
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < qn; q += blockDim.x) {
+        int h[kScanWarps];
+#pragma unroll
+        for (int w = 0; w < kScanWarps; ++w) h[w] = 0;
+        u64 *dst = a.partial + ((size_t)(q0 + q) * a.n_items + item_id) * N;
+        for (uint32_t r = 0; r < N; ++r) {
+            u64 best = kPadKey;
+            int bw = 0;
+#pragma unroll
+            for (int w = 0; w < kScanWarps; ++w) {
+                const u64 v = h[w] < (int)N ? lists[((size_t)w * qt + q) * N + h[w]] : kPadKey;
+                if (v < best) { best = v; bw = w; }
+            }
+            dst[r] = best;
+            if (best != kPadKey) ++h[bw];
+        }
+    }
+}
+
+size_t scan3_smem_bytes(uint32_t qt, uint32_t N, int kc) {
+    return sizeof(float) * kStages2 * kRows2 * kc + 2 * kStages2 * sizeof(uint64_t) + sizeof(float) * kMaxQT2 * kK +
+           sizeof(uint64_t) * kMaxQT2 * kc + sizeof(uint32_t) * kMaxQT2 + sizeof(u64) * kScanWarps * qt * N;
+}
+
+cudaError_t launch_scan3(int kc, const ScanArgs &a, size_t smem, int grid, cudaStream_t s) {
+    switch (kc) {
+#define OL_SCAN3_CASE(KC)                                                                     \
+    case KC:                                                                                  \
+        cudaFuncSetAttribute(scan3_kernel<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                             (int)smem);                                                      \
+        scan3_kernel<KC><<<grid, kScanThreads + 32, smem, s>>>(a);                            \
+        break;
+        OL_SCAN3_CASE(8)
+        OL_SCAN3_CASE(16)
+        OL_SCAN3_CASE(32)
+#undef OL_SCAN3_CASE
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+size_t scan2_smem_bytes(uint32_t qt, uint32_t N, int kc) {
+    return sizeof(float) * kMaxQT2 * kK + sizeof(uint64_t) * kMaxQT2 * kc + sizeof(uint32_t) * kMaxQT2 +
+           sizeof(u64) * kScanWarps * qt * N;
+}
+
+cudaError_t launch_scan2(int kc, const ScanArgs &a, size_t smem, int grid, cudaStream_t s) {
+    switch (kc) {
+#define OL_SCAN2_CASE(KC)                                                                     \
+    case KC:                                                                                  \
+        cudaFuncSetAttribute(scan2_kernel<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                             (int)smem);                                                      \
+        scan2_kernel<KC><<<grid, kScanThreads, smem, s>>>(a);                                 \
+        break;
+        OL_SCAN2_CASE(8)
+        OL_SCAN2_CASE(16)
+        OL_SCAN2_CASE(32)
+        OL_SCAN2_CASE(64)
+#undef OL_SCAN2_CASE
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_scan(int kc, const ScanArgs &a, size_t smem, int grid, cudaStream_t s) {
     switch (kc) {
 #define OL_SCAN_CASE(KC)                                                                      \
@@ -167,24 +556,22 @@ constexpr int kSeedMax = 4096;
 __global__ void __launch_bounds__(kSeedThreads) tau_seed_kernel(SeedArgs a) {
     __shared__ uint32_t v[kSeedMax];
     __shared__ float qs[kK];
-    const uint32_t q = blockIdx.x / a.n_sub, i = blockIdx.x % a.n_sub;
+    const uint32_t split = blockIdx.x % a.splits;
+    const uint32_t q = (blockIdx.x / a.splits) / a.n_sub, i = (blockIdx.x / a.splits) % a.n_sub;
     const SubInfo si = a.subs[i];
     const uint32_t S = (uint32_t)min((uint64_t)a.samples, si.count);
     if (threadIdx.x < kK) qs[threadIdx.x] = a.queries[(size_t)q * kK + threadIdx.x];
     __syncthreads();
-    if (S < a.N) {
-        if (threadIdx.x == 0) a.tau0[(size_t)q * a.n_sub + i] = kInfBits;
-        return;
-    }
+    if (S < a.N) return;   // the caller pre-filled +inf
     uint32_t P = 1;
     while (P < S) P <<= 1;
     for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
         uint32_t val = 0xFFFFFFFFu;
         if (s < S) {
-            const uint64_t row = si.row_begin + (uint64_t)s * si.count / S;
-            const float *c = a.coarse + row * a.kc;
+            // split j takes the j-th of `splits` interleaved sample grids
+            const uint64_t row = si.row_begin + (((uint64_t)s * a.splits + split) * si.count) / ((uint64_t)S * a.splits);
             float acc = 0.f;
-            for (uint32_t k = 0; k < a.kc; ++k) acc = chain_step(acc, qs[k], c[k]);
+            for (uint32_t k = 0; k < a.kc; ++k) acc = chain_step(acc, qs[k], a.coarse[coarse_off(row, k, a.kc)]);
             if (a.kc < (uint32_t)kK) {
                 const float *f = a.fine + row * (kK - a.kc);
                 for (uint32_t k = a.kc; k < (uint32_t)kK; ++k) acc = chain_step(acc, qs[k], f[k - a.kc]);
@@ -207,30 +594,35 @@ __global__ void __launch_bounds__(kSeedThreads) tau_seed_kernel(SeedArgs a) {
             __syncthreads();
         }
     }
-    if (threadIdx.x == 0) a.tau0[(size_t)q * a.n_sub + i] = v[a.N - 1];
+    // every split's N-th smallest is an upper bound of the true N-th: keep the least
+    if (threadIdx.x == 0) atomicMin(&a.tau0[(size_t)q * a.n_sub + i], v[a.N - 1]);
 }
 
 cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s) {
-    tau_seed_kernel<<<a.nq * a.n_sub, kSeedThreads, 0, s>>>(a);
+    tau_seed_kernel<<<a.nq * a.n_sub * a.splits, kSeedThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ upload helpers
-__global__ void relayout_kernel(const float *src, uint64_t rows, int kc, float *coarse,
+// [rows][64] source rows -> tiled coarse plane (rows dst_row0 ..) + row-major fine plane
+__global__ void relayout_kernel(const float *src, uint64_t rows, uint64_t dst_row0, int kc, float *coarse,
                                 float *fine) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < rows * kK;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t r = i / kK;
-        int k = (int)(i % kK);
-        float v = src[i];
-        if (k < kc) coarse[r * kc + k] = v;
-        else fine[r * (kK - kc) + (k - kc)] = v;
+        const uint64_t r = i / kK, d = dst_row0 + r;
+        const int k = (int)(i % kK);
+        const float v = src[i];
+        if (k < kc) coarse[coarse_off(d, k, kc)] = v;
+        else fine[d * (kK - kc) + (k - kc)] = v;
     }
 }
 
-cudaError_t launch_relayout(const float *src, uint64_t rows, int kc, float *coarse, float *fine,
-                            cudaStream_t s) {
-    relayout_kernel<<<148 * 8, 256, 0, s>>>(src, rows, kc, coarse, fine);
+cudaError_t launch_relayout(const float *src, uint64_t rows, uint64_t dst_row0, int kc, float *coarse,
+                            float *fine, cudaStream_t s) {
+    uint64_t blocks = (rows * kK + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks == 0) blocks = 1;
+    relayout_kernel<<<(unsigned)blocks, 256, 0, s>>>(src, rows, dst_row0, kc, coarse, fine);
     return cudaGetLastError();
 }
 

@@ -347,10 +347,10 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             const uint32_t rl = e >> 8, col = e & 0xFF;
             const uint64_t row = it.row_begin + rl;
             const float4 *qv = reinterpret_cast<const float4 *>(a.queries + (size_t)(q0 + col) * kK);
-            const float4 *cr = reinterpret_cast<const float4 *>(a.coarse + row * a.kc);
             float acc = 0.f;
             for (uint32_t k4 = 0; k4 < a.kc / 4; ++k4) {
-                const float4 x = __ldg(qv + k4), f = __ldg(cr + k4);
+                const float4 x = __ldg(qv + k4);
+                const float4 f = __ldg(reinterpret_cast<const float4 *>(a.coarse + coarse_off(row, 4 * k4, a.kc)));
                 acc = chain_step_tc(acc, x.x, f.x); acc = chain_step_tc(acc, x.y, f.y);
                 acc = chain_step_tc(acc, x.z, f.z); acc = chain_step_tc(acc, x.w, f.w);
             }
@@ -418,8 +418,8 @@ __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int 
         float amax = 0.f;
         __half2 *dst = reinterpret_cast<__half2 *>(plane + r * kK);
         for (int k = 0; k < kK; k += 2) {
-            const float f0 = k < kc ? coarse[r * kc + k] : fine[r * (kK - kc) + (k - kc)];
-            const float f1 = k + 1 < kc ? coarse[r * kc + k + 1] : fine[r * (kK - kc) + (k + 1 - kc)];
+            const float f0 = k < kc ? coarse[coarse_off(r, k, kc)] : fine[r * (kK - kc) + (k - kc)];
+            const float f1 = k + 1 < kc ? coarse[coarse_off(r, k + 1, kc)] : fine[r * (kK - kc) + (k + 1 - kc)];
             const __half h0 = __float2half_rn(f0), h1 = __float2half_rn(f1);
             dst[k / 2] = __halves2half2(h0, h1);
             const double d0 = (double)f0 - (double)__half2float(h0), d1 = (double)f1 - (double)__half2float(h1);
