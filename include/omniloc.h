@@ -233,6 +233,39 @@ OL_API ol_status ol_aggregate(ol_ctx *ctx, uint32_t n_bundles, const uint32_t *o
 OL_API ol_status ol_select_window(uint32_t n_frames, uint32_t m, uint32_t M, uint32_t *first,
                            uint32_t *len);
 
+/* ---- NEXT-1: shift-resolved re-scoring and heading ------------------------ */
+
+/* Upload the omnidirectional profiles ("one-dimensional omnidirectional
+ * vector"; W azimuth columns, fp32) of this rank's database rows, in the same
+ * subspace / shard order as ol_upload_db's features ([rows][W], host or device).
+ * Replaces previous profiles; synchronous.  Errors: NOT_READY (no database),
+ * INVALID_ARGUMENT (W outside 8..1024, NULL), NONFINITE, OOM, CUDA. */
+OL_API ol_status ol_upload_profiles(ol_ctx *ctx, const float *profiles, uint32_t W, int32_t on_device);
+
+/* For every candidate of the last finalized query: the circular shift s in
+ * [0, W) minimising the fp32 chain  acc_s = +0; for w = 0..W-1:
+ * d = RN32(q[(w+s) mod W] - p[w]); acc_s = fma32(d, d, acc_s)  between the query
+ * frame's profile q and the candidate's database profile p (the north star's
+ * "score ... over all circular shifts"), and that minimum; ties -> smallest s.
+ * s is the heading difference in columns (2 pi s / W radians).
+ * query_profiles: [n_bundles * M][W], host or device.  Candidates whose frame
+ * lies in another rank's shard get the key INT64_MAX, so ranks combine with a
+ * MIN reduction over ol_shift_keys.  Asynchronous.  Errors: NOT_READY (no
+ * finalized query or no profiles), INVALID_ARGUMENT, NONFINITE (host input), CUDA. */
+OL_API ol_status ol_shift_rescore(ol_ctx *ctx, const float *query_profiles, int32_t on_device);
+
+/* Device array (owned by the context) of the last ol_shift_rescore, one key per
+ * candidate in candidate order: (bits(min acc) << 32) | s, or INT64_MAX. */
+OL_API ol_status ol_shift_keys(ol_ctx *ctx, uint64_t **dev_keys, uint64_t *count);
+
+/* Copy those keys to `dst` (device memory, >= 8 bytes per candidate), stream-ordered;
+ * e.g. into a buffer the caller MIN-reduces across ranks. */
+OL_API ol_status ol_shift_keys_copy(ol_ctx *ctx, void *dst);
+
+/* Host copy of the keys as shift[i], dist2[i] (dist2 = +inf, shift = UINT32_MAX
+ * for INT64_MAX keys).  Synchronises.  Errors: NOT_READY, INVALID_ARGUMENT, CUDA. */
+OL_API ol_status ol_get_shifts(ol_ctx *ctx, uint32_t *shift, float *dist2, uint64_t capacity);
+
 /* ---- tuning / introspection (never changes results) ---------------------- */
 
 /* Launch-shape knobs for schedule-independence tests and tuning:

@@ -66,7 +66,7 @@ def lib():
         L.oracle_aggregate.argtypes = [i64, P, i32, dbl, dbl, dbl, P, P, P, P, P, P, P, P]
         L.oracle_aggregate.restype = i32
         L.oracle_shift_distance.argtypes = [P, P, i32, P]
-        L.oracle_shift_distance.restype = dbl
+        L.oracle_shift_distance.restype = flt
         _lib = L
     return _lib
 
@@ -197,8 +197,9 @@ def aggregate(xy, top_c: int = 10, toler_per: float = 0.2, radius_m: float = 3.0
 
 
 def shift_distance(q, d):
-    """min over circular shifts s of ||rot(q, s) - d||^2 and its smallest argmin."""
-    q = _c(q, np.float64); d = _c(d, np.float64)
+    """min over circular shifts s of the fp32 chain sum_w (q[(w+s) mod W] - d[w])^2
+    and its smallest argmin (NEXT-1; DESIGN R3/R21)."""
+    q = _c(q, np.float32); d = _c(d, np.float32)
     am = ctypes.c_int(0)
     v = lib().oracle_shift_distance(_p(q), _p(d), q.shape[0], ctypes.byref(am))
-    return v, am.value
+    return np.float32(v), am.value

@@ -306,19 +306,22 @@ int oracle_aggregate(int64_t total, const int32_t *xy, int top_c, double toler_p
 }
 
 /* ------------------------------------------------------------------------ */
-/* NEXT-1: explicit circular-shift distance between two          */
-/* profiles, min over s of sum_w (q[(w+s) mod W] - d[w])^2 and the smallest  */
-/* argmin s.  The north star's "score every entry over all circular shifts"; */
-/* P:121 motivates rotation.  binary64, plain double loop.                    */
+/* NEXT-1: explicit circular-shift distance between two           */
+/* omnidirectional profiles -- the north star's "score ... over all circular  */
+/* shifts (rotations)", P:121 ("FFT magnitude ... rotation-invariant" is the  */
+/* descriptor this complements).  For every shift s = 0..W-1 the same fp32    */
+/* fixed-order chain as oracle_acc (DESIGN R3) over w = 0..W-1 of             */
+/* d = RN32(q[(w+s) mod W] - p[w]); returns the minimum and its smallest      */
+/* argmin (a rotation of the camera heading by s columns).                    */
 /* ------------------------------------------------------------------------ */
-double oracle_shift_distance(const double *q, const double *d, int W, int *argmin) {
-    double best = INFINITY;
+float oracle_shift_distance(const float *q, const float *p, int W, int *argmin) {
+    float best = INFINITY;
     int bs = 0;
     for (int s = 0; s < W; ++s) {
-        double acc = 0.0;
+        float acc = 0.0f;
         for (int w = 0; w < W; ++w) {
-            double e = q[(w + s) % W] - d[w];
-            acc += e * e;
+            float d = q[(w + s) % W] - p[w];
+            acc = fmaf(d, d, acc);
         }
         if (acc < best) { best = acc; bs = s; }
     }

@@ -101,6 +101,11 @@ def lib():
             "ol_aggregate": ([P, u32, P, P, i32, ctypes.POINTER(ol_params), P], i32),
             "ol_select_window": ([u32, u32, u32, ctypes.POINTER(u32), ctypes.POINTER(u32)], i32),
             "ol_set_option": ([P, ctypes.c_char_p, i64], i32),
+            "ol_upload_profiles": ([P, P, u32, i32], i32),
+            "ol_shift_rescore": ([P, P, i32], i32),
+            "ol_shift_keys": ([P, ctypes.POINTER(P), ctypes.POINTER(u64)], i32),
+            "ol_get_shifts": ([P, P, P, u64], i32),
+            "ol_shift_keys_copy": ([P, P], i32),
             "ol_get_stat": ([P, ctypes.c_char_p, ctypes.POINTER(i64)], i32),
         }
         for name, (args, res) in sig.items():
@@ -329,6 +334,37 @@ class Engine:
                                     ctypes.c_void_p(xy.ctypes.data), 0, ctypes.byref(p),
                                     ctypes.c_void_p(out.ctypes.data)))
         return out
+
+    # ---------------------------------------------------------------- NEXT-1
+    def upload_profiles(self, profiles):
+        """This rank's database profiles [rows][W] fp32 (same order as upload())."""
+        self.sync_stream()
+        pp, pdev = _ptr(profiles)
+        self._ck(lib().ol_upload_profiles(self._h, ctypes.c_void_p(pp), int(profiles.shape[1]), pdev))
+
+    def shift_rescore(self, query_profiles):
+        """Heading of every candidate of the last query: -> (shift u32, dist2 f32) arrays.
+        query_profiles [B][M][W] (or [B*M][W]) fp32, host or device.  With world > 1 the
+        per-rank keys are MIN-reduced over the process group."""
+        self.sync_stream()
+        qp, qdev = _ptr(query_profiles)
+        self._ck(lib().ol_shift_rescore(self._h, ctypes.c_void_p(qp), qdev))
+        n = self.candidate_count()
+        if self.world > 1:
+            torch = self._torch
+            import torch.distributed as dist
+            keys = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
+            self._ck(lib().ol_shift_keys_copy(self._h, ctypes.c_void_p(keys.data_ptr())))
+            dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=self.group)
+            keys = keys[:n]
+            k = keys.cpu().numpy().view(np.uint64)
+            shift = (k & 0xFFFFFFFF).astype(np.uint32)
+            dist2 = (k >> 32).astype(np.uint32).view(np.float32)
+            return shift, dist2
+        shift = np.empty(n, np.uint32); dist2 = np.empty(n, np.float32)
+        self._ck(lib().ol_get_shifts(self._h, ctypes.c_void_p(shift.ctypes.data),
+                                     ctypes.c_void_p(dist2.ctypes.data), n))
+        return shift, dist2
 
     def set_option(self, key: str, value: int):
         self._ck(lib().ol_set_option(self._h, key.encode(), int(value)))

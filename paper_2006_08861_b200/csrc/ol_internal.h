@@ -114,7 +114,20 @@ struct TcScanArgs {
     unsigned long long *prof;     // [16] cycle counters (dbg & 8)
 };
 
+constexpr u64 kShiftPad = 0x7FFFFFFFFFFFFFFFull;   // "not scored on this rank" (MIN-reducible)
+
+struct ShiftArgs {
+    const ol_candidate *cand;
+    const SubInfo *subs;
+    const float *prof;            // [rows][W] database profiles (tile-padded row index)
+    const float *qprof;           // [nq][W] query profiles
+    u64 *keys;                    // [n_cand]
+    uint64_t n_cand;
+    uint32_t W, M;
+};
+
 // launchers (return cudaGetLastError())
+cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s);
 cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, uint64_t rows, void *plane,
                                 float2 *rmeta, uint32_t *nf_max, uint32_t *maxabs, cudaStream_t s);
 cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float2 *qmeta,

@@ -31,7 +31,7 @@ struct ol_ctx {
     // database
     bool db_ready = false;
     uint32_t n_sub = 0;
-    uint64_t rows = 0;
+    uint64_t rows = 0, rows_pad = 0;
     int32_t grid_w = 0, grid_h = 0;
     std::vector<SubInfo> subs;
     SubInfo *subs_d = nullptr;
@@ -47,6 +47,11 @@ struct ol_ctx {
     void *q16 = nullptr; size_t q16_cap = 0;
     float2 *qmeta = nullptr; size_t qmeta_cap = 0;
     bool used_tc = false;
+    // NEXT-1 profiles and shift keys
+    float *prof = nullptr; uint32_t prof_W = 0;
+    float *qprof_d = nullptr; size_t qprof_cap = 0;
+    u64 *shift_keys = nullptr; size_t shift_cap = 0;
+    bool shift_ready = false;
     // work items (cached per chunk size)
     std::vector<WorkItem> items;
     WorkItem *items_d = nullptr;
@@ -161,7 +166,8 @@ static ol_status check_params(ol_ctx *c, const ol_params *p, bool need_agg) {
 
 static void free_db(ol_ctx *c) {
     cudaFree(c->coarse); cudaFree(c->fine); cudaFree(c->coords); cudaFree(c->subs_d);
-    cudaFree(c->plane16); cudaFree(c->rmeta);
+    cudaFree(c->plane16); cudaFree(c->rmeta); cudaFree(c->prof);
+    c->prof = nullptr; c->prof_W = 0;
     c->coarse = c->fine = nullptr; c->coords = nullptr; c->subs_d = nullptr;
     c->plane16 = nullptr; c->rmeta = nullptr; c->tc_ok = false;
     c->db_ready = false;
@@ -217,7 +223,7 @@ void ol_destroy(ol_ctx *c) {
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
     cudaFree(c->prefix_d); cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
     cudaFree(c->flags_d); cudaFree(c->stat_d); cudaFree(c->tcstat_d); cudaFree(c->prof_d);
-    cudaFree(c->q16); cudaFree(c->qmeta);
+    cudaFree(c->q16); cudaFree(c->qmeta); cudaFree(c->qprof_d); cudaFree(c->shift_keys);
     for (auto &v : c->ev)
         for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -366,6 +372,7 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
                    make_tc_map(&c->map_rows, c->plane16, rows_pad, 128);
     }
     c->subs = subs;
+    c->rows_pad = rows_pad;
     c->n_sub = ns;
     c->rows = rows;
     c->grid_w = db->grid_w;
@@ -430,6 +437,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     OL_CUDA(c, cudaSetDevice(c->device));
     c->launches = 0;
     c->q_ready = c->finalized = false;
+    c->shift_ready = false;
 
     // launch shape (results never depend on it): tensor-core filter or CUDA-core
     // scan, query tile, chunk size
@@ -712,6 +720,102 @@ ol_status ol_aggregate(ol_ctx *c, uint32_t nb, const uint32_t *offsets, const in
     st = check_flags(c);
     c->finalized = false;  // est_d now holds these estimates, not the last query's
     return st;
+}
+
+// ---------------------------------------------------------------- NEXT-1 shift re-scoring
+ol_status ol_upload_profiles(ol_ctx *c, const float *profiles, uint32_t W, int32_t on_device) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->db_ready) return fail(c, OL_ERR_NOT_READY, "upload the database first");
+    if (!profiles || W < 8 || W > 1024) return fail(c, OL_ERR_INVALID_ARGUMENT, "W=%u outside 8..1024", W);
+    OL_CUDA(c, cudaSetDevice(c->device));
+    if (!on_device) {
+        for (uint64_t t = 0; t < c->rows * W; ++t)
+            if (!std::isfinite(profiles[t]))
+                return fail(c, OL_ERR_NONFINITE, "profile value %llu is not finite", (unsigned long long)t);
+    } else {
+        OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, sizeof(int), c->stream));
+        OL_CUDA(c, launch_check_finite(profiles, c->rows * W, c->flags_d, c->stream));
+        int fl = 0;
+        OL_CUDA(c, cudaMemcpyAsync(&fl, c->flags_d, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        OL_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (fl) return fail(c, OL_ERR_NONFINITE, "device profiles hold NaN/Inf");
+    }
+    cudaFree(c->prof);
+    c->prof = nullptr;
+    c->prof_W = 0;
+    const uint64_t R = c->rows_pad ? c->rows_pad : 32;
+    OL_CUDA(c, cudaMalloc((void **)&c->prof, sizeof(float) * R * W));
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    uint64_t src = 0;
+    for (auto &s : c->subs) {   // same tile-aligned row placement as the features
+        if (s.count)
+            OL_CUDA(c, cudaMemcpyAsync(c->prof + s.row_begin * W, profiles + src * W, sizeof(float) * s.count * W,
+                                       kind, c->stream));
+        src += s.count;
+    }
+    OL_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->prof_W = W;
+    return OL_OK;
+}
+
+ol_status ol_shift_rescore(ol_ctx *c, const float *qprof, int32_t on_device) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->finalized) return fail(c, OL_ERR_NOT_READY, "no finalized query");
+    if (!c->prof) return fail(c, OL_ERR_NOT_READY, "no profiles uploaded");
+    if (!qprof) return fail(c, OL_ERR_INVALID_ARGUMENT, "query_profiles is NULL");
+    OL_CUDA(c, cudaSetDevice(c->device));
+    const uint32_t W = c->prof_W;
+    const float *qp = qprof;
+    if (!on_device) {
+        for (uint64_t t = 0; t < (uint64_t)c->nq * W; ++t)
+            if (!std::isfinite(qprof[t]))
+                return fail(c, OL_ERR_NONFINITE, "query profile value %llu is not finite", (unsigned long long)t);
+        OL_CUDA(c, grow(&c->qprof_d, &c->qprof_cap, (size_t)c->nq * W));
+        OL_CUDA(c, cudaMemcpyAsync(c->qprof_d, qprof, sizeof(float) * c->nq * W, cudaMemcpyHostToDevice, c->stream));
+        qp = c->qprof_d;
+    }
+    OL_CUDA(c, grow(&c->shift_keys, &c->shift_cap, c->n_cand));
+    ShiftArgs sa;
+    sa.cand = c->cand_d; sa.subs = c->subs_d; sa.prof = c->prof; sa.qprof = qp; sa.keys = c->shift_keys;
+    sa.n_cand = c->n_cand; sa.W = W; sa.M = c->M;
+    if (c->n_cand) OL_LAUNCH(c, launch_shift(sa, c->stream));
+    c->shift_ready = true;
+    return OL_OK;
+}
+
+ol_status ol_shift_keys(ol_ctx *c, uint64_t **dev_keys, uint64_t *count) {
+    if (!c || !dev_keys || !count) return fail(c, OL_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!c->shift_ready) return fail(c, OL_ERR_NOT_READY, "no shift re-scoring");
+    *dev_keys = reinterpret_cast<uint64_t *>(c->shift_keys);
+    *count = c->n_cand;
+    return OL_OK;
+}
+
+ol_status ol_shift_keys_copy(ol_ctx *c, void *dst) {
+    if (!c || !dst) return fail(c, OL_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!c->shift_ready) return fail(c, OL_ERR_NOT_READY, "no shift re-scoring");
+    OL_CUDA(c, cudaSetDevice(c->device));
+    if (c->n_cand)
+        OL_CUDA(c, cudaMemcpyAsync(dst, c->shift_keys, sizeof(u64) * c->n_cand, cudaMemcpyDeviceToDevice, c->stream));
+    return OL_OK;
+}
+
+ol_status ol_get_shifts(ol_ctx *c, uint32_t *shift, float *dist2, uint64_t capacity) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->shift_ready) return fail(c, OL_ERR_NOT_READY, "no shift re-scoring");
+    if (!shift || !dist2 || capacity < c->n_cand) return fail(c, OL_ERR_INVALID_ARGUMENT, "capacity too small");
+    std::vector<u64> k(c->n_cand);
+    if (c->n_cand) {
+        OL_CUDA(c, cudaMemcpyAsync(k.data(), c->shift_keys, sizeof(u64) * c->n_cand, cudaMemcpyDeviceToHost, c->stream));
+    }
+    OL_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (uint64_t i = 0; i < c->n_cand; ++i) {
+        if (k[i] == kShiftPad) { shift[i] = 0xFFFFFFFFu; dist2[i] = INFINITY; continue; }
+        shift[i] = (uint32_t)k[i];
+        const uint32_t b = (uint32_t)(k[i] >> 32);
+        memcpy(&dist2[i], &b, 4);
+    }
+    return OL_OK;
 }
 
 // ---------------------------------------------------------------- options / stats

@@ -1,0 +1,106 @@
+"""NEXT-1 parity: shift-resolved re-scoring / heading recovery on the GPU vs the
+oracle's fp32 shift chain, bit-exact (shift and dist2 bits), and the north
+star's property: a rotated query retrieves its own entry at distance 0 with
+the right shift."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthgen
+import paper_2006_08861_b200 as ol
+
+pytestmark = pytest.mark.gpu
+
+
+def _db(spec):
+    pts = synthgen.entry_points(spec, 0, spec.n_entries)
+    r = synthgen.render_host(spec, pts, profiles=True)
+    return r["desc"], r["tiles"], r["profile"].astype(np.float32)
+
+
+def _check(e, qprof, F_prof, sizes, cands, sh, d2):
+    off = np.concatenate([[0], np.cumsum(sizes)])
+    M = qprof.shape[1]
+    for i, cd in enumerate(cands):
+        q = qprof[cd["bundle"], cd["query_frame"]]
+        p = F_prof[off[cd["subspace"]] + cd["frame"]]
+        v, s = oracle.shift_distance(q, p)
+        assert sh[i] == s and d2[i].view(np.uint32) == v.view(np.uint32), (i, sh[i], s, d2[i], v)
+
+
+@pytest.mark.parametrize("W", [256, 128])
+def test_shift_rescore_vs_oracle(W):
+    spec = synthgen.Spec(seed=41, n_floors=1, paths=3, frames_per_path=300, W=W)
+    F, C, P = _db(spec)
+    sizes = [300, 300, 300]
+    qp = synthgen.query_points(spec, 3, 12, "path", 0, 1)
+    r = synthgen.render_host(spec, qp, profiles=True)
+    Q = r["desc"].reshape(4, 3, 64)
+    QP = r["profile"].astype(np.float32).reshape(4, 3, W)
+    for tc in (0, 1):
+        e = ol.Engine(0)
+        e.set_option("tc", tc)
+        e.upload(F, C, sizes, spec.grid())
+        e.upload_profiles(P)
+        e.query(Q, N=7, aggregate=True)
+        cands = e.topk()
+        sh, d2 = e.shift_rescore(QP)
+        _check(e, QP, P, sizes, cands, sh, d2)
+        sh2, d22 = e.shift_rescore(torch.from_numpy(QP).cuda())   # device input path
+        assert np.array_equal(sh, sh2) and np.array_equal(d2.view(np.uint32), d22.view(np.uint32))
+
+
+def test_rotated_query_finds_itself_with_the_right_shift():   # north star
+    spec = synthgen.Spec(seed=42, n_floors=1, paths=2, frames_per_path=500)
+    F, C, P = _db(spec)
+    rng = np.random.default_rng(0)
+    rows = rng.choice(F.shape[0], 16, replace=False)
+    shifts = rng.integers(0, spec.W, 16)
+    Q = F[rows][:, None, :].copy()                       # descriptor: rotation invariant
+    QP = np.stack([np.roll(P[r], s) for r, s in zip(rows, shifts)])[:, None, :]
+    e = ol.Engine(0)
+    e.upload(F, C, [F.shape[0]], spec.grid())
+    e.upload_profiles(P)
+    e.query(Q, N=5, aggregate=False)
+    cands = e.topk()
+    sh, d2 = e.shift_rescore(QP)
+    for b, (r, s0) in enumerate(zip(rows, shifts)):
+        mine = np.nonzero((cands["bundle"] == b) & (cands["frame"] == r))[0]
+        assert len(mine) == 1
+        i = mine[0]
+        assert cands["dist2"][i] == 0.0                  # retrieves its own entry at distance 0
+        assert d2[i] == 0.0 and sh[i] == s0              # ... with the right shift
+
+
+def test_shift_keys_min_combine_over_logical_shards():
+    spec = synthgen.Spec(seed=43, n_floors=1, paths=1, frames_per_path=600)
+    F, C, P = _db(spec)
+    qp = synthgen.query_points(spec, 4, 6)
+    r = synthgen.render_host(spec, qp, profiles=True)
+    Q = r["desc"][:, None, :]
+    QP = r["profile"].astype(np.float32)[:, None, :]
+    one = ol.Engine(0)
+    one.upload(F, C, [600], spec.grid()); one.upload_profiles(P)
+    one.query(Q, N=9, aggregate=False)
+    want = one.shift_rescore(QP)
+    engines, pays = [], []
+    for rk in range(2):
+        e = ol.Engine(0, rank=rk, world=2)
+        b, c = ol.shard_range(600, rk, 2)
+        e.upload(F[b:b + c], C[b:b + c], [600], spec.grid()); e.upload_profiles(P[b:b + c])
+        e.query(Q, N=9, aggregate=False, exchange=False)
+        engines.append(e); pays.append(e.payload())
+    g = torch.cat(pays)
+    keys = []
+    for e in engines:
+        e.finalize_gathered(g)
+        n = e.candidate_count()
+        e._ck(ol.lib().ol_shift_rescore(e._h, ol.ctypes.c_void_p(QP.ctypes.data), 0))
+        k = torch.empty(n, dtype=torch.int64, device="cuda")
+        e._ck(ol.lib().ol_shift_keys_copy(e._h, ol.ctypes.c_void_p(k.data_ptr())))
+        torch.cuda.synchronize()
+        keys.append(k.cpu().numpy())
+    kmin = np.minimum(keys[0], keys[1]).view(np.uint64)
+    assert np.array_equal((kmin & 0xFFFFFFFF).astype(np.uint32), want[0])
+    assert np.array_equal((kmin >> 32).astype(np.uint32), want[1].view(np.uint32))

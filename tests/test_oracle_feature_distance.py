@@ -137,17 +137,30 @@ def test_acc_many_equals_acc():
 # ---------------------------------------------------------------- shift distance (NEXT-1)
 def test_shift_distance_recovers_rotation():
     rng = np.random.default_rng(5)
-    d = rng.random(256)
+    d = rng.random(256).astype(np.float32)
     for s0 in (0, 1, 37, 219, 255):
         q = np.roll(d, s0)          # q[(w + s0) mod W] == d[w]
         v, s = oracle.shift_distance(q, d)
         assert v == 0.0 and s == s0
 
 
-def test_shift_distance_brute_force():
+def test_shift_distance_brute_force_and_exact_chain():
     rng = np.random.default_rng(6)
-    for _ in range(5):
-        q = rng.random(64); d = rng.random(64)
-        vals = [np.sum((np.roll(q, -s) - d) ** 2) for s in range(64)]
+    for _ in range(4):
+        q = rng.random(64).astype(np.float32); d = rng.random(64).astype(np.float32)
+        # every shift's value is the pinned fp32 chain (oracle.acc) of the rotated profile
+        vals = [oracle.acc(np.roll(q, -s), d) for s in range(64)]
         v, s = oracle.shift_distance(q, d)
-        assert abs(v - min(vals)) < 1e-12 and s == int(np.argmin(vals))
+        assert v.view(np.uint32) == min(vals).view(np.uint32) and s == int(np.argmin(vals))
+        # and within the binary64 bound of the exact shift distance
+        v64 = min(float(np.sum((np.roll(q, -k).astype(np.float64) - d) ** 2)) for k in range(64))
+        assert abs(float(v) - v64) <= 66 * 2.0 ** -24 * v64 + 1e-30
+
+
+def test_shift_distance_ties_take_smallest_shift():
+    q = np.full(32, 0.5, np.float32)
+    v, s = oracle.shift_distance(q, q)
+    assert v == 0.0 and s == 0
+    p = np.tile(np.float32([0.1, 0.9]), 16)          # period 2: shifts 0, 2, 4 ... tie
+    v, s = oracle.shift_distance(np.roll(p, 1), p)
+    assert v == 0.0 and s == 1

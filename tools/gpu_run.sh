@@ -1,3 +1,3 @@
-timeout 1500 python -m pytest tests -m "gpu" -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-tail -2 gpurun_out/pytest_gpu.log
-timeout 300 python tools/sb_experiment.py 100000000 8
+timeout 600 python -m pytest tests/test_gpu_shift.py -x -q > gpurun_out/pytest_shift.log 2>&1; echo shift=$?
+tail -3 gpurun_out/pytest_shift.log
+grep -E "Error|assert" gpurun_out/pytest_shift.log | head -5
