@@ -224,8 +224,8 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             const uint32_t b_base = smem_u32(s.b);
             for (uint32_t t = 0; t < n_tiles; ++t) {
                 const uint32_t st = t % kStages, buf = t & 1;
-                mbar_wait(&s.full[st], (t / kStages) & 1);
-                if (t >= 2) mbar_wait(&s.tempty[buf], ((t >> 1) - 1) & 1);
+                mbar_wait_sleep(&s.full[st], (t / kStages) & 1);
+                if (t >= 2) mbar_wait_sleep(&s.tempty[buf], ((t >> 1) - 1) & 1);
                 tc_fence_after();
                 const uint32_t a_base = smem_u32(s.a[st]);
 #pragma unroll
@@ -253,9 +253,9 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             const uint32_t buf = t & 1, st = t % kStages;
             const uint32_t rl = t * kTileRows + r_in_tile;   // row within the item
             const bool valid = rl < it.count;
-            const uint32_t gt_prev = gt;   // loaded a tile ago (latency hidden)
-            if (rc < qn) gt = __ldcg(&a.g_tau[(size_t)(q0 + rc) * a.n_sub + it.sub]);
-            mbar_wait(&s.tfull[buf], (t >> 1) & 1);          // MMA t done (its stage landed)
+            const uint32_t gt_prev = gt;   // loaded 8 tiles ago (latency hidden)
+            if ((t & 7) == 0 && rc < qn) gt = __ldcg(&a.g_tau[(size_t)(q0 + rc) * a.n_sub + it.sub]);
+            mbar_wait_sleep(&s.tfull[buf], (t >> 1) & 1);    // MMA t done (its stage landed)
             tc_fence_after();
             const float2 m = s.rm[st][r_in_tile + (it.row_begin & 1)];   // (RD ||f||^2, RU e_f)
             __syncwarp();
@@ -294,15 +294,14 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 // cold path (rare): enqueue exactly the passing columns
                 if (!(a.dbg & 4) && valid && fmaxf(mx0, mx1) >= g) {   // (rows past the item
                     // end have g = +inf, which still passes while h = -inf: hence `valid`)
-                    uint32_t spill[64];
+                    uint32_t spill[64];   // cold path (rare): out of line, via local memory
 #pragma unroll
                     for (int j = 0; j < 32; ++j) { spill[j] = va[j]; spill[32 + j] = vb[j]; }
                     tc_cold(s, spill, g, part * 64, qn, rl, a.stat_flagged);
-                    if (a.dbg & 8) atomicAdd(&a.prof[part * 4 + quarter], 1ull);
                 }
             }
             // the threshold loaded a tile ago: tighten this column if another CTA did better
-            if (rc < qn && gt_prev < lds_u32(&s.tau[rc])) {
+            if ((t & 7) == 7 && rc < qn && gt_prev < lds_u32(&s.tau[rc])) {
                 atomicMin(&s.tau[rc], gt_prev);
                 s.h[rc] = h_of(s.alpha[rc], lds_u32(&s.tau[rc]));
             }
