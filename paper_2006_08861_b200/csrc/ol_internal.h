@@ -98,20 +98,16 @@ struct AggArgs {
 struct TcScanArgs {
     const WorkItem *items;
     const float2 *qmeta;          // [nq] (RD ||q||^2, RU ||q - fp16(q)||)
-    const float2 *rmeta;          // [rows] (RD ||f||^2, RU ||f - fp16(f)||)
-    const uint32_t *nq_max;       // bits of the batch norm bound
-    const uint32_t *force_all;    // nonzero: a frame left the fp16 range -> score every pair
+    const uint32_t *bounds;       // [2] batch norm bound bits, [3] force_all (a frame left the fp16 range)
     float nf_max;                 // database norm bound
     uint32_t *g_tau;              // [nq][n_sub] acc bits: seeded, then shared running minimum
     const float *queries;         // fp32 [nq][K]
     const float *coarse, *fine;   // fp32 planes (exact re-scoring)
     u64 *partial;                 // [nq][n_items][N]
     unsigned long long *stat_survivors;
-    unsigned long long *stat_flagged;   // (row, 32-column chunk) groups that took the cold path
-    uint32_t nq, n_items, n_qblocks, qb, qb_mma, n_sub, N, kc;
-    uint32_t dbg;                 // profiling only: 1 skip epilogue math, 2 skip MMA, 4 skip cold
-                                  // path (wrong results); 8 per-role clock64 accounting -> prof
-    unsigned long long *prof;     // [16] cycle counters (dbg & 8)
+    unsigned long long *stat_flagged;   // (frame, row tile) pairs that took the cold path
+    uint32_t nq, n_items, n_qblocks, qb, n_sub, N, kc, stages;
+    uint32_t dbg;                 // profiling only: 1 skip epilogue math, 2 skip MMA, 4 skip cold path
 };
 
 constexpr u64 kShiftPad = 0x7FFFFFFFFFFFFFFFull;   // "not scored on this rank" (MIN-reducible)
@@ -129,15 +125,15 @@ struct ShiftArgs {
 // launchers (return cudaGetLastError())
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s);
 cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, uint64_t rows, void *plane,
-                                float2 *rmeta, uint32_t *nf_max, uint32_t *maxabs, cudaStream_t s);
-cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float2 *qmeta,
-                                   uint32_t *nq_max, uint32_t *force_all, cudaStream_t s);
+                                void *ext, uint32_t *nf_max, uint32_t *maxabs, cudaStream_t s);
+cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, void *qx, float2 *qmeta,
+                                   uint32_t *bounds, cudaStream_t s);
 cudaError_t launch_fill_u32(uint32_t *p, uint64_t n, uint32_t v, cudaStream_t s);
-bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows);
-cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q, const TcScanArgs &a, int grid,
-                          cudaStream_t s);
-size_t tc_smem_bytes(uint32_t qb, uint32_t N);
-uint32_t tc_max_qb(uint32_t N);
+bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows, uint32_t width);
+cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_rowsx, const CUtensorMap &map_q,
+                          const CUtensorMap &map_qx, const TcScanArgs &a, int grid, cudaStream_t s);
+size_t tc_smem_bytes(uint32_t qb, uint32_t N, uint32_t stages);
+bool tc_shape(uint32_t N, uint32_t nq, uint32_t *qb, uint32_t *stages);
 cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s);
 cudaError_t launch_scan(int kc, const ScanArgs &a, size_t smem, int grid, cudaStream_t s);
 size_t scan_smem_bytes(uint32_t qt, uint32_t N);

@@ -38,13 +38,15 @@ struct ol_ctx {
     float *coarse = nullptr, *fine = nullptr;
     int32_t *coords = nullptr;
     // tensor-core filter operands (tcscan.cu): fp16 rows + per-row bound terms
-    void *plane16 = nullptr;
-    float2 *rmeta = nullptr;
-    uint32_t *tcstat_d = nullptr;  // [0] database norm bound bits, [1] max |f| bits
+    void *plane16 = nullptr;       // fp16 rows [rows][64]
+    void *ext16 = nullptr;         // fp16 extra K block [rows][16] = (hi, lo, ef16, 0...)
+    uint32_t *tcstat_d = nullptr;  // [0] database norm bound bits, [1] max |f| bits,
+                                   // [2] batch norm bound bits, [3] force_all
     bool tc_ok = false;
     float nf_max = 0.f;
-    CUtensorMap map_rows;
+    CUtensorMap map_rows, map_rowsx;
     void *q16 = nullptr; size_t q16_cap = 0;
+    void *qx16 = nullptr; size_t qx16_cap = 0;
     float2 *qmeta = nullptr; size_t qmeta_cap = 0;
     bool used_tc = false;
     // NEXT-1 profiles and shift keys
@@ -166,10 +168,10 @@ static ol_status check_params(ol_ctx *c, const ol_params *p, bool need_agg) {
 
 static void free_db(ol_ctx *c) {
     cudaFree(c->coarse); cudaFree(c->fine); cudaFree(c->coords); cudaFree(c->subs_d);
-    cudaFree(c->plane16); cudaFree(c->rmeta); cudaFree(c->prof);
+    cudaFree(c->plane16); cudaFree(c->ext16); cudaFree(c->prof);
     c->prof = nullptr; c->prof_W = 0;
     c->coarse = c->fine = nullptr; c->coords = nullptr; c->subs_d = nullptr;
-    c->plane16 = nullptr; c->rmeta = nullptr; c->tc_ok = false;
+    c->plane16 = nullptr; c->ext16 = nullptr; c->tc_ok = false;
     c->db_ready = false;
     c->items.clear();
     c->items_chunk = 0;
@@ -223,7 +225,7 @@ void ol_destroy(ol_ctx *c) {
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
     cudaFree(c->prefix_d); cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
     cudaFree(c->flags_d); cudaFree(c->stat_d); cudaFree(c->tcstat_d); cudaFree(c->prof_d);
-    cudaFree(c->q16); cudaFree(c->qmeta); cudaFree(c->qprof_d); cudaFree(c->shift_keys);
+    cudaFree(c->q16); cudaFree(c->qx16); cudaFree(c->qmeta); cudaFree(c->qprof_d); cudaFree(c->shift_keys);
     for (auto &v : c->ev)
         for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -351,10 +353,9 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
         }
         if (c->opt_tc != 0) {
             OL_CUDA(c, cudaMalloc(&c->plane16, sizeof(uint16_t) * rows_pad * OL_K));
-            OL_CUDA(c, cudaMalloc((void **)&c->rmeta, sizeof(float2) * (rows_pad + 132)));  // + a tile of pad
-            OL_CUDA(c, cudaMemsetAsync(c->rmeta + rows_pad, 0, sizeof(float2) * 132, c->stream));
+            OL_CUDA(c, cudaMalloc(&c->ext16, sizeof(uint16_t) * rows_pad * 16));
             OL_CUDA(c, cudaMemsetAsync(c->tcstat_d, 0, 4 * sizeof(uint32_t), c->stream));
-            OL_CUDA(c, launch_tc_prep_rows(c->coarse, c->fine, kc, rows_pad, c->plane16, c->rmeta, c->tcstat_d,
+            OL_CUDA(c, launch_tc_prep_rows(c->coarse, c->fine, kc, rows_pad, c->plane16, c->ext16, c->tcstat_d,
                                            c->tcstat_d + 1, c->stream));
         }
     }
@@ -367,9 +368,11 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
         OL_CUDA(c, cudaMemcpy(st, c->tcstat_d, sizeof(st), cudaMemcpyDeviceToHost));
         const float nf = *reinterpret_cast<float *>(&st[0]), amax = *reinterpret_cast<float *>(&st[1]);
         c->nf_max = nf;
-        // fp16 operands need |f| well inside the fp16 range, and the row count fits a TMA coordinate
-        c->tc_ok = std::isfinite(nf) && amax < 65000.f && rows_pad < (1ull << 31) &&
-                   make_tc_map(&c->map_rows, c->plane16, rows_pad, 128);
+        // fp16 operands need |f| and ||f||^2 / 2 inside the fp16 range, and the row count
+        // must fit a TMA coordinate
+        c->tc_ok = std::isfinite(nf) && amax < 65000.f && nf < 300.f && rows_pad < (1ull << 31) &&
+                   make_tc_map(&c->map_rows, c->plane16, rows_pad, 256, OL_K) &&
+                   make_tc_map(&c->map_rowsx, c->ext16, rows_pad, 256, 16);
     }
     c->subs = subs;
     c->rows_pad = rows_pad;
@@ -441,8 +444,9 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
 
     // launch shape (results never depend on it): tensor-core filter or CUDA-core
     // scan, query tile, chunk size
-    const bool use_tc = c->tc_ok && (c->opt_tc == 1 || (c->opt_tc == -1 && nq >= (uint32_t)c->opt_tc_min_frames));
-    uint32_t tc_qb = 0;
+    uint32_t tc_qb = 0, tc_stages = 0;
+    const bool use_tc = c->tc_ok && (c->opt_tc == 1 || (c->opt_tc == -1 && nq >= (uint32_t)c->opt_tc_min_frames)) &&
+                        tc_shape(N, nq, &tc_qb, &tc_stages);
     uint32_t qt = c->opt_qtile > 0 ? (uint32_t)c->opt_qtile : kMaxQT;
     while (qt > 8 && scan_smem_bytes(qt, N) > 150 * 1024) qt -= 8;
     if (qt > kMaxQT) qt = kMaxQT;
@@ -450,17 +454,14 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     uint32_t n_qtiles = (nq + qt - 1) / qt;
     uint64_t chunk = (uint64_t)c->opt_chunk;
     if (use_tc) {
-        tc_qb = tc_max_qb(N);
-        const uint32_t nq16 = (nq + 15) / 16 * 16;
-        if (tc_qb > nq16) tc_qb = nq16;
         n_qtiles = (nq + tc_qb - 1) / tc_qb;
         if (chunk == 0) {
             const uint64_t target = 148ull * 4;
             chunk = (c->rows * n_qtiles + target - 1) / target;
             if (chunk < 4096) chunk = 4096;
         }
-        chunk = (chunk + 127) / 128 * 128;
-        if (chunk > (1ull << 24) - 128) chunk = (1ull << 24) - 128;
+        chunk = (chunk + 255) / 256 * 256;   // whole 256-row tiles
+        if (chunk > (1ull << 24) - 256) chunk = (1ull << 24) - 256;
     } else if (chunk == 0) {
         const uint64_t target = 148ull * 8;
         chunk = (c->rows * n_qtiles + target - 1) / target;
@@ -513,24 +514,22 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     if (n_items && use_tc) {
         const uint32_t qb = tc_qb, n_qblocks = (nq + qb - 1) / qb, nq_pad = n_qblocks * qb;
         OL_CUDA(c, grow((uint16_t **)&c->q16, &c->q16_cap, (size_t)nq_pad * OL_K));
+        OL_CUDA(c, grow((uint16_t **)&c->qx16, &c->qx16_cap, (size_t)nq_pad * 16));
         OL_CUDA(c, grow(&c->qmeta, &c->qmeta_cap, nq));
         OL_CUDA(c, cudaMemsetAsync(c->tcstat_d + 2, 0, 2 * sizeof(uint32_t), c->stream));
-        OL_LAUNCH(c, launch_tc_prep_queries(q, nq, nq_pad, c->q16, c->qmeta, c->tcstat_d + 2, c->tcstat_d + 3,
-                                            c->stream));
+        OL_LAUNCH(c, launch_tc_prep_queries(q, nq, nq_pad, c->q16, c->qx16, c->qmeta, c->tcstat_d, c->stream));
         if (!seed) OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
-        CUtensorMap map_q;
-        if (!make_tc_map(&map_q, c->q16, nq_pad, qb)) return fail(c, OL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+        CUtensorMap map_q, map_qx;
+        if (!make_tc_map(&map_q, c->q16, nq_pad, qb, OL_K) || !make_tc_map(&map_qx, c->qx16, nq_pad, qb, 16))
+            return fail(c, OL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
         TcScanArgs a;
-        a.items = c->items_d; a.qmeta = c->qmeta; a.rmeta = c->rmeta; a.nq_max = c->tcstat_d + 2;
-        a.force_all = c->tcstat_d + 3;
-        a.nf_max = c->nf_max; a.g_tau = c->tau0_d; a.queries = q; a.coarse = c->coarse; a.fine = c->fine;
+        a.items = c->items_d; a.qmeta = c->qmeta; a.bounds = c->tcstat_d; a.nf_max = c->nf_max;
+        a.g_tau = c->tau0_d; a.queries = q; a.coarse = c->coarse; a.fine = c->fine;
         a.partial = c->partial_d; a.stat_survivors = c->stat_d; a.stat_flagged = c->stat_d + 1;
-        a.nq = nq; a.n_items = n_items; a.n_qblocks = n_qblocks; a.qb = qb; a.qb_mma = qb; a.n_sub = c->n_sub;
-        a.N = N; a.kc = (uint32_t)c->kc; a.dbg = (uint32_t)c->opt_tc_debug;
-        a.prof = c->prof_d;
-        if (c->opt_tc_debug & 8) OL_CUDA(c, cudaMemsetAsync(c->prof_d, 0, 16 * sizeof(unsigned long long), c->stream));
+        a.nq = nq; a.n_items = n_items; a.n_qblocks = n_qblocks; a.qb = qb; a.n_sub = c->n_sub;
+        a.N = N; a.kc = (uint32_t)c->kc; a.stages = tc_stages; a.dbg = (uint32_t)c->opt_tc_debug;
         TimeScope ts(c, ol_ctx::T_SCAN);
-        OL_LAUNCH(c, launch_tcscan(c->map_rows, map_q, a, (int)(n_items * n_qblocks), c->stream));
+        OL_LAUNCH(c, launch_tcscan(c->map_rows, c->map_rowsx, map_q, map_qx, a, (int)(n_items * n_qblocks), c->stream));
         c->used_tc = true;
     } else if (n_items) {
         ScanArgs a;

@@ -1,33 +1,37 @@
 // tcscan.cu -- tensor-core certified filter for the scan (NEXT-2 in SURVEY §8f,
-// kernel NK8), used when a batch has many query frames.
+// kernel NK8), used when a tile holds many query frames.
 //
 // The exact answer is still the fp32 chain of R3 (P:157 calculateDistance,
 // P:202 "smallest Euclidean distance"); tensor cores only decide which pairs
 // cannot possibly be in the top-N.  For fp32 vectors q, f with real squared
-// distance A = ||q||^2 + ||f||^2 - 2 q.f, and their fp16 roundings q^, f^:
-//   q.f <= D + 2^-14 |q^||f^| + ||q - q^|| ||f|| + ||q^|| ||f - f^||
-// where D is the tensor core's fp32-accumulated fp16 dot product (products of
-// fp16 are exact; 2^-14 over-covers any accumulation order of 64 terms).  With
-// Nq, Nf upper bounds of the norms (batch / database maxima):
-//   A >= alpha_q + beta_r - 2 D,
-//   alpha_q = RD(||q||^2) - 2 e_q Nf - 2^-13 Nq Nf - sigma,   e_q = RU||q - q^||,
-//   beta_r  = RD(||f||^2) - 2 Nq e_f,                          e_f = RU||f - f^||,
-// sigma = 2^-18 (Nq + Nf)^2 absorbing every fp32 rounding of this test.  The
-// fp32 chain satisfies acc >= A (1 - 66 u) >= A / (1 + 2^-17), so
-//   acc > tau  is guaranteed when  D < h_q + g_r,  h_q = (alpha_q - tau(1+2^-17))/2,
-//   g_r = beta_r / 2.
-// Pairs failing that test ("survivors", ~1e-4 of pairs on paper-shaped data)
-// are re-scored with the exact fp32 chain on CUDA cores and enter the top-N;
-// everything else is provably outside it.  Results are therefore bit-identical
-// to the one-pass scan (tests: test_gpu_parity, test_gpu_tc).
+// distance A = ||q||^2 + ||f||^2 - 2 q.f and their fp16 roundings q^, f^:
+//   q.f <= q^.f^ + ||q - q^|| ||f|| + ||q^|| ||f - f^||.
+// With Nq, Nf upper bounds of the norms (batch / database maxima):
+//   A >= alpha_q + beta_r - 2 q^.f^,
+//   alpha_q = RD||q||^2 - 2 e_q Nf,   beta_r = RD||f||^2 - 2 Nq e_f,
+// e = RU||x - x^||.  The tensor core computes, per (frame q, row r), the 80-term
+// fp16 product sum  D' = q^.f^ + [-1, -1, Nq16] . [hi_r, lo_r, ef16_r]  with
+// hi_r + lo_r <= beta_r's RD||f||^2 / 2 and Nq16 ef16_r >= Nq e_f (fp16, rounded
+// the safe way), i.e. D' >= q^.f^ - beta_r / 2 up to the fp32 accumulation error
+// of 80 exact products, <= 2^-14 sum|products| <= 2^-14 S (S bounded per batch).
+// The fp32 chain satisfies acc >= A (1 - 66 u) >= A / (1 + 2^-17).  Hence
+//   acc > tau_q  is guaranteed when  D' < h_q = (alpha'_q - tau_q (1 + 2^-17)) / 2,
+//   alpha'_q = alpha_q - 2^-13 S - sigma,  sigma = 2^-18 (Nq + Nf)^2
+// (sigma absorbs every fp32 rounding of the test).  Per (frame, row tile) the
+// epilogue only needs max_r D' >= h_q: one FMNMX3 per two accumulators.  Pairs
+// that pass ("survivors", ~1e-5 of pairs on paper-shaped data) are re-scored with
+// the exact fp32 chain on CUDA cores and enter the top-N; everything else is
+// provably outside it, so results are bit-identical to the one-pass scan
+// (tests: test_gpu_tc, test_gpu_parity, test_gpu_fullsize).
 //
-// CTA = one work item (rows of one subspace) x one block of <= 256 query frames.
-// Warp roles: 0 TMA producer of 128-row fp16 tiles (SW128, 4-stage mbarrier
-// ring); 1 TMEM allocator + single-thread tcgen05.mma issuer (M=128 rows,
-// N=query block, K=64 as 4 x K16) into a double-buffered TMEM accumulator
-// (2 x 256 columns); 2..17 epilogue (tcgen05.ld, threshold test, survivor
-// push; 4 warps per TMEM lane quarter, 64 columns each); 18..19 exact
-// re-scoring + top-N insertion.
+// CTA = one work item (rows of one subspace) x <= 128 query frames (one M-tile).
+// Warp roles: 0 TMA producer (128-row tiles: fp16 rows, 128-B swizzle; their
+// 16-wide extra K block, 32-B swizzle; a mbarrier ring of n_stages);
+// 1 TMEM allocator + single-thread tcgen05.mma issuer: per 256-row tile,
+// M=128 frames x N=256 rows x K=80 (4 K16 blocks SW128 + 1 SW32) into a
+// double-buffered fp32 TMEM accumulator (2 x 256 columns); 2..9 epilogue
+// (thread = one frame x 128 of the tile's rows: tcgen05.ld, release the buffer,
+// max, survivor enqueue); 10 exact re-scoring + top-N insertion.
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
@@ -38,24 +42,23 @@ namespace ol {
 
 using namespace tc;
 
-constexpr int kTileRows = 128;
-constexpr int kStages = 8;
-constexpr int kQB = 256;                 // max query frames per CTA (MMA N)
-constexpr int kEpiWarps = 16;
-constexpr int kExactWarps = 1;
+constexpr int kTileRows = 256;          // MMA N (rows per tile)
+constexpr int kQB = 128;                // frames per CTA: one M-tile
+constexpr int kKx = 16;                 // extra K block (fp16): [-1, -1, Nq16] . [hi, lo, ef16]
+constexpr int kMaxStages = 8;
+constexpr int kEpiWarps = 8;
+constexpr int kExactWarps = 2;
 constexpr int kTcThreads = 32 * (2 + kEpiWarps + kExactWarps);
-constexpr int kRing = 1024;              // survivor ring entries (r_local << 8 | q_local)
+constexpr int kRing = 1024;             // survivor ring entries (r_local << 8 | q_local)
 constexpr float kTauInflate = 1.0f + 1.0f / 131072.0f;   // 1 + 2^-17
+constexpr uint32_t kStageBytes = kTileRows * (kK + kKx) * 2;   // 20 KB
 
 struct TcSmem {
-    alignas(1024) __half b[kQB * kK];                // query block (resident)
-    alignas(1024) __half a[kStages][kTileRows * kK];  // row tiles
-    alignas(16) float2 rm[kStages][kTileRows + 2];   // the tiles' (RD ||f||^2, RU e_f), from an
-                                                     // even row (16-B aligned bulk copy)
-    uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], qbar;
+    alignas(1024) __half qm[kQB * kK];      // frames, main K (SW128), resident
+    alignas(1024) __half qx[kQB * kKx];     // frames, extra K block (SW32), resident
+    uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2], qbar;
     uint32_t tmem_base;
-    alignas(16) float alpha[kQB];
-    alignas(16) float h[kQB];   // h_q = (alpha_q - tau_q (1 + 2^-17)) / 2
+    float alpha[kQB];
     uint32_t tau[kQB];
     int lock[kQB];
     // survivor queue: bounded MPMC ring with per-slot sequence numbers (Vyukov):
@@ -63,36 +66,28 @@ struct TcSmem {
     uint32_t seq[kRing], val[kRing];
     unsigned int prod, cons_res, closed_at;
     int closed;
-    // top-N lists follow (dynamic): u64 [qb][N]
+    // dynamic, 1024-aligned: n_stages x {rows main [128][64] SW128, rows extra [128][16] SW32},
+    // then the top-N lists u64 [qb][N]
 };
 
-size_t tc_smem_bytes(uint32_t qb, uint32_t N) { return sizeof(TcSmem) + 1024 + sizeof(u64) * qb * N; }
+static __host__ __device__ constexpr size_t tc_fixed_bytes() { return (sizeof(TcSmem) + 1023) / 1024 * 1024; }
+
+size_t tc_smem_bytes(uint32_t qb, uint32_t N, uint32_t stages) {
+    return 1024 + tc_fixed_bytes() + (size_t)stages * kStageBytes + sizeof(u64) * qb * N;
+}
 
 __device__ __forceinline__ float chain_step_tc(float acc, float q, float f) {
     float d = __fsub_rn(q, f);
     return __fmaf_rn(d, d, acc);
 }
 
-__device__ __forceinline__ uint32_t lds_u32(const void *p) {  // volatile shared-memory load
+__device__ __forceinline__ uint32_t lds_u32(const void *p) {
     return *reinterpret_cast<const volatile uint32_t *>(p);
 }
 __device__ __forceinline__ uint64_t lds_u64(const void *p) {
     return *reinterpret_cast<const volatile uint64_t *>(p);
 }
-__device__ __forceinline__ void sts_u32(void *p, uint32_t v) {  // volatile shared-memory store
-    *reinterpret_cast<volatile uint32_t *>(p) = v;
-}
-
-__device__ __forceinline__ uint64_t pack2(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
-__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {  // FADD2: two RN fp32 subtractions
-    uint64_t r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-
-__device__ __forceinline__ float h_of(float alpha, uint32_t tau_bits) {
-    return 0.5f * (alpha - __uint_as_float(tau_bits) * kTauInflate);
-}
+__device__ __forceinline__ void sts_u32(void *p, uint32_t v) { *reinterpret_cast<volatile uint32_t *>(p) = v; }
 
 __device__ __forceinline__ float max3f(float a, float b, float c) {  // FMNMX3
     float r;
@@ -100,33 +95,7 @@ __device__ __forceinline__ float max3f(float a, float b, float c) {  // FMNMX3
     return r;
 }
 
-// Threshold test of 32 accumulator columns of one row: x = (D - g) - h per
-// column (two FADD2 per column pair); sets bit `chunk` of flags if any x >= 0.
-__device__ __forceinline__ void tc_test32(const uint32_t (&v)[32], uint64_t gg, const uint64_t *h2,
-                                          uint32_t &flags, int chunk) {
-    uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu;
-#pragma unroll
-    for (int j = 0; j < 16; j += 2) {
-        const uint64_t x0 = sub2(sub2(pack2(v[2 * j], v[2 * j + 1]), gg), h2[j]);
-        const uint64_t x1 = sub2(sub2(pack2(v[2 * j + 2], v[2 * j + 3]), gg), h2[j + 1]);
-        const uint32_t m = (uint32_t)x0 & (uint32_t)(x0 >> 32) & (uint32_t)x1 & (uint32_t)(x1 >> 32);
-        if (j & 2) a1 &= m; else a0 &= m;
-    }
-    flags |= ((~(a0 & a1)) >> 31) << chunk;
-}
-// Bit mask of the passing columns among 32 (same arithmetic as tc_test32).
-__device__ __forceinline__ uint32_t tc_mask32(const uint32_t (&v)[32], uint64_t gg, const uint64_t *h2) {
-    uint32_t mask = 0;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const uint64_t x = sub2(sub2(pack2(v[2 * j], v[2 * j + 1]), gg), h2[j]);
-        mask |= ((~(uint32_t)x >> 31) << (2 * j)) | ((~(uint32_t)(x >> 32) >> 31) << (2 * j + 1));
-    }
-    return mask;
-}
-
-// Enqueue a survivor (r_local << 8 | column) on the MPMC ring, waiting while
-// the ring is full.
+// Enqueue a survivor (r_local << 8 | q_local) on the MPMC ring, waiting while full.
 __device__ __forceinline__ void tc_enqueue(TcSmem &s, uint32_t e) {
     const unsigned pos = atomicAdd(&s.prod, 1u);
     uint32_t *sq = &s.seq[pos % kRing];
@@ -136,24 +105,48 @@ __device__ __forceinline__ void tc_enqueue(TcSmem &s, uint32_t e) {
     sts_u32(sq, pos + 1);
 }
 
-// Cold path of the epilogue: the row passed for some of its 64 columns; find them
-// (same arithmetic as the hot test) and enqueue them.  Kept out of line so the
-// hot loop's register allocation does not carry it.
-__device__ __noinline__ void tc_cold(TcSmem &s, const uint32_t *v, float g, uint32_t cb, uint32_t qn,
-                                     uint32_t rl, unsigned long long *stat_flagged) {
-    for (uint32_t j = 0; j < 64; ++j)
-        if (cb + j < qn && __fsub_rn(__uint_as_float(v[j]), s.h[cb + j]) >= g) tc_enqueue(s, (rl << 8) | (cb + j));
-    if (stat_flagged) atomicAdd(stat_flagged, 1ull);
+// Enqueue the passing columns of one frame's 128-row block with one reservation:
+// all values first, one fence, then the sequence numbers that publish them.
+__device__ __noinline__ void tc_enqueue_mask(TcSmem &s, uint32_t (&mk)[4], uint32_t rb, uint32_t ql, uint32_t cnt) {
+    const unsigned pos0 = atomicAdd(&s.prod, cnt);
+    unsigned pos = pos0;
+    for (int c = 0; c < 4; ++c)
+        for (uint32_t m = mk[c]; m; m &= m - 1, ++pos) {
+            const uint32_t j = __ffs(m) - 1;
+            while (lds_u32(&s.seq[pos % kRing]) != pos) __nanosleep(64);
+            s.val[pos % kRing] = ((rb + 32 * c + j) << 8) | ql;
+        }
+    __threadfence_block();
+    for (unsigned p = pos0; p != pos; ++p) sts_u32(&s.seq[p % kRing], p + 1);
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// max over 32 accumulator columns into two running maxima
+__device__ __forceinline__ void max32(const uint32_t (&v)[32], float &m0, float &m1) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+        m0 = max3f(m0, __uint_as_float(v[j]), __uint_as_float(v[j + 1]));
+        m1 = max3f(m1, __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+    }
+}
+// bit mask of the columns >= h, invalid columns (>= nvalid) excluded
+__device__ __forceinline__ uint32_t mask32(const uint32_t (&v)[32], float h, int base, uint32_t nvalid) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) m |= (uint32_t)(__uint_as_float(v[j]) >= h && (uint32_t)(base + j) < nvalid) << j;
+    return m;
+}
+
 __global__ void __launch_bounds__(kTcThreads, 1)
-tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constant__ CUtensorMap map_q,
-              TcScanArgs a) {
+tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constant__ CUtensorMap map_rowsx,
+              const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_qx, TcScanArgs a) {
     extern __shared__ __align__(1024) unsigned char raw[];
-    TcSmem &s = *reinterpret_cast<TcSmem *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-    u64 *lists = reinterpret_cast<u64 *>(&s + 1);
+    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    TcSmem &s = *reinterpret_cast<TcSmem *>(base);
+    unsigned char *stage0 = base + tc_fixed_bytes();
+    const uint32_t n_stages = a.stages;
+    u64 *lists = reinterpret_cast<u64 *>(stage0 + (size_t)n_stages * kStageBytes);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t item_id = blockIdx.x / a.n_qblocks;
     const uint32_t qblk = blockIdx.x % a.n_qblocks;
@@ -165,33 +158,30 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
 
     // ---------------------------------------------------------------- setup
     if (threadIdx.x == 0) {
-        // a stage is free once the MMA consumed its rows AND every epilogue warp read
-        // its bound terms (rm)
-        for (int i = 0; i < kStages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 1 + kEpiWarps); }
+        for (uint32_t i = 0; i < n_stages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 1); }
         for (int i = 0; i < 2; ++i) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], kEpiWarps); }
         mbar_init(&s.qbar, 1);
         fence_mbar_init();
         s.prod = s.cons_res = s.closed_at = 0;
         s.closed = 0;
         tma_prefetch(&map_rows);
-        tma_prefetch(&map_q);
+        tma_prefetch(&map_rowsx);
     }
     if (warp == 1) tmem_alloc<512>(&s.tmem_base);
-    const float nqm = __uint_as_float(*a.nq_max);
-    const bool force_all = *a.force_all != 0;
-    const float nfm = a.nf_max;
-    const float sigma = 3.814697265625e-06f * (nqm + nfm) * (nqm + nfm);  // 2^-18 (Nq + Nf)^2
-    const float c0 = 1.220703125e-04f * nqm * nfm;                        // 2^-13 Nq Nf
+    const float nqm = __uint_as_float(a.bounds[2]), nfm = a.nf_max;
+    const bool force_all = a.bounds[3] != 0;
+    const float sigma = 3.814697265625e-06f * (nqm + nfm) * (nqm + nfm);      // 2^-18 (Nq + Nf)^2
+    // 2^-13 x a bound of sum |products| over the 80 terms: Nq Nf + Nf^2 / 2 + Nq16 (2^-11 Nf + 2^-22)
+    const float S = nqm * nfm + 0.5f * nfm * nfm + 1.001f * nqm * (4.8828125e-04f * nfm + 2.384185791e-07f);
+    const float c0 = 1.220703125e-04f * S;
     for (uint32_t q = threadIdx.x; q < kQB; q += blockDim.x) {
         if (q < qn) {
             const float2 m = a.qmeta[q0 + q];  // (RD ||q||^2, RU e_q)
             s.alpha[q] = force_all ? -INFINITY : m.x - 2.f * m.y * nfm - c0 - sigma;
             s.tau[q] = a.g_tau[(size_t)(q0 + q) * a.n_sub + it.sub];
-            s.h[q] = h_of(s.alpha[q], s.tau[q]);
         } else {
-            s.alpha[q] = INFINITY;  // padded query column: h = +inf, never passes
+            s.alpha[q] = INFINITY;  // padded frame: h = +inf, never passes
             s.tau[q] = 0;
-            s.h[q] = INFINITY;
         }
         s.lock[q] = 0;
     }
@@ -203,108 +193,94 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     const uint32_t tmem = s.tmem_base;
 
     if (warp == 0) {
+        // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
-            // query block (resident B operand): 256 rows x 128 B, one box
-            mbar_expect_tx(&s.qbar, a.qb * kK * (uint32_t)sizeof(__half));
-            tma_load_2d(s.b, &map_q, &s.qbar, 0, (int)q0);
+            mbar_expect_tx(&s.qbar, a.qb * (kK + kKx) * (uint32_t)sizeof(__half));
+            tma_load_2d(s.qm, &map_q, &s.qbar, 0, (int)q0);
+            tma_load_2d(s.qx, &map_qx, &s.qbar, 0, (int)q0);
             for (uint32_t t = 0; t < n_tiles; ++t) {
-                const uint32_t st = t % kStages;
-                if (t >= kStages) mbar_wait_sleep(&s.empty[st], ((t / kStages) - 1) & 1);
-                const uint64_t r0 = it.row_begin + (uint64_t)t * kTileRows;
-                mbar_expect_tx(&s.full[st], sizeof(s.a[0]) + sizeof(s.rm[0]));
-                tma_load_2d(s.a[st], &map_rows, &s.full[st], 0, (int)r0);
-                bulk_load(s.rm[st], a.rmeta + (r0 & ~1ull), sizeof(s.rm[0]), &s.full[st]);  // rmeta padded
+                const uint32_t st = t % n_stages;
+                if (t >= n_stages) mbar_wait_sleep(&s.empty[st], ((t / n_stages) - 1) & 1);
+                unsigned char *sb = stage0 + (size_t)st * kStageBytes;
+                const int r0 = (int)(it.row_begin + (uint64_t)t * kTileRows);
+                mbar_expect_tx(&s.full[st], kStageBytes);
+                tma_load_2d(sb, &map_rows, &s.full[st], 0, r0);
+                tma_load_2d(sb + kTileRows * kK * 2, &map_rowsx, &s.full[st], 0, r0);
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
-            const uint32_t idesc = idesc_f16_f32(kTileRows, (int)a.qb_mma);
+            const uint32_t idesc = idesc_f16_f32(128, kTileRows);   // M = 128 frames, N = 256 rows
             mbar_wait(&s.qbar, 0);
-            const uint32_t b_base = smem_u32(s.b);
+            const uint32_t qm = smem_u32(s.qm), qx = smem_u32(s.qx);
             for (uint32_t t = 0; t < n_tiles; ++t) {
-                const uint32_t st = t % kStages, buf = t & 1;
-                mbar_wait_sleep(&s.full[st], (t / kStages) & 1);
+                const uint32_t st = t % n_stages, buf = t & 1;
+                mbar_wait_sleep(&s.full[st], (t / n_stages) & 1);
                 if (t >= 2) mbar_wait_sleep(&s.tempty[buf], ((t >> 1) - 1) & 1);
                 tc_fence_after();
-                const uint32_t a_base = smem_u32(s.a[st]);
+                const uint32_t rm = smem_u32(stage0 + (size_t)st * kStageBytes), rx = rm + kTileRows * kK * 2;
+                const uint32_t d = tmem + buf * kTileRows;
+                if (!(a.dbg & 2)) {
 #pragma unroll
-                for (int k = 0; k < ((a.dbg & 2) ? 0 : kK / 16); ++k)
-                    mma_f16(tmem + buf * kQB, desc_sw128_kmajor(a_base + k * 32),
-                            desc_sw128_kmajor(b_base + k * 32), idesc, k > 0 ? 1u : 0u);
+                    for (int k = 0; k < kK / 16; ++k)
+                        mma_f16(d, desc_sw128_kmajor(qm + k * 32), desc_sw128_kmajor(rm + k * 32), idesc, k > 0 ? 1u : 0u);
+                    mma_f16(d, desc_sw32_kmajor(qx), desc_sw32_kmajor(rx), idesc, 1u);
+                }
                 mma_commit(&s.empty[st]);
                 mma_commit(&s.tfull[buf]);
             }
         }
     } else if (warp < 2 + kEpiWarps) {
         // ------------------------------------------------------------ epilogue
-        // 16 warps: warp -> (TMEM lane quarter, 64 query columns); thread = one row.
-        // Per tile: read the 64 accumulator columns, hand the TMEM buffer back at once,
-        // then on registers: y_c = RN(D_c - h_c) (FADD2) and max over c (FMNMX3); the
-        // row survives for some column iff max_c y_c >= g (cold path, rare).
-        const int ew = warp - 2;                  // 0..15
+        // thread = one frame (TMEM lane) of one M-tile; its 128 row columns per tile
+        const int ew = warp - 2;                  // 0..7
         const uint32_t quarter = warp & 3;        // TMEM lanes 32*quarter ..
-        const uint32_t part = ew >> 2;            // columns part*64 .. +64
-        const uint32_t ncol = part * 64 < a.qb_mma ? min(64u, a.qb_mma - part * 64) : 0u;
-        const uint32_t r_in_tile = quarter * 32 + lane;
-        const uint32_t rc = ew * 32 + lane;       // threshold column refreshed by this thread
-        uint32_t gt = 0xFFFFFFFFu;                // shared running threshold, loaded one tile ahead
+        const uint32_t half = ew >> 2;            // row columns half*128 .. +128
+        const uint32_t ql = quarter * 32 + lane;  // frame within the CTA
+        const bool refresher = half == 0;         // one of the two warps per frame refreshes tau
+        const float alpha = s.alpha[ql];
+        uint32_t gt = 0xFFFFFFFFu;                // shared running threshold, loaded 8 tiles ahead
         for (uint32_t t = 0; t < n_tiles; ++t) {
-            const uint32_t buf = t & 1, st = t % kStages;
-            const uint32_t rl = t * kTileRows + r_in_tile;   // row within the item
-            const bool valid = rl < it.count;
-            const uint32_t gt_prev = gt;   // loaded 8 tiles ago (latency hidden)
-            if ((t & 7) == 0 && rc < qn) gt = __ldcg(&a.g_tau[(size_t)(q0 + rc) * a.n_sub + it.sub]);
-            mbar_wait_sleep(&s.tfull[buf], (t >> 1) & 1);    // MMA t done (its stage landed)
+            const uint32_t buf = t & 1;
+            const uint32_t gt_prev = gt;
+            if (refresher && (t & 7) == 0 && ql < qn) gt = __ldcg(&a.g_tau[(size_t)(q0 + ql) * a.n_sub + it.sub]);
+            mbar_wait_sleep(&s.tfull[buf], (t >> 1) & 1);
             tc_fence_after();
-            const float2 m = s.rm[st][r_in_tile + (it.row_begin & 1)];   // (RD ||f||^2, RU e_f)
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s.empty[st]);
-            const float g = valid ? 0.5f * (m.x - 2.f * nqm * m.y) : INFINITY;
-            const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * kQB + part * 64;
-            uint32_t va[32], vb[32];
-            if (ncol) {
-                tmem_ld32(taddr, va);
-                tmem_ld32(taddr + 32, vb);
-                tmem_ld_wait_regs(va);   // orders every use of va and vb after the wait
-                reg_fence(vb);
-            }
+            uint32_t v0[32], v1[32], v2[32], v3[32];
+            const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * kTileRows + half * 128;
+            tmem_ld32(taddr, v0);
+            tmem_ld32(taddr + 32, v1);
+            tmem_ld32(taddr + 64, v2);
+            tmem_ld32(taddr + 96, v3);
+            tmem_ld_wait_regs(v0);   // orders every use of v0..v3 after the wait
+            reg_fence(v1);
+            reg_fence(v2);
+            reg_fence(v3);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.tempty[buf]);
-            if (ncol && !(a.dbg & 1)) {
-                const float4 *H4 = reinterpret_cast<const float4 *>(s.h + part * 64);
-                float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float4 h = H4[j];
-                    const uint64_t y0 = sub2(pack2(va[4 * j], va[4 * j + 1]), pack2(__float_as_uint(h.x), __float_as_uint(h.y)));
-                    const uint64_t y1 = sub2(pack2(va[4 * j + 2], va[4 * j + 3]), pack2(__float_as_uint(h.z), __float_as_uint(h.w)));
-                    mx0 = max3f(mx0, __uint_as_float((uint32_t)y0), __uint_as_float((uint32_t)(y0 >> 32)));
-                    mx1 = max3f(mx1, __uint_as_float((uint32_t)y1), __uint_as_float((uint32_t)(y1 >> 32)));
-                }
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const float4 h = H4[8 + j];
-                    const uint64_t y0 = sub2(pack2(vb[4 * j], vb[4 * j + 1]), pack2(__float_as_uint(h.x), __float_as_uint(h.y)));
-                    const uint64_t y1 = sub2(pack2(vb[4 * j + 2], vb[4 * j + 3]), pack2(__float_as_uint(h.z), __float_as_uint(h.w)));
-                    mx0 = max3f(mx0, __uint_as_float((uint32_t)y0), __uint_as_float((uint32_t)(y0 >> 32)));
-                    mx1 = max3f(mx1, __uint_as_float((uint32_t)y1), __uint_as_float((uint32_t)(y1 >> 32)));
-                }
-                // cold path (rare): enqueue exactly the passing columns
-                if (!(a.dbg & 4) && valid && fmaxf(mx0, mx1) >= g) {   // (rows past the item
-                    // end have g = +inf, which still passes while h = -inf: hence `valid`)
-                    uint32_t spill[64];   // cold path (rare): out of line, via local memory
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) { spill[j] = va[j]; spill[32 + j] = vb[j]; }
-                    tc_cold(s, spill, g, part * 64, qn, rl, a.stat_flagged);
+            if (!(a.dbg & 1)) {
+                const float h = 0.5f * (alpha - __uint_as_float(lds_u32(&s.tau[ql])) * kTauInflate);
+                const uint32_t rb = t * kTileRows + half * 128;   // first row (within the item) of my columns
+                const uint32_t nvalid = rb < it.count ? min(128u, it.count - rb) : 0u;
+                float m0 = -INFINITY, m1 = -INFINITY;
+                max32(v0, m0, m1);
+                max32(v1, m0, m1);
+                max32(v2, m0, m1);
+                max32(v3, m0, m1);
+                // cold path (rare): enqueue exactly the passing columns; columns past the
+                // item's last row (last tile only) are excluded by the mask
+                if (fmaxf(m0, m1) >= h && ql < qn && !(a.dbg & 4)) {
+                    uint32_t mk[4] = {mask32(v0, h, 0, nvalid), mask32(v1, h, 32, nvalid),
+                                      mask32(v2, h, 64, nvalid), mask32(v3, h, 96, nvalid)};
+                    const uint32_t cnt = __popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]);
+                    if (cnt) tc_enqueue_mask(s, mk, rb, ql, cnt);
+                    if (a.stat_flagged) atomicAdd(a.stat_flagged, 1ull);
                 }
             }
-            // the threshold loaded a tile ago: tighten this column if another CTA did better
-            if ((t & 7) == 7 && rc < qn && gt_prev < lds_u32(&s.tau[rc])) {
-                atomicMin(&s.tau[rc], gt_prev);
-                s.h[rc] = h_of(s.alpha[rc], lds_u32(&s.tau[rc]));
-            }
+            // the shared threshold loaded 8 tiles ago: tighten this frame's if another CTA did better
+            if (refresher && (t & 7) == 7 && ql < qn && gt_prev < lds_u32(&s.tau[ql])) atomicMin(&s.tau[ql], gt_prev);
         }
         named_bar(1, 32 * kEpiWarps);
         if (warp == 2 && lane == 0) {
@@ -323,17 +299,12 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             while (true) {
                 if (lds_u32(sq) == p + 1) { got = true; break; }
                 if (lds_u32(&s.closed) && p >= lds_u32(&s.closed_at)) break;
-                // idle: now and then import the running thresholds other CTAs
-                // published (any value ever held is a valid bound, so races only loosen h)
-                {
-                    const uint32_t qi = (idle++ * (32 * kExactWarps) + (threadIdx.x - 32 * (2 + kEpiWarps))) % kQB;
-                    if (qi < qn) {
-                        const uint32_t gt = __ldcg(&a.g_tau[(size_t)(q0 + qi) * a.n_sub + it.sub]);
-                        if (gt < lds_u32(&s.tau[qi])) {
-                            atomicMin(&s.tau[qi], gt);
-                            s.h[qi] = h_of(s.alpha[qi], lds_u32(&s.tau[qi]));
-                        }
-                    }
+                // idle: import the running thresholds other CTAs published (any value
+                // ever held is a valid bound, so races only loosen the test)
+                const uint32_t qi = (idle++ * (32 * kExactWarps) + (threadIdx.x - 32 * (2 + kEpiWarps))) % kQB;
+                if (qi < qn) {
+                    const uint32_t g = __ldcg(&a.g_tau[(size_t)(q0 + qi) * a.n_sub + it.sub]);
+                    if (g < lds_u32(&s.tau[qi])) atomicMin(&s.tau[qi], g);
                 }
                 __nanosleep(nap);
                 if (nap < 2048) nap <<= 1;
@@ -373,7 +344,6 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                     if (L[N - 1] != kPadKey) {
                         const uint32_t tb = (uint32_t)(L[N - 1] >> 32);
                         atomicMin(&s.tau[col], tb);
-                        s.h[col] = h_of(s.alpha[col], lds_u32(&s.tau[col]));
                         atomicMin(&a.g_tau[(size_t)(q0 + col) * a.n_sub + it.sub], tb);
                     }
                 }
@@ -387,12 +357,6 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     // ---------------------------------------------------------------- teardown
     tc_fence_before();
     __syncthreads();
-    if ((a.dbg & 16) && blockIdx.x == 0)
-        for (uint32_t q = threadIdx.x; q < kQB; q += blockDim.x) {
-            a.prof[16 + q] = __float_as_uint(s.h[q]);
-            a.prof[16 + 256 + q] = s.tau[q];
-            a.prof[16 + 512 + q] = __float_as_uint(s.alpha[q]);
-        }
     if (warp == 1) tmem_dealloc<512>(tmem);
     for (uint32_t i = threadIdx.x; i < qn * N; i += blockDim.x) {
         const uint32_t q = i / N, r = i % N;
@@ -408,8 +372,13 @@ namespace ol {
 // Per database row: the fp16 operand (RN), RD(||f||^2), RU(||f - f^||), and the
 // row norm bound max(||f||, ||f^||) folded into a database maximum (atomicMax on
 // the bits of a non-negative float).  Also the largest |f| (fp16 range check).
+// Per database row: the fp16 operand (RN) [rows][64]; its extra K block [rows][16]
+// = (hi, lo, ef16, 0...) with hi = RN16(x), lo = RD16(x - hi) for x = RD||f||^2 / 2
+// (so hi + lo <= x) and ef16 = RU16(RU||f - f^||); the row norm bound
+// max(||f||, ||f^||) folded into a database maximum (atomicMax on the bits of a
+// non-negative float); the largest |f| (fp16 range check).
 __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int kc, uint64_t rows,
-                                    __half *plane, float2 *rmeta, uint32_t *nf_max, uint32_t *maxabs) {
+                                    __half *plane, __half *ext, uint32_t *nf_max, uint32_t *maxabs) {
     uint32_t lmax = 0, lnorm = 0;
     for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
          r += (uint64_t)gridDim.x * blockDim.x) {
@@ -429,7 +398,12 @@ __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int 
         }
         const float fn_lo = __double2float_rd(n2 * (1.0 - 1.0 / 1048576.0));
         const float ef = __double2float_ru(sqrt(e2) * (1.0 + 1.0 / 1048576.0));
-        rmeta[r] = make_float2(fn_lo, ef);
+        const float x = 0.5f * fn_lo;   // exact
+        const __half hi = __float2half_rn(x);
+        const __half lo = __float2half_rd(x - __half2float(hi));   // x - hi is exact in fp32
+        __half *xr = ext + r * 16;
+        xr[0] = hi; xr[1] = lo; xr[2] = __float2half_ru(ef);
+        for (int k = 3; k < 16; ++k) xr[k] = __float2half(0.f);
         const float nb = __double2float_ru(sqrt(fmax(n2, h2)) * (1.0 + 1.0 / 1048576.0));
         lnorm = max(lnorm, __float_as_uint(nb));
         lmax = max(lmax, __float_as_uint(amax));
@@ -442,12 +416,12 @@ __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int 
 }
 
 cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, uint64_t rows, void *plane,
-                                float2 *rmeta, uint32_t *nf_max, uint32_t *maxabs, cudaStream_t s) {
+                                void *ext, uint32_t *nf_max, uint32_t *maxabs, cudaStream_t s) {
     uint64_t blocks = (rows + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks == 0) blocks = 1;
-    tc_prep_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(coarse, fine, kc, rows, (__half *)plane, rmeta, nf_max,
-                                                         maxabs);
+    tc_prep_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(coarse, fine, kc, rows, (__half *)plane, (__half *)ext,
+                                                         nf_max, maxabs);
     return cudaGetLastError();
 }
 
@@ -488,10 +462,30 @@ __global__ void tc_prep_queries_kernel(const float *q, uint32_t nq, uint32_t nq_
     }
 }
 
-cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float2 *qmeta,
-                                   uint32_t *nq_max, uint32_t *force_all, cudaStream_t s) {
+// The frames' extra K block [nq_pad][16] = (-1, -1, RU16(Nq), 0...) once the batch
+// norm bound is known; zeros for padded / out-of-range frames.  A bound too large
+// for the fp16 products (Nq >= 300) sends the whole batch to exact re-scoring.
+__global__ void tc_prep_qext_kernel(uint32_t nq, uint32_t nq_pad, const float2 *qmeta, uint32_t *bounds,
+                                    __half *qx) {
+    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= nq_pad) return;
+    const float nq_max = __uint_as_float(bounds[2]);
+    if (w == 0 && !(nq_max < 300.f)) atomicOr(&bounds[3], 1u);
+    __half *x = qx + (size_t)w * 16;
+    const bool live = w < nq && nq_max < 300.f;
+    x[0] = __float2half(live ? -1.f : 0.f);
+    x[1] = __float2half(live ? -1.f : 0.f);
+    x[2] = live ? __float2half_ru(nq_max) : __float2half(0.f);
+    for (int k = 3; k < 16; ++k) x[k] = __float2half(0.f);
+}
+
+cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, void *qx, float2 *qmeta,
+                                   uint32_t *bounds, cudaStream_t s) {
     const uint32_t threads = 256, blocks = (nq_pad * 32 + threads - 1) / threads;
-    tc_prep_queries_kernel<<<blocks, threads, 0, s>>>(q, nq, nq_pad, (__half *)q16, qmeta, nq_max, force_all);
+    tc_prep_queries_kernel<<<blocks, threads, 0, s>>>(q, nq, nq_pad, (__half *)q16, qmeta, bounds + 2, bounds + 3);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    tc_prep_qext_kernel<<<(nq_pad + 255) / 256, 256, 0, s>>>(nq, nq_pad, qmeta, bounds, (__half *)qx);
     return cudaGetLastError();
 }
 
@@ -521,36 +515,40 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 2-D map over an fp16 [rows][64] array, box {64, box_rows}, 128-byte swizzle
-// (the UMMA K-major SW128 canonical layout).
-bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows) {
+// 2-D map over an fp16 [rows][width] array (width 64 -> 128-byte swizzle, width 16 ->
+// 32-byte swizzle: the UMMA K-major canonical layouts), box {width, box_rows}.
+bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows, uint32_t width) {
     auto fn = encode_fn();
     if (!fn) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)kK, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)kK * sizeof(__half)};
-    cuuint32_t box[2] = {(cuuint32_t)kK, box_rows};
+    cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)width * sizeof(__half)};
+    cuuint32_t box[2] = {width, box_rows};
     cuuint32_t estr[2] = {1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+              CU_TENSOR_MAP_INTERLEAVE_NONE, width == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q, const TcScanArgs &a, int grid,
-                          cudaStream_t s) {
-    const size_t smem = tc_smem_bytes(a.qb, a.N);
+cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_rowsx, const CUtensorMap &map_q,
+                          const CUtensorMap &map_qx, const TcScanArgs &a, int grid, cudaStream_t s) {
+    const size_t smem = tc_smem_bytes(a.qb, a.N, a.stages);
     cudaError_t e = cudaFuncSetAttribute(tcscan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    tcscan_kernel<<<grid, kTcThreads, smem, s>>>(map_rows, map_q, a);
+    tcscan_kernel<<<grid, kTcThreads, smem, s>>>(map_rows, map_rowsx, map_q, map_qx, a);
     return cudaGetLastError();
 }
 
-uint32_t tc_max_qb(uint32_t N) {
-    const size_t budget = 227 * 1024 - sizeof(TcSmem) - 1024;   // what the top-N lists may use
-    uint32_t qb = (uint32_t)(budget / (N * sizeof(u64)));
-    qb = qb / 16 * 16;
-    if (qb > (uint32_t)kQB) qb = kQB;
-    if (qb < 16) qb = 16;
-    return qb;
+// Frames per CTA (128 or 256) and pipeline depth for top-N lists of N: the lists
+// share the 227 KB of shared memory with the resident frames and the row stages.
+bool tc_shape(uint32_t N, uint32_t nq, uint32_t *qb, uint32_t *stages) {
+    (void)nq;
+    const size_t budget = 227 * 1024;
+    const size_t fixed = 1024 + tc_fixed_bytes() + sizeof(u64) * kQB * N;
+    if (fixed + 2 * kStageBytes > budget) return false;
+    const uint32_t st = (uint32_t)((budget - fixed) / kStageBytes);
+    *qb = kQB;
+    *stages = st > (uint32_t)kMaxStages ? (uint32_t)kMaxStages : st;
+    return true;
 }
 
 }  // namespace ol

@@ -32,7 +32,8 @@ def test_tc_paper_shaped(N):
     ref = oracle.retrieve([F.shape[0]], F, C, Q, N)
     for tc in (1, 0):
         e = _run(F, C, [F.shape[0]], Q, N, tc, spec.grid())
-        assert e.stat("used_tc") == tc
+        # lists of N = 128 leave no shared memory for the tensor-core pipeline: CUDA-core scan
+        assert e.stat("used_tc") == (tc if N < 128 else 0)
         assert_candidates_equal(e.topk(), ref, f"N={N} tc={tc}")
         if tc and N <= 15:
             assert e.stat("survivors") < 0.02 * e.stat("pairs")

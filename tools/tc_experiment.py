@@ -20,7 +20,7 @@ for dbg in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else '0
     ms = e.stat("time_scan_ns") / 5 / 1e6
     for k in ("seed", "merge", "final"): e.stat(f"time_{k}_ns")
     e.set_option("time_kernels", 0)
-    tiles = n / 128 * ((1024 + 255) // 256) / 148
+    tiles = n / 256 * ((1024 + 127) // 128) / 148   # 256-row x 128-frame tiles per SM
     if dbg & 8:
         print("   flagged by (part, quarter):", [e.stat(f"prof{i}") for i in range(16)])
     if dbg & 16:
@@ -43,4 +43,4 @@ for dbg in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else '0
         for nm, v in zip(names, vals):
             div = tiles_tot * (16 if nm.startswith("epi") else 1)
             print(f"   {nm:18s} {v/div:8.0f} cycles/tile")
-    print(f"dbg={dbg} scan {ms:.3f} ms  -> {ms*1e-3*1.9e9/tiles:.0f} cycles/tile  survivors/pair {e.stat('survivors')/e.stat('pairs'):.2e} flagged-chunks/tile {e.stat('flagged')/(tiles*148):.3f}")
+    print(f"dbg={dbg} scan {ms:.3f} ms  -> {ms*1e-3*1.9e9/tiles:.0f} cycles/tile(256x128)  survivors/pair {e.stat('survivors')/e.stat('pairs'):.2e} flagged-chunks/tile {e.stat('flagged')/(tiles*148):.3f}")

@@ -73,6 +73,24 @@ __global__ void probe_kernel(const __grid_constant__ CUtensorMap ma, const __gri
         }
         tc_fence_after();
     }
+    if (mode == 4 || mode == 5) {   // N=128 (mode 4) / N=256 (mode 5) rounds of 10 / 5 MMAs
+        const int NN = mode == 4 ? 128 : 256;
+        const uint32_t id2 = idesc_f16_f32(M, NN);
+        for (int r = 0; r < reps; ++r) {
+            if (threadIdx.x == 0) {
+                tc_fence_after();
+                const int nm = mode == 4 ? 10 : 5;
+                for (int i = 0; i < nm; ++i) {
+                    uint64_t da = desc_sw128_kmajor(smem_u32(s.a) + (i % 4) * 32);
+                    uint64_t db = desc_sw128_kmajor(smem_u32(s.b) + (i % 4) * 32);
+                    mma_f16(tmem + (mode == 4 ? (i / 5) * 128 : 0), da, db, id2, (i % 5) > 0 ? 1u : 0u);
+                }
+                if ((r % 16) == 15 || r == reps - 1) mma_commit(&s.bar_mma);
+            }
+            if ((r % 16) == 15 || r == reps - 1) { mbar_wait(&s.bar_mma, phase); phase ^= 1; }
+        }
+        tc_fence_after();
+    }
     long long t1 = clock64();
     if (mode == 2) {  // TMEM load throughput: all 4 warps read all 256 columns, reps times
         uint32_t acc = 0;
@@ -201,6 +219,14 @@ int main() {
     CK(cudaDeviceSynchronize());
     cudaEventElapsedTime(&ms, e0, e1);
     printf("148 CTAs tmem ld: %.3f ms -> %.1f TB/s total\n", ms, 128.0 * 1024 * 2048 * 148 / ms / 1e9);
+    for (int mode = 4; mode <= 5; ++mode) {
+        reps = 2048;
+        probe_kernel<<<1, 128, smem>>>(ma, mb, dD, reps, dc, mode);
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost));
+        printf("mode %d (%s): %.1f cycles per round (32768 x K80 pairs)\n", mode,
+               mode == 4 ? "10 x M128N128K16" : "5 x M128N256K16", (double)cyc / reps);
+    }
     CK(cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     reps = 256;
     probe_kernel<<<1, 256, smem>>>(ma, mb, dD, reps, dc, 3);
