@@ -107,7 +107,8 @@ struct TcScanArgs {
     unsigned long long *stat_survivors;
     unsigned long long *stat_flagged;   // (frame, row tile) pairs that took the cold path
     uint32_t nq, n_items, n_qblocks, qb, n_sub, N, kc, stages;
-    uint32_t dbg;                 // profiling only: 1 skip epilogue math, 2 skip MMA, 4 skip cold path
+    uint32_t dbg;
+    unsigned long long *prof;     // [16] per-role cycle counters when dbg & 32 (profiling only)                 // profiling only: 1 skip epilogue math, 2 skip MMA, 4 skip cold path
 };
 
 constexpr u64 kShiftPad = 0x7FFFFFFFFFFFFFFFull;   // "not scored on this rank" (MIN-reducible)

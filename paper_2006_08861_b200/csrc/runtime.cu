@@ -492,7 +492,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     if (on_device) OL_LAUNCH(c, launch_check_finite(q, nq64 * OL_K, c->flags_d, c->stream));
 
     const bool seed = c->opt_tau_seed != 0;
-    if (seed) {
+    if (seed && !(c->opt_tc_debug & 64)) {   // (tc_debug & 64: profiling, keep the last thresholds)
         SeedArgs sa;
         sa.coarse = c->coarse; sa.fine = c->fine; sa.queries = q; sa.subs = c->subs_d;
         sa.tau0 = c->tau0_d; sa.nq = nq; sa.n_sub = c->n_sub; sa.N = N; sa.kc = (uint32_t)c->kc;
@@ -518,7 +518,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         OL_CUDA(c, grow(&c->qmeta, &c->qmeta_cap, nq));
         OL_CUDA(c, cudaMemsetAsync(c->tcstat_d + 2, 0, 2 * sizeof(uint32_t), c->stream));
         OL_LAUNCH(c, launch_tc_prep_queries(q, nq, nq_pad, c->q16, c->qx16, c->qmeta, c->tcstat_d, c->stream));
-        if (!seed) OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
+        if (!seed && !(c->opt_tc_debug & 64)) OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
         CUtensorMap map_q, map_qx;
         if (!make_tc_map(&map_q, c->q16, nq_pad, qb, OL_K) || !make_tc_map(&map_qx, c->qx16, nq_pad, qb, 16))
             return fail(c, OL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -527,7 +527,8 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         a.g_tau = c->tau0_d; a.queries = q; a.coarse = c->coarse; a.fine = c->fine;
         a.partial = c->partial_d; a.stat_survivors = c->stat_d; a.stat_flagged = c->stat_d + 1;
         a.nq = nq; a.n_items = n_items; a.n_qblocks = n_qblocks; a.qb = qb; a.n_sub = c->n_sub;
-        a.N = N; a.kc = (uint32_t)c->kc; a.stages = tc_stages; a.dbg = (uint32_t)c->opt_tc_debug;
+        a.N = N; a.kc = (uint32_t)c->kc; a.stages = tc_stages; a.dbg = (uint32_t)c->opt_tc_debug; a.prof = c->prof_d;
+        if (a.dbg & 32) OL_CUDA(c, cudaMemsetAsync(c->prof_d, 0, 64 * sizeof(unsigned long long), c->stream));
         TimeScope ts(c, ol_ctx::T_SCAN);
         OL_LAUNCH(c, launch_tcscan(c->map_rows, c->map_rowsx, map_q, map_qx, a, (int)(n_items * n_qblocks), c->stream));
         c->used_tc = true;
@@ -828,7 +829,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "tc")) { if (v < -1 || v > 1) goto bad; c->opt_tc = v; }
     else if (!strcmp(key, "scan2")) { if (v < 0 || v > 2) goto bad; c->opt_scan2 = v; }
     else if (!strcmp(key, "tc_min_frames")) { if (v < 1) goto bad; c->opt_tc_min_frames = v; }
-    else if (!strcmp(key, "tc_debug")) { if (v < 0 || v > 31) goto bad; c->opt_tc_debug = v; }
+    else if (!strcmp(key, "tc_debug")) { if (v < 0 || v > 255) goto bad; c->opt_tc_debug = v; }
     else return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown option '%s'", key);
     return OL_OK;
 bad:

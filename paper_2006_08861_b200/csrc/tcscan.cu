@@ -49,7 +49,7 @@ constexpr int kMaxStages = 8;
 constexpr int kEpiWarps = 8;
 constexpr int kExactWarps = 2;
 constexpr int kTcThreads = 32 * (2 + kEpiWarps + kExactWarps);
-constexpr int kRing = 1024;             // survivor ring entries (r_local << 8 | q_local)
+constexpr int kEv = 128;                // survivor event ring entries per exact warp
 constexpr float kTauInflate = 1.0f + 1.0f / 131072.0f;   // 1 + 2^-17
 constexpr uint32_t kStageBytes = kTileRows * (kK + kKx) * 2;   // 20 KB
 
@@ -61,10 +61,14 @@ struct TcSmem {
     float alpha[kQB];
     uint32_t tau[kQB];
     int lock[kQB];
-    // survivor queue: bounded MPMC ring with per-slot sequence numbers (Vyukov):
-    // slot i is free for position p when seq == p, filled when seq == p + 1
-    uint32_t seq[kRing], val[kRing];
-    unsigned int prod, cons_res, closed_at;
+    // survivor events, one MPSC ring per exact warp (frames ql % kExactWarps == w):
+    // event = (first row of a 128-row block << 8 | ql, 4 x 32-row pass masks); slot i
+    // is free for position p when seq == p, filled when seq == p + 1 (Vyukov)
+    uint4 ev_mask[kExactWarps][kEv];
+    uint32_t ev_head[kExactWarps][kEv];
+    uint32_t seq[kExactWarps][kEv];
+    alignas(16) float qexact[kExactWarps][kK];   // the event's frame (fp32), per exact warp
+    unsigned int prod[kExactWarps], closed_at[kExactWarps];
     int closed;
     // dynamic, 1024-aligned: n_stages x {rows main [128][64] SW128, rows extra [128][16] SW32},
     // then the top-N lists u64 [qb][N]
@@ -95,29 +99,57 @@ __device__ __forceinline__ float max3f(float a, float b, float c) {  // FMNMX3
     return r;
 }
 
-// Enqueue a survivor (r_local << 8 | q_local) on the MPMC ring, waiting while full.
-__device__ __forceinline__ void tc_enqueue(TcSmem &s, uint32_t e) {
-    const unsigned pos = atomicAdd(&s.prod, 1u);
-    uint32_t *sq = &s.seq[pos % kRing];
-    while (lds_u32(sq) != pos) __nanosleep(64);
-    s.val[pos % kRing] = e;
+// Publish one survivor event (the passing rows of one frame's 128-row block) on
+// the ring of the exact warp that owns the frame, waiting while it is full.
+__device__ __noinline__ void tc_enqueue_event(TcSmem &s, const uint32_t (&mk)[4], uint32_t rb, uint32_t ql,
+                                              unsigned long long *prof) {
+    const uint32_t w = ql % kExactWarps;
+    const unsigned pos = atomicAdd(&s.prod[w], 1u);
+    uint32_t *sq = &s.seq[w][pos % kEv];
+    if (lds_u32(sq) != pos) {
+        const long long r0 = clock64();
+        while (lds_u32(sq) != pos) __nanosleep(64);
+        if (prof) atomicAdd(&prof[10], (unsigned long long)(clock64() - r0));
+    }
+    s.ev_mask[w][pos % kEv] = make_uint4(mk[0], mk[1], mk[2], mk[3]);
+    s.ev_head[w][pos % kEv] = (rb << 8) | ql;
     __threadfence_block();
     sts_u32(sq, pos + 1);
 }
 
-// Enqueue the passing columns of one frame's 128-row block with one reservation:
-// all values first, one fence, then the sequence numbers that publish them.
-__device__ __noinline__ void tc_enqueue_mask(TcSmem &s, uint32_t (&mk)[4], uint32_t rb, uint32_t ql, uint32_t cnt) {
-    const unsigned pos0 = atomicAdd(&s.prod, cnt);
-    unsigned pos = pos0;
-    for (int c = 0; c < 4; ++c)
-        for (uint32_t m = mk[c]; m; m &= m - 1, ++pos) {
-            const uint32_t j = __ffs(m) - 1;
-            while (lds_u32(&s.seq[pos % kRing]) != pos) __nanosleep(64);
-            s.val[pos % kRing] = ((rb + 32 * c + j) << 8) | ql;
-        }
-    __threadfence_block();
-    for (unsigned p = pos0; p != pos; ++p) sts_u32(&s.seq[p % kRing], p + 1);
+// Merge one key per lane (kPadKey = none) into the ascending list L[0..N) held in
+// shared memory, keeping the N smallest.  List element a goes to a + #(keys < L[a]);
+// key j to #(L < key_j) + #(keys < key_j).  Ranks of distinct keys are distinct, so
+// the scatter writes each slot < N exactly once.
+__device__ __noinline__ void tc_warp_merge(u64 *L, uint32_t N, u64 key, int lane) {
+    constexpr int kPer = (OL_MAX_N + 31) / 32;
+    u64 lv[kPer];
+    uint32_t rk[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        const uint32_t a = lane + 32 * i;
+        lv[i] = a < N ? L[a] : kPadKey;
+        rk[i] = a;
+    }
+    // my key's rank among the list: lower bound by binary search
+    uint32_t lo = 0, hi = N;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (L[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    uint32_t kr = lo;
+    for (int j = 0; j < 32; ++j) {
+        const u64 kj = __shfl_sync(0xffffffffu, key, j);
+        kr += kj < key;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) rk[i] += kj < lv[i];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < kPer; ++i)
+        if (lane + 32 * i < N && rk[i] < N) L[rk[i]] = lv[i];
+    if (key != kPadKey && kr < N) L[kr] = key;
+    __syncwarp();
 }
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -155,6 +187,8 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     const uint32_t qn = min(a.qb, a.nq - q0);
     const uint32_t N = a.N;
     const uint32_t n_tiles = (it.count + kTileRows - 1) / kTileRows;
+    const bool prof = (a.dbg & 32) != 0;
+    const long long t_start = clock64();
 
     // ---------------------------------------------------------------- setup
     if (threadIdx.x == 0) {
@@ -162,7 +196,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         for (int i = 0; i < 2; ++i) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], kEpiWarps); }
         mbar_init(&s.qbar, 1);
         fence_mbar_init();
-        s.prod = s.cons_res = s.closed_at = 0;
+        for (int w = 0; w < kExactWarps; ++w) s.prod[w] = s.closed_at[w] = 0;
         s.closed = 0;
         tma_prefetch(&map_rows);
         tma_prefetch(&map_rowsx);
@@ -185,7 +219,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         }
         s.lock[q] = 0;
     }
-    for (uint32_t i = threadIdx.x; i < kRing; i += blockDim.x) s.seq[i] = i;
+    for (uint32_t i = threadIdx.x; i < kExactWarps * kEv; i += blockDim.x) s.seq[i / kEv][i % kEv] = i % kEv;
     for (uint32_t i = threadIdx.x; i < a.qb * N; i += blockDim.x) lists[i] = kPadKey;
     tc_fence_before();
     __syncthreads();
@@ -203,6 +237,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 if (t >= n_stages) mbar_wait_sleep(&s.empty[st], ((t / n_stages) - 1) & 1);
                 unsigned char *sb = stage0 + (size_t)st * kStageBytes;
                 const int r0 = (int)(it.row_begin + (uint64_t)t * kTileRows);
+                if ((a.dbg & 128) && t >= n_stages) { mbar_arrive(&s.full[st]); continue; }   // profiling: stale rows
                 mbar_expect_tx(&s.full[st], kStageBytes);
                 tma_load_2d(sb, &map_rows, &s.full[st], 0, r0);
                 tma_load_2d(sb + kTileRows * kK * 2, &map_rowsx, &s.full[st], 0, r0);
@@ -212,12 +247,16 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         // ------------------------------------------------------------ MMA issuer
         if (lane == 0) {
             const uint32_t idesc = idesc_f16_f32(128, kTileRows);   // M = 128 frames, N = 256 rows
+            long long pw_full = 0, pw_tempty = 0;
             mbar_wait(&s.qbar, 0);
             const uint32_t qm = smem_u32(s.qm), qx = smem_u32(s.qx);
             for (uint32_t t = 0; t < n_tiles; ++t) {
                 const uint32_t st = t % n_stages, buf = t & 1;
+                long long c0 = clock64();
                 mbar_wait_sleep(&s.full[st], (t / n_stages) & 1);
+                long long c1 = clock64();
                 if (t >= 2) mbar_wait_sleep(&s.tempty[buf], ((t >> 1) - 1) & 1);
+                if (prof) { pw_full += c1 - c0; pw_tempty += clock64() - c1; }
                 tc_fence_after();
                 const uint32_t rm = smem_u32(stage0 + (size_t)st * kStageBytes), rx = rm + kTileRows * kK * 2;
                 const uint32_t d = tmem + buf * kTileRows;
@@ -230,6 +269,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 mma_commit(&s.empty[st]);
                 mma_commit(&s.tfull[buf]);
             }
+            if (prof) { atomicAdd(&a.prof[0], (unsigned long long)pw_full); atomicAdd(&a.prof[1], (unsigned long long)pw_tempty); }
         }
     } else if (warp < 2 + kEpiWarps) {
         // ------------------------------------------------------------ epilogue
@@ -241,11 +281,14 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         const bool refresher = half == 0;         // one of the two warps per frame refreshes tau
         const float alpha = s.alpha[ql];
         uint32_t gt = 0xFFFFFFFFu;                // shared running threshold, loaded 8 tiles ahead
+        long long ew_tfull = 0;
         for (uint32_t t = 0; t < n_tiles; ++t) {
             const uint32_t buf = t & 1;
             const uint32_t gt_prev = gt;
             if (refresher && (t & 7) == 0 && ql < qn) gt = __ldcg(&a.g_tau[(size_t)(q0 + ql) * a.n_sub + it.sub]);
+            const long long w0 = prof ? clock64() : 0;
             mbar_wait_sleep(&s.tfull[buf], (t >> 1) & 1);
+            if (prof && lane == 0) ew_tfull += clock64() - w0;
             tc_fence_after();
             uint32_t v0[32], v1[32], v2[32], v3[32];
             const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * kTileRows + half * 128;
@@ -272,85 +315,106 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 // cold path (rare): enqueue exactly the passing columns; columns past the
                 // item's last row (last tile only) are excluded by the mask
                 if (fmaxf(m0, m1) >= h && ql < qn && !(a.dbg & 4)) {
+                    const long long e0 = clock64();
                     uint32_t mk[4] = {mask32(v0, h, 0, nvalid), mask32(v1, h, 32, nvalid),
                                       mask32(v2, h, 64, nvalid), mask32(v3, h, 96, nvalid)};
                     const uint32_t cnt = __popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]);
-                    if (cnt) tc_enqueue_mask(s, mk, rb, ql, cnt);
+                    if (cnt) tc_enqueue_event(s, mk, rb, ql, prof ? a.prof : nullptr);
                     if (a.stat_flagged) atomicAdd(a.stat_flagged, 1ull);
+                    if (prof) {
+                        const unsigned long long d = clock64() - e0;
+                        atomicAdd(&a.prof[2], d); atomicMax(&a.prof[3], d); atomicAdd(&a.prof[4], (unsigned long long)cnt);
+                        atomicMax(&a.prof[5], (unsigned long long)cnt);
+                    }
                 }
             }
             // the shared threshold loaded 8 tiles ago: tighten this frame's if another CTA did better
             if (refresher && (t & 7) == 7 && ql < qn && gt_prev < lds_u32(&s.tau[ql])) atomicMin(&s.tau[ql], gt_prev);
         }
+        if (prof && lane == 0) atomicAdd(&a.prof[6], (unsigned long long)ew_tfull);
         named_bar(1, 32 * kEpiWarps);
         if (warp == 2 && lane == 0) {
             __threadfence_block();
-            sts_u32(&s.closed_at, lds_u32(&s.prod));
+            for (int w = 0; w < kExactWarps; ++w) sts_u32(&s.closed_at[w], lds_u32(&s.prod[w]));
             __threadfence_block();
             sts_u32(&s.closed, 1u);
         }
     } else {
         // ------------------------------------------------------------ exact re-scoring
-        while (true) {
-            const unsigned p = atomicAdd(&s.cons_res, 1u);
-            uint32_t *sq = &s.seq[p % kRing];
+        // one warp per event: lane j re-scores row rb + 32 c + j of each pass mask c with
+        // the exact fp32 chain (R3); the warp owns its frames' lists, so insertion needs
+        // no lock.  Idle lanes import the thresholds other CTAs published (any value ever
+        // held is a valid bound, so races only loosen the test).
+        const uint32_t xw = warp - (2 + kEpiWarps);
+        float *qe = s.qexact[xw];
+        for (unsigned p = 0;; ++p) {
+            uint32_t *sq = &s.seq[xw][p % kEv];
             bool got = false;
-            uint32_t idle = 0, nap = 64;
+            uint32_t idle = 0, nap = 32;
             while (true) {
                 if (lds_u32(sq) == p + 1) { got = true; break; }
-                if (lds_u32(&s.closed) && p >= lds_u32(&s.closed_at)) break;
-                // idle: import the running thresholds other CTAs published (any value
-                // ever held is a valid bound, so races only loosen the test)
-                const uint32_t qi = (idle++ * (32 * kExactWarps) + (threadIdx.x - 32 * (2 + kEpiWarps))) % kQB;
+                if (lds_u32(&s.closed) && p >= lds_u32(&s.closed_at[xw])) break;
+                const uint32_t qi = ((idle++ * 32 + lane) * kExactWarps + xw) % kQB;
                 if (qi < qn) {
                     const uint32_t g = __ldcg(&a.g_tau[(size_t)(q0 + qi) * a.n_sub + it.sub]);
                     if (g < lds_u32(&s.tau[qi])) atomicMin(&s.tau[qi], g);
                 }
                 __nanosleep(nap);
-                if (nap < 2048) nap <<= 1;
+                if (nap < 1024) nap <<= 1;
             }
             if (!got) break;
+            const long long x0 = prof ? clock64() : 0;
             __threadfence_block();
-            const uint32_t e = s.val[p % kRing];
+            const uint4 mv = s.ev_mask[xw][p % kEv];
+            const uint32_t head = s.ev_head[xw][p % kEv];
+            __syncwarp();
             __threadfence_block();
-            sts_u32(sq, p + kRing);
-            const uint32_t rl = e >> 8, col = e & 0xFF;
-            const uint64_t row = it.row_begin + rl;
-            const float4 *qv = reinterpret_cast<const float4 *>(a.queries + (size_t)(q0 + col) * kK);
-            float acc = 0.f;
-            for (uint32_t k4 = 0; k4 < a.kc / 4; ++k4) {
-                const float4 x = __ldg(qv + k4);
-                const float4 f = __ldg(reinterpret_cast<const float4 *>(a.coarse + coarse_off(row, 4 * k4, a.kc)));
-                acc = chain_step_tc(acc, x.x, f.x); acc = chain_step_tc(acc, x.y, f.y);
-                acc = chain_step_tc(acc, x.z, f.z); acc = chain_step_tc(acc, x.w, f.w);
-            }
-            if (a.kc < (uint32_t)kK) {
-                const float4 *fr = reinterpret_cast<const float4 *>(a.fine + row * (kK - a.kc));
-                for (uint32_t k4 = a.kc / 4; k4 < (uint32_t)kK / 4; ++k4) {
-                    const float4 x = __ldg(qv + k4), f = __ldg(fr + k4 - a.kc / 4);
-                    acc = chain_step_tc(acc, x.x, f.x); acc = chain_step_tc(acc, x.y, f.y);
-                    acc = chain_step_tc(acc, x.z, f.z); acc = chain_step_tc(acc, x.w, f.w);
-                }
-            }
-            const u64 key = ((u64)__float_as_uint(acc) << 32) | (u64)(it.frame_begin + rl);
+            if (lane == 0) sts_u32(sq, p + kEv);
+            if (a.dbg & 8) continue;   // profiling: drop survivors unscored (wrong results)
+            const uint32_t col = head & 0xFF, rb = head >> 8;
+            if (lane < kK / 4)
+                reinterpret_cast<float4 *>(qe)[lane] = __ldg(reinterpret_cast<const float4 *>(a.queries + (size_t)(q0 + col) * kK) + lane);
+            __syncwarp();
             u64 *L = lists + (size_t)col * N;
-            if (key < lds_u64(&L[N - 1])) {
-                while (atomicCAS(&s.lock[col], 0, 1) != 0) __nanosleep(16);
-                __threadfence_block();
-                if (key < L[N - 1]) {
-                    int pidx = (int)N - 1;
-                    while (pidx > 0 && L[pidx - 1] > key) { L[pidx] = L[pidx - 1]; --pidx; }
-                    L[pidx] = key;
-                    if (L[N - 1] != kPadKey) {
-                        const uint32_t tb = (uint32_t)(L[N - 1] >> 32);
-                        atomicMin(&s.tau[col], tb);
-                        atomicMin(&a.g_tau[(size_t)(q0 + col) * a.n_sub + it.sub], tb);
+            const uint32_t mks[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                if (!mks[c]) continue;
+                const bool act = (mks[c] >> lane) & 1u;
+                u64 key = kPadKey;
+                if (act) {
+                    const uint32_t rl = rb + 32 * c + lane;
+                    const uint64_t row = it.row_begin + rl;
+                    float4 f[kK / 4];
+#pragma unroll
+                    for (int k4 = 0; k4 < kK / 4; ++k4)
+                        f[k4] = 4 * k4 < (int)a.kc
+                                    ? __ldg(reinterpret_cast<const float4 *>(a.coarse + coarse_off(row, 4 * k4, a.kc)))
+                                    : __ldg(reinterpret_cast<const float4 *>(a.fine + row * (kK - a.kc) + (4 * k4 - a.kc)));
+                    float acc = 0.f;
+#pragma unroll
+                    for (int k4 = 0; k4 < kK / 4; ++k4) {
+                        const float4 x = reinterpret_cast<const float4 *>(qe)[k4];
+                        acc = chain_step_tc(acc, x.x, f[k4].x); acc = chain_step_tc(acc, x.y, f[k4].y);
+                        acc = chain_step_tc(acc, x.z, f[k4].z); acc = chain_step_tc(acc, x.w, f[k4].w);
                     }
+                    key = ((u64)__float_as_uint(acc) << 32) | (u64)(it.frame_begin + rl);
                 }
-                __threadfence_block();
-                atomicExch(&s.lock[col], 0);
+                // merge the warp's keys into the sorted list: every key's rank in the union
+                // (keys are distinct: one per (frame, row); pads rank last) is its new slot
+                if (__any_sync(0xffffffffu, key < lds_u64(&L[N - 1]))) tc_warp_merge(L, N, key, lane);
             }
-            if (a.stat_survivors) atomicAdd(a.stat_survivors, 1ull);
+            if (lane == 0) {
+                const u64 last = L[N - 1];
+                if (last != kPadKey) {
+                    const uint32_t tb = (uint32_t)(last >> 32);
+                    atomicMin(&s.tau[col], tb);
+                    atomicMin(&a.g_tau[(size_t)(q0 + col) * a.n_sub + it.sub], tb);
+                }
+                if (a.stat_survivors) atomicAdd(a.stat_survivors, (unsigned long long)(__popc(mv.x) + __popc(mv.y) + __popc(mv.z) + __popc(mv.w)));
+                if (prof) atomicAdd(&a.prof[7], (unsigned long long)(clock64() - x0));
+            }
+            __syncwarp();
         }
     }
 
@@ -358,6 +422,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     tc_fence_before();
     __syncthreads();
     if (warp == 1) tmem_dealloc<512>(tmem);
+    if (prof && threadIdx.x == 0) { atomicAdd(&a.prof[8], (unsigned long long)(clock64() - t_start)); atomicAdd(&a.prof[9], (unsigned long long)n_tiles); }
     for (uint32_t i = threadIdx.x; i < qn * N; i += blockDim.x) {
         const uint32_t q = i / N, r = i % N;
         a.partial[((size_t)(q0 + q) * a.n_items + item_id) * N + r] = lists[(size_t)q * N + r];

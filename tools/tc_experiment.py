@@ -1,5 +1,5 @@
 """Timing experiments on the tensor-core scan (C3-size DB, 1,024 frames)."""
-import sys, torch, time
+import sys, os, torch, time
 sys.path.insert(0, '.')
 import synthgen, paper_2006_08861_b200 as ol
 spec = synthgen.CONFIGS["C4"].spec
@@ -9,15 +9,17 @@ F, C = synthgen.db_device(spec, 0, n, dev)
 Q, _ = synthgen.render_device(spec, synthgen.query_points(spec, 4242, 1024), dev)
 e = ol.Engine(0)
 e.upload(F, C, [n], spec.grid())
+import os
+if os.environ.get("CHUNK"): e.set_option("chunk", int(os.environ["CHUNK"]))
 Q3 = Q.view(-1, 1, 64)
 for dbg in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else '0,1,4')]:
     e.set_option("tc_debug", dbg)
     for _ in range(2): e.query(Q3, N=15)
     torch.cuda.synchronize()
     e.set_option("time_kernels", 1)
-    for _ in range(5): e.query(Q3, N=15)
+    for _ in range(int(os.environ.get('REPS', 5))): e.query(Q3, N=15)
     torch.cuda.synchronize()
-    ms = e.stat("time_scan_ns") / 5 / 1e6
+    ms = e.stat("time_scan_ns") / int(os.environ.get("REPS", 5)) / 1e6
     for k in ("seed", "merge", "final"): e.stat(f"time_{k}_ns")
     e.set_option("time_kernels", 0)
     tiles = n / 256 * ((1024 + 127) // 128) / 148   # 256-row x 128-frame tiles per SM
@@ -43,4 +45,8 @@ for dbg in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else '0
         for nm, v in zip(names, vals):
             div = tiles_tot * (16 if nm.startswith("epi") else 1)
             print(f"   {nm:18s} {v/div:8.0f} cycles/tile")
-    print(f"dbg={dbg} scan {ms:.3f} ms  -> {ms*1e-3*1.9e9/tiles:.0f} cycles/tile(256x128)  survivors/pair {e.stat('survivors')/e.stat('pairs'):.2e} flagged-chunks/tile {e.stat('flagged')/(tiles*148):.3f}")
+    if dbg & 32:
+        P = [e.stat(f"prof{i}") for i in range(12)]
+        nt = P[9] * 1.0
+        print(f"   per tile: mma wait full {P[0]/nt:.0f} tempty {P[1]/nt:.0f}; epi cold {P[2]/nt/8:.0f}/warp (events {e.stat('flagged')}, max {P[3]}, cycles/ev {P[2]/max(e.stat('flagged'),1):.0f}, cnt/ev {P[4]/max(e.stat('flagged'),1):.1f} max {P[5]}); epi wait tfull {P[6]/nt/8:.0f}; exact busy {P[7]/nt/2:.0f}/warp; CTA cycles/tile {P[8]/nt:.0f}; ring-full wait {P[10]}")
+    print(f"chunk={e.stat('chunk')} items={e.stat('items')} dbg={dbg} scan {ms:.3f} ms  -> {ms*1e-3*1.9e9/tiles:.0f} cycles/tile(256x128)  survivors/pair {e.stat('survivors')/e.stat('pairs'):.2e} flagged-chunks/tile {e.stat('flagged')/(tiles*148):.3f}")
