@@ -97,6 +97,7 @@ struct AggArgs {
 
 struct TcScanArgs {
     const WorkItem *items;
+    const float2 *blk;            // [rows_pad / 32] per 32-row block: (min RD||f||^2/2, max RU e_f)
     const float2 *qmeta;          // [nq] (RD ||q||^2, RU ||q - fp16(q)||)
     const uint32_t *bounds;       // [2] batch norm bound bits, [3] force_all (a frame left the fp16 range)
     float nf_max;                 // database norm bound
@@ -107,8 +108,9 @@ struct TcScanArgs {
     unsigned long long *stat_survivors;
     unsigned long long *stat_flagged;   // (frame, row tile) pairs that took the cold path
     uint32_t nq, n_items, n_qblocks, qb, n_sub, N, kc, stages;
-    uint32_t dbg;
-    unsigned long long *prof;     // [16] per-role cycle counters when dbg & 32 (profiling only)                 // profiling only: 1 skip epilogue math, 2 skip MMA, 4 skip cold path
+    uint32_t dbg;                 // profiling only: 1 skip epilogue math, 2 skip MMA, 4 skip cold path, ...
+    uint32_t n_blk;               // rows_pad / 32
+    unsigned long long *prof;     // [16] per-role cycle counters when dbg & 32 (profiling only)
 };
 
 constexpr u64 kShiftPad = 0x7FFFFFFFFFFFFFFFull;   // "not scored on this rank" (MIN-reducible)
@@ -126,13 +128,14 @@ struct ShiftArgs {
 // launchers (return cudaGetLastError())
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s);
 cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, uint64_t rows, void *plane,
-                                void *ext, uint32_t *nf_max, uint32_t *maxabs, cudaStream_t s);
-cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, void *qx, float2 *qmeta,
+                                float2 *blk, uint32_t *stat, cudaStream_t s);
+cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float2 *qmeta,
                                    uint32_t *bounds, cudaStream_t s);
 cudaError_t launch_fill_u32(uint32_t *p, uint64_t n, uint32_t v, cudaStream_t s);
+cudaError_t launch_pad_rows(const SubInfo *subs, uint32_t n_sub, int kc, float *coarse, float *fine, cudaStream_t s);
 bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows, uint32_t width);
-cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_rowsx, const CUtensorMap &map_q,
-                          const CUtensorMap &map_qx, const TcScanArgs &a, int grid, cudaStream_t s);
+cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q, const TcScanArgs &a, int grid,
+                          cudaStream_t s);
 size_t tc_smem_bytes(uint32_t qb, uint32_t N, uint32_t stages);
 bool tc_shape(uint32_t N, uint32_t nq, uint32_t *qb, uint32_t *stages);
 cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s);

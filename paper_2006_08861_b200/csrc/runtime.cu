@@ -39,14 +39,13 @@ struct ol_ctx {
     int32_t *coords = nullptr;
     // tensor-core filter operands (tcscan.cu): fp16 rows + per-row bound terms
     void *plane16 = nullptr;       // fp16 rows [rows][64]
-    void *ext16 = nullptr;         // fp16 extra K block [rows][16] = (hi, lo, ef16, 0...)
+    float2 *blk = nullptr;         // per 32-row block: (min RD||f||^2/2, max RU e_f) of the row bound terms
     uint32_t *tcstat_d = nullptr;  // [0] database norm bound bits, [1] max |f| bits,
                                    // [2] batch norm bound bits, [3] force_all
     bool tc_ok = false;
     float nf_max = 0.f;
-    CUtensorMap map_rows, map_rowsx;
+    CUtensorMap map_rows;
     void *q16 = nullptr; size_t q16_cap = 0;
-    void *qx16 = nullptr; size_t qx16_cap = 0;
     float2 *qmeta = nullptr; size_t qmeta_cap = 0;
     bool used_tc = false;
     // NEXT-1 profiles and shift keys
@@ -82,7 +81,7 @@ struct ol_ctx {
     uint64_t n_cand = 0, per_bundle = 0, pairs = 0;
     int launches = 0;
     // options
-    int64_t opt_chunk = 0, opt_qtile = 0, opt_tau_seed = 1, opt_ctas = 0, opt_time = 0;
+    int64_t opt_chunk = 0, opt_qtile = 0, opt_tau_seed = 1, opt_ctas = 0, opt_time = 0, opt_seed_samples = 4096;
     int64_t opt_tc = -1;         // tensor-core filter: -1 auto (>= 32 frames), 0 off, 1 always
     int64_t opt_tc_min_frames = 32;
     int64_t opt_tc_debug = 0;
@@ -168,10 +167,10 @@ static ol_status check_params(ol_ctx *c, const ol_params *p, bool need_agg) {
 
 static void free_db(ol_ctx *c) {
     cudaFree(c->coarse); cudaFree(c->fine); cudaFree(c->coords); cudaFree(c->subs_d);
-    cudaFree(c->plane16); cudaFree(c->ext16); cudaFree(c->prof);
+    cudaFree(c->plane16); cudaFree(c->blk); cudaFree(c->prof);
     c->prof = nullptr; c->prof_W = 0;
     c->coarse = c->fine = nullptr; c->coords = nullptr; c->subs_d = nullptr;
-    c->plane16 = nullptr; c->ext16 = nullptr; c->tc_ok = false;
+    c->plane16 = nullptr; c->blk = nullptr; c->tc_ok = false;
     c->db_ready = false;
     c->items.clear();
     c->items_chunk = 0;
@@ -204,7 +203,7 @@ ol_status ol_create(const ol_config *cfg, ol_ctx **out) {
     }
     if (e == cudaSuccess) e = cudaMalloc((void **)&c->flags_d, 4 * sizeof(int));
     if (e == cudaSuccess) e = cudaMalloc((void **)&c->stat_d, 4 * sizeof(unsigned long long));
-    if (e == cudaSuccess) e = cudaMalloc((void **)&c->tcstat_d, 4 * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMalloc((void **)&c->tcstat_d, 8 * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMalloc((void **)&c->prof_d, 1024 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemset(c->flags_d, 0, 4 * sizeof(int));
     if (e != cudaSuccess) {
@@ -225,7 +224,7 @@ void ol_destroy(ol_ctx *c) {
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
     cudaFree(c->prefix_d); cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
     cudaFree(c->flags_d); cudaFree(c->stat_d); cudaFree(c->tcstat_d); cudaFree(c->prof_d);
-    cudaFree(c->q16); cudaFree(c->qx16); cudaFree(c->qmeta); cudaFree(c->qprof_d); cudaFree(c->shift_keys);
+    cudaFree(c->q16); cudaFree(c->qmeta); cudaFree(c->qprof_d); cudaFree(c->shift_keys);
     for (auto &v : c->ev)
         for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -351,12 +350,17 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
             OL_CUDA(c, launch_relayout(src + src_begin[i] * OL_K, subs[i].count, subs[i].row_begin, kc, c->coarse,
                                        c->fine, c->stream));
         }
+        // tile-padding rows repeat their subspace's last row (never reported: every kernel
+        // bounds rows by the subspace count), so per-block row terms stay tight
+        OL_CUDA(c, cudaMemcpyAsync(c->subs_d, subs.data(), sizeof(SubInfo) * ns, cudaMemcpyHostToDevice,
+                                   c->stream));
+        OL_CUDA(c, launch_pad_rows(c->subs_d, ns, kc, c->coarse, c->fine, c->stream));
         if (c->opt_tc != 0) {
             OL_CUDA(c, cudaMalloc(&c->plane16, sizeof(uint16_t) * rows_pad * OL_K));
-            OL_CUDA(c, cudaMalloc(&c->ext16, sizeof(uint16_t) * rows_pad * 16));
-            OL_CUDA(c, cudaMemsetAsync(c->tcstat_d, 0, 4 * sizeof(uint32_t), c->stream));
-            OL_CUDA(c, launch_tc_prep_rows(c->coarse, c->fine, kc, rows_pad, c->plane16, c->ext16, c->tcstat_d,
-                                           c->tcstat_d + 1, c->stream));
+            OL_CUDA(c, cudaMalloc((void **)&c->blk, sizeof(float2) * (rows_pad / 32)));
+            OL_CUDA(c, cudaMemsetAsync(c->tcstat_d, 0, 8 * sizeof(uint32_t), c->stream));
+            OL_CUDA(c, launch_tc_prep_rows(c->coarse, c->fine, kc, rows_pad, c->plane16, c->blk, c->tcstat_d,
+                                           c->stream));
         }
     }
     OL_CUDA(c, cudaMemcpyAsync(c->subs_d, subs.data(), sizeof(SubInfo) * ns, cudaMemcpyHostToDevice,
@@ -371,8 +375,7 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
         // fp16 operands need |f| and ||f||^2 / 2 inside the fp16 range, and the row count
         // must fit a TMA coordinate
         c->tc_ok = std::isfinite(nf) && amax < 65000.f && nf < 300.f && rows_pad < (1ull << 31) &&
-                   make_tc_map(&c->map_rows, c->plane16, rows_pad, 256, OL_K) &&
-                   make_tc_map(&c->map_rowsx, c->ext16, rows_pad, 256, 16);
+                   make_tc_map(&c->map_rows, c->plane16, rows_pad, 256, OL_K);
     }
     c->subs = subs;
     c->rows_pad = rows_pad;
@@ -498,7 +501,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         sa.tau0 = c->tau0_d; sa.nq = nq; sa.n_sub = c->n_sub; sa.N = N; sa.kc = (uint32_t)c->kc;
         // splits x (count/8, at most 4096) rows per subspace, about 64k sampled pairs per
         // row... i.e. more splits for few frames; below N rows per split: no seed (+inf)
-        uint32_t S = 4096;
+        uint32_t S = (uint32_t)c->opt_seed_samples;
         uint64_t minc = ~0ull;
         for (auto &s : c->subs) { uint64_t v = s.count / 8; if (v < S) S = (uint32_t)v; if (s.count < minc) minc = s.count; }
         sa.samples = S < 1 ? 1 : S;
@@ -514,23 +517,22 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     if (n_items && use_tc) {
         const uint32_t qb = tc_qb, n_qblocks = (nq + qb - 1) / qb, nq_pad = n_qblocks * qb;
         OL_CUDA(c, grow((uint16_t **)&c->q16, &c->q16_cap, (size_t)nq_pad * OL_K));
-        OL_CUDA(c, grow((uint16_t **)&c->qx16, &c->qx16_cap, (size_t)nq_pad * 16));
         OL_CUDA(c, grow(&c->qmeta, &c->qmeta_cap, nq));
         OL_CUDA(c, cudaMemsetAsync(c->tcstat_d + 2, 0, 2 * sizeof(uint32_t), c->stream));
-        OL_LAUNCH(c, launch_tc_prep_queries(q, nq, nq_pad, c->q16, c->qx16, c->qmeta, c->tcstat_d, c->stream));
+        OL_LAUNCH(c, launch_tc_prep_queries(q, nq, nq_pad, c->q16, c->qmeta, c->tcstat_d, c->stream));
         if (!seed && !(c->opt_tc_debug & 64)) OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
-        CUtensorMap map_q, map_qx;
-        if (!make_tc_map(&map_q, c->q16, nq_pad, qb, OL_K) || !make_tc_map(&map_qx, c->qx16, nq_pad, qb, 16))
+        CUtensorMap map_q;
+        if (!make_tc_map(&map_q, c->q16, nq_pad, qb, OL_K))
             return fail(c, OL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
         TcScanArgs a;
-        a.items = c->items_d; a.qmeta = c->qmeta; a.bounds = c->tcstat_d; a.nf_max = c->nf_max;
+        a.items = c->items_d; a.blk = c->blk; a.n_blk = (uint32_t)(c->rows_pad / 32); a.qmeta = c->qmeta; a.bounds = c->tcstat_d; a.nf_max = c->nf_max;
         a.g_tau = c->tau0_d; a.queries = q; a.coarse = c->coarse; a.fine = c->fine;
         a.partial = c->partial_d; a.stat_survivors = c->stat_d; a.stat_flagged = c->stat_d + 1;
         a.nq = nq; a.n_items = n_items; a.n_qblocks = n_qblocks; a.qb = qb; a.n_sub = c->n_sub;
         a.N = N; a.kc = (uint32_t)c->kc; a.stages = tc_stages; a.dbg = (uint32_t)c->opt_tc_debug; a.prof = c->prof_d;
         if (a.dbg & 32) OL_CUDA(c, cudaMemsetAsync(c->prof_d, 0, 64 * sizeof(unsigned long long), c->stream));
         TimeScope ts(c, ol_ctx::T_SCAN);
-        OL_LAUNCH(c, launch_tcscan(c->map_rows, c->map_rowsx, map_q, map_qx, a, (int)(n_items * n_qblocks), c->stream));
+        OL_LAUNCH(c, launch_tcscan(c->map_rows, map_q, a, (int)(n_items * n_qblocks), c->stream));
         c->used_tc = true;
     } else if (n_items) {
         ScanArgs a;
@@ -824,6 +826,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     if (!strcmp(key, "chunk")) { if (v < 0) goto bad; c->opt_chunk = v; }
     else if (!strcmp(key, "qtile")) { if (v < 0 || v > kMaxQT) goto bad; c->opt_qtile = v; }
     else if (!strcmp(key, "tau_seed")) { if (v != 0 && v != 1) goto bad; c->opt_tau_seed = v; }
+    else if (!strcmp(key, "seed_samples")) { if (v < 16 || v > 8192) goto bad; c->opt_seed_samples = v; }
     else if (!strcmp(key, "ctas")) { if (v < 0) goto bad; c->opt_ctas = v; }
     else if (!strcmp(key, "time_kernels")) { if (v != 0 && v != 1) goto bad; c->opt_time = v; }
     else if (!strcmp(key, "tc")) { if (v < -1 || v > 1) goto bad; c->opt_tc = v; }

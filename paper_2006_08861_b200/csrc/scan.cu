@@ -549,13 +549,19 @@ cudaError_t launch_scan(int kc, const ScanArgs &a, size_t smem, int grid, cudaSt
 // ------------------------------------------------------------------ tau seeding (NK3)
 // tau0[q][i] = the exact N-th smallest acc over an evenly spaced sample of this
 // rank's rows of subspace i (an upper bound on the true N-th acc, so pruning
-// with it is exact).  One CTA per (query, subspace); bitonic sort in smem.
+// with it is exact).  One CTA per (query, subspace, split): the sample's exact fp32
+// chains (float4 row loads, query in shared memory), then the N-th smallest by a
+// 4-pass radix select (8-bit digits) over the acc bits (non-negative floats order as
+// their bits).
 constexpr int kSeedThreads = 256;
-constexpr int kSeedMax = 4096;
+constexpr int kSeedMax = 8192;
 
-__global__ void __launch_bounds__(kSeedThreads) tau_seed_kernel(SeedArgs a) {
+template <int KC>
+__global__ void __launch_bounds__(kSeedThreads, 2) tau_seed_kernel(SeedArgs a) {
     __shared__ uint32_t v[kSeedMax];
-    __shared__ float qs[kK];
+    __shared__ alignas(16) float qs[kK];
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t sel[2];   // digit, count below it
     const uint32_t split = blockIdx.x % a.splits;
     const uint32_t q = (blockIdx.x / a.splits) / a.n_sub, i = (blockIdx.x / a.splits) % a.n_sub;
     const SubInfo si = a.subs[i];
@@ -563,43 +569,79 @@ __global__ void __launch_bounds__(kSeedThreads) tau_seed_kernel(SeedArgs a) {
     if (threadIdx.x < kK) qs[threadIdx.x] = a.queries[(size_t)q * kK + threadIdx.x];
     __syncthreads();
     if (S < a.N) return;   // the caller pre-filled +inf
-    uint32_t P = 1;
-    while (P < S) P <<= 1;
-    for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
-        uint32_t val = 0xFFFFFFFFu;
-        if (s < S) {
-            // split j takes the j-th of `splits` interleaved sample grids
-            const uint64_t row = si.row_begin + (((uint64_t)s * a.splits + split) * si.count) / ((uint64_t)S * a.splits);
-            float acc = 0.f;
-            for (uint32_t k = 0; k < a.kc; ++k) acc = chain_step(acc, qs[k], a.coarse[coarse_off(row, k, a.kc)]);
-            if (a.kc < (uint32_t)kK) {
-                const float *f = a.fine + row * (kK - a.kc);
-                for (uint32_t k = a.kc; k < (uint32_t)kK; ++k) acc = chain_step(acc, qs[k], f[k - a.kc]);
-            }
-            val = __float_as_uint(acc);
+    const float4 *q4 = reinterpret_cast<const float4 *>(qs);
+    for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) {
+        // split j takes the j-th of `splits` interleaved sample grids
+        const uint64_t row = si.row_begin + (((uint64_t)s * a.splits + split) * si.count) / ((uint64_t)S * a.splits);
+        float4 f[kK / 4];   // (KC is a compile-time constant: all 16 loads issue before the chain)
+#pragma unroll
+        for (int k4 = 0; k4 < kK / 4; ++k4)
+            f[k4] = 4 * k4 < KC ? __ldg(reinterpret_cast<const float4 *>(a.coarse + coarse_off(row, 4 * k4, KC)))
+                                : __ldg(reinterpret_cast<const float4 *>(a.fine + row * (kK - KC) + (4 * k4 - KC)));
+        float acc = 0.f;
+#pragma unroll
+        for (int k4 = 0; k4 < kK / 4; ++k4) {
+            const float4 x = q4[k4];
+            acc = chain_step(acc, x.x, f[k4].x); acc = chain_step(acc, x.y, f[k4].y);
+            acc = chain_step(acc, x.z, f[k4].z); acc = chain_step(acc, x.w, f[k4].w);
         }
-        v[s] = val;
+        v[s] = __float_as_uint(acc);
     }
-    __syncthreads();
-    for (uint32_t k = 2; k <= P; k <<= 1) {
-        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-            for (uint32_t t = threadIdx.x; t < P; t += blockDim.x) {
-                uint32_t o = t ^ j;
-                if (o > t) {
-                    bool up = (t & k) == 0;
-                    uint32_t x = v[t], y = v[o];
-                    if ((x > y) == up) { v[t] = y; v[o] = x; }
+    // radix select: the N-th smallest value (1-based), digit by digit from the top
+    uint32_t prefix = 0, pmask = 0, k = a.N;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (uint32_t t = threadIdx.x; t < 256; t += blockDim.x) hist[t] = 0;
+        __syncthreads();
+        // (values share their high digits: warp-aggregated increments avoid serializing
+        // on one bin)
+        for (uint32_t s0 = 0; s0 < S; s0 += blockDim.x) {
+            const uint32_t s = s0 + threadIdx.x;
+            const uint32_t x = s < S ? v[s] : 0u;
+            const bool in = s < S && (x & pmask) == prefix;
+            const uint32_t d = in ? (x >> shift) & 255u : 256u;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            if (in && (threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&hist[d], (uint32_t)__popc(peers));
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {   // one warp: 8 bins per lane, inclusive scan, first bin reaching k
+            const int lane = threadIdx.x;
+            uint32_t c[8], tot = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) { c[j] = hist[lane * 8 + j]; tot += c[j]; }
+            uint32_t incl = tot;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            uint32_t below = incl - tot;
+            const bool here = below < k && k <= incl;
+            if (here) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (below + c[j] >= k) { sel[0] = lane * 8 + j; sel[1] = below; break; }
+                    below += c[j];
                 }
             }
-            __syncthreads();
         }
+        __syncthreads();
+        prefix |= sel[0] << shift;
+        pmask |= 255u << shift;
+        k -= sel[1];
+        __syncthreads();
     }
     // every split's N-th smallest is an upper bound of the true N-th: keep the least
-    if (threadIdx.x == 0) atomicMin(&a.tau0[(size_t)q * a.n_sub + i], v[a.N - 1]);
+    if (threadIdx.x == 0) atomicMin(&a.tau0[(size_t)q * a.n_sub + i], prefix);
 }
 
 cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s) {
-    tau_seed_kernel<<<a.nq * a.n_sub * a.splits, kSeedThreads, 0, s>>>(a);
+    const unsigned grid = a.nq * a.n_sub * a.splits;
+    switch (a.kc) {
+        case 8: tau_seed_kernel<8><<<grid, kSeedThreads, 0, s>>>(a); break;
+        case 16: tau_seed_kernel<16><<<grid, kSeedThreads, 0, s>>>(a); break;
+        case 32: tau_seed_kernel<32><<<grid, kSeedThreads, 0, s>>>(a); break;
+        case 64: tau_seed_kernel<64><<<grid, kSeedThreads, 0, s>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
@@ -623,6 +665,27 @@ cudaError_t launch_relayout(const float *src, uint64_t rows, uint64_t dst_row0, 
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks == 0) blocks = 1;
     relayout_kernel<<<(unsigned)blocks, 256, 0, s>>>(src, rows, dst_row0, kc, coarse, fine);
+    return cudaGetLastError();
+}
+
+// Tile-padding rows (count .. next multiple of 32) of each subspace <- its last row.
+__global__ void pad_rows_kernel(const SubInfo *subs, uint32_t n_sub, int kc, float *coarse, float *fine) {
+    const uint32_t i = blockIdx.x;
+    const SubInfo si = subs[i];
+    const uint64_t pad = (si.count + 31) / 32 * 32;
+    if (si.count == 0) return;
+    const uint64_t src = si.row_begin + si.count - 1;
+    for (uint64_t p = si.count + threadIdx.x / kK; p < pad; p += blockDim.x / kK) {
+        const uint64_t dst = si.row_begin + p;
+        const int k = threadIdx.x % kK;
+        if (k < kc) coarse[coarse_off(dst, k, kc)] = coarse[coarse_off(src, k, kc)];
+        else fine[dst * (kK - kc) + (k - kc)] = fine[src * (kK - kc) + (k - kc)];
+    }
+}
+
+cudaError_t launch_pad_rows(const SubInfo *subs, uint32_t n_sub, int kc, float *coarse, float *fine, cudaStream_t s) {
+    if (n_sub == 0) return cudaSuccess;
+    pad_rows_kernel<<<n_sub, 256, 0, s>>>(subs, n_sub, kc, coarse, fine);
     return cudaGetLastError();
 }
 

