@@ -51,6 +51,7 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--small-batch", type=int, default=8, help="extra HBM-regime line (0 = off)")
+    ap.add_argument("--ingest", type=int, default=1 << 20, help="profiles for the NEXT-3 extraction line (0 = off)")
     ap.add_argument("--seconds", type=float, default=5.0, help="C5 streaming duration")
     return ap.parse_args()
 
@@ -292,6 +293,27 @@ def run_omniloc(a):
         out["small_batch"] = {"query_frames": b2, "ms_per_step": sms, "queries_per_s": b2 / (sms / 1e3),
                               "scan_ms": sscan * 1e3, "scan_hbm_gbs": gbs, "hbm_peak_gbs": hbm_peak,
                               "hbm_frac": gbs / hbm_peak}
+
+    # ------------------------------------------------ descriptor extraction (NEXT-3) line
+    if a.ingest and world == 1:
+        n_in, Wp = a.ingest, 256
+        g = torch.Generator(device=dev).manual_seed(1234)
+        prof = torch.rand((n_in, Wp), dtype=torch.float64, device=dev, generator=g)
+        for _ in range(2):
+            eng.extract_features(prof)
+        torch.cuda.synchronize()
+        reps = 5
+        e0.record(stream)
+        for _ in range(reps):
+            eng.extract_features(prof)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ims = e0.elapsed_time(e1) / reps
+        out["ingest"] = {"kernel": "extract_kernel", "profiles": n_in, "W": Wp, "ms": ims,
+                         "profiles_per_s": n_in / (ims / 1e3),
+                         "fp64_flops_per_profile": 64 * Wp * 4,
+                         "hbm_bytes_per_profile": Wp * 8 + 64 * 4 + 1}
+        del prof
 
     # ------------------------------------------------ e2e through the public API, host buffers
     if not a.no_e2e:

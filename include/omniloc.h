@@ -266,6 +266,25 @@ OL_API ol_status ol_shift_keys_copy(ol_ctx *ctx, void *dst);
  * for INT64_MAX keys).  Synchronises.  Errors: NOT_READY, INVALID_ARGUMENT, CUDA. */
 OL_API ol_status ol_get_shifts(ol_ctx *ctx, uint32_t *shift, float *dist2, uint64_t capacity);
 
+/* ---- descriptor extraction (NEXT-3, the step before the path) -------------- */
+
+/* The paper's rotation-invariant feature of omnidirectional profiles ("The
+ * FFT magnitude of the one-dimensional omnidirectional vector"): for each
+ * profile x[0..W-1], X[k] = sum_w x[w] e^{-2 pi i k w / W} for k = 1..64 (DC
+ * dropped), m_k = |X[k]|, descriptor = m / ||m|| if ||m|| > 1e-12, else all-zero
+ * and flagged degenerate (reading R4).  Binary64 arithmetic on the GPU.
+ *   profiles:   [n][W] binary64, host (on_device = 0) or device memory
+ *   out32:      [n][64] fp32 descriptors, RN of the binary64 values (the database /
+ *               query format of ol_upload_db and ol_query); may be NULL
+ *   out64:      [n][64] binary64 descriptors; may be NULL
+ *   degenerate: [n] bytes, 1 = degenerate; may be NULL
+ * Outputs live where the input lives (host or device; caller-owned).  Host calls
+ * synchronise; device calls are stream-ordered.  65 <= W <= 2048.
+ * Errors: INVALID_ARGUMENT (W, NULL profiles), NONFINITE (host input with NaN/Inf),
+ * CUDA. */
+OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64_t n, uint32_t W,
+                                     int32_t on_device, float *out32, double *out64, uint8_t *degenerate);
+
 /* ---- tuning / introspection (never changes results) ---------------------- */
 
 /* Launch-shape knobs for schedule-independence tests and tuning:

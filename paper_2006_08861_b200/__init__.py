@@ -107,6 +107,7 @@ def lib():
             "ol_get_shifts": ([P, P, P, u64], i32),
             "ol_shift_keys_copy": ([P, P], i32),
             "ol_get_stat": ([P, ctypes.c_char_p, ctypes.POINTER(i64)], i32),
+            "ol_extract_features": ([P, P, u64, u32, i32, P, P, P], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -365,6 +366,34 @@ class Engine:
         self._ck(lib().ol_get_shifts(self._h, ctypes.c_void_p(shift.ctypes.data),
                                      ctypes.c_void_p(dist2.ctypes.data), n))
         return shift, dist2
+
+    def extract_features(self, profiles, want64: bool = False):
+        """Descriptors of omnidirectional profiles (NEXT-3): [n][W] binary64,
+        host numpy or device torch -> (fp32 [n][64], degenerate bool [n][, binary64 [n][64]]),
+        same residency as the input.  Every step runs in extract_kernel."""
+        n, W = int(profiles.shape[0]), int(profiles.shape[1])
+        pp, pdev = _ptr(profiles)
+        if pdev:
+            torch = self._torch
+            self.sync_stream()
+            o32 = torch.empty((n, 64), dtype=torch.float32, device=profiles.device)
+            o64 = torch.empty((n, 64), dtype=torch.float64, device=profiles.device) if want64 else None
+            deg = torch.empty(n, dtype=torch.uint8, device=profiles.device)
+            p64 = o64.data_ptr() if want64 else None
+            self._ck(lib().ol_extract_features(self._h, ctypes.c_void_p(pp), n, W, 1,
+                                               ctypes.c_void_p(o32.data_ptr()), ctypes.c_void_p(p64),
+                                               ctypes.c_void_p(deg.data_ptr())))
+            deg = deg.bool()
+        else:
+            o32 = np.empty((n, 64), np.float32)
+            o64 = np.empty((n, 64), np.float64) if want64 else None
+            deg = np.empty(n, np.uint8)
+            self._ck(lib().ol_extract_features(self._h, ctypes.c_void_p(pp), n, W, 0,
+                                               ctypes.c_void_p(o32.ctypes.data),
+                                               ctypes.c_void_p(o64.ctypes.data if want64 else None),
+                                               ctypes.c_void_p(deg.ctypes.data)))
+            deg = deg.astype(bool)
+        return (o32, deg, o64) if want64 else (o32, deg)
 
     def set_option(self, key: str, value: int):
         self._ck(lib().ol_set_option(self._h, key.encode(), int(value)))

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libomniloc.so")
-SOURCES = ["runtime.cu", "scan.cu", "merge.cu", "aggregate.cu", "tcscan.cu", "shift.cu"]
+SOURCES = ["runtime.cu", "scan.cu", "merge.cu", "aggregate.cu", "tcscan.cu", "shift.cu", "extract.cu"]
 HEADERS = ["ol_internal.h", "tc_ptx.cuh", os.path.join("..", "..", "include", "omniloc.h")]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v",

@@ -132,6 +132,9 @@ cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, 
 cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float2 *qmeta,
                                    uint32_t *bounds, cudaStream_t s);
 cudaError_t launch_fill_u32(uint32_t *p, uint64_t n, uint32_t v, cudaStream_t s);
+size_t extract_smem_bytes(uint32_t W);
+cudaError_t launch_extract(const double *prof, uint64_t n, uint32_t W, float *out32, double *out64,
+                           uint8_t *degenerate, cudaStream_t s);
 cudaError_t launch_pad_rows(const SubInfo *subs, uint32_t n_sub, int kc, float *coarse, float *fine, cudaStream_t s);
 bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows, uint32_t width);
 cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q, const TcScanArgs &a, int grid,

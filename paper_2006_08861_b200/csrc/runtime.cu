@@ -760,6 +760,46 @@ ol_status ol_upload_profiles(ol_ctx *c, const float *profiles, uint32_t W, int32
     return OL_OK;
 }
 
+ol_status ol_extract_features(ol_ctx *c, const double *profiles, uint64_t n, uint32_t W, int32_t on_device,
+                              float *out32, double *out64, uint8_t *degenerate) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (W <= (uint32_t)OL_K || W > 2048) return fail(c, OL_ERR_INVALID_ARGUMENT, "W = %u outside 65..2048", W);
+    if (n == 0) return OL_OK;
+    if (!profiles) return fail(c, OL_ERR_INVALID_ARGUMENT, "profiles is NULL");
+    OL_CUDA(c, cudaSetDevice(c->device));
+    if (on_device) {
+        OL_LAUNCH(c, launch_extract(profiles, n, W, out32, out64, degenerate, c->stream));
+        return OL_OK;
+    }
+    for (uint64_t t = 0; t < n * W; ++t)
+        if (!std::isfinite(profiles[t]))
+            return fail(c, OL_ERR_NONFINITE, "profile value %llu is not finite", (unsigned long long)t);
+    double *dp = nullptr, *d64 = nullptr;
+    float *d32 = nullptr;
+    uint8_t *dd = nullptr;
+    ol_status st = OL_OK;
+    auto cleanup = [&]() { cudaFree(dp); cudaFree(d64); cudaFree(d32); cudaFree(dd); };
+#define OL_EX(x)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (x);                                                             \
+        if (e_ != cudaSuccess) { cleanup(); return fail(c, OL_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); } \
+    } while (0)
+    OL_EX(cudaMalloc((void **)&dp, sizeof(double) * n * W));
+    if (out64) OL_EX(cudaMalloc((void **)&d64, sizeof(double) * n * OL_K));
+    if (out32) OL_EX(cudaMalloc((void **)&d32, sizeof(float) * n * OL_K));
+    if (degenerate) OL_EX(cudaMalloc((void **)&dd, n));
+    OL_EX(cudaMemcpyAsync(dp, profiles, sizeof(double) * n * W, cudaMemcpyHostToDevice, c->stream));
+    OL_EX(launch_extract(dp, n, W, d32, d64, dd, c->stream));
+    ++c->launches;
+    if (out64) OL_EX(cudaMemcpyAsync(out64, d64, sizeof(double) * n * OL_K, cudaMemcpyDeviceToHost, c->stream));
+    if (out32) OL_EX(cudaMemcpyAsync(out32, d32, sizeof(float) * n * OL_K, cudaMemcpyDeviceToHost, c->stream));
+    if (degenerate) OL_EX(cudaMemcpyAsync(degenerate, dd, n, cudaMemcpyDeviceToHost, c->stream));
+    OL_EX(cudaStreamSynchronize(c->stream));
+#undef OL_EX
+    cleanup();
+    return st;
+}
+
 ol_status ol_shift_rescore(ol_ctx *c, const float *qprof, int32_t on_device) {
     if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!c->finalized) return fail(c, OL_ERR_NOT_READY, "no finalized query");
