@@ -1,0 +1,123 @@
+// pipe_probe.cu -- the tensor-core scan's TMEM pipeline in isolation: one thread issues
+// (optionally) 4 MMAs 128x256x16 per tile into a double-buffered accumulator and commits
+// tfull[buf]; epilogue warps wait tfull, tcgen05.ld their share, arrive tempty[buf].
+// Compares "all warps on every tile" with "two groups on alternate tiles".
+// nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a tools/pipe_probe.cu -o tools/pipe_probe -lcuda
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include "../paper_2006_08861_b200/csrc/tc_ptx.cuh"
+using namespace ol::tc;
+
+struct Smem {
+    alignas(1024) __half a[128 * 64];
+    alignas(1024) __half b[256 * 64];
+    uint64_t tfull[4], tempty[4];
+    uint32_t tmem;
+};
+
+// design 0: E warps all load every tile, each 256*4/E columns... (E = 16: 64 columns)
+// design 1: two groups of E/2 warps on alternate tiles, each warp 128 columns in two 64-col chunks
+__global__ void probe(int design, int E, int mma, int tiles, int NB, long long *out) {
+    const int TC = 512 / NB;   // columns per tile
+    extern __shared__ __align__(1024) unsigned char raw[];
+    Smem &s = *reinterpret_cast<Smem *>(raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 128 * 64; i += blockDim.x) s.a[i] = __float2half(0.001f * (i % 7));
+    for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) s.b[i] = __float2half(0.001f * (i % 5));
+    const int arrivals = design == 0 ? E : E / 2;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NB; ++i) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], arrivals); }
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<512>(&s.tmem);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s.tmem;
+    long long t0 = clock64();
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint32_t idesc = idesc_f16_f32(128, TC);
+            for (int t = 0; t < tiles; ++t) {
+                const int buf = t % NB;
+                if (t >= NB) mbar_wait(&s.tempty[buf], ((t / NB) - 1) & 1);
+                tc_fence_after();
+                if (mma)
+                    for (int k = 0; k < 4; ++k)
+                        mma_f16(tmem + buf * TC, desc_sw128_kmajor(smem_u32(s.a) + k * 32),
+                                desc_sw128_kmajor(smem_u32(s.b) + k * 32), idesc, k ? 1u : 0u);
+                mma_commit(&s.tfull[buf]);
+            }
+            out[1] = clock64() - t0;
+        }
+    } else if (warp <= E) {
+        const int ew = warp - 1, q = warp & 3;
+        uint32_t acc = 0;
+        if (design == 0) {
+            const int part = ew >> 2, cols = TC / (E / 4);
+            for (int t = 0; t < tiles; ++t) {
+                const int buf = t % NB;
+                mbar_wait(&s.tfull[buf], (t / NB) & 1);
+                tc_fence_after();
+                for (int c = 0; c < cols; c += 64) {
+                    uint32_t v0[32], v1[32];
+                    const uint32_t ta = tmem + ((q * 32) << 16) + buf * TC + part * cols + c;
+                    tmem_ld32(ta, v0);
+                    if (cols - c >= 64) { tmem_ld32(ta + 32, v1); tmem_ld_wait_regs(v0); reg_fence(v1); }
+                    else { tmem_ld_wait_regs(v0); for (int j = 0; j < 32; ++j) v1[j] = 0; }
+                    for (int j = 0; j < 32; ++j) acc += v0[j] ^ v1[j];
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.tempty[buf]);
+            }
+        } else {
+            const int grp = ew / (E / 2), half = (ew % (E / 2)) >> 2;   // E/2 = 8: half in {0, 1}
+            for (int t = grp; t < tiles; t += 2) {
+                const int buf = t & 1;
+                mbar_wait(&s.tfull[buf], (t >> 1) & 1);
+                tc_fence_after();
+                for (int c = 0; c < 128; c += 64) {
+                    uint32_t v0[32], v1[32];
+                    const uint32_t ta = tmem + ((q * 32) << 16) + buf * 256 + half * 128 + c;
+                    tmem_ld32(ta, v0); tmem_ld32(ta + 32, v1);
+                    tmem_ld_wait_regs(v0); reg_fence(v1);
+                    if (c == 64) { tc_fence_before(); __syncwarp(); if (lane == 0) mbar_arrive(&s.tempty[buf]); }
+                    for (int j = 0; j < 32; ++j) acc += v0[j] ^ v1[j];
+                }
+            }
+        }
+        if (acc == 0x1234567u) out[3] = acc;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) out[0] = clock64() - t0;
+    if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+int main() {
+    long long *d;
+    cudaMalloc(&d, 64);
+    size_t smem = sizeof(Smem) + 1024;
+    cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int tiles = 400;
+    for (int mma = 0; mma <= 1; ++mma)
+        for (int NB : {2, 4})
+        for (int design = 0; design <= 1; ++design)
+            for (int E : {8, 16}) {
+                if (design == 1 && (E != 16 || NB != 2)) continue;
+                if (NB == 4 && E == 16 && design == 0) {}   // 32 cols per warp at NB=4, E=16
+                long long h[4] = {0, 0, 0, 0};
+                probe<<<1, 32 * (1 + E), smem>>>(design, E, mma, tiles, NB, d);
+                cudaError_t e = cudaDeviceSynchronize();
+                if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+                cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
+                printf("mma=%d NB=%d %-26s E=%2d: %.0f cycles per 128 KB of accumulators\n", mma, NB,
+                       design == 0 ? "all warps every tile" : "two groups, alternate tiles", E,
+                       (double)h[0] / tiles * 2 / NB);
+            }
+    return 0;
+}
