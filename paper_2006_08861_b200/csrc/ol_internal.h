@@ -98,13 +98,15 @@ struct AggArgs {
 struct TcScanArgs {
     const WorkItem *items;
     const float2 *blk;            // [rows_pad / 32] per 32-row block: (min RD||f||^2/2, max RU e_f)
-    const float2 *qmeta;          // [nq] (RD ||q||^2, RU ||q - fp16(q)||)
-    const uint32_t *bounds;       // [2] batch norm bound bits, [3] force_all (a frame left the fp16 range)
+    const float4 *qmeta;          // [nq] (RD ||q||^2, RU ||q - fp16(q)||, RU ||q||^2, 0)
+    const uint32_t *bounds;       // [2] batch norm bound bits, [3] force_all (a frame left the fp16 range),
+                                  // [4] max RU||f||^2/2 bits, [5] max RU e_f bits (bound pre-pass)
     float nf_max;                 // database norm bound
     uint32_t *g_tau;              // [nq][n_sub] acc bits: seeded, then shared running minimum
     const float *queries;         // fp32 [nq][K]
     const float *coarse, *fine;   // fp32 planes (exact re-scoring)
-    u64 *partial;                 // [nq][n_items][N]
+    u64 *partial;                 // [nq][n_items][N] (unused by the bound pre-pass)
+    uint32_t bound;               // 1: bound pre-pass over a strided row view (items index that view)
     unsigned long long *stat_survivors;
     unsigned long long *stat_flagged;   // (frame, row tile) pairs that took the cold path
     uint32_t nq, n_items, n_qblocks, qb, n_sub, N, kc, stages;
@@ -129,14 +131,15 @@ struct ShiftArgs {
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s);
 cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, uint64_t rows, void *plane,
                                 float2 *blk, uint32_t *stat, cudaStream_t s);
-cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float2 *qmeta,
+cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float4 *qmeta,
                                    uint32_t *bounds, cudaStream_t s);
 cudaError_t launch_fill_u32(uint32_t *p, uint64_t n, uint32_t v, cudaStream_t s);
 size_t extract_smem_bytes(uint32_t W);
 cudaError_t launch_extract(const double *prof, uint64_t n, uint32_t W, float *out32, double *out64,
                            uint8_t *degenerate, cudaStream_t s);
 cudaError_t launch_pad_rows(const SubInfo *subs, uint32_t n_sub, int kc, float *coarse, float *fine, cudaStream_t s);
-bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows, uint32_t width);
+bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows, uint32_t width,
+                 uint32_t row_stride = 1);
 cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q, const TcScanArgs &a, int grid,
                           cudaStream_t s);
 size_t tc_smem_bytes(uint32_t qb, uint32_t N, uint32_t stages);

@@ -46,7 +46,7 @@ struct ol_ctx {
     float nf_max = 0.f;
     CUtensorMap map_rows;
     void *q16 = nullptr; size_t q16_cap = 0;
-    float2 *qmeta = nullptr; size_t qmeta_cap = 0;
+    float4 *qmeta = nullptr; size_t qmeta_cap = 0;
     bool used_tc = false;
     // NEXT-1 profiles and shift keys
     float *prof = nullptr; uint32_t prof_W = 0;
@@ -58,6 +58,13 @@ struct ol_ctx {
     WorkItem *items_d = nullptr;
     size_t items_cap = 0;
     uint64_t items_chunk = 0;
+    // tensor-core bound pre-pass (tau seed) over the strided view rows 0, S, 2S, ...
+    uint32_t seed_stride = 0;     // 0: not available (fp16 path off or tiny database)
+    CUtensorMap map_srows;
+    std::vector<WorkItem> sitems;
+    WorkItem *sitems_d = nullptr;
+    size_t sitems_cap = 0;
+    uint64_t sitems_chunk = 0;
     // per-query buffers
     float *q_d = nullptr; size_t q_cap = 0;
     uint32_t *tau0_d = nullptr; size_t tau_cap = 0;
@@ -85,6 +92,7 @@ struct ol_ctx {
     int64_t opt_tc = -1;         // tensor-core filter: -1 auto (>= 32 frames), 0 off, 1 always
     int64_t opt_tc_min_frames = 32;
     int64_t opt_tc_debug = 0;
+    int64_t opt_tc_seed = 1;     // tensor-core path: seed thresholds with the bound pre-pass
     int64_t opt_scan2 = 1;       // small batches (<= 16 frames per tile) use scan2_kernel    // profiling experiments only (results invalid when nonzero)
     // per-kernel-class CUDA-event timing (option "time_kernels"): pairs recorded on
     // the context stream around each launch; summed and released by ol_get_stat
@@ -174,6 +182,8 @@ static void free_db(ol_ctx *c) {
     c->db_ready = false;
     c->items.clear();
     c->items_chunk = 0;
+    c->sitems_chunk = 0;
+    c->seed_stride = 0;
 }
 
 extern "C" {
@@ -220,7 +230,7 @@ void ol_destroy(ol_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     free_db(c);
-    cudaFree(c->items_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
+    cudaFree(c->items_d); cudaFree(c->sitems_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
     cudaFree(c->prefix_d); cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
     cudaFree(c->flags_d); cudaFree(c->stat_d); cudaFree(c->tcstat_d); cudaFree(c->prof_d);
@@ -376,6 +386,11 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
         // must fit a TMA coordinate
         c->tc_ok = std::isfinite(nf) && amax < 65000.f && nf < 300.f && rows_pad < (1ull << 31) &&
                    make_tc_map(&c->map_rows, c->plane16, rows_pad, 256, OL_K);
+        // bound pre-pass view: ~128k sampled rows, at most 1/64 of the database
+        uint64_t S = 64;
+        while (rows_pad / (S * 2) >= 131072) S *= 2;
+        c->seed_stride = c->tc_ok && rows_pad / S >= 2048 &&
+                         make_tc_map(&c->map_srows, c->plane16, rows_pad, 256, OL_K, (uint32_t)S) ? (uint32_t)S : 0;
     }
     c->subs = subs;
     c->rows_pad = rows_pad;
@@ -416,6 +431,38 @@ static ol_status build_items(ol_ctx *c, uint64_t chunk) {
     OL_CUDA(c, cudaStreamSynchronize(c->stream));  // host vectors are pageable and reused
     c->items.swap(items);
     c->items_chunk = chunk;
+    return OL_OK;
+}
+
+// Work items of the pre-pass view (rows 0, S, 2S, ... of the device planes): per
+// subspace, its rows that are multiples of S, in chunks of `chunk` view rows.
+static ol_status build_sitems(ol_ctx *c, uint64_t chunk) {
+    if (chunk == c->sitems_chunk && !c->sitems.empty()) return OL_OK;
+    const uint64_t S = c->seed_stride;
+    std::vector<WorkItem> items;
+    for (uint32_t i = 0; i < c->n_sub; ++i) {
+        const SubInfo &s = c->subs[i];
+        if (!s.count) continue;
+        const uint64_t j0 = (s.row_begin + S - 1) / S, j1 = (s.row_begin + s.count - 1) / S;
+        if (j1 < j0) continue;
+        const uint64_t n = j1 - j0 + 1;
+        for (uint64_t o = 0; o < n; o += chunk) {
+            WorkItem w;
+            w.sub = i;
+            w.count = (uint32_t)((n - o) < chunk ? (n - o) : chunk);
+            w.row_begin = j0 + o;
+            w.frame_begin = 0;   // (the pre-pass reports no frames)
+            w._pad = 0;
+            items.push_back(w);
+        }
+    }
+    OL_CUDA(c, grow(&c->sitems_d, &c->sitems_cap, items.size() ? items.size() : 1));
+    if (!items.empty())
+        OL_CUDA(c, cudaMemcpyAsync(c->sitems_d, items.data(), sizeof(WorkItem) * items.size(),
+                                   cudaMemcpyHostToDevice, c->stream));
+    OL_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->sitems.swap(items);
+    c->sitems_chunk = chunk;
     return OL_OK;
 }
 
@@ -495,7 +542,12 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     if (on_device) OL_LAUNCH(c, launch_check_finite(q, nq64 * OL_K, c->flags_d, c->stream));
 
     const bool seed = c->opt_tau_seed != 0;
-    if (seed && !(c->opt_tc_debug & 64)) {   // (tc_debug & 64: profiling, keep the last thresholds)
+    // tensor-core path: seed with the bound pre-pass when every subspace has >= 32 N
+    // sampled rows (N <= 16: register lists); otherwise the exact sampled seed
+    bool tc_seed = use_tc && seed && c->opt_tc_seed && c->seed_stride && N <= 16;
+    for (auto &sb : c->subs)
+        if (tc_seed && sb.count / c->seed_stride < 32ull * N) tc_seed = false;
+    if (seed && (!tc_seed || c->opt_tc_seed == 2) && !(c->opt_tc_debug & 64)) {   // (tc_debug & 64: keep the last thresholds)
         SeedArgs sa;
         sa.coarse = c->coarse; sa.fine = c->fine; sa.queries = q; sa.subs = c->subs_d;
         sa.tau0 = c->tau0_d; sa.nq = nq; sa.n_sub = c->n_sub; sa.N = N; sa.kc = (uint32_t)c->kc;
@@ -520,17 +572,33 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         OL_CUDA(c, grow(&c->qmeta, &c->qmeta_cap, nq));
         OL_CUDA(c, cudaMemsetAsync(c->tcstat_d + 2, 0, 2 * sizeof(uint32_t), c->stream));
         OL_LAUNCH(c, launch_tc_prep_queries(q, nq, nq_pad, c->q16, c->qmeta, c->tcstat_d, c->stream));
-        if (!seed && !(c->opt_tc_debug & 64)) OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
+        if ((!seed || (tc_seed && c->opt_tc_seed != 2)) && !(c->opt_tc_debug & 64))
+            OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
         CUtensorMap map_q;
         if (!make_tc_map(&map_q, c->q16, nq_pad, qb, OL_K))
             return fail(c, OL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
         TcScanArgs a;
+        a.bound = 0;
         a.items = c->items_d; a.blk = c->blk; a.n_blk = (uint32_t)(c->rows_pad / 32); a.qmeta = c->qmeta; a.bounds = c->tcstat_d; a.nf_max = c->nf_max;
         a.g_tau = c->tau0_d; a.queries = q; a.coarse = c->coarse; a.fine = c->fine;
         a.partial = c->partial_d; a.stat_survivors = c->stat_d; a.stat_flagged = c->stat_d + 1;
         a.nq = nq; a.n_items = n_items; a.n_qblocks = n_qblocks; a.qb = qb; a.n_sub = c->n_sub;
         a.N = N; a.kc = (uint32_t)c->kc; a.stages = tc_stages; a.dbg = (uint32_t)c->opt_tc_debug; a.prof = c->prof_d;
         if (a.dbg & 32) OL_CUDA(c, cudaMemsetAsync(c->prof_d, 0, 64 * sizeof(unsigned long long), c->stream));
+        if (tc_seed && !(a.dbg & 64)) {
+            // bound pre-pass: tensor-core scores of every S-th row give each (frame,
+            // subspace) N distinct rows with certified upper bounds on their acc
+            uint64_t sch = ((c->rows_pad / c->seed_stride) * n_qblocks + 148 * 2 - 1) / (148 * 2);
+            sch = (sch + 255) / 256 * 256;
+            st = build_sitems(c, sch);
+            if (st) return st;
+            if (!c->sitems.empty()) {
+                TcScanArgs pa = a;
+                pa.bound = 1; pa.items = c->sitems_d; pa.n_items = (uint32_t)c->sitems.size(); pa.partial = nullptr;
+                TimeScope tp(c, ol_ctx::T_SEED);
+                OL_LAUNCH(c, launch_tcscan(c->map_srows, map_q, pa, (int)(pa.n_items * n_qblocks), c->stream));
+            }
+        }
         TimeScope ts(c, ol_ctx::T_SCAN);
         OL_LAUNCH(c, launch_tcscan(c->map_rows, map_q, a, (int)(n_items * n_qblocks), c->stream));
         c->used_tc = true;
@@ -870,6 +938,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "ctas")) { if (v < 0) goto bad; c->opt_ctas = v; }
     else if (!strcmp(key, "time_kernels")) { if (v != 0 && v != 1) goto bad; c->opt_time = v; }
     else if (!strcmp(key, "tc")) { if (v < -1 || v > 1) goto bad; c->opt_tc = v; }
+    else if (!strcmp(key, "tc_seed")) { if (v < 0 || v > 2) goto bad; c->opt_tc_seed = v; }
     else if (!strcmp(key, "scan2")) { if (v < 0 || v > 2) goto bad; c->opt_scan2 = v; }
     else if (!strcmp(key, "tc_min_frames")) { if (v < 1) goto bad; c->opt_tc_min_frames = v; }
     else if (!strcmp(key, "tc_debug")) { if (v < 0 || v > 255) goto bad; c->opt_tc_debug = v; }

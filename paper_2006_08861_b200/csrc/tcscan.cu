@@ -48,6 +48,7 @@ constexpr int kEpiWarps = 16;           // two groups of 8 (alternate tiles)
 constexpr int kExactWarps = 2;
 constexpr int kTcThreads = 32 * (2 + kEpiWarps + kExactWarps);
 constexpr int kEv = 128;                // survivor event ring entries per exact warp
+constexpr int kTrackMax = 16;           // largest N of the bound pre-pass (register list)
 constexpr float kTauInflate = 1.0f + 1.0f / 131072.0f;   // 1 + 2^-17
 constexpr uint32_t kStageBytes = kTileRows * kK * 2;   // 32 KB
 
@@ -166,7 +167,7 @@ __device__ __forceinline__ uint32_t mask32(const uint32_t (&v)[32], float h, int
     return m;
 }
 
-template <bool kProf>
+template <bool kProf, bool kBound>
 __global__ void __launch_bounds__(kTcThreads, 1)
 tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constant__ CUtensorMap map_q, TcScanArgs a) {
     extern __shared__ __align__(1024) unsigned char raw[];
@@ -205,7 +206,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     const float c0 = 1.220703125e-04f * nqm * nfm;                            // 2^-13 Nq Nf
     for (uint32_t q = threadIdx.x; q < kQB; q += blockDim.x) {
         if (q < qn) {
-            const float2 m = a.qmeta[q0 + q];  // (RD ||q||^2, RU e_q)
+            const float4 m = a.qmeta[q0 + q];  // (RD ||q||^2, RU e_q, RU ||q||^2)
             s.alpha[q] = force_all ? -INFINITY : m.x - 2.f * m.y * nfm - c0 - sigma;
             s.tau[q] = a.g_tau[(size_t)(q0 + q) * a.n_sub + it.sub];
         } else {
@@ -282,6 +283,32 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         };
         uint32_t gt = 0xFFFFFFFFu;                // shared running threshold, loaded 3 tiles ahead
         long long ew_tfull = 0, ew_ld = 0, ew_math = 0, ew_tile = 0;
+        // bound pre-pass (kBound): the thread keeps, in registers, the N largest
+        // y = RD(max_S P - G) over disjoint 16-row sets S of its sampled rows (the two running
+        // maxima of each 32-row block), G >= RU||f||^2/2 + Nq e_f for every row.  With
+        // gamma_q = RU(RU||q||^2 + 2 e_q Nf + 2^-13 Nq Nf):
+        //   acc <= A (1 + 2^-17) <= (gamma_q + 2 (G - P)) (1 + 2^-17)
+        // for the row attaining each maximum -- N distinct real rows -- so
+        // RU((gamma_q - 2 y_N)(1 + 2^-17)) bounds the N-th best acc of the subspace.
+        // The list is descending; the first kTrackMax - N slots hold +inf.
+        float tl[kBound ? kTrackMax : 1];
+        if constexpr (kBound) {
+#pragma unroll
+            for (int e = 0; e < kTrackMax; ++e) tl[e] = e < kTrackMax - (int)N ? INFINITY : -INFINITY;
+        }
+        const float Gg = kBound ? __fadd_ru(__uint_as_float(a.bounds[4]), __fmul_ru(nqm, __uint_as_float(a.bounds[5]))) : 0.f;
+        auto track = [&](float y) {
+            if constexpr (kBound) {
+                if (y > tl[kTrackMax - 1]) {
+#pragma unroll
+                    for (int e = 0; e < kTrackMax; ++e) {
+                        const float z = fmaxf(tl[e], y);
+                        y = fminf(tl[e], y);
+                        tl[e] = z;
+                    }
+                }
+            }
+        };
         // (register values loaded from global memory are only read tiles later and never
         // copied in between: a copy would stall on the load)
         auto tile = [&](uint32_t t, uint32_t i, const float2 gb) {
@@ -312,7 +339,13 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             tmem_ld32(taddr + 32, v1);
             tmem_ld_wait_regs(v0);   // orders every use of v0, v1 after the wait
             reg_fence(v1);
-            if (!(a.dbg & 1)) {
+            if (kBound) {
+                float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+                max32(v0, m0, m1);
+                max32(v1, m2, m3);
+                if (nvalid >= 32) { track(__fsub_rd(m0, Gg)); track(__fsub_rd(m1, Gg)); }
+                if (nvalid >= 64) { track(__fsub_rd(m2, Gg)); track(__fsub_rd(m3, Gg)); }
+            } else if (!(a.dbg & 1)) {
                 float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
                 max32(v0, m0, m1);
                 max32(v1, m2, m3);
@@ -332,7 +365,13 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             if (lane == 0) mbar_arrive(&s.tempty[buf]);
             const long long w2 = prof ? clock64() : 0;
             if (prof && lane == 0) ew_ld += w2 - w1;
-            if (!(a.dbg & 1)) {
+            if (kBound) {
+                float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+                max32(v0, m0, m1);
+                max32(v1, m2, m3);
+                if (nvalid >= 96) { track(__fsub_rd(m0, Gg)); track(__fsub_rd(m1, Gg)); }
+                if (nvalid >= 128) { track(__fsub_rd(m2, Gg)); track(__fsub_rd(m3, Gg)); }
+            } else if (!(a.dbg & 1)) {
                 float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
                 max32(v0, m0, m1);
                 max32(v1, m2, m3);
@@ -369,6 +408,14 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             tile(t + 2, i + 1, gC);
             if (t + 6 < n_tiles) gC = load_g(t + 6);
         }
+        if constexpr (kBound) {
+            if (ql < qn && !force_all && tl[kTrackMax - 1] > -INFINITY) {
+                const float4 m = a.qmeta[q0 + ql];
+                const float gam = __fadd_ru(__fadd_ru(m.z, __fmul_ru(2.f * m.y, nfm)), __fmul_ru(nqm, nfm) * 1.220703125e-04f);
+                const float tu = fmaxf(__fmul_ru(__fsub_ru(gam, 2.f * tl[kTrackMax - 1]), kTauInflate), 0.f);
+                atomicMin(&a.g_tau[(size_t)(q0 + ql) * a.n_sub + it.sub], __float_as_uint(tu));
+            }
+        }
         if (prof && lane == 0) {
             atomicAdd(&a.prof[6], (unsigned long long)ew_tfull);
             atomicAdd(&a.prof[12], (unsigned long long)ew_ld);
@@ -393,7 +440,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         // import the thresholds other CTAs published (any value ever held is a valid
         // bound, so races only loosen the test).
         const uint32_t xw = warp - (2 + kEpiWarps);
-        for (unsigned p = 0;;) {
+        for (unsigned p = 0; !kBound;) {
             bool got = false;
             uint32_t idle = 0, nap = 32;
             while (true) {
@@ -523,7 +570,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     __syncthreads();
     if (warp == 1) tmem_dealloc<512>(tmem);
     if (prof && threadIdx.x == 0) { atomicAdd(&a.prof[8], (unsigned long long)(clock64() - t_start)); atomicAdd(&a.prof[9], (unsigned long long)n_tiles); }
-    for (uint32_t i = threadIdx.x; i < qn * N; i += blockDim.x) {
+    for (uint32_t i = threadIdx.x; !kBound && i < qn * N; i += blockDim.x) {
         const uint32_t q = i / N, r = i % N;
         a.partial[((size_t)(q0 + q) * a.n_items + item_id) * N + r] = lists[(size_t)q * N + r];
     }
@@ -561,6 +608,10 @@ __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int 
         // the double sums carry relative error < 2^-45; the (1 -+ 2^-20) factors cover it
         float x = 0.5f * __double2float_rd(n2 * (1.0 - 1.0 / 1048576.0));   // halving is exact
         float ef = __double2float_ru(sqrt(e2) * (1.0 + 1.0 / 1048576.0));
+        // database maxima of RU||f||^2 / 2 and of e_f (the bound pre-pass's G); bits of
+        // non-negative floats order like the floats
+        atomicMax(&stat[4], __float_as_uint(0.5f * __double2float_ru(n2 * (1.0 + 1.0 / 1048576.0))));
+        atomicMax(&stat[5], __float_as_uint(ef));
         for (int o = 16; o; o >>= 1) {
             x = fminf(x, __shfl_xor_sync(0xffffffffu, x, o));
             ef = fmaxf(ef, __shfl_xor_sync(0xffffffffu, ef, o));
@@ -590,7 +641,7 @@ cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, 
 // RU e_q), and the batch norm bound in *nq_max (+inf if a value leaves the fp16
 // range: see force_all).  One warp per frame.
 __global__ void tc_prep_queries_kernel(const float *q, uint32_t nq, uint32_t nq_pad, __half *q16,
-                                       float2 *qmeta, uint32_t *nq_max, uint32_t *force_all) {
+                                       float4 *qmeta, uint32_t *nq_max, uint32_t *force_all) {
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= nq_pad) return;
     __half2 *dst = reinterpret_cast<__half2 *>(q16 + (size_t)w * kK);
@@ -602,7 +653,7 @@ __global__ void tc_prep_queries_kernel(const float *q, uint32_t nq, uint32_t nq_
     const bool bad = __any_sync(0xffffffffu, !(fabsf(f0) < 65000.f && fabsf(f1) < 65000.f));
     if (bad) {
         dst[lane] = zero;
-        if (lane == 0) { qmeta[w] = make_float2(0.f, 0.f); atomicOr(force_all, 1u); }
+        if (lane == 0) { qmeta[w] = make_float4(0.f, 0.f, 0.f, 0.f); atomicOr(force_all, 1u); }
         return;
     }
     const __half h0 = __float2half_rn(f0), h1 = __float2half_rn(f1);
@@ -616,14 +667,15 @@ __global__ void tc_prep_queries_kernel(const float *q, uint32_t nq, uint32_t nq_
         h2 += __shfl_xor_sync(0xffffffffu, h2, o);
     }
     if (lane == 0) {
-        qmeta[w] = make_float2(__double2float_rd(n2 * (1.0 - 1.0 / 1048576.0)),
-                               __double2float_ru(sqrt(e2) * (1.0 + 1.0 / 1048576.0)));
+        qmeta[w] = make_float4(__double2float_rd(n2 * (1.0 - 1.0 / 1048576.0)),
+                               __double2float_ru(sqrt(e2) * (1.0 + 1.0 / 1048576.0)),
+                               __double2float_ru(n2 * (1.0 + 1.0 / 1048576.0)), 0.f);
         const float nb = __double2float_ru(sqrt(fmax(n2, h2)) * (1.0 + 1.0 / 1048576.0));
         atomicMax(nq_max, __float_as_uint(nb));
     }
 }
 
-cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float2 *qmeta,
+cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float4 *qmeta,
                                    uint32_t *bounds, cudaStream_t s) {
     const uint32_t threads = 256, blocks = (nq_pad * 32 + threads - 1) / threads;
     tc_prep_queries_kernel<<<blocks, threads, 0, s>>>(q, nq, nq_pad, (__half *)q16, qmeta, bounds + 2, bounds + 3);
@@ -656,13 +708,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 2-D map over an fp16 [rows][width] array (width 64 -> 128-byte swizzle, width 16 ->
+// 2-D map over an fp16 [rows][width] array (every row_stride-th row: a strided view) (width 64 -> 128-byte swizzle, width 16 ->
 // 32-byte swizzle: the UMMA K-major canonical layouts), box {width, box_rows}.
-bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows, uint32_t width) {
+bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows, uint32_t width,
+                 uint32_t row_stride) {
     auto fn = encode_fn();
     if (!fn) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)width * sizeof(__half)};
+    cuuint64_t dims[2] = {(cuuint64_t)width, (cuuint64_t)(rows / row_stride)};
+    cuuint64_t strides[1] = {(cuuint64_t)width * sizeof(__half) * row_stride};
     cuuint32_t box[2] = {width, box_rows};
     cuuint32_t estr[2] = {1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
@@ -674,7 +727,8 @@ cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q,
                           cudaStream_t s) {
     const size_t smem = tc_smem_bytes(a.qb, a.N, a.stages);
     const bool prof = (a.dbg & 32) != 0;
-    auto kern = prof ? tcscan_kernel<true> : tcscan_kernel<false>;
+    auto kern = a.bound ? (prof ? tcscan_kernel<true, true> : tcscan_kernel<false, true>)
+                        : (prof ? tcscan_kernel<true, false> : tcscan_kernel<false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<grid, kTcThreads, smem, s>>>(map_rows, map_q, a);

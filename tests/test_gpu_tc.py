@@ -104,3 +104,32 @@ def test_tc_schedule_invariance():
         e.query(Q, N=15)
         outs.add(e.topk().tobytes() + e.estimates().tobytes())
     assert len(outs) == 1
+
+
+@pytest.mark.parametrize("kind", ["paper", "signed"])
+def test_tc_bound_prepass_seed(kind):
+    """The tensor-core bound pre-pass (tau seed from certified upper bounds of every S-th
+    row's tensor-core score) only changes thresholds: results stay bit-identical to the
+    oracle, with the pre-pass on or off, over 2 subspaces large enough to use it."""
+    if kind == "paper":
+        spec = synthgen.Spec(seed=33, n_floors=8, paths=5, frames_per_path=4000)   # 160k rows
+        F, C = synthgen.db_host(spec)
+        Q = synthgen.render_host(spec, synthgen.query_points(spec, 19, 160))["desc"][:, None, :]
+    else:
+        rng = np.random.default_rng(33)
+        F = (rng.standard_normal((160_000, 64)) * 2).astype(np.float32)     # signed, non-unit
+        C = rng.integers(0, 500, (160_000, 2)).astype(np.int32)
+        Q = (F[rng.integers(0, 160_000, 160)] + rng.standard_normal((160, 64)).astype(np.float32) * 0.05)[:, None, :]
+    sizes = [100_000, 60_000]
+    N = 15
+    outs = []
+    for ts in (1, 0):
+        e = _run(F, C, sizes, Q, N, 1, agg=False, tc_seed=ts)
+        assert e.stat("used_tc") == 1
+        outs.append(e.topk())
+    assert np.array_equal(outs[0], outs[1])
+    sub = np.arange(0, 160, 8)
+    ref = oracle.retrieve(sizes, F, C, Q[sub], N)
+    got = outs[0].reshape(160, -1)[sub].reshape(-1)
+    assert np.array_equal(got["frame"], ref.frame) and np.array_equal(got["subspace"], ref.subspace)
+    assert np.array_equal(got["dist2"].view(np.uint32), ref.acc.view(np.uint32))
