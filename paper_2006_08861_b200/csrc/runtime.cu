@@ -93,6 +93,7 @@ struct ol_ctx {
     int64_t opt_tc_min_frames = 32;
     int64_t opt_tc_debug = 0;
     int64_t opt_tc_seed = 1;     // tensor-core path: seed thresholds with the bound pre-pass
+    int64_t opt_cluster = 1;     // tensor-core path: CTAs per cluster (query blocks sharing rows)
     int64_t opt_scan2 = 1;       // small batches (<= 16 frames per tile) use scan2_kernel    // profiling experiments only (results invalid when nonzero)
     // per-kernel-class CUDA-event timing (option "time_kernels"): pairs recorded on
     // the context stream around each launch; summed and released by ol_get_stat
@@ -579,6 +580,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
             return fail(c, OL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
         TcScanArgs a;
         a.bound = 0;
+        a.cluster = (uint32_t)c->opt_cluster;
         a.items = c->items_d; a.blk = c->blk; a.n_blk = (uint32_t)(c->rows_pad / 32); a.qmeta = c->qmeta; a.bounds = c->tcstat_d; a.nf_max = c->nf_max;
         a.g_tau = c->tau0_d; a.queries = q; a.coarse = c->coarse; a.fine = c->fine;
         a.partial = c->partial_d; a.stat_survivors = c->stat_d; a.stat_flagged = c->stat_d + 1;
@@ -938,6 +940,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "ctas")) { if (v < 0) goto bad; c->opt_ctas = v; }
     else if (!strcmp(key, "time_kernels")) { if (v != 0 && v != 1) goto bad; c->opt_time = v; }
     else if (!strcmp(key, "tc")) { if (v < -1 || v > 1) goto bad; c->opt_tc = v; }
+    else if (!strcmp(key, "cluster")) { if (v != 1 && v != 2 && v != 4 && v != 8) goto bad; c->opt_cluster = v; }
     else if (!strcmp(key, "tc_seed")) { if (v < 0 || v > 2) goto bad; c->opt_tc_seed = v; }
     else if (!strcmp(key, "scan2")) { if (v < 0 || v > 2) goto bad; c->opt_scan2 = v; }
     else if (!strcmp(key, "tc_min_frames")) { if (v < 1) goto bad; c->opt_tc_min_frames = v; }

@@ -731,8 +731,27 @@ cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q,
                         : (prof ? tcscan_kernel<true, false> : tcscan_kernel<false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<grid, kTcThreads, smem, s>>>(map_rows, map_q, a);
-    return cudaGetLastError();
+    // thread-block clusters over the query blocks of one work item (consecutive blockIdx):
+    // co-scheduled on one GPC, so the CTAs streaming the same rows share a die's L2
+    uint32_t cs = a.cluster ? a.cluster : 1;
+    while (cs > 1 && (a.n_qblocks % cs || grid % cs)) cs >>= 1;
+    if (cs <= 1) {
+        kern<<<grid, kTcThreads, smem, s>>>(map_rows, map_q, a);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kTcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, map_rows, map_q, a);
 }
 
 // Frames per CTA (128 or 256) and pipeline depth for top-N lists of N: the lists
