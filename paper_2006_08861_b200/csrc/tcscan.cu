@@ -504,22 +504,18 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                     const uint64_t row = it.row_begin + rl;
                     const float4 *qv = reinterpret_cast<const float4 *>(a.queries + (size_t)(q0 + col) * kK);
                     float acc = 0.f;
+                    float4 f[kK / 4];   // all 16 row loads in flight (one selected address each)
 #pragma unroll
-                    for (int h8 = 0; h8 < kK / 4; h8 += 8) {   // 8 row loads in flight (register budget)
-                        float4 f[8];
+                    for (int k4 = 0; k4 < kK / 4; ++k4) {
+                        const float *src = 4 * k4 < (int)a.kc ? a.coarse + coarse_off(row, 4 * k4, a.kc)
+                                                              : a.fine + row * (kK - a.kc) + (4 * k4 - a.kc);
+                        f[k4] = __ldg(reinterpret_cast<const float4 *>(src));
+                    }
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const int k4 = h8 + j;
-                            f[j] = 4 * k4 < (int)a.kc
-                                       ? __ldg(reinterpret_cast<const float4 *>(a.coarse + coarse_off(row, 4 * k4, a.kc)))
-                                       : __ldg(reinterpret_cast<const float4 *>(a.fine + row * (kK - a.kc) + (4 * k4 - a.kc)));
-                        }
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const float4 x = __ldg(qv + h8 + j);
-                            acc = chain_step_tc(acc, x.x, f[j].x); acc = chain_step_tc(acc, x.y, f[j].y);
-                            acc = chain_step_tc(acc, x.z, f[j].z); acc = chain_step_tc(acc, x.w, f[j].w);
-                        }
+                    for (int k4 = 0; k4 < kK / 4; ++k4) {
+                        const float4 x = __ldg(qv + k4);
+                        acc = chain_step_tc(acc, x.x, f[k4].x); acc = chain_step_tc(acc, x.y, f[k4].y);
+                        acc = chain_step_tc(acc, x.z, f[k4].z); acc = chain_step_tc(acc, x.w, f[k4].w);
                     }
                     key = ((u64)__float_as_uint(acc) << 32) | (u64)(it.frame_begin + rl);
                     if (!(key < lists[(size_t)col * N + N - 1])) key = kPadKey;   // cannot enter the list
