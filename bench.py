@@ -57,16 +57,53 @@ def _args():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line): an NVML thread every 10 ms (started, and NVML
+    initialised, before the timed region so the first sample lands inside it); falls back
+    to `nvidia-smi -lms 200` when NVML is unavailable."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
+        import threading
         self.idx = gpu_index
         self.p = None
+        self.nv = None
+        self.samples = []
+        self.go = threading.Event()
+        self.halt = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.th = threading.Thread(target=self._loop, daemon=True)
+            self.th.start()
+        except Exception:
+            self.nv = None
+
+    def _loop(self):
+        nv = self.nv
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        self.go.wait()
+        while not self.halt.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, {n for n, b in bits.items() if r & b}))
+            except Exception:
+                pass
+            self.halt.wait(0.01)
 
     def start(self):
+        if self.nv is not None:
+            self.go.set()
+            return
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "200"],
@@ -75,6 +112,14 @@ class Clocks:
             self.p = None
 
     def stop(self):
+        if self.nv is not None:
+            self.halt.set()
+            self.go.set()
+            self.th.join(timeout=2)
+            sm = [x for x, _ in self.samples]
+            reasons = set().union(*[r for _, r in self.samples]) if self.samples else set()
+            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.smax,
+                    "samples": len(sm), "reasons": sorted(reasons), "source": "nvml, 10 ms"}
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
@@ -94,7 +139,7 @@ class Clocks:
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None, "samples": len(sm),
-                "reasons": sorted(reasons)}
+                "reasons": sorted(reasons), "source": "nvidia-smi, 200 ms"}
 
 
 def _dist_init(n_gpus):

@@ -108,6 +108,7 @@ struct TcScanArgs {
     u64 *partial;                 // [nq][n_items][N] (unused by the bound pre-pass)
     uint32_t bound;               // 1: bound pre-pass over a strided row view (items index that view)
     uint32_t cluster;             // CTAs per thread-block cluster (query blocks of one item); 0/1 = none
+    uint32_t pair;                // 1: CTA pairs (cta_group::2, M = 256) over query-block pairs; n_qblocks even
     unsigned long long *stat_survivors;
     unsigned long long *stat_flagged;   // (frame, row tile) pairs that took the cold path
     uint32_t nq, n_items, n_qblocks, qb, n_sub, N, kc, stages;

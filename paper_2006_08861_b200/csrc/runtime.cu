@@ -44,7 +44,7 @@ struct ol_ctx {
                                    // [2] batch norm bound bits, [3] force_all
     bool tc_ok = false;
     float nf_max = 0.f;
-    CUtensorMap map_rows;
+    CUtensorMap map_rows, map_rows_half;   // 256-row boxes; 128-row boxes (CTA pairs)
     void *q16 = nullptr; size_t q16_cap = 0;
     float4 *qmeta = nullptr; size_t qmeta_cap = 0;
     bool used_tc = false;
@@ -94,6 +94,7 @@ struct ol_ctx {
     int64_t opt_tc_debug = 0;
     int64_t opt_tc_seed = 1;     // tensor-core path: seed thresholds with the bound pre-pass
     int64_t opt_cluster = 1;     // tensor-core path: CTAs per cluster (query blocks sharing rows)
+    int64_t opt_pair = 1;        // tensor-core path: CTA pairs (cta_group::2, M = 256)
     int64_t opt_scan2 = 1;       // small batches (<= 16 frames per tile) use scan2_kernel    // profiling experiments only (results invalid when nonzero)
     // per-kernel-class CUDA-event timing (option "time_kernels"): pairs recorded on
     // the context stream around each launch; summed and released by ol_get_stat
@@ -386,7 +387,8 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
         // fp16 operands need |f| and ||f||^2 / 2 inside the fp16 range, and the row count
         // must fit a TMA coordinate
         c->tc_ok = std::isfinite(nf) && amax < 65000.f && nf < 300.f && rows_pad < (1ull << 31) &&
-                   make_tc_map(&c->map_rows, c->plane16, rows_pad, 256, OL_K);
+                   make_tc_map(&c->map_rows, c->plane16, rows_pad, 256, OL_K) &&
+                   make_tc_map(&c->map_rows_half, c->plane16, rows_pad, 128, OL_K);
         // bound pre-pass view: ~128k sampled rows, at most 1/64 of the database
         uint64_t S = 64;
         while (rows_pad / (S * 2) >= 131072) S *= 2;
@@ -568,7 +570,9 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     }
     c->used_tc = false;
     if (n_items && use_tc) {
-        const uint32_t qb = tc_qb, n_qblocks = (nq + qb - 1) / qb, nq_pad = n_qblocks * qb;
+        const bool pair = c->opt_pair != 0;
+        const uint32_t qb = tc_qb, n_qblocks = ((nq + qb - 1) / qb + (pair ? 1 : 0)) / (pair ? 2 : 1) * (pair ? 2 : 1),
+                       nq_pad = n_qblocks * qb;
         OL_CUDA(c, grow((uint16_t **)&c->q16, &c->q16_cap, (size_t)nq_pad * OL_K));
         OL_CUDA(c, grow(&c->qmeta, &c->qmeta_cap, nq));
         OL_CUDA(c, cudaMemsetAsync(c->tcstat_d + 2, 0, 2 * sizeof(uint32_t), c->stream));
@@ -581,6 +585,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         TcScanArgs a;
         a.bound = 0;
         a.cluster = (uint32_t)c->opt_cluster;
+        a.pair = pair ? 1u : 0u;
         a.items = c->items_d; a.blk = c->blk; a.n_blk = (uint32_t)(c->rows_pad / 32); a.qmeta = c->qmeta; a.bounds = c->tcstat_d; a.nf_max = c->nf_max;
         a.g_tau = c->tau0_d; a.queries = q; a.coarse = c->coarse; a.fine = c->fine;
         a.partial = c->partial_d; a.stat_survivors = c->stat_d; a.stat_flagged = c->stat_d + 1;
@@ -602,7 +607,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
             }
         }
         TimeScope ts(c, ol_ctx::T_SCAN);
-        OL_LAUNCH(c, launch_tcscan(c->map_rows, map_q, a, (int)(n_items * n_qblocks), c->stream));
+        OL_LAUNCH(c, launch_tcscan(pair ? c->map_rows_half : c->map_rows, map_q, a, (int)(n_items * n_qblocks), c->stream));
         c->used_tc = true;
     } else if (n_items) {
         ScanArgs a;
@@ -940,6 +945,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "ctas")) { if (v < 0) goto bad; c->opt_ctas = v; }
     else if (!strcmp(key, "time_kernels")) { if (v != 0 && v != 1) goto bad; c->opt_time = v; }
     else if (!strcmp(key, "tc")) { if (v < -1 || v > 1) goto bad; c->opt_tc = v; }
+    else if (!strcmp(key, "pair")) { if (v != 0 && v != 1) goto bad; c->opt_pair = v; }
     else if (!strcmp(key, "cluster")) { if (v != 1 && v != 2 && v != 4 && v != 8) goto bad; c->opt_cluster = v; }
     else if (!strcmp(key, "tc_seed")) { if (v < 0 || v > 2) goto bad; c->opt_tc_seed = v; }
     else if (!strcmp(key, "scan2")) { if (v < 0 || v > 2) goto bad; c->opt_scan2 = v; }

@@ -169,7 +169,7 @@ __device__ __forceinline__ uint32_t mask32(const uint32_t (&v)[32], float h, int
     return m;
 }
 
-template <bool kProf, bool kBound>
+template <bool kProf, bool kBound, bool kPair>
 __global__ void __launch_bounds__(kTcThreads, 1)
 tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constant__ CUtensorMap map_q, TcScanArgs a) {
     extern __shared__ __align__(1024) unsigned char raw[];
@@ -184,7 +184,10 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     const uint32_t qblk = blockIdx.x % a.n_qblocks;
     const WorkItem it = a.items[item_id];
     const uint32_t q0 = qblk * a.qb;
-    const uint32_t qn = min(a.qb, a.nq - q0);
+    const uint32_t qn = q0 < a.nq ? min(a.qb, a.nq - q0) : 0u;   // 0: a pair's padding CTA
+    // CTA pairs (kPair): the two query blocks of a cluster share every row tile; rank 0
+    // issues M = 256 MMAs over both CTAs' frames, each CTA loads half of each row tile
+    const uint32_t rank = kPair ? cluster_ctarank() : 0u;
     const uint32_t N = a.N;
     const uint32_t n_tiles = (it.count + kTileRows - 1) / kTileRows;
     constexpr bool prof = kProf;   // profiling counters (tc_debug & 32): a separate instantiation
@@ -193,14 +196,14 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     // ---------------------------------------------------------------- setup
     if (threadIdx.x == 0) {
         for (uint32_t i = 0; i < n_stages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 1); }
-        for (int i = 0; i < kTBufs; ++i) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], kEpiWarps / 2); }
+        for (int i = 0; i < kTBufs; ++i) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], (kPair ? 2 : 1) * kEpiWarps / 2); }
         mbar_init(&s.qbar, 1);
         fence_mbar_init();
         for (int w = 0; w < kExactWarps; ++w) s.prod[w] = s.closed_at[w] = 0;
         s.closed = 0;
         tma_prefetch(&map_rows);
     }
-    if (warp == 1) tmem_alloc<512>(&s.tmem_base);
+    if (warp == 1) { if (kPair) tmem_alloc2<512>(&s.tmem_base); else tmem_alloc<512>(&s.tmem_base); }
     const float nqm = __uint_as_float(a.bounds[2]), nfm = a.nf_max;
     // a frame outside the fp16 range, or an unbounded batch: every pair is re-scored
     const bool force_all = a.bounds[3] != 0 || !(nqm < 300.f);
@@ -220,20 +223,32 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     for (uint32_t i = threadIdx.x; i < kExactWarps * kEv; i += blockDim.x) s.seq[i / kEv][i % kEv] = i % kEv;
     for (uint32_t i = threadIdx.x; i < a.qb * N; i += blockDim.x) lists[i] = kPadKey;
     tc_fence_before();
-    __syncthreads();
+    if (kPair) cluster_sync(); else __syncthreads();   // (pair: the leader's barriers exist before any remote use)
     tc_fence_after();
     const uint32_t tmem = s.tmem_base;
 
     if (warp == 0) {
         // ------------------------------------------------------------ TMA producer
         if (lane == 0) {
-            mbar_expect_tx(&s.qbar, a.qb * kK * (uint32_t)sizeof(__half));
-            tma_load_2d(s.qm, &map_q, &s.qbar, 0, (int)q0);
+            if (kPair) {
+                // each CTA loads its own frames and its half of each row tile; the bytes of
+                // both complete on the leader's barriers
+                if (rank == 0) mbar_expect_tx(&s.qbar, 2 * a.qb * kK * (uint32_t)sizeof(__half));
+                tma_load_2d_pair(s.qm, &map_q, &s.qbar, 0, (int)q0);
+            } else {
+                mbar_expect_tx(&s.qbar, a.qb * kK * (uint32_t)sizeof(__half));
+                tma_load_2d(s.qm, &map_q, &s.qbar, 0, (int)q0);
+            }
             for (uint32_t t = 0; t < n_tiles; ++t) {
                 const uint32_t st = t % n_stages;
                 if (t >= n_stages) mbar_wait_sleep(&s.empty[st], ((t / n_stages) - 1) & 1);
                 unsigned char *sb = stage0 + (size_t)st * kStageBytes;
                 const int r0 = (int)(it.row_begin + (uint64_t)t * kTileRows);
+                if (kPair) {
+                    if (rank == 0) mbar_expect_tx(&s.full[st], kStageBytes);   // both halves
+                    tma_load_2d_pair(sb, &map_rows, &s.full[st], 0, r0 + (int)rank * (kTileRows / 2));
+                    continue;
+                }
                 if ((a.dbg & 128) && t >= n_stages) { mbar_arrive(&s.full[st]); continue; }   // profiling: stale rows
                 mbar_expect_tx(&s.full[st], kStageBytes);
                 tma_load_2d(sb, &map_rows, &s.full[st], 0, r0);
@@ -241,8 +256,9 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            const uint32_t idesc = idesc_f16_f32(128, kTileRows);   // M = 128 frames, N = 256 rows
+        if (lane == 0 && rank == 0) {
+            // M = 128 frames (pair: 256, both CTAs' frames), N = 256 rows
+            const uint32_t idesc = idesc_f16_f32(kPair ? 256 : 128, kTileRows);
             long long pw_full = 0, pw_tempty = 0;
             mbar_wait(&s.qbar, 0);
             const uint32_t qm = smem_u32(s.qm);
@@ -258,11 +274,13 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 const uint32_t d = tmem + buf * kTileRows;
                 if (!(a.dbg & 2)) {
 #pragma unroll
-                    for (int k = 0; k < kK / 16; ++k)
-                        mma_f16(d, desc_sw128_kmajor(qm + k * 32), desc_sw128_kmajor(rm + k * 32), idesc, k > 0 ? 1u : 0u);
+                    for (int k = 0; k < kK / 16; ++k) {
+                        if (kPair) mma_f16_pair(d, desc_sw128_kmajor(qm + k * 32), desc_sw128_kmajor(rm + k * 32), idesc, k > 0 ? 1u : 0u);
+                        else mma_f16(d, desc_sw128_kmajor(qm + k * 32), desc_sw128_kmajor(rm + k * 32), idesc, k > 0 ? 1u : 0u);
+                    }
                 }
-                mma_commit(&s.empty[st]);
-                mma_commit(&s.tfull[buf]);
+                if (kPair) { mma_commit_pair(&s.empty[st], 3); mma_commit_pair(&s.tfull[buf], 3); }
+                else { mma_commit(&s.empty[st]); mma_commit(&s.tfull[buf]); }
             }
             if (prof) { atomicAdd(&a.prof[0], (unsigned long long)pw_full); atomicAdd(&a.prof[1], (unsigned long long)pw_tempty); }
         }
@@ -364,7 +382,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             reg_fence(v1);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&s.tempty[buf]);
+            if (lane == 0) { if (kPair) mbar_arrive_leader(&s.tempty[buf]); else mbar_arrive(&s.tempty[buf]); }
             const long long w2 = prof ? clock64() : 0;
             if (prof && lane == 0) ew_ld += w2 - w1;
             if (kBound) {
@@ -565,8 +583,8 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
 
     // ---------------------------------------------------------------- teardown
     tc_fence_before();
-    __syncthreads();
-    if (warp == 1) tmem_dealloc<512>(tmem);
+    if (kPair) cluster_sync(); else __syncthreads();
+    if (warp == 1) { if (kPair) tmem_dealloc2<512>(tmem); else tmem_dealloc<512>(tmem); }
     if (prof && threadIdx.x == 0) { atomicAdd(&a.prof[8], (unsigned long long)(clock64() - t_start)); atomicAdd(&a.prof[9], (unsigned long long)n_tiles); }
     for (uint32_t i = threadIdx.x; !kBound && i < qn * N; i += blockDim.x) {
         const uint32_t q = i / N, r = i % N;
@@ -725,14 +743,17 @@ cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q,
                           cudaStream_t s) {
     const size_t smem = tc_smem_bytes(a.qb, a.N, a.stages);
     const bool prof = (a.dbg & 32) != 0;
-    auto kern = a.bound ? (prof ? tcscan_kernel<true, true> : tcscan_kernel<false, true>)
-                        : (prof ? tcscan_kernel<true, false> : tcscan_kernel<false, false>);
+    const bool pair = a.pair && !a.bound;
+    auto kern = a.bound ? (prof ? tcscan_kernel<true, true, false> : tcscan_kernel<false, true, false>)
+              : pair    ? (prof ? tcscan_kernel<true, false, true> : tcscan_kernel<false, false, true>)
+                        : (prof ? tcscan_kernel<true, false, false> : tcscan_kernel<false, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // thread-block clusters over the query blocks of one work item (consecutive blockIdx):
     // co-scheduled on one GPC, so the CTAs streaming the same rows share a die's L2
-    uint32_t cs = a.cluster ? a.cluster : 1;
-    while (cs > 1 && (a.n_qblocks % cs || grid % cs)) cs >>= 1;
+    uint32_t cs = pair ? 2u : a.cluster ? a.cluster : 1;
+    if (pair && (a.n_qblocks % 2 || grid % 2)) return cudaErrorInvalidValue;   // the runtime pads to pairs
+    while (!pair && cs > 1 && (a.n_qblocks % cs || grid % cs)) cs >>= 1;
     if (cs <= 1) {
         kern<<<grid, kTcThreads, smem, s>>>(map_rows, map_q, a);
         return cudaGetLastError();

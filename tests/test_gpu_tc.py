@@ -133,3 +133,22 @@ def test_tc_bound_prepass_seed(kind):
     got = outs[0].reshape(160, -1)[sub].reshape(-1)
     assert np.array_equal(got["frame"], ref.frame) and np.array_equal(got["subspace"], ref.subspace)
     assert np.array_equal(got["dist2"].view(np.uint32), ref.acc.view(np.uint32))
+
+
+@pytest.mark.parametrize("nq", [256, 300, 64 + 17])
+def test_tc_cta_pairs(nq):
+    """CTA pairs (tcgen05 cta_group::2, M = 256 over two query blocks, each CTA loading half
+    of every row tile): identical results to single CTAs and to the oracle, including an odd
+    number of query blocks (a padding CTA) and a ragged last tile."""
+    spec = synthgen.Spec(seed=34, n_floors=2, paths=5, frames_per_path=1207)
+    F, C = synthgen.db_host(spec)
+    Q = synthgen.render_host(spec, synthgen.query_points(spec, 21, nq))["desc"][:, None, :]
+    sizes = [7000, F.shape[0] - 7000]
+    outs = []
+    for pair in (1, 0):
+        e = _run(F, C, sizes, Q, 15, 1, agg=False, pair=pair)
+        assert e.stat("used_tc") == 1
+        outs.append(e.topk())
+    assert np.array_equal(outs[0], outs[1])
+    ref = oracle.retrieve(sizes, F, C, Q, 15)
+    assert_candidates_equal(outs[0], ref, f"pair nq={nq}")

@@ -10,6 +10,7 @@ Q, _ = synthgen.render_device(spec, synthgen.query_points(spec, 4242, 1024), dev
 e = ol.Engine(0)
 e.upload(F, C, [n], spec.grid())
 if os.environ.get("CHUNK"): e.set_option("chunk", int(os.environ["CHUNK"]))
+if os.environ.get("PAIR"): e.set_option("pair", int(os.environ["PAIR"]))
 if os.environ.get("CLUSTER"): e.set_option("cluster", int(os.environ["CLUSTER"]))
 if os.environ.get("TCSEED"): e.set_option("tc_seed", int(os.environ["TCSEED"]))
 Q3 = Q.view(-1, 1, 64)
@@ -23,4 +24,4 @@ for S in [int(x) for x in sys.argv[2].split(',')]:
     torch.cuda.synchronize()
     t = {k: e.stat(f"time_{k}_ns") / R / 1e6 for k in ("seed", "scan", "merge", "final")}
     e.set_option("time_kernels", 0)
-    print(f"cluster={os.environ.get('CLUSTER')} samples={S} seed {t['seed']:.3f} scan {t['scan']:.3f} merge {t['merge']:.3f} final {t['final']:.3f} total {sum(t.values()):.3f} ms items {e.stat('items')} survivors/pair {e.stat('survivors')/e.stat('pairs'):.2e}")
+    print(f"pair={os.environ.get('PAIR')} samples={S} seed {t['seed']:.3f} scan {t['scan']:.3f} merge {t['merge']:.3f} final {t['final']:.3f} total {sum(t.values()):.3f} ms items {e.stat('items')} survivors/pair {e.stat('survivors')/e.stat('pairs'):.2e}")
