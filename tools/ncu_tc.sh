@@ -8,4 +8,4 @@ REPS=1 CHUNK=0 timeout 900 ncu --set full --import-source on --clock-control non
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --small-batch 0 \
   > gpurun_out/ncu_launches.log 2>&1
-tail -3 gpurun_out/ncu_full.log gpurun_out/ncu_launches.log
+tail -n 3 gpurun_out/ncu_full.log; tail -n 3 gpurun_out/ncu_launches.log
