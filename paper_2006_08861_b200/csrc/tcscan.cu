@@ -47,9 +47,10 @@ constexpr int kMaxStages = 8;
 constexpr int kEpiWarps = 16;           // two groups of 8 (alternate tiles)
 constexpr int kExactWarps = 2;
 constexpr int kTcThreads = 32 * (2 + kEpiWarps + kExactWarps);
-constexpr int kEv = 16;                 // survivor event ring entries per exact warp: a short ring
+constexpr int kEv = 32;                 // survivor event ring entries per exact warp: a short ring
                                         // back-pressures the epilogue so thresholds stay fresh
-                                        // (measured: 8 / 16 / 64 / 128 / 512 -> 16 best)
+                                        // (measured single CTAs: 8/16/64/128/512 -> 16 best; CTA
+                                        // pairs, whose epilogues are coupled: 16/32/64 -> 32)
 constexpr int kTrackMax = 16;           // largest N of the bound pre-pass (register list)
 constexpr float kTauInflate = 1.0f + 1.0f / 131072.0f;   // 1 + 2^-17
 constexpr uint32_t kStageBytes = kTileRows * kK * 2;   // 32 KB
