@@ -287,11 +287,24 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
 
 /* ---- tuning / introspection (never changes results) ---------------------- */
 
-/* Launch-shape knobs for schedule-independence tests and tuning:
- *   "chunk"      entries per work item (0 = automatic)
- *   "qtile"      query frames per CTA tile (0 = automatic)
- *   "tau_seed"   1 (default) / 0: seed pruning thresholds from a sample
- *   "ctas"       cap on resident CTAs (0 = automatic)
+/* Launch-shape knobs for schedule-independence tests and tuning.  None of them can
+ * change a result: every path computes the exact top-N of R3 (tests force each one).
+ *   "chunk"         entries per work item (0 = automatic)
+ *   "qtile"         query frames per CTA tile of the CUDA-core scans (0 = automatic)
+ *   "tau_seed"      1 (default) / 0: seed pruning thresholds before the scan
+ *   "seed_samples"  rows sampled per (frame, subspace) by the exact seed (16..8192)
+ *   "tc"            -1 (default: automatic, >= tc_min_frames frames) / 1 / 0: the certified
+ *                   tensor-core filter (needs |f| < 65000 and ||f|| < 300 in the database)
+ *   "tc_min_frames" frames per query below which the CUDA-core scans are used (default 32)
+ *   "tc_seed"       1 (default) / 0 / 2: tensor-core bound pre-pass as the seed (N <= 16);
+ *                   2 runs it after the exact sampled seed
+ *   "pair"          1 (default) / 0: CTA pairs (tcgen05 cta_group::2) for the tensor-core scan
+ *   "cluster"       1 (default) / 2 / 4 / 8: thread-block clusters over a work item's query
+ *                   blocks when pairs are off
+ *   "scan2"         1 (default) / 0 / 2: small-batch CUDA-core kernel choice
+ *   "ctas"          cap on resident CTAs (0 = automatic)
+ *   "time_kernels"  1 / 0: per-stage CUDA-event timing (stats "time_{seed,scan,merge,final}_ns")
+ *   "tc_debug"      profiling only (results invalid when nonzero)
  * Errors: INVALID_ARGUMENT (unknown key or value). */
 OL_API ol_status ol_set_option(ol_ctx *ctx, const char *key, int64_t value);
 
