@@ -6,8 +6,9 @@
 // a rotation-invariant omnidirectional feature"; S:53 fixes the unnormalised forward
 // DFT X[k] = sum_w x[w] e^{-2 pi i k w / W}, bins k = 1..K (DC dropped), descriptor
 // m / ||m|| if ||m|| > 1e-12, else all-zero and flagged degenerate (reading R4).
-// Binary64 throughout, like the oracle; the angle of term (k, w) is reduced exactly
-// to 2 pi ((k w) mod W) / W and taken from a per-CTA table of sincospi(2 j / W).
+// Binary64 throughout, like the oracle; twiddles come from a per-CTA table of
+// sincospi(2 j / W) at the exactly reduced index (k w) mod W every 8 columns and are
+// advanced by one complex rotation in between.
 // Parity with the oracle is within a few ulps of binary64 (summation order of the
 // norm differs); the fp32 descriptor is RN32 of the binary64 value.
 #include "ol_internal.h"
@@ -34,20 +35,28 @@ extract_kernel(const double *prof, uint64_t n, uint32_t W, float *out32, double 
          p += (uint64_t)gridDim.x * kExtractWarps) {
         for (uint32_t w = lane; w < W; w += 32) pw[w] = prof[p * W + w];
         __syncwarp();
-        double m[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t k = lane + 1 + 32 * h;
-            double re = 0.0, im = 0.0;
-            uint32_t r = 0;                                    // (k w) mod W, exactly
-            for (uint32_t w = 0; w < W; ++w) {
-                re = fma(pw[w], tc[r], re);
-                im = fma(-pw[w], ts[r], im);
-                r += k;
-                if (r >= W) r -= W;
+        // lane l: bins k = l + 1 and l + 33.  The twiddle e^{-2 pi i k w / W} advances by a
+        // rotation per w; every 8 steps it is re-anchored exactly from the table at the
+        // reduced index (k w0) mod W, so rounding drift stays within ~8 rotations
+        const uint32_t k0 = lane + 1, k1 = lane + 33;
+        const double cr0 = tc[k0 % W], sr0 = ts[k0 % W], cr1 = tc[k1 % W], sr1 = ts[k1 % W];
+        double re0 = 0.0, im0 = 0.0, re1 = 0.0, im1 = 0.0;
+        for (uint32_t w0 = 0; w0 < W; w0 += 8) {
+            const uint32_t r0 = (uint32_t)(((uint64_t)k0 * w0) % W), r1 = (uint32_t)(((uint64_t)k1 * w0) % W);
+            double c0 = tc[r0], s0 = ts[r0], c1 = tc[r1], s1 = ts[r1];
+            const uint32_t jn = min(8u, W - w0);
+            for (uint32_t j = 0; j < jn; ++j) {
+                const double x = pw[w0 + j];
+                re0 = fma(x, c0, re0);
+                im0 = fma(-x, s0, im0);
+                re1 = fma(x, c1, re1);
+                im1 = fma(-x, s1, im1);
+                const double c0n = fma(c0, cr0, -s0 * sr0), s0n = fma(s0, cr0, c0 * sr0);
+                const double c1n = fma(c1, cr1, -s1 * sr1), s1n = fma(s1, cr1, c1 * sr1);
+                c0 = c0n; s0 = s0n; c1 = c1n; s1 = s1n;
             }
-            m[h] = sqrt(re * re + im * im);
         }
+        double m[2] = {sqrt(re0 * re0 + im0 * im0), sqrt(re1 * re1 + im1 * im1)};
         double n2 = m[0] * m[0] + m[1] * m[1];
         for (int o = 16; o; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
         const double norm = sqrt(n2);
