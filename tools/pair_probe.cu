@@ -24,7 +24,7 @@ struct Smem {
     uint32_t tmem;
 };
 
-template <bool kPair>
+template <bool kPair, int NB = 128>
 __global__ void __launch_bounds__(256, 1) probe(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb,
                                                  float *D, int reps, long long *cyc) {
     extern __shared__ __align__(1024) unsigned char raw[];
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256, 1) probe(const __grid_constant__ CUtensor
     if (rank == 0 && threadIdx.x == 32) {
         mbar_wait(&s.full, 0);
         tc_fence_after();
-        const uint32_t idesc = idesc_f16_f32(kPair ? 256 : 128, kPair ? 256 : 128);
+        const uint32_t idesc = idesc_f16_f32(kPair ? 256 : 128, kPair ? 2 * NB : NB);
         long long t0 = clock64();
         for (int r = 0; r < reps; ++r)
             for (int k = 0; k < 4; ++k) {
@@ -104,9 +104,9 @@ static CUtensorMap make_map(void *ptr, uint64_t rows) {
     return m;
 }
 
-template <bool kPair>
+template <bool kPair, int NB = 128>
 static void run(const CUtensorMap &ma, const CUtensorMap &mb, float *dD, long long *dc, int reps, int grid, size_t smem) {
-    CK(cudaFuncSetAttribute(probe<kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(probe<kPair, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(256);
@@ -115,7 +115,7 @@ static void run(const CUtensorMap &ma, const CUtensorMap &mb, float *dD, long lo
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = kPair ? 2 : 1; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at; cfg.numAttrs = 1;
-    CK(cudaLaunchKernelEx(&cfg, probe<kPair>, ma, mb, dD, reps, dc));
+    CK(cudaLaunchKernelEx(&cfg, probe<kPair, NB>, ma, mb, dD, reps, dc));
     CK(cudaDeviceSynchronize());
 }
 
@@ -152,5 +152,11 @@ int main() {
     run<false>(ma, mb, dD, dc, reps, 1, smem);
     CK(cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost));
     printf("single: %.1f cycles per M128xN128xK64\n", (double)cyc / reps);
+    run<true, 80>(ma, mb, dD, dc, reps, 2, smem);
+    CK(cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost));
+    printf("pair N=160: %.1f cycles per M256xN160xK64 (ideal 320)\n", (double)cyc / reps);
+    run<true, 64>(ma, mb, dD, dc, reps, 2, smem);
+    CK(cudaMemcpy(&cyc, dc, 8, cudaMemcpyDeviceToHost));
+    printf("pair N=128: %.1f cycles per M256xN128xK64 (ideal 256)\n", (double)cyc / reps);
     return 0;
 }
