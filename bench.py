@@ -170,6 +170,16 @@ def _max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def _cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -234,14 +244,18 @@ def run_omniloc(a):
     torch.cuda.synchronize()
     clocks.start()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]   # per-step spread
     e0.record(stream)
-    for _ in range(a.steps):
+    ev[0].record(stream)
+    for k in range(a.steps):
         step()
+        ev[k + 1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     _barrier(world)
     clk = clocks.stop()
     ms = _max_over_ranks(e0.elapsed_time(e1), world) / a.steps
+    per_step = np.array([ev[k].elapsed_time(ev[k + 1]) for k in range(a.steps)])
     scan_ns = eng.stat("time_scan_ns") / a.steps
     seed_ns = eng.stat("time_seed_ns") / a.steps
     merge_ns = eng.stat("time_merge_ns") / a.steps
@@ -313,6 +327,8 @@ def run_omniloc(a):
            "survivor_frac": survivors / max(pairs, 1), "scan_path": "tensor-core filter" if used_tc else "cuda-core",
            "gpu_launches": kernels_per_step * a.steps,
            "roofline": roofline, "clocks": clk,
+           "step_ms": {"p50": float(np.median(per_step)), "p99": float(np.quantile(per_step, 0.99)),
+                       "min": float(per_step.min()), "max": float(per_step.max())},
            "setup_s": {"generate": gen_s, "upload": upload_s}}
 
     # ------------------------------------------------ small-batch (HBM regime) line
@@ -337,7 +353,7 @@ def run_omniloc(a):
         gbs = rows_local * kc * 4 / sscan / 1e9
         out["small_batch"] = {"query_frames": b2, "ms_per_step": sms, "queries_per_s": b2 / (sms / 1e3),
                               "scan_ms": sscan * 1e3, "scan_hbm_gbs": gbs, "hbm_peak_gbs": hbm_peak,
-                              "hbm_frac": gbs / hbm_peak}
+                              "hbm_frac": gbs / hbm_peak, "hbm_frac_vs_8tbs": gbs / 8000.0}
 
     # ------------------------------------------------ descriptor extraction (NEXT-3) line
     if a.ingest and world == 1:
@@ -410,7 +426,7 @@ def cpu_baseline(F, C, Qd, cfg, n_total, budget_s: float = 15.0):
     oracle.retrieve([S], Fh, Ch, Qh[:nq, None, :], cfg.N)
     dt = time.perf_counter() - t0
     cps = nq * S / dt
-    return {"value": cps / n_total, "unit": "queries/s", "cores": _cores(), "kind": "oracle",
+    return {"value": cps / n_total, "unit": "queries/s", "cores": _cores(), "kind": "oracle", "cpu": _cpu_model(),
             "comparisons_per_sec": cps,
             "sample": f"{nq} query frames x first {S:,} of {n_total:,} DB rows (full-DB rate = "
                       f"comparisons/s / {n_total:,}); acc chain + sort-all top-{cfg.N}, OpenMP over rows",
