@@ -137,7 +137,7 @@ def test_schedule_and_hierarchy_invariance(c2):                  # S:219; R2
     assert all(o == outs[0] for o in outs)
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_logical_shards_equal_single(c2, world):               # §8e sharding, one GPU
     cfg, F, C, video = c2
     Q = video[100:400][:, None, :]
