@@ -92,7 +92,7 @@ struct ol_ctx {
     int64_t opt_tc = -1;         // tensor-core filter: -1 auto (>= 32 frames), 0 off, 1 always
     int64_t opt_tc_min_frames = 32;
     int64_t opt_tc_debug = 0;
-    int64_t opt_tc_seed = 1;     // tensor-core path: seed thresholds with the bound pre-pass
+    int64_t opt_tc_seed = 0;     // tensor-core path: 1 = seed thresholds with the bound pre-pass (off: the exact sampled seed is as fast at C4 and tighter at C3)
     int64_t opt_cluster = 1;     // tensor-core path: CTAs per cluster (query blocks sharing rows)
     int64_t opt_pair = 1;        // tensor-core path: CTA pairs (cta_group::2, M = 256)
     int64_t opt_scan2 = 1;       // small batches (<= 16 frames per tile) use scan2_kernel    // profiling experiments only (results invalid when nonzero)
@@ -549,7 +549,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     // sampled rows (N <= 16: register lists); otherwise the exact sampled seed
     bool tc_seed = use_tc && seed && c->opt_tc_seed && c->seed_stride && N <= 16;
     for (auto &sb : c->subs)
-        if (tc_seed && sb.count / c->seed_stride < 32ull * N) tc_seed = false;
+        if (tc_seed && sb.count / c->seed_stride < 256ull * N) tc_seed = false;   // >= one full item
     if (seed && (!tc_seed || c->opt_tc_seed == 2) && !(c->opt_tc_debug & 64)) {   // (tc_debug & 64: keep the last thresholds)
         SeedArgs sa;
         sa.coarse = c->coarse; sa.fine = c->fine; sa.queries = q; sa.subs = c->subs_d;
@@ -596,6 +596,9 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
             // bound pre-pass: tensor-core scores of every S-th row give each (frame,
             // subspace) N distinct rows with certified upper bounds on their acc
             uint64_t sch = ((c->rows_pad / c->seed_stride) * n_qblocks + 148 * 2 - 1) / (148 * 2);
+            // every epilogue thread sees a quarter of its item's rows as 16-row sets: keep at
+            // least 4 N sets per thread, or its list never fills and publishes nothing
+            if (sch < 256ull * N) sch = 256ull * N;
             sch = (sch + 255) / 256 * 256;
             st = build_sitems(c, sch);
             if (st) return st;

@@ -111,20 +111,22 @@ def test_tc_bound_prepass_seed(kind):
     """The tensor-core bound pre-pass (tau seed from certified upper bounds of every S-th
     row's tensor-core score) only changes thresholds: results stay bit-identical to the
     oracle, with the pre-pass on or off, over 2 subspaces large enough to use it."""
+    # (the pre-pass runs when every subspace has >= 256 N rows in its 1/64 sample)
     if kind == "paper":
-        spec = synthgen.Spec(seed=33, n_floors=8, paths=5, frames_per_path=4000)   # 160k rows
+        spec = synthgen.Spec(seed=33, n_floors=26, paths=5, frames_per_path=4000)   # 520k rows
         F, C = synthgen.db_host(spec)
         Q = synthgen.render_host(spec, synthgen.query_points(spec, 19, 160))["desc"][:, None, :]
     else:
         rng = np.random.default_rng(33)
-        F = (rng.standard_normal((160_000, 64)) * 2).astype(np.float32)     # signed, non-unit
-        C = rng.integers(0, 500, (160_000, 2)).astype(np.int32)
-        Q = (F[rng.integers(0, 160_000, 160)] + rng.standard_normal((160, 64)).astype(np.float32) * 0.05)[:, None, :]
-    sizes = [100_000, 60_000]
+        F = (rng.standard_normal((520_000, 64)) * 2).astype(np.float32)     # signed, non-unit
+        C = rng.integers(0, 500, (520_000, 2)).astype(np.int32)
+        Q = (F[rng.integers(0, 520_000, 160)] + rng.standard_normal((160, 64)).astype(np.float32) * 0.05)[:, None, :]
+    sizes = [260_000, 260_000]
     N = 15
+    grid = spec.grid() if kind == "paper" else (4096, 4096)
     outs = []
     for ts in (1, 0):
-        e = _run(F, C, sizes, Q, N, 1, agg=False, tc_seed=ts)
+        e = _run(F, C, sizes, Q, N, 1, grid=grid, agg=False, tc_seed=ts)
         assert e.stat("used_tc") == 1
         outs.append(e.topk())
     assert np.array_equal(outs[0], outs[1])
