@@ -61,6 +61,7 @@ struct SeedArgs {
     const SubInfo *subs;
     uint32_t *tau0;              // [nq][n_sub]
     uint32_t nq, n_sub, N, samples, kc, splits;   // splits: independent samples per (frame, sub)
+    uint32_t *scratch;           // [nq][n_sub][splits][samples] acc bits (seed_acc -> seed_select)
 };
 
 struct MergeArgs {

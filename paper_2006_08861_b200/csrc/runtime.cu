@@ -58,6 +58,7 @@ struct ol_ctx {
     WorkItem *items_d = nullptr;
     size_t items_cap = 0;
     uint64_t items_chunk = 0;
+    uint32_t *seed_scratch = nullptr; size_t seed_scratch_cap = 0;
     // tensor-core bound pre-pass (tau seed) over the strided view rows 0, S, 2S, ...
     uint32_t seed_stride = 0;     // 0: not available (fp16 path off or tiny database)
     CUtensorMap map_srows;
@@ -232,7 +233,7 @@ void ol_destroy(ol_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     free_db(c);
-    cudaFree(c->items_d); cudaFree(c->sitems_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
+    cudaFree(c->items_d); cudaFree(c->seed_scratch); cudaFree(c->sitems_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
     cudaFree(c->prefix_d); cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
     cudaFree(c->flags_d); cudaFree(c->stat_d); cudaFree(c->tcstat_d); cudaFree(c->prof_d);
@@ -564,6 +565,14 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         while (splits < 16 && (uint64_t)nq * c->n_sub * splits < 148 * 2 &&
                (uint64_t)sa.samples * splits * 2 * 8 <= minc) splits *= 2;
         sa.splits = splits;
+        // the two-kernel seed's scratch (acc bits of every (frame, subspace, split, sample));
+        // beyond 2^28 entries the one-CTA-per-(frame, subspace) kernel runs instead
+        const uint64_t nscr = (uint64_t)nq * c->n_sub * splits * sa.samples;
+        sa.scratch = nullptr;
+        if (nscr <= (1ull << 28)) {
+            OL_CUDA(c, grow(&c->seed_scratch, &c->seed_scratch_cap, (size_t)nscr));
+            sa.scratch = c->seed_scratch;
+        }
         TimeScope ts(c, ol_ctx::T_SEED);
         OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
         OL_LAUNCH(c, launch_tau_seed(sa, c->stream));

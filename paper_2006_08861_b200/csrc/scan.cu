@@ -633,7 +633,112 @@ __global__ void __launch_bounds__(kSeedThreads, 2) tau_seed_kernel(SeedArgs a) {
     if (threadIdx.x == 0) atomicMin(&a.tau0[(size_t)q * a.n_sub + i], prefix);
 }
 
+// Two-kernel seed (the default): every sample row is loaded ONCE per block and scored
+// against 32 frames (rows in registers, frames broadcast from shared memory), the
+// exact chains' acc bits go to a scratch array, then one warp per (frame, subspace,
+// split) radix-selects the N-th smallest from it (8-bit digits from the top, warp-
+// aggregated shared-memory histograms).  Same sample rows and the same values as
+// tau_seed_kernel, far fewer bytes: rows are reused across frames.
+constexpr int kSeedFrames = 32;
+
+template <int KC>
+__global__ void __launch_bounds__(256) seed_acc_kernel(SeedArgs a) {
+    __shared__ alignas(16) float qs[kSeedFrames][kK];
+    const uint32_t isp = blockIdx.x;                     // (subspace, split)
+    const uint32_t i = isp / a.splits, split = isp % a.splits;
+    const uint32_t f0 = blockIdx.z * kSeedFrames;
+    const uint32_t nf = min((uint32_t)kSeedFrames, a.nq - f0);
+    for (uint32_t t = threadIdx.x; t < nf * kK; t += blockDim.x) qs[t / kK][t % kK] = a.queries[(size_t)f0 * kK + t];
+    __syncthreads();
+    const SubInfo si = a.subs[i];
+    const uint32_t S = (uint32_t)min((uint64_t)a.samples, si.count);
+    const uint32_t smp = blockIdx.y * blockDim.x + threadIdx.x;
+    if (S < a.N || smp >= S) return;
+    const uint64_t row = si.row_begin + (((uint64_t)smp * a.splits + split) * si.count) / ((uint64_t)S * a.splits);
+    float4 f[kK / 4];
+#pragma unroll
+    for (int k4 = 0; k4 < kK / 4; ++k4)
+        f[k4] = 4 * k4 < KC ? __ldg(reinterpret_cast<const float4 *>(a.coarse + coarse_off(row, 4 * k4, KC)))
+                            : __ldg(reinterpret_cast<const float4 *>(a.fine + row * (kK - KC) + (4 * k4 - KC)));
+    for (uint32_t j = 0; j < nf; ++j) {
+        const float4 *q4 = reinterpret_cast<const float4 *>(qs[j]);
+        float acc = 0.f;
+#pragma unroll
+        for (int k4 = 0; k4 < kK / 4; ++k4) {
+            const float4 x = q4[k4];
+            acc = chain_step(acc, x.x, f[k4].x); acc = chain_step(acc, x.y, f[k4].y);
+            acc = chain_step(acc, x.z, f[k4].z); acc = chain_step(acc, x.w, f[k4].w);
+        }
+        a.scratch[(((size_t)(f0 + j) * a.n_sub + i) * a.splits + split) * a.samples + smp] = __float_as_uint(acc);
+    }
+}
+
+__global__ void __launch_bounds__(256) seed_select_kernel(SeedArgs a) {
+    __shared__ uint32_t hist[8][256];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t job = blockIdx.x * 8 + w;   // (frame, subspace, split)
+    if (job >= a.nq * a.n_sub * a.splits) return;   // (whole warps only: warp-level sync below)
+    const uint32_t i = (job / a.splits) % a.n_sub, q = (job / a.splits) / a.n_sub;
+    const uint32_t S = (uint32_t)min((uint64_t)a.samples, a.subs[i].count);
+    if (S < a.N) return;
+    const uint32_t *v = a.scratch + (size_t)job * a.samples;
+    uint32_t prefix = 0, pmask = 0, k = a.N;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int b = lane; b < 256; b += 32) hist[w][b] = 0;
+        __syncwarp();
+        for (uint32_t t0 = 0; t0 < S; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            const uint32_t x = t < S ? __ldcg(v + t) : 0u;
+            const bool in = t < S && (x & pmask) == prefix;
+            const uint32_t d = in ? (x >> shift) & 255u : 256u;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            if (in && lane == __ffs(peers) - 1) atomicAdd(&hist[w][d], (uint32_t)__popc(peers));
+        }
+        __syncwarp();
+        uint32_t c[8], tot = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { c[j] = hist[w][lane * 8 + j]; tot += c[j]; }
+        uint32_t incl = tot;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        uint32_t below = incl - tot, digit = 0, under = 0;
+        const bool here = below < k && k <= incl;
+        if (here) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (below + c[j] >= k) { digit = lane * 8 + j; under = below; break; }
+                below += c[j];
+            }
+        }
+        const int src = __ffs(__ballot_sync(0xffffffffu, here)) - 1;
+        digit = __shfl_sync(0xffffffffu, digit, src);
+        under = __shfl_sync(0xffffffffu, under, src);
+        prefix |= digit << shift;
+        pmask |= 255u << shift;
+        k -= under;
+        __syncwarp();
+    }
+    // every split's N-th smallest is an upper bound of the true N-th: keep the least
+    if (lane == 0) atomicMin(&a.tau0[(size_t)q * a.n_sub + i], prefix);
+}
+
 cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s) {
+    if (a.scratch) {
+        const dim3 g1(a.n_sub * a.splits, (a.samples + 255) / 256, (a.nq + kSeedFrames - 1) / kSeedFrames);
+        switch (a.kc) {
+            case 8: seed_acc_kernel<8><<<g1, 256, 0, s>>>(a); break;
+            case 16: seed_acc_kernel<16><<<g1, 256, 0, s>>>(a); break;
+            case 32: seed_acc_kernel<32><<<g1, 256, 0, s>>>(a); break;
+            case 64: seed_acc_kernel<64><<<g1, 256, 0, s>>>(a); break;
+            default: return cudaErrorInvalidValue;
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        seed_select_kernel<<<(a.nq * a.n_sub * a.splits + 7) / 8, 256, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     const unsigned grid = a.nq * a.n_sub * a.splits;
     switch (a.kc) {
         case 8: tau_seed_kernel<8><<<grid, kSeedThreads, 0, s>>>(a); break;
