@@ -579,7 +579,11 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     }
     c->used_tc = false;
     if (n_items && use_tc) {
-        const bool pair = c->opt_pair != 0;
+        // CTA pairs need an even number of query blocks: a lone block (<= 128 frames) or a
+        // small odd count would pay for a padding CTA's MMAs (measured: 1 block 1.8 ms single
+        // vs 2.6 ms paired at C4; 2 blocks 3.7 vs 3.3 ms)
+        const uint32_t nqb1 = (nq + tc_qb - 1) / tc_qb;
+        const bool pair = c->opt_pair != 0 && (nqb1 % 2 == 0 || nqb1 >= 5);
         const uint32_t qb = tc_qb, n_qblocks = ((nq + qb - 1) / qb + (pair ? 1 : 0)) / (pair ? 2 : 1) * (pair ? 2 : 1),
                        nq_pad = n_qblocks * qb;
         OL_CUDA(c, grow((uint16_t **)&c->q16, &c->q16_cap, (size_t)nq_pad * OL_K));

@@ -137,11 +137,12 @@ def test_tc_bound_prepass_seed(kind):
     assert np.array_equal(got["dist2"].view(np.uint32), ref.acc.view(np.uint32))
 
 
-@pytest.mark.parametrize("nq", [256, 300, 64 + 17])
+@pytest.mark.parametrize("nq", [256, 600, 647])
 def test_tc_cta_pairs(nq):
     """CTA pairs (tcgen05 cta_group::2, M = 256 over two query blocks, each CTA loading half
     of every row tile): identical results to single CTAs and to the oracle, including an odd
-    number of query blocks (a padding CTA) and a ragged last tile."""
+    number of query blocks (600 frames = 5 blocks: a padding CTA), a ragged last query block
+    (647) and a ragged last row tile."""
     spec = synthgen.Spec(seed=34, n_floors=2, paths=5, frames_per_path=1207)
     F, C = synthgen.db_host(spec)
     Q = synthgen.render_host(spec, synthgen.query_points(spec, 21, nq))["desc"][:, None, :]
