@@ -355,6 +355,31 @@ def run_omniloc(a):
                               "scan_ms": sscan * 1e3, "scan_hbm_gbs": gbs, "hbm_peak_gbs": hbm_peak,
                               "hbm_frac": gbs / hbm_peak, "hbm_frac_vs_8tbs": gbs / 8000.0}
 
+    # ------------------------------------------------ mid batch: the tensor-core scan HBM-bound
+    if a.small_batch and world == 1 and used_tc:
+        b3 = 64
+        Qm = Qd[:b3].contiguous().view(b3, 1, 64)
+        for _ in range(3):
+            eng.query(Qm, params=params, aggregate=True)
+        torch.cuda.synchronize()
+        eng.set_option("time_kernels", 1)
+        reps = 20
+        e0.record(stream)
+        for _ in range(reps):
+            eng.query(Qm, params=params, aggregate=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        mms = e0.elapsed_time(e1) / reps
+        mscan = eng.stat("time_scan_ns") / reps / 1e9
+        for k in ("seed", "merge", "final"):
+            eng.stat(f"time_{k}_ns")
+        eng.set_option("time_kernels", 0)
+        mbytes = rows_local * (64 * 2) + rows_local // 32 * 8   # fp16 rows + block bound terms
+        mg = mbytes / mscan / 1e9
+        out["mid_batch"] = {"query_frames": b3, "kernel": "tcscan_kernel", "ms_per_step": mms,
+                            "queries_per_s": b3 / (mms / 1e3), "scan_ms": mscan * 1e3, "scan_hbm_gbs": mg,
+                            "hbm_peak_gbs": hbm_peak, "hbm_frac": mg / hbm_peak, "hbm_frac_vs_8tbs": mg / 8000.0}
+
     # ------------------------------------------------ descriptor extraction (NEXT-3) line
     if a.ingest and world == 1:
         n_in, Wp = a.ingest, 256
