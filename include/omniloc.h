@@ -295,7 +295,7 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *   "seed_samples"  rows sampled per (frame, subspace) by the exact seed (16..8192)
  *   "tc"            -1 (default: automatic, >= tc_min_frames frames) / 1 / 0: the certified
  *                   tensor-core filter (needs |f| < 65000 and ||f|| < 300 in the database)
- *   "tc_min_frames" frames per query below which the CUDA-core scans are used (default 32)
+ *   "tc_min_frames" frames per query below which the CUDA-core scans are used (default 12)
  *   "tc_seed"       0 (default) / 1 / 2: tensor-core bound pre-pass as the seed (N <= 16);
  *                   2 runs it after the exact sampled seed
  *   "pair"          1 (default) / 0: CTA pairs (tcgen05 cta_group::2) for the tensor-core scan

@@ -90,8 +90,8 @@ struct ol_ctx {
     int launches = 0;
     // options
     int64_t opt_chunk = 0, opt_qtile = 0, opt_tau_seed = 1, opt_ctas = 0, opt_time = 0, opt_seed_samples = 4096;
-    int64_t opt_tc = -1;         // tensor-core filter: -1 auto (>= 32 frames), 0 off, 1 always
-    int64_t opt_tc_min_frames = 32;
+    int64_t opt_tc = -1;         // tensor-core filter: -1 auto (>= tc_min_frames frames), 0 off, 1 always
+    int64_t opt_tc_min_frames = 12;   // measured C4: 8 frames scan2 1.37 vs tc 1.77 ms; 16 frames 2.42 vs 1.77
     int64_t opt_tc_debug = 0;
     int64_t opt_tc_seed = 0;     // tensor-core path: 1 = seed thresholds with the bound pre-pass (off: the exact sampled seed is as fast at C4 and tighter at C3)
     int64_t opt_cluster = 1;     // tensor-core path: CTAs per cluster (query blocks sharing rows)

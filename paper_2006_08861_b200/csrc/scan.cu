@@ -726,12 +726,15 @@ __global__ void __launch_bounds__(256) seed_select_kernel(SeedArgs a) {
 
 cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s) {
     if (a.scratch) {
-        const dim3 g1(a.n_sub * a.splits, (a.samples + 255) / 256, (a.nq + kSeedFrames - 1) / kSeedFrames);
+        // 64-thread CTAs when 256 would leave SMs idle (few frames)
+        const uint32_t fz = (a.nq + kSeedFrames - 1) / kSeedFrames;
+        const uint32_t bt = (uint64_t)a.n_sub * a.splits * ((a.samples + 255) / 256) * fz < 2 * 148 ? 64 : 256;
+        const dim3 g1(a.n_sub * a.splits, (a.samples + bt - 1) / bt, fz);
         switch (a.kc) {
-            case 8: seed_acc_kernel<8><<<g1, 256, 0, s>>>(a); break;
-            case 16: seed_acc_kernel<16><<<g1, 256, 0, s>>>(a); break;
-            case 32: seed_acc_kernel<32><<<g1, 256, 0, s>>>(a); break;
-            case 64: seed_acc_kernel<64><<<g1, 256, 0, s>>>(a); break;
+            case 8: seed_acc_kernel<8><<<g1, bt, 0, s>>>(a); break;
+            case 16: seed_acc_kernel<16><<<g1, bt, 0, s>>>(a); break;
+            case 32: seed_acc_kernel<32><<<g1, bt, 0, s>>>(a); break;
+            case 64: seed_acc_kernel<64><<<g1, bt, 0, s>>>(a); break;
             default: return cudaErrorInvalidValue;
         }
         cudaError_t e = cudaGetLastError();
