@@ -293,6 +293,8 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *   "qtile"         query frames per CTA tile of the CUDA-core scans (0 = automatic)
  *   "tau_seed"      1 (default) / 0: seed pruning thresholds before the scan
  *   "seed_samples"  rows sampled per (frame, subspace) by the exact seed (16..8192)
+ *   "seed_kernel"   1 (default) / 0: two-kernel seed (sample rows reused across frames) for >= 1,024
+ *                   (frame, subspace, split) jobs, else one CTA per job
  *   "tc"            -1 (default: automatic, >= tc_min_frames frames) / 1 / 0: the certified
  *                   tensor-core filter (needs |f| < 65000 and ||f|| < 300 in the database)
  *   "tc_min_frames" frames per query below which the CUDA-core scans are used (default 12)

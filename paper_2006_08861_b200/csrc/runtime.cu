@@ -93,6 +93,7 @@ struct ol_ctx {
     int64_t opt_tc = -1;         // tensor-core filter: -1 auto (>= tc_min_frames frames), 0 off, 1 always
     int64_t opt_tc_min_frames = 12;   // measured C4: 8 frames scan2 1.37 vs tc 1.77 ms; 16 frames 2.42 vs 1.77
     int64_t opt_tc_debug = 0;
+    int64_t opt_seed_kernel = 1;   // 1: two-kernel seed (rows reused across frames), 0: one CTA per (frame, subspace)
     int64_t opt_tc_seed = 0;     // tensor-core path: 1 = seed thresholds with the bound pre-pass (off: the exact sampled seed is as fast at C4 and tighter at C3)
     int64_t opt_cluster = 1;     // tensor-core path: CTAs per cluster (query blocks sharing rows)
     int64_t opt_pair = 1;        // tensor-core path: CTA pairs (cta_group::2, M = 256)
@@ -566,10 +567,14 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
                (uint64_t)sa.samples * splits * 2 * 8 <= minc) splits *= 2;
         sa.splits = splits;
         // the two-kernel seed's scratch (acc bits of every (frame, subspace, split, sample));
-        // beyond 2^28 entries the one-CTA-per-(frame, subspace) kernel runs instead
+        // the one-CTA-per-(frame, subspace, split) kernel runs instead beyond 2^28 entries or
+        // for few (frame, subspace, split) jobs, where a warp-per-job select is too serial
+        // (measured: 8 / 256 frames at 10M rows 0.05 / 0.15 vs 0.16 / 0.17 ms; 1,024 frames at
+        // 100M 0.62 vs 0.24 ms; C2 0.92 vs 0.18 ms)
         const uint64_t nscr = (uint64_t)nq * c->n_sub * splits * sa.samples;
+        const uint64_t jobs = (uint64_t)nq * c->n_sub * splits;
         sa.scratch = nullptr;
-        if (nscr <= (1ull << 28)) {
+        if (nscr <= (1ull << 28) && jobs >= 1024 && c->opt_seed_kernel != 0) {
             OL_CUDA(c, grow(&c->seed_scratch, &c->seed_scratch_cap, (size_t)nscr));
             sa.scratch = c->seed_scratch;
         }
@@ -963,6 +968,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "tc")) { if (v < -1 || v > 1) goto bad; c->opt_tc = v; }
     else if (!strcmp(key, "pair")) { if (v != 0 && v != 1) goto bad; c->opt_pair = v; }
     else if (!strcmp(key, "cluster")) { if (v != 1 && v != 2 && v != 4 && v != 8) goto bad; c->opt_cluster = v; }
+    else if (!strcmp(key, "seed_kernel")) { if (v != 0 && v != 1) goto bad; c->opt_seed_kernel = v; }
     else if (!strcmp(key, "tc_seed")) { if (v < 0 || v > 2) goto bad; c->opt_tc_seed = v; }
     else if (!strcmp(key, "scan2")) { if (v < 0 || v > 2) goto bad; c->opt_scan2 = v; }
     else if (!strcmp(key, "tc_min_frames")) { if (v < 1) goto bad; c->opt_tc_min_frames = v; }

@@ -11,8 +11,8 @@ e = ol.Engine(0)
 e.upload(F, C, [n], spec.grid())
 for nq in [int(x) for x in sys.argv[2].split(',')]:
     Q3 = Q[:nq].contiguous().view(-1, 1, 64)
-    for tc, pair in [(1, 1), (1, 0), (0, 0)]:
-        e.set_option("tc", tc); e.set_option("pair", pair)
+    for tc, pair, sk in [(0, 0, 1), (0, 0, 0)]:
+        e.set_option("tc", tc); e.set_option("pair", pair); e.set_option("seed_kernel", sk)
         for _ in range(2): e.query(Q3, N=15)
         torch.cuda.synchronize()
         e.set_option("time_kernels", 1)
@@ -20,4 +20,4 @@ for nq in [int(x) for x in sys.argv[2].split(',')]:
         torch.cuda.synchronize()
         t = {k: e.stat(f"time_{k}_ns") / 5 / 1e6 for k in ("seed", "scan", "merge", "final")}
         e.set_option("time_kernels", 0)
-        print(f"nq={nq} tc={tc} pair={pair} used_tc={e.stat('used_tc')} seed {t['seed']:.3f} scan {t['scan']:.3f} total {sum(t.values()):.3f} ms")
+        print(f"nq={nq} tc={tc} seed_kernel={sk} used_tc={e.stat('used_tc')} seed {t['seed']:.3f} scan {t['scan']:.3f} total {sum(t.values()):.3f} ms")
