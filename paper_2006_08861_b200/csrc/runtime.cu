@@ -48,6 +48,7 @@ struct ol_ctx {
     void *q16 = nullptr; size_t q16_cap = 0;
     float4 *qmeta = nullptr; size_t qmeta_cap = 0;
     bool used_tc = false;
+    bool used_pair = false;
     // NEXT-1 profiles and shift keys
     float *prof = nullptr; uint32_t prof_W = 0;
     float *qprof_d = nullptr; size_t qprof_cap = 0;
@@ -96,7 +97,7 @@ struct ol_ctx {
     int64_t opt_seed_kernel = 1;   // 1: two-kernel seed (rows reused across frames), 0: one CTA per (frame, subspace)
     int64_t opt_tc_seed = 0;     // tensor-core path: 1 = seed thresholds with the bound pre-pass (off: the exact sampled seed is as fast at C4 and tighter at C3)
     int64_t opt_cluster = 1;     // tensor-core path: CTAs per cluster (query blocks sharing rows)
-    int64_t opt_pair = 1;        // tensor-core path: CTA pairs (cta_group::2, M = 256)
+    int64_t opt_pair = 1;        // tensor-core path: CTA pairs (cta_group::2, M = 256): 0 off, 1 auto, 2 on
     int64_t opt_scan2 = 1;       // small batches (<= 16 frames per tile) use scan2_kernel    // profiling experiments only (results invalid when nonzero)
     // per-kernel-class CUDA-event timing (option "time_kernels"): pairs recorded on
     // the context stream around each launch; summed and released by ol_get_stat
@@ -583,12 +584,17 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         OL_LAUNCH(c, launch_tau_seed(sa, c->stream));
     }
     c->used_tc = false;
+    c->used_pair = false;
     if (n_items && use_tc) {
         // CTA pairs need an even number of query blocks: a lone block (<= 128 frames) or a
         // small odd count would pay for a padding CTA's MMAs (measured: 1 block 1.8 ms single
-        // vs 2.6 ms paired at C4; 2 blocks 3.7 vs 3.3 ms)
+        // vs 2.6 ms paired at C4; 2 blocks 3.7 vs 3.3 ms).  Automatic mode also wants >= 2M
+        // rows: pairs halve the DRAM re-reads of a chunk's rows, which only matter once the
+        // plane outgrows L2 (1,024 frames: 1M rows 0.711 vs 0.695 ms single, 2M 0.888 vs
+        // 0.891, 5M 1.262 vs 1.290, 20M 2.70 vs 2.92)
         const uint32_t nqb1 = (nq + tc_qb - 1) / tc_qb;
-        const bool pair = c->opt_pair != 0 && (nqb1 % 2 == 0 || nqb1 >= 5);
+        const bool pair = (c->opt_pair == 2 || (c->opt_pair == 1 && c->rows >= 2000000)) &&
+                          (nqb1 % 2 == 0 || nqb1 >= 5);
         const uint32_t qb = tc_qb, n_qblocks = ((nq + qb - 1) / qb + (pair ? 1 : 0)) / (pair ? 2 : 1) * (pair ? 2 : 1),
                        nq_pad = n_qblocks * qb;
         OL_CUDA(c, grow((uint16_t **)&c->q16, &c->q16_cap, (size_t)nq_pad * OL_K));
@@ -630,6 +636,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         TimeScope ts(c, ol_ctx::T_SCAN);
         OL_LAUNCH(c, launch_tcscan(pair ? c->map_rows_half : c->map_rows, map_q, a, (int)(n_items * n_qblocks), c->stream));
         c->used_tc = true;
+        c->used_pair = pair;
     } else if (n_items) {
         ScanArgs a;
         a.coarse = c->coarse; a.fine = c->fine; a.queries = q; a.items = c->items_d;
@@ -966,7 +973,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "ctas")) { if (v < 0) goto bad; c->opt_ctas = v; }
     else if (!strcmp(key, "time_kernels")) { if (v != 0 && v != 1) goto bad; c->opt_time = v; }
     else if (!strcmp(key, "tc")) { if (v < -1 || v > 1) goto bad; c->opt_tc = v; }
-    else if (!strcmp(key, "pair")) { if (v != 0 && v != 1) goto bad; c->opt_pair = v; }
+    else if (!strcmp(key, "pair")) { if (v < 0 || v > 2) goto bad; c->opt_pair = v; }
     else if (!strcmp(key, "cluster")) { if (v != 1 && v != 2 && v != 4 && v != 8) goto bad; c->opt_cluster = v; }
     else if (!strcmp(key, "seed_kernel")) { if (v != 0 && v != 1) goto bad; c->opt_seed_kernel = v; }
     else if (!strcmp(key, "tc_seed")) { if (v < 0 || v > 2) goto bad; c->opt_tc_seed = v; }
@@ -1002,6 +1009,7 @@ ol_status ol_get_stat(ol_ctx *c, const char *key, int64_t *value) {
     else if (!strcmp(key, "chunk")) *value = (int64_t)c->items_chunk;
     else if (!strcmp(key, "items")) *value = (int64_t)c->items.size();
     else if (!strcmp(key, "used_tc")) *value = c->used_tc ? 1 : 0;
+    else if (!strcmp(key, "used_pair")) *value = c->used_pair ? 1 : 0;
     else if (!strcmp(key, "tc_ok")) *value = c->tc_ok ? 1 : 0;
     else if (!strncmp(key, "time_", 5)) {
         // time_seed_ns / time_scan_ns / time_merge_ns / time_final_ns: summed over the

@@ -148,9 +148,9 @@ def test_tc_cta_pairs(nq):
     Q = synthgen.render_host(spec, synthgen.query_points(spec, 21, nq))["desc"][:, None, :]
     sizes = [7000, F.shape[0] - 7000]
     outs = []
-    for pair in (1, 0):
+    for pair in (2, 0):
         e = _run(F, C, sizes, Q, 15, 1, agg=False, pair=pair)
-        assert e.stat("used_tc") == 1
+        assert e.stat("used_tc") == 1 and e.stat("used_pair") == (pair == 2)
         outs.append(e.topk())
     assert np.array_equal(outs[0], outs[1])
     ref = oracle.retrieve(sizes, F, C, Q, 15)
