@@ -274,9 +274,11 @@ def run_omniloc(a):
     sm_max = peaks.get("sm_max_mhz", 1965.0)
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     if used_tc:
-        # tensor-core certified filter: 2 x 64 fp16 MMA flops per (query, row) pair; peak =
-        # measured dense bf16 burst (fp16 and bf16 have the same nominal tensor rate)
-        flops = 2.0 * 64 * pairs
+        # tensor-core certified filter: 2 x kf fp16 MMA flops per (query, row) pair (kf = the
+        # filter's dimensions, option tc_k: 32 at C4); peak = measured dense bf16 (fp16 and
+        # bf16 have the same nominal tensor rate)
+        kf = eng.stat("tc_k")
+        flops = 2.0 * kf * pairs
         # the scan runs back to back inside a long step (power-capped clocks): the
         # sustained measured figure is the denominator
         tc_peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
@@ -297,8 +299,13 @@ def run_omniloc(a):
                     "traffic_source": "profiles/r01_tcscan_ncu.json (ncu --set full, one launch)" if traffic else None,
                     "peak_source": "MEASURED_PEAKS bf16_tflops_sustained (fp16 = bf16 nominal rate); "
                                    f"burst {peaks.get('bf16_tflops')}",
-                    "per_launch": {"pairs": pairs, "mma_flops": flops, "algorithmic_bytes": alg_bytes,
+                    "per_launch": {"pairs": pairs, "filter_k": kf, "mma_flops": flops, "algorithmic_bytes": alg_bytes,
                                    "avg_ms": scan_s * 1e3,
+                                   # the epilogue reads every fp32 accumulator once (tcgen05.ld):
+                                   # 4 B per pair; tools/tmem_probe.cu measured ~271 B/clk/SM
+                                   # with 16 warps (x 148 SMs x max clock)
+                                   "tmem_read_tbs": pairs * 4 / scan_s / 1e12 if scan_s > 0 else None,
+                                   "tmem_probe_peak_tbs": 271 * 148 * sm_max * 1e6 / 1e12,
                                    "hbm_gbs": alg_bytes / scan_s / 1e9 if scan_s > 0 else None,
                                    "exact_rescored_pairs": survivors}}
     else:

@@ -300,6 +300,10 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *   "tc_min_frames" frames per query below which the CUDA-core scans are used (default 12)
  *   "tc_seed"       0 (default) / 1 / 2: tensor-core bound pre-pass as the seed (N <= 16);
  *                   2 runs it after the exact sampled seed
+ *   "tc_k"          0 (default: 32 when every subspace holds >= 32M rows on this rank, else
+ *                   64) / 16 / 32 / 48 / 64: dimensions (a prefix) the certified tensor-core
+ *                   filter scores; fewer halve its MMA work, more pairs reach the exact
+ *                   re-score.  Results are identical.  Takes effect at the next ol_upload_db
  *   "pair"          1 (default: when the rank holds >= 2M rows) / 2 (always) / 0 (never): CTA
  *                   pairs (tcgen05 cta_group::2) for the tensor-core scan
  *   "cluster"       1 (default) / 2 / 4 / 8: thread-block clusters over a work item's query
@@ -314,7 +318,7 @@ OL_API ol_status ol_set_option(ol_ctx *ctx, const char *key, int64_t value);
 /* Read statistics of the last query: "survivors" (pairs that passed the coarse
  * bound), "pairs" (pairs scanned), "kernels" (kernel launches of the last
  * ol_query + ol_finalize), "used_tc" / "used_pair" (1 if the tensor-core scan / CTA pairs
- * ran), "items" / "chunk" (work items and rows per item), "time_{seed,scan,merge,final}_ns"
+ * ran), "tc_k" (the filter's dimensions), "items" / "chunk" (work items and rows per item), "time_{seed,scan,merge,final}_ns"
  * (accumulated stage times while option "time_kernels" is 1; reading resets them).
  * Unknown key: INVALID_ARGUMENT.  Synchronises. */
 OL_API ol_status ol_get_stat(ol_ctx *ctx, const char *key, int64_t *value);

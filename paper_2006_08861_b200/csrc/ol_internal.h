@@ -115,6 +115,7 @@ struct TcScanArgs {
     uint32_t nq, n_items, n_qblocks, qb, n_sub, N, kc, stages;
     uint32_t dbg;                 // profiling only: 1 skip epilogue math, 2 skip MMA, 4 skip cold path, ...
     uint32_t n_blk;               // rows_pad / 32
+    uint32_t kf;                  // filter on the first kf of K dimensions (16..64, multiple of 16)
     unsigned long long *prof;     // [16] per-role cycle counters when dbg & 32 (profiling only)
 };
 
@@ -133,9 +134,9 @@ struct ShiftArgs {
 // launchers (return cudaGetLastError())
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s);
 cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, uint64_t rows, void *plane,
-                                float2 *blk, uint32_t *stat, cudaStream_t s);
+                                float2 *blk, uint32_t *stat, uint32_t kf, cudaStream_t s);
 cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float4 *qmeta,
-                                   uint32_t *bounds, cudaStream_t s);
+                                   uint32_t *bounds, uint32_t kf, cudaStream_t s);
 cudaError_t launch_fill_u32(uint32_t *p, uint64_t n, uint32_t v, cudaStream_t s);
 size_t extract_smem_bytes(uint32_t W);
 cudaError_t launch_extract(const double *prof, uint64_t n, uint32_t W, float *out32, double *out64,

@@ -95,6 +95,8 @@ struct ol_ctx {
     int64_t opt_tc_min_frames = 12;   // measured C4: 8 frames scan2 1.37 vs tc 1.77 ms; 16 frames 2.42 vs 1.77
     int64_t opt_tc_debug = 0;
     int64_t opt_seed_kernel = 1;   // 1: two-kernel seed (rows reused across frames), 0: one CTA per (frame, subspace)
+    int64_t opt_tc_k = 0;        // tensor-core filter dimensions (prefix; applied at upload); 0 = auto
+    uint32_t tc_kf = 64;
     int64_t opt_tc_seed = 0;     // tensor-core path: 1 = seed thresholds with the bound pre-pass (off: the exact sampled seed is as fast at C4 and tighter at C3)
     int64_t opt_cluster = 1;     // tensor-core path: CTAs per cluster (query blocks sharing rows)
     int64_t opt_pair = 1;        // tensor-core path: CTA pairs (cta_group::2, M = 256): 0 off, 1 auto, 2 on
@@ -374,8 +376,15 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
             OL_CUDA(c, cudaMalloc(&c->plane16, sizeof(uint16_t) * rows_pad * OL_K));
             OL_CUDA(c, cudaMalloc((void **)&c->blk, sizeof(float2) * (rows_pad / 32)));
             OL_CUDA(c, cudaMemsetAsync(c->tcstat_d, 0, 8 * sizeof(uint32_t), c->stream));
+            // the filter on the first 32 dimensions halves the MMA work but passes more
+            // pairs to the exact path (1,024 frames: 20M rows 2.87 vs 2.72 ms, 35M 4.15 vs
+            // 4.39, 50M 5.57 vs 6.09, 100M 9.88 vs 12.0 ms for 32 vs 64): automatic mode takes
+            // 32 once every subspace holds >= 32M rows on this rank
+            uint64_t minc = ~0ull;
+            for (auto &sb : subs) minc = sb.count < minc ? sb.count : minc;
+            c->tc_kf = c->opt_tc_k ? (uint32_t)c->opt_tc_k : (minc >= 32000000ull ? 32u : 64u);
             OL_CUDA(c, launch_tc_prep_rows(c->coarse, c->fine, kc, rows_pad, c->plane16, c->blk, c->tcstat_d,
-                                           c->stream));
+                                           c->tc_kf, c->stream));
         }
     }
     OL_CUDA(c, cudaMemcpyAsync(c->subs_d, subs.data(), sizeof(SubInfo) * ns, cudaMemcpyHostToDevice,
@@ -550,7 +559,8 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     const bool seed = c->opt_tau_seed != 0;
     // tensor-core path: seed with the bound pre-pass when every subspace has >= 32 N
     // sampled rows (N <= 16: register lists); otherwise the exact sampled seed
-    bool tc_seed = use_tc && seed && c->opt_tc_seed && c->seed_stride && N <= 16;
+    // (the pre-pass needs upper bounds on the full distance: only with a full-K filter)
+    bool tc_seed = use_tc && seed && c->opt_tc_seed && c->seed_stride && N <= 16 && c->tc_kf == OL_K;
     for (auto &sb : c->subs)
         if (tc_seed && sb.count / c->seed_stride < 256ull * N) tc_seed = false;   // >= one full item
     if (seed && (!tc_seed || c->opt_tc_seed == 2) && !(c->opt_tc_debug & 64)) {   // (tc_debug & 64: keep the last thresholds)
@@ -600,7 +610,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         OL_CUDA(c, grow((uint16_t **)&c->q16, &c->q16_cap, (size_t)nq_pad * OL_K));
         OL_CUDA(c, grow(&c->qmeta, &c->qmeta_cap, nq));
         OL_CUDA(c, cudaMemsetAsync(c->tcstat_d + 2, 0, 2 * sizeof(uint32_t), c->stream));
-        OL_LAUNCH(c, launch_tc_prep_queries(q, nq, nq_pad, c->q16, c->qmeta, c->tcstat_d, c->stream));
+        OL_LAUNCH(c, launch_tc_prep_queries(q, nq, nq_pad, c->q16, c->qmeta, c->tcstat_d, c->tc_kf, c->stream));
         if ((!seed || (tc_seed && c->opt_tc_seed != 2)) && !(c->opt_tc_debug & 64))
             OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
         CUtensorMap map_q;
@@ -614,6 +624,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         a.g_tau = c->tau0_d; a.queries = q; a.coarse = c->coarse; a.fine = c->fine;
         a.partial = c->partial_d; a.stat_survivors = c->stat_d; a.stat_flagged = c->stat_d + 1;
         a.nq = nq; a.n_items = n_items; a.n_qblocks = n_qblocks; a.qb = qb; a.n_sub = c->n_sub;
+        a.kf = c->tc_kf;
         a.N = N; a.kc = (uint32_t)c->kc; a.stages = tc_stages; a.dbg = (uint32_t)c->opt_tc_debug; a.prof = c->prof_d;
         if (a.dbg & 32) OL_CUDA(c, cudaMemsetAsync(c->prof_d, 0, 64 * sizeof(unsigned long long), c->stream));
         if (tc_seed && !(a.dbg & 64)) {
@@ -976,6 +987,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "pair")) { if (v < 0 || v > 2) goto bad; c->opt_pair = v; }
     else if (!strcmp(key, "cluster")) { if (v != 1 && v != 2 && v != 4 && v != 8) goto bad; c->opt_cluster = v; }
     else if (!strcmp(key, "seed_kernel")) { if (v != 0 && v != 1) goto bad; c->opt_seed_kernel = v; }
+    else if (!strcmp(key, "tc_k")) { if (v != 0 && (v < 16 || v > 64 || v % 16)) goto bad; c->opt_tc_k = v; }
     else if (!strcmp(key, "tc_seed")) { if (v < 0 || v > 2) goto bad; c->opt_tc_seed = v; }
     else if (!strcmp(key, "scan2")) { if (v < 0 || v > 2) goto bad; c->opt_scan2 = v; }
     else if (!strcmp(key, "tc_min_frames")) { if (v < 1) goto bad; c->opt_tc_min_frames = v; }
@@ -1010,6 +1022,7 @@ ol_status ol_get_stat(ol_ctx *c, const char *key, int64_t *value) {
     else if (!strcmp(key, "items")) *value = (int64_t)c->items.size();
     else if (!strcmp(key, "used_tc")) *value = c->used_tc ? 1 : 0;
     else if (!strcmp(key, "used_pair")) *value = c->used_pair ? 1 : 0;
+    else if (!strcmp(key, "tc_k")) *value = (int64_t)c->tc_kf;
     else if (!strcmp(key, "tc_ok")) *value = c->tc_ok ? 1 : 0;
     else if (!strncmp(key, "time_", 5)) {
         // time_seed_ns / time_scan_ns / time_merge_ns / time_final_ns: summed over the

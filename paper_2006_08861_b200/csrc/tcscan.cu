@@ -276,6 +276,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 if (!(a.dbg & 2)) {
 #pragma unroll
                     for (int k = 0; k < kK / 16; ++k) {
+                        if (k * 16 >= (int)a.kf) break;
                         if (kPair) mma_f16_pair(d, desc_sw128_kmajor(qm + k * 32), desc_sw128_kmajor(rm + k * 32), idesc, k > 0 ? 1u : 0u);
                         else mma_f16(d, desc_sw128_kmajor(qm + k * 32), desc_sw128_kmajor(rm + k * 32), idesc, k > 0 ? 1u : 0u);
                     }
@@ -604,7 +605,7 @@ namespace ol {
 // the bits of a non-negative float); the largest |f| (fp16 range check).  rows is a
 // multiple of 32 (tile-padded), so every warp owns whole blocks.
 __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int kc, uint64_t rows,
-                                    __half *plane, float2 *blk, uint32_t *stat) {
+                                    __half *plane, float2 *blk, uint32_t *stat, int kf) {
     uint32_t lmax = 0, lnorm = 0;
     for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
          r += (uint64_t)gridDim.x * blockDim.x) {
@@ -616,11 +617,12 @@ __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int 
             const float f1 = k + 1 < kc ? coarse[coarse_off(r, k + 1, kc)] : fine[r * (kK - kc) + (k + 1 - kc)];
             const __half h0 = __float2half_rn(f0), h1 = __float2half_rn(f1);
             dst[k / 2] = __halves2half2(h0, h1);
+            amax = fmaxf(amax, fmaxf(fabsf(f0), fabsf(f1)));
+            if (k >= kf) continue;   // the filter's terms cover dimensions < kf only
             const double d0 = (double)f0 - (double)__half2float(h0), d1 = (double)f1 - (double)__half2float(h1);
             n2 += (double)f0 * f0 + (double)f1 * f1;
             e2 += d0 * d0 + d1 * d1;
             h2 += (double)__half2float(h0) * __half2float(h0) + (double)__half2float(h1) * __half2float(h1);
-            amax = fmaxf(amax, fmaxf(fabsf(f0), fabsf(f1)));
         }
         // the double sums carry relative error < 2^-45; the (1 -+ 2^-20) factors cover it
         float x = 0.5f * __double2float_rd(n2 * (1.0 - 1.0 / 1048576.0));   // halving is exact
@@ -646,11 +648,11 @@ __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int 
 }
 
 cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, uint64_t rows, void *plane,
-                                float2 *blk, uint32_t *stat, cudaStream_t s) {
+                                float2 *blk, uint32_t *stat, uint32_t kf, cudaStream_t s) {
     uint64_t blocks = (rows + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks == 0) blocks = 1;
-    tc_prep_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(coarse, fine, kc, rows, (__half *)plane, blk, stat);
+    tc_prep_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(coarse, fine, kc, rows, (__half *)plane, blk, stat, (int)kf);
     return cudaGetLastError();
 }
 
@@ -658,7 +660,7 @@ cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, 
 // RU e_q), and the batch norm bound in *nq_max (+inf if a value leaves the fp16
 // range: see force_all).  One warp per frame.
 __global__ void tc_prep_queries_kernel(const float *q, uint32_t nq, uint32_t nq_pad, __half *q16,
-                                       float4 *qmeta, uint32_t *nq_max, uint32_t *force_all) {
+                                       float4 *qmeta, uint32_t *nq_max, uint32_t *force_all, uint32_t kf) {
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= nq_pad) return;
     __half2 *dst = reinterpret_cast<__half2 *>(q16 + (size_t)w * kK);
@@ -676,8 +678,9 @@ __global__ void tc_prep_queries_kernel(const float *q, uint32_t nq, uint32_t nq_
     const __half h0 = __float2half_rn(f0), h1 = __float2half_rn(f1);
     dst[lane] = __halves2half2(h0, h1);
     const double d0 = (double)f0 - (double)__half2float(h0), d1 = (double)f1 - (double)__half2float(h1);
-    double n2 = (double)f0 * f0 + (double)f1 * f1, e2 = d0 * d0 + d1 * d1;
-    double h2 = (double)__half2float(h0) * __half2float(h0) + (double)__half2float(h1) * __half2float(h1);
+    const bool in = 2 * lane < kf;   // the filter's terms cover dimensions < kf only
+    double n2 = in ? (double)f0 * f0 + (double)f1 * f1 : 0.0, e2 = in ? d0 * d0 + d1 * d1 : 0.0;
+    double h2 = in ? (double)__half2float(h0) * __half2float(h0) + (double)__half2float(h1) * __half2float(h1) : 0.0;
     for (int o = 16; o; o >>= 1) {
         n2 += __shfl_xor_sync(0xffffffffu, n2, o);
         e2 += __shfl_xor_sync(0xffffffffu, e2, o);
@@ -693,9 +696,9 @@ __global__ void tc_prep_queries_kernel(const float *q, uint32_t nq, uint32_t nq_
 }
 
 cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float4 *qmeta,
-                                   uint32_t *bounds, cudaStream_t s) {
+                                   uint32_t *bounds, uint32_t kf, cudaStream_t s) {
     const uint32_t threads = 256, blocks = (nq_pad * 32 + threads - 1) / threads;
-    tc_prep_queries_kernel<<<blocks, threads, 0, s>>>(q, nq, nq_pad, (__half *)q16, qmeta, bounds + 2, bounds + 3);
+    tc_prep_queries_kernel<<<blocks, threads, 0, s>>>(q, nq, nq_pad, (__half *)q16, qmeta, bounds + 2, bounds + 3, kf);
     return cudaGetLastError();
 }
 

@@ -155,3 +155,25 @@ def test_tc_cta_pairs(nq):
     assert np.array_equal(outs[0], outs[1])
     ref = oracle.retrieve(sizes, F, C, Q, 15)
     assert_candidates_equal(outs[0], ref, f"pair nq={nq}")
+
+
+@pytest.mark.parametrize("kf", [16, 32, 48])
+def test_tc_prefix_filter(kf):
+    """Option tc_k: the certified filter on the first kf dimensions only (the prefix
+    distance is a lower bound of the full one, so pruning stays exact): bit-identical
+    to the oracle and to the full-K filter, with pairs and single CTAs."""
+    spec = synthgen.Spec(seed=36, n_floors=2, paths=5, frames_per_path=1207)
+    F, C = synthgen.db_host(spec)
+    Q = synthgen.render_host(spec, synthgen.query_points(spec, 25, 600))["desc"][:, None, :]
+    sizes = [7000, F.shape[0] - 7000]
+    ref = oracle.retrieve(sizes, F, C, Q, 15)
+    for pair in (2, 0):
+        e = _run(F, C, sizes, Q, 15, 1, agg=False, pair=pair, tc_k=kf)
+        assert e.stat("used_tc") == 1
+        assert_candidates_equal(e.topk(), ref, f"tc_k={kf} pair={pair}")
+    rng = np.random.default_rng(kf)
+    G = (rng.standard_normal((5000, 64)) * 2).astype(np.float32)      # signed, non-unit
+    CG = rng.integers(0, 500, (5000, 2)).astype(np.int32)
+    QG = (G[rng.integers(0, 5000, 200)] + rng.standard_normal((200, 64)).astype(np.float32) * 0.05)[:, None, :]
+    e = _run(G, CG, [5000], QG, 15, 1, agg=False, tc_k=kf)
+    assert_candidates_equal(e.topk(), oracle.retrieve([5000], G, CG, QG, 15), f"tc_k={kf} signed")

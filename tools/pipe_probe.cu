@@ -1,7 +1,9 @@
 // pipe_probe.cu -- the tensor-core scan's TMEM pipeline in isolation: one thread issues
 // (optionally) 4 MMAs 128x256x16 per tile into a double-buffered accumulator and commits
 // tfull[buf]; epilogue warps wait tfull, tcgen05.ld their share, arrive tempty[buf].
-// Compares "all warps on every tile" with "two groups on alternate tiles".
+// Compares "all warps on every tile" with "two groups on alternate tiles" (2 x 256-column
+// buffers, each warp two 64-column chunks) and "two groups on alternate tiles over 4 x 128-column
+// buffers" (design 2: each warp one 64-column chunk, released before its math); kst = K/16 steps.
 // nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a tools/pipe_probe.cu -o tools/pipe_probe -lcuda
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -19,7 +21,7 @@ struct Smem {
 
 // design 0: E warps all load every tile, each 256*4/E columns... (E = 16: 64 columns)
 // design 1: two groups of E/2 warps on alternate tiles, each warp 128 columns in two 64-col chunks
-__global__ void probe(int design, int E, int mma, int tiles, int NB, long long *out) {
+__global__ void __launch_bounds__(544, 1) probe(int design, int E, int mma, int tiles, int NB, int kst, long long *out) {
     const int TC = 512 / NB;   // columns per tile
     extern __shared__ __align__(1024) unsigned char raw[];
     Smem &s = *reinterpret_cast<Smem *>(raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u));
@@ -46,7 +48,7 @@ __global__ void probe(int design, int E, int mma, int tiles, int NB, long long *
                 if (t >= NB) mbar_wait(&s.tempty[buf], ((t / NB) - 1) & 1);
                 tc_fence_after();
                 if (mma)
-                    for (int k = 0; k < 4; ++k)
+                    for (int k = 0; k < kst; ++k)
                         mma_f16(tmem + buf * TC, desc_sw128_kmajor(smem_u32(s.a) + k * 32),
                                 desc_sw128_kmajor(smem_u32(s.b) + k * 32), idesc, k ? 1u : 0u);
                 mma_commit(&s.tfull[buf]);
@@ -73,6 +75,19 @@ __global__ void probe(int design, int E, int mma, int tiles, int NB, long long *
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s.tempty[buf]);
+            }
+        } else if (design == 2) {
+            const int grp = ew / (E / 2), half = (ew % (E / 2)) >> 2;   // E/2 = 8: half in {0, 1}
+            for (int t = grp; t < tiles; t += 2) {
+                const int buf = t % NB;
+                mbar_wait(&s.tfull[buf], (t / NB) & 1);
+                tc_fence_after();
+                uint32_t v0[32], v1[32];
+                const uint32_t ta = tmem + ((q * 32) << 16) + buf * TC + half * 64;
+                tmem_ld32(ta, v0); tmem_ld32(ta + 32, v1);
+                tmem_ld_wait_regs(v0); reg_fence(v1);
+                tc_fence_before(); __syncwarp(); if (lane == 0) mbar_arrive(&s.tempty[buf]);
+                for (int j = 0; j < 32; ++j) acc += v0[j] ^ v1[j];
             }
         } else {
             const int grp = ew / (E / 2), half = (ew % (E / 2)) >> 2;   // E/2 = 8: half in {0, 1}
@@ -104,20 +119,23 @@ int main() {
     size_t smem = sizeof(Smem) + 1024;
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int tiles = 400;
-    for (int mma = 0; mma <= 1; ++mma)
-        for (int NB : {2, 4})
-        for (int design = 0; design <= 1; ++design)
-            for (int E : {8, 16}) {
-                if (design == 1 && (E != 16 || NB != 2)) continue;
-                if (NB == 4 && E == 16 && design == 0) {}   // 32 cols per warp at NB=4, E=16
+    for (int kst : {4, 2, 1})
+        for (int mma = 0; mma <= 1; ++mma) {
+            if (!mma && kst < 4) continue;
+            for (int design = 0; design <= 2; ++design) {
+                const int NB = design == 2 ? 4 : 2, E = 16;
                 long long h[4] = {0, 0, 0, 0};
-                probe<<<1, 32 * (1 + E), smem>>>(design, E, mma, tiles, NB, d);
-                cudaError_t e = cudaDeviceSynchronize();
+                probe<<<1, 32 * (1 + E), smem>>>(design, E, mma, tiles, NB, kst, d);
+                cudaError_t e = cudaGetLastError();
+                if (e == cudaSuccess) e = cudaDeviceSynchronize();
                 if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
-                cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
-                printf("mma=%d NB=%d %-26s E=%2d: %.0f cycles per 128 KB of accumulators\n", mma, NB,
-                       design == 0 ? "all warps every tile" : "two groups, alternate tiles", E,
-                       (double)h[0] / tiles * 2 / NB);
+                e = cudaMemcpy(h, d, 32, cudaMemcpyDeviceToHost);
+                if (e != cudaSuccess) { printf("copy error %s\n", cudaGetErrorString(e)); return 1; }
+                printf("[total %lld, mma thread %lld] ", h[0], h[1]);
+                printf("K=%d mma=%d NB=%d %-34s: %.0f cycles per 128 KB of accumulators\n", kst * 16, mma, NB,
+                       design == 0 ? "all 16 warps on every tile" : design == 1 ? "two groups, 2 x 256-col buffers" : "two groups, 4 x 128-col buffers",
+                       (double)h[0] / tiles * NB / 2);   // NB = 4: tiles of 64 KB
             }
+        }
     return 0;
 }

@@ -8,6 +8,8 @@ dev = torch.device("cuda", 0)
 F, C = synthgen.db_device(spec, 0, n, dev)
 Q, _ = synthgen.render_device(spec, synthgen.query_points(spec, 4242, 1024), dev)
 e = ol.Engine(0)
+import os
+if os.environ.get("TCK"): e.set_option("tc_k", int(os.environ["TCK"]))
 e.upload(F, C, [n], spec.grid())
 if os.environ.get("CHUNK"): e.set_option("chunk", int(os.environ["CHUNK"]))
 if os.environ.get("PAIR"): e.set_option("pair", int(os.environ["PAIR"]))
