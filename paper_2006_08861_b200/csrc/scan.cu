@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(kSeedThreads, 2) tau_seed_kernel(SeedArgs a) {
 
 // Two-kernel seed (the default): every sample row is loaded ONCE per block and scored
 // against 32 frames (rows in registers, frames broadcast from shared memory), the
-// exact chains' acc bits go to a scratch array, then one warp per (frame, subspace,
+// exact chains' acc bits go to a scratch array, then one CTA per (frame, subspace,
 // split) radix-selects the N-th smallest from it (8-bit digits from the top, warp-
 // aggregated shared-memory histograms).  Same sample rows and the same values as
 // tau_seed_kernel, far fewer bytes: rows are reused across frames.
@@ -673,55 +673,61 @@ __global__ void __launch_bounds__(256) seed_acc_kernel(SeedArgs a) {
     }
 }
 
+// One CTA per (frame, subspace, split): the N-th smallest of its S acc bits by radix
+// select (4 passes of 8-bit digits, most significant first).  Every pass streams the
+// job's values from L2 with all of a thread's loads in flight; counts go to one shared
+// histogram (warp-aggregated increments: equal digits of a warp add once); a CTA-wide
+// scan of the 256 counts finds the digit holding the k-th value.
 __global__ void __launch_bounds__(256) seed_select_kernel(SeedArgs a) {
-    __shared__ uint32_t hist[8][256];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t job = blockIdx.x * 8 + w;   // (frame, subspace, split)
-    if (job >= a.nq * a.n_sub * a.splits) return;   // (whole warps only: warp-level sync below)
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t wsum[8];
+    __shared__ uint32_t pick[2];
+    const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+    const uint32_t job = blockIdx.x;   // (frame, subspace, split)
     const uint32_t i = (job / a.splits) % a.n_sub, q = (job / a.splits) / a.n_sub;
     const uint32_t S = (uint32_t)min((uint64_t)a.samples, a.subs[i].count);
-    if (S < a.N) return;
+    if (S < a.N) return;   // (uniform over the CTA)
     const uint32_t *v = a.scratch + (size_t)job * a.samples;
     uint32_t prefix = 0, pmask = 0, k = a.N;
     for (int shift = 24; shift >= 0; shift -= 8) {
-        for (int b = lane; b < 256; b += 32) hist[w][b] = 0;
-        __syncwarp();
-        for (uint32_t t0 = 0; t0 < S; t0 += 32) {
-            const uint32_t t = t0 + lane;
-            const uint32_t x = t < S ? __ldcg(v + t) : 0u;
-            const bool in = t < S && (x & pmask) == prefix;
-            const uint32_t d = in ? (x >> shift) & 255u : 256u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            if (in && lane == __ffs(peers) - 1) atomicAdd(&hist[w][d], (uint32_t)__popc(peers));
-        }
-        __syncwarp();
-        uint32_t c[8], tot = 0;
+        hist[tid] = 0;
+        __syncthreads();
+        for (uint32_t t0 = 0; t0 < S; t0 += 8 * 256) {
+            uint32_t x[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) { c[j] = hist[w][lane * 8 + j]; tot += c[j]; }
-        uint32_t incl = tot;
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t t = t0 + j * 256 + tid;
+                x[j] = t < S ? __ldcg(v + t) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t t = t0 + j * 256 + tid;
+                const bool in = t < S && (x[j] & pmask) == prefix;
+                const uint32_t d = in ? (x[j] >> shift) & 255u : 256u;
+                const uint32_t peers = __match_any_sync(0xffffffffu, d);
+                if (in && lane == __ffs(peers) - 1) atomicAdd(&hist[d], (uint32_t)__popc(peers));
+            }
+        }
+        __syncthreads();
+        // inclusive scan of the 256 counts (thread = digit)
+        const uint32_t c = hist[tid];
+        uint32_t incl = c;
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        uint32_t below = incl - tot, digit = 0, under = 0;
-        const bool here = below < k && k <= incl;
-        if (here) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (below + c[j] >= k) { digit = lane * 8 + j; under = below; break; }
-                below += c[j];
-            }
-        }
-        const int src = __ffs(__ballot_sync(0xffffffffu, here)) - 1;
-        digit = __shfl_sync(0xffffffffu, digit, src);
-        under = __shfl_sync(0xffffffffu, under, src);
-        prefix |= digit << shift;
+        if (lane == 31) wsum[w] = incl;
+        __syncthreads();
+        for (int j = 0; j < w; ++j) incl += wsum[j];
+        if (incl - c < k && k <= incl) { pick[0] = (uint32_t)tid; pick[1] = incl - c; }
+        __syncthreads();
+        prefix |= pick[0] << shift;
         pmask |= 255u << shift;
-        k -= under;
-        __syncwarp();
+        k -= pick[1];
+        __syncthreads();
     }
     // every split's N-th smallest is an upper bound of the true N-th: keep the least
-    if (lane == 0) atomicMin(&a.tau0[(size_t)q * a.n_sub + i], prefix);
+    if (tid == 0) atomicMin(&a.tau0[(size_t)q * a.n_sub + i], prefix);
 }
 
 cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s) {
@@ -739,7 +745,7 @@ cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s) {
         }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        seed_select_kernel<<<(a.nq * a.n_sub * a.splits + 7) / 8, 256, 0, s>>>(a);
+        seed_select_kernel<<<a.nq * a.n_sub * a.splits, 256, 0, s>>>(a);
         return cudaGetLastError();
     }
     const unsigned grid = a.nq * a.n_sub * a.splits;
