@@ -17,7 +17,6 @@ constexpr int kScanWarps = kScanThreads / 32;
 constexpr int kMaxQT = 64;            // query frames per scan CTA
 constexpr int kAggMax = 8192;         // candidates per bundle in the aggregation kernel
 constexpr u64 kPadKey = ~0ull;
-constexpr uint32_t kTauSlots = 32;
 constexpr uint32_t kInfBits = 0x7F800000u;  // +inf: "no threshold yet"
 
 // Coarse plane layout: tiles of 32 rows; inside a tile, 16-byte columns of 4
@@ -105,8 +104,6 @@ struct TcScanArgs {
                                   // [4] max RU||f||^2/2 bits, [5] max RU e_f bits (bound pre-pass)
     float nf_max;                 // database norm bound
     uint32_t *g_tau;              // [nq][n_sub] acc bits: seeded, then shared running minimum
-    u64 *slots;                   // [nq][n_sub][kTauSlots] or null: per row class (frame index mod
-                                  // kTauSlots) the least exact key any CTA scored (N <= kTauSlots)
     const float *queries;         // fp32 [nq][K]
     const float *coarse, *fine;   // fp32 planes (exact re-scoring)
     u64 *partial;                 // [nq][n_items][N] (unused by the bound pre-pass)

@@ -70,7 +70,6 @@ struct ol_ctx {
     // per-query buffers
     float *q_d = nullptr; size_t q_cap = 0;
     uint32_t *tau0_d = nullptr; size_t tau_cap = 0;
-    u64 *slots_d = nullptr; size_t slots_cap = 0;
     u64 *partial_d = nullptr; size_t partial_cap = 0;
     uint4 *payload_d = nullptr; size_t payload_cap = 0;
     uint4 *final_d = nullptr; size_t final_cap = 0;
@@ -96,7 +95,6 @@ struct ol_ctx {
     int64_t opt_tc_min_frames = 12;   // measured C4: 8 frames scan2 1.37 vs tc 1.77 ms; 16 frames 2.42 vs 1.77
     int64_t opt_tc_debug = 0;
     int64_t opt_seed_kernel = 1;   // 1: two-kernel seed (rows reused across frames), 0: one CTA per (frame, subspace)
-    int64_t opt_tau_slots = 1;   // tensor-core path: class-minimum thresholds shared by all CTAs (N <= 32)
     int64_t opt_tc_k = 0;        // tensor-core filter dimensions (prefix; applied at upload); 0 = auto
     uint32_t tc_kf = 64;
     int64_t opt_tc_seed = 0;     // tensor-core path: 1 = seed thresholds with the bound pre-pass (off: the exact sampled seed is as fast at C4 and tighter at C3)
@@ -239,7 +237,7 @@ void ol_destroy(ol_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     free_db(c);
-    cudaFree(c->items_d); cudaFree(c->seed_scratch); cudaFree(c->sitems_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->slots_d); cudaFree(c->partial_d);
+    cudaFree(c->items_d); cudaFree(c->seed_scratch); cudaFree(c->sitems_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
     cudaFree(c->prefix_d); cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
     cudaFree(c->flags_d); cudaFree(c->stat_d); cudaFree(c->tcstat_d); cudaFree(c->prof_d);
@@ -625,13 +623,6 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         a.pair = pair ? 1u : 0u;
         a.items = c->items_d; a.blk = c->blk; a.n_blk = (uint32_t)(c->rows_pad / 32); a.qmeta = c->qmeta; a.bounds = c->tcstat_d; a.nf_max = c->nf_max;
         a.g_tau = c->tau0_d; a.queries = q; a.coarse = c->coarse; a.fine = c->fine;
-        a.slots = nullptr;
-        if (c->opt_tau_slots && N <= kTauSlots && !(c->opt_tc_debug & 64)) {
-            OL_CUDA(c, grow(&c->slots_d, &c->slots_cap, (size_t)nq * c->n_sub * kTauSlots));
-            OL_LAUNCH(c, launch_fill_u32(reinterpret_cast<uint32_t *>(c->slots_d),
-                                         (uint64_t)nq * c->n_sub * kTauSlots * 2, 0xFFFFFFFFu, c->stream));
-            a.slots = c->slots_d;
-        }
         a.partial = c->partial_d; a.stat_survivors = c->stat_d; a.stat_flagged = c->stat_d + 1;
         a.nq = nq; a.n_items = n_items; a.n_qblocks = n_qblocks; a.qb = qb; a.n_sub = c->n_sub;
         a.kf = c->tc_kf;
@@ -997,7 +988,6 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "pair")) { if (v < 0 || v > 2) goto bad; c->opt_pair = v; }
     else if (!strcmp(key, "cluster")) { if (v != 1 && v != 2 && v != 4 && v != 8) goto bad; c->opt_cluster = v; }
     else if (!strcmp(key, "seed_kernel")) { if (v != 0 && v != 1) goto bad; c->opt_seed_kernel = v; }
-    else if (!strcmp(key, "tau_slots")) { if (v != 0 && v != 1) goto bad; c->opt_tau_slots = v; }
     else if (!strcmp(key, "tc_k")) { if (v != 0 && (v < 16 || v > 64 || v % 16)) goto bad; c->opt_tc_k = v; }
     else if (!strcmp(key, "tc_seed")) { if (v < 0 || v > 2) goto bad; c->opt_tc_seed = v; }
     else if (!strcmp(key, "scan2")) { if (v < 0 || v > 2) goto bad; c->opt_scan2 = v; }

@@ -513,7 +513,6 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 const bool act = sidx < total;
                 uint32_t col = 0xFFFFFFFFu;
                 u64 key = kPadKey;
-                bool slot_up = false;
                 if (act) {
                     uint32_t k = sidx - (e_incl - e_cnt), wsel = 0, w = w0;
                     if (k >= (uint32_t)__popc(w)) { k -= __popc(w); w = w1; wsel = 1;
@@ -539,28 +538,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                         acc = chain_step_tc(acc, x.z, f[k4].z); acc = chain_step_tc(acc, x.w, f[k4].w);
                     }
                     key = ((u64)__float_as_uint(acc) << 32) | (u64)(it.frame_begin + rl);
-                    // the least key of the row's class, over every CTA (rows of distinct classes
-                    // are distinct rows)
-                    if (a.slots)
-                        slot_up = atomicMin(&a.slots[((size_t)(q0 + col) * a.n_sub + it.sub) * kTauSlots +
-                                                     ((it.frame_begin + rl) & (kTauSlots - 1))], key) > key;
                     if (!(key < lists[(size_t)col * N + N - 1])) key = kPadKey;   // cannot enter the list
-                }
-                // a class minimum improved: the N-th smallest of the kTauSlots class minima is
-                // the acc of one of N distinct rows, so it bounds the N-th best acc of the
-                // (frame, subspace) over the whole database -- a threshold every CTA can use
-                // long before any one CTA's own list holds N rows that good
-                for (uint32_t upd = __ballot_sync(0xffffffffu, slot_up); upd;) {
-                    const uint32_t f = __shfl_sync(0xffffffffu, col, __ffs(upd) - 1);
-                    upd &= ~__ballot_sync(0xffffffffu, slot_up && col == f);
-                    const u64 v = __ldcg(&a.slots[((size_t)(q0 + f) * a.n_sub + it.sub) * kTauSlots + lane]);
-                    uint32_t less = 0;
-                    for (int j = 0; j < 32; ++j) less += __shfl_sync(0xffffffffu, v, j) < v;
-                    if (less == N - 1 && v != kPadKey) {
-                        const uint32_t tb = (uint32_t)(v >> 32);
-                        atomicMin(&s.tau[f], tb);
-                        atomicMin(&a.g_tau[(size_t)(q0 + f) * a.n_sub + it.sub], tb);
-                    }
                 }
                 // insert the keys into their frames' sorted lists: lanes of distinct frames in
                 // parallel, lanes sharing a frame one after another (match groups)

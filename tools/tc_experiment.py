@@ -14,7 +14,6 @@ e.upload(F, C, [n], spec.grid())
 import os
 if os.environ.get("CHUNK"): e.set_option("chunk", int(os.environ["CHUNK"]))
 if os.environ.get("PAIR"): e.set_option("pair", int(os.environ["PAIR"]))
-if os.environ.get("SLOTS"): e.set_option("tau_slots", int(os.environ["SLOTS"]))
 Q3 = Q.view(-1, 1, 64)
 for dbg in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else '0,1,4')]:
     e.set_option("tc_debug", dbg)
