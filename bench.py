@@ -283,7 +283,8 @@ def run_omniloc(a):
         # sustained measured figure is the denominator
         tc_peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
         achieved = flops / scan_s / 1e12 if scan_s > 0 else None
-        alg_bytes = rows_local * (64 * 2 + 8)          # fp16 row + 8 B bound terms, once
+        pw = 32 if kf == 32 else 64                    # fp16 plane row width (halves)
+        alg_bytes = rows_local * pw * 2 + rows_local // 32 * 8   # fp16 rows + 8 B bound terms per 32 rows, once
         # traffic: DRAM bytes of one launch from the committed `ncu --set full` capture of this
         # workload (profiles/r01_tcscan_ncu.json), only when this run is that workload
         traffic = None
@@ -357,8 +358,13 @@ def run_omniloc(a):
         for k in ("seed", "merge", "final"):
             eng.stat(f"time_{k}_ns")
         eng.set_option("time_kernels", 0)
-        gbs = rows_local * kc * 4 / sscan / 1e9
-        out["small_batch"] = {"query_frames": b2, "ms_per_step": sms, "queries_per_s": b2 / (sms / 1e3),
+        if eng.stat("used_tc"):   # tensor-core filter: the fp16 plane (64-B rows at tc_k = 32) + block terms
+            pw2 = 32 if eng.stat("tc_k") == 32 else 64
+            sbytes, skern = rows_local * pw2 * 2 + rows_local // 32 * 8, "tcscan_kernel"
+        else:                     # CUDA-core scan: the fp32 coarse plane
+            sbytes, skern = rows_local * kc * 4, f"scan2_kernel<{kc}>"
+        gbs = sbytes / sscan / 1e9
+        out["small_batch"] = {"query_frames": b2, "kernel": skern, "ms_per_step": sms, "queries_per_s": b2 / (sms / 1e3),
                               "scan_ms": sscan * 1e3, "scan_hbm_gbs": gbs, "hbm_peak_gbs": hbm_peak,
                               "hbm_frac": gbs / hbm_peak, "hbm_frac_vs_8tbs": gbs / 8000.0}
 
@@ -381,7 +387,8 @@ def run_omniloc(a):
         for k in ("seed", "merge", "final"):
             eng.stat(f"time_{k}_ns")
         eng.set_option("time_kernels", 0)
-        mbytes = rows_local * (64 * 2) + rows_local // 32 * 8   # fp16 rows + block bound terms
+        pw = 32 if eng.stat("tc_k") == 32 else 64
+        mbytes = rows_local * pw * 2 + rows_local // 32 * 8   # fp16 rows + block bound terms
         mg = mbytes / mscan / 1e9
         out["mid_batch"] = {"query_frames": b3, "kernel": "tcscan_kernel", "ms_per_step": mms,
                             "queries_per_s": b3 / (mms / 1e3), "scan_ms": mscan * 1e3, "scan_hbm_gbs": mg,

@@ -116,6 +116,7 @@ struct TcScanArgs {
     uint32_t dbg;                 // profiling only: 1 skip epilogue math, 2 skip MMA, 4 skip cold path, ...
     uint32_t n_blk;               // rows_pad / 32
     uint32_t kf;                  // filter on the first kf of K dimensions (16..64, multiple of 16)
+    uint32_t pw;                  // fp16 plane / frame row width in halves: 64 (128-B rows, SW128) or 32 (kf = 32: 64-B rows, SW64)
     unsigned long long *prof;     // [16] per-role cycle counters when dbg & 32 (profiling only)
 };
 
@@ -134,9 +135,9 @@ struct ShiftArgs {
 // launchers (return cudaGetLastError())
 cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s);
 cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, uint64_t rows, void *plane,
-                                float2 *blk, uint32_t *stat, uint32_t kf, cudaStream_t s);
+                                float2 *blk, uint32_t *stat, uint32_t kf, uint32_t pw, cudaStream_t s);
 cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float4 *qmeta,
-                                   uint32_t *bounds, uint32_t kf, cudaStream_t s);
+                                   uint32_t *bounds, uint32_t kf, uint32_t pw, cudaStream_t s);
 cudaError_t launch_fill_u32(uint32_t *p, uint64_t n, uint32_t v, cudaStream_t s);
 size_t extract_smem_bytes(uint32_t W);
 cudaError_t launch_extract(const double *prof, uint64_t n, uint32_t W, float *out32, double *out64,
@@ -146,8 +147,8 @@ bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_ro
                  uint32_t row_stride = 1);
 cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q, const TcScanArgs &a, int grid,
                           cudaStream_t s);
-size_t tc_smem_bytes(uint32_t qb, uint32_t N, uint32_t stages);
-bool tc_shape(uint32_t N, uint32_t nq, uint32_t *qb, uint32_t *stages);
+size_t tc_smem_bytes(uint32_t qb, uint32_t N, uint32_t stages, uint32_t pw);
+bool tc_shape(uint32_t N, uint32_t nq, uint32_t pw, uint32_t *qb, uint32_t *stages);
 cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s);
 cudaError_t launch_scan(int kc, const ScanArgs &a, size_t smem, int grid, cudaStream_t s);
 size_t scan_smem_bytes(uint32_t qt, uint32_t N);

@@ -92,11 +92,14 @@ struct ol_ctx {
     // options
     int64_t opt_chunk = 0, opt_qtile = 0, opt_tau_seed = 1, opt_ctas = 0, opt_time = 0, opt_seed_samples = 4096;
     int64_t opt_tc = -1;         // tensor-core filter: -1 auto (>= tc_min_frames frames), 0 off, 1 always
-    int64_t opt_tc_min_frames = 12;   // measured C4: 8 frames scan2 1.37 vs tc 1.77 ms; 16 frames 2.42 vs 1.77
+    int64_t opt_tc_min_frames = 0;    // 0 = automatic: 6 with the 64-B plane (kf = 32), else 12.  Measured C4:
+                                      // 64-B plane: 4 frames scan2 0.94 vs tc 1.02 ms, 8: 1.28 vs 1.02;
+                                      // 128-B plane: 8 frames 1.37 vs 1.77, 16: 2.42 vs 1.77
     int64_t opt_tc_debug = 0;
     int64_t opt_seed_kernel = 1;   // 1: two-kernel seed (rows reused across frames), 0: one CTA per (frame, subspace)
     int64_t opt_tc_k = 0;        // tensor-core filter dimensions (prefix; applied at upload); 0 = auto
     uint32_t tc_kf = 64;
+    uint32_t tc_pw = 64;         // fp16 plane row width (halves): 32 when tc_kf = 32
     int64_t opt_tc_seed = 0;     // tensor-core path: 1 = seed thresholds with the bound pre-pass (off: the exact sampled seed is as fast at C4 and tighter at C3)
     int64_t opt_cluster = 1;     // tensor-core path: CTAs per cluster (query blocks sharing rows)
     int64_t opt_pair = 1;        // tensor-core path: CTA pairs (cta_group::2, M = 256): 0 off, 1 auto, 2 on
@@ -373,9 +376,6 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
                                    c->stream));
         OL_CUDA(c, launch_pad_rows(c->subs_d, ns, kc, c->coarse, c->fine, c->stream));
         if (c->opt_tc != 0) {
-            OL_CUDA(c, cudaMalloc(&c->plane16, sizeof(uint16_t) * rows_pad * OL_K));
-            OL_CUDA(c, cudaMalloc((void **)&c->blk, sizeof(float2) * (rows_pad / 32)));
-            OL_CUDA(c, cudaMemsetAsync(c->tcstat_d, 0, 8 * sizeof(uint32_t), c->stream));
             // the filter on the first 32 dimensions halves the MMA work but passes more
             // pairs to the exact path (1,024 frames: 20M rows 2.87 vs 2.72 ms, 35M 4.15 vs
             // 4.39, 50M 5.57 vs 6.09, 100M 9.88 vs 12.0 ms for 32 vs 64): automatic mode takes
@@ -383,8 +383,14 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
             uint64_t minc = ~0ull;
             for (auto &sb : subs) minc = sb.count < minc ? sb.count : minc;
             c->tc_kf = c->opt_tc_k ? (uint32_t)c->opt_tc_k : (minc >= 32000000ull ? 32u : 64u);
+            // kf = 32: the plane holds only those dimensions (64-B rows): half the bytes
+            // streamed, and what makes few-frame batches HBM-bound at half the time
+            c->tc_pw = c->tc_kf == 32 ? 32u : 64u;
+            OL_CUDA(c, cudaMalloc(&c->plane16, sizeof(uint16_t) * rows_pad * c->tc_pw));
+            OL_CUDA(c, cudaMalloc((void **)&c->blk, sizeof(float2) * (rows_pad / 32)));
+            OL_CUDA(c, cudaMemsetAsync(c->tcstat_d, 0, 8 * sizeof(uint32_t), c->stream));
             OL_CUDA(c, launch_tc_prep_rows(c->coarse, c->fine, kc, rows_pad, c->plane16, c->blk, c->tcstat_d,
-                                           c->tc_kf, c->stream));
+                                           c->tc_kf, c->tc_pw, c->stream));
         }
     }
     OL_CUDA(c, cudaMemcpyAsync(c->subs_d, subs.data(), sizeof(SubInfo) * ns, cudaMemcpyHostToDevice,
@@ -399,13 +405,13 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
         // fp16 operands need |f| and ||f||^2 / 2 inside the fp16 range, and the row count
         // must fit a TMA coordinate
         c->tc_ok = std::isfinite(nf) && amax < 65000.f && nf < 300.f && rows_pad < (1ull << 31) &&
-                   make_tc_map(&c->map_rows, c->plane16, rows_pad, 256, OL_K) &&
-                   make_tc_map(&c->map_rows_half, c->plane16, rows_pad, 128, OL_K);
+                   make_tc_map(&c->map_rows, c->plane16, rows_pad, 256, c->tc_pw) &&
+                   make_tc_map(&c->map_rows_half, c->plane16, rows_pad, 128, c->tc_pw);
         // bound pre-pass view: ~128k sampled rows, at most 1/64 of the database
         uint64_t S = 64;
         while (rows_pad / (S * 2) >= 131072) S *= 2;
         c->seed_stride = c->tc_ok && rows_pad / S >= 2048 &&
-                         make_tc_map(&c->map_srows, c->plane16, rows_pad, 256, OL_K, (uint32_t)S) ? (uint32_t)S : 0;
+                         make_tc_map(&c->map_srows, c->plane16, rows_pad, 256, c->tc_pw, (uint32_t)S) ? (uint32_t)S : 0;
     }
     c->subs = subs;
     c->rows_pad = rows_pad;
@@ -510,8 +516,9 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     // launch shape (results never depend on it): tensor-core filter or CUDA-core
     // scan, query tile, chunk size
     uint32_t tc_qb = 0, tc_stages = 0;
-    const bool use_tc = c->tc_ok && (c->opt_tc == 1 || (c->opt_tc == -1 && nq >= (uint32_t)c->opt_tc_min_frames)) &&
-                        tc_shape(N, nq, &tc_qb, &tc_stages);
+    const uint32_t min_frames = c->opt_tc_min_frames ? (uint32_t)c->opt_tc_min_frames : (c->tc_pw == 32 ? 6u : 12u);
+    const bool use_tc = c->tc_ok && (c->opt_tc == 1 || (c->opt_tc == -1 && nq >= min_frames)) &&
+                        tc_shape(N, nq, c->tc_pw, &tc_qb, &tc_stages);
     uint32_t qt = c->opt_qtile > 0 ? (uint32_t)c->opt_qtile : kMaxQT;
     while (qt > 8 && scan_smem_bytes(qt, N) > 150 * 1024) qt -= 8;
     if (qt > kMaxQT) qt = kMaxQT;
@@ -608,14 +615,14 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
                           (nqb1 % 2 == 0 || nqb1 >= 5);
         const uint32_t qb = tc_qb, n_qblocks = ((nq + qb - 1) / qb + (pair ? 1 : 0)) / (pair ? 2 : 1) * (pair ? 2 : 1),
                        nq_pad = n_qblocks * qb;
-        OL_CUDA(c, grow((uint16_t **)&c->q16, &c->q16_cap, (size_t)nq_pad * OL_K));
+        OL_CUDA(c, grow((uint16_t **)&c->q16, &c->q16_cap, (size_t)nq_pad * c->tc_pw));
         OL_CUDA(c, grow(&c->qmeta, &c->qmeta_cap, nq));
         OL_CUDA(c, cudaMemsetAsync(c->tcstat_d + 2, 0, 2 * sizeof(uint32_t), c->stream));
-        OL_LAUNCH(c, launch_tc_prep_queries(q, nq, nq_pad, c->q16, c->qmeta, c->tcstat_d, c->tc_kf, c->stream));
+        OL_LAUNCH(c, launch_tc_prep_queries(q, nq, nq_pad, c->q16, c->qmeta, c->tcstat_d, c->tc_kf, c->tc_pw, c->stream));
         if ((!seed || (tc_seed && c->opt_tc_seed != 2)) && !(c->opt_tc_debug & 64))
             OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
         CUtensorMap map_q;
-        if (!make_tc_map(&map_q, c->q16, nq_pad, qb, OL_K))
+        if (!make_tc_map(&map_q, c->q16, nq_pad, qb, c->tc_pw))
             return fail(c, OL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
         TcScanArgs a;
         a.bound = 0;
@@ -625,7 +632,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         a.g_tau = c->tau0_d; a.queries = q; a.coarse = c->coarse; a.fine = c->fine;
         a.partial = c->partial_d; a.stat_survivors = c->stat_d; a.stat_flagged = c->stat_d + 1;
         a.nq = nq; a.n_items = n_items; a.n_qblocks = n_qblocks; a.qb = qb; a.n_sub = c->n_sub;
-        a.kf = c->tc_kf;
+        a.kf = c->tc_kf; a.pw = c->tc_pw;
         a.N = N; a.kc = (uint32_t)c->kc; a.stages = tc_stages; a.dbg = (uint32_t)c->opt_tc_debug; a.prof = c->prof_d;
         if (a.dbg & 32) OL_CUDA(c, cudaMemsetAsync(c->prof_d, 0, 64 * sizeof(unsigned long long), c->stream));
         if (tc_seed && !(a.dbg & 64)) {
@@ -991,7 +998,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "tc_k")) { if (v != 0 && (v < 16 || v > 64 || v % 16)) goto bad; c->opt_tc_k = v; }
     else if (!strcmp(key, "tc_seed")) { if (v < 0 || v > 2) goto bad; c->opt_tc_seed = v; }
     else if (!strcmp(key, "scan2")) { if (v < 0 || v > 2) goto bad; c->opt_scan2 = v; }
-    else if (!strcmp(key, "tc_min_frames")) { if (v < 1) goto bad; c->opt_tc_min_frames = v; }
+    else if (!strcmp(key, "tc_min_frames")) { if (v < 0) goto bad; c->opt_tc_min_frames = v; }
     else if (!strcmp(key, "tc_debug")) { if (v < 0 || v > 1023) goto bad; c->opt_tc_debug = v; }
     else return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown option '%s'", key);
     return OL_OK;

@@ -238,6 +238,17 @@ __device__ __forceinline__ uint64_t desc_sw32_kmajor(uint32_t smem_addr) {
     d |= (uint64_t)6 << 61;
     return d;
 }
+// Same, 64-byte swizzle (rows of 32 fp16 = 64 B, 8-row atoms of 512 B): layout
+// SWIZZLE_64B = 4, SBO = 512 >> 4.  Tile base 512-byte aligned.
+__device__ __forceinline__ uint64_t desc_sw64_kmajor(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(512 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;
+    return d;
+}
 // Instruction descriptor, kind::f16: D fp32 (c_format 1 at [4,6)), A/B fp16
 // (format 0), both K-major, N>>3 at [17,23), M>>4 at [24,29).
 __host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N) {

@@ -53,7 +53,7 @@ constexpr int kEv = 32;                 // survivor event ring entries per exact
                                         // pairs, whose epilogues are coupled: 16/32/64 -> 32)
 constexpr int kTrackMax = 16;           // largest N of the bound pre-pass (register list)
 constexpr float kTauInflate = 1.0f + 1.0f / 131072.0f;   // 1 + 2^-17
-constexpr uint32_t kStageBytes = kTileRows * kK * 2;   // 32 KB
+constexpr uint32_t kStageBytesMax = kTileRows * kK * 2;   // 32 KB (pw = 64; 16 KB at pw = 32)
 
 struct TcSmem {
     alignas(1024) __half qm[kQB * kK];      // frames, main K (SW128), resident
@@ -70,14 +70,14 @@ struct TcSmem {
     uint32_t seq[kExactWarps][kEv];
     unsigned int prod[kExactWarps], closed_at[kExactWarps];
     int closed;
-    // dynamic, 1024-aligned: n_stages x rows [256][64] fp16 SW128, then the top-N
-    // lists u64 [qb][N]
+    // dynamic, 1024-aligned: n_stages x rows [256][pw] fp16 (SW128 / SW64), then the
+    // top-N lists u64 [qb][N]
 };
 
 static __host__ __device__ constexpr size_t tc_fixed_bytes() { return (sizeof(TcSmem) + 1023) / 1024 * 1024; }
 
-size_t tc_smem_bytes(uint32_t qb, uint32_t N, uint32_t stages) {
-    return 1024 + tc_fixed_bytes() + (size_t)stages * kStageBytes + sizeof(u64) * qb * N;
+size_t tc_smem_bytes(uint32_t qb, uint32_t N, uint32_t stages, uint32_t pw) {
+    return 1024 + tc_fixed_bytes() + (size_t)stages * (kTileRows * pw * 2) + sizeof(u64) * qb * N;
 }
 
 __device__ __forceinline__ float chain_step_tc(float acc, float q, float f) {
@@ -179,7 +179,8 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     TcSmem &s = *reinterpret_cast<TcSmem *>(base);
     unsigned char *stage0 = base + tc_fixed_bytes();
     const uint32_t n_stages = a.stages;
-    u64 *lists = reinterpret_cast<u64 *>(stage0 + (size_t)n_stages * kStageBytes);
+    const uint32_t stage_bytes = kTileRows * a.pw * 2;
+    u64 *lists = reinterpret_cast<u64 *>(stage0 + (size_t)n_stages * stage_bytes);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t item_id = blockIdx.x / a.n_qblocks;
     const uint32_t qblk = blockIdx.x % a.n_qblocks;
@@ -234,24 +235,24 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             if (kPair) {
                 // each CTA loads its own frames and its half of each row tile; the bytes of
                 // both complete on the leader's barriers
-                if (rank == 0) mbar_expect_tx(&s.qbar, 2 * a.qb * kK * (uint32_t)sizeof(__half));
+                if (rank == 0) mbar_expect_tx(&s.qbar, 2 * a.qb * a.pw * (uint32_t)sizeof(__half));
                 tma_load_2d_pair(s.qm, &map_q, &s.qbar, 0, (int)q0);
             } else {
-                mbar_expect_tx(&s.qbar, a.qb * kK * (uint32_t)sizeof(__half));
+                mbar_expect_tx(&s.qbar, a.qb * a.pw * (uint32_t)sizeof(__half));
                 tma_load_2d(s.qm, &map_q, &s.qbar, 0, (int)q0);
             }
             for (uint32_t t = 0; t < n_tiles; ++t) {
                 const uint32_t st = t % n_stages;
                 if (t >= n_stages) mbar_wait_sleep(&s.empty[st], ((t / n_stages) - 1) & 1);
-                unsigned char *sb = stage0 + (size_t)st * kStageBytes;
+                unsigned char *sb = stage0 + (size_t)st * stage_bytes;
                 const int r0 = (int)(it.row_begin + (uint64_t)t * kTileRows);
                 if (kPair) {
-                    if (rank == 0) mbar_expect_tx(&s.full[st], kStageBytes);   // both halves
+                    if (rank == 0) mbar_expect_tx(&s.full[st], stage_bytes);   // both halves
                     tma_load_2d_pair(sb, &map_rows, &s.full[st], 0, r0 + (int)rank * (kTileRows / 2));
                     continue;
                 }
                 if ((a.dbg & 128) && t >= n_stages) { mbar_arrive(&s.full[st]); continue; }   // profiling: stale rows
-                mbar_expect_tx(&s.full[st], kStageBytes);
+                mbar_expect_tx(&s.full[st], stage_bytes);
                 tma_load_2d(sb, &map_rows, &s.full[st], 0, r0);
             }
         }
@@ -271,14 +272,17 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 if (t >= kTBufs) mbar_wait_sleep(&s.tempty[buf], ((t / kTBufs) - 1) & 1);
                 if (prof) { pw_full += c1 - c0; pw_tempty += clock64() - c1; }
                 tc_fence_after();
-                const uint32_t rm = smem_u32(stage0 + (size_t)st * kStageBytes);
+                const uint32_t rm = smem_u32(stage0 + (size_t)st * stage_bytes);
                 const uint32_t d = tmem + buf * kTileRows;
                 if (!(a.dbg & 2)) {
 #pragma unroll
                     for (int k = 0; k < kK / 16; ++k) {
                         if (k * 16 >= (int)a.kf) break;
-                        if (kPair) mma_f16_pair(d, desc_sw128_kmajor(qm + k * 32), desc_sw128_kmajor(rm + k * 32), idesc, k > 0 ? 1u : 0u);
-                        else mma_f16(d, desc_sw128_kmajor(qm + k * 32), desc_sw128_kmajor(rm + k * 32), idesc, k > 0 ? 1u : 0u);
+                        // (K-step k: +32 B along the rows, inside the swizzle atom)
+                        const uint64_t da = a.pw == 64 ? desc_sw128_kmajor(qm + k * 32) : desc_sw64_kmajor(qm + k * 32);
+                        const uint64_t db = a.pw == 64 ? desc_sw128_kmajor(rm + k * 32) : desc_sw64_kmajor(rm + k * 32);
+                        if (kPair) mma_f16_pair(d, da, db, idesc, k > 0 ? 1u : 0u);
+                        else mma_f16(d, da, db, idesc, k > 0 ? 1u : 0u);
                     }
                 }
                 if (kPair) { mma_commit_pair(&s.empty[st], 3); mma_commit_pair(&s.tfull[buf], 3); }
@@ -342,6 +346,12 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             const long long w1 = prof ? clock64() : 0;
             if (prof && lane == 0) ew_tfull += w1 - w0;
             tc_fence_after();
+            if (quarter * 32 >= qn) {   // no frame in this warp's TMEM lanes (few frames, a pair's padding CTA)
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) { if (kPair) mbar_arrive_leader(&s.tempty[buf]); else mbar_arrive(&s.tempty[buf]); }
+                return;
+            }
             const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * kTileRows + half * 128;
             const float h = 0.5f * (alpha - __uint_as_float(s.tau[ql]) * kTauInflate);
             // lanes 0..3 (block c = lane): gB <= g_r on the block
@@ -605,18 +615,18 @@ namespace ol {
 // the bits of a non-negative float); the largest |f| (fp16 range check).  rows is a
 // multiple of 32 (tile-padded), so every warp owns whole blocks.
 __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int kc, uint64_t rows,
-                                    __half *plane, float2 *blk, uint32_t *stat, int kf) {
+                                    __half *plane, float2 *blk, uint32_t *stat, int kf, int pw) {
     uint32_t lmax = 0, lnorm = 0;
     for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
          r += (uint64_t)gridDim.x * blockDim.x) {
         double n2 = 0, e2 = 0, h2 = 0;
         float amax = 0.f;
-        __half2 *dst = reinterpret_cast<__half2 *>(plane + r * kK);
+        __half2 *dst = reinterpret_cast<__half2 *>(plane + r * pw);
         for (int k = 0; k < kK; k += 2) {
             const float f0 = k < kc ? coarse[coarse_off(r, k, kc)] : fine[r * (kK - kc) + (k - kc)];
             const float f1 = k + 1 < kc ? coarse[coarse_off(r, k + 1, kc)] : fine[r * (kK - kc) + (k + 1 - kc)];
             const __half h0 = __float2half_rn(f0), h1 = __float2half_rn(f1);
-            dst[k / 2] = __halves2half2(h0, h1);
+            if (k < pw) dst[k / 2] = __halves2half2(h0, h1);
             amax = fmaxf(amax, fmaxf(fabsf(f0), fabsf(f1)));
             if (k >= kf) continue;   // the filter's terms cover dimensions < kf only
             const double d0 = (double)f0 - (double)__half2float(h0), d1 = (double)f1 - (double)__half2float(h1);
@@ -648,11 +658,11 @@ __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int 
 }
 
 cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, uint64_t rows, void *plane,
-                                float2 *blk, uint32_t *stat, uint32_t kf, cudaStream_t s) {
+                                float2 *blk, uint32_t *stat, uint32_t kf, uint32_t pw, cudaStream_t s) {
     uint64_t blocks = (rows + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks == 0) blocks = 1;
-    tc_prep_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(coarse, fine, kc, rows, (__half *)plane, blk, stat, (int)kf);
+    tc_prep_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(coarse, fine, kc, rows, (__half *)plane, blk, stat, (int)kf, (int)pw);
     return cudaGetLastError();
 }
 
@@ -660,23 +670,24 @@ cudaError_t launch_tc_prep_rows(const float *coarse, const float *fine, int kc, 
 // RU e_q), and the batch norm bound in *nq_max (+inf if a value leaves the fp16
 // range: see force_all).  One warp per frame.
 __global__ void tc_prep_queries_kernel(const float *q, uint32_t nq, uint32_t nq_pad, __half *q16,
-                                       float4 *qmeta, uint32_t *nq_max, uint32_t *force_all, uint32_t kf) {
+                                       float4 *qmeta, uint32_t *nq_max, uint32_t *force_all, uint32_t kf, uint32_t pw) {
     const uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= nq_pad) return;
-    __half2 *dst = reinterpret_cast<__half2 *>(q16 + (size_t)w * kK);
+    __half2 *dst = reinterpret_cast<__half2 *>(q16 + (size_t)w * pw);
     const __half2 zero = __halves2half2(__float2half(0.f), __float2half(0.f));
-    if (w >= nq) { dst[lane] = zero; return; }
+    const bool wr = 2 * lane < pw;   // lanes holding a plane column
+    if (w >= nq) { if (wr) dst[lane] = zero; return; }
     const float f0 = q[(size_t)w * kK + 2 * lane], f1 = q[(size_t)w * kK + 2 * lane + 1];
     // a value outside the fp16 range (or non-finite): this batch is scored exactly
     // for every pair (force_all); the frame's fp16 operand is zeroed to stay finite
     const bool bad = __any_sync(0xffffffffu, !(fabsf(f0) < 65000.f && fabsf(f1) < 65000.f));
     if (bad) {
-        dst[lane] = zero;
+        if (wr) dst[lane] = zero;
         if (lane == 0) { qmeta[w] = make_float4(0.f, 0.f, 0.f, 0.f); atomicOr(force_all, 1u); }
         return;
     }
     const __half h0 = __float2half_rn(f0), h1 = __float2half_rn(f1);
-    dst[lane] = __halves2half2(h0, h1);
+    if (wr) dst[lane] = __halves2half2(h0, h1);
     const double d0 = (double)f0 - (double)__half2float(h0), d1 = (double)f1 - (double)__half2float(h1);
     const bool in = 2 * lane < kf;   // the filter's terms cover dimensions < kf only
     double n2 = in ? (double)f0 * f0 + (double)f1 * f1 : 0.0, e2 = in ? d0 * d0 + d1 * d1 : 0.0;
@@ -696,9 +707,9 @@ __global__ void tc_prep_queries_kernel(const float *q, uint32_t nq, uint32_t nq_
 }
 
 cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad, void *q16, float4 *qmeta,
-                                   uint32_t *bounds, uint32_t kf, cudaStream_t s) {
+                                   uint32_t *bounds, uint32_t kf, uint32_t pw, cudaStream_t s) {
     const uint32_t threads = 256, blocks = (nq_pad * 32 + threads - 1) / threads;
-    tc_prep_queries_kernel<<<blocks, threads, 0, s>>>(q, nq, nq_pad, (__half *)q16, qmeta, bounds + 2, bounds + 3, kf);
+    tc_prep_queries_kernel<<<blocks, threads, 0, s>>>(q, nq, nq_pad, (__half *)q16, qmeta, bounds + 2, bounds + 3, kf, pw);
     return cudaGetLastError();
 }
 
@@ -739,13 +750,14 @@ bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_ro
     cuuint32_t box[2] = {width, box_rows};
     cuuint32_t estr[2] = {1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, width == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE,
+              width == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : width == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q, const TcScanArgs &a, int grid,
                           cudaStream_t s) {
-    const size_t smem = tc_smem_bytes(a.qb, a.N, a.stages);
+    const size_t smem = tc_smem_bytes(a.qb, a.N, a.stages, a.pw);
     const bool prof = (a.dbg & 32) != 0;
     const bool pair = a.pair && !a.bound;
     auto kern = a.bound ? (prof ? tcscan_kernel<true, true, false> : tcscan_kernel<false, true, false>)
@@ -779,12 +791,12 @@ cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q,
 
 // Frames per CTA (128 or 256) and pipeline depth for top-N lists of N: the lists
 // share the 227 KB of shared memory with the resident frames and the row stages.
-bool tc_shape(uint32_t N, uint32_t nq, uint32_t *qb, uint32_t *stages) {
+bool tc_shape(uint32_t N, uint32_t nq, uint32_t pw, uint32_t *qb, uint32_t *stages) {
     (void)nq;
-    const size_t budget = 227 * 1024;
+    const size_t budget = 227 * 1024, sb = kTileRows * pw * 2;
     const size_t fixed = 1024 + tc_fixed_bytes() + sizeof(u64) * kQB * N;
-    if (fixed + 2 * kStageBytes > budget) return false;
-    const uint32_t st = (uint32_t)((budget - fixed) / kStageBytes);
+    if (fixed + 2 * sb > budget) return false;
+    const uint32_t st = (uint32_t)((budget - fixed) / sb);
     *qb = kQB;
     *stages = st > (uint32_t)kMaxStages ? (uint32_t)kMaxStages : st;
     return true;

@@ -1,3 +1,2 @@
-# seed sample count (new CTA-per-job select) vs seed time, survivors, scan at C4
-timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "seed or tau" 2>&1 | tail -2
-timeout 600 python tools/seed_experiment.py 100000000 4096,8192,16384,32768,4096 2>&1 | tail -5
+timeout 600 python bench.py > gpurun_out/bench_pw.json 2> gpurun_out/bench_pw.err; echo "bench rc=$?"
+python -c "import json; d=json.load(open('gpurun_out/bench_pw.json')); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['roofline']['per_launch']['hbm_gbs'], d['e2e']['value'], d['stages_ms'], d['clocks']); print(d['small_batch']); print(d['mid_batch'])"
