@@ -46,6 +46,8 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="omniloc", choices=["omniloc", "reference"])
     ap.add_argument("--config", default="C4")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="cross-GPU merge at N > 1: NCCL all-gather + merge kernel, or one peer-memory kernel")
     ap.add_argument("--batch", type=int, default=0, help="query frames per step (0 = config)")
     ap.add_argument("--coarse-k", type=int, default=16)
     ap.add_argument("--no-e2e", action="store_true")
@@ -215,7 +217,7 @@ def run_omniloc(a):
     if world > 1:
         import torch.distributed as dist
         group = dist.group.WORLD
-    eng = ol.Engine(local, coarse_k=a.coarse_k, process_group=group)
+    eng = ol.Engine(local, coarse_k=a.coarse_k, process_group=group, exchange=a.exchange)
     t0 = time.time()
     eng.upload(F, C, [n_total], spec.grid())
     torch.cuda.synchronize()
@@ -328,6 +330,7 @@ def run_omniloc(a):
            "config": {"workload": a.config, "db_entries": n_total, "query_frames": B, "M": 1, "N": cfg.N,
                       "aggregate": True, "top_c": 10, "toler_per": 0.2, "radius_m": 3.0,
                       "coarse_k": a.coarse_k, "parallelism": f"db-shard{world}",
+                      "exchange": (a.exchange if world > 1 else None),
                       "l2": "inputs larger than L2 (coarse plane %.1f GB/rank)" % (rows_local * kc * 4 / 1e9)},
            "comparisons_per_sec": cps,
            "stages_ms": {"tau_seed": seed_ns / 1e6, "scan": scan_ns / 1e6, "merge": merge_ns / 1e6,
@@ -503,7 +506,7 @@ def run_streaming(a):
     if world > 1:
         import torch.distributed as dist
         group = dist.group.WORLD
-    eng = ol.Engine(local, coarse_k=16, process_group=group)
+    eng = ol.Engine(local, coarse_k=16, process_group=group, exchange=a.exchange)
     eng.upload(F, C, [n_total], spec.grid())
     del F, C
     params = ol.Params(N=cfg.N)

@@ -196,6 +196,39 @@ OL_API ol_status ol_payload_copy(ol_ctx *ctx, void *dst);
  * NOT_READY (no preceding ol_query), INVALID_ARGUMENT (world mismatch), CUDA. */
 OL_API ol_status ol_finalize(ol_ctx *ctx, const void *gathered, int32_t world);
 
+/* ---- peer-memory exchange (NVLink / NVSwitch, one node) --------------------
+ * The cross-GPU step as one kernel instead of an NCCL all-gather +
+ * ol_finalize: every rank stores its payload straight into slot `rank` of every
+ * rank's mailbox over peer memory, signals each receiver (system-scope release
+ * counter), waits for all ranks' slots in its own mailbox and merges them into
+ * the global top-N; then candidates and estimates as ol_finalize.  Identical
+ * results to ol_finalize on every rank.  Collective: every rank calls each of
+ * these in the same order. */
+
+/* Allocate this rank's mailbox (2 x world x max_payload_bytes + 256 B of
+ * counters; max_payload_bytes >= the ol_payload bytes of every later query, a
+ * multiple of 16) and write its CUDA IPC handle (64 bytes) to handle_out (may be
+ * NULL when the caller emulates ranks on one GPU).  1 <= world <= 8.  Replaces
+ * an earlier mailbox.  Errors: INVALID_ARGUMENT, OOM, CUDA. */
+OL_API ol_status ol_p2p_open(ol_ctx *ctx, int32_t world, int32_t rank, uint64_t max_payload_bytes,
+                             void *handle_out);
+
+/* Open every other rank's mailbox: `handles` = world x 64 bytes in rank order
+ * (the caller all-gathers the ol_p2p_open handles, e.g. over torch.distributed).
+ * Errors: NOT_READY (no ol_p2p_open), INVALID_ARGUMENT, CUDA (IPC unavailable). */
+OL_API ol_status ol_p2p_connect(ol_ctx *ctx, const void *handles);
+
+/* After ol_query on every rank: exchange + merge + candidates (+ estimates), one
+ * cooperative kernel for the exchange and merge, stream-ordered.  Errors:
+ * NOT_READY (no query / not connected), INVALID_ARGUMENT (payload larger than
+ * the mailbox), CUDA. */
+OL_API ol_status ol_p2p_finalize(ol_ctx *ctx);
+
+/* Tests: the same kernel emulating `world` ranks on ONE GPU as one cooperative
+ * launch (group g = rank g, mailboxes local): ctxs[g] opened with
+ * ol_p2p_open(world, g, ..), each after its ol_query.  Synchronises. */
+OL_API ol_status ol_p2p_emulate(ol_ctx **ctxs, int32_t world);
+
 /* ---- results ------------------------------------------------------------- */
 
 /* Number of candidates of the last query: n_bundles * M * sum_i min(N, |n_i|). */

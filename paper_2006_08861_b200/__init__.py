@@ -94,6 +94,10 @@ def lib():
             "ol_payload": ([P, ctypes.POINTER(P), ctypes.POINTER(u64)], i32),
             "ol_payload_copy": ([P, P], i32),
             "ol_finalize": ([P, P, i32], i32),
+            "ol_p2p_open": ([P, i32, i32, u64, P], i32),
+            "ol_p2p_connect": ([P, P], i32),
+            "ol_p2p_finalize": ([P], i32),
+            "ol_p2p_emulate": ([ctypes.POINTER(P), i32], i32),
             "ol_candidate_count": ([P, ctypes.POINTER(u64)], i32),
             "ol_get_topk": ([P, P, u64, ctypes.POINTER(u64)], i32),
             "ol_topk_device": ([P, ctypes.POINTER(P), ctypes.POINTER(u64)], i32),
@@ -160,11 +164,13 @@ class Engine:
     """One context on one GPU: upload a (sharded) feature database, query bundles.
 
     ``process_group``: a torch.distributed group whose ranks each hold one shard;
-    the per-rank top-N payloads are all-gathered through it (NCCL on GPUs).
+    the per-rank top-N payloads are all-gathered through it (NCCL on GPUs), or, with
+    ``exchange="p2p"``, exchanged and merged by one kernel over NVLink peer memory
+    (mailbox handles are exchanged through the group once).
     """
 
     def __init__(self, device: int = 0, coarse_k: int = 16, process_group=None, rank: int | None = None,
-                 world: int | None = None, stream=None):
+                 world: int | None = None, stream=None, exchange: str = "nccl"):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("omniloc needs a CUDA device (no CPU fallback)")
@@ -186,6 +192,10 @@ class Engine:
         self.params = Params()
         self._gather_buf = None
         self._payload_buf = None
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' or 'p2p'")
+        self.exchange = exchange
+        self._mbox_bytes = 0
 
     def _stream_ptr(self):
         if self._stream is not None:
@@ -258,8 +268,37 @@ class Engine:
         self._ck(lib().ol_query(self._h, B, Mq, ctypes.c_void_p(fp), fdev, ctypes.byref(pc),
                                 1 if aggregate else 0))
         if self.world > 1 and exchange:
-            self._exchange_and_finalize()
+            if self.exchange == "p2p":
+                self._p2p_finalize()
+            else:
+                self._exchange_and_finalize()
         self._last = (B, Mq, p, aggregate)
+
+    # ---------------------------------------------------------------- peer-memory exchange
+    def p2p_open(self, world: int, rank: int, max_payload_bytes: int) -> bytes:
+        """Allocate this rank's mailbox; returns its 64-byte CUDA IPC handle."""
+        h = ctypes.create_string_buffer(64)
+        self._ck(lib().ol_p2p_open(self._h, world, rank, max_payload_bytes, h))
+        self._mbox_bytes = max_payload_bytes
+        return h.raw
+
+    def p2p_connect(self, handles: bytes):
+        """Open the peers' mailboxes (world x 64 bytes, rank order)."""
+        buf = ctypes.create_string_buffer(handles, len(handles))
+        self._ck(lib().ol_p2p_connect(self._h, buf))
+
+    def _p2p_finalize(self):
+        """Cross-GPU merge over peer memory (one kernel: push to every rank's mailbox,
+        signal, wait, merge).  The first call, and a payload larger than the mailbox,
+        (re)build the mailboxes collectively: every rank has the same payload size."""
+        ptr = ctypes.c_void_p(); nbytes = ctypes.c_uint64()
+        self._ck(lib().ol_payload(self._h, ctypes.byref(ptr), ctypes.byref(nbytes)))
+        if nbytes.value > self._mbox_bytes:
+            cap = max(nbytes.value, 2 * self._mbox_bytes)
+            cap = (cap + 15) // 16 * 16
+            handle = self.p2p_open(self.world, self.rank, cap)
+            self.p2p_connect(gather_handles(handle, self.group))
+        self._ck(lib().ol_p2p_finalize(self._h))
 
     def _exchange_and_finalize(self):
         """Cross-GPU merge: all-gather the per-rank top-N payloads
@@ -402,6 +441,23 @@ class Engine:
         v = ctypes.c_int64()
         self._ck(lib().ol_get_stat(self._h, key.encode(), ctypes.byref(v)))
         return v.value
+
+
+def gather_handles(handle: bytes, group=None) -> bytes:
+    """All ranks' 64-byte mailbox handles, concatenated in rank order (host objects
+    over the process group: gloo or NCCL)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, handle, group=group)
+    return b"".join(out)
+
+
+def p2p_emulate(engines):
+    """Tests: the peer-memory exchange kernel emulating len(engines) ranks on one GPU
+    as one cooperative launch (engine g = rank g, each after p2p_open(world, g, ..)
+    and its own query(..., exchange=False))."""
+    arr = (ctypes.c_void_p * len(engines))(*[e._h.value for e in engines])
+    _check(lib().ol_p2p_emulate(arr, len(engines)), engines[0]._h)
 
 
 def exchange_payloads(src, dst, group=None):

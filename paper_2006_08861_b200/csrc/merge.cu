@@ -71,11 +71,9 @@ cudaError_t launch_merge_chunks(const MergeArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// One warp per (query, subspace): the N smallest of world sorted lists.
-__global__ void __launch_bounds__(kMergeThreads) merge_ranks_kernel(RankMergeArgs a) {
-    const uint32_t gw = (blockIdx.x * kMergeThreads + threadIdx.x) / 32;
-    const int lane = threadIdx.x & 31;
-    if (gw >= a.nq * a.n_sub) return;
+// One warp, one (query, subspace) gw: the N smallest of world sorted lists gathered
+// back to back ([world][nq][n_sub][N] records).
+__device__ void merge_rank_lists(RankMergeArgs a, uint32_t gw, int lane) {
     const size_t per_rank = (size_t)a.nq * a.n_sub * a.N;
     const size_t base = (size_t)gw * a.N;
     const uint32_t nk = a.world * a.N;
@@ -85,7 +83,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_ranks_kernel(RankMergeArg
         u64 best = kPadKey;
         uint32_t bt = 0xFFFFFFFFu;
         for (uint32_t t = lane; t < nk; t += 32) {
-            const uint4 rec = a.gathered[(t / a.N) * per_rank + base + (t % a.N)];
+            const uint4 rec = __ldcg(&a.gathered[(t / a.N) * per_rank + base + (t % a.N)]);   // (L2: peers write it)
             const u64 v = ((u64)rec.x << 32) | rec.y;
             if ((!have_last || v > last) && v < best) { best = v; bt = t; }
         }
@@ -98,10 +96,72 @@ __global__ void __launch_bounds__(kMergeThreads) merge_ranks_kernel(RankMergeArg
             break;
         }
         if (lane == __ffs(owner) - 1)
-            a.records[base + r] = a.gathered[(bt / a.N) * per_rank + base + (bt % a.N)];
+            a.records[base + r] = __ldcg(&a.gathered[(bt / a.N) * per_rank + base + (bt % a.N)]);
         last = wbest;
         have_last = true;
     }
+}
+
+__global__ void __launch_bounds__(kMergeThreads) merge_ranks_kernel(RankMergeArgs a) {
+    const uint32_t gw = (blockIdx.x * kMergeThreads + threadIdx.x) / 32;
+    if (gw >= a.nq * a.n_sub) return;
+    merge_rank_lists(a, gw, threadIdx.x & 31);
+}
+
+// ---------------------------------------------------------------- peer-memory exchange
+// The cross-GPU step as ONE kernel over NVLink/NVSwitch peer memory (§8e: all-gather of
+// the per-rank top-N, then the N smallest of W·N): every block of rank r stores its
+// slice of r's payload into slot r of every rank's mailbox (plain st.global to peer
+// addresses opened by CUDA IPC), fences system-wide and adds 1 to the receiver's
+// counter flag[r]; then waits until its own mailbox holds every rank's slices
+// (flag[s] = epoch x blocks for all s, acquire loads) and merges its share of the
+// (frame, subspace) lists straight out of the mailbox.  Mailbox data is double-
+// buffered by epoch parity: a rank can only push epoch e + 1 after every rank has
+// pushed e, i.e. after every rank finished merging e - 1.  Blocks wait on blocks of
+// their own grid, so the launch is cooperative (co-resident).  Groups: with G > 1
+// the grid emulates G ranks on one GPU (tests), group g acting as rank rank0 + g.
+__global__ void __launch_bounds__(kMergeThreads) xchg_merge_kernel(XchgArgs a) {
+    const uint32_t g = blockIdx.x / a.blocks, b = blockIdx.x % a.blocks;
+    const uint32_t r = a.rank0 + g;
+    const size_t P = (size_t)a.nq * a.n_sub * a.N;            // records per rank
+    const size_t lo = P * b / a.blocks, hi = P * (b + 1) / a.blocks;
+    const uint32_t par = a.epoch & 1u;
+    const uint4 *src = a.payload[g];
+    for (uint32_t p = 0; p < a.world; ++p) {
+        uint4 *dst = a.mbox[p] + ((size_t)par * a.world + r) * P;
+        for (size_t t = lo + threadIdx.x; t < hi; t += blockDim.x) dst[t] = src[t];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x < a.world) {
+        unsigned int *f = a.flag[threadIdx.x] + r;
+        asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(f) : "memory");
+    }
+    const unsigned int target = a.epoch * a.blocks;
+    if (threadIdx.x < a.world) {
+        const unsigned int *f = a.flag[r] + threadIdx.x;
+        unsigned int v;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            if ((int)(v - target) >= 0) break;
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+    RankMergeArgs m;
+    m.gathered = a.mbox[r] + (size_t)par * a.world * P;
+    m.records = a.records[g];
+    m.nq = a.nq; m.n_sub = a.n_sub; m.N = a.N; m.world = a.world;
+    const uint32_t warps = a.blocks * (kMergeThreads / 32);
+    for (uint32_t gw = b * (kMergeThreads / 32) + threadIdx.x / 32; gw < a.nq * a.n_sub; gw += warps)
+        merge_rank_lists(m, gw, threadIdx.x & 31);
+}
+
+cudaError_t launch_xchg_merge(const XchgArgs &a, uint32_t groups, cudaStream_t s) {
+    XchgArgs x = a;
+    void *args[] = {&x};
+    return cudaLaunchCooperativeKernel((const void *)xchg_merge_kernel, dim3(groups * a.blocks), dim3(kMergeThreads),
+                                       args, 0, s);
 }
 
 cudaError_t launch_merge_ranks(const RankMergeArgs &a, cudaStream_t s) {

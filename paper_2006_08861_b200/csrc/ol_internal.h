@@ -78,6 +78,18 @@ struct RankMergeArgs {
     uint32_t nq, n_sub, N, world;
 };
 
+constexpr int kXchgMax = 8;   // ranks of the peer-memory exchange (one NVSwitch node)
+constexpr uint32_t kXchgBlocks = 16;   // blocks per rank of xchg_merge_kernel (fixed: the arrival counters count them)
+
+struct XchgArgs {
+    uint4 *mbox[kXchgMax];        // rank p's mailbox records: [2 (epoch parity)][world][nq][n_sub][N]
+    unsigned int *flag[kXchgMax]; // rank p's arrival counters [world] (monotonic: epoch x blocks)
+    const uint4 *payload[kXchgMax];   // group g's own payload [nq][n_sub][N]
+    uint4 *records[kXchgMax];     // group g's merged output [nq][n_sub][N]
+    uint32_t rank0, world, blocks, epoch;
+    uint32_t nq, n_sub, N;
+};
+
 struct CandArgs {
     const uint4 *records;        // [nq][n_sub][N]
     const uint32_t *sub_prefix;  // [n_sub+1] prefix of min(N, |n_i|)
@@ -158,6 +170,7 @@ cudaError_t launch_scan3(int kc, const ScanArgs &a, size_t smem, int grid, cudaS
 size_t scan3_smem_bytes(uint32_t qt, uint32_t N, int kc);
 cudaError_t launch_merge_chunks(const MergeArgs &a, cudaStream_t s);
 cudaError_t launch_merge_ranks(const RankMergeArgs &a, cudaStream_t s);
+cudaError_t launch_xchg_merge(const XchgArgs &a, uint32_t groups, cudaStream_t s);
 cudaError_t launch_candidates(const CandArgs &a, cudaStream_t s);
 cudaError_t launch_aggregate(const AggArgs &a, cudaStream_t s);
 cudaError_t launch_check_finite(const float *p, uint64_t n, int *flag, cudaStream_t s);

@@ -73,6 +73,14 @@ struct ol_ctx {
     u64 *partial_d = nullptr; size_t partial_cap = 0;
     uint4 *payload_d = nullptr; size_t payload_cap = 0;
     uint4 *final_d = nullptr; size_t final_cap = 0;
+    // peer-memory exchange (ol_p2p_*): this rank's mailbox (256 B of arrival counters, then
+    // 2 x world x max_records records) and the peers' mailboxes opened by CUDA IPC
+    unsigned char *mbox_d = nullptr;
+    void *peer_base[kXchgMax] = {};
+    uint64_t mbox_records = 0;
+    int p2p_world = 0, p2p_rank = 0;
+    bool p2p_ready = false;
+    uint32_t p2p_epoch = 0;
     ol_candidate *cand_d = nullptr; size_t cand_cap = 0;
     ol_estimate *est_d = nullptr; size_t est_cap = 0;
     uint32_t *prefix_d = nullptr; size_t prefix_cap = 0;
@@ -235,6 +243,16 @@ ol_status ol_create(const ol_config *cfg, ol_ctx **out) {
     return OL_OK;
 }
 
+// release the peer mailboxes opened by IPC and this rank's own
+static void p2p_close(ol_ctx *c) {
+    for (int p = 0; p < kXchgMax; ++p)
+        if (c->peer_base[p]) { cudaIpcCloseMemHandle(c->peer_base[p]); c->peer_base[p] = nullptr; }
+    cudaFree(c->mbox_d);
+    c->mbox_d = nullptr;
+    c->p2p_ready = false;
+    c->p2p_world = 0;
+}
+
 void ol_destroy(ol_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
@@ -242,6 +260,7 @@ void ol_destroy(ol_ctx *c) {
     free_db(c);
     cudaFree(c->items_d); cudaFree(c->seed_scratch); cudaFree(c->sitems_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
+    p2p_close(c);
     cudaFree(c->prefix_d); cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
     cudaFree(c->flags_d); cudaFree(c->stat_d); cudaFree(c->tcstat_d); cudaFree(c->prof_d);
     cudaFree(c->q16); cudaFree(c->qmeta); cudaFree(c->qprof_d); cudaFree(c->shift_keys);
@@ -703,6 +722,8 @@ ol_status ol_payload_copy(ol_ctx *c, void *dst) {
     return OL_OK;
 }
 
+static ol_status finalize_tail(ol_ctx *c, const uint4 *rec);
+
 static ol_status finalize_impl(ol_ctx *c, const uint4 *gathered, int world) {
     TimeScope ts(c, ol_ctx::T_FINAL);
     const uint32_t nq = c->nq, N = c->N, ns = c->n_sub;
@@ -715,6 +736,12 @@ static ol_status finalize_impl(ol_ctx *c, const uint4 *gathered, int world) {
         OL_LAUNCH(c, launch_merge_ranks(ra, c->stream));
         rec = c->final_d;
     }
+    return finalize_tail(c, rec);
+}
+
+// candidates (and estimates) from the merged records [nq][n_sub][N]
+static ol_status finalize_tail(ol_ctx *c, const uint4 *rec) {
+    const uint32_t nq = c->nq, N = c->N, ns = c->n_sub;
     if (c->prefix_N != N) {
         std::vector<uint32_t> prefix(ns + 1, 0);
         for (uint32_t i = 0; i < ns; ++i)
@@ -751,6 +778,104 @@ ol_status ol_finalize(ol_ctx *c, const void *gathered, int32_t world) {
         return fail(c, OL_ERR_INVALID_ARGUMENT, "world %d != context world %d", world, c->world);
     OL_CUDA(c, cudaSetDevice(c->device));
     return finalize_impl(c, (const uint4 *)gathered, world);
+}
+
+// ---------------------------------------------------------------- peer-memory exchange
+static constexpr size_t kMboxFlagBytes = 256;
+
+ol_status ol_p2p_open(ol_ctx *c, int32_t world, int32_t rank, uint64_t max_payload_bytes, void *handle_out) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (world < 1 || world > kXchgMax || rank < 0 || rank >= world)
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "world %d / rank %d (1 <= world <= %d)", world, rank, kXchgMax);
+    if (max_payload_bytes == 0 || max_payload_bytes % sizeof(uint4))
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "max_payload_bytes must be a positive multiple of 16");
+    OL_CUDA(c, cudaSetDevice(c->device));
+    OL_CUDA(c, cudaStreamSynchronize(c->stream));
+    p2p_close(c);
+    const size_t bytes = kMboxFlagBytes + 2 * (size_t)world * max_payload_bytes;
+    if (cudaMalloc(&c->mbox_d, bytes) != cudaSuccess) { c->mbox_d = nullptr; return fail(c, OL_ERR_OOM, "mailbox of %zu bytes", bytes); }
+    OL_CUDA(c, cudaMemset(c->mbox_d, 0, kMboxFlagBytes));
+    c->mbox_records = max_payload_bytes / sizeof(uint4);
+    c->p2p_world = world; c->p2p_rank = rank; c->p2p_epoch = 0;
+    if (handle_out) {
+        cudaIpcMemHandle_t h;
+        OL_CUDA(c, cudaIpcGetMemHandle(&h, c->mbox_d));
+        memcpy(handle_out, &h, sizeof(h));
+    }
+    return OL_OK;
+}
+
+ol_status ol_p2p_connect(ol_ctx *c, const void *handles) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->mbox_d) return fail(c, OL_ERR_NOT_READY, "ol_p2p_open first");
+    if (!handles && c->p2p_world > 1) return fail(c, OL_ERR_INVALID_ARGUMENT, "handles is NULL");
+    OL_CUDA(c, cudaSetDevice(c->device));
+    for (int p = 0; p < c->p2p_world; ++p) {
+        if (p == c->p2p_rank) continue;
+        cudaIpcMemHandle_t h;
+        memcpy(&h, (const unsigned char *)handles + (size_t)p * sizeof(h), sizeof(h));
+        OL_CUDA(c, cudaIpcOpenMemHandle(&c->peer_base[p], h, cudaIpcMemLazyEnablePeerAccess));
+    }
+    c->p2p_ready = true;
+    return OL_OK;
+}
+
+static void xchg_fill(XchgArgs &x, ol_ctx *c, int p, void *base) {
+    x.flag[p] = reinterpret_cast<unsigned int *>(base);
+    x.mbox[p] = reinterpret_cast<uint4 *>(static_cast<unsigned char *>(base) + kMboxFlagBytes);
+    (void)c;
+}
+
+ol_status ol_p2p_finalize(ol_ctx *c) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->q_ready) return fail(c, OL_ERR_NOT_READY, "no query to finalize");
+    if (!c->p2p_ready) return fail(c, OL_ERR_NOT_READY, "ol_p2p_connect first");
+    const uint64_t P = (uint64_t)c->nq * c->n_sub * c->N;
+    if (P > c->mbox_records) return fail(c, OL_ERR_INVALID_ARGUMENT, "payload of %llu records exceeds the mailbox (%llu)",
+                                        (unsigned long long)P, (unsigned long long)c->mbox_records);
+    OL_CUDA(c, cudaSetDevice(c->device));
+    TimeScope ts(c, ol_ctx::T_FINAL);
+    OL_CUDA(c, grow(&c->final_d, &c->final_cap, (size_t)P));
+    XchgArgs x = {};
+    for (int p = 0; p < c->p2p_world; ++p) xchg_fill(x, c, p, p == c->p2p_rank ? (void *)c->mbox_d : c->peer_base[p]);
+    x.payload[0] = c->payload_d; x.records[0] = c->final_d;
+    x.rank0 = (uint32_t)c->p2p_rank; x.world = (uint32_t)c->p2p_world; x.blocks = kXchgBlocks;
+    x.epoch = ++c->p2p_epoch; x.nq = c->nq; x.n_sub = c->n_sub; x.N = c->N;
+    OL_LAUNCH(c, launch_xchg_merge(x, 1, c->stream));
+    return finalize_tail(c, c->final_d);
+}
+
+ol_status ol_p2p_emulate(ol_ctx **ctxs, int32_t world) {
+    if (!ctxs || world < 1 || world > kXchgMax) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctxs / world");
+    ol_ctx *c0 = ctxs[0];
+    for (int g = 0; g < world; ++g) {
+        ol_ctx *c = ctxs[g];
+        if (!c || !c->mbox_d || c->p2p_world != world || c->p2p_rank != g || c->device != c0->device)
+            return fail(c ? c : c0, OL_ERR_INVALID_ARGUMENT, "context %d: ol_p2p_open(world, rank = %d) on one device", g, g);
+        if (!c->q_ready) return fail(c, OL_ERR_NOT_READY, "context %d has no query to finalize", g);
+        if (c->nq != c0->nq || c->n_sub != c0->n_sub || c->N != c0->N || c->p2p_epoch != c0->p2p_epoch)
+            return fail(c, OL_ERR_INVALID_ARGUMENT, "context %d: a different query shape or epoch", g);
+        if ((uint64_t)c->nq * c->n_sub * c->N > c->mbox_records) return fail(c, OL_ERR_INVALID_ARGUMENT, "mailbox too small");
+    }
+    OL_CUDA(c0, cudaSetDevice(c0->device));
+    XchgArgs x = {};
+    for (int g = 0; g < world; ++g) {
+        ol_ctx *c = ctxs[g];
+        OL_CUDA(c, cudaStreamSynchronize(c->stream));
+        OL_CUDA(c, grow(&c->final_d, &c->final_cap, (size_t)c->nq * c->n_sub * c->N));
+        xchg_fill(x, c, g, c->mbox_d);
+        x.payload[g] = c->payload_d; x.records[g] = c->final_d;
+        ++c->p2p_epoch;
+    }
+    x.rank0 = 0; x.world = (uint32_t)world; x.blocks = kXchgBlocks; x.epoch = c0->p2p_epoch;
+    x.nq = c0->nq; x.n_sub = c0->n_sub; x.N = c0->N;
+    OL_LAUNCH(c0, launch_xchg_merge(x, (uint32_t)world, c0->stream));
+    OL_CUDA(c0, cudaStreamSynchronize(c0->stream));
+    for (int g = 0; g < world; ++g) {
+        ol_status st = finalize_tail(ctxs[g], ctxs[g]->final_d);
+        if (st) return st;
+    }
+    return OL_OK;
 }
 
 // ---------------------------------------------------------------- results

@@ -226,3 +226,44 @@ def test_error_paths():
     e.query(F[:1][:, None, :], N=5, aggregate=False)
     with pytest.raises(ol.OmnilocError, match="EMPTY"):
         e.estimates()
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_p2p_exchange_emulated_equals_single(c2, world):        # §8e, the peer-memory exchange
+    """The fused exchange + merge kernel (ol_p2p_*), `world` ranks emulated on one GPU
+    by one cooperative launch: every rank's candidates and estimates equal the W = 1
+    answer, over consecutive queries of different sizes (mailbox double-buffering,
+    monotonic arrival counters) and a mailbox re-open."""
+    cfg, F, C, video = c2
+    off = np.concatenate([[0], np.cumsum(cfg.subspace_sizes)])
+    engines = []
+    for r in range(world):
+        e = ol.Engine(0, coarse_k=16, rank=r, world=world)
+        rows = np.concatenate([np.arange(off[i] + b, off[i] + b + c) for i, n in enumerate(cfg.subspace_sizes)
+                               for b, c in [ol.shard_range(n, r, world)]])
+        e.upload(F[rows], C[rows], cfg.subspace_sizes, cfg.spec.grid())
+        engines.append(e)
+    one = _engine(16)
+    one.upload(F, C, cfg.subspace_sizes, cfg.spec.grid())
+    cap = 300 * len(cfg.subspace_sizes) * 15 * 16
+    for r, e in enumerate(engines):
+        assert len(e.p2p_open(world, r, cap)) == 64
+    for it, (a, b) in enumerate([(100, 400), (0, 37), (500, 800), (7, 8), (200, 500)]):
+        Q = video[a:b][:, None, :]
+        one.query(Q, N=15, aggregate=True)
+        want = one.topk().tobytes(), one.estimates().tobytes()
+        for e in engines:
+            e.query(Q, N=15, aggregate=True, exchange=False)
+        ol.p2p_emulate(engines)
+        for r, e in enumerate(engines):
+            assert (e.topk().tobytes(), e.estimates().tobytes()) == want, f"query {it} rank {r}"
+        if it == 2:   # a re-open (new mailboxes, epochs restart)
+            for r, e in enumerate(engines):
+                e.p2p_open(world, r, cap * 2)
+    # a payload larger than the mailbox is refused
+    Q = video[:400][:, None, :]
+    for e in engines:
+        e.query(Q, N=15, aggregate=True, exchange=False)
+    with pytest.raises(ol.OmnilocError):
+        engines[0].p2p_open(world, 0, 16)
+        ol.p2p_emulate(engines)

@@ -109,3 +109,24 @@ def test_gloo_sharded_merge_equals_single(world):
     for r in range(world):
         got = [[tuple(int(v) for v in t) for t in lst] for lst in result[r]]
         assert got == exp, f"rank {r}"
+
+
+def _handle_worker(rank, world, port, result):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    h = bytes([rank]) * 32 + bytes(range(32))          # a 64-byte stand-in for a CUDA IPC handle
+    result[rank] = ol.gather_handles(h)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_p2p_handle_exchange(world):
+    """The peer-memory exchange's setup (Engine exchange="p2p"): every rank receives all
+    ranks' 64-byte mailbox handles in rank order, as ol_p2p_connect expects."""
+    port = _free_port()
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_handle_worker, args=(world, port, result), nprocs=world, join=True)
+    want = b"".join(bytes([r]) * 32 + bytes(range(32)) for r in range(world))
+    for r in range(world):
+        assert result[r] == want
