@@ -60,6 +60,11 @@ def _args():
     return ap.parse_args()
 
 
+# tools/pipe_probe.cu on a B200 (round 1): cycles per 128-frame x 256-row accumulator tile of
+# the tensor-core scan's MMA -> TMEM -> epilogue pipeline alone, by filter dimensions K
+PIPE_PROBE = {16: 773, 32: 841, 64: 953}
+
+
 class Clocks:
     """SM clock and clock-event (throttle) reasons sampled DURING the timed region
     (B200_PROFILING.md clocks line): an NVML thread every 10 ms (started, and NVML
@@ -311,6 +316,12 @@ def run_omniloc(a):
                                    # with 16 warps (x 148 SMs x max clock)
                                    "tmem_read_tbs": pairs * 4 / scan_s / 1e12 if scan_s > 0 else None,
                                    "tmem_probe_peak_tbs": 271 * 148 * sm_max * 1e6 / 1e12,
+                                   # the MMA -> TMEM -> epilogue pipeline alone (tools/pipe_probe.cu,
+                                   # two 8-warp groups, 2 x 256-column buffers): cycles per 128-frame
+                                   # x 256-row tile at this K; the kernel's ceiling at max clock
+                                   "pipeline_probe_cycles_per_tile": PIPE_PROBE.get(kf),
+                                   "pipeline_probe_frac": (pairs / scan_s) / (148 * 32768 / PIPE_PROBE[kf] * sm_max * 1e6)
+                                   if scan_s > 0 and kf in PIPE_PROBE else None,
                                    "hbm_gbs": alg_bytes / scan_s / 1e9 if scan_s > 0 else None,
                                    "exact_rescored_pairs": survivors}}
     else:

@@ -12,6 +12,18 @@
 #include "../paper_2006_08861_b200/csrc/tc_ptx.cuh"
 using namespace ol::tc;
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(taddr));
+}
+
+__device__ __forceinline__ void reg_fence16(uint32_t (&r)[16]) {
+    asm volatile("" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                      "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]));
+}
+
 struct Smem {
     alignas(1024) __half a[128 * 64];
     alignas(1024) __half b[256 * 64];
@@ -22,7 +34,7 @@ struct Smem {
 // design 0: E warps all load every tile, each 256*4/E columns... (E = 16: 64 columns)
 // design 1: two groups of E/2 warps on alternate tiles, each warp 128 columns in two 64-col chunks
 __global__ void __launch_bounds__(544, 1) probe(int design, int E, int mma, int tiles, int NB, int kst, long long *out) {
-    const int TC = 512 / NB;   // columns per tile
+    const int TC = NB == 3 ? 160 : 512 / NB;   // columns per tile (NB = 3: 3 x 160 columns)
     extern __shared__ __align__(1024) unsigned char raw[];
     Smem &s = *reinterpret_cast<Smem *>(raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -76,6 +88,22 @@ __global__ void __launch_bounds__(544, 1) probe(int design, int E, int mma, int 
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s.tempty[buf]);
             }
+        } else if (design == 3) {
+            // 3 buffers of 160 columns, two groups on alternate tiles: the MMA can run one tile
+            // ahead of both groups; each warp reads 80 columns (x32 + x32 + x16, one wait)
+            const int grp = ew / (E / 2), half = (ew % (E / 2)) >> 2;
+            for (int t = grp; t < tiles; t += 2) {
+                const int buf = t % 3;
+                mbar_wait(&s.tfull[buf], (t / 3) & 1);
+                tc_fence_after();
+                uint32_t v0[32], v1[32], v2[16];
+                const uint32_t ta = tmem + ((q * 32) << 16) + buf * TC + half * 80;
+                tmem_ld32(ta, v0); tmem_ld32(ta + 32, v1); tmem_ld16(ta + 64, v2);
+                tmem_ld_wait_regs(v0); reg_fence(v1); reg_fence16(v2);
+                tc_fence_before(); __syncwarp(); if (lane == 0) mbar_arrive(&s.tempty[buf]);
+                for (int j = 0; j < 32; ++j) acc += v0[j] ^ v1[j];
+                for (int j = 0; j < 16; ++j) acc += v2[j];
+            }
         } else if (design == 2) {
             const int grp = ew / (E / 2), half = (ew % (E / 2)) >> 2;   // E/2 = 8: half in {0, 1}
             for (int t = grp; t < tiles; t += 2) {
@@ -122,8 +150,8 @@ int main() {
     for (int kst : {4, 2, 1})
         for (int mma = 0; mma <= 1; ++mma) {
             if (!mma && kst < 4) continue;
-            for (int design = 0; design <= 2; ++design) {
-                const int NB = design == 2 ? 4 : 2, E = 16;
+            for (int design = 0; design <= 3; ++design) {
+                const int NB = design == 2 ? 4 : design == 3 ? 3 : 2, E = 16;
                 long long h[4] = {0, 0, 0, 0};
                 probe<<<1, 32 * (1 + E), smem>>>(design, E, mma, tiles, NB, kst, d);
                 cudaError_t e = cudaGetLastError();
@@ -133,8 +161,8 @@ int main() {
                 if (e != cudaSuccess) { printf("copy error %s\n", cudaGetErrorString(e)); return 1; }
                 printf("[total %lld, mma thread %lld] ", h[0], h[1]);
                 printf("K=%d mma=%d NB=%d %-34s: %.0f cycles per 128 KB of accumulators\n", kst * 16, mma, NB,
-                       design == 0 ? "all 16 warps on every tile" : design == 1 ? "two groups, 2 x 256-col buffers" : "two groups, 4 x 128-col buffers",
-                       (double)h[0] / tiles * NB / 2);   // NB = 4: tiles of 64 KB
+                       design == 0 ? "all 16 warps on every tile" : design == 1 ? "two groups, 2 x 256-col buffers" : design == 2 ? "two groups, 4 x 128-col buffers" : "two groups, 3 x 160-col buffers",
+                       (double)h[0] / tiles * 256.0 / (NB == 3 ? 160 : 512 / NB));   // per 256 columns (128 KB)
             }
         }
     return 0;
