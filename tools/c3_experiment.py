@@ -8,7 +8,7 @@ dev = torch.device("cuda", 0)
 F, C = synthgen.db_device(spec, 0, spec.n_entries, dev)
 Q, _ = synthgen.render_device(spec, synthgen.query_points(spec, 4242, 1024), dev)
 Q3 = Q.view(-1, 1, 64)
-for tc, extra in [(1, {}), (0, {}), (1, {"tc_k": 32}), (1, {"tc_k": 48})]:
+for tc, extra in [(1, {}), (0, {}), (1, {"tc_k": 32})]:
     e = ol.Engine(0)
     e.set_option("tc", tc)
     for k, v in extra.items(): e.set_option(k, v)
