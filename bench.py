@@ -344,7 +344,9 @@ def run_omniloc(a):
                       "aggregate": True, "top_c": 10, "toler_per": 0.2, "radius_m": 3.0,
                       "coarse_k": a.coarse_k, "parallelism": f"db-shard{world}",
                       "exchange": (a.exchange if world > 1 else None),
-                      "l2": "inputs larger than L2 (coarse plane %.1f GB/rank)" % (rows_local * kc * 4 / 1e9)},
+                      "l2": ("inputs larger than L2 (coarse plane %.1f GB/rank)" % (rows_local * kc * 4 / 1e9)
+                             if rows_local * 64 * 4 > 126e6 else
+                             "database fits in L2 (%.1f MB): a latency configuration, L2 not flushed" % (rows_local * 64 * 4 / 1e6))},
            "comparisons_per_sec": cps,
            "stages_ms": {"tau_seed": seed_ns / 1e6, "scan": scan_ns / 1e6, "merge": merge_ns / 1e6,
                          "finalize": final_ns / 1e6},
