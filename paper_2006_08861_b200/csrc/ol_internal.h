@@ -125,7 +125,9 @@ struct TcScanArgs {
     unsigned long long *stat_survivors;
     unsigned long long *stat_flagged;   // (frame, row tile) pairs that took the cold path
     uint32_t nq, n_items, n_qblocks, qb, n_sub, N, kc, stages;
-    uint32_t dbg;                 // profiling only: 1 skip epilogue math, 2 skip MMA, 4 skip cold path, ...
+    uint32_t dbg;                 // profiling only: 1 skip epilogue math, 2 skip MMA, 4 skip cold path, 8 drop
+                                  // survivors, 16 / 32 counters, 64 keep the last thresholds, 128 stale rows,
+                                  // 256 no threshold refresh
     uint32_t n_blk;               // rows_pad / 32
     uint32_t kf;                  // filter on the first kf of K dimensions (16..64, multiple of 16)
     uint32_t pw;                  // fp16 plane / frame row width in halves: 64 (128-B rows, SW128) or 32 (kf = 32: 64-B rows, SW64)

@@ -300,7 +300,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         const uint32_t half = (ew >> 2) & 1;      // row columns half*128 .. +128
         const uint32_t grp = ew >> 3;             // tile parity
         const uint32_t ql = quarter * 32 + lane;  // frame within the CTA
-        const bool refresher = half == 0 && (grp == 0 || (a.dbg & 512)) && !(a.dbg & 256);   // one warp per frame refreshes tau
+        const bool refresher = half == 0 && grp == 0 && !(a.dbg & 256);   // one warp per frame refreshes tau (dbg 256: none, profiling)
         const float alpha = s.alpha[ql];
         // lanes 0..3: the row-term bound g_B of this warp's 4 blocks
         auto load_g = [&](uint32_t t) -> float2 {
