@@ -177,3 +177,18 @@ def test_tc_prefix_filter(kf):
     QG = (G[rng.integers(0, 5000, 200)] + rng.standard_normal((200, 64)).astype(np.float32) * 0.05)[:, None, :]
     e = _run(G, CG, [5000], QG, 15, 1, agg=False, tc_k=kf)
     assert_candidates_equal(e.topk(), oracle.retrieve([5000], G, CG, QG, 15), f"tc_k={kf} signed")
+
+
+@pytest.mark.parametrize("N,nq", [(64, 300), (128, 130), (1, 7)])
+def test_tc_narrow_plane_large_and_small_N(N, nq):
+    """The 64-B fp16 plane (tc_k = 32): deeper pipelines fit next to large top-N lists (N up to
+    128), and few frames (7: epilogue warps without frames skip their TMEM reads)."""
+    spec = synthgen.Spec(seed=37, n_floors=2, paths=5, frames_per_path=1000)
+    F, C = synthgen.db_host(spec)
+    Q = synthgen.render_host(spec, synthgen.query_points(spec, 27, nq))["desc"][:, None, :]
+    sizes = [6000, F.shape[0] - 6000]
+    ref = oracle.retrieve(sizes, F, C, Q, N)
+    for pair in (2, 0):
+        e = _run(F, C, sizes, Q, N, 1, agg=False, pair=pair, tc_k=32)
+        assert e.stat("used_tc") == 1 and e.stat("tc_k") == 32
+        assert_candidates_equal(e.topk(), ref, f"N={N} nq={nq} pair={pair}")
