@@ -1,2 +1,2 @@
-timeout 600 python bench.py > gpurun_out/bench_pw.json 2> gpurun_out/bench_pw.err; echo "bench rc=$?"
-python -c "import json; d=json.load(open('gpurun_out/bench_pw.json')); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['roofline']['per_launch']['hbm_gbs'], d['e2e']['value'], d['stages_ms'], d['clocks']); print(d['small_batch']); print(d['mid_batch'])"
+# survivor-row L2 prefetch at enqueue (default) vs none (tc_debug 512)
+for n in 100000000 20000000 1000000; do for d in 0 512 0 512; do echo "n=$n dbg=$d"; REPS=10 timeout 400 python tools/tc_experiment.py $n $d 2>&1 | tail -1; done; done
