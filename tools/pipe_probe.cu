@@ -123,6 +123,10 @@ __global__ void __launch_bounds__(544, 1) probe(int design, int E, int mma, int 
                 const int buf = t & 1;
                 mbar_wait(&s.tfull[buf], (t >> 1) & 1);
                 tc_fence_after();
+                if (design == 4) {   // the handoff alone: no accumulator reads
+                    tc_fence_before(); __syncwarp(); if (lane == 0) mbar_arrive(&s.tempty[buf]);
+                    continue;
+                }
                 for (int c = 0; c < 128; c += 64) {
                     uint32_t v0[32], v1[32];
                     const uint32_t ta = tmem + ((q * 32) << 16) + buf * 256 + half * 128 + c;
@@ -150,7 +154,7 @@ int main() {
     for (int kst : {4, 2, 1})
         for (int mma = 0; mma <= 1; ++mma) {
             if (!mma && kst < 4) continue;
-            for (int design = 0; design <= 3; ++design) {
+            for (int design = 0; design <= 4; ++design) {
                 const int NB = design == 2 ? 4 : design == 3 ? 3 : 2, E = 16;
                 long long h[4] = {0, 0, 0, 0};
                 probe<<<1, 32 * (1 + E), smem>>>(design, E, mma, tiles, NB, kst, d);
@@ -161,7 +165,7 @@ int main() {
                 if (e != cudaSuccess) { printf("copy error %s\n", cudaGetErrorString(e)); return 1; }
                 printf("[total %lld, mma thread %lld] ", h[0], h[1]);
                 printf("K=%d mma=%d NB=%d %-34s: %.0f cycles per 128 KB of accumulators\n", kst * 16, mma, NB,
-                       design == 0 ? "all 16 warps on every tile" : design == 1 ? "two groups, 2 x 256-col buffers" : design == 2 ? "two groups, 4 x 128-col buffers" : "two groups, 3 x 160-col buffers",
+                       design == 0 ? "all 16 warps on every tile" : design == 1 ? "two groups, 2 x 256-col buffers" : design == 2 ? "two groups, 4 x 128-col buffers" : design == 3 ? "two groups, 3 x 160-col buffers" : "two groups, handoff only (no reads)",
                        (double)h[0] / tiles * 256.0 / (NB == 3 ? 160 : 512 / NB));   // per 256 columns (128 KB)
             }
         }

@@ -1,2 +1,2 @@
-# survivor-row L2 prefetch at enqueue (default) vs none (tc_debug 512)
-for n in 100000000 20000000 1000000; do for d in 0 512 0 512; do echo "n=$n dbg=$d"; REPS=10 timeout 400 python tools/tc_experiment.py $n $d 2>&1 | tail -1; done; done
+# mbarrier waits: suspend-hint try_wait (default) vs spinning try_wait (1024: MMA warp, 2048: epilogue)
+for d in 0 1024 2048 3072 0; do echo "C4 dbg=$d"; REPS=10 timeout 400 python tools/tc_experiment.py 100000000 $d 2>&1 | tail -1; done
