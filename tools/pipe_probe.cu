@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(544, 1) probe(int design, int E, int mma, int 
     for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) s.b[i] = __float2half(0.001f * (i % 5));
     const int arrivals = design == 0 ? E : E / 2;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < NB; ++i) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], arrivals); }
+        for (int i = 0; i < (design == 5 ? 4 : NB); ++i) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], arrivals); }
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc<512>(&s.tmem);
@@ -55,6 +55,22 @@ __global__ void __launch_bounds__(544, 1) probe(int design, int E, int mma, int 
     if (warp == 0) {
         if (lane == 0) {
             const uint32_t idesc = idesc_f16_f32(128, TC);
+            if (design == 5) {   // each tile as two N = 128 halves, each with its own handshake
+                const uint32_t idh = idesc_f16_f32(128, 128);
+                for (int t = 0; t < tiles; ++t) {
+                    const int buf = t & 1;
+                    for (int hb = 0; hb < 2; ++hb) {
+                        if (t >= 2) mbar_wait(&s.tempty[2 * hb + buf], ((t >> 1) - 1) & 1);
+                        tc_fence_after();
+                        if (mma)
+                            for (int k = 0; k < kst; ++k)
+                                mma_f16(tmem + buf * 256 + hb * 128, desc_sw128_kmajor(smem_u32(s.a) + k * 32),
+                                        desc_sw128_kmajor(smem_u32(s.b) + hb * 128 * 128 + k * 32), idh, k ? 1u : 0u);
+                        mma_commit(&s.tfull[2 * hb + buf]);
+                    }
+                }
+                out[1] = clock64() - t0;
+            } else
             for (int t = 0; t < tiles; ++t) {
                 const int buf = t % NB;
                 if (t >= NB) mbar_wait(&s.tempty[buf], ((t / NB) - 1) & 1);
@@ -103,6 +119,21 @@ __global__ void __launch_bounds__(544, 1) probe(int design, int E, int mma, int 
                 tc_fence_before(); __syncwarp(); if (lane == 0) mbar_arrive(&s.tempty[buf]);
                 for (int j = 0; j < 32; ++j) acc += v0[j] ^ v1[j];
                 for (int j = 0; j < 16; ++j) acc += v2[j];
+            }
+        } else if (design == 5) {
+            const int grp = ew / (E / 2), half = (ew % (E / 2)) >> 2;
+            for (int t = grp; t < tiles; t += 2) {
+                const int buf = t & 1;
+                uint32_t v0[32], v1[32];
+                for (int hb = 0; hb < 2; ++hb) {
+                    mbar_wait(&s.tfull[2 * hb + buf], (t >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t ta = tmem + ((q * 32) << 16) + buf * 256 + hb * 128 + half * 64;
+                    tmem_ld32(ta, v0); tmem_ld32(ta + 32, v1);
+                    tmem_ld_wait_regs(v0); reg_fence(v1);
+                    tc_fence_before(); __syncwarp(); if (lane == 0) mbar_arrive(&s.tempty[2 * hb + buf]);
+                    for (int j = 0; j < 32; ++j) acc += v0[j] ^ v1[j];
+                }
             }
         } else if (design == 2) {
             const int grp = ew / (E / 2), half = (ew % (E / 2)) >> 2;   // E/2 = 8: half in {0, 1}
@@ -154,7 +185,7 @@ int main() {
     for (int kst : {4, 2, 1})
         for (int mma = 0; mma <= 1; ++mma) {
             if (!mma && kst < 4) continue;
-            for (int design = 0; design <= 4; ++design) {
+            for (int design = 0; design <= 5; ++design) {
                 const int NB = design == 2 ? 4 : design == 3 ? 3 : 2, E = 16;
                 long long h[4] = {0, 0, 0, 0};
                 probe<<<1, 32 * (1 + E), smem>>>(design, E, mma, tiles, NB, kst, d);
@@ -165,7 +196,7 @@ int main() {
                 if (e != cudaSuccess) { printf("copy error %s\n", cudaGetErrorString(e)); return 1; }
                 printf("[total %lld, mma thread %lld] ", h[0], h[1]);
                 printf("K=%d mma=%d NB=%d %-34s: %.0f cycles per 128 KB of accumulators\n", kst * 16, mma, NB,
-                       design == 0 ? "all 16 warps on every tile" : design == 1 ? "two groups, 2 x 256-col buffers" : design == 2 ? "two groups, 4 x 128-col buffers" : design == 3 ? "two groups, 3 x 160-col buffers" : "two groups, handoff only (no reads)",
+                       design == 0 ? "all 16 warps on every tile" : design == 1 ? "two groups, 2 x 256-col buffers" : design == 2 ? "two groups, 4 x 128-col buffers" : design == 3 ? "two groups, 3 x 160-col buffers" : design == 4 ? "two groups, handoff only (no reads)" : "two groups, 2 x 256, half handshakes",
                        (double)h[0] / tiles * 256.0 / (NB == 3 ? 160 : 512 / NB));   // per 256 columns (128 KB)
             }
         }
