@@ -1,4 +1,2 @@
-# CTA pairs: per-half accumulator handshakes (default) vs whole buffers (tc_debug 1024)
-timeout 900 python -m pytest tests/test_gpu_tc.py -x -q 2>&1 | tail -2
-for d in 0 1024 0 1024; do echo "C4 dbg=$d"; REPS=10 timeout 400 python tools/tc_experiment.py 100000000 $d 2>&1 | tail -1; done
-for d in 0 1024; do echo "20M dbg=$d"; REPS=10 timeout 400 python tools/tc_experiment.py 20000000 $d 2>&1 | tail -1; done
+# exact warps' idle back-off cap: 1024 ns (default) vs 128 ns (tc_debug 2048)
+for n in 100000000 20000000 1000000; do for d in 0 2048 0 2048; do echo "n=$n dbg=$d"; REPS=10 timeout 400 python tools/tc_experiment.py $n $d 2>&1 | tail -1; done; done
