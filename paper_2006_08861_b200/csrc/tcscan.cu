@@ -23,13 +23,20 @@
 // bit-identical to the one-pass scan (tests: test_gpu_tc, test_gpu_parity,
 // test_gpu_fullsize).
 //
-// CTA = one work item (rows of one subspace) x <= 128 query frames (one M-tile).
-// Warp roles: 0 TMA producer (256-row tiles of fp16 rows, 128-B swizzle, a
-// mbarrier ring of n_stages); 1 TMEM allocator + single-thread tcgen05.mma issuer:
-// per tile, M=128 frames x N=256 rows x K=64 (4 K16 MMAs) into a double-buffered
-// fp32 TMEM accumulator (2 x 256 columns); 2..9 epilogue (thread = one frame x 128
-// of the tile's rows: tcgen05.ld, release the buffer, per-block max, survivor
-// events); 10..11 exact re-scoring + top-N insertion.
+// Prefix filter (a.kf < 64): every quantity above taken over the first kf coordinates
+// only bounds the prefix distance, itself <= A, so pruning stays exact;
+// kf = 32 halves the MMA work, and the fp16 plane then holds just those 32 columns
+// (a.pw = 32: 64-B rows, 64-byte swizzle).
+//
+// CTA = one work item (rows of one subspace) x <= 128 query frames (one M-tile); CTA
+// pairs (kPair, cluster of 2) share each row tile: M = 256 frames, each CTA loads half.
+// Warp roles: 0 TMA producer (256-row tiles of fp16 rows, 128-B or 64-B swizzle, a
+// mbarrier ring of n_stages); 1 TMEM allocator + single-thread tcgen05.mma issuer (the
+// pair's leader): per tile, M = 128 / 256 frames x N = 256 rows x K = kf (kf / 16 K16
+// MMAs) into a double-buffered fp32 TMEM accumulator (2 x 256 columns); 2..17 epilogue
+// in two groups of 8 warps on alternate tiles (thread = one frame x 128 of the tile's
+// rows: tcgen05.ld, release the buffer, per-block max, survivor events); 18..19 exact
+// re-scoring + top-N insertion.
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
