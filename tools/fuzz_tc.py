@@ -4,7 +4,7 @@ Each case draws random values for:
 - database size and subspace split, and the data kind;
 - N, the frame count and bundle size M;
 - tc_k, CTA pairs, chunk size and seeding;
-- the path (tensor-core or CUDA-core).
+- the path (tensor-core or CUDA-core), and whether Algorithm 2 runs.
 
 Every case must be bit-identical to the oracle.
 usage: python tools/fuzz_tc.py [seconds] [seed]   (tests/test_gpu_fuzz.py runs a few cases)"""
@@ -21,7 +21,7 @@ for p in (ROOT, os.path.join(ROOT, "tests")):
 import oracle  # noqa: E402
 import synthgen  # noqa: E402
 import paper_2006_08861_b200 as ol  # noqa: E402
-from gpu_helpers import assert_candidates_equal  # noqa: E402
+from gpu_helpers import assert_candidates_equal, assert_estimates_equal  # noqa: E402
 
 
 def one_case(rng, idx):
@@ -60,10 +60,13 @@ def one_case(rng, idx):
     for k, v in opts.items():
         e.set_option(k, v)
     e.upload(F, C, sizes, (4096, 4096))
-    e.query(Q, N=N, aggregate=False)
+    agg = bool(rng.random() < 0.5)
+    e.query(Q, N=N, aggregate=agg)
     ref = oracle.retrieve(sizes, F, C, Q, N)
-    assert_candidates_equal(e.topk(), ref,
-                            f"case {idx}: {kind} rows={rows} sizes={sizes} B={B} M={M} N={N} {opts}")
+    ctx = f"case {idx}: {kind} rows={rows} sizes={sizes} B={B} M={M} N={N} agg={agg} {opts}"
+    assert_candidates_equal(e.topk(), ref, ctx)
+    if agg:
+        assert_estimates_equal(e.estimates(), ref, ctx=ctx)
     e.close()
 
 
