@@ -12,7 +12,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
-from dataclasses import dataclass, field, replace
+from dataclasses import dataclass
 
 import numpy as np
 

@@ -1,5 +1,5 @@
 """C1 (2,000 rows, 1 frame, N = 5): per-query latency with and without the tau seed."""
-import sys, torch, numpy as np
+import sys, torch
 sys.path.insert(0, '.')
 import synthgen, paper_2006_08861_b200 as ol
 cfg = synthgen.CONFIGS["C1"]; spec = cfg.spec

@@ -1,5 +1,5 @@
 """C2 (20k rows in 5 path subspaces, 1,000 bundles of M = 5 + Alg. 2): per-stage times, tc on/off."""
-import sys, torch, numpy as np
+import sys, torch
 sys.path.insert(0, '.')
 import synthgen, paper_2006_08861_b200 as ol
 cfg = synthgen.CONFIGS["C2"]; spec = cfg.spec

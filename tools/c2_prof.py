@@ -1,5 +1,5 @@
 """C2 exact-path profile: cycles per re-scored pair in the exact warps (tc_debug & 32)."""
-import sys, torch, numpy as np
+import sys, torch
 sys.path.insert(0, '.')
 import synthgen, paper_2006_08861_b200 as ol
 cfg = synthgen.CONFIGS["C2"]; spec = cfg.spec

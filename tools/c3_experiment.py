@@ -1,5 +1,5 @@
 """C3 (1M rows, 1,024 frames): tensor-core filter vs CUDA-core scan, survivors and time."""
-import sys, os, torch
+import sys, torch
 sys.path.insert(0, '.')
 import synthgen, paper_2006_08861_b200 as ol
 cfgn = sys.argv[1] if len(sys.argv) > 1 else "C3"

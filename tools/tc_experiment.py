@@ -1,5 +1,5 @@
-"""Timing experiments on the tensor-core scan (C3-size DB, 1,024 frames)."""
-import sys, os, torch, time
+"""Timing experiments on the tensor-core scan (C4-shaped DB of argv[1] rows, 1,024 frames; argv[2] = tc_debug values)."""
+import sys, os, torch
 sys.path.insert(0, '.')
 import synthgen, paper_2006_08861_b200 as ol
 spec = synthgen.CONFIGS["C4"].spec
@@ -8,10 +8,8 @@ dev = torch.device("cuda", 0)
 F, C = synthgen.db_device(spec, 0, n, dev)
 Q, _ = synthgen.render_device(spec, synthgen.query_points(spec, 4242, 1024), dev)
 e = ol.Engine(0)
-import os
 if os.environ.get("TCK"): e.set_option("tc_k", int(os.environ["TCK"]))
 e.upload(F, C, [n], spec.grid())
-import os
 if os.environ.get("CHUNK"): e.set_option("chunk", int(os.environ["CHUNK"]))
 if os.environ.get("PAIR"): e.set_option("pair", int(os.environ["PAIR"]))
 Q3 = Q.view(-1, 1, 64)
