@@ -54,10 +54,11 @@ constexpr int kMaxStages = 8;
 constexpr int kEpiWarps = 16;           // two groups of 8 (alternate tiles)
 constexpr int kExactWarps = 2;
 constexpr int kTcThreads = 32 * (2 + kEpiWarps + kExactWarps);
-constexpr int kEv = 32;                 // survivor event ring entries per exact warp: a short ring
+constexpr int kEv = 8;                  // survivor event ring entries per exact warp: a short ring
                                         // back-pressures the epilogue so thresholds stay fresh
-                                        // (measured single CTAs: 8/16/64/128/512 -> 16 best; CTA
-                                        // pairs, whose epilogues are coupled: 16/32/64 -> 32)
+                                        // (measured with the 32-dim filter, 1,024 frames, ring
+                                        // 32 / 16 / 8 / 4: 100M rows 10.05 / 9.93 / 9.95 / 9.96 ms,
+                                        // 20M 2.82 / 2.70 / 2.66 / 2.67, 1M 0.68 / - / 0.58 / 0.57)
 constexpr int kTrackMax = 16;           // largest N of the bound pre-pass (register list)
 constexpr float kTauInflate = 1.0f + 1.0f / 131072.0f;   // 1 + 2^-17
 constexpr uint32_t kStageBytesMax = kTileRows * kK * 2;   // 32 KB (pw = 64; 16 KB at pw = 32)
