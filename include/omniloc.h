@@ -339,7 +339,8 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *                   64) / 16 / 32 / 48 / 64: dimensions (a prefix) the certified tensor-core
  *                   filter scores; fewer halve its MMA work, more pairs reach the exact
  *                   re-score.  Results are identical.  Takes effect at the next ol_upload_db
- *   "pair"          1 (default: when the rank holds >= 2M rows) / 2 (always) / 0 (never): CTA
+ *   "pair"          1 (default: with the 128-B filter plane and >= 10M rows on the rank) / 2
+ *                   (always) / 0 (never): CTA
  *                   pairs (tcgen05 cta_group::2) for the tensor-core scan
  *   "cluster"       1 (default) / 2 / 4 / 8: thread-block clusters over a work item's query
  *                   blocks when pairs are off

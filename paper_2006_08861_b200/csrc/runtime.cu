@@ -625,12 +625,13 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     if (n_items && use_tc) {
         // CTA pairs need an even number of query blocks: a lone block (<= 128 frames) or a
         // small odd count would pay for a padding CTA's MMAs (measured: 1 block 1.8 ms single
-        // vs 2.6 ms paired at C4; 2 blocks 3.7 vs 3.3 ms).  Automatic mode also wants >= 2M
-        // rows: pairs halve the DRAM re-reads of a chunk's rows, which only matter once the
-        // plane outgrows L2 (1,024 frames: 1M rows 0.711 vs 0.695 ms single, 2M 0.888 vs
-        // 0.891, 5M 1.262 vs 1.290, 20M 2.70 vs 2.92)
+        // vs 2.6 ms paired at C4; 2 blocks 3.7 vs 3.3 ms).  Automatic mode also wants the
+        // 128-B plane and >= 10M rows: pairs halve the re-reads of a chunk's rows, which pay
+        // once the plane outgrows L2; with the 64-B plane they no longer do (1,024 frames,
+        // single vs pairs, final kernel: 5M rows 0.99 vs 1.03 ms, 20M 2.73 vs 2.63 (128-B
+        // plane); 50M 5.46 vs 5.73, 100M 10.61 vs 10.64 (64-B plane))
         const uint32_t nqb1 = (nq + tc_qb - 1) / tc_qb;
-        const bool pair = (c->opt_pair == 2 || (c->opt_pair == 1 && c->rows >= 2000000)) &&
+        const bool pair = (c->opt_pair == 2 || (c->opt_pair == 1 && c->tc_pw == 64 && c->rows >= 10000000)) &&
                           (nqb1 % 2 == 0 || nqb1 >= 5);
         const uint32_t qb = tc_qb, n_qblocks = ((nq + qb - 1) / qb + (pair ? 1 : 0)) / (pair ? 2 : 1) * (pair ? 2 : 1),
                        nq_pad = n_qblocks * qb;
