@@ -325,8 +325,9 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *   "chunk"         entries per work item (0 = automatic)
  *   "qtile"         query frames per CTA tile of the CUDA-core scans (0 = automatic)
  *   "tau_seed"      1 (default) / 0: seed pruning thresholds before the scan
- *   "seed_samples"  rows sampled per (frame, subspace) by the exact seed (16..32768, default
- *                   4096; at most 8192 when the one-CTA-per-job seed kernel runs)
+ *   "seed_samples"  rows sampled per (frame, subspace) by the exact seed (16..32768; default 0:
+ *                   8192 for >= 1,024 (frame, subspace) jobs, else 4096; at most 8192 when the
+ *                   one-CTA-per-job seed kernel runs)
  *   "seed_kernel"   1 (default) / 0: two-kernel seed (sample rows reused across frames) for >= 1,024
  *                   (frame, subspace, split) jobs, else one CTA per job
  *   "tc"            -1 (default: automatic, >= tc_min_frames frames) / 1 / 0: the certified
