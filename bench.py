@@ -51,6 +51,9 @@ def _args():
     ap.add_argument("--batch", type=int, default=0, help="query frames per step (0 = config)")
     ap.add_argument("--coarse-k", type=int, default=16)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="CUDA-graph replay of the query's launch sequence (option 'graph'); the "
+                         "stage split then comes from an extra eager pass after the timed region")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--small-batch", type=int, default=8, help="extra HBM-regime line (0 = off)")
     ap.add_argument("--ingest", type=int, default=1 << 20, help="profiles for the NEXT-3 extraction line (0 = off)")
@@ -240,12 +243,16 @@ def run_omniloc(a):
     def step():
         eng.query(Q3, params=params, aggregate=True)
 
+    if a.graph:
+        eng.set_option("graph", 1)
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize()
     kernels_per_step = eng.stat("kernels")
     survivors = eng.stat("survivors")
-    eng.set_option("time_kernels", 1)
+    replays0 = eng.stat("graph_replays")
+    if not a.graph:
+        eng.set_option("time_kernels", 1)
 
     stream = torch.cuda.current_stream(dev)
     clocks = Clocks(local)
@@ -265,6 +272,13 @@ def run_omniloc(a):
     clk = clocks.stop()
     ms = _max_over_ranks(e0.elapsed_time(e1), world) / a.steps
     per_step = np.array([ev[k].elapsed_time(ev[k + 1]) for k in range(a.steps)])
+    graph_replays = eng.stat("graph_replays") - replays0
+    if a.graph:
+        # stage split from an eager pass (time_kernels retires the graph; not the timed region)
+        eng.set_option("time_kernels", 1)
+        for _ in range(a.steps):
+            step()
+        torch.cuda.synchronize()
     scan_ns = eng.stat("time_scan_ns") / a.steps
     seed_ns = eng.stat("time_seed_ns") / a.steps
     merge_ns = eng.stat("time_merge_ns") / a.steps
@@ -344,6 +358,7 @@ def run_omniloc(a):
                       "aggregate": True, "top_c": 10, "toler_per": 0.2, "radius_m": 3.0,
                       "coarse_k": a.coarse_k, "parallelism": f"db-shard{world}",
                       "exchange": (a.exchange if world > 1 else None),
+                      "graph": bool(a.graph),
                       "l2": ("inputs larger than L2 (coarse plane %.1f GB/rank)" % (rows_local * kc * 4 / 1e9)
                              if rows_local * 64 * 4 > 126e6 else
                              "database fits in L2 (%.1f MB): a latency configuration, L2 not flushed" % (rows_local * 64 * 4 / 1e6))},
@@ -352,6 +367,7 @@ def run_omniloc(a):
                          "finalize": final_ns / 1e6},
            "survivor_frac": survivors / max(pairs, 1), "scan_path": "tensor-core filter" if used_tc else "cuda-core",
            "gpu_launches": kernels_per_step * a.steps,
+           "graph_replays": graph_replays,
            "roofline": roofline, "clocks": clk,
            "step_ms": {"p50": float(np.median(per_step)), "p99": float(np.quantile(per_step, 0.99)),
                        "min": float(per_step.min()), "max": float(per_step.max())},

@@ -349,13 +349,22 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *   "ctas"          cap on resident CTAs (0 = automatic)
  *   "time_kernels"  1 / 0: per-stage CUDA-event timing (stats "time_{seed,scan,merge,final}_ns")
  *   "tc_debug"      profiling only (results invalid when nonzero)
+ *   "graph"         0 (default) / 1: CUDA-graph replay for repeated query shapes (world 1,
+ *                   time_kernels off).  The first ol_query of a shape runs eagerly and then
+ *                   captures its launch sequence on a private stream; later calls with the
+ *                   same frames pointer (device frames; host frames are copied into the
+ *                   context's own buffer first), n_bundles, M, params and aggregate flag
+ *                   replay it as one cudaGraphLaunch on the context stream.  Results are
+ *                   identical.  Any ol_set_option or ol_upload_db retires the graph.  If the
+ *                   capture fails the shape keeps running eagerly (no error).
+ * Every call (any key) retires a captured query graph.
  * Errors: INVALID_ARGUMENT (unknown key or value). */
 OL_API ol_status ol_set_option(ol_ctx *ctx, const char *key, int64_t value);
 
 /* Read statistics of the last query: "survivors" (pairs that passed the coarse
  * bound), "pairs" (pairs scanned), "kernels" (kernel launches of the last
  * ol_query + ol_finalize), "used_tc" / "used_pair" (1 if the tensor-core scan / CTA pairs
- * ran), "tc_k" (the filter's dimensions), "items" / "chunk" (work items and rows per item), "time_{seed,scan,merge,final}_ns"
+ * ran), "graph_replays" (queries served by graph replay so far), "tc_k" (the filter's dimensions), "items" / "chunk" (work items and rows per item), "time_{seed,scan,merge,final}_ns"
  * (accumulated stage times while option "time_kernels" is 1; reading resets them).
  * Unknown key: INVALID_ARGUMENT.  Synchronises. */
 OL_API ol_status ol_get_stat(ol_ctx *ctx, const char *key, int64_t *value);

@@ -1,0 +1,99 @@
+"""CUDA-graph replay of repeated query shapes (option "graph", include/omniloc.h): a
+replayed query returns exactly what the oracle returns for the new frames (Alg. 1 top-N,
+P:95-108; Alg. 2 estimates), on the CUDA-core and tensor-core paths, for
+device and host frames; options and uploads retire the graph."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthgen
+import paper_2006_08861_b200 as ol
+from gpu_helpers import assert_candidates_equal, assert_estimates_equal
+
+pytestmark = pytest.mark.gpu
+
+
+def _db(seed=5, paths=2, frames=1000):
+    spec = synthgen.Spec(seed=seed, n_floors=1, paths=paths, frames_per_path=frames, path_y0=50.0)
+    F, C = synthgen.db_host(spec)
+    return spec, F, C, [frames] * paths
+
+
+def _bundles(spec, seed, nb, M):
+    n = nb * M + M
+    video = synthgen.render_host(spec, synthgen.query_points(spec, seed, n, "path", 0, 0))["desc"]
+    return np.ascontiguousarray(video[:nb * M].reshape(nb, M, -1))
+
+
+@pytest.mark.parametrize("tc,nb,M", [(0, 1, 1), (0, 3, 3), (1, 64, 1)])
+def test_graph_replay_matches_oracle_device_frames(tc, nb, M):
+    spec, F, C, sizes = _db()
+    eng = ol.Engine(0)
+    eng.upload(F, C, sizes, spec.grid())
+    eng.set_option("tc", tc)
+    eng.set_option("graph", 1)
+    qbuf = torch.empty((nb, M, 64), dtype=torch.float32, device="cuda")
+    kernels = None
+    for it in range(4):
+        Q = _bundles(spec, 100 + it, nb, M)
+        qbuf.copy_(torch.from_numpy(Q))
+        eng.query(qbuf, N=5, aggregate=True)
+        got, est = eng.topk(), eng.estimates()
+        assert eng.stat("graph_replays") == it
+        assert eng.stat("used_tc") == tc
+        k = eng.stat("kernels")
+        assert kernels is None or k == kernels
+        kernels = k
+        ref = oracle.retrieve(sizes, F, C, Q, 5)
+        assert_candidates_equal(got, ref, f"iteration {it}")
+        assert_estimates_equal(est, ref, ctx=f"iteration {it}")
+
+
+def test_graph_replay_host_frames_and_retire():
+    spec, F, C, sizes = _db(seed=9)
+    eng = ol.Engine(0)
+    eng.upload(F, C, sizes, spec.grid())
+    eng.set_option("graph", 1)
+    for it in range(3):
+        Q = _bundles(spec, 200 + it, 2, 5)
+        eng.query(Q, N=7, aggregate=True)
+        ref = oracle.retrieve(sizes, F, C, Q, 7)
+        assert_candidates_equal(eng.topk(), ref, f"host iteration {it}")
+        assert_estimates_equal(eng.estimates(), ref, ctx=f"host iteration {it}")
+    assert eng.stat("graph_replays") == 2
+    # another shape: eager + capture, then replay
+    Q = _bundles(spec, 300, 1, 5)
+    eng.query(Q, N=7, aggregate=True)
+    assert eng.stat("graph_replays") == 2
+    # any option retires the graph: the next call runs eagerly and re-captures
+    eng.set_option("graph", 1)
+    eng.query(Q, N=7, aggregate=True)
+    assert eng.stat("graph_replays") == 2
+    eng.query(Q, N=7, aggregate=True)
+    assert eng.stat("graph_replays") == 3
+    ref = oracle.retrieve(sizes, F, C, Q, 7)
+    assert_candidates_equal(eng.topk(), ref, "after retire")
+    # a new upload retires it as well (different database, same shape)
+    spec2, F2, C2, sizes2 = _db(seed=10)
+    eng.upload(F2, C2, sizes2, spec2.grid())
+    eng.query(Q, N=7, aggregate=True)
+    assert eng.stat("graph_replays") == 3
+    ref = oracle.retrieve(sizes2, F2, C2, Q, 7)
+    assert_candidates_equal(eng.topk(), ref, "after upload")
+
+
+def test_graph_nonfinite_frames_still_rejected():
+    spec, F, C, sizes = _db(seed=11)
+    eng = ol.Engine(0)
+    eng.upload(F, C, sizes, spec.grid())
+    eng.set_option("graph", 1)
+    qbuf = torch.from_numpy(_bundles(spec, 400, 1, 1)).cuda()
+    eng.query(qbuf, N=5)
+    eng.query(qbuf, N=5)
+    assert eng.stat("graph_replays") == 1
+    qbuf[0, 0, 3] = float("nan")
+    eng.query(qbuf, N=5)           # replayed: the finiteness check is part of the graph
+    assert eng.stat("graph_replays") == 2
+    with pytest.raises(ol.OmnilocError, match="NONFINITE"):
+        eng.topk()
