@@ -539,6 +539,8 @@ def run_streaming(a):
         group = dist.group.WORLD
     eng = ol.Engine(local, coarse_k=16, process_group=group, exchange=a.exchange)
     eng.upload(F, C, [n_total], spec.grid())
+    if a.graph and world == 1:
+        eng.set_option("graph", 1)
     del F, C
     params = ol.Params(N=cfg.N)
     cache = [dict() for _ in range(users)]
@@ -585,7 +587,7 @@ def run_streaming(a):
            "value": float(np.percentile(lat, 50)), "unit": "ms", "p99_ms": float(np.percentile(lat, 99)),
            "n_gpus": world, "localizations": int(lat.size), "higher_is_better": False,
            "config": {"workload": "C5", "db_entries": n_total, "users": users, "fps": fps, "seconds": secs,
-                      "M": M, "N": cfg.N},
+                      "M": M, "N": cfg.N, "graph": bool(a.graph and world == 1)},
            "data": "synthetic (seeded generator G, DESIGN.md §4)"}
     if cap is not None:
         out["capacity"] = cap

@@ -355,9 +355,10 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *                   same frames pointer (device frames; host frames are copied into the
  *                   context's own buffer first), n_bundles, M, params and aggregate flag
  *                   replay it as one cudaGraphLaunch on the context stream.  Results are
- *                   identical.  Any ol_set_option or ol_upload_db retires the graph.  If the
- *                   capture fails the shape keeps running eagerly (no error).
- * Every call (any key) retires a captured query graph.
+ *                   identical.  Up to 16 shapes are kept (least recently used evicted).
+ *                   Any ol_set_option or ol_upload_db retires them.  If a capture fails
+ *                   that shape keeps running eagerly (no error).
+ * Every call (any key) retires the captured query graphs.
  * Errors: INVALID_ARGUMENT (unknown key or value). */
 OL_API ol_status ol_set_option(ol_ctx *ctx, const char *key, int64_t value);
 

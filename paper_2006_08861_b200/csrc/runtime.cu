@@ -10,6 +10,7 @@
 //   merge_ranks     NK4' N smallest of the W gathered payloads   (world > 1 only)
 //   candidates           records -> ol_candidate rows, SPEC order
 //   aggregate       NK5  Algorithm 2 per bundle                  (if requested)
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -23,6 +24,10 @@
 using namespace ol;
 
 static thread_local std::string g_thread_err = "no error";
+
+// bumped whenever grow() (re)allocates a buffer: a captured query graph holds raw
+// device pointers, so it is valid only in the allocation epoch it was captured in
+static std::atomic<uint64_t> g_alloc_epoch{0};
 
 struct ol_ctx {
     int device = 0, rank = 0, world = 1, kc = 16;
@@ -122,10 +127,10 @@ struct ol_ctx {
     // on a private stream after one eager run and replayed while the key matches.
     // Any ol_set_option / ol_upload_db bumps `gen` and so retires the graph.
     struct QueryKey {
-        const float *q; uint32_t nb, M, on_device, aggregate; ol_params p; uint64_t gen;
+        const float *q; uint32_t nb, M, on_device, aggregate; ol_params p; uint64_t gen, epoch;
         bool operator==(const QueryKey &o) const {
             return q == o.q && nb == o.nb && M == o.M && on_device == o.on_device && aggregate == o.aggregate &&
-                   gen == o.gen && !memcmp(&p, &o.p, sizeof(p));
+                   gen == o.gen && epoch == o.epoch && !memcmp(&p, &o.p, sizeof(p));
         }
     };
     struct QueryState {   // what the launch sequence leaves on the host side
@@ -136,12 +141,16 @@ struct ol_ctx {
         uint64_t n_cand, per_bundle, pairs;
         int launches;
     };
+    struct GraphEntry {
+        QueryKey key;
+        QueryState state;
+        cudaGraphExec_t exec;   // NULL: the capture failed, this shape runs eagerly
+        uint64_t last_use;
+    };
+    static constexpr size_t kMaxGraphs = 16;   // shapes kept (least recently used evicted)
     int64_t opt_graph = 0;
-    uint64_t gen = 0;
-    bool gkey_set = false;
-    QueryKey gkey{};
-    QueryState gstate{};
-    cudaGraphExec_t gexec = nullptr;   // NULL with gkey_set: capture failed for this key
+    uint64_t gen = 0, graph_clock = 0;
+    std::vector<GraphEntry> graphs;
     cudaStream_t cap_stream = nullptr;
     uint64_t graph_replays = 0;
 };
@@ -196,6 +205,7 @@ static cudaError_t grow(T **p, size_t *cap, size_t n) {
     *p = nullptr;
     *cap = 0;
     size_t want = n < 1 ? 1 : n;
+    g_alloc_epoch.fetch_add(1);
     cudaError_t e = cudaMalloc((void **)p, want * sizeof(T));
     if (e == cudaSuccess) *cap = want;
     return e;
@@ -294,7 +304,8 @@ void ol_destroy(ol_ctx *c) {
     for (auto &v : c->ev)
         for (auto &p : v) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
-    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    for (auto &g : c->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     delete c;
 }
@@ -556,13 +567,21 @@ static void load_state(ol_ctx *c, const ol_ctx::QueryState &s) {
 
 // Capture query_body's launch sequence (already run eagerly once, so its caches and
 // buffers are warm and it makes no synchronising call) on the private stream.  A
-// failed capture leaves gexec NULL for this key: later calls run eagerly.
+// failed capture leaves the entry's exec NULL: this shape then runs eagerly.
 static void capture_query(ol_ctx *c, const ol_ctx::QueryKey &k, uint32_t nb, uint32_t M, const float *q,
                           int32_t on_device, const ol_params *p, int32_t aggregate, uint64_t per_q) {
-    if (c->gexec) { cudaGraphExecDestroy(c->gexec); c->gexec = nullptr; }
-    c->gkey = k;
-    c->gkey_set = true;
+    if (c->graphs.size() >= ol_ctx::kMaxGraphs) {   // evict the least recently used shape
+        size_t lru = 0;
+        for (size_t i = 1; i < c->graphs.size(); ++i)
+            if (c->graphs[i].last_use < c->graphs[lru].last_use) lru = i;
+        if (c->graphs[lru].exec) cudaGraphExecDestroy(c->graphs[lru].exec);
+        c->graphs.erase(c->graphs.begin() + lru);
+    }
     const ol_ctx::QueryState st0 = save_state(c);
+    ol_ctx::QueryKey k2 = k;
+    k2.epoch = g_alloc_epoch.load();   // the eager run may have grown buffers
+    c->graphs.push_back({k2, st0, nullptr, ++c->graph_clock});
+    ol_ctx::GraphEntry &ge = c->graphs.back();
     const std::string err0 = c->err;
     if (!c->cap_stream && cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
         cudaGetLastError();
@@ -576,14 +595,13 @@ static void capture_query(ol_ctx *c, const ol_ctx::QueryKey &k, uint32_t nb, uin
         const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
         cudaGraphExec_t ex = nullptr;
         if (st == OL_OK && e == cudaSuccess && g && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess)
-            c->gexec = ex;
+            ge.exec = ex;
         if (g) cudaGraphDestroy(g);
     }
     cudaGetLastError();
     c->stream = s0;
     c->err = err0;
     load_state(c, st0);
-    c->gstate = st0;
 }
 
 // ---------------------------------------------------------------- query
@@ -620,15 +638,23 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     }
     // graph replay: one launch for the whole sequence when this shape ran before
     const bool graph = c->opt_graph && !c->opt_time && c->world == 1;
-    const ol_ctx::QueryKey key{q, nb, M, (uint32_t)(on_device != 0), (uint32_t)(aggregate != 0), *p, c->gen};
-    if (graph && c->gkey_set && c->gkey == key) {
-        if (c->gexec) {
-            OL_CUDA(c, cudaGraphLaunch(c->gexec, c->stream));
-            load_state(c, c->gstate);
+    const ol_ctx::QueryKey key{q, nb, M, (uint32_t)(on_device != 0), (uint32_t)(aggregate != 0), *p, c->gen,
+                               g_alloc_epoch.load()};
+    if (graph) {
+        for (size_t i = 0; i < c->graphs.size();)   // retire the graphs of older generations / epochs
+            if (c->graphs[i].key.gen != key.gen || c->graphs[i].key.epoch != key.epoch) {
+                if (c->graphs[i].exec) cudaGraphExecDestroy(c->graphs[i].exec);
+                c->graphs.erase(c->graphs.begin() + i);
+            } else ++i;
+        for (auto &ge : c->graphs) {
+            if (!(ge.key == key)) continue;
+            ge.last_use = ++c->graph_clock;
+            if (!ge.exec) return query_body(c, nb, M, q, on_device, p, aggregate, per_q);
+            OL_CUDA(c, cudaGraphLaunch(ge.exec, c->stream));
+            load_state(c, ge.state);
             ++c->graph_replays;
             return OL_OK;
         }
-        return query_body(c, nb, M, q, on_device, p, aggregate, per_q);
     }
     st = query_body(c, nb, M, q, on_device, p, aggregate, per_q);
     if (st || !graph) return st;

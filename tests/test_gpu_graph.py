@@ -97,3 +97,46 @@ def test_graph_nonfinite_frames_still_rejected():
     assert eng.stat("graph_replays") == 2
     with pytest.raises(ol.OmnilocError, match="NONFINITE"):
         eng.topk()
+
+
+def test_graph_cache_alternating_shapes():
+    """Micro-batches of varying size (the streaming service) each keep their own graph."""
+    spec, F, C, sizes = _db(seed=12)
+    eng = ol.Engine(0)
+    eng.upload(F, C, sizes, spec.grid())
+    eng.set_option("graph", 1)
+    shapes = [1, 3, 2, 1, 3, 2, 3]
+    for it, nb in enumerate(shapes):
+        Q = _bundles(spec, 500 + it, nb, 5)
+        eng.query(Q, N=5, aggregate=True)
+        ref = oracle.retrieve(sizes, F, C, Q, 5)
+        assert_candidates_equal(eng.topk(), ref, f"shape {nb} iteration {it}")
+        assert_estimates_equal(eng.estimates(), ref, ctx=f"shape {nb} iteration {it}")
+    # host frames go through the context buffer, which grows to 3 bundles on the second call:
+    # shape 1 captured at the old buffer is re-captured once; every later call replays
+    assert eng.stat("graph_replays") >= 3
+
+
+def test_graph_survives_buffer_growth_elsewhere():
+    """ol_aggregate on many bundles grows the estimate buffer a captured graph writes to:
+    the allocation epoch retires the graph, and the next query is still exact."""
+    spec, F, C, sizes = _db(seed=13)
+    eng = ol.Engine(0)
+    eng.upload(F, C, sizes, spec.grid())
+    eng.set_option("graph", 1)
+    Q = _bundles(spec, 600, 1, 3)
+    eng.query(Q, N=5, aggregate=True)
+    eng.query(Q, N=5, aggregate=True)
+    assert eng.stat("graph_replays") == 1
+    rng = np.random.default_rng(3)
+    xy = rng.integers(0, 50, size=(4000, 2)).astype(np.int32)
+    eng.aggregate(xy, np.arange(0, 4001, 10, dtype=np.uint32))
+    Q2 = _bundles(spec, 601, 1, 3)
+    eng.query(Q2, N=5, aggregate=True)
+    assert eng.stat("graph_replays") == 1      # eager: the graph's buffers moved
+    ref = oracle.retrieve(sizes, F, C, Q2, 5)
+    assert_candidates_equal(eng.topk(), ref, "after growth")
+    assert_estimates_equal(eng.estimates(), ref, ctx="after growth")
+    eng.query(Q2, N=5, aggregate=True)
+    assert eng.stat("graph_replays") == 2
+    assert_estimates_equal(eng.estimates(), ref, ctx="replay after growth")
