@@ -6,12 +6,28 @@
 //    checking the geo-referenced mapping table") -> this rank's payload.
 //  merge_ranks: the N smallest of the W gathered payloads (cross-GPU merge).
 //  candidates: records -> ol_candidate rows in (bundle, frame, subspace, rank)
-//    order, dist = RN32(sqrt(acc)) (R3).
+//    order, dist = RN32(sqrt(acc)) (R3).  At world 1 merge_chunks writes
+//    these rows itself (one launch fewer); candidates_kernel serves the W > 1 merge.
 // Keys (acc bits << 32 | frame) are unique within a subspace apart from the
 // all-ones pad, so "N rounds of extract-the-minimum" is the exact top-N.
 #include "ol_internal.h"
 
 namespace ol {
+
+// record -> candidate row (R3: dist = RN32(sqrt(acc)))
+__device__ __forceinline__ ol_candidate make_candidate(const uint4 rec, uint32_t i, uint32_t q, uint32_t M) {
+    const float acc = __uint_as_float(rec.x);
+    ol_candidate o;
+    o.subspace = i;
+    o.frame = rec.y;
+    o.bundle = q / M;
+    o.query_frame = q % M;
+    o.dist2 = acc;
+    o.dist = __fsqrt_rn(acc);
+    o.x = (int32_t)rec.z;
+    o.y = (int32_t)rec.w;
+    return o;
+}
 
 __device__ __forceinline__ u64 warp_min_u64(u64 v) {
     for (int o = 16; o; o >>= 1) {
@@ -33,6 +49,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_chunks_kernel(MergeArgs a
     const uint32_t nk = (si.chunk_end - si.chunk_begin) * a.N;
     const u64 *src = a.partial + ((size_t)q * a.n_items + si.chunk_begin) * a.N;
     uint4 *dst = a.records + ((size_t)q * a.n_sub + i) * a.N;
+    // fused candidate rows (world 1): rank r < c of this (frame, subspace)
+    const uint32_t c = a.cand ? a.sub_prefix[i + 1] - a.sub_prefix[i] : 0;
+    ol_candidate *co = a.cand ? a.cand + (uint64_t)q * a.sub_prefix[a.n_sub] + a.sub_prefix[i] : nullptr;
     u64 last = 0;
     bool have_last = false;
     for (uint32_t r = 0; r < a.N; ++r) {
@@ -53,10 +72,14 @@ __global__ void __launch_bounds__(kMergeThreads) merge_chunks_kernel(MergeArgs a
                                  (uint32_t)a.coords[2 * row + 1]);
             }
             dst[r] = rec;
+            if (r < c) co[r] = make_candidate(rec, i, q, a.M);
         }
         if (best == kPadKey) {  // the rest are pads too
-            for (uint32_t rr = r + 1 + lane; rr < a.N; rr += 32)
-                dst[rr] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u);
+            for (uint32_t rr = r + 1 + lane; rr < a.N; rr += 32) {
+                const uint4 pad = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u);
+                dst[rr] = pad;
+                if (rr < c) co[rr] = make_candidate(pad, i, q, a.M);
+            }
             break;
         }
         last = best;
@@ -180,18 +203,7 @@ __global__ void candidates_kernel(CandArgs a) {
     const uint32_t q = (uint32_t)(t / ((uint64_t)a.N * a.n_sub));
     const uint32_t c = a.sub_prefix[i + 1] - a.sub_prefix[i];
     if (r >= c) return;
-    const uint4 rec = a.records[t];
-    const float acc = __uint_as_float(rec.x);
-    ol_candidate o;
-    o.subspace = i;
-    o.frame = rec.y;
-    o.bundle = q / a.M;
-    o.query_frame = q % a.M;
-    o.dist2 = acc;
-    o.dist = __fsqrt_rn(acc);
-    o.x = (int32_t)rec.z;
-    o.y = (int32_t)rec.w;
-    a.out[(uint64_t)q * a.sub_prefix[a.n_sub] + a.sub_prefix[i] + r] = o;
+    a.out[(uint64_t)q * a.sub_prefix[a.n_sub] + a.sub_prefix[i] + r] = make_candidate(a.records[t], i, q, a.M);
 }
 
 cudaError_t launch_candidates(const CandArgs &a, cudaStream_t s) {

@@ -70,6 +70,10 @@ struct MergeArgs {
     const int32_t *coords;       // [rows][2]
     uint4 *records;              // [nq][n_sub][N]
     uint32_t nq, n_items, n_sub, N;
+    // world 1: also write the candidate rows (candidates_kernel's output) when non-null
+    ol_candidate *cand;
+    const uint32_t *sub_prefix;  // [n_sub+1] prefix of min(N, |n_i|)
+    uint32_t M;
 };
 
 struct RankMergeArgs {

@@ -90,6 +90,7 @@ struct ol_ctx {
     ol_estimate *est_d = nullptr; size_t est_cap = 0;
     uint32_t *prefix_d = nullptr; size_t prefix_cap = 0;
     uint32_t prefix_N = 0;  // N the device prefix was built for (0 = none)
+    bool cand_fused = false;  // world 1: merge_chunks_kernel wrote the candidate rows
     uint32_t *agg_off_d = nullptr; size_t agg_off_cap = 0;
     int32_t *agg_xy_d = nullptr; size_t agg_xy_cap = 0;
     int *flags_d = nullptr;                // [0] nonfinite frames, [1] aggregation error
@@ -547,6 +548,21 @@ static ol_status build_sitems(ol_ctx *c, uint64_t chunk) {
     return OL_OK;
 }
 
+// device prefix of min(N, |n_i|) over the subspaces (candidate row offsets)
+static ol_status ensure_prefix(ol_ctx *c, uint32_t N) {
+    if (c->prefix_N == N) return OL_OK;
+    const uint32_t ns = c->n_sub;
+    std::vector<uint32_t> prefix(ns + 1, 0);
+    for (uint32_t i = 0; i < ns; ++i)
+        prefix[i + 1] = prefix[i] + (c->subs[i].global_size < N ? c->subs[i].global_size : N);
+    OL_CUDA(c, grow(&c->prefix_d, &c->prefix_cap, ns + 1));
+    OL_CUDA(c, cudaMemcpyAsync(c->prefix_d, prefix.data(), sizeof(uint32_t) * (ns + 1),
+                               cudaMemcpyHostToDevice, c->stream));
+    OL_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->prefix_N = N;
+    return OL_OK;
+}
+
 static ol_status finalize_impl(ol_ctx *c, const uint4 *gathered, int world);
 static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, int32_t on_device,
                             const ol_params *p, int32_t aggregate, uint64_t per_q);
@@ -823,6 +839,15 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
     MergeArgs ma;
     ma.partial = c->partial_d; ma.subs = c->subs_d; ma.coords = c->coords; ma.records = c->payload_d;
     ma.nq = nq; ma.n_items = n_items; ma.n_sub = c->n_sub; ma.N = N;
+    ma.cand = nullptr; ma.sub_prefix = nullptr; ma.M = M;
+    c->cand_fused = false;
+    if (c->world == 1) {   // the merge also writes the candidate rows (one launch fewer)
+        st = ensure_prefix(c, N);
+        if (st) return st;
+        OL_CUDA(c, grow(&c->cand_d, &c->cand_cap, per_q * nq));
+        ma.cand = c->cand_d; ma.sub_prefix = c->prefix_d;
+        c->cand_fused = true;
+    }
     {
         TimeScope ts(c, ol_ctx::T_MERGE);
         OL_LAUNCH(c, launch_merge_chunks(ma, c->stream));
@@ -874,21 +899,15 @@ static ol_status finalize_impl(ol_ctx *c, const uint4 *gathered, int world) {
 // candidates (and estimates) from the merged records [nq][n_sub][N]
 static ol_status finalize_tail(ol_ctx *c, const uint4 *rec) {
     const uint32_t nq = c->nq, N = c->N, ns = c->n_sub;
-    if (c->prefix_N != N) {
-        std::vector<uint32_t> prefix(ns + 1, 0);
-        for (uint32_t i = 0; i < ns; ++i)
-            prefix[i + 1] = prefix[i] + (c->subs[i].global_size < N ? c->subs[i].global_size : N);
-        OL_CUDA(c, grow(&c->prefix_d, &c->prefix_cap, ns + 1));
-        OL_CUDA(c, cudaMemcpyAsync(c->prefix_d, prefix.data(), sizeof(uint32_t) * (ns + 1),
-                                   cudaMemcpyHostToDevice, c->stream));
-        OL_CUDA(c, cudaStreamSynchronize(c->stream));
-        c->prefix_N = N;
+    if (!(c->cand_fused && rec == c->payload_d)) {
+        ol_status st = ensure_prefix(c, N);
+        if (st) return st;
+        OL_CUDA(c, grow(&c->cand_d, &c->cand_cap, c->n_cand));
+        CandArgs ca;
+        ca.records = rec; ca.sub_prefix = c->prefix_d; ca.out = c->cand_d; ca.nq = nq; ca.n_sub = ns;
+        ca.N = N; ca.M = c->M;
+        OL_LAUNCH(c, launch_candidates(ca, c->stream));
     }
-    OL_CUDA(c, grow(&c->cand_d, &c->cand_cap, c->n_cand));
-    CandArgs ca;
-    ca.records = rec; ca.sub_prefix = c->prefix_d; ca.out = c->cand_d; ca.nq = nq; ca.n_sub = ns;
-    ca.N = N; ca.M = c->M;
-    OL_LAUNCH(c, launch_candidates(ca, c->stream));
     if (c->aggregate) {
         OL_CUDA(c, grow(&c->est_d, &c->est_cap, c->nb));
         AggArgs ag;
