@@ -68,15 +68,16 @@ __global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
     if (a.cand) { begin = b * a.per_bundle; total = a.per_bundle; }
     else { begin = a.offsets[b]; total = a.offsets[b + 1] - begin; }
     ol_estimate *out = a.out + b;
-    if (total == 0 || total > (uint32_t)kAggMax) {
+    const uint32_t cap = a.cap ? a.cap : (uint32_t)kAggMax;   // shared-memory entries
+    if (total == 0 || total > cap) {
         if (threadIdx.x == 0) { *a.err_empty = total == 0 ? 1 : 2; out->total = total; }
         return;
     }
     uint32_t P = 1;
     while (P < total) P <<= 1;
     u64 *keys = reinterpret_cast<u64 *>(smem);          // [P]  sorted candidate tiles
-    u64 *dtile = keys + kAggMax;                        // [P]  occupied tiles
-    uint32_t *dcount = reinterpret_cast<uint32_t *>(dtile + kAggMax);  // [P]
+    u64 *dtile = keys + cap;                            // [P]  occupied tiles
+    uint32_t *dcount = reinterpret_cast<uint32_t *>(dtile + cap);  // [P]
     for (uint32_t t = threadIdx.x; t < P; t += blockDim.x) {
         u64 k = kPadKey;
         if (t < total) {
@@ -178,8 +179,11 @@ __global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
 }
 
 cudaError_t launch_aggregate(const AggArgs &a, cudaStream_t s) {
-    const size_t smem = sizeof(u64) * kAggMax * 2 + sizeof(uint32_t) * kAggMax;
-    cudaFuncSetAttribute(aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // sized to the largest bundle: small bundles fit several CTAs per SM
+    const size_t cap = a.cap ? a.cap : (size_t)kAggMax;
+    const size_t smem = sizeof(u64) * cap * 2 + sizeof(uint32_t) * cap;
+    const size_t max_smem = sizeof(u64) * kAggMax * 2 + sizeof(uint32_t) * kAggMax;
+    cudaFuncSetAttribute(aggregate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem);
     aggregate_kernel<<<a.n_bundles, kAggThreads, smem, s>>>(a);
     return cudaGetLastError();
 }

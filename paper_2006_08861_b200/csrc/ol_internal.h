@@ -110,6 +110,7 @@ struct AggArgs {
     int *err_empty;              // device flag
     uint32_t n_bundles, top_c;
     double toler_per, r2, tile_m;
+    uint32_t cap;                // power of two >= every bundle's size (<= kAggMax); 0 = kAggMax
 };
 
 struct TcScanArgs {

@@ -916,6 +916,9 @@ static ol_status finalize_tail(ol_ctx *c, const uint4 *rec) {
         ag.top_c = c->params.top_c; ag.toler_per = c->params.toler_per;
         const double r = c->params.radius_m / c->params.tile_m;
         ag.r2 = r * r; ag.tile_m = c->params.tile_m;
+        uint32_t cap = 32;
+        while (cap < c->per_bundle) cap <<= 1;
+        ag.cap = cap;
         OL_LAUNCH(c, launch_aggregate(ag, c->stream));
     }
     c->finalized = true;
@@ -1091,7 +1094,13 @@ ol_status ol_aggregate(ol_ctx *c, uint32_t nb, const uint32_t *offsets, const in
     OL_CUDA(c, cudaSetDevice(c->device));
     const uint32_t *off_d = offsets;
     const int32_t *xy_d = xy;
+    uint32_t cap = 0;   // device offsets: sizes unknown on the host, kAggMax
     if (!on_device) {
+        uint32_t mx = 1;
+        for (uint32_t b = 0; b < nb; ++b)
+            if (offsets[b + 1] > offsets[b] && offsets[b + 1] - offsets[b] > mx) mx = offsets[b + 1] - offsets[b];
+        cap = 32;
+        while (cap < mx && cap < (uint32_t)kAggMax) cap <<= 1;
         for (uint32_t b = 0; b < nb; ++b) {
             if (offsets[b + 1] < offsets[b]) return fail(c, OL_ERR_INVALID_ARGUMENT, "offsets decrease");
             if (offsets[b + 1] == offsets[b]) return fail(c, OL_ERR_EMPTY, "bundle %u has no candidates", b);
@@ -1115,6 +1124,7 @@ ol_status ol_aggregate(ol_ctx *c, uint32_t nb, const uint32_t *offsets, const in
     ag.err_empty = c->flags_d + 1; ag.n_bundles = nb; ag.top_c = p->top_c; ag.toler_per = p->toler_per;
     const double r = p->radius_m / p->tile_m;
     ag.r2 = r * r; ag.tile_m = p->tile_m;
+    ag.cap = cap;
     OL_CUDA(c, launch_aggregate(ag, c->stream));
     OL_CUDA(c, cudaMemcpyAsync(out, c->est_d, sizeof(ol_estimate) * nb, cudaMemcpyDeviceToHost, c->stream));
     st = check_flags(c);
