@@ -252,9 +252,13 @@ OL_API ol_status ol_get_estimates(ol_ctx *ctx, ol_estimate *out, uint32_t capaci
 
 /* Algorithm 2 alone on caller-provided candidate tiles: bundle b owns
  * xy[offsets[b] .. offsets[b+1]) (pairs of int32).  offsets/xy host or device
- * (on_device); out is a host array of n_bundles.  Synchronous.  Errors: EMPTY
- * (a bundle with zero candidates), INVALID_ARGUMENT (parameters as in
- * ol_query; a bundle with more than 8192 candidates), CUDA. */
+ * (on_device); out is a host array of n_bundles.  Synchronous.  Tiles rank by
+ * count, then signed (y, x) ascending (R7), for any int32 tile.
+ * Errors: EMPTY (a bundle with zero candidates), OUT_OF_RANGE (a tile
+ * outside the uploaded database's grid 0 <= x < grid_w, 0 <= y < grid_h -- a
+ * DB/grid mismatch, S:102, S:262 -- or, with no database uploaded, outside
+ * [-2^30, 2^30)), INVALID_ARGUMENT (parameters as in ol_query; a bundle with
+ * more than 8192 candidates), CUDA. */
 OL_API ol_status ol_aggregate(ol_ctx *ctx, uint32_t n_bundles, const uint32_t *offsets,
                        const int32_t *xy, int32_t on_device, const ol_params *p,
                        ol_estimate *out);

@@ -173,6 +173,8 @@ class Estimate:
     ranked_xy: np.ndarray
     ranked_count: np.ndarray
     ranked_circle: np.ndarray
+    x_m: float = 0.0      # tile centre in metres: tile_m * x in binary64 (DESIGN R14)
+    y_m: float = 0.0
 
 
 def aggregate(xy, top_c: int = 10, toler_per: float = 0.2, radius_m: float = 3.0,
@@ -193,7 +195,8 @@ def aggregate(xy, top_c: int = 10, toler_per: float = 0.2, radius_m: float = 3.0
         raise ValueError(f"oracle_aggregate rc={rc}")
     k = nr.value
     return Estimate(ox.value, oy.value, conf.value, bool(low.value), rxy[:k].copy(),
-                    rc_[:k].copy(), rci[:k].copy())
+                    rc_[:k].copy(), rci[:k].copy(), float(tile_m) * float(ox.value),
+                    float(tile_m) * float(oy.value))
 
 
 def shift_distance(q, d):

@@ -363,16 +363,22 @@ class Engine:
         return out
 
     def aggregate(self, xy, offsets, params: Params | None = None) -> np.ndarray:
-        """Algorithm 2 alone: bundle b owns xy[offsets[b]:offsets[b+1]]."""
+        """Algorithm 2 alone: bundle b owns xy[offsets[b]:offsets[b+1]].  xy / offsets are
+        host arrays, or both device tensors (int32 [n][2], uint32-valued int32 [nb+1])."""
         p = (params or self.params).c()
-        xy = np.ascontiguousarray(xy, np.int32).reshape(-1, 2)
-        off = np.ascontiguousarray(offsets, np.uint32)
-        nb = off.shape[0] - 1
+        if hasattr(xy, "is_cuda") and xy.is_cuda:
+            xy_p, dev = _ptr(xy.contiguous())
+            off_p, odev = _ptr(offsets.contiguous())
+            assert odev, "offsets must live with xy"
+            nb = int(offsets.shape[0]) - 1
+        else:
+            xy = np.ascontiguousarray(xy, np.int32).reshape(-1, 2)
+            off = np.ascontiguousarray(offsets, np.uint32)
+            xy_p, off_p, dev, nb = xy.ctypes.data, off.ctypes.data, 0, off.shape[0] - 1
         out = np.empty(nb, ESTIMATE_DTYPE)
         self.sync_stream()
-        self._ck(lib().ol_aggregate(self._h, nb, ctypes.c_void_p(off.ctypes.data),
-                                    ctypes.c_void_p(xy.ctypes.data), 0, ctypes.byref(p),
-                                    ctypes.c_void_p(out.ctypes.data)))
+        self._ck(lib().ol_aggregate(self._h, nb, ctypes.c_void_p(off_p), ctypes.c_void_p(xy_p), dev,
+                                    ctypes.byref(p), ctypes.c_void_p(out.ctypes.data)))
         return out
 
     # ---------------------------------------------------------------- NEXT-1

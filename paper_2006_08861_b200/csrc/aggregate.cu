@@ -58,6 +58,15 @@ __device__ uint32_t block_excl_scan(uint32_t v, uint32_t *scratch, uint32_t *tot
     return res;
 }
 
+// Tile sort key: (y, x) with both halves biased by 2^31, so unsigned key order is the
+// signed (y asc, x asc) order of the ranking tie-break (R7) for any int32 tile,
+// negative ones included (the unbiased key sorted negative tiles last).
+__device__ __forceinline__ u64 tile_key(int32_t x, int32_t y) {
+    return ((u64)((uint32_t)y ^ 0x80000000u) << 32) | ((uint32_t)x ^ 0x80000000u);
+}
+__device__ __forceinline__ int32_t key_x(u64 k) { return (int32_t)((uint32_t)k ^ 0x80000000u); }
+__device__ __forceinline__ int32_t key_y(u64 k) { return (int32_t)((uint32_t)(k >> 32) ^ 0x80000000u); }
+
 __global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t scratch[32];
@@ -84,7 +93,7 @@ __global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
             int32_t x, y;
             if (a.cand) { x = a.cand[begin + t].x; y = a.cand[begin + t].y; }
             else { x = a.xy[2 * (size_t)(begin + t)]; y = a.xy[2 * (size_t)(begin + t) + 1]; }
-            k = ((u64)(uint32_t)y << 32) | (uint32_t)x;
+            k = tile_key(x, y);
         }
         keys[t] = k;
     }
@@ -125,12 +134,12 @@ __global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint32_t r = 0; r < nr; ++r) {
         const u64 c = dtile[(uint32_t)keys[r]];
-        const int64_t cx = (int32_t)(uint32_t)c, cy = (int32_t)(uint32_t)(c >> 32);
+        const int64_t cx = key_x(c), cy = key_y(c);
         uint32_t s = 0;
         for (uint32_t d = threadIdx.x; d < nd; d += blockDim.x) {
             const u64 t = dtile[d];
-            const int64_t dx = (int64_t)(int32_t)(uint32_t)t - cx;
-            const int64_t dy = (int64_t)(int32_t)(uint32_t)(t >> 32) - cy;
+            const int64_t dx = (int64_t)key_x(t) - cx;
+            const int64_t dy = (int64_t)key_y(t) - cy;
             if ((double)(dx * dx + dy * dy) <= a.r2) s += dcount[d];
         }
         for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -154,8 +163,8 @@ __global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
         uint32_t low = 0;
         if (chosen < 0) { chosen = best; low = 1; }
         const u64 c = dtile[(uint32_t)keys[chosen]];
-        out->x = (int32_t)(uint32_t)c;
-        out->y = (int32_t)(uint32_t)(c >> 32);
+        out->x = key_x(c);
+        out->y = key_y(c);
         out->x_m = a.tile_m * (double)out->x;
         out->y_m = a.tile_m * (double)out->y;
         out->confidence = (double)circ[chosen] / (double)total;
@@ -169,8 +178,8 @@ __global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
         if (r < nr) {
             const uint32_t d = (uint32_t)keys[r];
             const u64 c = dtile[d];
-            rt.x = (int32_t)(uint32_t)c;
-            rt.y = (int32_t)(uint32_t)(c >> 32);
+            rt.x = key_x(c);
+            rt.y = key_y(c);
             rt.count = dcount[d];
             rt.circle = circ[r];
         }

@@ -183,7 +183,8 @@ cudaError_t launch_aggregate(const AggArgs &a, cudaStream_t s);
 cudaError_t launch_check_finite(const float *p, uint64_t n, int *flag, cudaStream_t s);
 cudaError_t launch_relayout(const float *src, uint64_t rows, uint64_t dst_row0, int kc, float *coarse,
                             float *fine, cudaStream_t s);
-cudaError_t launch_check_coords(const int32_t *xy, uint64_t rows, int32_t gw, int32_t gh,
-                                int *flag, cudaStream_t s);
+// flag = 1 if any (x, y) lies outside [x0, x1) x [y0, y1)
+cudaError_t launch_check_coords(const int32_t *xy, uint64_t rows, int32_t x0, int32_t x1, int32_t y0,
+                                int32_t y1, int *flag, cudaStream_t s);
 
 }  // namespace ol

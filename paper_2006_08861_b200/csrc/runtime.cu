@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <string>
 #include <vector>
 
@@ -59,11 +60,23 @@ struct ol_ctx {
     float *qprof_d = nullptr; size_t qprof_cap = 0;
     u64 *shift_keys = nullptr; size_t shift_cap = 0;
     bool shift_ready = false;
-    // work items (cached per chunk size)
-    std::vector<WorkItem> items;
-    WorkItem *items_d = nullptr;
-    size_t items_cap = 0;
+    // work items, one immutable table per chunk size: a captured query graph holds the
+    // device pointers of the table it ran with, so a table is never rewritten in place
+    // (rewriting items / chunk ranges under a graph of another shape made it
+    // scan the wrong rows).  Dropped only with the database, or all at once (gen++) when
+    // more than kMaxTables chunk sizes were seen.
+    struct ItemTable {
+        uint64_t chunk;
+        std::vector<WorkItem> items;
+        WorkItem *items_d;
+        SubInfo *subs_d;          // the subspaces with this table's chunk_begin / chunk_end
+    };
+    static constexpr size_t kMaxTables = 16;
+    std::deque<ItemTable> tables;    // (a deque: push_back keeps `cur` valid)
+    const ItemTable *cur = nullptr;  // the table of the last query_body
+    WorkItem *items_d = nullptr;     // == cur->items_d
     uint64_t items_chunk = 0;
+    size_t n_items() const { return cur ? cur->items.size() : 0; }
     uint32_t *seed_scratch = nullptr; size_t seed_scratch_cap = 0;
     // tensor-core bound pre-pass (tau seed) over the strided view rows 0, S, 2S, ...
     uint32_t seed_stride = 0;     // 0: not available (fp16 path off or tiny database)
@@ -88,8 +101,9 @@ struct ol_ctx {
     uint32_t p2p_epoch = 0;
     ol_candidate *cand_d = nullptr; size_t cand_cap = 0;
     ol_estimate *est_d = nullptr; size_t est_cap = 0;
-    uint32_t *prefix_d = nullptr; size_t prefix_cap = 0;
-    uint32_t prefix_N = 0;  // N the device prefix was built for (0 = none)
+    // device prefixes of min(N, |n_i|), one immutable array per N (same reason as tables)
+    std::vector<std::pair<uint32_t, uint32_t *>> prefixes;
+    uint32_t *prefix_d = nullptr;   // the prefix of the last ensure_prefix
     bool cand_fused = false;  // world 1: merge_chunks_kernel wrote the candidate rows
     uint32_t *agg_off_d = nullptr; size_t agg_off_cap = 0;
     int32_t *agg_xy_d = nullptr; size_t agg_xy_cap = 0;
@@ -141,6 +155,8 @@ struct ol_ctx {
         ol_params params;
         uint64_t n_cand, per_bundle, pairs;
         int launches;
+        const ItemTable *cur;   // the (immutable) tables the captured launches read
+        uint32_t *prefix_d;
     };
     struct GraphEntry {
         QueryKey key;
@@ -229,15 +245,25 @@ static ol_status check_params(ol_ctx *c, const ol_params *p, bool need_agg) {
     return OL_OK;
 }
 
+static void free_tables(ol_ctx *c) {
+    for (auto &t : c->tables) { cudaFree(t.items_d); cudaFree(t.subs_d); }
+    c->tables.clear();
+    c->cur = nullptr;
+    c->items_d = nullptr;
+    c->items_chunk = 0;
+    for (auto &p : c->prefixes) cudaFree(p.second);
+    c->prefixes.clear();
+    c->prefix_d = nullptr;
+}
+
 static void free_db(ol_ctx *c) {
+    free_tables(c);
     cudaFree(c->coarse); cudaFree(c->fine); cudaFree(c->coords); cudaFree(c->subs_d);
     cudaFree(c->plane16); cudaFree(c->blk); cudaFree(c->prof);
     c->prof = nullptr; c->prof_W = 0;
     c->coarse = c->fine = nullptr; c->coords = nullptr; c->subs_d = nullptr;
     c->plane16 = nullptr; c->blk = nullptr; c->tc_ok = false;
     c->db_ready = false;
-    c->items.clear();
-    c->items_chunk = 0;
     c->sitems_chunk = 0;
     c->seed_stride = 0;
 }
@@ -296,10 +322,10 @@ void ol_destroy(ol_ctx *c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     free_db(c);
-    cudaFree(c->items_d); cudaFree(c->seed_scratch); cudaFree(c->sitems_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
+    cudaFree(c->seed_scratch); cudaFree(c->sitems_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
     p2p_close(c);
-    cudaFree(c->prefix_d); cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
+    cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
     cudaFree(c->flags_d); cudaFree(c->stat_d); cudaFree(c->tcstat_d); cudaFree(c->prof_d);
     cudaFree(c->q16); cudaFree(c->qmeta); cudaFree(c->qprof_d); cudaFree(c->shift_keys);
     for (auto &v : c->ev)
@@ -409,7 +435,7 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
         if (db->on_device) {
             OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 2 * sizeof(int), c->stream));
             OL_CUDA(c, launch_check_finite(db->features, rows * OL_K, c->flags_d, c->stream));
-            OL_CUDA(c, launch_check_coords(db->coords, rows, db->grid_w, db->grid_h, c->flags_d + 1,
+            OL_CUDA(c, launch_check_coords(db->coords, rows, 0, db->grid_w, 0, db->grid_h, c->flags_d + 1,
                                            c->stream));
             int fl[2];
             OL_CUDA(c, cudaMemcpyAsync(fl, c->flags_d, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
@@ -482,16 +508,27 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
     c->db_ready = true;
     ++c->gen;
     c->q_ready = false;
-    c->prefix_N = 0;
     return OL_OK;
 }
 
 // ---------------------------------------------------------------- work decomposition
 static ol_status build_items(ol_ctx *c, uint64_t chunk) {
-    if (chunk == c->items_chunk && !c->items.empty()) return OL_OK;
+    for (auto &t : c->tables)
+        if (t.chunk == chunk) {
+            c->cur = &t; c->items_d = t.items_d; c->items_chunk = chunk;
+            return OL_OK;
+        }
+    if (c->tables.size() >= ol_ctx::kMaxTables) {   // retire every graph before freeing tables
+        OL_CUDA(c, cudaStreamSynchronize(c->stream));
+        for (auto &t : c->tables) { cudaFree(t.items_d); cudaFree(t.subs_d); }
+        c->tables.clear();
+        c->cur = nullptr;
+        ++c->gen;
+    }
     std::vector<WorkItem> items;
+    std::vector<SubInfo> subs = c->subs;
     for (uint32_t i = 0; i < c->n_sub; ++i) {
-        SubInfo &s = c->subs[i];
+        SubInfo &s = subs[i];
         s.chunk_begin = (uint32_t)items.size();
         for (uint64_t o = 0; o < s.count; o += chunk) {
             WorkItem w;
@@ -504,15 +541,21 @@ static ol_status build_items(ol_ctx *c, uint64_t chunk) {
         }
         s.chunk_end = (uint32_t)items.size();
     }
-    OL_CUDA(c, grow(&c->items_d, &c->items_cap, items.size()));
+    ol_ctx::ItemTable t{chunk, items, nullptr, nullptr};
+    OL_CUDA(c, cudaMalloc((void **)&t.items_d, sizeof(WorkItem) * (items.empty() ? 1 : items.size())));
+    if (cudaMalloc((void **)&t.subs_d, sizeof(SubInfo) * c->n_sub) != cudaSuccess) {
+        cudaFree(t.items_d);
+        return fail(c, OL_ERR_OOM, "work-item table");
+    }
+    c->tables.push_back(t);
+    ol_ctx::ItemTable &tb = c->tables.back();
     if (!items.empty())
-        OL_CUDA(c, cudaMemcpyAsync(c->items_d, items.data(), sizeof(WorkItem) * items.size(),
+        OL_CUDA(c, cudaMemcpyAsync(tb.items_d, tb.items.data(), sizeof(WorkItem) * items.size(),
                                    cudaMemcpyHostToDevice, c->stream));
-    OL_CUDA(c, cudaMemcpyAsync(c->subs_d, c->subs.data(), sizeof(SubInfo) * c->n_sub,
-                               cudaMemcpyHostToDevice, c->stream));
-    OL_CUDA(c, cudaStreamSynchronize(c->stream));  // host vectors are pageable and reused
-    c->items.swap(items);
-    c->items_chunk = chunk;
+    OL_CUDA(c, cudaMemcpyAsync(tb.subs_d, subs.data(), sizeof(SubInfo) * c->n_sub, cudaMemcpyHostToDevice,
+                               c->stream));
+    OL_CUDA(c, cudaStreamSynchronize(c->stream));  // host vectors are pageable
+    c->cur = &tb; c->items_d = tb.items_d; c->items_chunk = chunk;
     return OL_OK;
 }
 
@@ -538,6 +581,9 @@ static ol_status build_sitems(ol_ctx *c, uint64_t chunk) {
             items.push_back(w);
         }
     }
+    // rewritten in place (the bound pre-pass is not the default): retire captured graphs
+    OL_CUDA(c, cudaStreamSynchronize(c->stream));
+    ++c->gen;
     OL_CUDA(c, grow(&c->sitems_d, &c->sitems_cap, items.size() ? items.size() : 1));
     if (!items.empty())
         OL_CUDA(c, cudaMemcpyAsync(c->sitems_d, items.data(), sizeof(WorkItem) * items.size(),
@@ -550,16 +596,18 @@ static ol_status build_sitems(ol_ctx *c, uint64_t chunk) {
 
 // device prefix of min(N, |n_i|) over the subspaces (candidate row offsets)
 static ol_status ensure_prefix(ol_ctx *c, uint32_t N) {
-    if (c->prefix_N == N) return OL_OK;
+    for (auto &p : c->prefixes)
+        if (p.first == N) { c->prefix_d = p.second; return OL_OK; }
     const uint32_t ns = c->n_sub;
     std::vector<uint32_t> prefix(ns + 1, 0);
     for (uint32_t i = 0; i < ns; ++i)
         prefix[i + 1] = prefix[i] + (c->subs[i].global_size < N ? c->subs[i].global_size : N);
-    OL_CUDA(c, grow(&c->prefix_d, &c->prefix_cap, ns + 1));
-    OL_CUDA(c, cudaMemcpyAsync(c->prefix_d, prefix.data(), sizeof(uint32_t) * (ns + 1),
-                               cudaMemcpyHostToDevice, c->stream));
+    uint32_t *d = nullptr;
+    OL_CUDA(c, cudaMalloc((void **)&d, sizeof(uint32_t) * (ns + 1)));
+    c->prefixes.push_back({N, d});   // at most OL_MAX_N entries of n_sub + 1 words
+    OL_CUDA(c, cudaMemcpyAsync(d, prefix.data(), sizeof(uint32_t) * (ns + 1), cudaMemcpyHostToDevice, c->stream));
     OL_CUDA(c, cudaStreamSynchronize(c->stream));
-    c->prefix_N = N;
+    c->prefix_d = d;
     return OL_OK;
 }
 
@@ -569,13 +617,15 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
 
 static ol_ctx::QueryState save_state(const ol_ctx *c) {
     return {c->used_tc, c->used_pair, c->nb, c->M, c->N, c->nq, c->qt, c->aggregate, c->params,
-            c->n_cand, c->per_bundle, c->pairs, c->launches};
+            c->n_cand, c->per_bundle, c->pairs, c->launches, c->cur, c->prefix_d};
 }
 
 static void load_state(ol_ctx *c, const ol_ctx::QueryState &s) {
     c->used_tc = s.used_tc; c->used_pair = s.used_pair; c->nb = s.nb; c->M = s.M; c->N = s.N; c->nq = s.nq;
     c->qt = s.qt; c->aggregate = s.aggregate; c->params = s.params; c->n_cand = s.n_cand;
     c->per_bundle = s.per_bundle; c->pairs = s.pairs; c->launches = s.launches;
+    c->cur = s.cur; c->items_d = s.cur ? s.cur->items_d : nullptr; c->items_chunk = s.cur ? s.cur->chunk : 0;
+    c->prefix_d = s.prefix_d;
     c->q_ready = true;
     c->finalized = c->world == 1;
     c->shift_ready = false;
@@ -595,7 +645,8 @@ static void capture_query(ol_ctx *c, const ol_ctx::QueryKey &k, uint32_t nb, uin
     }
     const ol_ctx::QueryState st0 = save_state(c);
     ol_ctx::QueryKey k2 = k;
-    k2.epoch = g_alloc_epoch.load();   // the eager run may have grown buffers
+    k2.epoch = g_alloc_epoch.load();   // the eager run may have grown buffers ...
+    k2.gen = c->gen;                   // ... or retired graphs (table cache full, pre-pass items)
     c->graphs.push_back({k2, st0, nullptr, ++c->graph_clock});
     ol_ctx::GraphEntry &ge = c->graphs.back();
     const std::string err0 = c->err;
@@ -715,7 +766,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
     if (chunk > 0xFFFFFFFFull) chunk = 0xFFFFFFFFull;
     st = build_items(c, chunk);
     if (st) return st;
-    const uint32_t n_items = (uint32_t)c->items.size();
+    const uint32_t n_items = (uint32_t)c->n_items();
 
     // buffers
     OL_CUDA(c, grow(&c->tau0_d, &c->tau_cap, (size_t)nq * c->n_sub));
@@ -837,7 +888,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
             OL_LAUNCH(c, launch_scan(c->kc, a, scan_smem_bytes(qt, N), (int)(n_items * n_qtiles), c->stream));
     }
     MergeArgs ma;
-    ma.partial = c->partial_d; ma.subs = c->subs_d; ma.coords = c->coords; ma.records = c->payload_d;
+    ma.partial = c->partial_d; ma.subs = c->cur ? c->cur->subs_d : c->subs_d; ma.coords = c->coords; ma.records = c->payload_d;
     ma.nq = nq; ma.n_items = n_items; ma.n_sub = c->n_sub; ma.N = N;
     ma.cand = nullptr; ma.sub_prefix = nullptr; ma.M = M;
     c->cand_fused = false;
@@ -1092,6 +1143,12 @@ ol_status ol_aggregate(ol_ctx *c, uint32_t nb, const uint32_t *offsets, const in
     if (st) return st;
     if (nb == 0 || !offsets || !xy || !out) return fail(c, OL_ERR_INVALID_ARGUMENT, "empty/NULL input");
     OL_CUDA(c, cudaSetDevice(c->device));
+    // tiles must lie in the database's grid when one is uploaded (a coordinate
+    // outside the grid signals a DB/grid mismatch), else in [-2^30, 2^30) so that the circle
+    // test's dx^2 + dy^2 cannot overflow int64
+    const bool grid = c->db_ready;
+    const int32_t x0 = grid ? 0 : -(1 << 30), x1 = grid ? c->grid_w : (1 << 30);
+    const int32_t y0 = grid ? 0 : -(1 << 30), y1 = grid ? c->grid_h : (1 << 30);
     const uint32_t *off_d = offsets;
     const int32_t *xy_d = xy;
     uint32_t cap = 0;   // device offsets: sizes unknown on the host, kAggMax
@@ -1108,6 +1165,12 @@ ol_status ol_aggregate(ol_ctx *c, uint32_t nb, const uint32_t *offsets, const in
                 return fail(c, OL_ERR_INVALID_ARGUMENT, "bundle %u exceeds %d candidates", b, kAggMax);
         }
         const uint64_t tot = offsets[nb];
+        for (uint64_t t = offsets[0]; t < tot; ++t) {
+            const int32_t x = xy[2 * t], y = xy[2 * t + 1];
+            if (x < x0 || x >= x1 || y < y0 || y >= y1)
+                return fail(c, OL_ERR_OUT_OF_RANGE, "tile (%d,%d) of candidate %llu outside [%d,%d)x[%d,%d)%s", x, y,
+                            (unsigned long long)t, x0, x1, y0, y1, grid ? " (the database grid)" : "");
+        }
         OL_CUDA(c, grow(&c->agg_off_d, &c->agg_off_cap, nb + 1));
         OL_CUDA(c, grow(&c->agg_xy_d, &c->agg_xy_cap, 2 * (tot ? tot : 1)));
         OL_CUDA(c, cudaMemcpyAsync(c->agg_off_d, offsets, sizeof(uint32_t) * (nb + 1),
@@ -1118,7 +1181,16 @@ ol_status ol_aggregate(ol_ctx *c, uint32_t nb, const uint32_t *offsets, const in
         xy_d = c->agg_xy_d;
     }
     OL_CUDA(c, grow(&c->est_d, &c->est_cap, nb));
-    OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 2 * sizeof(int), c->stream));
+    OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 3 * sizeof(int), c->stream));
+    if (on_device) {   // the tiles' range, checked on the device (ol_aggregate is synchronous anyway)
+        uint32_t ends[2];
+        OL_CUDA(c, cudaMemcpyAsync(&ends[0], offsets, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        OL_CUDA(c, cudaMemcpyAsync(&ends[1], offsets + nb, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+        OL_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (ends[1] > ends[0])
+            OL_CUDA(c, launch_check_coords(xy + 2 * (uint64_t)ends[0], ends[1] - ends[0], x0, x1, y0, y1,
+                                           c->flags_d + 2, c->stream));
+    }
     AggArgs ag;
     ag.cand = nullptr; ag.per_bundle = 0; ag.offsets = off_d; ag.xy = xy_d; ag.out = c->est_d;
     ag.err_empty = c->flags_d + 1; ag.n_bundles = nb; ag.top_c = p->top_c; ag.toler_per = p->toler_per;
@@ -1127,9 +1199,14 @@ ol_status ol_aggregate(ol_ctx *c, uint32_t nb, const uint32_t *offsets, const in
     ag.cap = cap;
     OL_CUDA(c, launch_aggregate(ag, c->stream));
     OL_CUDA(c, cudaMemcpyAsync(out, c->est_d, sizeof(ol_estimate) * nb, cudaMemcpyDeviceToHost, c->stream));
+    int oor = 0;
+    OL_CUDA(c, cudaMemcpyAsync(&oor, c->flags_d + 2, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     st = check_flags(c);
     c->finalized = false;  // est_d now holds these estimates, not the last query's
-    return st;
+    if (st) return st;
+    if (oor) return fail(c, OL_ERR_OUT_OF_RANGE, "device tiles outside [%d,%d)x[%d,%d)%s", x0, x1, y0, y1,
+                         grid ? " (the database grid)" : "");
+    return OL_OK;
 }
 
 // ---------------------------------------------------------------- NEXT-1 shift re-scoring
@@ -1316,7 +1393,7 @@ ol_status ol_get_stat(ol_ctx *c, const char *key, int64_t *value) {
     else if (!strcmp(key, "graph_replays")) *value = (int64_t)c->graph_replays;
     else if (!strcmp(key, "qtile")) *value = c->qt;
     else if (!strcmp(key, "chunk")) *value = (int64_t)c->items_chunk;
-    else if (!strcmp(key, "items")) *value = (int64_t)c->items.size();
+    else if (!strcmp(key, "items")) *value = (int64_t)c->n_items();
     else if (!strcmp(key, "used_tc")) *value = c->used_tc ? 1 : 0;
     else if (!strcmp(key, "used_pair")) *value = c->used_pair ? 1 : 0;
     else if (!strcmp(key, "tc_k")) *value = (int64_t)c->tc_kf;

@@ -872,21 +872,21 @@ cudaError_t launch_check_finite(const float *p, uint64_t n, int *flag, cudaStrea
     return cudaGetLastError();
 }
 
-__global__ void check_coords_kernel(const int32_t *xy, uint64_t rows, int32_t gw, int32_t gh,
-                                    int *flag) {
+__global__ void check_coords_kernel(const int32_t *xy, uint64_t rows, int32_t x0, int32_t x1, int32_t y0,
+                                    int32_t y1, int *flag) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < rows;
          i += (uint64_t)gridDim.x * blockDim.x) {
         int32_t x = xy[2 * i], y = xy[2 * i + 1];
-        if (x < 0 || x >= gw || y < 0 || y >= gh) *flag = 1;
+        if (x < x0 || x >= x1 || y < y0 || y >= y1) *flag = 1;
     }
 }
 
-cudaError_t launch_check_coords(const int32_t *xy, uint64_t rows, int32_t gw, int32_t gh,
-                                int *flag, cudaStream_t s) {
+cudaError_t launch_check_coords(const int32_t *xy, uint64_t rows, int32_t x0, int32_t x1, int32_t y0,
+                                int32_t y1, int *flag, cudaStream_t s) {
     uint64_t blocks = (rows + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks == 0) blocks = 1;
-    check_coords_kernel<<<(unsigned)blocks, 256, 0, s>>>(xy, rows, gw, gh, flag);
+    check_coords_kernel<<<(unsigned)blocks, 256, 0, s>>>(xy, rows, x0, x1, y0, y1, flag);
     return cudaGetLastError();
 }
 

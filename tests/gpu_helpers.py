@@ -26,6 +26,7 @@ def assert_estimates_equal(est: np.ndarray, ref: "oracle.Candidates", params=Non
         assert (int(g["x"]), int(g["y"]), bool(g["low_confidence"])) == (e.x, e.y, e.low_confidence), \
             f"{ctx} bundle {b}: {(g['x'], g['y'], g['low_confidence'])} vs {(e.x, e.y, e.low_confidence)}"
         assert g["confidence"] == e.confidence, ctx
+        assert g["x_m"] == e.x_m and g["y_m"] == e.y_m, f"{ctx} bundle {b}: metres"
         k = int(g["n_ranked"])
         assert k == len(e.ranked_count)
         assert np.array_equal(g["ranked"]["x"][:k], e.ranked_xy[:, 0])

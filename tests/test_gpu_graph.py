@@ -140,3 +140,35 @@ def test_graph_survives_buffer_growth_elsewhere():
     eng.query(Q2, N=5, aggregate=True)
     assert eng.stat("graph_replays") == 2
     assert_estimates_equal(eng.estimates(), ref, ctx="replay after growth")
+
+
+def test_graph_alternating_paths_and_N_on_large_db():
+    """graphs of different launch layouts must not share work-item /
+    chunk-range / prefix tables.  On 120k rows the CUDA-core scan (1 and 9 frames) and the
+    tensor-core filter (64 frames) use different chunk sizes, and N changes the candidate
+    prefix; interleaved replays of all three shapes must each stay exact (Alg. 1, P:162;
+    Alg. 2, P:173-197)."""
+    spec, F, C, sizes = _db(seed=14, paths=2, frames=60000)
+    eng = ol.Engine(0)
+    eng.upload(F, C, sizes, spec.grid())
+    eng.set_option("graph", 1)
+    shapes = [(1, 1, 5, 0), (64, 1, 15, 1), (3, 3, 7, 0)]   # (nb, M, N, expect tensor-core)
+    bufs = [torch.empty((nb, M, 64), dtype=torch.float32, device="cuda") for nb, M, _, _ in shapes]
+    chunks = set()
+    replays = []
+    for it in range(9):
+        s = it % 3
+        nb, M, N, tc = shapes[s]
+        Q = _bundles(spec, 700 + it, nb, M)
+        bufs[s].copy_(torch.from_numpy(Q))
+        eng.query(bufs[s], N=N, aggregate=True)
+        got, est = eng.topk(), eng.estimates()
+        assert eng.stat("used_tc") == tc
+        chunks.add(eng.stat("chunk"))
+        replays.append(eng.stat("graph_replays"))
+        ref = oracle.retrieve(sizes, F, C, Q, N)
+        assert_candidates_equal(got, ref, f"shape {s} iteration {it}")
+        assert_estimates_equal(est, ref, ctx=f"shape {s} iteration {it}")
+    assert len(chunks) >= 2, chunks           # the shapes really use different tables
+    # buffers grown by a later shape retire earlier graphs once; the last round all replays
+    assert replays[6] - replays[5] == replays[7] - replays[6] == replays[8] - replays[7] == 1, replays

@@ -195,6 +195,70 @@ def test_aggregate_standalone_vs_oracle():
             assert np.array_equal(g["ranked"]["count"][:k], r.ranked_count)
 
 
+def test_aggregate_negative_tiles_and_grid_range():
+    """Standalone Alg. 2 ranks tiles by count, then signed (y, x) ascending (R7) for
+    any tile, negative ones included (ADVICE r01: the unbiased sort key put them last);
+    with a database uploaded, tiles outside its grid are rejected."""
+    rng = np.random.default_rng(78)
+    e = _engine(16)
+    sets = []
+    for s in range(120):
+        n = int(rng.integers(1, 400))
+        kind = s % 4
+        if kind == 0:      # ties across the sign boundary: equal counts at (-1, y) and (1, y)
+            base = np.array([[-1, -1], [1, -1], [-1, 1], [1, 1], [0, 0]])
+            xy = base[rng.integers(0, 5, n)]
+        elif kind == 1:
+            xy = rng.integers(-40, 40, (n, 2))
+        elif kind == 2:
+            xy = rng.integers(-(1 << 30), (1 << 30), (n, 2))
+        else:
+            c = rng.integers(-300, 300, (4, 2))
+            xy = c[rng.integers(0, 4, n)] + rng.integers(-5, 6, (n, 2))
+        sets.append(xy.astype(np.int32))
+    off = np.concatenate([[0], np.cumsum([len(x) for x in sets])]).astype(np.uint32)
+    allxy = np.concatenate(sets)
+    for params in (ol.Params(), ol.Params(top_c=64, toler_per=0.9, radius_m=0.6)):
+        for dev in (False, True):
+            if dev:
+                est = e.aggregate(torch.from_numpy(allxy).cuda(), torch.from_numpy(off.astype(np.int32)).cuda(),
+                                  params)
+            else:
+                est = e.aggregate(allxy, off, params)
+            for b, xy in enumerate(sets):
+                r = oracle.aggregate(xy, params.top_c, params.toler_per, params.radius_m, params.tile_m)
+                g = est[b]
+                assert (g["x"], g["y"], bool(g["low_confidence"]), g["confidence"]) == \
+                    (r.x, r.y, r.low_confidence, r.confidence), (b, dev)
+                assert g["x_m"] == r.x_m and g["y_m"] == r.y_m
+                k = int(g["n_ranked"])
+                assert np.array_equal(g["ranked"]["x"][:k], r.ranked_xy[:, 0]), (b, dev)
+                assert np.array_equal(g["ranked"]["y"][:k], r.ranked_xy[:, 1]), (b, dev)
+                assert np.array_equal(g["ranked"]["count"][:k], r.ranked_count)
+                assert np.array_equal(g["ranked"]["circle"][:k], r.ranked_circle)
+    # outside the int32 safety range (no database): rejected, host and device
+    big = np.array([[1 << 30, 0]], np.int32)
+    with pytest.raises(ol.OmnilocError, match="OUT_OF_RANGE"):
+        e.aggregate(big, np.array([0, 1], np.uint32))
+    with pytest.raises(ol.OmnilocError, match="OUT_OF_RANGE"):
+        e.aggregate(torch.from_numpy(big).cuda(), torch.tensor([0, 1], dtype=torch.int32, device="cuda"))
+    # with a database: its grid bounds the tiles
+    cfg = synthgen.CONFIGS["C1"]
+    F, C = synthgen.db_host(cfg.spec)
+    e.upload(F, C, cfg.subspace_sizes, cfg.spec.grid())
+    gw, gh = cfg.spec.grid()
+    for bad in ([-1, 0], [0, -1], [gw, 0], [0, gh]):
+        xy = np.array([[1, 1], bad], np.int32)
+        with pytest.raises(ol.OmnilocError, match="OUT_OF_RANGE"):
+            e.aggregate(xy, np.array([0, 2], np.uint32))
+        with pytest.raises(ol.OmnilocError, match="OUT_OF_RANGE"):
+            e.aggregate(torch.from_numpy(xy).cuda(), torch.tensor([0, 2], dtype=torch.int32, device="cuda"))
+    ok = np.array([[0, 0], [gw - 1, gh - 1]], np.int32)
+    est = e.aggregate(ok, np.array([0, 2], np.uint32))
+    r = oracle.aggregate(ok)
+    assert (est[0]["x"], est[0]["y"]) == (r.x, r.y)
+
+
 def test_error_paths():
     cfg = synthgen.CONFIGS["C1"]
     F, C = synthgen.db_host(cfg.spec)

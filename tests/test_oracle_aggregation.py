@@ -154,3 +154,19 @@ def test_majority_guarantee():
         xy = np.concatenate([np.full((k, 2), 77), rng.integers(200, 900, (n - k, 2))]).astype(np.int32)
         e = oracle.aggregate(xy)
         assert (e.x, e.y) == (77, 77) and not e.low_confidence
+
+
+def test_metres_are_correctly_rounded_tile_centres():        # S:329, DESIGN R14
+    """x_m = tile_m * x is the binary64 product, i.e. the exact rational product of the
+    binary64 tile_m and the tile index, rounded once to nearest (Fraction -> float rounds
+    correctly); checked for positive, negative and large tiles and a non-default tile_m."""
+    from fractions import Fraction
+    for tile_m in (0.3, 0.25, 0.1):
+        for t in ((10, 20), (-7, 3), (123456, -654321), (0, 0)):
+            e = oracle.aggregate(np.array([t], np.int32), tile_m=tile_m, radius_m=3 * tile_m / 0.3)
+            assert (e.x, e.y) == t
+            assert e.x_m == float(Fraction(tile_m) * t[0])
+            assert e.y_m == float(Fraction(tile_m) * t[1])
+    # the tile centre is not the decimal product when tile_m is not a dyadic rational
+    e = oracle.aggregate(np.array([[3, 0]], np.int32))
+    assert e.x_m != 0.9 and abs(e.x_m - 0.9) <= np.spacing(0.9)
