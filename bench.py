@@ -46,8 +46,10 @@ def _args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="omniloc", choices=["omniloc", "reference"])
     ap.add_argument("--config", default="C4")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
-                    help="cross-GPU merge at N > 1: NCCL all-gather + merge kernel, or one peer-memory kernel")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "torch", "p2p"],
+                    help="cross-GPU step at N > 1: the library's own NCCL communicator (threshold MIN "
+                         "all-reduce + all-gather + merge inside ol_query), torch.distributed all-gather + "
+                         "ol_finalize, or one peer-memory kernel")
     ap.add_argument("--batch", type=int, default=0, help="query frames per step (0 = config)")
     ap.add_argument("--coarse-k", type=int, default=16)
     ap.add_argument("--no-e2e", action="store_true")
@@ -154,12 +156,28 @@ class Clocks:
                 "reasons": sorted(reasons), "source": "nvidia-smi, 200 ms"}
 
 
+def _spawn_ranks(n_gpus: int) -> int:
+    """`bench.py --gpus N` (N > 1) outside a launcher: start N ranks, one process per GPU,
+    under torchrun on 127.0.0.1 with this same command line; rank 0 prints the line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def _dist_init(n_gpus):
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"bench.py: --gpus {n_gpus} but WORLD_SIZE={world} (launch with --gpus matching the "
+                         "launcher, or without a launcher so bench.py starts the ranks itself)")
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -457,19 +475,24 @@ def run_omniloc(a):
         eng.query(Q3h.numpy(), params=params, aggregate=True)
         ncand = eng.candidate_count()
         res = torch.empty(ncand * 32, dtype=torch.uint8).pin_memory()
+        est = torch.empty(B * ol.ESTIMATE_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
         torch.cuda.synchronize()
         _barrier(world)
         t0 = time.perf_counter()
         e0.record(stream)
         for _ in range(a.steps):
             eng.query(Q3h.numpy(), params=params, aggregate=True)   # H2D inside (pinned host)
-            eng.topk_into(res)                                        # D2H of the result
+            eng.topk_into(res)                                        # D2H of the candidates ...
+            eng.estimates_into(est)                                   # ... and of the Alg. 2 estimates
         e1.record(stream)
         torch.cuda.synchronize()
         wall = (time.perf_counter() - t0) / a.steps * 1e3
         ems = _max_over_ranks(max(e0.elapsed_time(e1) / a.steps, wall), world)
         out["e2e"] = {"value": B / (ems / 1e3), "unit": "queries/s", "ms_per_step": ems,
-                      "h2d_bytes_per_step": B * 64 * 4, "d2h_bytes_per_step": ncand * 32}
+                      "h2d_bytes_per_step": B * 64 * 4,
+                      "d2h_bytes_per_step": ncand * 32 + B * ol.ESTIMATE_DTYPE.itemsize,
+                      "copies": "frames H2D from pinned host inside ol_query; candidates (32 B each) and "
+                                "estimates (1,072 B each) D2H into pinned host"}
 
     # ------------------------------------------------ CPU oracle baseline (rank 0, N = 1)
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -693,6 +716,12 @@ def run_reference(a):
 
 if __name__ == "__main__":
     args = _args()
+    if args.impl != "reference" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn_ranks(args.gpus))
+    if os.environ.get("OL_BENCH_RANK_PROBE"):   # tests: the launch plumbing only, no GPU work
+        print(json.dumps({"rank": int(os.environ.get("RANK", "0")), "world": int(os.environ.get("WORLD_SIZE", "1")),
+                          "gpus": args.gpus}), flush=True)
+        sys.exit(0 if int(os.environ.get("WORLD_SIZE", "1")) == args.gpus else 3)
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "C5":

@@ -56,6 +56,9 @@ typedef int32_t ol_status;
 #define OL_ERR_NOT_READY           (-7)  /* query before upload / get before query      */
 #define OL_ERR_EMPTY               (-8)  /* a bundle with no candidates, or no
                                             estimates because aggregation was off      */
+#define OL_ERR_NCCL                (-9)  /* NCCL missing, or a communicator error       */
+
+#define OL_NCCL_ID_BYTES 128  /* ncclUniqueId */
 
 #define OL_K 64           /* descriptor length: |DFT| bins 1..64       */
 #define OL_MAX_N 128      /* largest supported top-N per (frame, subspace)          */
@@ -74,6 +77,13 @@ typedef struct {
     uint32_t K;            /* must be OL_K                                           */
     uint32_t coarse_k;     /* prefix length of the coarse pass (R2): 0 or 64 = one
                               pass over full rows; 8, 16 or 32 = exact coarse/fine  */
+    const void *nccl_unique_id;  /* OL_NCCL_ID_BYTES from ol_nccl_unique_id() on one rank,
+                              broadcast to all (e.g. torch.distributed); NULL = no
+                              communicator.  With an id, ol_create is collective over
+                              `world` ranks and the context owns a NCCL communicator:
+                              ol_query then exchanges and merges the per-rank top-N
+                              itself.  Allowed at world 1 (a 1-rank
+                              communicator: the same code path).                  */
 } ol_config;
 
 /* Database to upload (ol_upload_db).  The database is n_subspaces independent
@@ -138,10 +148,19 @@ typedef struct {
 
 /* Create a context on cfg->device.  Errors: INVALID_ARGUMENT (world < 1, rank
  * outside [0, world), coarse_k not in {0, 8, 16, 32, 64}), DIMENSION_MISMATCH
- * (K != 64), CUDA.  On error *out is NULL and ol_last_error(NULL) explains. */
+ * (K != 64), CUDA, NCCL (cfg->nccl_unique_id set and NCCL cannot be loaded or
+ * ncclCommInitRank fails).  On error *out is NULL and ol_last_error(NULL)
+ * explains. */
 OL_API ol_status ol_create(const ol_config *cfg, ol_ctx **out);
 
-/* Free all device/host resources of the context (NULL is a no-op). */
+/* A fresh NCCL unique id (OL_NCCL_ID_BYTES bytes written to out) for
+ * ol_config.nccl_unique_id: one rank creates it and sends it to the others by any
+ * means.  Pure host function; loads NCCL on first use ("libnccl.so.2", or the path
+ * in $OL_NCCL_LIB).  Errors: INVALID_ARGUMENT (NULL), NCCL. */
+OL_API ol_status ol_nccl_unique_id(void *out);
+
+/* Free all device/host resources of the context, the NCCL communicator included
+ * (aborted if it is in an error state).  NULL is a no-op. */
 OL_API void ol_destroy(ol_ctx *ctx);
 
 /* Replace the stream all later calls are ordered on (borrowed; NULL = the
@@ -171,13 +190,22 @@ OL_API ol_status ol_upload_db(ol_ctx *ctx, const ol_db_desc *db);
  * if `aggregate`, fuse every bundle (Alg. 2).  frames: [n_bundles][M][K] fp32,
  * host or device (on_device).  Asynchronous on the context stream: a host
  * `frames` buffer is read before return; results stay valid until the next
- * ol_query.  With world > 1 this call produces only this rank's top-N (the
- * "payload"); the caller all-gathers payloads and calls ol_finalize.
+ * ol_query.  With world > 1:
+ *   - context with a NCCL communicator (ol_config.nccl_unique_id): the call is
+ *     collective -- every rank calls it with identical arguments -- and it does the
+ *     whole cross-GPU step on the context stream: a MIN all-reduce of the seeded
+ *     thresholds before the scan (each rank's seed bounds the global N-th best, so
+ *     the least one is still exact), then an all-gather of the per-rank top-N
+ *     records and their merge.  Every rank ends with the global results.
+ *   - without a communicator it produces only this rank's top-N (the "payload");
+ *     the caller all-gathers payloads and calls ol_finalize (or ol_p2p_finalize).
  * Errors: NOT_READY (no database), INVALID_ARGUMENT (n_bundles = 0, M even or
  * 0 or > OL_MAX_M, N = 0 or > OL_MAX_N, top_c = 0 or > OL_MAX_TOP_C,
  * toler_per outside (0, 1], radius_m <= 0, tile_m <= 0, a bundle with more than
  * 8192 candidates when aggregating), NONFINITE (host frames; device frames
- * are checked on the device and reported by the next ol_get_*), OOM, CUDA. */
+ * are checked on the device and reported by the next ol_get_*), OOM, CUDA,
+ * NCCL (a collective failed to enqueue, or the communicator reports an
+ * asynchronous error; ol_get_* poll it as well). */
 OL_API ol_status ol_query(ol_ctx *ctx, uint32_t n_bundles, uint32_t M, const float *frames,
                    int32_t on_device, const ol_params *p, int32_t aggregate);
 
@@ -287,8 +315,10 @@ OL_API ol_status ol_upload_profiles(ol_ctx *ctx, const float *profiles, uint32_t
  * s is the heading difference in columns (2 pi s / W radians).
  * query_profiles: [n_bundles * M][W], host or device.  Candidates whose frame
  * lies in another rank's shard get the key INT64_MAX, so ranks combine with a
- * MIN reduction over ol_shift_keys.  Asynchronous.  Errors: NOT_READY (no
- * finalized query or no profiles), INVALID_ARGUMENT, NONFINITE (host input), CUDA. */
+ * MIN reduction over ol_shift_keys: done inside this call (collective, NCCL
+ * all-reduce on the context stream) when the context owns a communicator, else by
+ * the caller.  Asynchronous.  Errors: NOT_READY (no finalized query or no
+ * profiles), INVALID_ARGUMENT, NONFINITE (host input), CUDA, NCCL. */
 OL_API ol_status ol_shift_rescore(ol_ctx *ctx, const float *query_profiles, int32_t on_device);
 
 /* Device array (owned by the context) of the last ol_shift_rescore, one key per
@@ -366,7 +396,8 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  * Errors: INVALID_ARGUMENT (unknown key or value). */
 OL_API ol_status ol_set_option(ol_ctx *ctx, const char *key, int64_t value);
 
-/* Read statistics of the last query: "survivors" (pairs that passed the coarse
+/* Read statistics of the last query: "nccl" (1 if the context owns a communicator),
+ * "nccl_version" (of the loaded NCCL, 0 if none), "survivors" (pairs that passed the coarse
  * bound), "pairs" (pairs scanned), "kernels" (kernel launches of the last
  * ol_query + ol_finalize), "used_tc" / "used_pair" (1 if the tensor-core scan / CTA pairs
  * ran), "graph_replays" (queries served by graph replay so far), "tc_k" (the filter's dimensions), "items" / "chunk" (work items and rows per item), "time_{seed,scan,merge,final}_ns"

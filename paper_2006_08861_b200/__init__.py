@@ -5,7 +5,9 @@ argument marshalling only.  Every step of the path -- distance chain, coarse
 pruning, fine completion, top-N selection, merges and Algorithm 2 -- runs in the
 library's sm_100a kernels.  PyTorch provides device memory, the CUDA stream and
 (for sharded databases) the ``torch.distributed`` all-gather of the per-rank
-top-N payloads.  There is no CPU fallback: if the library or a GPU is missing,
+top-N payloads (only in the "torch" exchange mode; the default "nccl" mode runs the
+collectives inside the library on its own communicator, torch only broadcasts the
+NCCL unique id).  There is no CPU fallback: if the library or a GPU is missing,
 ``Engine`` raises.
 """
 from __future__ import annotations
@@ -24,12 +26,14 @@ LIB_PATH = os.path.join(_HERE, "libomniloc.so")
 
 OL_OK, OL_ERR_INVALID_ARGUMENT, OL_ERR_DIMENSION_MISMATCH, OL_ERR_NONFINITE = 0, -1, -2, -3
 OL_ERR_OUT_OF_RANGE, OL_ERR_OOM, OL_ERR_CUDA, OL_ERR_NOT_READY, OL_ERR_EMPTY = -4, -5, -6, -7, -8
+OL_ERR_NCCL = -9
+NCCL_ID_BYTES = 128
 K = 64
 MAX_TOP_C = 64
 PAYLOAD_RECORD_BYTES = 16
 
 _NAMES = {0: "OK", -1: "INVALID_ARGUMENT", -2: "DIMENSION_MISMATCH", -3: "NONFINITE",
-          -4: "OUT_OF_RANGE", -5: "OOM", -6: "CUDA", -7: "NOT_READY", -8: "EMPTY"}
+          -4: "OUT_OF_RANGE", -5: "OOM", -6: "CUDA", -7: "NOT_READY", -8: "EMPTY", -9: "NCCL"}
 
 
 class OmnilocError(RuntimeError):
@@ -40,7 +44,8 @@ class OmnilocError(RuntimeError):
 
 class ol_config(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("cuda_stream", ctypes.c_void_p), ("K", ctypes.c_uint32), ("coarse_k", ctypes.c_uint32)]
+                ("cuda_stream", ctypes.c_void_p), ("K", ctypes.c_uint32), ("coarse_k", ctypes.c_uint32),
+                ("nccl_unique_id", ctypes.c_void_p)]
 
 
 class ol_db_desc(ctypes.Structure):
@@ -80,12 +85,16 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} missing: run paper_2006_08861_b200.build() "
                               "(or __graft_entry__.build()) first; there is no CPU fallback")
+        # torch first: its NCCL (libnccl.so.2) is then the one already in the process, and the
+        # library's on-demand dlopen of NCCL resolves to it rather than to another copy
+        import torch  # noqa: F401
         L = ctypes.CDLL(LIB_PATH)
         P, u32, u64, i32, i64 = (ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32,
                                  ctypes.c_int64)
         sig = {
             "ol_create": ([ctypes.POINTER(ol_config), ctypes.POINTER(P)], i32),
             "ol_destroy": ([P], None),
+            "ol_nccl_unique_id": ([P], i32),
             "ol_last_error": ([P], ctypes.c_char_p),
             "ol_set_stream": ([P, P], i32),
             "ol_shard_range": ([u64, i32, i32, ctypes.POINTER(u64), ctypes.POINTER(u64)], i32),
@@ -163,14 +172,22 @@ class Params:
 class Engine:
     """One context on one GPU: upload a (sharded) feature database, query bundles.
 
-    ``process_group``: a torch.distributed group whose ranks each hold one shard;
-    the per-rank top-N payloads are all-gathered through it (NCCL on GPUs), or, with
-    ``exchange="p2p"``, exchanged and merged by one kernel over NVLink peer memory
-    (mailbox handles are exchanged through the group once).
+    ``process_group``: a torch.distributed group whose ranks each hold one shard.
+    ``exchange`` picks how the ranks' top-N meet:
+
+    - ``"nccl"`` (default): the library owns a NCCL communicator (rank 0's
+      ``ol_nccl_unique_id`` broadcast over the group, the only thing torch does) and
+      ``ol_query`` runs the threshold MIN all-reduce, the all-gather and the merge
+      itself.  ``comm=True`` also builds it at world 1 (a 1-rank communicator).
+    - ``"torch"``: ``ol_query`` returns this rank's payload; the binding all-gathers it
+      with ``torch.distributed`` (any backend: gloo stages through the host) and calls
+      ``ol_finalize``.
+    - ``"p2p"``: one kernel exchanges and merges over NVLink peer memory (mailbox
+      handles are exchanged through the group once).
     """
 
     def __init__(self, device: int = 0, coarse_k: int = 16, process_group=None, rank: int | None = None,
-                 world: int | None = None, stream=None, exchange: str = "nccl"):
+                 world: int | None = None, stream=None, exchange: str = "nccl", comm: bool | None = None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("omniloc needs a CUDA device (no CPU fallback)")
@@ -184,17 +201,38 @@ class Engine:
         self.rank = 0 if rank is None else rank
         self.world = 1 if world is None else world
         self._stream = stream
+        if exchange not in ("nccl", "torch", "p2p"):
+            raise ValueError("exchange must be 'nccl', 'torch' or 'p2p'")
+        self.exchange = exchange
+        if comm is None:
+            comm = exchange == "nccl" and self.world > 1
+        if comm and exchange != "nccl":
+            raise ValueError("comm=True needs exchange='nccl'")
+        if self.world > 1 and exchange == "nccl" and not comm:
+            raise ValueError("exchange='nccl' at world > 1 needs the library communicator")
         L = lib()
-        cfg = ol_config(device, self.rank, self.world, self._stream_ptr(), K, coarse_k)
+        uid = None
+        if comm:
+            uid = ctypes.create_string_buffer(NCCL_ID_BYTES)
+            if self.rank == 0:
+                _check(L.ol_nccl_unique_id(uid))
+            if self.world > 1:
+                if process_group is None:
+                    raise ValueError("a NCCL communicator over world > 1 needs a process group")
+                import torch.distributed as dist
+                obj = [uid.raw if self.rank == 0 else None]
+                dist.broadcast_object_list(obj, src=dist.get_global_rank(process_group, 0), group=process_group)
+                uid = ctypes.create_string_buffer(obj[0], NCCL_ID_BYTES)
+        self.comm = bool(comm)
+        torch.cuda.set_device(self.device)
+        cfg = ol_config(device, self.rank, self.world, self._stream_ptr(), K, coarse_k,
+                        ctypes.cast(uid, ctypes.c_void_p) if uid is not None else None)
         h = ctypes.c_void_p()
         _check(L.ol_create(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h
         self.params = Params()
         self._gather_buf = None
         self._payload_buf = None
-        if exchange not in ("nccl", "p2p"):
-            raise ValueError("exchange must be 'nccl' or 'p2p'")
-        self.exchange = exchange
         self._mbox_bytes = 0
 
     def _stream_ptr(self):
@@ -267,7 +305,7 @@ class Engine:
         pc = p.c()
         self._ck(lib().ol_query(self._h, B, Mq, ctypes.c_void_p(fp), fdev, ctypes.byref(pc),
                                 1 if aggregate else 0))
-        if self.world > 1 and exchange:
+        if self.world > 1 and exchange and not self.comm:   # (with a communicator: done in ol_query)
             if self.exchange == "p2p":
                 self._p2p_finalize()
             else:
@@ -350,6 +388,13 @@ class Engine:
                                    pinned.numel() // CANDIDATE_DTYPE.itemsize, ctypes.byref(w)))
         return n * CANDIDATE_DTYPE.itemsize
 
+    def estimates_into(self, pinned) -> int:
+        """D2H of the estimates into a (pinned) torch uint8 host tensor; returns bytes."""
+        B = self._last[0]
+        self._ck(lib().ol_get_estimates(self._h, ctypes.c_void_p(pinned.data_ptr()),
+                                        pinned.numel() // ESTIMATE_DTYPE.itemsize))
+        return B * ESTIMATE_DTYPE.itemsize
+
     def topk_device(self):
         """(device pointer, count) of the candidate array (owned by the engine)."""
         p = ctypes.c_void_p(); n = ctypes.c_uint64()
@@ -396,12 +441,11 @@ class Engine:
         qp, qdev = _ptr(query_profiles)
         self._ck(lib().ol_shift_rescore(self._h, ctypes.c_void_p(qp), qdev))
         n = self.candidate_count()
-        if self.world > 1:
+        if self.world > 1 and not self.comm:   # (with a communicator ol_shift_rescore MIN-reduces)
             torch = self._torch
-            import torch.distributed as dist
             keys = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
             self._ck(lib().ol_shift_keys_copy(self._h, ctypes.c_void_p(keys.data_ptr())))
-            dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=self.group)
+            min_reduce(keys, self.group)
             keys = keys[:n]
             k = keys.cpu().numpy().view(np.uint64)
             shift = (k & 0xFFFFFFFF).astype(np.uint32)
@@ -466,9 +510,32 @@ def p2p_emulate(engines):
     _check(lib().ol_p2p_emulate(arr, len(engines)), engines[0]._h)
 
 
+def _host_staged(t, group) -> bool:
+    """gloo moves host tensors only: device tensors are staged through the host."""
+    import torch.distributed as dist
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def exchange_payloads(src, dst, group=None):
     """All-gather equal-size uint8 payload tensors in rank order (NCCL on CUDA
-    tensors, gloo on CPU tensors).  The only collective of the path (§8e)."""
+    tensors; gloo through host copies).  The "torch" exchange mode's collective (§8e)."""
     import torch.distributed as dist
+    if _host_staged(src, group):
+        h = dst.new_empty(dst.shape, device="cpu")
+        dist.all_gather_into_tensor(h, src.cpu(), group=group)
+        dst.copy_(h)
+        return dst
     dist.all_gather_into_tensor(dst, src, group=group)
     return dst
+
+
+def min_reduce(t, group=None):
+    """In-place MIN all-reduce (the "torch" mode's combine of NEXT-1 shift keys)."""
+    import torch.distributed as dist
+    if _host_staged(t, group):
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MIN, group=group)
+        t.copy_(h)
+        return t
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return t

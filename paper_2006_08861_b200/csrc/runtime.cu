@@ -20,9 +20,57 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <mutex>
+#include <nccl.h>   // types and signatures only: the library is loaded on demand (dlopen)
+
 #include "ol_internal.h"
 
 using namespace ol;
+
+// ---------------------------------------------------------------- NCCL, loaded on demand
+// The cross-GPU step of SURVEY §8e (all-gather of the per-rank top-N, plus the MIN
+// all-reduce of the seeded thresholds) runs on a communicator the context owns.  NCCL is
+// dlopen'ed the first time a context asks for it, so a world-1 process never needs it;
+// "libnccl.so.2" resolves to the copy already in the process when there is one (torch's),
+// else the system library; OL_NCCL_LIB overrides the path.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) getUniqueId;
+    decltype(&ncclCommInitRank) commInitRank;
+    decltype(&ncclCommDestroy) commDestroy;
+    decltype(&ncclCommAbort) commAbort;
+    decltype(&ncclCommGetAsyncError) commGetAsyncError;
+    decltype(&ncclAllGather) allGather;
+    decltype(&ncclAllReduce) allReduce;
+    decltype(&ncclGetErrorString) getErrorString;
+    decltype(&ncclGetVersion) getVersion;
+};
+
+static const NcclApi *nccl_api(std::string *why) {
+    static std::once_flag once;
+    static NcclApi api;
+    static bool ok = false;
+    static std::string err;
+    std::call_once(once, [] {
+        const char *env = getenv("OL_NCCL_LIB");
+        void *h = dlopen(env && *env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) { err = std::string("dlopen NCCL: ") + dlerror(); return; }
+        bool all = true;
+        auto sym = [&](const char *n) { void *f = dlsym(h, n); if (!f) { all = false; err = std::string("NCCL lacks ") + n; } return f; };
+        api.getUniqueId = (decltype(api.getUniqueId))sym("ncclGetUniqueId");
+        api.commInitRank = (decltype(api.commInitRank))sym("ncclCommInitRank");
+        api.commDestroy = (decltype(api.commDestroy))sym("ncclCommDestroy");
+        api.commAbort = (decltype(api.commAbort))sym("ncclCommAbort");
+        api.commGetAsyncError = (decltype(api.commGetAsyncError))sym("ncclCommGetAsyncError");
+        api.allGather = (decltype(api.allGather))sym("ncclAllGather");
+        api.allReduce = (decltype(api.allReduce))sym("ncclAllReduce");
+        api.getErrorString = (decltype(api.getErrorString))sym("ncclGetErrorString");
+        api.getVersion = (decltype(api.getVersion))sym("ncclGetVersion");
+        ok = all;
+    });
+    if (!ok && why) *why = err;
+    return ok ? &api : nullptr;
+}
 
 static thread_local std::string g_thread_err = "no error";
 
@@ -33,6 +81,8 @@ static std::atomic<uint64_t> g_alloc_epoch{0};
 struct ol_ctx {
     int device = 0, rank = 0, world = 1, kc = 16;
     cudaStream_t stream = nullptr;  // borrowed (NULL = legacy default stream)
+    ncclComm_t comm = nullptr;      // owned; set when ol_config carried a NCCL unique id
+    uint4 *gather_d = nullptr; size_t gather_cap = 0;   // [world][payload] all-gathered records
     std::string err = "no error";
     // database
     bool db_ready = false;
@@ -209,6 +259,27 @@ static ol_status fail(ol_ctx *c, ol_status s, const char *fmt, ...) {
                         "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
     } while (0)
 
+#define OL_NCCL(c, call)                                                                     \
+    do {                                                                                     \
+        ncclResult_t r_ = (call);                                                            \
+        if (r_ != ncclSuccess)                                                               \
+            return fail((c), OL_ERR_NCCL, "%s: %s (%s:%d)", #call, nccl_api(nullptr)->getErrorString(r_), \
+                        __FILE__, __LINE__);                                                 \
+    } while (0)
+
+// a communicator error raised asynchronously (a peer died, a network fault)
+static ol_status fail(ol_ctx *c, ol_status s, const char *fmt, ...);
+static ol_status nccl_poll(ol_ctx *c) {
+    if (!c->comm) return OL_OK;
+    ncclResult_t a = ncclSuccess;
+    const NcclApi *api = nccl_api(nullptr);
+    const ncclResult_t r = api->commGetAsyncError(c->comm, &a);
+    if (r != ncclSuccess) return fail(c, OL_ERR_NCCL, "ncclCommGetAsyncError: %s", api->getErrorString(r));
+    if (a != ncclSuccess && a != ncclInProgress)
+        return fail(c, OL_ERR_NCCL, "NCCL communicator error: %s", api->getErrorString(a));
+    return OL_OK;
+}
+
 #define OL_LAUNCH(c, call)  \
     do {                    \
         OL_CUDA(c, call);   \
@@ -303,9 +374,37 @@ ol_status ol_create(const ol_config *cfg, ol_ctx **out) {
         ol_destroy(c);
         return OL_ERR_CUDA;
     }
+    if (cfg->nccl_unique_id) {   // collective: every rank of `world` calls ol_create with the same id
+        std::string why;
+        const NcclApi *api = nccl_api(&why);
+        if (!api) { ol_destroy(c); return fail(nullptr, OL_ERR_NCCL, "%s", why.c_str()); }
+        ncclUniqueId id;
+        memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+        const ncclResult_t r = api->commInitRank(&c->comm, c->world, id, c->rank);
+        if (r != ncclSuccess) {
+            c->comm = nullptr;
+            ol_destroy(c);
+            return fail(nullptr, OL_ERR_NCCL, "ncclCommInitRank(world %d, rank %d): %s", cfg->world, cfg->rank,
+                        api->getErrorString(r));
+        }
+    }
     *out = c;
     return OL_OK;
 }
+
+ol_status ol_nccl_unique_id(void *out) {
+    if (!out) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "out is NULL");
+    std::string why;
+    const NcclApi *api = nccl_api(&why);
+    if (!api) return fail(nullptr, OL_ERR_NCCL, "%s", why.c_str());
+    ncclUniqueId id;
+    const ncclResult_t r = api->getUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, OL_ERR_NCCL, "ncclGetUniqueId: %s", api->getErrorString(r));
+    static_assert(sizeof(id) == OL_NCCL_ID_BYTES, "ncclUniqueId size");
+    memcpy(out, &id, sizeof(id));
+    return OL_OK;
+}
+
 
 // release the peer mailboxes opened by IPC and this rank's own
 static void p2p_close(ol_ctx *c) {
@@ -321,6 +420,14 @@ void ol_destroy(ol_ctx *c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    if (c->comm) {   // a communicator in error state cannot be destroyed cleanly: abort it
+        const NcclApi *api = nccl_api(nullptr);
+        ncclResult_t a = ncclSuccess;
+        if (api->commGetAsyncError(c->comm, &a) == ncclSuccess && a == ncclSuccess) api->commDestroy(c->comm);
+        else api->commAbort(c->comm);
+        c->comm = nullptr;
+    }
+    cudaFree(c->gather_d);
     free_db(c);
     cudaFree(c->seed_scratch); cudaFree(c->sitems_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
@@ -704,7 +811,7 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
         q = c->q_d;
     }
     // graph replay: one launch for the whole sequence when this shape ran before
-    const bool graph = c->opt_graph && !c->opt_time && c->world == 1;
+    const bool graph = c->opt_graph && !c->opt_time && c->world == 1 && !c->comm;
     const ol_ctx::QueryKey key{q, nb, M, (uint32_t)(on_device != 0), (uint32_t)(aggregate != 0), *p, c->gen,
                                g_alloc_epoch.load()};
     if (graph) {
@@ -726,6 +833,18 @@ ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int3
     st = query_body(c, nb, M, q, on_device, p, aggregate, per_q);
     if (st || !graph) return st;
     capture_query(c, key, nb, M, q, on_device, p, aggregate, per_q);
+    return OL_OK;
+}
+
+// Threshold sharing: every rank's seeded threshold for a (frame, subspace) is
+// the N-th smallest acc of N distinct rows of that subspace, so it bounds the GLOBAL N-th
+// smallest from above, and so does the minimum over ranks.  Pruning stays strict (acc > tau),
+// so every row of the global top-N survives on its rank and results stay exact; smaller
+// shards no longer start from looser thresholds than the whole database would.
+static ol_status share_tau(ol_ctx *c, uint32_t nq) {
+    if (!c->comm) return OL_OK;
+    OL_NCCL(c, nccl_api(nullptr)->allReduce(c->tau0_d, c->tau0_d, (size_t)nq * c->n_sub, ncclUint32, ncclMin,
+                                            c->comm, c->stream));
     return OL_OK;
 }
 
@@ -870,6 +989,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
                 OL_LAUNCH(c, launch_tcscan(c->map_srows, map_q, pa, (int)(pa.n_items * n_qblocks), c->stream));
             }
         }
+        if (!(a.dbg & 64)) { st = share_tau(c, nq); if (st) return st; }
         TimeScope ts(c, ol_ctx::T_SCAN);
         OL_LAUNCH(c, launch_tcscan(pair ? c->map_rows_half : c->map_rows, map_q, a, (int)(n_items * n_qblocks), c->stream));
         c->used_tc = true;
@@ -879,6 +999,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         a.coarse = c->coarse; a.fine = c->fine; a.queries = q; a.items = c->items_d;
         a.tau0 = seed ? c->tau0_d : nullptr; a.partial = c->partial_d; a.stat_survivors = c->stat_d;
         a.nq = nq; a.n_items = n_items; a.n_qtiles = n_qtiles; a.qt = qt; a.n_sub = c->n_sub; a.N = N;
+        if (seed) { st = share_tau(c, nq); if (st) return st; }
         TimeScope ts(c, ol_ctx::T_SCAN);
         if (qt <= 16 && c->opt_scan2 == 2 && c->kc < OL_K)   // few frames: TMA-fed row-pair kernel
             OL_LAUNCH(c, launch_scan3(c->kc, a, scan3_smem_bytes(qt, N, c->kc), (int)(n_items * n_qtiles), c->stream));
@@ -909,6 +1030,18 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
     c->n_cand = per_q * nq;
     c->pairs = (uint64_t)nq * c->rows;
     c->q_ready = true;
+    if (c->comm) {   // the exchange inside the call: all-gather the per-rank top-N, merge
+        const size_t P = (size_t)nq * c->n_sub * N;
+        OL_CUDA(c, grow(&c->gather_d, &c->gather_cap, P * c->world));
+        {
+            TimeScope ts(c, ol_ctx::T_FINAL);
+            OL_NCCL(c, nccl_api(nullptr)->allGather(c->payload_d, c->gather_d, P * sizeof(uint4), ncclUint8, c->comm,
+                                                    c->stream));
+        }
+        st = finalize_impl(c, c->gather_d, c->world);
+        if (st) return st;
+        return nccl_poll(c);
+    }
     if (c->world == 1) return finalize_impl(c, c->payload_d, 1);
     return OL_OK;
 }
@@ -1085,6 +1218,7 @@ ol_status ol_p2p_emulate(ol_ctx **ctxs, int32_t world) {
 
 // ---------------------------------------------------------------- results
 static ol_status check_flags(ol_ctx *c) {
+    if (ol_status e = nccl_poll(c)) return e;
     int fl[2];
     OL_CUDA(c, cudaMemcpyAsync(fl, c->flags_d, sizeof(fl), cudaMemcpyDeviceToHost, c->stream));
     OL_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -1306,6 +1440,9 @@ ol_status ol_shift_rescore(ol_ctx *c, const float *qprof, int32_t on_device) {
     sa.cand = c->cand_d; sa.subs = c->subs_d; sa.prof = c->prof; sa.qprof = qp; sa.keys = c->shift_keys;
     sa.n_cand = c->n_cand; sa.W = W; sa.M = c->M;
     if (c->n_cand) OL_LAUNCH(c, launch_shift(sa, c->stream));
+    if (c->comm && c->n_cand)   // ranks scored only their own rows: keep the least key of every candidate
+        OL_NCCL(c, nccl_api(nullptr)->allReduce(c->shift_keys, c->shift_keys, c->n_cand, ncclUint64, ncclMin, c->comm,
+                                                c->stream));
     c->shift_ready = true;
     return OL_OK;
 }
@@ -1398,6 +1535,13 @@ ol_status ol_get_stat(ol_ctx *c, const char *key, int64_t *value) {
     else if (!strcmp(key, "used_pair")) *value = c->used_pair ? 1 : 0;
     else if (!strcmp(key, "tc_k")) *value = (int64_t)c->tc_kf;
     else if (!strcmp(key, "tc_ok")) *value = c->tc_ok ? 1 : 0;
+    else if (!strcmp(key, "nccl")) *value = c->comm ? 1 : 0;
+    else if (!strcmp(key, "nccl_version")) {
+        int v = 0;
+        const NcclApi *api = nccl_api(nullptr);
+        if (api) api->getVersion(&v);
+        *value = v;
+    }
     else if (!strncmp(key, "time_", 5)) {
         // time_seed_ns / time_scan_ns / time_merge_ns / time_final_ns: summed over the
         // launches since the last read (then released); time_*_n: how many launches

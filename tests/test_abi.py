@@ -61,19 +61,45 @@ def test_create_without_gpu_fails_cleanly():
     import torch
     if torch.cuda.is_available():
         pytest.skip("GPU present")
-    cfg = ol.ol_config(0, 0, 1, None, 64, 16)
+    cfg = ol.ol_config(0, 0, 1, None, 64, 16, None)
     h = ctypes.c_void_p()
     st = ol.lib().ol_create(ctypes.byref(cfg), ctypes.byref(h))
     assert st == ol.OL_ERR_CUDA and not h.value
     assert b"CUDA" in ol.lib().ol_last_error(None) or len(ol.lib().ol_last_error(None)) > 0
-    bad = ol.ol_config(0, 0, 1, None, 32, 16)
+    bad = ol.ol_config(0, 0, 1, None, 32, 16, None)
     assert ol.lib().ol_create(ctypes.byref(bad), ctypes.byref(h)) == ol.OL_ERR_DIMENSION_MISMATCH
     with pytest.raises(RuntimeError):
         ol.Engine(0)
 
 
-def test_struct_layouts_match_header():
-    assert ctypes.sizeof(ol.ol_config) == 32
-    assert ctypes.sizeof(ol.ol_params) == 32
-    assert ol.CANDIDATE_DTYPE.itemsize == 32
-    assert ol.ESTIMATE_DTYPE.itemsize == 1072
+def test_struct_layouts_match_header(tmp_path):
+    """The binding's ctypes / numpy layouts equal what a C compiler makes of the header."""
+    src = tmp_path / "layout.c"
+    src.write_text(r"""
+#include <stddef.h>
+#include <stdio.h>
+#include "omniloc.h"
+int main(void) {
+    printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(ol_config), offsetof(ol_config, nccl_unique_id),
+           sizeof(ol_params), sizeof(ol_candidate), sizeof(ol_estimate), offsetof(ol_estimate, ranked),
+           sizeof(ol_db_desc), offsetof(ol_db_desc, grid_w));
+    return 0;
+}
+""")
+    exe = tmp_path / "layout"
+    import subprocess
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = [int(v) for v in subprocess.check_output([str(exe)]).split()]
+    assert got == [ctypes.sizeof(ol.ol_config), ol.ol_config.nccl_unique_id.offset, ctypes.sizeof(ol.ol_params),
+                   ol.CANDIDATE_DTYPE.itemsize, ol.ESTIMATE_DTYPE.itemsize, ol.ESTIMATE_DTYPE.fields["ranked"][1],
+                   ctypes.sizeof(ol.ol_db_desc), ol.ol_db_desc.grid_w.offset]
+
+
+def test_nccl_unique_id_without_gpu():
+    """ol_nccl_unique_id is a host function: NCCL is loaded on demand (dlopen) and the id
+    is 128 bytes (ncclUniqueId), fresh on every call."""
+    a = ctypes.create_string_buffer(ol.NCCL_ID_BYTES)
+    b = ctypes.create_string_buffer(ol.NCCL_ID_BYTES)
+    assert ol.lib().ol_nccl_unique_id(a) == 0 and ol.lib().ol_nccl_unique_id(b) == 0
+    assert a.raw != b.raw and any(a.raw)
+    assert ol.lib().ol_nccl_unique_id(None) == ol.OL_ERR_INVALID_ARGUMENT

@@ -148,7 +148,7 @@ def test_logical_shards_equal_single(c2, world):               # §8e sharding, 
     engines, payloads = [], []
     off = np.concatenate([[0], np.cumsum(cfg.subspace_sizes)])
     for r in range(world):
-        e = ol.Engine(0, coarse_k=16, rank=r, world=world)
+        e = ol.Engine(0, coarse_k=16, rank=r, world=world, exchange="torch")
         rows = []
         for i, n in enumerate(cfg.subspace_sizes):
             b, c = ol.shard_range(n, r, world)
@@ -161,9 +161,13 @@ def test_logical_shards_equal_single(c2, world):               # §8e sharding, 
         e.query(Q, N=15, aggregate=True, exchange=False)
         payloads.append(e.payload())
     gathered = torch.cat(payloads)
-    for e in engines:
+    ref = oracle.retrieve(cfg.subspace_sizes, F, C, Q, 15)     # Alg. 1 over the whole database
+    for r, e in enumerate(engines):
         e.finalize_gathered(gathered)
-        assert (e.topk().tobytes(), e.estimates().tobytes()) == want
+        got, est = e.topk(), e.estimates()
+        assert_candidates_equal(got, ref, f"world {world} rank {r}")
+        assert_estimates_equal(est, ref, ctx=f"world {world} rank {r}")
+        assert (got.tobytes(), est.tobytes()) == want
 
 
 def test_aggregate_standalone_vs_oracle():
@@ -302,7 +306,7 @@ def test_p2p_exchange_emulated_equals_single(c2, world):        # §8e, the peer
     off = np.concatenate([[0], np.cumsum(cfg.subspace_sizes)])
     engines = []
     for r in range(world):
-        e = ol.Engine(0, coarse_k=16, rank=r, world=world)
+        e = ol.Engine(0, coarse_k=16, rank=r, world=world, exchange="torch")
         rows = np.concatenate([np.arange(off[i] + b, off[i] + b + c) for i, n in enumerate(cfg.subspace_sizes)
                                for b, c in [ol.shard_range(n, r, world)]])
         e.upload(F[rows], C[rows], cfg.subspace_sizes, cfg.spec.grid())
@@ -319,8 +323,12 @@ def test_p2p_exchange_emulated_equals_single(c2, world):        # §8e, the peer
         for e in engines:
             e.query(Q, N=15, aggregate=True, exchange=False)
         ol.p2p_emulate(engines)
+        ref = oracle.retrieve(cfg.subspace_sizes, F, C, Q, 15)
         for r, e in enumerate(engines):
-            assert (e.topk().tobytes(), e.estimates().tobytes()) == want, f"query {it} rank {r}"
+            got, est = e.topk(), e.estimates()
+            assert_candidates_equal(got, ref, f"query {it} rank {r}")
+            assert_estimates_equal(est, ref, ctx=f"query {it} rank {r}")
+            assert (got.tobytes(), est.tobytes()) == want, f"query {it} rank {r}"
         if it == 2:   # a re-open (new mailboxes, epochs restart)
             for r, e in enumerate(engines):
                 e.p2p_open(world, r, cap * 2)

@@ -86,7 +86,7 @@ def test_shift_keys_min_combine_over_logical_shards():
     want = one.shift_rescore(QP)
     engines, pays = [], []
     for rk in range(2):
-        e = ol.Engine(0, rank=rk, world=2)
+        e = ol.Engine(0, rank=rk, world=2, exchange="torch")
         b, c = ol.shard_range(600, rk, 2)
         e.upload(F[b:b + c], C[b:b + c], [600], spec.grid()); e.upload_profiles(P[b:b + c])
         e.query(Q, N=9, aggregate=False, exchange=False)
@@ -104,3 +104,9 @@ def test_shift_keys_min_combine_over_logical_shards():
     kmin = np.minimum(keys[0], keys[1]).view(np.uint64)
     assert np.array_equal((kmin & 0xFFFFFFFF).astype(np.uint32), want[0])
     assert np.array_equal((kmin >> 32).astype(np.uint32), want[1].view(np.uint32))
+    # and against the oracle's shift distance of every candidate (NEXT-1, DESIGN R21)
+    cands = engines[0].topk()
+    for i in range(len(cands)):
+        d2, s = oracle.shift_distance(QP[cands["bundle"][i], 0], P[cands["frame"][i]])
+        assert int(kmin[i] & 0xFFFFFFFF) == s
+        assert int(kmin[i] >> 32) == int(np.float32(d2).view(np.uint32))
