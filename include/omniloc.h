@@ -224,6 +224,15 @@ OL_API ol_status ol_payload_copy(ol_ctx *ctx, void *dst);
  * NOT_READY (no preceding ol_query), INVALID_ARGUMENT (world mismatch), CUDA. */
 OL_API ol_status ol_finalize(ol_ctx *ctx, const void *gathered, int32_t world);
 
+/* The pruning thresholds of the last query: [frames][subspace] acc bits (fp32, ordered
+ * as unsigned), owned by the context, valid until the next ol_query.  Before the scan
+ * they hold the seed (an upper bound of the N-th smallest acc of every (frame,
+ * subspace)); after it, the running minimum the scan converged to.  Introspection and
+ * multi-rank experiments (option "tc_debug" 512 stops ol_query after the seed; 64 makes
+ * the next ol_query start from the values found here instead of seeding -- exact only if
+ * they are such upper bounds).  Errors: INVALID_ARGUMENT, NOT_READY. */
+OL_API ol_status ol_thresholds(ol_ctx *ctx, void **dev_ptr, uint64_t *count);
+
 /* ---- peer-memory exchange (NVLink / NVSwitch, one node) --------------------
  * The cross-GPU step as one kernel instead of an NCCL all-gather +
  * ol_finalize: every rank stores its payload straight into slot `rank` of every
@@ -256,6 +265,16 @@ OL_API ol_status ol_p2p_finalize(ol_ctx *ctx);
  * launch (group g = rank g, mailboxes local): ctxs[g] opened with
  * ol_p2p_open(world, g, ..), each after its ol_query.  Synchronises. */
 OL_API ol_status ol_p2p_emulate(ol_ctx **ctxs, int32_t world);
+
+/* Tests / measurements: link `world` contexts on ONE device as if they were ranks sharing
+ * thresholds during the scan (what NCCL mode does over peer memory at world > 1): each
+ * context's tensor-core scan MIN-s every threshold it publishes into the other contexts'
+ * threshold arrays.  Use only with contexts that query the same frames in lock-step, each
+ * after all of them ran that shape once (the arrays must be allocated); destroying a
+ * context unlinks it; world = 1 unlinks ctxs[0].  Nothing waits on anything, so the
+ * contexts' queries may run concurrently on separate streams.  Errors: INVALID_ARGUMENT
+ * (NULL, different devices, a context owning a NCCL communicator). */
+OL_API ol_status ol_tau_share_emulate(ol_ctx **ctxs, int32_t world);
 
 /* ---- results ------------------------------------------------------------- */
 
@@ -382,7 +401,17 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *   "scan2"         1 (default) / 0 / 2: small-batch CUDA-core kernel choice
  *   "ctas"          cap on resident CTAs (0 = automatic)
  *   "time_kernels"  1 / 0: per-stage CUDA-event timing (stats "time_{seed,scan,merge,final}_ns")
- *   "tc_debug"      profiling only (results invalid when nonzero)
+ *   "tc_debug"      profiling only (results invalid when nonzero; host-side bits 64 = keep
+ *                   the thresholds found in ol_thresholds instead of seeding, 512 = stop
+ *                   after the seed)
+ *   "tau_share"     1 (default) / 0: NCCL mode at world > 1: the tensor-core scan MIN-s every
+ *                   threshold it publishes into the other ranks' threshold arrays over peer
+ *                   memory (handles exchanged collectively through the communicator); any
+ *                   rank's published threshold bounds the global N-th best, so results are
+ *                   identical and small shards prune as well as the whole database
+ *   "poison"        0 (default) / 1: tests (an initcheck stand-in): the next uploads fill padding
+ *                   rows and coords with NaN bytes instead of zeros, and every query first
+ *                   fills its scratch and output buffers with garbage; results must not change
  *   "graph"         0 (default) / 1: CUDA-graph replay for repeated query shapes (world 1,
  *                   time_kernels off).  The first ol_query of a shape runs eagerly and then
  *                   captures its launch sequence on a private stream; later calls with the
@@ -397,6 +426,7 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
 OL_API ol_status ol_set_option(ol_ctx *ctx, const char *key, int64_t value);
 
 /* Read statistics of the last query: "nccl" (1 if the context owns a communicator),
+ * "tau_peers" (other ranks' threshold arrays the tensor-core scan publishes into),
  * "nccl_version" (of the loaded NCCL, 0 if none), "survivors" (pairs that passed the coarse
  * bound), "pairs" (pairs scanned), "kernels" (kernel launches of the last
  * ol_query + ol_finalize), "used_tc" / "used_pair" (1 if the tensor-core scan / CTA pairs

@@ -22,7 +22,9 @@ __all__ = ["Engine", "OmnilocError", "lib", "select_window", "shard_range", "CAN
            "ESTIMATE_DTYPE", "PAYLOAD_RECORD_BYTES", "build"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libomniloc.so")
+# OL_LIB=checked loads the bounds-checked build (tests / tools/sanitize_cases.py only)
+LIB_PATH = os.path.join(_HERE, "libomniloc_checked.so" if os.environ.get("OL_LIB") == "checked"
+                        else "libomniloc.so")
 
 OL_OK, OL_ERR_INVALID_ARGUMENT, OL_ERR_DIMENSION_MISMATCH, OL_ERR_NONFINITE = 0, -1, -2, -3
 OL_ERR_OUT_OF_RANGE, OL_ERR_OOM, OL_ERR_CUDA, OL_ERR_NOT_READY, OL_ERR_EMPTY = -4, -5, -6, -7, -8
@@ -101,12 +103,14 @@ def lib():
             "ol_upload_db": ([P, ctypes.POINTER(ol_db_desc)], i32),
             "ol_query": ([P, u32, u32, P, i32, ctypes.POINTER(ol_params), i32], i32),
             "ol_payload": ([P, ctypes.POINTER(P), ctypes.POINTER(u64)], i32),
+            "ol_thresholds": ([P, ctypes.POINTER(P), ctypes.POINTER(u64)], i32),
             "ol_payload_copy": ([P, P], i32),
             "ol_finalize": ([P, P, i32], i32),
             "ol_p2p_open": ([P, i32, i32, u64, P], i32),
             "ol_p2p_connect": ([P, P], i32),
             "ol_p2p_finalize": ([P], i32),
             "ol_p2p_emulate": ([ctypes.POINTER(P), i32], i32),
+            "ol_tau_share_emulate": ([ctypes.POINTER(P), i32], i32),
             "ol_candidate_count": ([P, ctypes.POINTER(u64)], i32),
             "ol_get_topk": ([P, P, u64, ctypes.POINTER(u64)], i32),
             "ol_topk_device": ([P, ctypes.POINTER(P), ctypes.POINTER(u64)], i32),
@@ -358,6 +362,17 @@ class Engine:
         """Finalize with payloads gathered by the caller (device tensor, rank order)."""
         self._ck(lib().ol_finalize(self._h, ctypes.c_void_p(gathered.data_ptr()), self.world))
 
+    def thresholds(self):
+        """Zero-copy device view (torch int32, [frames * subspaces]) of the last query's
+        pruning thresholds (acc bits of non-negative floats, < 2^31, as int32); see ol_thresholds."""
+        ptr = ctypes.c_void_p(); n = ctypes.c_uint64()
+        self._ck(lib().ol_thresholds(self._h, ctypes.byref(ptr), ctypes.byref(n)))
+
+        class _View:
+            __cuda_array_interface__ = {"shape": (n.value,), "typestr": "<i4", "data": (ptr.value, False),
+                                        "version": 3, "strides": None}
+        return self._torch.as_tensor(_View(), device=self.device)
+
     def payload(self):
         """This rank's payload as a new device uint8 tensor."""
         ptr = ctypes.c_void_p(); nbytes = ctypes.c_uint64()
@@ -514,6 +529,13 @@ def _host_staged(t, group) -> bool:
     """gloo moves host tensors only: device tensors are staged through the host."""
     import torch.distributed as dist
     return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def tau_share_emulate(engines):
+    """Tests / measurements: link engines on one GPU so their tensor-core scans share
+    thresholds as NCCL-mode ranks do over peer memory (ol_tau_share_emulate)."""
+    arr = (ctypes.c_void_p * len(engines))(*[e._h.value for e in engines])
+    _check(lib().ol_tau_share_emulate(arr, len(engines)), engines[0]._h)
 
 
 def exchange_payloads(src, dst, group=None):

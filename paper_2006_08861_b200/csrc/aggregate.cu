@@ -11,6 +11,7 @@
 //   4. the first ranked tile whose circle > toler_per * total (strict)
 //      wins; if none does, the ranked tile with the largest circle (earliest
 //      rank on ties) flagged low-confidence (R12).
+#define OL_TU 3
 #include "ol_internal.h"
 
 namespace ol {
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
     }
     uint32_t P = 1;
     while (P < total) P <<= 1;
+    if (!OL_DCHECK(P <= cap && cap <= (uint32_t)kAggMax)) return;   // the sort fits the shared arrays
     u64 *keys = reinterpret_cast<u64 *>(smem);          // [P]  sorted candidate tiles
     u64 *dtile = keys + cap;                            // [P]  occupied tiles
     uint32_t *dcount = reinterpret_cast<uint32_t *>(dtile + cap);  // [P]
@@ -196,5 +198,7 @@ cudaError_t launch_aggregate(const AggArgs &a, cudaStream_t s) {
     aggregate_kernel<<<a.n_bundles, kAggThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
+
+OL_CHECK_EXPORT(check_aggregate)
 
 }  // namespace ol

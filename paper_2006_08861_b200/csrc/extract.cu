@@ -11,6 +11,7 @@
 // advanced by one complex rotation in between.
 // Parity with the oracle is within a few ulps of binary64 (summation order of the
 // norm differs); the fp32 descriptor is RN32 of the binary64 value.
+#define OL_TU 6
 #include "ol_internal.h"
 
 namespace ol {
@@ -86,5 +87,7 @@ cudaError_t launch_extract(const double *prof, uint64_t n, uint32_t W, float *ou
     extract_kernel<<<(unsigned)blocks, 32 * kExtractWarps, smem, s>>>(prof, n, W, out32, out64, degenerate);
     return cudaGetLastError();
 }
+
+OL_CHECK_EXPORT(check_extract)
 
 }  // namespace ol

@@ -10,6 +10,7 @@
 //    these rows itself (one launch fewer); candidates_kernel serves the W > 1 merge.
 // Keys (acc bits << 32 | frame) are unique within a subspace apart from the
 // all-ones pad, so "N rounds of extract-the-minimum" is the exact top-N.
+#define OL_TU 2
 #include "ol_internal.h"
 
 namespace ol {
@@ -46,6 +47,10 @@ __global__ void __launch_bounds__(kMergeThreads) merge_chunks_kernel(MergeArgs a
     if (gw >= a.nq * a.n_sub) return;
     const uint32_t q = gw / a.n_sub, i = gw % a.n_sub;
     const SubInfo si = a.subs[i];
+    // the subspace's work items exist; its candidate rows fit the candidate array
+    if (!OL_DCHECK(si.chunk_begin <= si.chunk_end && si.chunk_end <= a.n_items &&
+                   (!a.cand || (uint64_t)(q + 1) * a.sub_prefix[a.n_sub] <= a.n_cand)))
+        return;
     const uint32_t nk = (si.chunk_end - si.chunk_begin) * a.N;
     const u64 *src = a.partial + ((size_t)q * a.n_items + si.chunk_begin) * a.N;
     uint4 *dst = a.records + ((size_t)q * a.n_sub + i) * a.N;
@@ -68,8 +73,10 @@ __global__ void __launch_bounds__(kMergeThreads) merge_chunks_kernel(MergeArgs a
             } else {
                 const uint32_t frame = (uint32_t)best;
                 const uint64_t row = si.row_begin + (frame - si.shard_begin);
-                rec = make_uint4((uint32_t)(best >> 32), frame, (uint32_t)a.coords[2 * row],
-                                 (uint32_t)a.coords[2 * row + 1]);
+                // a winner is a row of this rank's slice of this subspace
+                const bool ok = OL_DCHECK(frame >= si.shard_begin && frame - si.shard_begin < si.count);
+                rec = make_uint4((uint32_t)(best >> 32), frame, ok ? (uint32_t)a.coords[2 * row] : 0u,
+                                 ok ? (uint32_t)a.coords[2 * row + 1] : 0u);
             }
             dst[r] = rec;
             if (r < c) co[r] = make_candidate(rec, i, q, a.M);
@@ -203,7 +210,8 @@ __global__ void candidates_kernel(CandArgs a) {
     const uint32_t q = (uint32_t)(t / ((uint64_t)a.N * a.n_sub));
     const uint32_t c = a.sub_prefix[i + 1] - a.sub_prefix[i];
     if (r >= c) return;
-    a.out[(uint64_t)q * a.sub_prefix[a.n_sub] + a.sub_prefix[i] + r] = make_candidate(a.records[t], i, q, a.M);
+    if (OL_DCHECK((uint64_t)q * a.sub_prefix[a.n_sub] + a.sub_prefix[i] + r < a.n_cand))
+        a.out[(uint64_t)q * a.sub_prefix[a.n_sub] + a.sub_prefix[i] + r] = make_candidate(a.records[t], i, q, a.M);
 }
 
 cudaError_t launch_candidates(const CandArgs &a, cudaStream_t s) {
@@ -211,5 +219,7 @@ cudaError_t launch_candidates(const CandArgs &a, cudaStream_t s) {
     candidates_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(a);
     return cudaGetLastError();
 }
+
+OL_CHECK_EXPORT(check_merge)
 
 }  // namespace ol

@@ -11,6 +11,42 @@ namespace ol {
 
 typedef unsigned long long u64;
 
+// ---- checked build (-DOL_CHECKED: libomniloc_checked.so, _build.py) ------------------
+// compute-sanitizer is closed on this GPU pool, so every kernel states the index
+// invariants its global / shared accesses rely on with OL_DCHECK(cond).  In the checked
+// library a failed check records (translation unit << 24 | line) of the first failure in
+// a device word that ol_get_stat("check") reads back (and the guarded access is skipped);
+// in the product library OL_DCHECK is the constant true and generates no code.
+#ifndef OL_TU
+#define OL_TU 0
+#endif
+#ifdef OL_CHECKED
+static __device__ unsigned int g_ol_check;
+__device__ __forceinline__ bool ol_check(bool ok, unsigned line) {
+    if (!ok) atomicCAS(&g_ol_check, 0u, ((unsigned)OL_TU << 24) | line);
+    return ok;
+}
+#define OL_DCHECK(cond) ::ol::ol_check((cond), __LINE__)
+#define OL_CHECK_EXPORT(fn)                                                        \
+    uint32_t fn(bool reset) {                                                      \
+        unsigned v = 0, z = 0;                                                     \
+        cudaMemcpyFromSymbol(&v, g_ol_check, sizeof(v));                           \
+        if (reset) cudaMemcpyToSymbol(g_ol_check, &z, sizeof(z));                  \
+        return v;                                                                  \
+    }
+#else
+#define OL_DCHECK(cond) true
+#define OL_CHECK_EXPORT(fn) \
+    uint32_t fn(bool) { return 0; }
+#endif
+// first failed check of each translation unit (0 = none); reset clears it
+uint32_t check_scan(bool reset);
+uint32_t check_merge(bool reset);
+uint32_t check_aggregate(bool reset);
+uint32_t check_tcscan(bool reset);
+uint32_t check_shift(bool reset);
+uint32_t check_extract(bool reset);
+
 constexpr int kK = OL_K;
 constexpr int kScanThreads = 256;
 constexpr int kScanWarps = kScanThreads / 32;
@@ -54,6 +90,7 @@ struct ScanArgs {
     u64 *partial;                // [nq][n_items][N]
     unsigned long long *stat_survivors;  // may be null
     uint32_t nq, n_items, n_qtiles, qt, n_sub, N;
+    uint64_t rows_pad;           // device rows (bounds checks)
 };
 
 struct SeedArgs {
@@ -62,6 +99,7 @@ struct SeedArgs {
     uint32_t *tau0;              // [nq][n_sub]
     uint32_t nq, n_sub, N, samples, kc, splits;   // splits: independent samples per (frame, sub)
     uint32_t *scratch;           // [nq][n_sub][splits][samples] acc bits (seed_acc -> seed_select)
+    uint64_t rows_pad;           // device rows (bounds checks)
 };
 
 struct MergeArgs {
@@ -74,6 +112,7 @@ struct MergeArgs {
     ol_candidate *cand;
     const uint32_t *sub_prefix;  // [n_sub+1] prefix of min(N, |n_i|)
     uint32_t M;
+    uint64_t n_cand;             // candidate rows (bounds checks)
 };
 
 struct RankMergeArgs {
@@ -83,6 +122,7 @@ struct RankMergeArgs {
 };
 
 constexpr int kXchgMax = 8;   // ranks of the peer-memory exchange (one NVSwitch node)
+static_assert(kXchgMax - 1 <= 7, "TcScanArgs::peer_tau");
 constexpr uint32_t kXchgBlocks = 16;   // blocks per rank of xchg_merge_kernel (fixed: the arrival counters count them)
 
 struct XchgArgs {
@@ -99,6 +139,7 @@ struct CandArgs {
     const uint32_t *sub_prefix;  // [n_sub+1] prefix of min(N, |n_i|)
     ol_candidate *out;
     uint32_t nq, n_sub, N, M;
+    uint64_t n_cand;             // candidate rows (bounds checks)
 };
 
 struct AggArgs {
@@ -137,6 +178,12 @@ struct TcScanArgs {
     uint32_t kf;                  // filter on the first kf of K dimensions (16..64, multiple of 16)
     uint32_t pw;                  // fp16 plane / frame row width in halves: 64 (128-B rows, SW128) or 32 (kf = 32: 64-B rows, SW64)
     unsigned long long *prof;     // [16] per-role cycle counters when dbg & 32 (profiling only)
+    // other ranks' threshold arrays (same [nq][n_sub] layout, peer memory over NVLink): every
+    // threshold this CTA publishes is also MIN-ed into them (each is a valid bound for every
+    // rank: the N-th best of N real rows of the subspace), so small shards converge like the
+    // whole database would
+    uint32_t *peer_tau[7];
+    uint32_t n_peer;
 };
 
 constexpr u64 kShiftPad = 0x7FFFFFFFFFFFFFFFull;   // "not scored on this rank" (MIN-reducible)
@@ -149,6 +196,7 @@ struct ShiftArgs {
     u64 *keys;                    // [n_cand]
     uint64_t n_cand;
     uint32_t W, M;
+    uint32_t nq;                  // query frames (bounds checks)
 };
 
 // launchers (return cudaGetLastError())

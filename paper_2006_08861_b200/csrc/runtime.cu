@@ -23,6 +23,7 @@
 #include <dlfcn.h>
 #include <mutex>
 #include <nccl.h>   // types and signatures only: the library is loaded on demand (dlopen)
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing unless a profiler attaches
 
 #include "ol_internal.h"
 
@@ -83,6 +84,15 @@ struct ol_ctx {
     cudaStream_t stream = nullptr;  // borrowed (NULL = legacy default stream)
     ncclComm_t comm = nullptr;      // owned; set when ol_config carried a NCCL unique id
     uint4 *gather_d = nullptr; size_t gather_cap = 0;   // [world][payload] all-gathered records
+    // in-scan threshold sharing (NCCL mode at world > 1, option "tau_share"): the other ranks'
+    // threshold arrays, opened by CUDA IPC after a collective exchange of handles whenever the
+    // (identically sized) arrays are reallocated
+    void *tau_peer[kXchgMax] = {};
+    size_t tau_shared_cap = 0;
+    unsigned char *hbuf_d = nullptr;
+    int64_t opt_tau_share = 1;
+    int64_t opt_poison = 0;            // tests: fill padding and per-query outputs with garbage first
+    std::vector<ol_ctx *> emu_peers;   // tests: contexts on this device linked by ol_tau_share_emulate
     std::string err = "no error";
     // database
     bool db_ready = false;
@@ -229,9 +239,20 @@ static cudaEvent_t take_event(ol_ctx *c) {
     return e;
 }
 
-struct TimeScope {  // records an event pair around a launch when timing is on
+// NVTX range (host timeline of the launch sequence, for nsys / ncu --nvtx)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
+struct TimeScope {  // a stage of the launch sequence: an NVTX range, and an event pair when timing is on
     ol_ctx *c; int cls; cudaEvent_t a = nullptr;
-    TimeScope(ol_ctx *c_, int cls_) : c(c_), cls(cls_) {
+    NvtxRange nv;
+    static const char *name(int cls) {
+        static const char *n[] = {"ol.seed", "ol.scan", "ol.merge", "ol.finalize"};
+        return n[cls];
+    }
+    TimeScope(ol_ctx *c_, int cls_) : c(c_), cls(cls_), nv(name(cls_)) {
         if (c->opt_time) { a = take_event(c); cudaEventRecord(a, c->stream); }
     }
     ~TimeScope() {
@@ -428,6 +449,14 @@ void ol_destroy(ol_ctx *c) {
         c->comm = nullptr;
     }
     cudaFree(c->gather_d);
+    for (auto &p : c->tau_peer)
+        if (p) { cudaIpcCloseMemHandle(p); p = nullptr; }
+    cudaFree(c->hbuf_d);
+    for (ol_ctx *o : c->emu_peers) {   // unlink from the emulated group
+        auto &v = o->emu_peers;
+        for (size_t i = 0; i < v.size(); ++i)
+            if (v[i] == c) { v.erase(v.begin() + i); break; }
+    }
     free_db(c);
     cudaFree(c->seed_scratch); cudaFree(c->sitems_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
@@ -480,6 +509,7 @@ ol_status ol_select_window(uint32_t n_frames, uint32_t m, uint32_t M, uint32_t *
 
 // ---------------------------------------------------------------- database
 ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
+    NvtxRange nv("ol_upload_db");
     if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!db || db->n_subspaces == 0 || !db->global_sizes || !db->features || !db->coords)
         return fail(c, OL_ERR_INVALID_ARGUMENT, "database descriptor incomplete");
@@ -527,13 +557,15 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
     const int kc = c->kc;
     const uint64_t R = rows_pad ? rows_pad : 32;
     OL_CUDA(c, cudaMalloc((void **)&c->coarse, sizeof(float) * R * kc));
-    OL_CUDA(c, cudaMemsetAsync(c->coarse, 0, sizeof(float) * R * kc, c->stream));   // padding rows = 0
+    // padding rows = 0 (option "poison": NaN bytes, so a padding element that is ever read shows)
+    const int fillb = c->opt_poison ? 0xFF : 0;
+    OL_CUDA(c, cudaMemsetAsync(c->coarse, fillb, sizeof(float) * R * kc, c->stream));
     if (kc < OL_K) {
         OL_CUDA(c, cudaMalloc((void **)&c->fine, sizeof(float) * R * (OL_K - kc)));
-        OL_CUDA(c, cudaMemsetAsync(c->fine, 0, sizeof(float) * R * (OL_K - kc), c->stream));
+        OL_CUDA(c, cudaMemsetAsync(c->fine, fillb, sizeof(float) * R * (OL_K - kc), c->stream));
     }
     OL_CUDA(c, cudaMalloc((void **)&c->coords, sizeof(int32_t) * 2 * R));
-    OL_CUDA(c, cudaMemsetAsync(c->coords, 0, sizeof(int32_t) * 2 * R, c->stream));
+    OL_CUDA(c, cudaMemsetAsync(c->coords, fillb, sizeof(int32_t) * 2 * R, c->stream));
     OL_CUDA(c, cudaMalloc((void **)&c->subs_d, sizeof(SubInfo) * ns));
     const float *src = db->features;
     float *tmp = nullptr;
@@ -781,6 +813,7 @@ static void capture_query(ol_ctx *c, const ol_ctx::QueryKey &k, uint32_t nb, uin
 // ---------------------------------------------------------------- query
 ol_status ol_query(ol_ctx *c, uint32_t nb, uint32_t M, const float *frames, int32_t on_device,
                    const ol_params *p, int32_t aggregate) {
+    NvtxRange nv("ol_query");
     if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!c->db_ready) return fail(c, OL_ERR_NOT_READY, "no database uploaded");
     ol_status st = check_params(c, p, aggregate != 0);
@@ -848,6 +881,56 @@ static ol_status share_tau(ol_ctx *c, uint32_t nq) {
     return OL_OK;
 }
 
+// Open the other ranks' threshold arrays for in-scan sharing.  Collective (NCCL mode): every
+// rank reallocates its array at the same query (identical shapes), so every rank comes here at
+// the same query.  Publishing into a peer's array is safe across queries because the seed MIN
+// all-reduce of query k+1 completes on a rank only after every rank finished its scan of k and
+// seeded k+1.  A handle that cannot be opened (no peer access) just leaves that peer out.
+static ol_status ensure_tau_peers(ol_ctx *c) {
+    if (!c->comm || c->world == 1 || !c->opt_tau_share || c->tau_shared_cap == c->tau_cap) return OL_OK;
+    for (auto &p : c->tau_peer)
+        if (p) { cudaIpcCloseMemHandle(p); p = nullptr; }
+    constexpr size_t H = sizeof(cudaIpcMemHandle_t);
+    std::vector<unsigned char> hs((size_t)c->world * H, 0);
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, c->tau0_d) == cudaSuccess) memcpy(&hs[(size_t)c->rank * H], &h, H);
+    cudaGetLastError();
+    if (!c->hbuf_d) OL_CUDA(c, cudaMalloc((void **)&c->hbuf_d, kXchgMax * H));
+    OL_CUDA(c, cudaMemcpyAsync(c->hbuf_d + (size_t)c->rank * H, &hs[(size_t)c->rank * H], H, cudaMemcpyHostToDevice,
+                               c->stream));
+    OL_NCCL(c, nccl_api(nullptr)->allGather(c->hbuf_d + (size_t)c->rank * H, c->hbuf_d, H, ncclUint8, c->comm,
+                                            c->stream));
+    OL_CUDA(c, cudaMemcpyAsync(hs.data(), c->hbuf_d, (size_t)c->world * H, cudaMemcpyDeviceToHost, c->stream));
+    OL_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (int p = 0; p < c->world && p < kXchgMax; ++p) {
+        if (p == c->rank) continue;
+        bool any = false;
+        for (size_t b = 0; b < H; ++b) any |= hs[(size_t)p * H + b] != 0;
+        if (!any) continue;
+        memcpy(&h, &hs[(size_t)p * H], H);
+        if (cudaIpcOpenMemHandle(&c->tau_peer[p], h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            c->tau_peer[p] = nullptr;
+            cudaGetLastError();
+        }
+    }
+    c->tau_shared_cap = c->tau_cap;
+    return OL_OK;
+}
+
+// the peer threshold arrays the scan publishes into (NCCL mode, or an emulated group)
+static uint32_t peer_taus(const ol_ctx *c, uint64_t need, uint32_t **out) {
+    uint32_t n = 0;
+    if (!c->opt_tau_share) return 0;
+    if (c->comm) {
+        for (int p = 0; p < kXchgMax && n < kXchgMax - 1; ++p)
+            if (c->tau_peer[p]) out[n++] = (uint32_t *)c->tau_peer[p];
+    } else {
+        for (const ol_ctx *o : c->emu_peers)   // tests: all linked contexts ran this shape (tau_cap >= need)
+            if (n < kXchgMax - 1 && o->tau0_d && o->tau_cap >= need) out[n++] = o->tau0_d;
+    }
+    return n;
+}
+
 static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, int32_t on_device,
                             const ol_params *p, int32_t aggregate, uint64_t per_q) {
     const uint64_t nq64 = (uint64_t)nb * M;
@@ -888,9 +971,27 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
     const uint32_t n_items = (uint32_t)c->n_items();
 
     // buffers
-    OL_CUDA(c, grow(&c->tau0_d, &c->tau_cap, (size_t)nq * c->n_sub));
+    {   // (NCCL mode: whole powers of two, so the shared arrays are rarely reallocated and re-exchanged)
+        size_t want = (size_t)nq * c->n_sub;
+        if (c->comm && c->world > 1) { size_t r = 4096; while (r < want) r <<= 1; want = r; }
+        OL_CUDA(c, grow(&c->tau0_d, &c->tau_cap, want));
+    }
     OL_CUDA(c, grow(&c->partial_d, &c->partial_cap, (size_t)nq * (n_items ? n_items : 1) * N));
     OL_CUDA(c, grow(&c->payload_d, &c->payload_cap, (size_t)nq * c->n_sub * N));
+    if (c->opt_poison) {   // every per-query output must be written before it is read: fill them with garbage
+        OL_CUDA(c, grow(&c->cand_d, &c->cand_cap, per_q * nq));
+        OL_CUDA(c, grow(&c->final_d, &c->final_cap, (size_t)nq * c->n_sub * N));
+        OL_CUDA(c, grow(&c->est_d, &c->est_cap, nb));
+        OL_CUDA(c, cudaMemsetAsync(c->partial_d, 0xA5, sizeof(u64) * c->partial_cap, c->stream));
+        OL_CUDA(c, cudaMemsetAsync(c->payload_d, 0xA5, sizeof(uint4) * c->payload_cap, c->stream));
+        OL_CUDA(c, cudaMemsetAsync(c->cand_d, 0xA5, sizeof(ol_candidate) * c->cand_cap, c->stream));
+        OL_CUDA(c, cudaMemsetAsync(c->final_d, 0xA5, sizeof(uint4) * c->final_cap, c->stream));
+        OL_CUDA(c, cudaMemsetAsync(c->est_d, 0xA5, sizeof(ol_estimate) * c->est_cap, c->stream));
+        if (c->gather_d) OL_CUDA(c, cudaMemsetAsync(c->gather_d, 0xA5, sizeof(uint4) * c->gather_cap, c->stream));
+        if (c->seed_scratch) OL_CUDA(c, cudaMemsetAsync(c->seed_scratch, 0xA5, sizeof(uint32_t) * c->seed_scratch_cap, c->stream));
+        if (c->q16) OL_CUDA(c, cudaMemsetAsync(c->q16, 0xA5, sizeof(uint16_t) * c->q16_cap, c->stream));
+        if (c->qmeta) OL_CUDA(c, cudaMemsetAsync(c->qmeta, 0xA5, sizeof(float4) * c->qmeta_cap, c->stream));
+    }
     OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 2 * sizeof(int), c->stream));
     OL_CUDA(c, cudaMemsetAsync(c->stat_d, 0, 2 * sizeof(unsigned long long), c->stream));
     if (on_device) OL_LAUNCH(c, launch_check_finite(q, nq64 * OL_K, c->flags_d, c->stream));
@@ -906,6 +1007,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         SeedArgs sa;
         sa.coarse = c->coarse; sa.fine = c->fine; sa.queries = q; sa.subs = c->subs_d;
         sa.tau0 = c->tau0_d; sa.nq = nq; sa.n_sub = c->n_sub; sa.N = N; sa.kc = (uint32_t)c->kc;
+        sa.rows_pad = c->rows_pad;
         // splits x (count/8, at most 4096) rows per subspace, about 64k sampled pairs per
         // row... i.e. more splits for few frames; below N rows per split: no seed (+inf)
         // automatic: 8,192 samples for >= 1,024 (frame, subspace) jobs (1,024 frames: 1M rows
@@ -937,6 +1039,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
         OL_LAUNCH(c, launch_tau_seed(sa, c->stream));
     }
+    if (c->opt_tc_debug & 512) { c->nq = nq; return OL_OK; }   // profiling: stop after the seed (ol_thresholds reads it)
     c->used_tc = false;
     c->used_pair = false;
     if (n_items && use_tc) {
@@ -963,6 +1066,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
             return fail(c, OL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
         TcScanArgs a;
         a.bound = 0;
+        a.n_peer = 0;
         a.cluster = (uint32_t)c->opt_cluster;
         a.pair = pair ? 1u : 0u;
         a.items = c->items_d; a.blk = c->blk; a.n_blk = (uint32_t)(c->rows_pad / 32); a.qmeta = c->qmeta; a.bounds = c->tcstat_d; a.nf_max = c->nf_max;
@@ -990,6 +1094,9 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
             }
         }
         if (!(a.dbg & 64)) { st = share_tau(c, nq); if (st) return st; }
+        st = ensure_tau_peers(c);
+        if (st) return st;
+        a.n_peer = peer_taus(c, (uint64_t)nq * c->n_sub, a.peer_tau);
         TimeScope ts(c, ol_ctx::T_SCAN);
         OL_LAUNCH(c, launch_tcscan(pair ? c->map_rows_half : c->map_rows, map_q, a, (int)(n_items * n_qblocks), c->stream));
         c->used_tc = true;
@@ -999,6 +1106,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         a.coarse = c->coarse; a.fine = c->fine; a.queries = q; a.items = c->items_d;
         a.tau0 = seed ? c->tau0_d : nullptr; a.partial = c->partial_d; a.stat_survivors = c->stat_d;
         a.nq = nq; a.n_items = n_items; a.n_qtiles = n_qtiles; a.qt = qt; a.n_sub = c->n_sub; a.N = N;
+        a.rows_pad = c->rows_pad;
         if (seed) { st = share_tau(c, nq); if (st) return st; }
         TimeScope ts(c, ol_ctx::T_SCAN);
         if (qt <= 16 && c->opt_scan2 == 2 && c->kc < OL_K)   // few frames: TMA-fed row-pair kernel
@@ -1011,7 +1119,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
     MergeArgs ma;
     ma.partial = c->partial_d; ma.subs = c->cur ? c->cur->subs_d : c->subs_d; ma.coords = c->coords; ma.records = c->payload_d;
     ma.nq = nq; ma.n_items = n_items; ma.n_sub = c->n_sub; ma.N = N;
-    ma.cand = nullptr; ma.sub_prefix = nullptr; ma.M = M;
+    ma.cand = nullptr; ma.sub_prefix = nullptr; ma.M = M; ma.n_cand = per_q * nq;
     c->cand_fused = false;
     if (c->world == 1) {   // the merge also writes the candidate rows (one launch fewer)
         st = ensure_prefix(c, N);
@@ -1043,6 +1151,14 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         return nccl_poll(c);
     }
     if (c->world == 1) return finalize_impl(c, c->payload_d, 1);
+    return OL_OK;
+}
+
+ol_status ol_thresholds(ol_ctx *c, void **dev_ptr, uint64_t *count) {
+    if (!c || !dev_ptr || !count) return fail(c, OL_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!c->tau0_d) return fail(c, OL_ERR_NOT_READY, "no query");
+    *dev_ptr = c->tau0_d;
+    *count = (uint64_t)c->nq * c->n_sub;
     return OL_OK;
 }
 
@@ -1089,7 +1205,7 @@ static ol_status finalize_tail(ol_ctx *c, const uint4 *rec) {
         OL_CUDA(c, grow(&c->cand_d, &c->cand_cap, c->n_cand));
         CandArgs ca;
         ca.records = rec; ca.sub_prefix = c->prefix_d; ca.out = c->cand_d; ca.nq = nq; ca.n_sub = ns;
-        ca.N = N; ca.M = c->M;
+        ca.N = N; ca.M = c->M; ca.n_cand = c->n_cand;
         OL_LAUNCH(c, launch_candidates(ca, c->stream));
     }
     if (c->aggregate) {
@@ -1110,6 +1226,7 @@ static ol_status finalize_tail(ol_ctx *c, const uint4 *rec) {
 }
 
 ol_status ol_finalize(ol_ctx *c, const void *gathered, int32_t world) {
+    NvtxRange nv("ol_finalize");
     if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!c->q_ready) return fail(c, OL_ERR_NOT_READY, "no query to finalize");
     if (world != c->world || !gathered)
@@ -1165,6 +1282,7 @@ static void xchg_fill(XchgArgs &x, ol_ctx *c, int p, void *base) {
 }
 
 ol_status ol_p2p_finalize(ol_ctx *c) {
+    NvtxRange nv("ol_p2p_finalize");
     if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!c->q_ready) return fail(c, OL_ERR_NOT_READY, "no query to finalize");
     if (!c->p2p_ready) return fail(c, OL_ERR_NOT_READY, "ol_p2p_connect first");
@@ -1213,6 +1331,27 @@ ol_status ol_p2p_emulate(ol_ctx **ctxs, int32_t world) {
         ol_status st = finalize_tail(ctxs[g], ctxs[g]->final_d);
         if (st) return st;
     }
+    return OL_OK;
+}
+
+ol_status ol_tau_share_emulate(ol_ctx **ctxs, int32_t world) {
+    if (!ctxs || world < 1 || world > kXchgMax) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctxs / world");
+    for (int g = 0; g < world; ++g) {
+        if (!ctxs[g] || ctxs[g]->device != ctxs[0]->device || ctxs[g]->comm)
+            return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "context %d: NULL, another device, or owns a communicator", g);
+    }
+    for (int g = 0; g < world; ++g) {   // unlink from any earlier group, then link to this one
+        ol_ctx *c = ctxs[g];
+        for (ol_ctx *o : c->emu_peers) {
+            auto &v = o->emu_peers;
+            for (size_t i = 0; i < v.size(); ++i)
+                if (v[i] == c) { v.erase(v.begin() + i); break; }
+        }
+        c->emu_peers.clear();
+    }
+    for (int g = 0; g < world; ++g)
+        for (int o = 0; o < world; ++o)
+            if (o != g) ctxs[g]->emu_peers.push_back(ctxs[o]);
     return OL_OK;
 }
 
@@ -1272,6 +1411,7 @@ ol_status ol_get_estimates(ol_ctx *c, ol_estimate *out, uint32_t capacity) {
 
 ol_status ol_aggregate(ol_ctx *c, uint32_t nb, const uint32_t *offsets, const int32_t *xy,
                        int32_t on_device, const ol_params *p, ol_estimate *out) {
+    NvtxRange nv("ol_aggregate");
     if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
     ol_status st = check_params(c, p, true);
     if (st) return st;
@@ -1420,6 +1560,7 @@ ol_status ol_extract_features(ol_ctx *c, const double *profiles, uint64_t n, uin
 }
 
 ol_status ol_shift_rescore(ol_ctx *c, const float *qprof, int32_t on_device) {
+    NvtxRange nv("ol_shift_rescore");
     if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!c->finalized) return fail(c, OL_ERR_NOT_READY, "no finalized query");
     if (!c->prof) return fail(c, OL_ERR_NOT_READY, "no profiles uploaded");
@@ -1438,7 +1579,7 @@ ol_status ol_shift_rescore(ol_ctx *c, const float *qprof, int32_t on_device) {
     OL_CUDA(c, grow(&c->shift_keys, &c->shift_cap, c->n_cand));
     ShiftArgs sa;
     sa.cand = c->cand_d; sa.subs = c->subs_d; sa.prof = c->prof; sa.qprof = qp; sa.keys = c->shift_keys;
-    sa.n_cand = c->n_cand; sa.W = W; sa.M = c->M;
+    sa.n_cand = c->n_cand; sa.W = W; sa.M = c->M; sa.nq = c->nq;
     if (c->n_cand) OL_LAUNCH(c, launch_shift(sa, c->stream));
     if (c->comm && c->n_cand)   // ranks scored only their own rows: keep the least key of every candidate
         OL_NCCL(c, nccl_api(nullptr)->allReduce(c->shift_keys, c->shift_keys, c->n_cand, ncclUint64, ncclMin, c->comm,
@@ -1501,6 +1642,8 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "tc_min_frames")) { if (v < 0) goto bad; c->opt_tc_min_frames = v; }
     else if (!strcmp(key, "tc_debug")) { if (v < 0 || v > 1023) goto bad; c->opt_tc_debug = v; }
     else if (!strcmp(key, "graph")) { if (v != 0 && v != 1) goto bad; c->opt_graph = v; }
+    else if (!strcmp(key, "tau_share")) { if (v != 0 && v != 1) goto bad; c->opt_tau_share = v; }
+    else if (!strcmp(key, "poison")) { if (v != 0 && v != 1) goto bad; c->opt_poison = v; }
     else return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown option '%s'", key);
     ++c->gen;   // every option can change the launch sequence: retire a captured graph
     return OL_OK;
@@ -1536,6 +1679,28 @@ ol_status ol_get_stat(ol_ctx *c, const char *key, int64_t *value) {
     else if (!strcmp(key, "tc_k")) *value = (int64_t)c->tc_kf;
     else if (!strcmp(key, "tc_ok")) *value = c->tc_ok ? 1 : 0;
     else if (!strcmp(key, "nccl")) *value = c->comm ? 1 : 0;
+    else if (!strcmp(key, "check") || !strcmp(key, "check_reset")) {
+        // checked library only (-DOL_CHECKED): the first failed device bounds check, as
+        // (translation unit << 24 | source line), 0 = none; always 0 in the product library
+        OL_CUDA(c, cudaDeviceSynchronize());
+        const bool r = key[5] != 0;
+        uint32_t v = 0;
+        for (uint32_t x : {check_scan(r), check_merge(r), check_aggregate(r), check_tcscan(r), check_shift(r),
+                           check_extract(r)})
+            if (!v) v = x;
+        *value = v;
+    }
+    else if (!strcmp(key, "checked")) {
+#ifdef OL_CHECKED
+        *value = 1;
+#else
+        *value = 0;
+#endif
+    }
+    else if (!strcmp(key, "tau_peers")) {
+        uint32_t *pp[kXchgMax];
+        *value = peer_taus(c, (uint64_t)c->nq * c->n_sub, pp);
+    }
     else if (!strcmp(key, "nccl_version")) {
         int v = 0;
         const NcclApi *api = nccl_api(nullptr);

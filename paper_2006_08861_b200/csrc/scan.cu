@@ -12,6 +12,7 @@
 // (acc bits << 32 | global frame).  tau = min(seeded bound, any list's N-th acc)
 // is always >= the true N-th distance, so no true top-N pair is ever pruned.
 // kc == K is the one-pass scan (NK1).
+#define OL_TU 1
 #include "ol_internal.h"
 #include "tc_ptx.cuh"
 
@@ -49,6 +50,10 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
     const WorkItem it = a.items[item_id];
     const uint32_t q0 = qtile * qt;
     const uint32_t qn = min(qt, a.nq - q0);
+    // (a work item's rows lie inside the planes, its subspace and frame tile exist)
+    if (!OL_DCHECK(item_id < a.n_items && it.row_begin + it.count <= a.rows_pad && it.sub < a.n_sub && q0 < a.nq &&
+                   qt <= kMaxQT))
+        return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     for (uint32_t i = threadIdx.x; i < qn * kK; i += blockDim.x)
@@ -240,6 +245,10 @@ __global__ void __launch_bounds__(kScanThreads) scan2_kernel(ScanArgs a) {
     const WorkItem it = a.items[item_id];
     const uint32_t q0 = qtile * qt;
     const uint32_t qn = min(qt, a.nq - q0);
+    // (a work item's rows lie inside the planes, its subspace and frame tile exist)
+    if (!OL_DCHECK(item_id < a.n_items && it.row_begin + it.count <= a.rows_pad && it.sub < a.n_sub && q0 < a.nq &&
+                   qt <= kMaxQT))
+        return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
     for (uint32_t i = threadIdx.x; i < kMaxQT2 * kK; i += blockDim.x) {
@@ -346,6 +355,10 @@ __global__ void __launch_bounds__(kScanThreads + 32) scan3_kernel(ScanArgs a) {
     const WorkItem it = a.items[item_id];
     const uint32_t q0 = qtile * qt;
     const uint32_t qn = min(qt, a.nq - q0);
+    // (a work item's rows lie inside the planes, its subspace and frame tile exist)
+    if (!OL_DCHECK(item_id < a.n_items && it.row_begin + it.count <= a.rows_pad && it.sub < a.n_sub && q0 < a.nq &&
+                   qt <= kMaxQT))
+        return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t n_stages_total = (it.count + kRows2 - 1) / kRows2;
 
@@ -573,6 +586,7 @@ __global__ void __launch_bounds__(kSeedThreads, 2) tau_seed_kernel(SeedArgs a) {
     for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) {
         // split j takes the j-th of `splits` interleaved sample grids
         const uint64_t row = si.row_begin + (((uint64_t)s * a.splits + split) * si.count) / ((uint64_t)S * a.splits);
+        if (!OL_DCHECK(row < si.row_begin + si.count && row < a.rows_pad && s < (uint32_t)kSeedMax)) continue;
         float4 f[kK / 4];   // (KC is a compile-time constant: all 16 loads issue before the chain)
 #pragma unroll
         for (int k4 = 0; k4 < kK / 4; ++k4)
@@ -655,6 +669,7 @@ __global__ void __launch_bounds__(256) seed_acc_kernel(SeedArgs a) {
     const uint32_t smp = blockIdx.y * blockDim.x + threadIdx.x;
     if (S < a.N || smp >= S) return;
     const uint64_t row = si.row_begin + (((uint64_t)smp * a.splits + split) * si.count) / ((uint64_t)S * a.splits);
+    if (!OL_DCHECK(row < si.row_begin + si.count && row < a.rows_pad && f0 + nf <= a.nq)) return;
     float4 f[kK / 4];
 #pragma unroll
     for (int k4 = 0; k4 < kK / 4; ++k4)
@@ -889,5 +904,7 @@ cudaError_t launch_check_coords(const int32_t *xy, uint64_t rows, int32_t x0, in
     check_coords_kernel<<<(unsigned)blocks, 256, 0, s>>>(xy, rows, x0, x1, y0, y1, flag);
     return cudaGetLastError();
 }
+
+OL_CHECK_EXPORT(check_scan)
 
 }  // namespace ol

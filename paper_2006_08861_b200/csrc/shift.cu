@@ -6,6 +6,7 @@
 // descriptor (FFT magnitude) is rotation invariant; this step recovers the
 // rotation it discards.  One warp per candidate: the two profiles in shared
 // memory, lane l scores shifts l, l+32, ...; a warp min over (acc bits, s) keys.
+#define OL_TU 5
 #include "ol_internal.h"
 
 namespace ol {
@@ -26,6 +27,7 @@ __global__ void __launch_bounds__(32 * kShiftWarps) shift_kernel(ShiftArgs a) {
         return;
     }
     const uint64_t row = si.row_begin + (cd.frame - si.shard_begin);
+    if (!OL_DCHECK((uint64_t)cd.bundle * a.M + cd.query_frame < a.nq && cd.query_frame < a.M)) return;
     const float *qs = a.qprof + ((uint64_t)cd.bundle * a.M + cd.query_frame) * W;
     const float *ps = a.prof + row * W;
     for (uint32_t w = lane; w < W; w += 32) { q[w] = qs[w]; p[w] = ps[w]; }
@@ -56,5 +58,7 @@ cudaError_t launch_shift(const ShiftArgs &a, cudaStream_t s) {
     shift_kernel<<<(unsigned)(blocks ? blocks : 1), 32 * kShiftWarps, smem, s>>>(a);
     return cudaGetLastError();
 }
+
+OL_CHECK_EXPORT(check_shift)
 
 }  // namespace ol

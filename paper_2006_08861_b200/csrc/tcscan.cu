@@ -40,6 +40,7 @@
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
+#define OL_TU 4
 #include "ol_internal.h"
 #include "tc_ptx.cuh"
 
@@ -200,7 +201,12 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     const uint32_t rank = kPair ? cluster_ctarank() : 0u;
     const uint32_t N = a.N;
     const uint32_t n_tiles = (it.count + kTileRows - 1) / kTileRows;
-    constexpr bool prof = kProf;   // profiling counters (tc_debug & 32): a separate instantiation
+    constexpr bool prof = kProf;
+    // a work item's rows lie inside the planes (the pre-pass: inside its strided view), its
+    // subspace and query block exist, the lists fit the frames
+    if (!OL_DCHECK(item_id < a.n_items && qblk < a.n_qblocks && it.sub < a.n_sub && a.qb <= (uint32_t)kQB &&
+                   (kBound || it.row_begin + it.count <= (uint64_t)a.n_blk * 32)))
+        return;   // (uniform over the CTA / cluster: before any barrier)   // profiling counters (tc_debug & 32): a separate instantiation
     const long long t_start = clock64();
 
     // ---------------------------------------------------------------- setup
@@ -543,23 +549,25 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                     col = eh & 0xFF;
                     const uint32_t rl = (eh >> 8) + 32 * wsel + bit;
                     const uint64_t row = it.row_begin + rl;
-                    const float4 *qv = reinterpret_cast<const float4 *>(a.queries + (size_t)(q0 + col) * kK);
-                    float acc = 0.f;
-                    float4 f[kK / 4];   // all 16 row loads in flight (one selected address each)
+                    if (OL_DCHECK(rl < it.count && col < qn && q0 + col < a.nq)) {
+                        const float4 *qv = reinterpret_cast<const float4 *>(a.queries + (size_t)(q0 + col) * kK);
+                        float acc = 0.f;
+                        float4 f[kK / 4];   // all 16 row loads in flight (one selected address each)
 #pragma unroll
-                    for (int k4 = 0; k4 < kK / 4; ++k4) {
-                        const float *src = 4 * k4 < (int)a.kc ? a.coarse + coarse_off(row, 4 * k4, a.kc)
-                                                              : a.fine + row * (kK - a.kc) + (4 * k4 - a.kc);
-                        f[k4] = __ldg(reinterpret_cast<const float4 *>(src));
-                    }
+                        for (int k4 = 0; k4 < kK / 4; ++k4) {
+                            const float *src = 4 * k4 < (int)a.kc ? a.coarse + coarse_off(row, 4 * k4, a.kc)
+                                                                  : a.fine + row * (kK - a.kc) + (4 * k4 - a.kc);
+                            f[k4] = __ldg(reinterpret_cast<const float4 *>(src));
+                        }
 #pragma unroll
-                    for (int k4 = 0; k4 < kK / 4; ++k4) {
-                        const float4 x = __ldg(qv + k4);
-                        acc = chain_step_tc(acc, x.x, f[k4].x); acc = chain_step_tc(acc, x.y, f[k4].y);
-                        acc = chain_step_tc(acc, x.z, f[k4].z); acc = chain_step_tc(acc, x.w, f[k4].w);
-                    }
-                    key = ((u64)__float_as_uint(acc) << 32) | (u64)(it.frame_begin + rl);
-                    if (!(key < lists[(size_t)col * N + N - 1])) key = kPadKey;   // cannot enter the list
+                        for (int k4 = 0; k4 < kK / 4; ++k4) {
+                            const float4 x = __ldg(qv + k4);
+                            acc = chain_step_tc(acc, x.x, f[k4].x); acc = chain_step_tc(acc, x.y, f[k4].y);
+                            acc = chain_step_tc(acc, x.z, f[k4].z); acc = chain_step_tc(acc, x.w, f[k4].w);
+                        }
+                        key = ((u64)__float_as_uint(acc) << 32) | (u64)(it.frame_begin + rl);
+                        if (!(key < lists[(size_t)col * N + N - 1])) key = kPadKey;   // cannot enter the list
+                    } else col = 0xFFFFFFFFu;
                 }
                 // insert the keys into their frames' sorted lists: lanes of distinct frames in
                 // parallel, lanes sharing a frame one after another (match groups)
@@ -578,7 +586,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 } else for (uint32_t r = 0; r <= maxrank; ++r) {
                     if (has && rank == r) {
                         u64 *L = lists + (size_t)col * N;
-                        if (key < L[N - 1]) {
+                        if (OL_DCHECK(col < qn) && key < L[N - 1]) {
                             int pidx = (int)N - 1;
                             while (pidx > 0 && L[pidx - 1] > key) { L[pidx] = L[pidx - 1]; --pidx; }
                             L[pidx] = key;
@@ -591,7 +599,9 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                     if (last != kPadKey) {
                         const uint32_t tb = (uint32_t)(last >> 32);
                         atomicMin(&s.tau[col], tb);
-                        atomicMin(&a.g_tau[(size_t)(q0 + col) * a.n_sub + it.sub], tb);
+                        const size_t ti = (size_t)(q0 + col) * a.n_sub + it.sub;
+                        atomicMin(&a.g_tau[ti], tb);
+                        for (uint32_t pr = 0; pr < a.n_peer; ++pr) atomicMin(&a.peer_tau[pr][ti], tb);   // (RED over NVLink)
                     }
                 }
                 __syncwarp();
@@ -611,7 +621,8 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     if (prof && threadIdx.x == 0) { atomicAdd(&a.prof[8], (unsigned long long)(clock64() - t_start)); atomicAdd(&a.prof[9], (unsigned long long)n_tiles); }
     for (uint32_t i = threadIdx.x; !kBound && i < qn * N; i += blockDim.x) {
         const uint32_t q = i / N, r = i % N;
-        a.partial[((size_t)(q0 + q) * a.n_items + item_id) * N + r] = lists[(size_t)q * N + r];
+        if (OL_DCHECK(q0 + q < a.nq))
+            a.partial[((size_t)(q0 + q) * a.n_items + item_id) * N + r] = lists[(size_t)q * N + r];
     }
 }
 
@@ -812,5 +823,7 @@ bool tc_shape(uint32_t N, uint32_t nq, uint32_t pw, uint32_t *qb, uint32_t *stag
     *stages = st > (uint32_t)kMaxStages ? (uint32_t)kMaxStages : st;
     return true;
 }
+
+OL_CHECK_EXPORT(check_tcscan)
 
 }  // namespace ol

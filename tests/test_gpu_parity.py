@@ -339,3 +339,45 @@ def test_p2p_exchange_emulated_equals_single(c2, world):        # §8e, the peer
     with pytest.raises(ol.OmnilocError):
         engines[0].p2p_open(world, 0, 16)
         ol.p2p_emulate(engines)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_tau_share_emulated_shards_match_oracle(c2, world):        # §8e, in-scan threshold sharing
+    """Ranks that MIN their published thresholds into each other's arrays during the scan (NCCL
+    mode over peer memory; here `world` contexts on one GPU linked by ol_tau_share_emulate,
+    their queries running concurrently on separate streams) still return exactly the oracle's
+    top-N and estimates: any rank's threshold bounds the global N-th best (Alg. 1)."""
+    cfg, F, C, video = c2
+    off = np.concatenate([[0], np.cumsum(cfg.subspace_sizes)])
+    engines, streams = [], []
+    for r in range(world):
+        st = torch.cuda.Stream()
+        e = ol.Engine(0, coarse_k=16, rank=r, world=world, exchange="torch", stream=st)
+        e.set_option("tc", 1)
+        rows = np.concatenate([np.arange(off[i] + b, off[i] + b + c) for i, n in enumerate(cfg.subspace_sizes)
+                               for b, c in [ol.shard_range(n, r, world)]])
+        e.upload(F[rows], C[rows], cfg.subspace_sizes, cfg.spec.grid())
+        engines.append(e); streams.append(st)
+    Qs = [np.ascontiguousarray(video[a:a + 300][:, None, :]) for a in (0, 300, 600)]
+    Qd = [torch.from_numpy(q).cuda() for q in Qs]
+    torch.cuda.synchronize()
+    for e in engines:                      # every context allocates this shape's arrays first
+        e.query(Qd[0], N=15, aggregate=True, exchange=False)
+    torch.cuda.synchronize()
+    ol.tau_share_emulate(engines)
+    for k, q in enumerate(Qd):
+        for e in engines:                  # all ranks' scans in flight at once
+            e.query(q, N=15, aggregate=True, exchange=False)
+        assert all(e.stat("tau_peers") == world - 1 for e in engines)
+        pays = [e.payload() for e in engines]
+        torch.cuda.synchronize()
+        g = torch.cat(pays)
+        torch.cuda.synchronize()
+        ref = oracle.retrieve(cfg.subspace_sizes, F, C, Qs[k], 15)
+        for r, e in enumerate(engines):
+            e.finalize_gathered(g)
+            assert_candidates_equal(e.topk(), ref, f"tau share world {world} query {k} rank {r}")
+            assert_estimates_equal(e.estimates(), ref, ctx=f"tau share world {world} query {k} rank {r}")
+    e = engines.pop()
+    e.close()                              # unlinks itself from the others
+    assert engines[0].stat("tau_peers") == world - 2

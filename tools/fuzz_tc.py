@@ -57,6 +57,8 @@ def one_case(rng, idx):
     if rng.random() < 0.15:
         opts["tc"] = 0
     e = ol.Engine(0, coarse_k=16)
+    if os.environ.get("OL_POISON") == "1":
+        e.set_option("poison", 1)
     for k, v in opts.items():
         e.set_option(k, v)
     e.upload(F, C, sizes, (4096, 4096))
