@@ -23,8 +23,9 @@ __all__ = ["Engine", "OmnilocError", "lib", "select_window", "shard_range", "CAN
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # OL_LIB=checked loads the bounds-checked build (tests / tools/sanitize_cases.py only)
-LIB_PATH = os.path.join(_HERE, "libomniloc_checked.so" if os.environ.get("OL_LIB") == "checked"
-                        else "libomniloc.so")
+# (OL_LIB_PATH: another build of the same library, for A/B timing tools)
+LIB_PATH = os.environ.get("OL_LIB_PATH") or os.path.join(
+    _HERE, "libomniloc_checked.so" if os.environ.get("OL_LIB") == "checked" else "libomniloc.so")
 
 OL_OK, OL_ERR_INVALID_ARGUMENT, OL_ERR_DIMENSION_MISMATCH, OL_ERR_NONFINITE = 0, -1, -2, -3
 OL_ERR_OUT_OF_RANGE, OL_ERR_OOM, OL_ERR_CUDA, OL_ERR_NOT_READY, OL_ERR_EMPTY = -4, -5, -6, -7, -8

@@ -53,6 +53,9 @@ constexpr int kScanWarps = kScanThreads / 32;
 constexpr int kMaxQT = 64;            // query frames per scan CTA
 constexpr int kAggMax = 8192;         // candidates per bundle in the aggregation kernel
 constexpr u64 kPadKey = ~0ull;
+// every subspace starts on a 256-row tile of the device planes (padding rows repeat its last
+// row): a tensor-core row tile's 32-row block bounds are then one aligned 64-byte copy
+constexpr uint64_t kPadRows = 256;
 constexpr uint32_t kInfBits = 0x7F800000u;  // +inf: "no threshold yet"
 
 // Coarse plane layout: tiles of 32 rows; inside a tile, 16-byte columns of 4

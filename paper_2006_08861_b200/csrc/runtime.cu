@@ -521,7 +521,7 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
     const uint32_t ns = db->n_subspaces;
     std::vector<SubInfo> subs(ns);
     std::vector<uint64_t> src_begin(ns);   // row offset of subspace i in the caller's arrays
-    uint64_t rows = 0, rows_pad = 0;       // device rows: each subspace starts on a 32-row tile
+    uint64_t rows = 0, rows_pad = 0;       // device rows: each subspace starts on a 256-row tile (kPadRows)
     for (uint32_t i = 0; i < ns; ++i) {
         const uint64_t gs = db->global_sizes[i];
         if (gs == 0 || gs > 0xFFFFFFFEull)
@@ -539,7 +539,7 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
         subs[i].shard_begin = (uint32_t)b;
         subs[i].global_size = (uint32_t)gs;
         rows += n;
-        rows_pad += (n + 31) / 32 * 32;
+        rows_pad += (n + kPadRows - 1) / kPadRows * kPadRows;
     }
     // validate inputs (S:32 finite values; S:102 coords inside the grid)
     if (!db->on_device) {
@@ -1097,6 +1097,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         st = ensure_tau_peers(c);
         if (st) return st;
         a.n_peer = peer_taus(c, (uint64_t)nq * c->n_sub, a.peer_tau);
+
         TimeScope ts(c, ol_ctx::T_SCAN);
         OL_LAUNCH(c, launch_tcscan(pair ? c->map_rows_half : c->map_rows, map_q, a, (int)(n_items * n_qblocks), c->stream));
         c->used_tc = true;
@@ -1640,7 +1641,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "tc_seed")) { if (v < 0 || v > 2) goto bad; c->opt_tc_seed = v; }
     else if (!strcmp(key, "scan2")) { if (v < 0 || v > 2) goto bad; c->opt_scan2 = v; }
     else if (!strcmp(key, "tc_min_frames")) { if (v < 0) goto bad; c->opt_tc_min_frames = v; }
-    else if (!strcmp(key, "tc_debug")) { if (v < 0 || v > 1023) goto bad; c->opt_tc_debug = v; }
+    else if (!strcmp(key, "tc_debug")) { if (v < 0 || v > 65535) goto bad; c->opt_tc_debug = v; }
     else if (!strcmp(key, "graph")) { if (v != 0 && v != 1) goto bad; c->opt_graph = v; }
     else if (!strcmp(key, "tau_share")) { if (v != 0 && v != 1) goto bad; c->opt_tau_share = v; }
     else if (!strcmp(key, "poison")) { if (v != 0 && v != 1) goto bad; c->opt_poison = v; }

@@ -856,7 +856,7 @@ cudaError_t launch_relayout(const float *src, uint64_t rows, uint64_t dst_row0, 
 __global__ void pad_rows_kernel(const SubInfo *subs, uint32_t n_sub, int kc, float *coarse, float *fine) {
     const uint32_t i = blockIdx.x;
     const SubInfo si = subs[i];
-    const uint64_t pad = (si.count + 31) / 32 * 32;
+    const uint64_t pad = (si.count + kPadRows - 1) / kPadRows * kPadRows;
     if (si.count == 0) return;
     const uint64_t src = si.row_begin + si.count - 1;
     for (uint64_t p = si.count + threadIdx.x / kK; p < pad; p += blockDim.x / kK) {

@@ -60,13 +60,22 @@ constexpr int kEv = 8;                  // survivor event ring entries per exact
                                         // (measured with the 32-dim filter, 1,024 frames, ring
                                         // 32 / 16 / 8 / 4: 100M rows 10.05 / 9.93 / 9.95 / 9.96 ms,
                                         // 20M 2.82 / 2.70 / 2.66 / 2.67, 1M 0.68 / - / 0.58 / 0.57)
-constexpr int kTrackMax = 16;           // largest N of the bound pre-pass (register list)
+constexpr int kTrackMax = 16;
+constexpr int kBndRing = 16;            // >= kMaxStages + kTBufs: see TcSmem::bnd           // largest N of the bound pre-pass (register list)
 constexpr float kTauInflate = 1.0f + 1.0f / 131072.0f;   // 1 + 2^-17
 constexpr uint32_t kStageBytesMax = kTileRows * kK * 2;   // 32 KB (pw = 64; 16 KB at pw = 32)
 
 struct TcSmem {
     alignas(1024) __half qm[kQB * kK];      // frames, main K (SW128), resident
     uint64_t full[kMaxStages], empty[kMaxStages], tfull[kTBufs], tempty[kTBufs], qbar;
+    // single CTAs: the row-term bounds of tile t's 8 32-row blocks, in slot t % kBndRing, brought
+    // by the producer's bulk copy next to the rows (subspaces start on 256-row tiles, so a
+    // tile's 64 bytes of bounds are 64-byte aligned): the epilogue reads them from shared
+    // memory -- a global load in its per-tile path stalls the tcgen05.wait::ld after it.  The
+    // producer runs at most n_stages tiles ahead of the MMA and the MMA at most kTBufs ahead
+    // of the epilogue, so a slot is never rewritten while it is read.
+    alignas(16) float2 bnd[kBndRing][kTileRows / 32];
+    uint64_t bfull[kBndRing];
     uint32_t tmem_base;
     float alpha[kQB];
     uint32_t tau[kQB];
@@ -213,6 +222,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
     if (threadIdx.x == 0) {
         for (uint32_t i = 0; i < n_stages; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], 1); }
         for (int i = 0; i < kTBufs; ++i) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], (kPair ? 2 : 1) * kEpiWarps / 2); }
+        for (int i = 0; i < kBndRing; ++i) mbar_init(&s.bfull[i], 1);
         mbar_init(&s.qbar, 1);
         fence_mbar_init();
         for (int w = 0; w < kExactWarps; ++w) s.prod[w] = s.closed_at[w] = 0;
@@ -264,6 +274,11 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                     if (rank == 0) mbar_expect_tx(&s.full[st], stage_bytes);   // both halves
                     tma_load_2d_pair(sb, &map_rows, &s.full[st], 0, r0 + (int)rank * (kTileRows / 2));
                     continue;
+                }
+                if (!kBound) {   // this tile's block bounds (64 B, aligned: items start on 256-row tiles)
+                    const uint32_t sl = t % kBndRing;
+                    mbar_expect_tx(&s.bfull[sl], (kTileRows / 32) * sizeof(float2));
+                    bulk_load(&s.bnd[sl][0], &a.blk[(size_t)r0 >> 5], (kTileRows / 32) * sizeof(float2), &s.bfull[sl]);
                 }
                 if ((a.dbg & 128) && t >= n_stages) { mbar_arrive(&s.full[st]); continue; }   // profiling: stale rows
                 mbar_expect_tx(&s.full[st], stage_bytes);
@@ -318,6 +333,8 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         const float alpha = s.alpha[ql];
         // lanes 0..3: the row-term bound g_B of this warp's 4 blocks
         auto load_g = [&](uint32_t t) -> float2 {
+            if (!kPair && !kBound) return make_float2(0.f, 0.f);   // (single CTAs: bounds staged in shared memory)
+            if (a.dbg & 4096) return make_float2(0.f, 0.f);   // (profiling: no bound loads)
             const uint32_t b = min((uint32_t)((it.row_begin + t * kTileRows + half * 128) >> 5) + (lane & 3), a.n_blk - 1);
             return __ldg(&a.blk[b]);
         };
@@ -368,12 +385,24 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             }
             const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * kTileRows + half * 128;
             const float h = 0.5f * (alpha - __uint_as_float(s.tau[ql]) * kTauInflate);
-            // lanes 0..3 (block c = lane): gB <= g_r on the block
-            const float gB = __fsub_rd(gb.x, __fmul_ru(nqm, gb.y));
-            const float th0 = __fadd_rd(h, __shfl_sync(0xffffffffu, gB, 0));
-            const float th1 = __fadd_rd(h, __shfl_sync(0xffffffffu, gB, 1));
-            const float th2 = __fadd_rd(h, __shfl_sync(0xffffffffu, gB, 2));
-            const float th3 = __fadd_rd(h, __shfl_sync(0xffffffffu, gB, 3));
+            float th0, th1, th2, th3;
+            if (!kPair && !kBound) {   // this half's 4 blocks from the staged bounds (broadcast loads)
+                const uint32_t sl = t % kBndRing;
+                mbar_wait(&s.bfull[sl], (t / kBndRing) & 1);   // (long complete: loaded with the rows)
+                const float4 *bp = reinterpret_cast<const float4 *>(&s.bnd[sl][half * 4]);
+                const float4 b01 = bp[0], b23 = bp[1];   // (g, e) of blocks 0, 1 | 2, 3
+                th0 = __fadd_rd(h, __fsub_rd(b01.x, __fmul_ru(nqm, b01.y)));
+                th1 = __fadd_rd(h, __fsub_rd(b01.z, __fmul_ru(nqm, b01.w)));
+                th2 = __fadd_rd(h, __fsub_rd(b23.x, __fmul_ru(nqm, b23.y)));
+                th3 = __fadd_rd(h, __fsub_rd(b23.z, __fmul_ru(nqm, b23.w)));
+            } else {
+                // lanes 0..3 (block c = lane): gB <= g_r on the block
+                const float gB = __fsub_rd(gb.x, __fmul_ru(nqm, gb.y));
+                th0 = __fadd_rd(h, __shfl_sync(0xffffffffu, gB, 0));
+                th1 = __fadd_rd(h, __shfl_sync(0xffffffffu, gB, 1));
+                th2 = __fadd_rd(h, __shfl_sync(0xffffffffu, gB, 2));
+                th3 = __fadd_rd(h, __shfl_sync(0xffffffffu, gB, 3));
+            }
             const uint32_t rb = t * kTileRows + half * 128;   // first row (within the item) of my columns
             const uint32_t nvalid = rb < it.count ? min(128u, it.count - rb) : 0u;
             const bool live = ql < qn && !(a.dbg & 4);

@@ -20,7 +20,7 @@ for dbg in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else '0
     e.set_option("time_kernels", 1)
     for _ in range(int(os.environ.get('REPS', 5))): e.query(Q3, N=15)
     torch.cuda.synchronize()
-    ms = e.stat("time_seed_ns" if dbg & 128 else "time_scan_ns") / int(os.environ.get("REPS", 5)) / 1e6
+    ms = e.stat("time_seed_ns" if os.environ.get("SEEDTIME") else "time_scan_ns") / int(os.environ.get("REPS", 5)) / 1e6
     for k in ("seed", "merge", "final"): e.stat(f"time_{k}_ns")
     e.set_option("time_kernels", 0)
     tiles = n / 256 * ((1024 + 127) // 128) / 148   # 256-row x 128-frame tiles per SM
