@@ -68,7 +68,7 @@ constexpr uint32_t kStageBytesMax = kTileRows * kK * 2;   // 32 KB (pw = 64; 16 
 struct TcSmem {
     alignas(1024) __half qm[kQB * kK];      // frames, main K (SW128), resident
     uint64_t full[kMaxStages], empty[kMaxStages], tfull[kTBufs], tempty[kTBufs], qbar;
-    // single CTAs: the row-term bounds of tile t's 8 32-row blocks, in slot t % kBndRing, brought
+    // the row-term bounds of tile t's 8 32-row blocks, in slot t % kBndRing, brought
     // by the producer's bulk copy next to the rows (subspaces start on 256-row tiles, so a
     // tile's 64 bytes of bounds are 64-byte aligned): the epilogue reads them from shared
     // memory -- a global load in its per-tile path stalls the tcgen05.wait::ld after it.  The
@@ -270,15 +270,16 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 if (t >= n_stages) mbar_wait_sleep(&s.empty[st], ((t / n_stages) - 1) & 1);
                 unsigned char *sb = stage0 + (size_t)st * stage_bytes;
                 const int r0 = (int)(it.row_begin + (uint64_t)t * kTileRows);
+                if (!kBound) {   // this tile's block bounds (64 B, aligned: items start on 256-row tiles;
+                                 // pairs: each CTA its own copy)
+                    const uint32_t sl = t % kBndRing;
+                    mbar_expect_tx(&s.bfull[sl], (kTileRows / 32) * sizeof(float2));
+                    bulk_load(&s.bnd[sl][0], &a.blk[(size_t)r0 >> 5], (kTileRows / 32) * sizeof(float2), &s.bfull[sl]);
+                }
                 if (kPair) {
                     if (rank == 0) mbar_expect_tx(&s.full[st], stage_bytes);   // both halves
                     tma_load_2d_pair(sb, &map_rows, &s.full[st], 0, r0 + (int)rank * (kTileRows / 2));
                     continue;
-                }
-                if (!kBound) {   // this tile's block bounds (64 B, aligned: items start on 256-row tiles)
-                    const uint32_t sl = t % kBndRing;
-                    mbar_expect_tx(&s.bfull[sl], (kTileRows / 32) * sizeof(float2));
-                    bulk_load(&s.bnd[sl][0], &a.blk[(size_t)r0 >> 5], (kTileRows / 32) * sizeof(float2), &s.bfull[sl]);
                 }
                 if ((a.dbg & 128) && t >= n_stages) { mbar_arrive(&s.full[st]); continue; }   // profiling: stale rows
                 mbar_expect_tx(&s.full[st], stage_bytes);
@@ -333,7 +334,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         const float alpha = s.alpha[ql];
         // lanes 0..3: the row-term bound g_B of this warp's 4 blocks
         auto load_g = [&](uint32_t t) -> float2 {
-            if (!kPair && !kBound) return make_float2(0.f, 0.f);   // (single CTAs: bounds staged in shared memory)
+            if (!kBound) return make_float2(0.f, 0.f);   // (bounds staged in shared memory)
             if (a.dbg & 4096) return make_float2(0.f, 0.f);   // (profiling: no bound loads)
             const uint32_t b = min((uint32_t)((it.row_begin + t * kTileRows + half * 128) >> 5) + (lane & 3), a.n_blk - 1);
             return __ldg(&a.blk[b]);
@@ -386,7 +387,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             const uint32_t taddr = tmem + ((quarter * 32) << 16) + buf * kTileRows + half * 128;
             const float h = 0.5f * (alpha - __uint_as_float(s.tau[ql]) * kTauInflate);
             float th0, th1, th2, th3;
-            if (!kPair && !kBound) {   // this half's 4 blocks from the staged bounds (broadcast loads)
+            if (!kBound) {   // this half's 4 blocks from the staged bounds (broadcast loads)
                 const uint32_t sl = t % kBndRing;
                 mbar_wait(&s.bfull[sl], (t / kBndRing) & 1);   // (long complete: loaded with the rows)
                 const float4 *bp = reinterpret_cast<const float4 *>(&s.bnd[sl][half * 4]);
