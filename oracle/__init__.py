@@ -67,6 +67,8 @@ def lib():
         L.oracle_aggregate.restype = i32
         L.oracle_shift_distance.argtypes = [P, P, i32, P]
         L.oracle_shift_distance.restype = flt
+        L.oracle_shift_profile.argtypes = [P, i32, i32, P, P]
+        L.oracle_shift_profile.restype = i32
         _lib = L
     return _lib
 
@@ -89,6 +91,18 @@ def extract_feature(profile, K: int = 64):
     if rc != OR_OK:
         raise ValueError(f"oracle_extract_feature rc={rc}")
     return out, bool(deg.value)
+
+
+def shift_profile(profile, K: int = 64):
+    """NEXT-1 stored profile: (x - mean x) / ||m||, ||m|| the descriptor's normaliser
+    (|DFT| bins 1..K) -> (binary64 [W], fp32 [W] = RN32 of it); zeros if degenerate."""
+    p = _c(profile, np.float64)
+    o64 = np.zeros(p.shape[0], np.float64)
+    o32 = np.zeros(p.shape[0], np.float32)
+    rc = lib().oracle_shift_profile(_p(p), p.shape[0], K, _p(o64), _p(o32))
+    if rc != OR_OK:
+        raise ValueError(f"oracle_shift_profile rc={rc}")
+    return o64, o32
 
 
 # --------------------------------------------------------------------------- distance

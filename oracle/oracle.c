@@ -71,6 +71,46 @@ int oracle_extract_feature(const double *profile, int W, int K, double *coeffs,
 }
 
 /* ------------------------------------------------------------------------ */
+/* NEXT-1 stored profile: the mean-removed profile scaled  */
+/* by 1/||m||, ||m|| = the norm of the |DFT| bins 1..K the descriptor is      */
+/* normalised by (oracle_extract_feature above).  With this scaling the */
+/* descriptor c = m/||m|| is exactly |DFT(x_hat)| on bins 1..K, so Parseval    */
+/* and the reverse triangle inequality give, for every circular shift s,      */
+/*   sum_w (x_hat_q[(w+s) mod W] - x_hat_d[w])^2 >= (2/W) ||c_q - c_d||^2     */
+/* (bins k and W-k both contribute for a real profile, K < W/2).  Degenerate  */
+/* profiles (||m|| <= 1e-12) give all zeros.  Binary64; out32 = RN32 of it.   */
+/* ------------------------------------------------------------------------ */
+int oracle_shift_profile(const double *profile, int W, int K, double *out64, float *out32) {
+    if (W < 1 || K < 1 || K >= W) return OR_ERR_INVALID;
+    double *coeffs = (double *)malloc(sizeof(double) * (size_t)K);
+    /* ||m|| is the descriptor's normaliser: recompute the bins, keep the norm */
+    double norm2 = 0.0;
+    for (int k = 1; k <= K; ++k) {
+        double re = 0.0, im = 0.0;
+        for (int w = 0; w < W; ++w) {
+            long long r = ((long long)k * (long long)w) % W;
+            double ang = 2.0 * M_PI * (double)r / (double)W;
+            re += profile[w] * cos(ang);
+            im -= profile[w] * sin(ang);
+        }
+        double m = sqrt(re * re + im * im);
+        coeffs[k - 1] = m;
+        norm2 += m * m;
+    }
+    free(coeffs);
+    double norm = sqrt(norm2);
+    double mean = 0.0;
+    for (int w = 0; w < W; ++w) mean += profile[w];
+    mean /= (double)W;
+    for (int w = 0; w < W; ++w) {
+        double v = norm > 1e-12 ? (profile[w] - mean) / norm : 0.0;
+        if (out64) out64[w] = v;
+        if (out32) out32[w] = (float)v;
+    }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* calculateDistance (Alg. 1 step 7; Euclidean per P:202).  The fp32  */
 /* fixed-order chain of reading R3.  Returns acc = squared distance.         */
 /* ------------------------------------------------------------------------ */

@@ -164,3 +164,66 @@ def test_shift_distance_ties_take_smallest_shift():
     p = np.tile(np.float32([0.1, 0.9]), 16)          # period 2: shifts 0, 2, 4 ... tie
     v, s = oracle.shift_distance(np.roll(p, 1), p)
     assert v == 0.0 and s == 1
+
+
+# ---------------------------------------------------------------- NEXT-1 stored profile
+def _profiles(seed, n=6, W=256):
+    """Synthetic omnidirectional profiles: a few Gaussian bumps on an offset + noise."""
+    rng = np.random.default_rng(seed)
+    w = np.arange(W)
+    out = []
+    for _ in range(n):
+        x = 0.5 + 0.02 * rng.standard_normal(W)
+        for _ in range(int(rng.integers(3, 9))):
+            c, a, s = rng.uniform(0, W), rng.uniform(0.1, 0.5), rng.uniform(2, 12)
+            d = (w - c + W / 2) % W - W / 2
+            x += a * np.exp(-0.5 * (d / s) ** 2)
+        out.append(x)
+    return np.array(out)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_shift_profile_spectrum_is_the_descriptor(seed):          # S:53, SURVEY 8f NEXT-1
+    """numpy.fft of the stored profile: zero mean (DC bin 0) and |X_k| bins 1..64 equal the
+    descriptor (the oracle's own direct DFT feature) to 1e-12 -- the scaling is 1/||m||."""
+    for x in _profiles(seed):
+        p64, p32 = oracle.shift_profile(x)
+        c, deg = oracle.extract_feature(x)
+        assert not deg
+        X = np.fft.fft(p64)
+        assert abs(X[0]) < 1e-12
+        assert np.max(np.abs(np.abs(X[1:65]) - c)) < 1e-12
+        assert np.array_equal(p32, p64.astype(np.float32))
+
+
+def test_shift_profile_invariances_and_degenerate():                 # S:56, S:71-73
+    """Affine invariance (brightness offset, positive gain) and rotation equivariance of the
+    stored profile; a constant profile is all zeros (degenerate)."""
+    for x in _profiles(7):
+        p, _ = oracle.shift_profile(x)
+        q, _ = oracle.shift_profile(3.5 * x + 0.7)
+        assert np.max(np.abs(p - q)) < 1e-12
+        r, _ = oracle.shift_profile(np.roll(x, 37))
+        assert np.max(np.abs(r - np.roll(p, 37))) < 1e-12
+    z64, z32 = oracle.shift_profile(np.full(256, 0.42))
+    assert not z64.any() and not z32.any()
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_shift_distance_lower_bounded_by_descriptor_distance(seed):   # Parseval, SURVEY 8f NEXT-1
+    """For every pair of stored profiles and EVERY circular shift s, the binary64 profile
+    distance is >= (2/W) ||c_q - c_d||^2 (Parseval + the reverse triangle inequality on bins
+    k and W-k); checked by brute force over all 256 shifts, and the bound is not vacuous."""
+    P = _profiles(100 + seed, n=8)
+    W = P.shape[1]
+    prof = [oracle.shift_profile(x)[0] for x in P]
+    desc = [oracle.extract_feature(x)[0] for x in P]
+    ratios = []
+    for i in range(len(P)):
+        for j in range(len(P)):
+            lb = (2.0 / W) * np.sum((desc[i] - desc[j]) ** 2)
+            d = np.array([np.sum((np.roll(prof[i], -s) - prof[j]) ** 2) for s in range(W)])
+            assert np.all(d >= lb * (1 - 1e-12) - 1e-15), (i, j, d.min(), lb)
+            if i != j:
+                ratios.append(lb / d.min())
+    assert max(ratios) > 0.05     # the descriptor distance is a real (not trivial) bound
