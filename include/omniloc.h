@@ -340,6 +340,16 @@ OL_API ol_status ol_upload_profiles(ol_ctx *ctx, const float *profiles, uint32_t
  * profiles), INVALID_ARGUMENT, NONFINITE (host input), CUDA, NCCL. */
 OL_API ol_status ol_shift_rescore(ol_ctx *ctx, const float *query_profiles, int32_t on_device);
 
+/* The same re-scoring with the database profiles of exactly the final candidates
+ * supplied by the caller ([n_cand][W] fp32 in candidate order, ol_get_topk's order;
+ * host or device like query_profiles), instead of profiles of every database row
+ * uploaded with ol_upload_profiles ("W = 256 fp32 = 1 KB/entry, for final candidates
+ * only").  Every candidate is scored on this rank (no MIN reduction
+ * needed).  8 <= W <= 1024.  Asynchronous.  Errors: NOT_READY (no finalized query),
+ * INVALID_ARGUMENT, NONFINITE (host input), CUDA. */
+OL_API ol_status ol_shift_rescore_cands(ol_ctx *ctx, const float *query_profiles, const float *cand_profiles,
+                                        uint32_t W, int32_t on_device);
+
 /* Device array (owned by the context) of the last ol_shift_rescore, one key per
  * candidate in candidate order: (bits(min acc) << 32) | s, or INT64_MAX. */
 OL_API ol_status ol_shift_keys(ol_ctx *ctx, uint64_t **dev_keys, uint64_t *count);
@@ -358,18 +368,24 @@ OL_API ol_status ol_get_shifts(ol_ctx *ctx, uint32_t *shift, float *dist2, uint6
  * FFT magnitude of the one-dimensional omnidirectional vector"): for each
  * profile x[0..W-1], X[k] = sum_w x[w] e^{-2 pi i k w / W} for k = 1..64 (DC
  * dropped), m_k = |X[k]|, descriptor = m / ||m|| if ||m|| > 1e-12, else all-zero
- * and flagged degenerate (reading R4).  Binary64 arithmetic on the GPU.
- *   profiles:   [n][W] binary64, host (on_device = 0) or device memory
- *   out32:      [n][64] fp32 descriptors, RN of the binary64 values (the database /
- *               query format of ol_upload_db and ol_query); may be NULL
- *   out64:      [n][64] binary64 descriptors; may be NULL
- *   degenerate: [n] bytes, 1 = degenerate; may be NULL
+ * and flagged degenerate (reading R4).  Binary64 arithmetic on the GPU: an FFT
+ * (one warp per profile) for W = 128, 256, 512, a direct sum for other W.
+ *   profiles:    [n][W] binary64, host (on_device = 0) or device memory
+ *   out32:       [n][64] fp32 descriptors, RN of the binary64 values (the database /
+ *                query format of ol_upload_db and ol_query); may be NULL
+ *   out64:       [n][64] binary64 descriptors; may be NULL
+ *   degenerate:  [n] bytes, 1 = degenerate; may be NULL
+ *   profile_out: [n][W] fp32, RN of (x - mean x) / ||m|| (all-zero if degenerate):
+ *                the NEXT-1 stored profile, whose |DFT| on bins 1..64 is the
+ *                descriptor, so the shift distance of two of them is at least
+ *                (2/W) x the squared descriptor distance (Parseval); may be NULL
  * Outputs live where the input lives (host or device; caller-owned).  Host calls
  * synchronise; device calls are stream-ordered.  65 <= W <= 2048.
  * Errors: INVALID_ARGUMENT (W, NULL profiles), NONFINITE (host input with NaN/Inf),
  * CUDA. */
 OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64_t n, uint32_t W,
-                                     int32_t on_device, float *out32, double *out64, uint8_t *degenerate);
+                                     int32_t on_device, float *out32, double *out64, uint8_t *degenerate,
+                                     float *profile_out);
 
 /* ---- tuning / introspection (never changes results) ---------------------- */
 

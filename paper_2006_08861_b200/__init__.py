@@ -121,11 +121,12 @@ def lib():
             "ol_set_option": ([P, ctypes.c_char_p, i64], i32),
             "ol_upload_profiles": ([P, P, u32, i32], i32),
             "ol_shift_rescore": ([P, P, i32], i32),
+            "ol_shift_rescore_cands": ([P, P, P, u32, i32], i32),
             "ol_shift_keys": ([P, ctypes.POINTER(P), ctypes.POINTER(u64)], i32),
             "ol_get_shifts": ([P, P, P, u64], i32),
             "ol_shift_keys_copy": ([P, P], i32),
             "ol_get_stat": ([P, ctypes.c_char_p, ctypes.POINTER(i64)], i32),
-            "ol_extract_features": ([P, P, u64, u32, i32, P, P, P], i32),
+            "ol_extract_features": ([P, P, u64, u32, i32, P, P, P, P], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -472,10 +473,30 @@ class Engine:
                                      ctypes.c_void_p(dist2.ctypes.data), n))
         return shift, dist2
 
-    def extract_features(self, profiles, want64: bool = False):
+    def shift_rescore_cands(self, query_profiles, cand_profiles, fetch: bool = True):
+        """Heading of every candidate from caller-supplied candidate profiles [n_cand][W] (candidate
+        order) and query profiles [B*M][W], both host or both device fp32 -> (shift, dist2) when
+        fetch, else nothing (results stay on the device: ol_shift_keys)."""
+        self.sync_stream()
+        qp, qdev = _ptr(query_profiles)
+        cp, cdev = _ptr(cand_profiles)
+        if qdev != cdev:
+            raise ValueError("query and candidate profiles must both be host or both device")
+        self._ck(lib().ol_shift_rescore_cands(self._h, ctypes.c_void_p(qp), ctypes.c_void_p(cp),
+                                              int(cand_profiles.shape[-1]), qdev))
+        if not fetch:
+            return None
+        n = self.candidate_count()
+        shift = np.empty(n, np.uint32); dist2 = np.empty(n, np.float32)
+        self._ck(lib().ol_get_shifts(self._h, ctypes.c_void_p(shift.ctypes.data),
+                                     ctypes.c_void_p(dist2.ctypes.data), n))
+        return shift, dist2
+
+    def extract_features(self, profiles, want64: bool = False, want_profiles: bool = False):
         """Descriptors of omnidirectional profiles (NEXT-3): [n][W] binary64,
-        host numpy or device torch -> (fp32 [n][64], degenerate bool [n][, binary64 [n][64]]),
-        same residency as the input.  Every step runs in extract_kernel."""
+        host numpy or device torch -> (fp32 [n][64], degenerate bool [n]) plus binary64 [n][64]
+        if want64, plus the NEXT-1 stored profiles fp32 [n][W] ((x - mean)/||m||) if
+        want_profiles; same residency as the input.  Every step runs in the library's kernels."""
         n, W = int(profiles.shape[0]), int(profiles.shape[1])
         pp, pdev = _ptr(profiles)
         if pdev:
@@ -483,22 +504,31 @@ class Engine:
             self.sync_stream()
             o32 = torch.empty((n, 64), dtype=torch.float32, device=profiles.device)
             o64 = torch.empty((n, 64), dtype=torch.float64, device=profiles.device) if want64 else None
+            po = torch.empty((n, W), dtype=torch.float32, device=profiles.device) if want_profiles else None
             deg = torch.empty(n, dtype=torch.uint8, device=profiles.device)
-            p64 = o64.data_ptr() if want64 else None
             self._ck(lib().ol_extract_features(self._h, ctypes.c_void_p(pp), n, W, 1,
-                                               ctypes.c_void_p(o32.data_ptr()), ctypes.c_void_p(p64),
-                                               ctypes.c_void_p(deg.data_ptr())))
+                                               ctypes.c_void_p(o32.data_ptr()),
+                                               ctypes.c_void_p(o64.data_ptr() if want64 else None),
+                                               ctypes.c_void_p(deg.data_ptr()),
+                                               ctypes.c_void_p(po.data_ptr() if want_profiles else None)))
             deg = deg.bool()
         else:
             o32 = np.empty((n, 64), np.float32)
             o64 = np.empty((n, 64), np.float64) if want64 else None
+            po = np.empty((n, W), np.float32) if want_profiles else None
             deg = np.empty(n, np.uint8)
             self._ck(lib().ol_extract_features(self._h, ctypes.c_void_p(pp), n, W, 0,
                                                ctypes.c_void_p(o32.ctypes.data),
                                                ctypes.c_void_p(o64.ctypes.data if want64 else None),
-                                               ctypes.c_void_p(deg.ctypes.data)))
+                                               ctypes.c_void_p(deg.ctypes.data),
+                                               ctypes.c_void_p(po.ctypes.data if want_profiles else None)))
             deg = deg.astype(bool)
-        return (o32, deg, o64) if want64 else (o32, deg)
+        out = (o32, deg)
+        if want64:
+            out += (o64,)
+        if want_profiles:
+            out += (po,)
+        return out
 
     def set_option(self, key: str, value: int):
         self._ck(lib().ol_set_option(self._h, key.encode(), int(value)))

@@ -1,16 +1,23 @@
 // extract.cu -- GPU descriptor extraction (NEXT-3 in SURVEY §8f, kernel NK9): the
 // step before the hot path, for query ingestion at video rate and for building
-// large databases on the device.
+// large databases on the device; and the NEXT-1 stored profile.
 //
 // P:121 "The FFT magnitude of the one-dimensional omnidirectional vector is used as
 // a rotation-invariant omnidirectional feature"; S:53 fixes the unnormalised forward
 // DFT X[k] = sum_w x[w] e^{-2 pi i k w / W}, bins k = 1..K (DC dropped), descriptor
 // m / ||m|| if ||m|| > 1e-12, else all-zero and flagged degenerate (reading R4).
-// Binary64 throughout, like the oracle; twiddles come from a per-CTA table of
-// sincospi(2 j / W) at the exactly reduced index (k w) mod W every 8 columns and are
-// advanced by one complex rotation in between.
-// Parity with the oracle is within a few ulps of binary64 (summation order of the
-// norm differs); the fp32 descriptor is RN32 of the binary64 value.
+// The NEXT-1 stored profile is (x - mean x) / ||m|| (zeros if degenerate): its |DFT| on
+// bins 1..K is then the descriptor itself (the Parseval link).
+// Binary64 throughout, like the oracle.  Two kernels:
+//  - fft_extract_kernel<R> (W = 32 R, R in {4, 8, 16}: W = 128, 256, 512): the paper's FFT.
+//    One warp per profile, lane l holds x[l + 32 j]; an R-point DFT per lane over j, the
+//    twiddle e^{-2 pi i l k1 / W}, then a 32-point radix-2 DIF FFT across the lanes
+//    (shuffles): X[k1 + R k2] lands in lane bitrev5(k2).  ~19k flops per profile instead of
+//    the direct sum's 65k, and HBM-bound (2 KB read per profile).
+//  - extract_kernel (any W): the direct sum, twiddles from a per-CTA sincospi table at the
+//    exactly reduced index (k w) mod W every 8 columns, advanced by a rotation in between.
+// Parity with the oracle's direct sum is within a few ulps of binary64; the fp32 outputs are
+// RN32 of the binary64 values.
 #define OL_TU 6
 #include "ol_internal.h"
 
@@ -20,7 +27,8 @@ constexpr int kExtractWarps = 8;   // profiles per CTA (one warp each)
 
 // One warp per profile; lane l computes bins l + 1 and l + 33.
 __global__ void __launch_bounds__(32 * kExtractWarps)
-extract_kernel(const double *prof, uint64_t n, uint32_t W, float *out32, double *out64, uint8_t *degenerate) {
+extract_kernel(const double *prof, uint64_t n, uint32_t W, float *out32, double *out64, uint8_t *degenerate,
+               float *prof_out) {
     extern __shared__ double ex_smem[];
     double *tc = ex_smem, *ts = ex_smem + W;                 // cos / sin of 2 pi j / W
     double *pw = ex_smem + 2 * W + (threadIdx.x >> 5) * W;   // this warp's profile
@@ -70,21 +78,140 @@ extract_kernel(const double *prof, uint64_t n, uint32_t W, float *out32, double 
             if (out32) out32[o] = __double2float_rn(c);
         }
         if (degenerate && lane == 0) degenerate[p] = deg ? 1 : 0;
+        if (prof_out) {   // NEXT-1 stored profile: (x - mean) / ||m||
+            double sum = 0.0;
+            for (uint32_t w = lane; w < W; w += 32) sum += pw[w];
+            for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            const double mean = sum / (double)W;
+            for (uint32_t w = lane; w < W; w += 32)
+                prof_out[p * W + w] = deg ? 0.f : __double2float_rn((pw[w] - mean) / norm);
+        }
         __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------- FFT path (W = 32 R)
+template <int R>
+__global__ void __launch_bounds__(32 * kExtractWarps)
+fft_extract_kernel(const double *prof, uint64_t n, float *out32, double *out64, uint8_t *degenerate, float *prof_out) {
+    constexpr uint32_t W = 32u * R;
+    __shared__ double tc[W], ts[W];   // cos / sin of 2 pi j / W
+    for (uint32_t j = threadIdx.x; j < W; j += blockDim.x) {
+        double sn, cs;
+        sincospi(2.0 * (double)j / (double)W, &sn, &cs);
+        tc[j] = cs;
+        ts[j] = sn;
+    }
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    // lane -> its 32-point output k2 (DIF leaves the outputs bit-reversed)
+    const uint32_t k2 = __brev(lane) >> 27;
+    for (uint64_t p = (uint64_t)blockIdx.x * kExtractWarps + (threadIdx.x >> 5); p < n;
+         p += (uint64_t)gridDim.x * kExtractWarps) {
+        double x[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) x[j] = __ldcs(&prof[p * W + lane + 32 * j]);   // (streamed once)
+        // step 1: R-point DFT over j of x[l + 32 j] (real input: A[R - k1] = conj A[k1])
+        double re[R], im[R];
+#pragma unroll
+        for (int k1 = 0; k1 <= R / 2; ++k1) {
+            double a = 0.0, b = 0.0;
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                const int t = (32 * j * k1) % (int)W;   // e^{-2 pi i j k1 / R} = table[32 j k1 mod W]
+                a = fma(x[j], tc[t], a);
+                b = fma(-x[j], ts[t], b);
+            }
+            re[k1] = a;
+            im[k1] = b;
+        }
+#pragma unroll
+        for (int k1 = R / 2 + 1; k1 < R; ++k1) { re[k1] = re[R - k1]; im[k1] = -im[R - k1]; }
+        // step 2: twiddle e^{-2 pi i l k1 / W}
+#pragma unroll
+        for (int k1 = 1; k1 < R; ++k1) {
+            const uint32_t t = (lane * (uint32_t)k1) % W;
+            const double c = tc[t], sn = ts[t];
+            const double r = re[k1], i = im[k1];
+            re[k1] = fma(r, c, i * sn);       // (r + i i)(c - i sn)
+            im[k1] = fma(i, c, -r * sn);
+        }
+        // step 3: 32-point radix-2 DIF FFT across the lanes, every k1
+#pragma unroll
+        for (int h = 16; h >= 1; h >>= 1) {
+            const bool lower = (lane & h) != 0;
+            const uint32_t e = (lane & (h - 1)) * (W / (2 * h));   // W_{2h}^{lane mod h}
+            const double c = tc[e], sn = ts[e];
+#pragma unroll
+            for (int k1 = 0; k1 < R; ++k1) {
+                const double pr = __shfl_xor_sync(0xffffffffu, re[k1], h);
+                const double pi = __shfl_xor_sync(0xffffffffu, im[k1], h);
+                if (!lower) {
+                    re[k1] += pr;
+                    im[k1] += pi;
+                } else {
+                    const double dr = pr - re[k1], di = pi - im[k1];
+                    re[k1] = fma(dr, c, di * sn);
+                    im[k1] = fma(di, c, -dr * sn);
+                }
+            }
+        }
+        // step 4: magnitudes of bins 1..K held by this lane (k = k1 + R k2), norm, outputs
+        double n2 = 0.0;
+#pragma unroll
+        for (int k1 = 0; k1 < R; ++k1) {
+            const uint32_t k = (uint32_t)k1 + R * k2;
+            if (k >= 1 && k <= (uint32_t)kK) {
+                re[k1] = sqrt(re[k1] * re[k1] + im[k1] * im[k1]);
+                n2 += re[k1] * re[k1];
+            }
+        }
+        for (int o = 16; o; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+        const double norm = sqrt(n2);
+        const bool deg = !(norm > 1e-12);
+#pragma unroll
+        for (int k1 = 0; k1 < R; ++k1) {
+            const uint32_t k = (uint32_t)k1 + R * k2;
+            if (k >= 1 && k <= (uint32_t)kK) {
+                const double c = deg ? 0.0 : re[k1] / norm;
+                const uint64_t o = p * kK + (k - 1);
+                if (out64) out64[o] = c;
+                if (out32) out32[o] = __double2float_rn(c);
+            }
+        }
+        if (degenerate && lane == 0) degenerate[p] = deg ? 1 : 0;
+        if (prof_out) {   // NEXT-1 stored profile: (x - mean) / ||m||
+            double sum = 0.0;
+#pragma unroll
+            for (int j = 0; j < R; ++j) sum += x[j];
+            for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            const double mean = sum / (double)W;
+#pragma unroll
+            for (int j = 0; j < R; ++j)
+                prof_out[p * W + lane + 32 * j] = deg ? 0.f : __double2float_rn((x[j] - mean) / norm);
+        }
     }
 }
 
 size_t extract_smem_bytes(uint32_t W) { return sizeof(double) * W * (2 + kExtractWarps); }
 
 cudaError_t launch_extract(const double *prof, uint64_t n, uint32_t W, float *out32, double *out64,
-                           uint8_t *degenerate, cudaStream_t s) {
+                           uint8_t *degenerate, float *prof_out, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    if (W == 128 || W == 256 || W == 512) {   // the FFT
+        uint64_t blocks = (n + kExtractWarps - 1) / kExtractWarps;
+        if (blocks > 148 * 32) blocks = 148 * 32;
+        if (W == 128) fft_extract_kernel<4><<<(unsigned)blocks, 32 * kExtractWarps, 0, s>>>(prof, n, out32, out64, degenerate, prof_out);
+        else if (W == 256) fft_extract_kernel<8><<<(unsigned)blocks, 32 * kExtractWarps, 0, s>>>(prof, n, out32, out64, degenerate, prof_out);
+        else fft_extract_kernel<16><<<(unsigned)blocks, 32 * kExtractWarps, 0, s>>>(prof, n, out32, out64, degenerate, prof_out);
+        return cudaGetLastError();
+    }
     const size_t smem = extract_smem_bytes(W);
     cudaError_t e = cudaFuncSetAttribute(extract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     uint64_t blocks = (n + kExtractWarps - 1) / kExtractWarps;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    extract_kernel<<<(unsigned)blocks, 32 * kExtractWarps, smem, s>>>(prof, n, W, out32, out64, degenerate);
+    extract_kernel<<<(unsigned)blocks, 32 * kExtractWarps, smem, s>>>(prof, n, W, out32, out64, degenerate, prof_out);
     return cudaGetLastError();
 }
 

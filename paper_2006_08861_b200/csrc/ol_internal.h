@@ -195,6 +195,7 @@ struct ShiftArgs {
     const ol_candidate *cand;
     const SubInfo *subs;
     const float *prof;            // [rows][W] database profiles (tile-padded row index)
+    const float *cprof;           // or, when non-null: [n_cand][W] profiles in candidate order
     const float *qprof;           // [nq][W] query profiles
     u64 *keys;                    // [n_cand]
     uint64_t n_cand;
@@ -211,7 +212,7 @@ cudaError_t launch_tc_prep_queries(const float *q, uint32_t nq, uint32_t nq_pad,
 cudaError_t launch_fill_u32(uint32_t *p, uint64_t n, uint32_t v, cudaStream_t s);
 size_t extract_smem_bytes(uint32_t W);
 cudaError_t launch_extract(const double *prof, uint64_t n, uint32_t W, float *out32, double *out64,
-                           uint8_t *degenerate, cudaStream_t s);
+                           uint8_t *degenerate, float *prof_out, cudaStream_t s);
 cudaError_t launch_pad_rows(const SubInfo *subs, uint32_t n_sub, int kc, float *coarse, float *fine, cudaStream_t s);
 bool make_tc_map(CUtensorMap *m, const void *ptr, uint64_t rows, uint32_t box_rows, uint32_t width,
                  uint32_t row_stride = 1);

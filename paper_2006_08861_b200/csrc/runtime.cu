@@ -1521,24 +1521,24 @@ ol_status ol_upload_profiles(ol_ctx *c, const float *profiles, uint32_t W, int32
 }
 
 ol_status ol_extract_features(ol_ctx *c, const double *profiles, uint64_t n, uint32_t W, int32_t on_device,
-                              float *out32, double *out64, uint8_t *degenerate) {
+                              float *out32, double *out64, uint8_t *degenerate, float *profile_out) {
     if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (W <= (uint32_t)OL_K || W > 2048) return fail(c, OL_ERR_INVALID_ARGUMENT, "W = %u outside 65..2048", W);
     if (n == 0) return OL_OK;
     if (!profiles) return fail(c, OL_ERR_INVALID_ARGUMENT, "profiles is NULL");
     OL_CUDA(c, cudaSetDevice(c->device));
     if (on_device) {
-        OL_LAUNCH(c, launch_extract(profiles, n, W, out32, out64, degenerate, c->stream));
+        OL_LAUNCH(c, launch_extract(profiles, n, W, out32, out64, degenerate, profile_out, c->stream));
         return OL_OK;
     }
     for (uint64_t t = 0; t < n * W; ++t)
         if (!std::isfinite(profiles[t]))
             return fail(c, OL_ERR_NONFINITE, "profile value %llu is not finite", (unsigned long long)t);
     double *dp = nullptr, *d64 = nullptr;
-    float *d32 = nullptr;
+    float *d32 = nullptr, *dpo = nullptr;
     uint8_t *dd = nullptr;
     ol_status st = OL_OK;
-    auto cleanup = [&]() { cudaFree(dp); cudaFree(d64); cudaFree(d32); cudaFree(dd); };
+    auto cleanup = [&]() { cudaFree(dp); cudaFree(d64); cudaFree(d32); cudaFree(dd); cudaFree(dpo); };
 #define OL_EX(x)                                                                          \
     do {                                                                                  \
         cudaError_t e_ = (x);                                                             \
@@ -1548,45 +1548,66 @@ ol_status ol_extract_features(ol_ctx *c, const double *profiles, uint64_t n, uin
     if (out64) OL_EX(cudaMalloc((void **)&d64, sizeof(double) * n * OL_K));
     if (out32) OL_EX(cudaMalloc((void **)&d32, sizeof(float) * n * OL_K));
     if (degenerate) OL_EX(cudaMalloc((void **)&dd, n));
+    if (profile_out) OL_EX(cudaMalloc((void **)&dpo, sizeof(float) * n * W));
     OL_EX(cudaMemcpyAsync(dp, profiles, sizeof(double) * n * W, cudaMemcpyHostToDevice, c->stream));
-    OL_EX(launch_extract(dp, n, W, d32, d64, dd, c->stream));
+    OL_EX(launch_extract(dp, n, W, d32, d64, dd, dpo, c->stream));
     ++c->launches;
     if (out64) OL_EX(cudaMemcpyAsync(out64, d64, sizeof(double) * n * OL_K, cudaMemcpyDeviceToHost, c->stream));
     if (out32) OL_EX(cudaMemcpyAsync(out32, d32, sizeof(float) * n * OL_K, cudaMemcpyDeviceToHost, c->stream));
     if (degenerate) OL_EX(cudaMemcpyAsync(degenerate, dd, n, cudaMemcpyDeviceToHost, c->stream));
+    if (profile_out) OL_EX(cudaMemcpyAsync(profile_out, dpo, sizeof(float) * n * W, cudaMemcpyDeviceToHost, c->stream));
     OL_EX(cudaStreamSynchronize(c->stream));
 #undef OL_EX
     cleanup();
     return st;
 }
 
-ol_status ol_shift_rescore(ol_ctx *c, const float *qprof, int32_t on_device) {
-    NvtxRange nv("ol_shift_rescore");
+static ol_status shift_rescore_impl(ol_ctx *c, const float *qprof, const float *cprof, uint32_t Wc, int32_t on_device) {
     if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    NvtxRange nv("ol_shift_rescore");
     if (!c->finalized) return fail(c, OL_ERR_NOT_READY, "no finalized query");
-    if (!c->prof) return fail(c, OL_ERR_NOT_READY, "no profiles uploaded");
+    if (!cprof && !c->prof) return fail(c, OL_ERR_NOT_READY, "no profiles uploaded");
     if (!qprof) return fail(c, OL_ERR_INVALID_ARGUMENT, "query_profiles is NULL");
+    if (cprof && (Wc < 8 || Wc > 1024)) return fail(c, OL_ERR_INVALID_ARGUMENT, "W=%u outside 8..1024", Wc);
     OL_CUDA(c, cudaSetDevice(c->device));
-    const uint32_t W = c->prof_W;
-    const float *qp = qprof;
+    const uint32_t W = cprof ? Wc : c->prof_W;
+    const float *qp = qprof, *cp = cprof;
     if (!on_device) {
         for (uint64_t t = 0; t < (uint64_t)c->nq * W; ++t)
             if (!std::isfinite(qprof[t]))
                 return fail(c, OL_ERR_NONFINITE, "query profile value %llu is not finite", (unsigned long long)t);
-        OL_CUDA(c, grow(&c->qprof_d, &c->qprof_cap, (size_t)c->nq * W));
+        if (cprof)
+            for (uint64_t t = 0; t < c->n_cand * W; ++t)
+                if (!std::isfinite(cprof[t]))
+                    return fail(c, OL_ERR_NONFINITE, "candidate profile value %llu is not finite", (unsigned long long)t);
+        OL_CUDA(c, grow(&c->qprof_d, &c->qprof_cap, (size_t)c->nq * W + (cprof ? c->n_cand * W : 0)));
         OL_CUDA(c, cudaMemcpyAsync(c->qprof_d, qprof, sizeof(float) * c->nq * W, cudaMemcpyHostToDevice, c->stream));
         qp = c->qprof_d;
+        if (cprof) {
+            OL_CUDA(c, cudaMemcpyAsync(c->qprof_d + (size_t)c->nq * W, cprof, sizeof(float) * c->n_cand * W,
+                                       cudaMemcpyHostToDevice, c->stream));
+            cp = c->qprof_d + (size_t)c->nq * W;
+        }
     }
     OL_CUDA(c, grow(&c->shift_keys, &c->shift_cap, c->n_cand));
     ShiftArgs sa;
-    sa.cand = c->cand_d; sa.subs = c->subs_d; sa.prof = c->prof; sa.qprof = qp; sa.keys = c->shift_keys;
+    sa.cand = c->cand_d; sa.subs = c->subs_d; sa.prof = c->prof; sa.cprof = cp; sa.qprof = qp; sa.keys = c->shift_keys;
     sa.n_cand = c->n_cand; sa.W = W; sa.M = c->M; sa.nq = c->nq;
     if (c->n_cand) OL_LAUNCH(c, launch_shift(sa, c->stream));
-    if (c->comm && c->n_cand)   // ranks scored only their own rows: keep the least key of every candidate
+    if (!cprof && c->comm && c->n_cand)   // ranks scored only their own rows: keep the least key of every candidate
         OL_NCCL(c, nccl_api(nullptr)->allReduce(c->shift_keys, c->shift_keys, c->n_cand, ncclUint64, ncclMin, c->comm,
                                                 c->stream));
     c->shift_ready = true;
     return OL_OK;
+}
+
+ol_status ol_shift_rescore(ol_ctx *c, const float *qprof, int32_t on_device) {
+    return shift_rescore_impl(c, qprof, nullptr, 0, on_device);
+}
+
+ol_status ol_shift_rescore_cands(ol_ctx *c, const float *qprof, const float *cand_prof, uint32_t W, int32_t on_device) {
+    if (!cand_prof) return fail(c, OL_ERR_INVALID_ARGUMENT, "cand_prof is NULL");
+    return shift_rescore_impl(c, qprof, cand_prof, W, on_device);
 }
 
 ol_status ol_shift_keys(ol_ctx *c, uint64_t **dev_keys, uint64_t *count) {

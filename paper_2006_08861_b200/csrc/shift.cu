@@ -21,15 +21,19 @@ __global__ void __launch_bounds__(32 * kShiftWarps) shift_kernel(ShiftArgs a) {
     const uint32_t W = a.W;
     float *q = sh + (size_t)warp * 2 * W, *p = q + W;
     const ol_candidate cd = a.cand[c];
-    const SubInfo si = a.subs[cd.subspace];
-    if (cd.frame < si.shard_begin || cd.frame >= si.shard_begin + si.count) {
-        if (lane == 0) a.keys[c] = kShiftPad;   // another rank owns this frame
-        return;
+    const float *ps;
+    if (a.cprof) {   // the caller supplied every candidate's database profile, in candidate order
+        ps = a.cprof + c * W;
+    } else {
+        const SubInfo si = a.subs[cd.subspace];
+        if (cd.frame < si.shard_begin || cd.frame >= si.shard_begin + si.count) {
+            if (lane == 0) a.keys[c] = kShiftPad;   // another rank owns this frame
+            return;
+        }
+        ps = a.prof + (si.row_begin + (cd.frame - si.shard_begin)) * W;
     }
-    const uint64_t row = si.row_begin + (cd.frame - si.shard_begin);
     if (!OL_DCHECK((uint64_t)cd.bundle * a.M + cd.query_frame < a.nq && cd.query_frame < a.M)) return;
     const float *qs = a.qprof + ((uint64_t)cd.bundle * a.M + cd.query_frame) * W;
-    const float *ps = a.prof + row * W;
     for (uint32_t w = lane; w < W; w += 32) { q[w] = qs[w]; p[w] = ps[w]; }
     __syncwarp();
     u64 best = ~0ull;

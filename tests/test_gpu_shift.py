@@ -110,3 +110,39 @@ def test_shift_keys_min_combine_over_logical_shards():
         d2, s = oracle.shift_distance(QP[cands["bundle"][i], 0], P[cands["frame"][i]])
         assert int(kmin[i] & 0xFFFFFFFF) == s
         assert int(kmin[i] >> 32) == int(np.float32(d2).view(np.uint32))
+
+
+def test_parseval_bound_end_to_end_on_gpu():
+    """The whole NEXT-1 path on the GPU: profiles -> extraction (descriptors + stored profiles,
+    FFT kernel) -> retrieval -> shift re-scoring.  For every candidate the fp32 shift distance
+    is >= (2/W) x its fp32 descriptor distance (the binary64 inequality, minus the fp32 chains'
+    rounding: 1e-4 relative + 1e-7), and is exactly the oracle's chain on the same profiles."""
+    spec = synthgen.Spec(seed=47, n_floors=1, paths=3, frames_per_path=400)
+    pts = synthgen.entry_points(spec, 0, spec.n_entries)
+    DB = synthgen.render_host(spec, pts, profiles=True)
+    qr = synthgen.render_host(spec, synthgen.query_points(spec, 8, 24), profiles=True)
+    e = ol.Engine(0)
+    F, fdeg, FP = e.extract_features(DB["profile"], want_profiles=True)
+    Q, qdeg, QP = e.extract_features(qr["profile"], want_profiles=True)
+    assert not fdeg.any() and not qdeg.any()
+    e.upload(F, DB["tiles"], [400, 400, 400], spec.grid())
+    e.upload_profiles(FP)
+    e.query(Q[:, None, :], N=10, aggregate=False)
+    cands = e.topk()
+    sh, d2 = e.shift_rescore(QP)
+    W = spec.W
+    off = np.array([0, 400, 800])
+    ratios = []
+    for i, cd in enumerate(cands):
+        lb = (2.0 / W) * float(cd["dist2"])
+        assert float(d2[i]) >= lb * (1 - 1e-4) - 1e-7, (i, float(d2[i]), lb)
+        ratios.append(lb / max(float(d2[i]), 1e-30))
+        v, s = oracle.shift_distance(QP[cd["bundle"]], FP[off[cd["subspace"]] + cd["frame"]])
+        assert (int(sh[i]), d2[i].view(np.uint32)) == (s, v.view(np.uint32))
+    assert max(ratios) > 0.1          # the bound is informative on paper-shaped data
+    # the candidate-ordered variant (final candidates' profiles only) gives the same keys
+    CP = np.stack([FP[off[cd["subspace"]] + cd["frame"]] for cd in cands])
+    sh2, d22 = e.shift_rescore_cands(QP, CP)
+    assert np.array_equal(sh, sh2) and np.array_equal(d2.view(np.uint32), d22.view(np.uint32))
+    sh3, d23 = e.shift_rescore_cands(torch.from_numpy(QP).cuda(), torch.from_numpy(CP).cuda())
+    assert np.array_equal(sh, sh3) and np.array_equal(d2.view(np.uint32), d23.view(np.uint32))

@@ -34,7 +34,7 @@ __device__ __forceinline__ float max3f(float a, float b, float c) {
 struct Smem {
     alignas(1024) __half a[128 * 64];
     alignas(1024) __half b[256 * 64];
-    uint64_t tfull[8], tempty[8];
+    uint64_t tfull[8], tempty[8], dummy[8];
     uint32_t tmem;
 };
 
@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(544, 1) probe(int mma, int tiles, long long *o
     for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) s.b[i] = __float2half(0.001f * (i % 5));
     if (threadIdx.x == 0) {
         for (int i = 0; i < NB; ++i) { mbar_init(&s.tfull[i], 1); mbar_init(&s.tempty[i], WPG); }
+        for (int i = 0; i < 8; ++i) mbar_init(&s.dummy[i], 1);
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc<512>(&s.tmem);
@@ -71,6 +72,7 @@ __global__ void __launch_bounds__(544, 1) probe(int mma, int tiles, long long *o
                     for (int k = 0; k < 2; ++k)
                         mma_f16(tmem + buf * TC, desc_sw128_kmajor(smem_u32(s.a) + k * 32),
                                 desc_sw128_kmajor(smem_u32(s.b) + k * 32), idesc, k ? 1u : 0u);
+                if (LDG == 3) mma_commit(&s.dummy[t & 7]);   // a second commit per tile (tcscan frees the TMA stage)
                 mma_commit(&s.tfull[buf]);
             }
         }
@@ -144,9 +146,7 @@ int main() {
     long long *d;
     cudaMalloc(&d, 64);
     run<2, 256, 2, false, 0>(d, "tcscan r01 (2 groups)");
-    run<2, 256, 2, false, 1>(d, "+ LDG consumed 2 tiles later");
-    run<2, 256, 2, false, 2>(d, "+ LDG consumed same tile");
-    run<2, 256, 1, true, 0>(d, "all warps every tile");
-    run<2, 256, 1, true, 1>(d, "+ LDG 2 tiles later");
+    run<2, 256, 2, false, 3>(d, "+ 2nd commit per tile");
+    run<2, 256, 2, true, 3>(d, "+ 2nd commit per tile");
     return 0;
 }
