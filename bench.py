@@ -59,6 +59,7 @@ def _args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--small-batch", type=int, default=8, help="extra HBM-regime line (0 = off)")
     ap.add_argument("--ingest", type=int, default=1 << 20, help="profiles for the NEXT-3 extraction line (0 = off)")
+    ap.add_argument("--heading", type=int, default=1, help="NEXT-1 shift re-scoring line of the step's candidates (0 = off)")
     ap.add_argument("--seconds", type=float, default=5.0, help="C5 streaming duration")
     ap.add_argument("--capacity", action="store_true",
                     help="C5: also sweep the number of 30 fps users for the largest with p99 < 33 ms")
@@ -391,6 +392,10 @@ def run_omniloc(a):
                        "min": float(per_step.min()), "max": float(per_step.max())},
            "setup_s": {"generate": gen_s, "upload": upload_s}}
 
+    # ------------------------------------------------ NEXT-1 heading line: shift re-scoring of the step's candidates
+    if a.heading and world == 1:
+        out["heading"] = heading_line(eng, spec, qpts, stream, sm_max)
+
     # ------------------------------------------------ small-batch (HBM regime) line
     if a.small_batch and world == 1:
         b2 = a.small_batch
@@ -461,10 +466,15 @@ def run_omniloc(a):
         e1.record(stream)
         torch.cuda.synchronize()
         ims = e0.elapsed_time(e1) / reps
-        out["ingest"] = {"kernel": "extract_kernel", "profiles": n_in, "W": Wp, "ms": ims,
-                         "profiles_per_s": n_in / (ims / 1e3),
-                         "fp64_flops_per_profile": 64 * Wp * 4,
-                         "hbm_bytes_per_profile": Wp * 8 + 64 * 4 + 1}
+        ib = Wp * 8 + 64 * 4 + 1    # profile in (binary64), fp32 descriptor + degenerate flag out
+        igbs = n_in * ib / (ims / 1e3) / 1e9
+        out["ingest"] = {"kernel": "fft_extract_kernel<8>", "profiles": n_in, "W": Wp, "ms": ims,
+                         "profiles_per_s": n_in / (ims / 1e3), "hbm_bytes_per_profile": ib,
+                         "roofline": {"bound": "hbm", "achieved": igbs, "peak": hbm_peak, "unit": "GB/s",
+                                      "frac": igbs / hbm_peak,
+                                      "peak_source": "MEASURED_PEAKS hbm_gbs (copy)",
+                                      "note": "FFT (P:121): ~12.8k binary64 operations per profile at W = 256, "
+                                              "vs 65.5k for the round-1 direct sum"}}
         del prof
 
     # ------------------------------------------------ e2e through the public API, host buffers
@@ -502,6 +512,46 @@ def run_omniloc(a):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def heading_line(eng, spec, qpts, stream, sm_max):
+    """NEXT-1: the circular-shift distance and heading of every final candidate
+    of the step just timed (C4: 1,024 frames x N = 15 = 15,360 candidates), from the stored
+    profiles (x - mean)/||m|| of those candidates only (ol_shift_rescore_cands; rendered by
+    the generator, normalised by the library's extraction kernel).  A shift comparison is one
+    (candidate, shift) pair: W fp32 chain steps (FSUB + FFMA)."""
+    import torch
+    import synthgen
+    cands = eng.topk()
+    rows = cands["frame"].astype(np.int64)            # (single subspace: frame = database row)
+    pts = np.concatenate([synthgen.entry_points(spec, int(r), 1) for r in rows])
+    cpr = synthgen.render_host(spec, pts, profiles=True)["profile"]
+    qpr = synthgen.render_host(spec, qpts, profiles=True)["profile"]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    _, _, CP = eng.extract_features(torch.from_numpy(cpr).to(dev), want_profiles=True)
+    _, _, QP = eng.extract_features(torch.from_numpy(qpr).to(dev), want_profiles=True)
+    W = spec.W
+    for _ in range(3):
+        eng.shift_rescore_cands(QP, CP, fetch=False)
+    torch.cuda.synchronize()
+    reps = 20
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        eng.shift_rescore_cands(QP, CP, fetch=False)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    n = len(cands)
+    lane_instr = 2.0 * n * W * W
+    peak = 148 * 128 * sm_max * 1e6 / 1e12
+    ach = lane_instr / (ms / 1e3) / 1e12
+    return {"kernel": "shift_kernel", "candidates": n, "W": W, "ms": ms, "candidates_per_s": n / (ms / 1e3),
+            "shift_comparisons_per_s": n * W / (ms / 1e3),
+            "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "T lane-instr/s", "frac": ach / peak,
+                         "peak_source": f"148 SMs x 128 FP32 lanes x {sm_max:.0f} MHz",
+                         "per_launch": {"lane_instr": lane_instr, "note": "2 FP32 instructions (FSUB, FFMA) per "
+                                        "(candidate, shift, column): the fixed-order chain of R21"}}}
 
 
 def cpu_baseline(F, C, Qd, cfg, n_total, budget_s: float = 15.0):

@@ -92,7 +92,7 @@ extract_kernel(const double *prof, uint64_t n, uint32_t W, float *out32, double 
 
 // ---------------------------------------------------------------- FFT path (W = 32 R)
 template <int R>
-__global__ void __launch_bounds__(32 * kExtractWarps)
+__global__ void __launch_bounds__(32 * kExtractWarps, R <= 8 ? 3 : 1)
 fft_extract_kernel(const double *prof, uint64_t n, float *out32, double *out64, uint8_t *degenerate, float *prof_out) {
     constexpr uint32_t W = 32u * R;
     __shared__ double tc[W], ts[W];   // cos / sin of 2 pi j / W
@@ -169,11 +169,14 @@ fft_extract_kernel(const double *prof, uint64_t n, float *out32, double *out64, 
         for (int o = 16; o; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
         const double norm = sqrt(n2);
         const bool deg = !(norm > 1e-12);
+        // one division, then products (a division per output costs as much as the whole FFT;
+        // the results stay within an ulp of binary64 of m / ||m||)
+        const double inv = deg ? 0.0 : 1.0 / norm;
 #pragma unroll
         for (int k1 = 0; k1 < R; ++k1) {
             const uint32_t k = (uint32_t)k1 + R * k2;
             if (k >= 1 && k <= (uint32_t)kK) {
-                const double c = deg ? 0.0 : re[k1] / norm;
+                const double c = re[k1] * inv;
                 const uint64_t o = p * kK + (k - 1);
                 if (out64) out64[o] = c;
                 if (out32) out32[o] = __double2float_rn(c);
@@ -188,7 +191,7 @@ fft_extract_kernel(const double *prof, uint64_t n, float *out32, double *out64, 
             const double mean = sum / (double)W;
 #pragma unroll
             for (int j = 0; j < R; ++j)
-                prof_out[p * W + lane + 32 * j] = deg ? 0.f : __double2float_rn((x[j] - mean) / norm);
+                prof_out[p * W + lane + 32 * j] = __double2float_rn((x[j] - mean) * inv);
         }
     }
 }
