@@ -554,29 +554,76 @@ def heading_line(eng, spec, qpts, stream, sm_max):
                                         "(candidate, shift, column): the fixed-order chain of R21"}}}
 
 
-def cpu_baseline(F, C, Qd, cfg, n_total, budget_s: float = 15.0):
-    """The oracle as it stands, on the host cores, on a bounded sample of the same
-    workload: the first S rows of the DB and the first q query frames; the rate is
-    scaled to queries/s over the full DB (comparisons/s / n_total)."""
+def cpu_baseline(F, C, Qd, cfg, n_total, budget_s: float = 12.0):
+    """The oracle as it stands, on the host cores (SURVEY 8d "Oracle timing"), each on a
+    bounded sample so the default bench stays within minutes:
+      - value: this workload (C4) on all cores -- the first S rows of the DB and the first q
+        query frames, the rate scaled to queries/s over the full DB (comparisons/s / n_total);
+      - single_thread: the same sample shape on one thread;
+      - coverage: C1 and C2 in full (Alg. 1 + Alg. 2, localisations/s) and C3 on its first
+        64 query frames (queries/s over its whole 1M-row DB), all cores."""
     import oracle
+    import synthgen
     S = min(F.shape[0], 2_000_000)
     Fh = F[:S].cpu().numpy()
     Ch = C[:S].cpu().numpy()
     Qh = Qd.cpu().numpy()
     oracle.lib()
-    t0 = time.perf_counter()
-    oracle.retrieve([S], Fh, Ch, Qh[:1, None, :], cfg.N)
-    t1 = time.perf_counter() - t0
-    nq = int(max(1, min(Qh.shape[0], budget_s / max(t1, 1e-3))))
-    t0 = time.perf_counter()
-    oracle.retrieve([S], Fh, Ch, Qh[:nq, None, :], cfg.N)
-    dt = time.perf_counter() - t0
-    cps = nq * S / dt
-    return {"value": cps / n_total, "unit": "queries/s", "cores": _cores(), "kind": "oracle", "cpu": _cpu_model(),
-            "comparisons_per_sec": cps,
-            "sample": f"{nq} query frames x first {S:,} of {n_total:,} DB rows (full-DB rate = "
-                      f"comparisons/s / {n_total:,}); acc chain + sort-all top-{cfg.N}, OpenMP over rows",
-            "seconds": dt}
+    cores = _cores()
+
+    def rate(nthreads, budget):
+        oracle.set_threads(nthreads)
+        t0 = time.perf_counter()
+        oracle.retrieve([S], Fh, Ch, Qh[:1, None, :], cfg.N)
+        t1 = time.perf_counter() - t0
+        nq = int(max(1, min(Qh.shape[0], budget / max(t1, 1e-3))))
+        t0 = time.perf_counter()
+        oracle.retrieve([S], Fh, Ch, Qh[:nq, None, :], cfg.N)
+        dt = time.perf_counter() - t0
+        return nq, nq * S / dt, dt
+
+    nq, cps, dt = rate(0, budget_s)
+    nq1, cps1, dt1 = rate(1, budget_s / 4)
+    oracle.set_threads(0)
+    out = {"value": cps / n_total, "unit": "queries/s", "cores": cores, "kind": "oracle", "cpu": _cpu_model(),
+           "comparisons_per_sec": cps,
+           "sample": f"{nq} query frames x first {S:,} of {n_total:,} DB rows (full-DB rate = "
+                     f"comparisons/s / {n_total:,}); acc chain + sort-all top-{cfg.N}, OpenMP over rows",
+           "seconds": dt,
+           "single_thread": {"value": cps1 / n_total, "unit": "queries/s", "cores": 1, "comparisons_per_sec": cps1,
+                             "sample": f"{nq1} query frames x first {S:,} DB rows", "seconds": dt1}}
+    cov = {}
+    try:
+        for name in ("C1", "C2"):
+            c = synthgen.CONFIGS[name]
+            Fx, Cx = synthgen.db_host(c.spec)
+            if name == "C1":
+                Qx = synthgen.render_host(c.spec, synthgen.query_points(c.spec, 11, 1))["desc"][:, None, :]
+            else:
+                video = synthgen.render_host(c.spec, synthgen.query_points(c.spec, 22, c.n_queries, "path", 0, 2))["desc"]
+                firsts = [oracle.select_window(len(video), m, c.M)[0] for m in range(len(video))]
+                Qx = synthgen.gather_windows(video, firsts, c.M)
+            t0 = time.perf_counter()
+            ref = oracle.retrieve(c.subspace_sizes, Fx, Cx, Qx, c.N)
+            for b in range(Qx.shape[0]):
+                sel = ref.bundle == b
+                oracle.aggregate(np.column_stack([ref.x[sel], ref.y[sel]]))
+            dt = time.perf_counter() - t0
+            cov[name] = {"bundles": int(Qx.shape[0]), "M": int(Qx.shape[1]), "db_entries": int(Fx.shape[0]),
+                         "seconds": dt, "localisations_per_s": Qx.shape[0] / dt,
+                         "comparisons_per_sec": Qx.shape[0] * Qx.shape[1] * Fx.shape[0] / dt, "sample": "full"}
+        c = synthgen.CONFIGS["C3"]
+        Fx, Cx = synthgen.db_host(c.spec)
+        Qx = synthgen.render_host(c.spec, synthgen.query_points(c.spec, QSEED, 64))["desc"][:, None, :]
+        t0 = time.perf_counter()
+        oracle.retrieve(c.subspace_sizes, Fx, Cx, Qx, c.N)
+        dt = time.perf_counter() - t0
+        cov["C3"] = {"query_frames": 64, "db_entries": int(Fx.shape[0]), "seconds": dt, "queries_per_s": 64 / dt,
+                     "comparisons_per_sec": 64 * Fx.shape[0] / dt, "sample": "first 64 of 1,024 query frames, full DB"}
+    except Exception as ex:   # context only: never fail the bench line
+        cov["error"] = repr(ex)[:200]
+    out["coverage"] = cov
+    return out
 
 
 # =========================================================================== C5 streaming

@@ -69,6 +69,8 @@ def lib():
         L.oracle_shift_distance.restype = flt
         L.oracle_shift_profile.argtypes = [P, i32, i32, P, P]
         L.oracle_shift_profile.restype = i32
+        L.oracle_set_threads.argtypes = [i32]
+        L.oracle_set_threads.restype = None
         _lib = L
     return _lib
 
@@ -91,6 +93,11 @@ def extract_feature(profile, K: int = 64):
     if rc != OR_OK:
         raise ValueError(f"oracle_extract_feature rc={rc}")
     return out, bool(deg.value)
+
+
+def set_threads(n: int):
+    """OpenMP threads of the oracle's parallel loops (timing only; n < 1: all cores)."""
+    lib().oracle_set_threads(int(n))
 
 
 def shift_profile(profile, K: int = 64):

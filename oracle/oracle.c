@@ -24,6 +24,7 @@
  * Parity unpinned: nothing (every function has at least one external pin).
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -368,3 +369,7 @@ float oracle_shift_distance(const float *q, const float *p, int W, int *argmin) 
     *argmin = bs;
     return best;
 }
+
+/* Timing infrastructure (bench.py's cpu_baseline: single-thread and all-core rates); no
+ * arithmetic.  n < 1 restores the OpenMP default. */
+void oracle_set_threads(int n) { omp_set_num_threads(n > 0 ? n : omp_get_num_procs()); }

@@ -15,7 +15,18 @@ from gpu_helpers import assert_candidates_equal, assert_estimates_equal
 pytestmark = pytest.mark.gpu
 
 
-def _sampled_parity(name, sample, kc=16):
+def near_tie_frames(e, Qd, N, k):
+    """The k query frames whose N-th and (N+1)-th best squared distances are closest (relative
+    gap), found with one extra top-(N+1) query: where a wrong prune or a wrong tie order would
+    show first (P:202 top N).  Only picks which frames to check; expected values come from
+    the oracle."""
+    e.query(Qd.view(-1, 1, 64), N=N + 1, aggregate=False)
+    g = e.topk()["dist2"].reshape(-1, N + 1).astype(np.float64)
+    gap = (g[:, N] - g[:, N - 1]) / np.maximum(g[:, N - 1], 1e-30)
+    return [int(i) for i in np.argsort(gap, kind="stable")[:k]]
+
+
+def _sampled_parity(name, sample, kc=16, near_ties=0):
     cfg = synthgen.CONFIGS[name]
     spec = cfg.spec
     n = spec.n_entries
@@ -24,6 +35,8 @@ def _sampled_parity(name, sample, kc=16):
     Qd, _ = synthgen.render_device(spec, synthgen.query_points(spec, 4242, cfg.n_queries), dev)
     e = ol.Engine(0, coarse_k=kc)
     e.upload(F, C, [n], spec.grid())
+    if near_ties:
+        sample = sorted(set(sample) | set(near_tie_frames(e, Qd, cfg.N, near_ties)))
     e.query(Qd.view(-1, 1, 64), N=cfg.N, aggregate=True)
     got = e.topk()
     est = e.estimates()
@@ -56,4 +69,7 @@ def test_c3_sampled():
 
 @pytest.mark.slow
 def test_c4_sampled_bench_config():
-    _sampled_parity("C4", [0, 777])
+    """C4 (100M rows) in the bench's launch configuration: 2 fixed frames plus the 8 frames
+    with the smallest relative gap between their 15th and 16th best distances."""
+    e = _sampled_parity("C4", [0, 777], near_ties=8)
+    assert e.stat("used_tc") == 1
