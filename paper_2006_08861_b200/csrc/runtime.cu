@@ -976,6 +976,9 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         if (c->comm && c->world > 1) { size_t r = 4096; while (r < want) r <<= 1; want = r; }
         OL_CUDA(c, grow(&c->tau0_d, &c->tau_cap, want));
     }
+    // (collective in NCCL mode: every rank reaches it at the same query, whatever path it takes)
+    st = ensure_tau_peers(c);
+    if (st) return st;
     OL_CUDA(c, grow(&c->partial_d, &c->partial_cap, (size_t)nq * (n_items ? n_items : 1) * N));
     OL_CUDA(c, grow(&c->payload_d, &c->payload_cap, (size_t)nq * c->n_sub * N));
     if (c->opt_poison) {   // every per-query output must be written before it is read: fill them with garbage
@@ -1039,6 +1042,9 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         OL_LAUNCH(c, launch_fill_u32(c->tau0_d, (uint64_t)nq * c->n_sub, kInfBits, c->stream));
         OL_LAUNCH(c, launch_tau_seed(sa, c->stream));
     }
+    // NCCL mode: the seeds' MIN over the ranks, at one point of the launch sequence for every
+    // scan path (the collective sequence must not depend on a rank's own data)
+    if (seed && !(c->opt_tc_debug & 64)) { st = share_tau(c, nq); if (st) return st; }
     if (c->opt_tc_debug & 512) { c->nq = nq; return OL_OK; }   // profiling: stop after the seed (ol_thresholds reads it)
     c->used_tc = false;
     c->used_pair = false;
@@ -1093,9 +1099,6 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
                 OL_LAUNCH(c, launch_tcscan(c->map_srows, map_q, pa, (int)(pa.n_items * n_qblocks), c->stream));
             }
         }
-        if (!(a.dbg & 64)) { st = share_tau(c, nq); if (st) return st; }
-        st = ensure_tau_peers(c);
-        if (st) return st;
         a.n_peer = peer_taus(c, (uint64_t)nq * c->n_sub, a.peer_tau);
 
         TimeScope ts(c, ol_ctx::T_SCAN);
@@ -1108,7 +1111,6 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         a.tau0 = seed ? c->tau0_d : nullptr; a.partial = c->partial_d; a.stat_survivors = c->stat_d;
         a.nq = nq; a.n_items = n_items; a.n_qtiles = n_qtiles; a.qt = qt; a.n_sub = c->n_sub; a.N = N;
         a.rows_pad = c->rows_pad;
-        if (seed) { st = share_tau(c, nq); if (st) return st; }
         TimeScope ts(c, ol_ctx::T_SCAN);
         if (qt <= 16 && c->opt_scan2 == 2 && c->kc < OL_K)   // few frames: TMA-fed row-pair kernel
             OL_LAUNCH(c, launch_scan3(c->kc, a, scan3_smem_bytes(qt, N, c->kc), (int)(n_items * n_qtiles), c->stream));
