@@ -66,9 +66,10 @@ def _args():
     return ap.parse_args()
 
 
-# tools/pipe_probe.cu on a B200 (round 1): cycles per 128-frame x 256-row accumulator tile of
-# the tensor-core scan's MMA -> TMEM -> epilogue pipeline alone, by filter dimensions K
-PIPE_PROBE = {16: 773, 32: 841, 64: 953}
+# tools/pipe_probe2.cu on a B200 (round 2): cycles per 128-frame x 256-row accumulator tile of
+# the tensor-core scan's MMA -> TMEM -> epilogue pipeline alone (K = 32, two 8-warp groups,
+# 2 x 256-column buffers, FMNMX3 math); round 1's probe (841) had a serial-chain epilogue
+PIPE_PROBE = {32: 456}
 
 
 class Clocks:
@@ -328,18 +329,18 @@ def run_omniloc(a):
         pw = 32 if kf == 32 else 64                    # fp16 plane row width (halves)
         alg_bytes = rows_local * pw * 2 + rows_local // 32 * 8   # fp16 rows + 8 B bound terms per 32 rows, once
         # traffic: DRAM bytes of one launch from the committed `ncu --set full` capture of this
-        # workload (profiles/r01_tcscan_ncu.json), only when this run is that workload
+        # workload (profiles/r02_tcscan_ncu.json), only when this run is that workload
         traffic = None
         try:
             prof = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                               "r01_tcscan_ncu.json")))
+                                               "r02_tcscan_ncu.json")))
             if a.config == "C4" and B == 1024 and world == 1:
                 traffic = prof["traffic_bytes_per_launch"]
         except (OSError, KeyError, ValueError):
             pass
         roofline = {"kernel": "tcscan_kernel", "bound": "tensor", "achieved": achieved, "peak": tc_peak,
                     "unit": "TFLOP/s", "frac": achieved / tc_peak if achieved else None, "traffic": traffic,
-                    "traffic_source": "profiles/r01_tcscan_ncu.json (ncu --set full, one launch)" if traffic else None,
+                    "traffic_source": "profiles/r02_tcscan_ncu.json (ncu --set full, one launch)" if traffic else None,
                     "peak_source": "MEASURED_PEAKS bf16_tflops_sustained (fp16 = bf16 nominal rate); "
                                    f"burst {peaks.get('bf16_tflops')}",
                     "per_launch": {"pairs": pairs, "filter_k": kf, "mma_flops": flops, "algorithmic_bytes": alg_bytes,
@@ -349,7 +350,7 @@ def run_omniloc(a):
                                    # with 16 warps (x 148 SMs x max clock)
                                    "tmem_read_tbs": pairs * 4 / scan_s / 1e12 if scan_s > 0 else None,
                                    "tmem_probe_peak_tbs": 271 * 148 * sm_max * 1e6 / 1e12,
-                                   # the MMA -> TMEM -> epilogue pipeline alone (tools/pipe_probe.cu,
+                                   # the MMA -> TMEM -> epilogue pipeline alone (tools/pipe_probe2.cu,
                                    # two 8-warp groups, 2 x 256-column buffers): cycles per 128-frame
                                    # x 256-row tile at this K; the kernel's ceiling at max clock
                                    "pipeline_probe_cycles_per_tile": PIPE_PROBE.get(kf),
@@ -474,7 +475,8 @@ def run_omniloc(a):
                                       "frac": igbs / hbm_peak,
                                       "peak_source": "MEASURED_PEAKS hbm_gbs (copy)",
                                       "note": "FFT (P:121): ~12.8k binary64 operations per profile at W = 256, "
-                                              "vs 65.5k for the round-1 direct sum"}}
+                                              "vs 65.5k for the round-1 direct sum; the kernel is FP64-issue "
+                                              "bound: ncu fp64 pipe 50 % active (profiles/r02_summary.md)"}}
         del prof
 
     # ------------------------------------------------ e2e through the public API, host buffers
