@@ -60,6 +60,7 @@ def _args():
     ap.add_argument("--small-batch", type=int, default=8, help="extra HBM-regime line (0 = off)")
     ap.add_argument("--ingest", type=int, default=1 << 20, help="profiles for the NEXT-3 extraction line (0 = off)")
     ap.add_argument("--heading", type=int, default=1, help="NEXT-1 shift re-scoring line of the step's candidates (0 = off)")
+    ap.add_argument("--c5-seconds", type=float, default=3.0, help="C5 streaming sub-line duration (0 = off)")
     ap.add_argument("--seconds", type=float, default=5.0, help="C5 streaming duration")
     ap.add_argument("--capacity", action="store_true",
                     help="C5: also sweep the number of 30 fps users for the largest with p99 < 33 ms")
@@ -506,6 +507,25 @@ def run_omniloc(a):
                       "copies": "frames H2D from pinned host inside ol_query; candidates (32 B each) and "
                                 "estimates (1,072 B each) D2H into pinned host"}
 
+    # ------------------------------------------------ C5 streaming sub-line (BASELINE configs[4])
+    if a.c5_seconds > 0 and world == 1:
+        del eng
+        torch.cuda.empty_cache()
+        c5 = synthgen.CONFIGS["C5"]
+        F5, C5 = synthgen.db_device(c5.spec, 0, c5.spec.n_entries, dev)
+        e5 = ol.Engine(local, coarse_k=16)
+        e5.upload(F5, C5, [c5.spec.n_entries], c5.spec.grid())
+        del F5, C5
+        lat = stream_latencies(e5, c5.spec, c5, 8, 30.0, a.c5_seconds, 5, 1, ol.Params(N=c5.N))
+        out["c5_streaming"] = {"metric": "latency, arrival of frame m+2 -> estimate of frame m on the host",
+                               "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+                               "localizations": int(lat.size), "users": 8, "fps": 30.0, "seconds": a.c5_seconds,
+                               "db_entries": c5.spec.n_entries, "M": 5, "N": c5.N,
+                               "note": "host wall clock, one process; every request scores its micro-batch "
+                                       "(M = 1) against the 10M-row DB and localises with Alg. 2 (75 candidates)"}
+        del e5
+        torch.cuda.empty_cache()
+
     # ------------------------------------------------ CPU oracle baseline (rank 0, N = 1)
     if rank == 0 and world == 1 and not a.no_cpu:
         out["cpu_baseline"] = cpu_baseline(F, C, Qd, cfg, n_total)
@@ -629,46 +649,23 @@ def cpu_baseline(F, C, Qd, cfg, n_total, budget_s: float = 12.0):
 
 
 # =========================================================================== C5 streaming
-def run_streaming(a):
-    """C5 (SURVEY §8d): 8 users x 30 fps against a 10M-row DB for `--seconds`.  Frames
-    arrive on a staggered 30 Hz schedule (wall clock); whenever the GPU is free the
-    server scores every frame that has arrived (a micro-batch of <= 8, M = 1, N = 15)
-    and caches its top-N; when user u's frame m+2 arrives, frame m is localised by
-    Algorithm 2 over the M = 5 window's cached candidates (75).  Latency = arrival of
-    frame m+2 -> estimate readable on the host.  Reports p50 / p99."""
-    import torch
+def stream_latencies(eng, spec, cfg, users, fps, secs, M, world, params):
+    """The C5 serving loop: frames of `users` walkers arrive at `fps` with
+    staggered phases; whenever the GPU is free every arrived frame is scored in one micro-batch
+    (M = 1, N = 15) and its top-N cached; when frame m+2 of a user arrives, frame m is
+    localised by Algorithm 2 over its M = 5 window's cached candidates.  Returns the latencies
+    (ms) from the arrival of frame m+2 to the estimate being readable on the host."""
     import synthgen
     import paper_2006_08861_b200 as ol
-    rank, world, local = _dist_init(a.gpus)
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-    cfg = synthgen.CONFIGS["C5"]
-    spec = cfg.spec
-    n_total = spec.n_entries
-    b0, cnt = ol.shard_range(n_total, rank, world)
-    F, C = synthgen.db_device(spec, b0, cnt, dev)
-    users, fps, secs, M = 8, 30.0, a.seconds, 5
     n_frames = int(fps * secs)
-    # each user walks a test path of its own floor; frames rendered up front
     vids = []
-    for u in range(users):
+    for u in range(users):   # each user walks a test path of its own floor; frames rendered up front
         pts = synthgen.query_points(spec, 7000 + u, n_frames, "path", floor=(u * 37) % spec.n_floors,
                                     path=u % spec.paths)
         vids.append(synthgen.render_host(spec, pts)["desc"])
-    group = None
-    if world > 1:
-        import torch.distributed as dist
-        group = dist.group.WORLD
-    eng = ol.Engine(local, coarse_k=16, process_group=group, exchange=a.exchange)
-    eng.upload(F, C, [n_total], spec.grid())
-    if a.graph and world == 1:
-        eng.set_option("graph", 1)
-    del F, C
-    params = ol.Params(N=cfg.N)
     cache = [dict() for _ in range(users)]
     arrive = np.array([[(m + u / users) / fps for u in range(users)] for m in range(n_frames)])  # [m][u]
-    # warm-up
-    eng.query(vids[0][:users][:, None, :].copy(), params=params, aggregate=False)
+    eng.query(vids[0][:users][:, None, :].copy(), params=params, aggregate=False)   # warm-up
     eng.topk()
     lat = []
     done = np.zeros(users, np.int64)          # frames scored per user
@@ -703,6 +700,39 @@ def run_streaming(a):
             eng.aggregate(np.concatenate(xy), np.array(offs, np.uint32), params)
             t = time.perf_counter() - t0
             lat.extend((t - o) * 1e3 for o in owners)
+    return np.array(lat)
+
+
+def run_streaming(a):
+    """C5 (SURVEY §8d): 8 users x 30 fps against a 10M-row DB for `--seconds`.  Frames
+    arrive on a staggered 30 Hz schedule (wall clock); whenever the GPU is free the
+    server scores every frame that has arrived (a micro-batch of <= 8, M = 1, N = 15)
+    and caches its top-N; when user u's frame m+2 arrives, frame m is localised by
+    Algorithm 2 over the M = 5 window's cached candidates (75).  Latency = arrival of
+    frame m+2 -> estimate readable on the host.  Reports p50 / p99."""
+    import torch
+    import synthgen
+    import paper_2006_08861_b200 as ol
+    rank, world, local = _dist_init(a.gpus)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg = synthgen.CONFIGS["C5"]
+    spec = cfg.spec
+    n_total = spec.n_entries
+    b0, cnt = ol.shard_range(n_total, rank, world)
+    F, C = synthgen.db_device(spec, b0, cnt, dev)
+    users, fps, secs, M = 8, 30.0, a.seconds, 5
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        group = dist.group.WORLD
+    eng = ol.Engine(local, coarse_k=16, process_group=group, exchange=a.exchange)
+    eng.upload(F, C, [n_total], spec.grid())
+    if a.graph and world == 1:
+        eng.set_option("graph", 1)
+    del F, C
+    params = ol.Params(N=cfg.N)
+    lat = stream_latencies(eng, spec, cfg, users, fps, secs, M, world, params)
     lat = np.array(lat)
     cap = _capacity(eng, spec, params, M, fps) if a.capacity and world == 1 else None
     out = {"metric": "C5 streaming latency (arrival of frame m+2 -> estimate of frame m)",
