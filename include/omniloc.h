@@ -425,6 +425,10 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *                   memory (handles exchanged collectively through the communicator); any
  *                   rank's published threshold bounds the global N-th best, so results are
  *                   identical and small shards prune as well as the whole database
+ *   "micro"         1 (default) / 0: world-1 queries with <= 8,192 rows per subspace and <= 65,536
+ *                   (frame, row) pairs run as ONE kernel (NK10: exact scan, top-N, candidate
+ *                   rows, Algorithm 2 by each bundle's last job) instead of the launch
+ *                   sequence; not used when "tc", "chunk" or "qtile" force a path or schedule
  *   "poison"        0 (default) / 1: tests (an initcheck stand-in): the next uploads fill padding
  *                   rows and coords with NaN bytes instead of zeros, and every query first
  *                   fills its scratch and output buffers with garbage; results must not change
@@ -443,6 +447,7 @@ OL_API ol_status ol_set_option(ol_ctx *ctx, const char *key, int64_t value);
 
 /* Read statistics of the last query: "nccl" (1 if the context owns a communicator),
  * "tau_peers" (other ranks' threshold arrays the tensor-core scan publishes into),
+ * "used_micro" (1 if the last query ran as the single small-problem kernel),
  * "nccl_version" (of the loaded NCCL, 0 if none), "survivors" (pairs that passed the coarse
  * bound), "pairs" (pairs scanned), "kernels" (kernel launches of the last
  * ol_query + ol_finalize), "used_tc" / "used_pair" (1 if the tensor-core scan / CTA pairs

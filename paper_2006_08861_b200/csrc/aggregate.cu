@@ -68,12 +68,12 @@ __device__ __forceinline__ u64 tile_key(int32_t x, int32_t y) {
 __device__ __forceinline__ int32_t key_x(u64 k) { return (int32_t)((uint32_t)k ^ 0x80000000u); }
 __device__ __forceinline__ int32_t key_y(u64 k) { return (int32_t)((uint32_t)(k >> 32) ^ 0x80000000u); }
 
-__global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
-    extern __shared__ __align__(16) unsigned char smem[];
+// Algorithm 2 for bundle b, by the whole CTA (kAggThreads threads); smem: the dynamic shared
+// memory (2 x cap u64 + cap u32).  Shared by aggregate_kernel and micro_kernel.
+__device__ __noinline__ void aggregate_block(const AggArgs &a, uint32_t b, unsigned char *smem) {
     __shared__ uint32_t scratch[32];
     __shared__ uint32_t circ[OL_MAX_TOP_C];
     __shared__ uint32_t red[kAggThreads / 32];
-    const uint32_t b = blockIdx.x;
     uint32_t begin, total;
     if (a.cand) { begin = b * a.per_bundle; total = a.per_bundle; }
     else { begin = a.offsets[b]; total = a.offsets[b + 1] - begin; }
@@ -187,6 +187,118 @@ __global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
         }
         out->ranked[r] = rt;
     }
+}
+
+__global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    aggregate_block(a, blockIdx.x, smem);
+}
+
+// ---------------------------------------------------------------- small problems (NK10)
+// The whole launch sequence of a small world-1 query in ONE kernel (the latency configs:
+// C1 = 2,000 rows x 1 frame ran 6 launches, ~5 us each): one CTA per (frame, subspace) job
+// checks its frame, scores every row of the subspace with the exact chain of R3 (k = 0..63 in
+// order; the coarse plane for k < kc, the fine plane after -- the same values as one pass),
+// keeps the keys (acc bits << 32 | frame) in shared memory, extracts the N smallest by N
+// rounds of a block-wide minimum above the previous one (keys are unique), writes the
+// candidate rows in SPEC order and, when it is the last job of its bundle to finish
+// (a counter per bundle, reset by that CTA), runs Algorithm 2 for the bundle.  Results are
+// the plain definition's, bit for bit, like every other path.
+__global__ void __launch_bounds__(kAggThreads) micro_kernel(MicroArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ __align__(16) float qs[kK];
+    __shared__ u64 wmin[kAggThreads / 32];
+    __shared__ u64 last_key;
+    __shared__ uint32_t is_last;
+    const uint32_t job = blockIdx.x, q = job / a.n_sub, i = job % a.n_sub;
+    const SubInfo si = a.subs[i];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < kK) {
+        const float v = a.queries[(size_t)q * kK + threadIdx.x];
+        qs[threadIdx.x] = v;
+        if (a.check_finite && !isfinite(v)) *a.flag_nonfinite = 1;
+    }
+    __syncthreads();
+    u64 *keys = reinterpret_cast<u64 *>(smem);   // [si.count]
+    const uint32_t n = (uint32_t)si.count;
+    for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+        const uint64_t row = si.row_begin + r;
+        float acc = 0.f;
+#pragma unroll 4
+        for (int k = 0; k < kK; ++k) {
+            const float f = k < (int)a.kc ? a.coarse[coarse_off(row, (uint32_t)k, a.kc)]
+                                          : a.fine[row * (kK - a.kc) + (k - a.kc)];
+            const float d = __fsub_rn(qs[k], f);
+            acc = __fmaf_rn(d, d, acc);
+        }
+        keys[r] = ((u64)__float_as_uint(acc) << 32) | (u64)(si.shard_begin + r);
+    }
+    if (threadIdx.x == 0) last_key = 0;
+    __syncthreads();
+    const uint32_t c = min(a.N, n);   // min(N, |n_i|) rows
+    ol_candidate *co = a.cand + (uint64_t)q * a.sub_prefix[a.n_sub] + a.sub_prefix[i];
+    for (uint32_t r = 0; r < c; ++r) {
+        const u64 lo = last_key;
+        const bool first = r == 0;
+        u64 best = kPadKey;
+        for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+            const u64 v = keys[t];
+            if ((first || v > lo) && v < best) best = v;
+        }
+        for (int o = 16; o; o >>= 1) {
+            const u64 w = __shfl_xor_sync(0xffffffffu, best, o);
+            best = w < best ? w : best;
+        }
+        if (lane == 0) wmin[warp] = best;
+        __syncthreads();
+        if (warp == 0) {
+            u64 v = lane < kAggThreads / 32 ? wmin[lane] : kPadKey;
+            for (int o = 16; o; o >>= 1) {
+                const u64 w = __shfl_xor_sync(0xffffffffu, v, o);
+                v = w < v ? w : v;
+            }
+            if (lane == 0) {
+                last_key = v;
+                const uint32_t frame = (uint32_t)v;
+                const uint64_t row = si.row_begin + (frame - si.shard_begin);
+                const float acc = __uint_as_float((uint32_t)(v >> 32));
+                ol_candidate o;
+                o.subspace = i; o.frame = frame; o.bundle = q / a.M; o.query_frame = q % a.M;
+                o.dist2 = acc; o.dist = __fsqrt_rn(acc);
+                const bool ok = OL_DCHECK(frame >= si.shard_begin && frame - si.shard_begin < si.count);
+                o.x = ok ? a.coords[2 * row] : 0; o.y = ok ? a.coords[2 * row + 1] : 0;
+                co[r] = o;
+            }
+        }
+        __syncthreads();
+    }
+    if (!a.aggregate) return;
+    // Algorithm 2 once the bundle's last job has written its rows
+    __threadfence();
+    __syncthreads();
+    const uint32_t b = q / a.M;
+    if (threadIdx.x == 0) {
+        const uint32_t done = atomicAdd(&a.bundle_count[b], 1u) + 1;
+        is_last = done == a.M * a.n_sub;
+        if (is_last) a.bundle_count[b] = 0;   // (ready for the next query)
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    aggregate_block(a.agg, b, smem);
+}
+
+size_t micro_smem_bytes(uint64_t max_rows, uint32_t agg_cap) {
+    const size_t rows = sizeof(u64) * max_rows;
+    const size_t agg = agg_cap ? sizeof(u64) * agg_cap * 2 + sizeof(uint32_t) * agg_cap : 0;
+    return rows > agg ? rows : agg;
+}
+
+cudaError_t launch_micro(const MicroArgs &a, size_t smem, cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(micro_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    micro_kernel<<<a.nq * a.n_sub, kAggThreads, smem, s>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_aggregate(const AggArgs &a, cudaStream_t s) {

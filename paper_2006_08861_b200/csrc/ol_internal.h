@@ -157,6 +157,24 @@ struct AggArgs {
     uint32_t cap;                // power of two >= every bundle's size (<= kAggMax); 0 = kAggMax
 };
 
+// NK10: one kernel for a whole small world-1 query (aggregate.cu)
+struct MicroArgs {
+    const float *coarse, *fine, *queries;   // planes, frames [nq][K]
+    const SubInfo *subs;
+    const int32_t *coords;
+    const uint32_t *sub_prefix;             // [n_sub+1] prefix of min(N, |n_i|)
+    ol_candidate *cand;
+    uint32_t *bundle_count;                 // [n_bundles] zeroed; each last job resets its own
+    int *flag_nonfinite;
+    uint32_t nq, n_sub, N, M, kc;
+    int check_finite, aggregate;
+    AggArgs agg;                            // cand / per_bundle / out / params of Algorithm 2
+};
+constexpr uint64_t kMicroMaxRows = 8192;    // per subspace (64 KB of keys in shared memory)
+constexpr uint64_t kMicroMaxPairs = 1u << 16;   // frames x rows of the whole query
+size_t micro_smem_bytes(uint64_t max_rows, uint32_t agg_cap);
+cudaError_t launch_micro(const MicroArgs &a, size_t smem, cudaStream_t s);
+
 struct TcScanArgs {
     const WorkItem *items;
     const float2 *blk;            // [rows_pad / 32] per 32-row block: (min RD||f||^2/2, max RU e_f)

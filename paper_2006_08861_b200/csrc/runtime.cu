@@ -166,6 +166,9 @@ struct ol_ctx {
     uint32_t *prefix_d = nullptr;   // the prefix of the last ensure_prefix
     bool cand_fused = false;  // world 1: merge_chunks_kernel wrote the candidate rows
     uint32_t *agg_off_d = nullptr; size_t agg_off_cap = 0;
+    uint32_t *bcount_d = nullptr; size_t bcount_cap = 0;   // NK10 per-bundle job counters (kept zero)
+    bool used_micro = false;
+    int64_t opt_micro = 1;
     int32_t *agg_xy_d = nullptr; size_t agg_xy_cap = 0;
     int *flags_d = nullptr;                // [0] nonfinite frames, [1] aggregation error
     unsigned long long *stat_d = nullptr;  // [0] survivors
@@ -217,6 +220,7 @@ struct ol_ctx {
         int launches;
         const ItemTable *cur;   // the (immutable) tables the captured launches read
         uint32_t *prefix_d;
+        bool used_micro;
     };
     struct GraphEntry {
         QueryKey key;
@@ -461,7 +465,7 @@ void ol_destroy(ol_ctx *c) {
     cudaFree(c->seed_scratch); cudaFree(c->sitems_d); cudaFree(c->q_d); cudaFree(c->tau0_d); cudaFree(c->partial_d);
     cudaFree(c->payload_d); cudaFree(c->final_d); cudaFree(c->cand_d); cudaFree(c->est_d);
     p2p_close(c);
-    cudaFree(c->agg_off_d); cudaFree(c->agg_xy_d);
+    cudaFree(c->agg_off_d); cudaFree(c->bcount_d); cudaFree(c->agg_xy_d);
     cudaFree(c->flags_d); cudaFree(c->stat_d); cudaFree(c->tcstat_d); cudaFree(c->prof_d);
     cudaFree(c->q16); cudaFree(c->qmeta); cudaFree(c->qprof_d); cudaFree(c->shift_keys);
     for (auto &v : c->ev)
@@ -756,7 +760,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
 
 static ol_ctx::QueryState save_state(const ol_ctx *c) {
     return {c->used_tc, c->used_pair, c->nb, c->M, c->N, c->nq, c->qt, c->aggregate, c->params,
-            c->n_cand, c->per_bundle, c->pairs, c->launches, c->cur, c->prefix_d};
+            c->n_cand, c->per_bundle, c->pairs, c->launches, c->cur, c->prefix_d, c->used_micro};
 }
 
 static void load_state(ol_ctx *c, const ol_ctx::QueryState &s) {
@@ -765,6 +769,7 @@ static void load_state(ol_ctx *c, const ol_ctx::QueryState &s) {
     c->per_bundle = s.per_bundle; c->pairs = s.pairs; c->launches = s.launches;
     c->cur = s.cur; c->items_d = s.cur ? s.cur->items_d : nullptr; c->items_chunk = s.cur ? s.cur->chunk : 0;
     c->prefix_d = s.prefix_d;
+    c->used_micro = s.used_micro;
     c->q_ready = true;
     c->finalized = c->world == 1;
     c->shift_ready = false;
@@ -937,6 +942,57 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
     const uint32_t nq = (uint32_t)nq64, N = p->N;
     ol_status st;
     c->launches = 0;
+    c->used_micro = false;
+
+    // small world-1 problems (the latency configurations): the whole sequence in one kernel
+    uint64_t max_rows = 0;
+    for (auto &sb : c->subs) max_rows = sb.count > max_rows ? sb.count : max_rows;
+    // (not when an option forces a scan path or schedule: tests of those paths keep them)
+    if (c->opt_micro && c->opt_tc == -1 && !c->opt_chunk && !c->opt_qtile && !(c->opt_tc_debug & 512) &&
+        c->world == 1 && !c->comm && max_rows <= kMicroMaxRows && max_rows > 0 &&
+        (uint64_t)nq * c->rows <= kMicroMaxPairs) {
+        st = ensure_prefix(c, N);
+        if (st) return st;
+        OL_CUDA(c, grow(&c->cand_d, &c->cand_cap, per_q * nq));
+        uint32_t cap = 0;
+        if (aggregate) {
+            OL_CUDA(c, grow(&c->est_d, &c->est_cap, nb));
+            if (nb > c->bcount_cap || !c->bcount_d) {
+                OL_CUDA(c, grow(&c->bcount_d, &c->bcount_cap, nb));
+                OL_CUDA(c, cudaMemsetAsync(c->bcount_d, 0, sizeof(uint32_t) * c->bcount_cap, c->stream));
+            }
+            cap = 32;
+            while (cap < per_q * M) cap <<= 1;
+        }
+        OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 2 * sizeof(int), c->stream));
+        MicroArgs ma;
+        ma.coarse = c->coarse; ma.fine = c->fine; ma.queries = q; ma.subs = c->subs_d; ma.coords = c->coords;
+        ma.sub_prefix = c->prefix_d; ma.cand = c->cand_d; ma.bundle_count = c->bcount_d;
+        ma.flag_nonfinite = c->flags_d;
+        ma.nq = nq; ma.n_sub = c->n_sub; ma.N = N; ma.M = M; ma.kc = (uint32_t)c->kc;
+        ma.check_finite = on_device ? 1 : 0;   // (host frames were checked on the host)
+        ma.aggregate = aggregate ? 1 : 0;
+        AggArgs &ag = ma.agg;
+        ag.cand = c->cand_d; ag.per_bundle = (uint32_t)(per_q * M); ag.offsets = nullptr; ag.xy = nullptr;
+        ag.out = c->est_d; ag.err_empty = c->flags_d + 1; ag.n_bundles = nb; ag.top_c = p->top_c;
+        ag.toler_per = p->toler_per;
+        const double r = p->radius_m / p->tile_m;
+        ag.r2 = r * r; ag.tile_m = p->tile_m; ag.cap = cap;
+        {
+            TimeScope ts(c, ol_ctx::T_SCAN);
+            OL_LAUNCH(c, launch_micro(ma, micro_smem_bytes(max_rows, cap), c->stream));
+        }
+        c->used_tc = c->used_pair = false;
+        c->used_micro = true;
+        c->cand_fused = true;
+        c->nb = nb; c->M = M; c->N = N; c->nq = nq; c->qt = 0; c->aggregate = aggregate; c->params = *p;
+        c->per_bundle = per_q * M;
+        c->n_cand = per_q * nq;
+        c->pairs = (uint64_t)nq * c->rows;
+        c->q_ready = true;
+        c->finalized = true;
+        return OL_OK;
+    }
 
     // launch shape (results never depend on it): tensor-core filter or CUDA-core
     // scan, query tile, chunk size
@@ -1667,6 +1723,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "tc_debug")) { if (v < 0 || v > 65535) goto bad; c->opt_tc_debug = v; }
     else if (!strcmp(key, "graph")) { if (v != 0 && v != 1) goto bad; c->opt_graph = v; }
     else if (!strcmp(key, "tau_share")) { if (v != 0 && v != 1) goto bad; c->opt_tau_share = v; }
+    else if (!strcmp(key, "micro")) { if (v != 0 && v != 1) goto bad; c->opt_micro = v; }
     else if (!strcmp(key, "poison")) { if (v != 0 && v != 1) goto bad; c->opt_poison = v; }
     else return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown option '%s'", key);
     ++c->gen;   // every option can change the launch sequence: retire a captured graph
@@ -1677,7 +1734,8 @@ bad:
 
 ol_status ol_get_stat(ol_ctx *c, const char *key, int64_t *value) {
     if (!c || !key || !value) return fail(c, OL_ERR_INVALID_ARGUMENT, "NULL argument");
-    if (!strcmp(key, "survivors")) {
+    if (!strcmp(key, "survivors") && c->used_micro) *value = (int64_t)c->pairs;   // (NK10: every pair scored)
+    else if (!strcmp(key, "survivors")) {
         unsigned long long v = 0;
         OL_CUDA(c, cudaMemcpyAsync(&v, c->stat_d, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
         OL_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -1700,6 +1758,7 @@ ol_status ol_get_stat(ol_ctx *c, const char *key, int64_t *value) {
     else if (!strcmp(key, "items")) *value = (int64_t)c->n_items();
     else if (!strcmp(key, "used_tc")) *value = c->used_tc ? 1 : 0;
     else if (!strcmp(key, "used_pair")) *value = c->used_pair ? 1 : 0;
+    else if (!strcmp(key, "used_micro")) *value = c->used_micro ? 1 : 0;
     else if (!strcmp(key, "tc_k")) *value = (int64_t)c->tc_kf;
     else if (!strcmp(key, "tc_ok")) *value = c->tc_ok ? 1 : 0;
     else if (!strcmp(key, "nccl")) *value = c->comm ? 1 : 0;

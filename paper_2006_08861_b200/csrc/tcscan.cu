@@ -291,7 +291,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
         if (lane == 0 && rank == 0) {
             // M = 128 frames (pair: 256, both CTAs' frames), N = 256 rows
             const uint32_t idesc = idesc_f16_f32(kPair ? 256 : 128, kTileRows);
-            long long pw_full = 0, pw_tempty = 0;
+            long long pw_full = 0, pw_tempty = 0, pw_issue = 0;   // (profiling: prof[0], [1], [16])
             mbar_wait(&s.qbar, 0);
             const uint32_t qm = smem_u32(s.qm);
             for (uint32_t t = 0; t < n_tiles; ++t) {
@@ -300,7 +300,8 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 mbar_wait_sleep(&s.full[st], (t / n_stages) & 1);
                 long long c1 = clock64();
                 if (t >= kTBufs) mbar_wait_sleep(&s.tempty[buf], ((t / kTBufs) - 1) & 1);
-                if (prof) { pw_full += c1 - c0; pw_tempty += clock64() - c1; }
+                long long c2 = prof ? clock64() : 0;
+                if (prof) { pw_full += c1 - c0; pw_tempty += c2 - c1; }
                 tc_fence_after();
                 const uint32_t rm = smem_u32(stage0 + (size_t)st * stage_bytes);
                 const uint32_t d = tmem + buf * kTileRows;
@@ -317,8 +318,10 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 }
                 if (kPair) { mma_commit_pair(&s.empty[st], 3); mma_commit_pair(&s.tfull[buf], 3); }
                 else { mma_commit(&s.empty[st]); mma_commit(&s.tfull[buf]); }
+                if (prof) pw_issue += clock64() - c2;
             }
-            if (prof) { atomicAdd(&a.prof[0], (unsigned long long)pw_full); atomicAdd(&a.prof[1], (unsigned long long)pw_tempty); }
+            if (prof) { atomicAdd(&a.prof[0], (unsigned long long)pw_full); atomicAdd(&a.prof[1], (unsigned long long)pw_tempty);
+                        atomicAdd(&a.prof[16], (unsigned long long)pw_issue); }
         }
     } else if (warp < 2 + kEpiWarps) {
         // ------------------------------------------------------------ epilogue

@@ -381,3 +381,44 @@ def test_tau_share_emulated_shards_match_oracle(c2, world):        # §8e, in-sc
     e = engines.pop()
     e.close()                              # unlinks itself from the others
     assert engines[0].stat("tau_peers") == world - 2
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_micro_kernel_small_queries_vs_oracle(seed):            # NK10, the latency configurations
+    """Small world-1 queries run as ONE kernel (scan, top-N, candidate rows, Alg. 2 by each
+    bundle's last job): candidates and estimates equal the oracle's, with several subspaces
+    (one smaller than N), bundles of M = 1/3/5, ties from duplicated rows, and graph
+    replay; the same queries with the kernel disabled give the same bytes."""
+    rng = np.random.default_rng(900 + seed)
+    sizes = [int(rng.integers(2, 3000)) for _ in range(int(rng.integers(1, 4)))]
+    sizes[0] = min(sizes[0], 9)                                   # an undersized subspace
+    F = np.abs(rng.standard_normal((sum(sizes), 64))).astype(np.float32)
+    F /= np.linalg.norm(F, axis=1, keepdims=True)
+    F[rng.integers(0, len(F), 20)] = F[rng.integers(0, len(F), 20)]   # exact duplicates: ties
+    C = rng.integers(0, 60, (sum(sizes), 2)).astype(np.int32)
+    M = int(rng.choice([1, 3, 5]))
+    nb = int(rng.integers(1, 6))
+    nb = max(1, min(nb, (1 << 16) // (len(F) * M)))   # within the single-kernel size
+    M = M if nb * M * len(F) <= (1 << 16) else 1
+    Q = (F[rng.integers(0, len(F), nb * M)] + 1e-3 * rng.standard_normal((nb * M, 64))).astype(np.float32)
+    Q = np.ascontiguousarray(Q.reshape(nb, M, 64))
+    N = int(rng.choice([1, 5, 15, 40]))
+    ref = oracle.retrieve(sizes, F, C, Q, N)
+    e = _engine(16)
+    e.upload(F, C, sizes, (64, 64))
+    e.query(Q, N=N, aggregate=True)
+    assert e.stat("used_micro") == 1 and e.stat("kernels") == 1
+    got, est = e.topk(), e.estimates()
+    assert_candidates_equal(got, ref, f"micro seed {seed}")
+    assert_estimates_equal(est, ref, ctx=f"micro seed {seed}")
+    e.set_option("graph", 1)
+    qd = torch.from_numpy(Q).cuda()
+    for _ in range(3):
+        e.query(qd, N=N, aggregate=True)
+    assert e.stat("graph_replays") == 2 and e.stat("used_micro") == 1
+    assert e.topk().tobytes() == got.tobytes() and e.estimates().tobytes() == est.tobytes()
+    e.set_option("graph", 0)
+    e.set_option("micro", 0)
+    e.query(Q, N=N, aggregate=True)
+    assert e.stat("used_micro") == 0
+    assert e.topk().tobytes() == got.tobytes() and e.estimates().tobytes() == est.tobytes()

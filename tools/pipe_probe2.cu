@@ -73,9 +73,14 @@ __global__ void __launch_bounds__(640, 1) probe(int mma, int tiles, long long *o
                 if (t >= NB) mbar_wait(&s.tempty[buf], ((t / NB) - 1) & 1);
                 tc_fence_after();
                 if (mma)
-                    for (int k = 0; k < 2; ++k)
-                        mma_f16(tmem + buf * TC, desc_sw128_kmajor(smem_u32(s.a) + k * 32),
-                                desc_sw128_kmajor(smem_u32(s.b) + k * 32), idesc, k ? 1u : 0u);
+                    for (int k = 0; k < 2; ++k) {
+                        if (extra & 4)   // the 64-byte plane (tcscan at kf = 32): SW64 K-major operands
+                            mma_f16(tmem + buf * TC, desc_sw64_kmajor(smem_u32(s.a) + k * 32),
+                                    desc_sw64_kmajor(smem_u32(s.b) + k * 32), idesc, k ? 1u : 0u);
+                        else
+                            mma_f16(tmem + buf * TC, desc_sw128_kmajor(smem_u32(s.a) + k * 32),
+                                    desc_sw128_kmajor(smem_u32(s.b) + k * 32), idesc, k ? 1u : 0u);
+                    }
                 if (LDG == 3) mma_commit(&s.dummy[t & 7]);   // a second commit per tile (tcscan frees the TMA stage)
                 mma_commit(&s.tfull[buf]);
             }
@@ -171,12 +176,9 @@ void run(long long *d, const char *name, int extra = 0, int grid = 1) {
 int main() {
     long long *d;
     cudaMalloc(&d, 64);
-    run<2, 256, 2, false, 0>(d, "tcscan shape", 0, 1);
-    run<2, 256, 2, false, 0>(d, "+ threshold work", 1, 1);
-    run<2, 256, 2, false, 0>(d, "+ idle warps (20 warps)", 2, 1);
-    run<2, 256, 2, false, 0>(d, "+ both", 3, 1);
-    run<2, 256, 2, false, 0>(d, "148 CTAs", 0, 148);
-    run<2, 256, 2, false, 0>(d, "148 CTAs + both", 3, 148);
-    run<2, 256, 2, false, 3>(d, "148 CTAs + 2nd commit + both", 3, 148);
+    run<2, 256, 2, false, 0>(d, "SW128 operands", 0, 1);
+    run<2, 256, 2, false, 0>(d, "SW64 operands", 4, 1);
+    run<2, 256, 2, false, 3>(d, "148 CTAs + both, SW128", 3, 148);
+    run<2, 256, 2, false, 3>(d, "148 CTAs + both, SW64", 7, 148);
     return 0;
 }
