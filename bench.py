@@ -395,11 +395,11 @@ def run_omniloc(a):
            "setup_s": {"generate": gen_s, "upload": upload_s}}
 
     # ------------------------------------------------ NEXT-1 heading line: shift re-scoring of the step's candidates
-    if a.heading and world == 1:
+    if a.heading and world == 1 and a.config == "C4":
         out["heading"] = heading_line(eng, spec, qpts, stream, sm_max)
 
     # ------------------------------------------------ small-batch (HBM regime) line
-    if a.small_batch and world == 1:
+    if a.small_batch and world == 1 and B >= a.small_batch:
         b2 = a.small_batch
         Qs = Qd[:b2].view(b2, 1, 64)
         for _ in range(3):
@@ -428,7 +428,7 @@ def run_omniloc(a):
                               "hbm_frac": gbs / hbm_peak, "hbm_frac_vs_8tbs": gbs / 8000.0}
 
     # ------------------------------------------------ mid batch: the tensor-core scan HBM-bound
-    if a.small_batch and world == 1 and used_tc:
+    if a.small_batch and world == 1 and used_tc and B >= 64:
         b3 = 64
         Qm = Qd[:b3].contiguous().view(b3, 1, 64)
         for _ in range(3):
@@ -508,7 +508,7 @@ def run_omniloc(a):
                                 "estimates (1,072 B each) D2H into pinned host"}
 
     # ------------------------------------------------ C5 streaming sub-line (BASELINE configs[4])
-    if a.c5_seconds > 0 and world == 1:
+    if a.c5_seconds > 0 and world == 1 and a.config == "C4":
         del eng
         torch.cuda.empty_cache()
         c5 = synthgen.CONFIGS["C5"]

@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(kAggThreads) micro_kernel(MicroArgs a) {
     __shared__ __align__(16) float qs[kK];
     __shared__ u64 wmin[kAggThreads / 32];
     __shared__ u64 last_key;
+    __shared__ u64 sel[OL_MAX_N];
     __shared__ uint32_t is_last;
     const uint32_t job = blockIdx.x, q = job / a.n_sub, i = job % a.n_sub;
     const SubInfo si = a.subs[i];
@@ -221,17 +222,37 @@ __global__ void __launch_bounds__(kAggThreads) micro_kernel(MicroArgs a) {
     __syncthreads();
     u64 *keys = reinterpret_cast<u64 *>(smem);   // [si.count]
     const uint32_t n = (uint32_t)si.count;
-    for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
-        const uint64_t row = si.row_begin + r;
-        float acc = 0.f;
-#pragma unroll 4
-        for (int k = 0; k < kK; ++k) {
-            const float f = k < (int)a.kc ? a.coarse[coarse_off(row, (uint32_t)k, a.kc)]
-                                          : a.fine[row * (kK - a.kc) + (k - a.kc)];
-            const float d = __fsub_rn(qs[k], f);
-            acc = __fmaf_rn(d, d, acc);
+    // two rows per thread per pass: the 2 x 16 float4 loads of both rows in flight together
+    // (a small query is latency-bound: one L2 round trip per pass); the coarse plane's 16-byte
+    // columns for k < kc, the fine plane's row after
+    const float4 *q4 = reinterpret_cast<const float4 *>(qs);
+    for (uint32_t r0 = threadIdx.x; r0 < n; r0 += 2 * blockDim.x) {
+        float4 f[2][kK / 4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t r = r0 + h * blockDim.x;
+            const uint64_t row = si.row_begin + (r < n ? r : 0);
+#pragma unroll
+            for (int k4 = 0; k4 < kK / 4; ++k4) {
+                const float *src = 4 * k4 < (int)a.kc ? a.coarse + coarse_off(row, 4 * k4, a.kc)
+                                                      : a.fine + row * (kK - a.kc) + (4 * k4 - a.kc);
+                f[h][k4] = __ldg(reinterpret_cast<const float4 *>(src));
+            }
         }
-        keys[r] = ((u64)__float_as_uint(acc) << 32) | (u64)(si.shard_begin + r);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t r = r0 + h * blockDim.x;
+            float acc = 0.f;
+#pragma unroll
+            for (int k4 = 0; k4 < kK / 4; ++k4) {
+                const float4 x = q4[k4];
+                float d = __fsub_rn(x.x, f[h][k4].x); acc = __fmaf_rn(d, d, acc);
+                d = __fsub_rn(x.y, f[h][k4].y); acc = __fmaf_rn(d, d, acc);
+                d = __fsub_rn(x.z, f[h][k4].z); acc = __fmaf_rn(d, d, acc);
+                d = __fsub_rn(x.w, f[h][k4].w); acc = __fmaf_rn(d, d, acc);
+            }
+            if (r < n) keys[r] = ((u64)__float_as_uint(acc) << 32) | (u64)(si.shard_begin + r);
+        }
     }
     if (threadIdx.x == 0) last_key = 0;
     __syncthreads();
@@ -257,20 +278,22 @@ __global__ void __launch_bounds__(kAggThreads) micro_kernel(MicroArgs a) {
                 const u64 w = __shfl_xor_sync(0xffffffffu, v, o);
                 v = w < v ? w : v;
             }
-            if (lane == 0) {
-                last_key = v;
-                const uint32_t frame = (uint32_t)v;
-                const uint64_t row = si.row_begin + (frame - si.shard_begin);
-                const float acc = __uint_as_float((uint32_t)(v >> 32));
-                ol_candidate o;
-                o.subspace = i; o.frame = frame; o.bundle = q / a.M; o.query_frame = q % a.M;
-                o.dist2 = acc; o.dist = __fsqrt_rn(acc);
-                const bool ok = OL_DCHECK(frame >= si.shard_begin && frame - si.shard_begin < si.count);
-                o.x = ok ? a.coords[2 * row] : 0; o.y = ok ? a.coords[2 * row + 1] : 0;
-                co[r] = o;
-            }
+            if (lane == 0) { last_key = v; sel[r] = v; }
         }
         __syncthreads();
+    }
+    // the candidate rows, all c in parallel (one coords round trip, not c)
+    for (uint32_t r = threadIdx.x; r < c; r += blockDim.x) {
+        const u64 v = sel[r];
+        const uint32_t frame = (uint32_t)v;
+        const uint64_t row = si.row_begin + (frame - si.shard_begin);
+        const float acc = __uint_as_float((uint32_t)(v >> 32));
+        ol_candidate o;
+        o.subspace = i; o.frame = frame; o.bundle = q / a.M; o.query_frame = q % a.M;
+        o.dist2 = acc; o.dist = __fsqrt_rn(acc);
+        const bool ok = OL_DCHECK(frame >= si.shard_begin && frame - si.shard_begin < si.count);
+        o.x = ok ? a.coords[2 * row] : 0; o.y = ok ? a.coords[2 * row + 1] : 0;
+        co[r] = o;
     }
     if (!a.aggregate) return;
     // Algorithm 2 once the bundle's last job has written its rows
