@@ -61,7 +61,8 @@ constexpr int kEv = 8;                  // survivor event ring entries per exact
                                         // 32 / 16 / 8 / 4: 100M rows 10.05 / 9.93 / 9.95 / 9.96 ms,
                                         // 20M 2.82 / 2.70 / 2.66 / 2.67, 1M 0.68 / - / 0.58 / 0.57)
 constexpr int kTrackMax = 16;
-constexpr int kBndRing = 16;            // >= kMaxStages + kTBufs: see TcSmem::bnd           // largest N of the bound pre-pass (register list)
+constexpr int kBndRing = 16;
+constexpr uint32_t kL2Ahead = 24;       // row tiles prefetched into L2 ahead of the TMA stage loads            // >= kMaxStages + kTBufs: see TcSmem::bnd           // largest N of the bound pre-pass (register list)
 constexpr float kTauInflate = 1.0f + 1.0f / 131072.0f;   // 1 + 2^-17
 constexpr uint32_t kStageBytesMax = kTileRows * kK * 2;   // 32 KB (pw = 64; 16 KB at pw = 32)
 
@@ -75,6 +76,7 @@ struct TcSmem {
     // producer runs at most n_stages tiles ahead of the MMA and the MMA at most kTBufs ahead
     // of the epilogue, so a slot is never rewritten while it is read.
     alignas(16) float2 bnd[kBndRing][kTileRows / 32];
+    long long tma_t0[kMaxStages];   // profiling (prof): when the stage's TMA was issued
     uint64_t bfull[kBndRing];
     uint32_t tmem_base;
     float alpha[kQB];
@@ -282,18 +284,28 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                     continue;
                 }
                 if ((a.dbg & 128) && t >= n_stages) { mbar_arrive(&s.full[st]); continue; }   // profiling: stale rows
+                // rows further ahead into L2 (a tile whose rows miss in L2 stalls the MMA: the
+                // 8 query blocks of an item drift apart, and the leading one reads from DRAM)
+                if (!(a.dbg & 4096) && t + kL2Ahead < n_tiles)
+                    tma_prefetch_l2_2d(&map_rows, 0, r0 + (int)(kL2Ahead * kTileRows));
+                if (kProf) s.tma_t0[st] = clock64();
                 mbar_expect_tx(&s.full[st], stage_bytes);
                 tma_load_2d(sb, &map_rows, &s.full[st], 0, r0);
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0 && rank == 0) {
+        // The whole warp runs the loop and the waits (so stage / buffer / descriptor values are
+        // warp-uniform and live in uniform registers); one elected lane issues the MMAs and
+        // commits.  Round 2: with lane 0 alone in a divergent branch every operand went through
+        // R2UR first -- 291 cycles to issue the tile's two MMAs and 149 for its two commits.
+        if (rank == 0) {
             // M = 128 frames (pair: 256, both CTAs' frames), N = 256 rows
             const uint32_t idesc = idesc_f16_f32(kPair ? 256 : 128, kTileRows);
-            long long pw_full = 0, pw_tempty = 0, pw_issue = 0;   // (profiling: prof[0], [1], [16])
+            long long pw_full = 0, pw_tempty = 0, pw_issue = 0, pw_lat = 0, pw_commit = 0;   // (profiling: prof[0], [1], [16..18])
             mbar_wait(&s.qbar, 0);
             const uint32_t qm = smem_u32(s.qm);
+            const bool leader = elect_one();
             for (uint32_t t = 0; t < n_tiles; ++t) {
                 const uint32_t st = t % n_stages, buf = t % kTBufs;
                 long long c0 = clock64();
@@ -301,7 +313,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 long long c1 = clock64();
                 if (t >= kTBufs) mbar_wait_sleep(&s.tempty[buf], ((t / kTBufs) - 1) & 1);
                 long long c2 = prof ? clock64() : 0;
-                if (prof) { pw_full += c1 - c0; pw_tempty += c2 - c1; }
+                if (prof) { pw_full += c1 - c0; pw_tempty += c2 - c1; pw_lat += c1 - *(volatile long long *)&s.tma_t0[st]; }
                 tc_fence_after();
                 const uint32_t rm = smem_u32(stage0 + (size_t)st * stage_bytes);
                 const uint32_t d = tmem + buf * kTileRows;
@@ -312,16 +324,25 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                         // (K-step k: +32 B along the rows, inside the swizzle atom)
                         const uint64_t da = a.pw == 64 ? desc_sw128_kmajor(qm + k * 32) : desc_sw64_kmajor(qm + k * 32);
                         const uint64_t db = a.pw == 64 ? desc_sw128_kmajor(rm + k * 32) : desc_sw64_kmajor(rm + k * 32);
-                        if (kPair) mma_f16_pair(d, da, db, idesc, k > 0 ? 1u : 0u);
-                        else mma_f16(d, da, db, idesc, k > 0 ? 1u : 0u);
+                        if (leader) {
+                            if (kPair) mma_f16_pair(d, da, db, idesc, k > 0 ? 1u : 0u);
+                            else mma_f16(d, da, db, idesc, k > 0 ? 1u : 0u);
+                        }
                     }
                 }
-                if (kPair) { mma_commit_pair(&s.empty[st], 3); mma_commit_pair(&s.tfull[buf], 3); }
-                else { mma_commit(&s.empty[st]); mma_commit(&s.tfull[buf]); }
-                if (prof) pw_issue += clock64() - c2;
+                long long c3 = prof ? clock64() : 0;
+                if (leader) {
+                    if (kPair) { mma_commit_pair(&s.empty[st], 3); mma_commit_pair(&s.tfull[buf], 3); }
+                    else { mma_commit(&s.empty[st]); mma_commit(&s.tfull[buf]); }
+                }
+                __syncwarp();
+                if (prof) { pw_issue += c3 - c2; pw_commit += clock64() - c3; }
             }
-            if (prof) { atomicAdd(&a.prof[0], (unsigned long long)pw_full); atomicAdd(&a.prof[1], (unsigned long long)pw_tempty);
-                        atomicAdd(&a.prof[16], (unsigned long long)pw_issue); }
+            if (prof && leader) {
+                atomicAdd(&a.prof[0], (unsigned long long)pw_full); atomicAdd(&a.prof[1], (unsigned long long)pw_tempty);
+                atomicAdd(&a.prof[16], (unsigned long long)pw_issue); atomicAdd(&a.prof[17], (unsigned long long)pw_lat);
+                atomicAdd(&a.prof[18], (unsigned long long)pw_commit);
+            }
         }
     } else if (warp < 2 + kEpiWarps) {
         // ------------------------------------------------------------ epilogue

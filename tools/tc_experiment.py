@@ -47,8 +47,8 @@ for dbg in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else '0
             div = tiles_tot * (16 if nm.startswith("epi") else 1)
             print(f"   {nm:18s} {v/div:8.0f} cycles/tile")
     if dbg & 32:
-        P = [e.stat(f"prof{i}") for i in range(18)]
-        print(f"   mma thread per tile: issue+commit {P[16] / P[9]:.0f} cycles")
+        P = [e.stat(f"prof{i}") for i in range(19)]
+        print(f"   mma thread per tile: MMA issue {P[16] / P[9]:.0f}, commits {P[18] / P[9]:.0f} cycles; TMA issue -> stage seen full {P[17] / P[9]:.0f} cycles")
         nt = P[9] * 1.0
         ncta = e.stat('items') * 8 if not dbg & 128 else 296
         print(f"   per tile: mma wait full {P[0]/nt:.0f} tempty {P[1]/nt:.0f}; epi cold {P[2]/nt/16:.0f}/warp (events {e.stat('flagged')}, max {P[3]}, cycles/ev {P[2]/max(e.stat('flagged'),1):.0f}, cnt/ev {P[4]/max(e.stat('flagged'),1):.1f} max {P[5]}); epi wait tfull {P[6]/nt/16:.0f} ld {P[12]/nt/16:.0f} math {P[13]/nt/16:.0f} loop {P[14]/nt/16:.0f} tile {P[11]/nt/16:.0f} pre {P[15]/16/ncta:.0f}/CTA n_tiles {P[9]}; exact busy {P[7]/nt/2:.0f}/warp; CTA cycles/tile(256 rows) {P[8]/nt:.0f}; ring-full wait {P[10]}; track inserts/tile {P[16]/nt:.2f} publishes/tile {P[17]/nt:.2f}")
