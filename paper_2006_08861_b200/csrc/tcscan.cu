@@ -284,10 +284,6 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                     continue;
                 }
                 if ((a.dbg & 128) && t >= n_stages) { mbar_arrive(&s.full[st]); continue; }   // profiling: stale rows
-                // rows further ahead into L2 (a tile whose rows miss in L2 stalls the MMA: the
-                // 8 query blocks of an item drift apart, and the leading one reads from DRAM)
-                if (!(a.dbg & 4096) && t + kL2Ahead < n_tiles)
-                    tma_prefetch_l2_2d(&map_rows, 0, r0 + (int)(kL2Ahead * kTileRows));
                 if (kProf) s.tma_t0[st] = clock64();
                 mbar_expect_tx(&s.full[st], stage_bytes);
                 tma_load_2d(sb, &map_rows, &s.full[st], 0, r0);
