@@ -105,3 +105,23 @@ def test_nccl_unique_id_without_gpu():
     assert ol.lib().ol_nccl_unique_id(a) == 0 and ol.lib().ol_nccl_unique_id(b) == 0
     assert a.raw != b.raw and any(a.raw)
     assert ol.lib().ol_nccl_unique_id(None) == ol.OL_ERR_INVALID_ARGUMENT
+
+
+def _build_c_caller(tmp_path):
+    import subprocess
+    import oracle
+    oracle.build()
+    libdir = os.path.dirname(ol.LIB_PATH)
+    odir = os.path.join(ROOT, "oracle")
+    exe = tmp_path / "c_caller"
+    # link the product library under its own name (libomniloc.so) and the oracle's
+    subprocess.check_call(["gcc", "-O2", "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "c", "c_caller.c"),
+                           os.path.join(libdir, "libomniloc.so"), os.path.join(odir, "liboracle.so"), "-lm",
+                           f"-Wl,-rpath,{libdir}:{odir}", "-o", str(exe)])
+    return exe
+
+
+def test_c_caller_builds_and_links(tmp_path):
+    """The ABI compiles and links from plain C (gcc, no Python, no torch): every symbol the
+    C test program calls resolves.  (It runs on the GPU: test_gpu_nccl.py.)"""
+    assert _build_c_caller(tmp_path).exists()

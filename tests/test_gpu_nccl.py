@@ -62,3 +62,15 @@ def test_nccl_world1_shift_keys_all_reduce():
     for i in range(len(cands)):
         rd2, rs = oracle.shift_distance(r["profile"][cands["bundle"][i]].astype(np.float32), P[cands["frame"][i]])
         assert (int(sh[i]), d2[i].view(np.uint32)) == (rs, np.float32(rd2).view(np.uint32))
+
+
+def test_plain_c_caller_world1_nccl(tmp_path):
+    """A plain C program (tests/c/c_caller.c: no Python, no torch, the system NCCL loaded by the
+    library itself) creates a world-1 context with a NCCL id, queries bundles with Alg. 2 and
+    gets candidates and estimates equal to the oracle's."""
+    import subprocess
+    from test_abi import _build_c_caller
+    exe = _build_c_caller(tmp_path)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "equal to the oracle" in out.stdout
