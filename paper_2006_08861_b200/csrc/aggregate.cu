@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(kAggThreads) micro_kernel(MicroArgs a) {
     __shared__ u64 sel[OL_MAX_N];
     __shared__ uint32_t is_last;
     const uint32_t job = blockIdx.x, q = job / a.n_sub, i = job % a.n_sub;
+    const long long p0 = clock64();
     const SubInfo si = a.subs[i];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < kK) {
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(kAggThreads) micro_kernel(MicroArgs a) {
     }
     if (threadIdx.x == 0) last_key = 0;
     __syncthreads();
+    const long long p1 = clock64();
     const uint32_t c = min(a.N, n);   // min(N, |n_i|) rows
     ol_candidate *co = a.cand + (uint64_t)q * a.sub_prefix[a.n_sub] + a.sub_prefix[i];
     for (uint32_t r = 0; r < c; ++r) {
@@ -295,6 +297,9 @@ __global__ void __launch_bounds__(kAggThreads) micro_kernel(MicroArgs a) {
         o.x = ok ? a.coords[2 * row] : 0; o.y = ok ? a.coords[2 * row + 1] : 0;
         co[r] = o;
     }
+    const long long p2 = clock64();
+    if (a.prof && threadIdx.x == 0) { atomicAdd(&a.prof[0], (unsigned long long)(p1 - p0));
+                                      atomicAdd(&a.prof[1], (unsigned long long)(p2 - p1)); }
     if (!a.aggregate) return;
     // Algorithm 2 once the bundle's last job has written its rows
     __threadfence();
@@ -308,7 +313,10 @@ __global__ void __launch_bounds__(kAggThreads) micro_kernel(MicroArgs a) {
     __syncthreads();
     if (!is_last) return;
     __threadfence();
+    const long long p3 = clock64();
     aggregate_block(a.agg, b, smem);
+    if (a.prof && threadIdx.x == 0) { atomicAdd(&a.prof[2], (unsigned long long)(p3 - p2));
+                                      atomicAdd(&a.prof[3], (unsigned long long)(clock64() - p3)); }
 }
 
 size_t micro_smem_bytes(uint64_t max_rows, uint32_t agg_cap) {

@@ -169,6 +169,7 @@ struct MicroArgs {
     uint32_t nq, n_sub, N, M, kc;
     int check_finite, aggregate;
     AggArgs agg;                            // cand / per_bundle / out / params of Algorithm 2
+    unsigned long long *prof;               // profiling only (tc_debug & 32): phase cycles, or null
 };
 constexpr uint64_t kMicroMaxRows = 8192;    // per subspace (64 KB of keys in shared memory)
 constexpr uint64_t kMicroMaxPairs = 1u << 16;   // frames x rows of the whole query

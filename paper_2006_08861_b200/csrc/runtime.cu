@@ -948,7 +948,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
     uint64_t max_rows = 0;
     for (auto &sb : c->subs) max_rows = sb.count > max_rows ? sb.count : max_rows;
     // (not when an option forces a scan path or schedule: tests of those paths keep them)
-    if (c->opt_micro && c->opt_tc == -1 && !c->opt_chunk && !c->opt_qtile && !(c->opt_tc_debug & 512) &&
+    if (c->opt_micro && c->opt_tc == -1 && !c->opt_chunk && !c->opt_qtile && !(c->opt_tc_debug & ~32) &&
         c->world == 1 && !c->comm && max_rows <= kMicroMaxRows && max_rows > 0 &&
         (uint64_t)nq * c->rows <= kMicroMaxPairs) {
         st = ensure_prefix(c, N);
@@ -978,6 +978,8 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         ag.toler_per = p->toler_per;
         const double r = p->radius_m / p->tile_m;
         ag.r2 = r * r; ag.tile_m = p->tile_m; ag.cap = cap;
+        ma.prof = (c->opt_tc_debug & 32) ? c->prof_d : nullptr;
+        if (ma.prof) OL_CUDA(c, cudaMemsetAsync(c->prof_d, 0, 64 * sizeof(unsigned long long), c->stream));
         {
             TimeScope ts(c, ol_ctx::T_SCAN);
             OL_LAUNCH(c, launch_micro(ma, micro_smem_bytes(max_rows, cap), c->stream));

@@ -20,3 +20,10 @@ for micro in (1, 0):
         for _ in range(500): e.query(qd, N=cfg.N, aggregate=agg)
         s1.record(); torch.cuda.synchronize()
         print(f"micro={micro} aggregate={agg}: {s0.elapsed_time(s1) / 500 * 1e3:.1f} us/query, {e.stat('kernels')} launches")
+
+e.set_option("micro", 1)
+e.set_option("tc_debug", 32)
+e.query(qd, N=cfg.N, aggregate=True)
+torch.cuda.synchronize()
+print("micro phases (cycles): scan", e.stat("prof0"), "top-N + rows", e.stat("prof1"), "bundle count", e.stat("prof2"),
+      "Alg. 2", e.stat("prof3"))
