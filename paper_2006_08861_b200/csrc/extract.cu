@@ -113,6 +113,18 @@ fft_extract_kernel(const double *prof, uint64_t n, float *out32, double *out64, 
         for (int j = 0; j < R; ++j) x[j] = __ldcs(&prof[p * W + lane + 32 * j]);   // (streamed once)
         // step 1: R-point DFT over j of x[l + 32 j] (real input: A[R - k1] = conj A[k1])
         double re[R], im[R];
+        if constexpr (R == 8) {   // the 8-point real DFT by hand (~20 operations instead of 80)
+            constexpr double c = 0.70710678118654752440;   // cos(pi/4) = sin(pi/4), RN
+            const double a0 = x[0] + x[4], a1 = x[1] + x[5], a2 = x[2] + x[6], a3 = x[3] + x[7];
+            const double b0 = x[0] - x[4], b1 = x[1] - x[5], b2 = x[2] - x[6], b3 = x[3] - x[7];
+            const double s02 = a0 + a2, s13 = a1 + a3;
+            re[0] = s02 + s13; im[0] = 0.0;
+            re[4] = s02 - s13; im[4] = 0.0;
+            re[2] = a0 - a2;   im[2] = a3 - a1;
+            const double cp = c * (b1 - b3), cm = c * (b1 + b3);
+            re[1] = b0 + cp;   im[1] = -(b2 + cm);
+            re[3] = b0 - cp;   im[3] = b2 - cm;
+        } else {
 #pragma unroll
         for (int k1 = 0; k1 <= R / 2; ++k1) {
             double a = 0.0, b = 0.0;
@@ -124,6 +136,7 @@ fft_extract_kernel(const double *prof, uint64_t n, float *out32, double *out64, 
             }
             re[k1] = a;
             im[k1] = b;
+        }
         }
 #pragma unroll
         for (int k1 = R / 2 + 1; k1 < R; ++k1) { re[k1] = re[R - k1]; im[k1] = -im[R - k1]; }
@@ -138,22 +151,20 @@ fft_extract_kernel(const double *prof, uint64_t n, float *out32, double *out64, 
         }
         // step 3: 32-point radix-2 DIF FFT across the lanes, every k1
 #pragma unroll
+        // (branch-free: the upper lane of a pair computes mine + partner, times 1; the lower
+        // one partner - mine, times the twiddle -- no divergence between the two halves)
         for (int h = 16; h >= 1; h >>= 1) {
             const bool lower = (lane & h) != 0;
             const uint32_t e = (lane & (h - 1)) * (W / (2 * h));   // W_{2h}^{lane mod h}
-            const double c = tc[e], sn = ts[e];
+            const double c = lower ? tc[e] : 1.0, sn = lower ? ts[e] : 0.0;
+            const double sg = lower ? -1.0 : 1.0;
 #pragma unroll
             for (int k1 = 0; k1 < R; ++k1) {
                 const double pr = __shfl_xor_sync(0xffffffffu, re[k1], h);
                 const double pi = __shfl_xor_sync(0xffffffffu, im[k1], h);
-                if (!lower) {
-                    re[k1] += pr;
-                    im[k1] += pi;
-                } else {
-                    const double dr = pr - re[k1], di = pi - im[k1];
-                    re[k1] = fma(dr, c, di * sn);
-                    im[k1] = fma(di, c, -dr * sn);
-                }
+                const double dr = fma(sg, re[k1], pr), di = fma(sg, im[k1], pi);   // (lower: pr - re)
+                re[k1] = lower ? fma(dr, c, di * sn) : dr;
+                im[k1] = lower ? fma(di, c, -dr * sn) : di;
             }
         }
         // step 4: magnitudes of bins 1..K held by this lane (k = k1 + R k2), norm, outputs
