@@ -426,9 +426,13 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *                   rank's published threshold bounds the global N-th best, so results are
  *                   identical and small shards prune as well as the whole database
  *   "micro"         1 (default) / 0: world-1 queries with <= 8,192 rows per subspace and <= 65,536
- *                   (frame, row) pairs run as ONE kernel (NK10: exact scan, top-N, candidate
- *                   rows, Algorithm 2 by each bundle's last job) instead of the launch
+ *                   (frame, row) pairs run as ONE kernel (NK10: a cluster of 1-8 CTAs per
+ *                   (frame, subspace) scores its shares of the rows exactly, rank 0 merges
+ *                   the shares' top-N over distributed shared memory and writes the candidate
+ *                   rows, each bundle's last job runs Algorithm 2) instead of the launch
  *                   sequence; not used when "tc", "chunk" or "qtile" force a path or schedule
+ *   "agg_block"     0 (default) / 1: tests: Algorithm 2 by the CTA-wide kernel for bundles of
+ *                   <= 32 candidates too (default: one warp, shuffles only); same results
  *   "poison"        0 (default) / 1: tests (an initcheck stand-in): the next uploads fill padding
  *                   rows and coords with NaN bytes instead of zeros, and every query first
  *                   fills its scratch and output buffers with garbage; results must not change

@@ -13,8 +13,12 @@
 //      rank on ties) flagged low-confidence (R12).
 #define OL_TU 3
 #include "ol_internal.h"
+#include "tc_ptx.cuh"   // (cluster barrier, shared-memory addresses)
 
 namespace ol {
+
+using tc::cluster_sync;
+using tc::smem_u32;
 
 constexpr int kAggThreads = 512;
 
@@ -68,8 +72,109 @@ __device__ __forceinline__ u64 tile_key(int32_t x, int32_t y) {
 __device__ __forceinline__ int32_t key_x(u64 k) { return (int32_t)((uint32_t)k ^ 0x80000000u); }
 __device__ __forceinline__ int32_t key_y(u64 k) { return (int32_t)((uint32_t)(k >> 32) ^ 0x80000000u); }
 
+// one key per lane -> the warp's 32 keys ascending across the lanes (bitonic network)
+__device__ __forceinline__ u64 warp_sort32(u64 k, int lane) {
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            const u64 o = __shfl_xor_sync(0xffffffffu, k, j);
+            const bool keep_min = ((lane & j) == 0) == ((lane & kk) == 0);
+            k = keep_min ? (o < k ? o : k) : (o > k ? o : k);
+        }
+    }
+    return k;
+}
+// two ascending 32-key warp lists -> the 32 smallest of both, ascending: min(a_i, b_{31-i})
+// is the lower half of the bitonic merge of a with b reversed, then 5 half-cleaner steps
+__device__ __forceinline__ u64 warp_merge32(u64 a, u64 b, int lane) {
+    const u64 br = __shfl_sync(0xffffffffu, b, 31 - lane);
+    u64 v = a < br ? a : br;
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const u64 o = __shfl_xor_sync(0xffffffffu, v, j);
+        v = (lane & j) == 0 ? (o < v ? o : v) : (o > v ? o : v);
+    }
+    return v;
+}
+
+// Algorithm 2 for a bundle of 1..32 candidates by one warp, lane = candidate: the steps and
+// tie rules of aggregate_block below, with shuffles in place of its shared-memory sorts and
+// block barriers (a bundle of C4 / C1 size costs a few hundred cycles instead of ~12k).
+__device__ __noinline__ void aggregate_warp(const AggArgs &a, uint32_t b, uint32_t begin, uint32_t total) {
+    constexpr uint32_t kAll = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    ol_estimate *out = a.out + b;
+    u64 k = kPadKey;
+    if ((uint32_t)lane < total) {
+        int32_t x, y;
+        if (a.cand) { x = a.cand[begin + lane].x; y = a.cand[begin + lane].y; }
+        else { x = a.xy[2 * (size_t)(begin + lane)]; y = a.xy[2 * (size_t)(begin + lane) + 1]; }
+        k = tile_key(x, y);
+    }
+    // step 1: the 32 keys sorted ascending across the lanes; runs of equal keys are the occupied
+    // tiles, a run's length its count
+    k = warp_sort32(k, lane);
+    const u64 prev = __shfl_up_sync(kAll, k, 1);
+    const bool start = (uint32_t)lane < total && (lane == 0 || k != prev);
+    const uint32_t starts = __ballot_sync(kAll, start);
+    const uint32_t nd = __popc(starts);
+    uint32_t cnt = 0;
+    if (start) {
+        const uint32_t later = lane == 31 ? 0u : starts & ~((2u << lane) - 1u);
+        cnt = (later ? (uint32_t)(__ffs(later) - 1) : total) - (uint32_t)lane;
+    }
+    // step 2: rank = #tiles before it in (count desc, (y, x) asc) order; lanes of run starts are
+    // in (y, x) order already
+    uint32_t rank = 0;
+    for (int j = 0; j < 32; ++j) {
+        const uint32_t cj = __shfl_sync(kAll, cnt, j);
+        if (((starts >> j) & 1u) && (cj > cnt || (cj == cnt && j < lane))) ++rank;
+    }
+    const uint32_t nr = min(a.top_c, nd);
+    const bool ranked = start && rank < nr;
+    // step 3: the tolerance circle of every ranked tile
+    const int64_t cx = key_x(k), cy = key_y(k);
+    uint32_t circ = 0;
+    for (int j = 0; j < 32; ++j) {
+        const u64 kj = __shfl_sync(kAll, k, j);
+        const uint32_t cj = __shfl_sync(kAll, cnt, j);
+        if ((starts >> j) & 1u) {
+            const int64_t dx = (int64_t)key_x(kj) - cx;
+            const int64_t dy = (int64_t)key_y(kj) - cy;
+            if ((double)(dx * dx + dy * dy) <= a.r2) circ += cj;
+        }
+    }
+    // step 4: the first ranked tile whose circle > toler_per * total, else the largest circle
+    // (earliest rank on ties), low confidence
+    const double thresh = a.toler_per * (double)total;
+    const uint32_t chosen = __reduce_min_sync(kAll, ranked && (double)circ > thresh ? rank : 0xFFFFFFFFu);
+    const uint32_t best = 63u - (__reduce_max_sync(kAll, ranked ? (circ << 6) | (63u - rank) : 0u) & 63u);
+    const uint32_t low = chosen == 0xFFFFFFFFu ? 1u : 0u;
+    const uint32_t win = low ? best : chosen;
+    if (ranked && rank == win) {
+        out->x = key_x(k);
+        out->y = key_y(k);
+        out->x_m = a.tile_m * (double)out->x;
+        out->y_m = a.tile_m * (double)out->y;
+        out->confidence = (double)circ / (double)total;
+        out->low_confidence = low;
+        out->n_ranked = nr;
+        out->total = total;
+        out->_pad = 0;
+    }
+    if (ranked) {
+        ol_ranked_tile rt;
+        rt.x = key_x(k); rt.y = key_y(k); rt.count = cnt; rt.circle = circ;
+        out->ranked[rank] = rt;
+    }
+    for (uint32_t r = lane; r < OL_MAX_TOP_C; r += 32)
+        if (r >= nr) out->ranked[r] = ol_ranked_tile{0, 0, 0, 0};
+}
+
 // Algorithm 2 for bundle b, by the whole CTA (kAggThreads threads); smem: the dynamic shared
-// memory (2 x cap u64 + cap u32).  Shared by aggregate_kernel and micro_kernel.
+// memory (2 x cap u64 + cap u32).  Shared by aggregate_kernel and micro_kernel.  Bundles of
+// at most 32 candidates go to aggregate_warp (warp 0; the other warps return).
 __device__ __noinline__ void aggregate_block(const AggArgs &a, uint32_t b, unsigned char *smem) {
     __shared__ uint32_t scratch[32];
     __shared__ uint32_t circ[OL_MAX_TOP_C];
@@ -81,6 +186,10 @@ __device__ __noinline__ void aggregate_block(const AggArgs &a, uint32_t b, unsig
     const uint32_t cap = a.cap ? a.cap : (uint32_t)kAggMax;   // shared-memory entries
     if (total == 0 || total > cap) {
         if (threadIdx.x == 0) { *a.err_empty = total == 0 ? 1 : 2; out->total = total; }
+        return;
+    }
+    if (total <= 32 && !a.block_only) {
+        if (threadIdx.x < 32) aggregate_warp(a, b, begin, total);
         return;
     }
     uint32_t P = 1;
@@ -196,95 +305,143 @@ __global__ void __launch_bounds__(kAggThreads) aggregate_kernel(AggArgs a) {
 
 // ---------------------------------------------------------------- small problems (NK10)
 // The whole launch sequence of a small world-1 query in ONE kernel (the latency configs:
-// C1 = 2,000 rows x 1 frame ran 6 launches, ~5 us each): one CTA per (frame, subspace) job
-// checks its frame, scores every row of the subspace with the exact chain of R3 (k = 0..63 in
-// order; the coarse plane for k < kc, the fine plane after -- the same values as one pass),
-// keeps the keys (acc bits << 32 | frame) in shared memory, extracts the N smallest by N
-// rounds of a block-wide minimum above the previous one (keys are unique), writes the
-// candidate rows in SPEC order and, when it is the last job of its bundle to finish
-// (a counter per bundle, reset by that CTA), runs Algorithm 2 for the bundle.  Results are
-// the plain definition's, bit for bit, like every other path.
+// C1 = 2,000 rows x 1 frame ran 6 launches, ~5 us each).  Each (frame, subspace) job is one
+// cluster of a.split CTAs (1, 2, 4 or 8; a single CTA read C1's 512 KB of rows at one SM's L2
+// bandwidth, ~14 us): CTA g scores its contiguous share of the subspace's rows with the exact
+// chain of R3 (k = 0..63 in order; the coarse plane for k < kc, the fine plane after -- the
+// same values as one pass), keeps the keys (acc bits << 32 | frame) in shared memory and
+// selects its min(N, rows) smallest (warp 0, rounds of a warp minimum above the previous one;
+// keys are unique).  Cluster rank 0 reads the shares' lists over distributed shared memory
+// and selects the N smallest of them -- the N smallest of the union, as every row is in
+// exactly one share -- writes the candidate rows in SPEC order and, when its job is
+// the last of its bundle (a counter per bundle; none for one-job bundles), runs Algorithm 2
+// for the bundle.  Results are the plain definition's, bit for bit, like every other path.
+//
+// The c smallest keys above nothing of keys[0..n) (shared memory), ascending, into sel[0..c),
+// by warp 0.
+__device__ __forceinline__ void micro_select(const u64 *keys, uint32_t n, uint32_t c, u64 *sel, int lane) {
+    u64 lo = 0;
+    for (uint32_t r = 0; r < c; ++r) {
+        u64 best = kPadKey;
+        for (uint32_t t = lane; t < n; t += 32) {
+            const u64 v = keys[t];
+            if ((r == 0 || v > lo) && v < best) best = v;
+        }
+        for (int o = 16; o; o >>= 1) {
+            const u64 w = __shfl_xor_sync(0xffffffffu, best, o);
+            best = w < best ? w : best;
+        }
+        lo = best;
+        if (lane == 0) sel[r] = best;
+    }
+}
+
+// The c <= 32 smallest of keys[0..n) (shared memory), ascending, into sel[0..c), by the whole
+// CTA: every warp folds its 32-key chunks into a running sorted 32-list (sort, merge), then
+// the warps' lists are merged pairwise in 4 rounds (scratch: 32 per warp).  Unique keys, so
+// the result is the same set and order as micro_select's.
+__device__ void block_select32(const u64 *keys, uint32_t n, uint32_t c, u64 *sel, u64 *scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    u64 run = kPadKey;
+    for (uint32_t base = 32u * warp; base < n; base += 32u * nw) {
+        const u64 v = base + lane < n ? keys[base + lane] : kPadKey;
+        run = warp_merge32(run, warp_sort32(v, lane), lane);
+    }
+    for (int st = 1; st < nw; st <<= 1) {
+        scratch[warp * 32 + lane] = run;
+        __syncthreads();
+        if (warp % (2 * st) == 0 && warp + st < nw) run = warp_merge32(run, scratch[(warp + st) * 32 + lane], lane);
+        __syncthreads();
+    }
+    if (warp == 0 && (uint32_t)lane < c) sel[lane] = run;
+}
+
 __global__ void __launch_bounds__(kAggThreads) micro_kernel(MicroArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(16) float qs[kK];
-    __shared__ u64 wmin[kAggThreads / 32];
-    __shared__ u64 last_key;
     __shared__ u64 sel[OL_MAX_N];
+    __shared__ u64 scratch[kAggThreads];
     __shared__ uint32_t is_last;
-    const uint32_t job = blockIdx.x, q = job / a.n_sub, i = job % a.n_sub;
+    const uint32_t split = a.split;
+    const uint32_t job = blockIdx.x / split, g = blockIdx.x % split;
+    const uint32_t q = job / a.n_sub, i = job % a.n_sub;
     const long long p0 = clock64();
     const SubInfo si = a.subs[i];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < kK) {
         const float v = a.queries[(size_t)q * kK + threadIdx.x];
         qs[threadIdx.x] = v;
-        if (a.check_finite && !isfinite(v)) *a.flag_nonfinite = 1;
+        if (a.check_finite && g == 0 && !isfinite(v)) *a.flag_nonfinite = 1;
     }
     __syncthreads();
-    u64 *keys = reinterpret_cast<u64 *>(smem);   // [si.count]
+    u64 *keys = reinterpret_cast<u64 *>(smem);   // [share]
     const uint32_t n = (uint32_t)si.count;
-    // two rows per thread per pass: the 2 x 16 float4 loads of both rows in flight together
-    // (a small query is latency-bound: one L2 round trip per pass); the coarse plane's 16-byte
-    // columns for k < kc, the fine plane's row after
+    const uint32_t per = (n + split - 1) / split;          // this job's rows per share
+    const uint32_t r_lo = min(n, g * per), cnt = min(n, r_lo + per) - r_lo;
+    // one row per thread per pass, its 16 float4 loads in flight together (a small query is
+    // latency-bound: one L2 round trip per pass); the coarse plane's 16-byte columns for
+    // k < kc, the fine plane's row after
     const float4 *q4 = reinterpret_cast<const float4 *>(qs);
-    for (uint32_t r0 = threadIdx.x; r0 < n; r0 += 2 * blockDim.x) {
-        float4 f[2][kK / 4];
+    for (uint32_t r = threadIdx.x; r < cnt; r += blockDim.x) {
+        const uint64_t row = si.row_begin + r_lo + r;
+        float4 f[kK / 4];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t r = r0 + h * blockDim.x;
-            const uint64_t row = si.row_begin + (r < n ? r : 0);
-#pragma unroll
-            for (int k4 = 0; k4 < kK / 4; ++k4) {
-                const float *src = 4 * k4 < (int)a.kc ? a.coarse + coarse_off(row, 4 * k4, a.kc)
-                                                      : a.fine + row * (kK - a.kc) + (4 * k4 - a.kc);
-                f[h][k4] = __ldg(reinterpret_cast<const float4 *>(src));
-            }
+        for (int k4 = 0; k4 < kK / 4; ++k4) {
+            const float *src = 4 * k4 < (int)a.kc ? a.coarse + coarse_off(row, 4 * k4, a.kc)
+                                                  : a.fine + row * (kK - a.kc) + (4 * k4 - a.kc);
+            f[k4] = __ldg(reinterpret_cast<const float4 *>(src));
         }
+        float acc = 0.f;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint32_t r = r0 + h * blockDim.x;
-            float acc = 0.f;
-#pragma unroll
-            for (int k4 = 0; k4 < kK / 4; ++k4) {
-                const float4 x = q4[k4];
-                float d = __fsub_rn(x.x, f[h][k4].x); acc = __fmaf_rn(d, d, acc);
-                d = __fsub_rn(x.y, f[h][k4].y); acc = __fmaf_rn(d, d, acc);
-                d = __fsub_rn(x.z, f[h][k4].z); acc = __fmaf_rn(d, d, acc);
-                d = __fsub_rn(x.w, f[h][k4].w); acc = __fmaf_rn(d, d, acc);
-            }
-            if (r < n) keys[r] = ((u64)__float_as_uint(acc) << 32) | (u64)(si.shard_begin + r);
+        for (int k4 = 0; k4 < kK / 4; ++k4) {
+            const float4 x = q4[k4];
+            float d = __fsub_rn(x.x, f[k4].x); acc = __fmaf_rn(d, d, acc);
+            d = __fsub_rn(x.y, f[k4].y); acc = __fmaf_rn(d, d, acc);
+            d = __fsub_rn(x.z, f[k4].z); acc = __fmaf_rn(d, d, acc);
+            d = __fsub_rn(x.w, f[k4].w); acc = __fmaf_rn(d, d, acc);
         }
+        keys[r] = ((u64)__float_as_uint(acc) << 32) | (u64)(si.shard_begin + r_lo + r);
     }
-    if (threadIdx.x == 0) last_key = 0;
     __syncthreads();
     const long long p1 = clock64();
     const uint32_t c = min(a.N, n);   // min(N, |n_i|) rows
-    ol_candidate *co = a.cand + (uint64_t)q * a.sub_prefix[a.n_sub] + a.sub_prefix[i];
-    for (uint32_t r = 0; r < c; ++r) {
-        const u64 lo = last_key;
-        const bool first = r == 0;
-        u64 best = kPadKey;
-        for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
-            const u64 v = keys[t];
-            if ((first || v > lo) && v < best) best = v;
-        }
-        for (int o = 16; o; o >>= 1) {
-            const u64 w = __shfl_xor_sync(0xffffffffu, best, o);
-            best = w < best ? w : best;
-        }
-        if (lane == 0) wmin[warp] = best;
+    if (split == 1) {
+        if (c <= 32) block_select32(keys, cnt, c, sel, scratch);
+        else if (warp == 0) micro_select(keys, cnt, c, sel, lane);
+    } else {
+        // this share's min(N, cnt) smallest, padded to N; rank 0 gathers every share's list
+        const uint32_t cl = min(a.N, cnt);
+        if (cl <= 32) block_select32(keys, cnt, cl, sel, scratch);
+        else if (warp == 0) micro_select(keys, cnt, cl, sel, lane);
         __syncthreads();
-        if (warp == 0) {
-            u64 v = lane < kAggThreads / 32 ? wmin[lane] : kPadKey;
-            for (int o = 16; o; o >>= 1) {
-                const u64 w = __shfl_xor_sync(0xffffffffu, v, o);
-                v = w < v ? w : v;
+        for (uint32_t r = cl + threadIdx.x; r < a.N; r += blockDim.x) sel[r] = kPadKey;
+        const long long pa = clock64();
+        cluster_sync();   // (release / acquire: the lists are visible across the cluster)
+        const long long pb = clock64();
+        if (a.prof && threadIdx.x == 0 && g == 0) { atomicAdd(&a.prof[4], (unsigned long long)(pa - p1));
+                                                    atomicAdd(&a.prof[5], (unsigned long long)(pb - pa)); }
+        if (g == 0) {
+            const uint32_t local = smem_u32(sel);
+            for (uint32_t t = threadIdx.x; t < split * a.N; t += blockDim.x) {
+                uint32_t ra;
+                u64 v;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local + 8u * (t % a.N)), "r"(t / a.N));
+                asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(ra) : "memory");
+                keys[t] = v;
             }
-            if (lane == 0) { last_key = v; sel[r] = v; }
         }
+        cluster_sync();   // (the other shares may exit once rank 0 has read them)
+        if (g != 0) return;
+        const long long pc = clock64();
         __syncthreads();
+        if (c <= 32) block_select32(keys, split * a.N, c, sel, scratch);
+        else if (warp == 0) micro_select(keys, split * a.N, c, sel, lane);
+        if (a.prof && threadIdx.x == 0) { atomicAdd(&a.prof[6], (unsigned long long)(pc - pb)); }
     }
+    const long long pd = clock64();
+    __syncthreads();
     // the candidate rows, all c in parallel (one coords round trip, not c)
+    ol_candidate *co = a.cand + (uint64_t)q * a.sub_prefix[a.n_sub] + a.sub_prefix[i];
     for (uint32_t r = threadIdx.x; r < c; r += blockDim.x) {
         const u64 v = sel[r];
         const uint32_t frame = (uint32_t)v;
@@ -298,29 +455,44 @@ __global__ void __launch_bounds__(kAggThreads) micro_kernel(MicroArgs a) {
         co[r] = o;
     }
     const long long p2 = clock64();
-    if (a.prof && threadIdx.x == 0) { atomicAdd(&a.prof[0], (unsigned long long)(p1 - p0));
+    if (a.prof && threadIdx.x == 0) { atomicAdd(&a.prof[7], (unsigned long long)(p2 - pd));
+                                      atomicAdd(&a.prof[0], (unsigned long long)(p1 - p0));
                                       atomicAdd(&a.prof[1], (unsigned long long)(p2 - p1)); }
     if (!a.aggregate) return;
-    // Algorithm 2 once the bundle's last job has written its rows
-    __threadfence();
-    __syncthreads();
     const uint32_t b = q / a.M;
-    if (threadIdx.x == 0) {
-        const uint32_t done = atomicAdd(&a.bundle_count[b], 1u) + 1;
-        is_last = done == a.M * a.n_sub;
-        if (is_last) a.bundle_count[b] = 0;   // (ready for the next query)
+    if (a.M * a.n_sub > 1) {
+        // Algorithm 2 once the bundle's last job has written its rows
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t done = atomicAdd(&a.bundle_count[b], 1u) + 1;
+            is_last = done == a.M * a.n_sub;
+            if (is_last) a.bundle_count[b] = 0;   // (ready for the next query)
+        }
+        __syncthreads();
+        if (!is_last) return;
+        __threadfence();
+    } else {
+        __syncthreads();   // (the bundle is this job: its rows were written by this CTA)
     }
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
     const long long p3 = clock64();
     aggregate_block(a.agg, b, smem);
     if (a.prof && threadIdx.x == 0) { atomicAdd(&a.prof[2], (unsigned long long)(p3 - p2));
                                       atomicAdd(&a.prof[3], (unsigned long long)(clock64() - p3)); }
 }
 
-size_t micro_smem_bytes(uint64_t max_rows, uint32_t agg_cap) {
-    const size_t rows = sizeof(u64) * max_rows;
+// CTAs per job (the cluster size): a power of two <= 8, shares of >= ~256 rows, and no more
+// CTAs in all than two per SM
+uint32_t micro_split(uint64_t max_rows, uint64_t jobs) {
+    const uint64_t want = (max_rows + 255) / 256, by_sm = 296 / (jobs ? jobs : 1);
+    uint32_t g = 1;
+    while (g < 8 && 2 * g <= want && 2 * g <= by_sm) g *= 2;
+    return g;
+}
+
+size_t micro_smem_bytes(uint64_t max_rows, uint32_t split, uint32_t N, uint32_t agg_cap) {   // (split x N <= 1,024)
+    const uint64_t share = (max_rows + split - 1) / split, merge = split > 1 ? (uint64_t)split * N : 0;
+    const size_t rows = sizeof(u64) * (share > merge ? share : merge);
     const size_t agg = agg_cap ? sizeof(u64) * agg_cap * 2 + sizeof(uint32_t) * agg_cap : 0;
     return rows > agg ? rows : agg;
 }
@@ -328,8 +500,17 @@ size_t micro_smem_bytes(uint64_t max_rows, uint32_t agg_cap) {
 cudaError_t launch_micro(const MicroArgs &a, size_t smem, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(micro_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    micro_kernel<<<a.nq * a.n_sub, kAggThreads, smem, s>>>(a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.nq * a.n_sub * a.split);
+    cfg.blockDim = dim3(kAggThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = a.split; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, micro_kernel, a);
 }
 
 cudaError_t launch_aggregate(const AggArgs &a, cudaStream_t s) {

@@ -155,6 +155,7 @@ struct AggArgs {
     uint32_t n_bundles, top_c;
     double toler_per, r2, tile_m;
     uint32_t cap;                // power of two >= every bundle's size (<= kAggMax); 0 = kAggMax
+    uint32_t block_only = 0;     // 1: the CTA-wide version for small bundles too (tests: both agree)
 };
 
 // NK10: one kernel for a whole small world-1 query (aggregate.cu)
@@ -165,6 +166,7 @@ struct MicroArgs {
     const uint32_t *sub_prefix;             // [n_sub+1] prefix of min(N, |n_i|)
     ol_candidate *cand;
     uint32_t *bundle_count;                 // [n_bundles] zeroed; each last job resets its own
+    uint32_t split;                         // CTAs per (frame, subspace) job: the cluster size, 1..8
     int *flag_nonfinite;
     uint32_t nq, n_sub, N, M, kc;
     int check_finite, aggregate;
@@ -173,7 +175,8 @@ struct MicroArgs {
 };
 constexpr uint64_t kMicroMaxRows = 8192;    // per subspace (64 KB of keys in shared memory)
 constexpr uint64_t kMicroMaxPairs = 1u << 16;   // frames x rows of the whole query
-size_t micro_smem_bytes(uint64_t max_rows, uint32_t agg_cap);
+size_t micro_smem_bytes(uint64_t max_rows, uint32_t split, uint32_t N, uint32_t agg_cap);
+uint32_t micro_split(uint64_t max_rows, uint64_t jobs);
 cudaError_t launch_micro(const MicroArgs &a, size_t smem, cudaStream_t s);
 
 struct TcScanArgs {

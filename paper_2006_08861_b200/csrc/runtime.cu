@@ -169,6 +169,7 @@ struct ol_ctx {
     uint32_t *bcount_d = nullptr; size_t bcount_cap = 0;   // NK10 per-bundle job counters (kept zero)
     bool used_micro = false;
     int64_t opt_micro = 1;
+    int64_t opt_agg_block = 0;   // 1: Algorithm 2 by the CTA-wide kernel for bundles <= 32 too (tests)
     int32_t *agg_xy_d = nullptr; size_t agg_xy_cap = 0;
     int *flags_d = nullptr;                // [0] nonfinite frames, [1] aggregation error
     unsigned long long *stat_d = nullptr;  // [0] survivors
@@ -964,8 +965,14 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
             cap = 32;
             while (cap < per_q * M) cap <<= 1;
         }
+        const uint32_t split = micro_split(max_rows, (uint64_t)nq * c->n_sub);   // (a cluster per job)
+        if (c->opt_poison) {   // (as below: outputs and scratch must be written before they are read)
+            OL_CUDA(c, cudaMemsetAsync(c->cand_d, 0xA5, sizeof(ol_candidate) * c->cand_cap, c->stream));
+            if (aggregate) OL_CUDA(c, cudaMemsetAsync(c->est_d, 0xA5, sizeof(ol_estimate) * c->est_cap, c->stream));
+        }
         OL_CUDA(c, cudaMemsetAsync(c->flags_d, 0, 2 * sizeof(int), c->stream));
         MicroArgs ma;
+        ma.split = split;
         ma.coarse = c->coarse; ma.fine = c->fine; ma.queries = q; ma.subs = c->subs_d; ma.coords = c->coords;
         ma.sub_prefix = c->prefix_d; ma.cand = c->cand_d; ma.bundle_count = c->bcount_d;
         ma.flag_nonfinite = c->flags_d;
@@ -973,6 +980,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         ma.check_finite = on_device ? 1 : 0;   // (host frames were checked on the host)
         ma.aggregate = aggregate ? 1 : 0;
         AggArgs &ag = ma.agg;
+        ag.block_only = (uint32_t)c->opt_agg_block;
         ag.cand = c->cand_d; ag.per_bundle = (uint32_t)(per_q * M); ag.offsets = nullptr; ag.xy = nullptr;
         ag.out = c->est_d; ag.err_empty = c->flags_d + 1; ag.n_bundles = nb; ag.top_c = p->top_c;
         ag.toler_per = p->toler_per;
@@ -982,7 +990,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         if (ma.prof) OL_CUDA(c, cudaMemsetAsync(c->prof_d, 0, 64 * sizeof(unsigned long long), c->stream));
         {
             TimeScope ts(c, ol_ctx::T_SCAN);
-            OL_LAUNCH(c, launch_micro(ma, micro_smem_bytes(max_rows, cap), c->stream));
+            OL_LAUNCH(c, launch_micro(ma, micro_smem_bytes(max_rows, split, N, cap), c->stream));
         }
         c->used_tc = c->used_pair = false;
         c->used_micro = true;
@@ -1272,6 +1280,7 @@ static ol_status finalize_tail(ol_ctx *c, const uint4 *rec) {
     if (c->aggregate) {
         OL_CUDA(c, grow(&c->est_d, &c->est_cap, c->nb));
         AggArgs ag;
+        ag.block_only = (uint32_t)c->opt_agg_block;
         ag.cand = c->cand_d; ag.per_bundle = (uint32_t)c->per_bundle; ag.offsets = nullptr;
         ag.xy = nullptr; ag.out = c->est_d; ag.err_empty = c->flags_d + 1; ag.n_bundles = c->nb;
         ag.top_c = c->params.top_c; ag.toler_per = c->params.toler_per;
@@ -1527,6 +1536,7 @@ ol_status ol_aggregate(ol_ctx *c, uint32_t nb, const uint32_t *offsets, const in
                                            c->flags_d + 2, c->stream));
     }
     AggArgs ag;
+    ag.block_only = (uint32_t)c->opt_agg_block;
     ag.cand = nullptr; ag.per_bundle = 0; ag.offsets = off_d; ag.xy = xy_d; ag.out = c->est_d;
     ag.err_empty = c->flags_d + 1; ag.n_bundles = nb; ag.top_c = p->top_c; ag.toler_per = p->toler_per;
     const double r = p->radius_m / p->tile_m;
@@ -1726,6 +1736,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "graph")) { if (v != 0 && v != 1) goto bad; c->opt_graph = v; }
     else if (!strcmp(key, "tau_share")) { if (v != 0 && v != 1) goto bad; c->opt_tau_share = v; }
     else if (!strcmp(key, "micro")) { if (v != 0 && v != 1) goto bad; c->opt_micro = v; }
+    else if (!strcmp(key, "agg_block")) { if (v != 0 && v != 1) goto bad; c->opt_agg_block = v; }
     else if (!strcmp(key, "poison")) { if (v != 0 && v != 1) goto bad; c->opt_poison = v; }
     else return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown option '%s'", key);
     ++c->gen;   // every option can change the launch sequence: retire a captured graph

@@ -199,6 +199,88 @@ def test_aggregate_standalone_vs_oracle():
             assert np.array_equal(g["ranked"]["count"][:k], r.ranked_count)
 
 
+def test_aggregate_small_bundles_warp_vs_block_vs_oracle():
+    """Bundles of <= 32 candidates take the one-warp Algorithm 2 (aggregate_warp); option
+    agg_block = 1 forces the CTA-wide version.  Both equal the oracle (ranking ties by count
+    then signed (y, x), inclusive circles, the strict toler_per test and the low-confidence
+    fallback) and each other byte for byte, padding of the ranked list included."""
+    rng = np.random.default_rng(79)
+    e = _engine(16)
+    sets = []
+    for s in range(400):
+        n = int(rng.integers(1, 41))
+        kind = s % 5
+        if kind == 0:
+            xy = rng.integers(0, 4, (n, 2))                              # many count ties
+        elif kind == 1:
+            xy = rng.integers(-6, 6, (n, 2))
+        elif kind == 2:
+            c = rng.integers(-50, 50, (3, 2))
+            xy = c[rng.integers(0, 3, n)] + rng.integers(-2, 3, (n, 2))
+        elif kind == 3:
+            xy = np.repeat(rng.integers(-9, 9, (1, 2)), n, axis=0)       # one tile
+        else:
+            xy = rng.integers(-(1 << 30), 1 << 30, (n, 2))               # all distinct, far apart
+        sets.append(xy.astype(np.int32))
+    off = np.concatenate([[0], np.cumsum([len(x) for x in sets])]).astype(np.uint32)
+    allxy = np.concatenate(sets)
+    for params in (ol.Params(), ol.Params(top_c=3, toler_per=0.5, radius_m=0.9),
+                   ol.Params(top_c=64, toler_per=1.0, radius_m=1.5), ol.Params(top_c=1, toler_per=0.05)):
+        outs = []
+        for block in (0, 1):
+            e.set_option("agg_block", block)
+            est = e.aggregate(allxy, off, params)
+            outs.append(est.tobytes())
+            for b, xy in enumerate(sets):
+                r = oracle.aggregate(xy, params.top_c, params.toler_per, params.radius_m, params.tile_m)
+                g = est[b]
+                assert (g["x"], g["y"], bool(g["low_confidence"]), g["confidence"]) == \
+                    (r.x, r.y, r.low_confidence, r.confidence), (b, block)
+                assert g["x_m"] == r.x_m and g["y_m"] == r.y_m and int(g["total"]) == len(xy)
+                k = int(g["n_ranked"])
+                assert k == len(r.ranked_circle), (b, block)
+                assert np.array_equal(g["ranked"]["x"][:k], r.ranked_xy[:, 0]), (b, block)
+                assert np.array_equal(g["ranked"]["y"][:k], r.ranked_xy[:, 1]), (b, block)
+                assert np.array_equal(g["ranked"]["circle"][:k], r.ranked_circle), (b, block)
+                assert np.array_equal(g["ranked"]["count"][:k], r.ranked_count), (b, block)
+                assert not g["ranked"][k:].tobytes().strip(b"\0"), (b, block)
+        assert outs[0] == outs[1]
+    e.set_option("agg_block", 0)
+
+
+def test_micro_kernel_split_shares_vs_oracle():
+    """NK10 splits each (frame, subspace) job over several CTAs (shares of >= 256 rows, the
+    last CTA merges the shares' lists): subspaces of 1..8,192 rows, N up to 128 (a 1,024-key
+    merge), bundles of several jobs, against the oracle; the block-wide Alg. 2 agrees."""
+    rng = np.random.default_rng(950)
+    for case in range(6):
+        sizes = [[8192], [8000, 3], [257, 255, 1], [2000], [4097, 4096], [600, 700, 800]][case]
+        F = np.abs(rng.standard_normal((sum(sizes), 64))).astype(np.float32)
+        F /= np.linalg.norm(F, axis=1, keepdims=True)
+        F[rng.integers(0, len(F), 30)] = F[rng.integers(0, len(F), 30)]   # exact duplicates: ties
+        C = rng.integers(0, 60, (sum(sizes), 2)).astype(np.int32)
+        M = [1, 1, 3, 1, 1, 5][case]
+        nb = max(1, (1 << 16) // (len(F) * M))
+        nb = min(nb, 3)
+        Q = (F[rng.integers(0, len(F), nb * M)] + 1e-3 * rng.standard_normal((nb * M, 64))).astype(np.float32)
+        Q = np.ascontiguousarray(Q.reshape(nb, M, 64))
+        for N in ([128, 15] if case < 2 else [5, 40]):
+            ref = oracle.retrieve(sizes, F, C, Q, N)
+            e = _engine(16)
+            e.upload(F, C, sizes, (64, 64))
+            outs = []
+            for block in (0, 1):
+                e.set_option("agg_block", block)
+                e.query(Q, N=N, aggregate=True)
+                assert e.stat("used_micro") == 1 and e.stat("kernels") == 1
+                got, est = e.topk(), e.estimates()
+                assert_candidates_equal(got, ref, f"split case {case} N {N}")
+                assert_estimates_equal(est, ref, ctx=f"split case {case} N {N}")
+                outs.append((got.tobytes(), est.tobytes()))
+            assert outs[0] == outs[1]
+            e.close()
+
+
 def test_aggregate_negative_tiles_and_grid_range():
     """Standalone Alg. 2 ranks tiles by count, then signed (y, x) ascending (R7) for
     any tile, negative ones included (ADVICE r01: the unbiased sort key put them last);

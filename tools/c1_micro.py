@@ -27,3 +27,5 @@ e.query(qd, N=cfg.N, aggregate=True)
 torch.cuda.synchronize()
 print("micro phases (cycles): scan", e.stat("prof0"), "top-N + rows", e.stat("prof1"), "bundle count", e.stat("prof2"),
       "Alg. 2", e.stat("prof3"))
+print("  of top-N + rows: own select", e.stat("prof4"), "cluster barrier", e.stat("prof5"), "gather + barrier", e.stat("prof6"),
+      "rows", e.stat("prof7"))
