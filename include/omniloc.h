@@ -397,8 +397,9 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *   "seed_samples"  rows sampled per (frame, subspace) by the exact seed (16..32768; default 0:
  *                   8192 for >= 1,024 (frame, subspace) jobs, else 4096; at most 8192 when the
  *                   one-CTA-per-job seed kernel runs)
- *   "seed_kernel"   1 (default) / 0: two-kernel seed (sample rows reused across frames) for >= 1,024
- *                   (frame, subspace, split) jobs, else one CTA per job
+ *   "seed_kernel"   1 (default) / 0: two-kernel seed (sample rows reused across frames; one CTA
+ *                   per job when its scratch would exceed 2^28 entries) / one CTA per
+ *                   (frame, subspace, split) job
  *   "tc"            -1 (default: automatic, >= tc_min_frames frames) / 1 / 0: the certified
  *                   tensor-core filter (needs |f| < 65000 and ||f|| < 300 in the database)
  *   "tc_min_frames" frames per query below which the CUDA-core scans are used (default 0:

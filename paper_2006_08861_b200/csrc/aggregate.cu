@@ -72,32 +72,6 @@ __device__ __forceinline__ u64 tile_key(int32_t x, int32_t y) {
 __device__ __forceinline__ int32_t key_x(u64 k) { return (int32_t)((uint32_t)k ^ 0x80000000u); }
 __device__ __forceinline__ int32_t key_y(u64 k) { return (int32_t)((uint32_t)(k >> 32) ^ 0x80000000u); }
 
-// one key per lane -> the warp's 32 keys ascending across the lanes (bitonic network)
-__device__ __forceinline__ u64 warp_sort32(u64 k, int lane) {
-#pragma unroll
-    for (int kk = 2; kk <= 32; kk <<= 1) {
-#pragma unroll
-        for (int j = kk >> 1; j > 0; j >>= 1) {
-            const u64 o = __shfl_xor_sync(0xffffffffu, k, j);
-            const bool keep_min = ((lane & j) == 0) == ((lane & kk) == 0);
-            k = keep_min ? (o < k ? o : k) : (o > k ? o : k);
-        }
-    }
-    return k;
-}
-// two ascending 32-key warp lists -> the 32 smallest of both, ascending: min(a_i, b_{31-i})
-// is the lower half of the bitonic merge of a with b reversed, then 5 half-cleaner steps
-__device__ __forceinline__ u64 warp_merge32(u64 a, u64 b, int lane) {
-    const u64 br = __shfl_sync(0xffffffffu, b, 31 - lane);
-    u64 v = a < br ? a : br;
-#pragma unroll
-    for (int j = 16; j > 0; j >>= 1) {
-        const u64 o = __shfl_xor_sync(0xffffffffu, v, j);
-        v = (lane & j) == 0 ? (o < v ? o : v) : (o > v ? o : v);
-    }
-    return v;
-}
-
 // Algorithm 2 for a bundle of 1..32 candidates by one warp, lane = candidate: the steps and
 // tie rules of aggregate_block below, with shuffles in place of its shared-memory sorts and
 // block barriers (a bundle of C4 / C1 size costs a few hundred cycles instead of ~12k).
@@ -334,26 +308,6 @@ __device__ __forceinline__ void micro_select(const u64 *keys, uint32_t n, uint32
         lo = best;
         if (lane == 0) sel[r] = best;
     }
-}
-
-// The c <= 32 smallest of keys[0..n) (shared memory), ascending, into sel[0..c), by the whole
-// CTA: every warp folds its 32-key chunks into a running sorted 32-list (sort, merge), then
-// the warps' lists are merged pairwise in 4 rounds (scratch: 32 per warp).  Unique keys, so
-// the result is the same set and order as micro_select's.
-__device__ void block_select32(const u64 *keys, uint32_t n, uint32_t c, u64 *sel, u64 *scratch) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    u64 run = kPadKey;
-    for (uint32_t base = 32u * warp; base < n; base += 32u * nw) {
-        const u64 v = base + lane < n ? keys[base + lane] : kPadKey;
-        run = warp_merge32(run, warp_sort32(v, lane), lane);
-    }
-    for (int st = 1; st < nw; st <<= 1) {
-        scratch[warp * 32 + lane] = run;
-        __syncthreads();
-        if (warp % (2 * st) == 0 && warp + st < nw) run = warp_merge32(run, scratch[(warp + st) * 32 + lane], lane);
-        __syncthreads();
-    }
-    if (warp == 0 && (uint32_t)lane < c) sel[lane] = run;
 }
 
 __global__ void __launch_bounds__(kAggThreads) micro_kernel(MicroArgs a) {

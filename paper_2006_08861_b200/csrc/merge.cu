@@ -39,65 +39,118 @@ __device__ __forceinline__ u64 warp_min_u64(u64 v) {
 }
 
 constexpr int kMergeThreads = 256;
+constexpr uint32_t kMergeBuf = 2048;   // keys <= T gathered in shared memory
 
-// One warp per (query, subspace).
+// the smallest value over the CTA (every thread passes v; all get the result)
+__device__ __forceinline__ u64 block_min_u64(u64 v, u64 *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_min_u64(v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    u64 m = kPadKey;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = red[w] < m ? red[w] : m;
+    __syncthreads();
+    return m;
+}
+
+// One CTA per (query, subspace): the N smallest keys over the subspace's work-item lists.
+// Every list is ascending (the scans write sorted lists, pads last), so the global N-th best
+// is <= T = min over lists of list[N-1] (that list holds N keys <= T).  Pass 1 computes T
+// (one load per list), pass 2 gathers every key <= T -- a prefix of each list, usually
+// empty -- into shared memory, and the N smallest of those are the answer.  (Round 1 ran N
+// passes over all lists with one warp: 0.2-0.4 ms for small batches, where a frame's
+// subspace has thousands of items.)  More than kMergeBuf keys <= T: N rounds of a CTA-wide
+// "minimum above the last" over all keys instead.  Keys are unique apart from the all-ones
+// pad, so either way the result is the exact top-N.
 __global__ void __launch_bounds__(kMergeThreads) merge_chunks_kernel(MergeArgs a) {
-    const uint32_t gw = (blockIdx.x * kMergeThreads + threadIdx.x) / 32;
-    const int lane = threadIdx.x & 31;
-    if (gw >= a.nq * a.n_sub) return;
-    const uint32_t q = gw / a.n_sub, i = gw % a.n_sub;
+    __shared__ u64 buf[kMergeBuf];
+    __shared__ u64 sel[OL_MAX_N];
+    __shared__ u64 scratch[kMergeThreads];
+    __shared__ u64 red[kMergeThreads / 32];
+    __shared__ uint32_t nbuf;
+    const uint32_t job = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t q = job / a.n_sub, i = job % a.n_sub;
     const SubInfo si = a.subs[i];
     // the subspace's work items exist; its candidate rows fit the candidate array
     if (!OL_DCHECK(si.chunk_begin <= si.chunk_end && si.chunk_end <= a.n_items &&
                    (!a.cand || (uint64_t)(q + 1) * a.sub_prefix[a.n_sub] <= a.n_cand)))
-        return;
-    const uint32_t nk = (si.chunk_end - si.chunk_begin) * a.N;
-    const u64 *src = a.partial + ((size_t)q * a.n_items + si.chunk_begin) * a.N;
-    uint4 *dst = a.records + ((size_t)q * a.n_sub + i) * a.N;
-    // fused candidate rows (world 1): rank r < c of this (frame, subspace)
+        return;   // (uniform over the CTA)
+    const uint32_t N = a.N, nl = si.chunk_end - si.chunk_begin;
+    const u64 *src = a.partial + ((size_t)q * a.n_items + si.chunk_begin) * N;
+    if (threadIdx.x == 0) nbuf = 0;
+    u64 t = kPadKey;
+    for (uint32_t j = threadIdx.x; j < nl; j += blockDim.x) {
+        const u64 v = src[(size_t)j * N + N - 1];
+        t = v < t ? v : t;
+    }
+    const u64 T = block_min_u64(t, red);   // (its barriers also publish nbuf = 0)
+    for (uint32_t j = threadIdx.x; j < nl; j += blockDim.x) {
+        const u64 *L = src + (size_t)j * N;
+        for (uint32_t r = 0; r < N; ++r) {
+            const u64 v = L[r];
+            if (v > T || v == kPadKey) break;
+            OL_DCHECK(r == 0 || L[r - 1] < v);   // (the lists are ascending)
+            const uint32_t pos = atomicAdd(&nbuf, 1u);
+            if (pos < kMergeBuf) buf[pos] = v;
+        }
+    }
+    __syncthreads();
+    const uint32_t nb = nbuf;
+    if (nb <= kMergeBuf) {
+        if (N <= 32) block_select32(buf, nb, N, sel, scratch);
+        else if (warp == 0) {
+            u64 lo = 0;
+            for (uint32_t r = 0; r < N; ++r) {
+                u64 best = kPadKey;
+                for (uint32_t k = lane; k < nb; k += 32) {
+                    const u64 v = buf[k];
+                    if ((r == 0 || v > lo) && v < best) best = v;
+                }
+                best = warp_min_u64(best);
+                lo = best;
+                if (lane == 0) sel[r] = best;
+            }
+        }
+    } else {
+        const uint32_t nk = nl * N;
+        u64 lo = 0;
+        for (uint32_t r = 0; r < N; ++r) {
+            u64 best = kPadKey;
+            for (uint32_t k = threadIdx.x; k < nk; k += blockDim.x) {
+                const u64 v = src[k];
+                if ((r == 0 || v > lo) && v < best) best = v;
+            }
+            best = block_min_u64(best, red);
+            lo = best;
+            if (threadIdx.x == 0) sel[r] = best;
+        }
+    }
+    __syncthreads();
+    // records (and at world 1 the candidate rows: rank r < c of this (frame, subspace))
+    uint4 *dst = a.records + ((size_t)q * a.n_sub + i) * N;
     const uint32_t c = a.cand ? a.sub_prefix[i + 1] - a.sub_prefix[i] : 0;
     ol_candidate *co = a.cand ? a.cand + (uint64_t)q * a.sub_prefix[a.n_sub] + a.sub_prefix[i] : nullptr;
-    u64 last = 0;
-    bool have_last = false;
-    for (uint32_t r = 0; r < a.N; ++r) {
-        u64 best = kPadKey;
-        for (uint32_t t = lane; t < nk; t += 32) {
-            u64 v = src[t];
-            if ((!have_last || v > last) && v < best) best = v;
+    for (uint32_t r = threadIdx.x; r < N; r += blockDim.x) {
+        const u64 best = sel[r];
+        uint4 rec;
+        if (best == kPadKey) {
+            rec = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u);
+        } else {
+            const uint32_t frame = (uint32_t)best;
+            const uint64_t row = si.row_begin + (frame - si.shard_begin);
+            // a winner is a row of this rank's slice of this subspace
+            const bool ok = OL_DCHECK(frame >= si.shard_begin && frame - si.shard_begin < si.count);
+            rec = make_uint4((uint32_t)(best >> 32), frame, ok ? (uint32_t)a.coords[2 * row] : 0u,
+                             ok ? (uint32_t)a.coords[2 * row + 1] : 0u);
         }
-        best = warp_min_u64(best);
-        if (lane == 0) {
-            uint4 rec;
-            if (best == kPadKey) {
-                rec = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u);
-            } else {
-                const uint32_t frame = (uint32_t)best;
-                const uint64_t row = si.row_begin + (frame - si.shard_begin);
-                // a winner is a row of this rank's slice of this subspace
-                const bool ok = OL_DCHECK(frame >= si.shard_begin && frame - si.shard_begin < si.count);
-                rec = make_uint4((uint32_t)(best >> 32), frame, ok ? (uint32_t)a.coords[2 * row] : 0u,
-                                 ok ? (uint32_t)a.coords[2 * row + 1] : 0u);
-            }
-            dst[r] = rec;
-            if (r < c) co[r] = make_candidate(rec, i, q, a.M);
-        }
-        if (best == kPadKey) {  // the rest are pads too
-            for (uint32_t rr = r + 1 + lane; rr < a.N; rr += 32) {
-                const uint4 pad = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0u);
-                dst[rr] = pad;
-                if (rr < c) co[rr] = make_candidate(pad, i, q, a.M);
-            }
-            break;
-        }
-        last = best;
-        have_last = true;
+        dst[r] = rec;
+        if (r < c) co[r] = make_candidate(rec, i, q, a.M);
     }
 }
 
 cudaError_t launch_merge_chunks(const MergeArgs &a, cudaStream_t s) {
-    uint64_t warps = (uint64_t)a.nq * a.n_sub;
-    uint64_t blocks = (warps * 32 + kMergeThreads - 1) / kMergeThreads;
-    merge_chunks_kernel<<<(unsigned)blocks, kMergeThreads, 0, s>>>(a);
+    merge_chunks_kernel<<<(unsigned)((uint64_t)a.nq * a.n_sub), kMergeThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -261,4 +261,51 @@ cudaError_t launch_relayout(const float *src, uint64_t rows, uint64_t dst_row0, 
 cudaError_t launch_check_coords(const int32_t *xy, uint64_t rows, int32_t x0, int32_t x1, int32_t y0,
                                 int32_t y1, int *flag, cudaStream_t s);
 
+// ---- warp / block selection of the smallest unique u64 keys (NK4 merges, NK10)
+// one key per lane -> the warp's 32 keys ascending across the lanes (bitonic network)
+__device__ __forceinline__ u64 warp_sort32(u64 k, int lane) {
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            const u64 o = __shfl_xor_sync(0xffffffffu, k, j);
+            const bool keep_min = ((lane & j) == 0) == ((lane & kk) == 0);
+            k = keep_min ? (o < k ? o : k) : (o > k ? o : k);
+        }
+    }
+    return k;
+}
+// two ascending 32-key warp lists -> the 32 smallest of both, ascending: min(a_i, b_{31-i})
+// is the lower half of the bitonic merge of a with b reversed, then 5 half-cleaner steps
+__device__ __forceinline__ u64 warp_merge32(u64 a, u64 b, int lane) {
+    const u64 br = __shfl_sync(0xffffffffu, b, 31 - lane);
+    u64 v = a < br ? a : br;
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const u64 o = __shfl_xor_sync(0xffffffffu, v, j);
+        v = (lane & j) == 0 ? (o < v ? o : v) : (o > v ? o : v);
+    }
+    return v;
+}
+
+// The c <= 32 smallest of keys[0..n) (shared memory), ascending, into sel[0..c), by the whole
+// CTA: every warp folds its 32-key chunks into a running sorted 32-list (sort, merge), then
+// the warps' lists are merged pairwise in log2(warps) rounds (scratch: 32 per warp).  Keys
+// are unique, so this is the same set and order as c rounds of "the minimum above the last".
+__device__ inline void block_select32(const u64 *keys, uint32_t n, uint32_t c, u64 *sel, u64 *scratch) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    u64 run = kPadKey;
+    for (uint32_t base = 32u * warp; base < n; base += 32u * nw) {
+        const u64 v = base + lane < n ? keys[base + lane] : kPadKey;
+        run = warp_merge32(run, warp_sort32(v, lane), lane);
+    }
+    for (int st = 1; st < nw; st <<= 1) {
+        scratch[warp * 32 + lane] = run;
+        __syncthreads();
+        if (warp % (2 * st) == 0 && warp + st < nw) run = warp_merge32(run, scratch[(warp + st) * 32 + lane], lane);
+        __syncthreads();
+    }
+    if (warp == 0 && (uint32_t)lane < c) sel[lane] = run;
+}
+
 }  // namespace ol

@@ -1092,14 +1092,13 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
                (uint64_t)sa.samples * splits * 2 * 8 <= minc) splits *= 2;
         sa.splits = splits;
         // the two-kernel seed's scratch (acc bits of every (frame, subspace, split, sample));
-        // the one-CTA-per-(frame, subspace, split) kernel runs instead beyond 2^28 entries or
-        // for few (frame, subspace, split) jobs, where a warp-per-job select is too serial
-        // (measured: 8 / 256 frames at 10M rows 0.05 / 0.15 vs 0.16 / 0.17 ms; 1,024 frames at
-        // 100M 0.62 vs 0.24 ms; C2 0.92 vs 0.18 ms)
+        // the one-CTA-per-(frame, subspace, split) kernel runs instead beyond 2^28 entries
+        // (round 2, with the CTA-per-job select, tools/seed_small.py: 8 / 64 / 256 frames at
+        // 100M rows 0.036 / 0.049 / 0.051 vs 0.084 / 0.284 / 0.280 ms, 10M rows 0.034 / 0.046 /
+        // 0.044 vs 0.050 / 0.147 / 0.147 ms; round 1: 1,024 frames at 100M 0.24 vs 0.62 ms)
         const uint64_t nscr = (uint64_t)nq * c->n_sub * splits * sa.samples;
-        const uint64_t jobs = (uint64_t)nq * c->n_sub * splits;
         sa.scratch = nullptr;
-        if (nscr <= (1ull << 28) && jobs >= 1024 && c->opt_seed_kernel != 0) {
+        if (nscr <= (1ull << 28) && c->opt_seed_kernel != 0) {
             OL_CUDA(c, grow(&c->seed_scratch, &c->seed_scratch_cap, (size_t)nscr));
             sa.scratch = c->seed_scratch;
         }

@@ -2,14 +2,15 @@
 seeded with the converged thresholds of the previous query (tc_debug 64: start from
 ol_thresholds as they are), which is the limit any better seed could reach.
   python tools/seed_gain.py [rows]"""
-import sys, torch
+import os, sys, torch
 sys.path.insert(0, '.')
 import synthgen, paper_2006_08861_b200 as ol
 spec = synthgen.CONFIGS["C4"].spec
 n = int(sys.argv[1]) if len(sys.argv) > 1 else spec.n_entries
 dev = torch.device("cuda", 0)
 F, C = synthgen.db_device(spec, 0, n, dev)
-Q, _ = synthgen.render_device(spec, synthgen.query_points(spec, 4242, 1024), dev)
+NQ = int(os.environ.get("NQ", 1024))
+Q, _ = synthgen.render_device(spec, synthgen.query_points(spec, 4242, NQ), dev)
 e = ol.Engine(0)
 e.upload(F, C, [n], spec.grid())
 del F, C

@@ -6,7 +6,8 @@ spec = synthgen.CONFIGS["C4"].spec
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 20_000_000
 dev = torch.device("cuda", 0)
 F, C = synthgen.db_device(spec, 0, n, dev)
-Q, _ = synthgen.render_device(spec, synthgen.query_points(spec, 4242, 1024), dev)
+NQ = int(os.environ.get("NQ", 1024))
+Q, _ = synthgen.render_device(spec, synthgen.query_points(spec, 4242, NQ), dev)
 e = ol.Engine(0)
 if os.environ.get("TCK"): e.set_option("tc_k", int(os.environ["TCK"]))
 e.upload(F, C, [n], spec.grid())
@@ -23,7 +24,7 @@ for dbg in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else '0
     ms = e.stat("time_seed_ns" if os.environ.get("SEEDTIME") else "time_scan_ns") / int(os.environ.get("REPS", 5)) / 1e6
     for k in ("seed", "merge", "final"): e.stat(f"time_{k}_ns")
     e.set_option("time_kernels", 0)
-    tiles = n / 256 * ((1024 + 127) // 128) / 148   # 256-row x 128-frame tiles per SM
+    tiles = n / 256 * ((NQ + 127) // 128) / 148   # 256-row x 128-frame tiles per SM
     if dbg & 8:
         print("   flagged by (part, quarter):", [e.stat(f"prof{i}") for i in range(16)])
     if dbg & 16:
