@@ -38,8 +38,8 @@ __device__ __forceinline__ u64 warp_min_u64(u64 v) {
     return v;
 }
 
-constexpr int kMergeThreads = 256;
-constexpr uint32_t kMergeBuf = 2048;   // keys <= T gathered in shared memory
+constexpr int kMergeThreads = 256;     // (at most; fewer for subspaces of few work items)
+constexpr uint32_t kMergeBuf = 2048;   // keys <= T gathered in shared memory (at most)
 
 // the smallest value over the CTA (every thread passes v; all get the result)
 __device__ __forceinline__ u64 block_min_u64(u64 v, u64 *red) {
@@ -61,12 +61,15 @@ __device__ __forceinline__ u64 block_min_u64(u64 v, u64 *red) {
 // passes over all lists with one warp: 0.2-0.4 ms for small batches, where a frame's
 // subspace has thousands of items.)  More than kMergeBuf keys <= T: N rounds of a CTA-wide
 // "minimum above the last" over all keys instead.  Keys are unique apart from the all-ones
-// pad, so either way the result is the exact top-N.
+// pad, so either way the result is the exact top-N.  The buffer holds a.buf_cap keys (<=
+// kMergeBuf; = lists x N when that is smaller, so the fallback never runs then) and the CTA
+// is one warp when a subspace has at most 8 lists (C2: thousands of tiny jobs).
 __global__ void __launch_bounds__(kMergeThreads) merge_chunks_kernel(MergeArgs a) {
-    __shared__ u64 buf[kMergeBuf];
-    __shared__ u64 sel[OL_MAX_N];
-    __shared__ u64 scratch[kMergeThreads];
-    __shared__ u64 red[kMergeThreads / 32];
+    extern __shared__ __align__(16) unsigned char msm[];
+    u64 *buf = reinterpret_cast<u64 *>(msm);                  // [buf_cap]
+    u64 *sel = buf + a.buf_cap;                               // [N]
+    u64 *scratch = sel + a.N;                                 // [blockDim]
+    u64 *red = scratch + blockDim.x;                          // [blockDim / 32]
     __shared__ uint32_t nbuf;
     const uint32_t job = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -92,12 +95,12 @@ __global__ void __launch_bounds__(kMergeThreads) merge_chunks_kernel(MergeArgs a
             if (v > T || v == kPadKey) break;
             OL_DCHECK(r == 0 || L[r - 1] < v);   // (the lists are ascending)
             const uint32_t pos = atomicAdd(&nbuf, 1u);
-            if (pos < kMergeBuf) buf[pos] = v;
+            if (pos < a.buf_cap) buf[pos] = v;
         }
     }
     __syncthreads();
     const uint32_t nb = nbuf;
-    if (nb <= kMergeBuf) {
+    if (nb <= a.buf_cap) {
         if (N <= 32) block_select32(buf, nb, N, sel, scratch);
         else if (warp == 0) {
             u64 lo = 0;
@@ -149,8 +152,13 @@ __global__ void __launch_bounds__(kMergeThreads) merge_chunks_kernel(MergeArgs a
     }
 }
 
-cudaError_t launch_merge_chunks(const MergeArgs &a, cudaStream_t s) {
-    merge_chunks_kernel<<<(unsigned)((uint64_t)a.nq * a.n_sub), kMergeThreads, 0, s>>>(a);
+cudaError_t launch_merge_chunks(const MergeArgs &a_in, cudaStream_t s) {
+    MergeArgs a = a_in;
+    const uint64_t keys = (uint64_t)a.max_lists * a.N;
+    a.buf_cap = (uint32_t)(keys < kMergeBuf ? (keys ? keys : 1) : kMergeBuf);
+    const uint32_t threads = a.max_lists <= 8 ? 32u : a.max_lists <= 64 ? 128u : (uint32_t)kMergeThreads;
+    const size_t smem = sizeof(u64) * ((size_t)a.buf_cap + a.N + threads + threads / 32);
+    merge_chunks_kernel<<<(unsigned)((uint64_t)a.nq * a.n_sub), threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -116,6 +116,8 @@ struct MergeArgs {
     const uint32_t *sub_prefix;  // [n_sub+1] prefix of min(N, |n_i|)
     uint32_t M;
     uint64_t n_cand;             // candidate rows (bounds checks)
+    uint32_t max_lists;          // the most work items of one subspace (launch shape)
+    uint32_t buf_cap;            // (set by launch_merge_chunks)
 };
 
 struct RankMergeArgs {

@@ -130,6 +130,7 @@ struct ol_ctx {
         std::vector<WorkItem> items;
         WorkItem *items_d;
         SubInfo *subs_d;          // the subspaces with this table's chunk_begin / chunk_end
+        uint32_t max_lists;       // the most work items of one subspace
     };
     static constexpr size_t kMaxTables = 16;
     std::deque<ItemTable> tables;    // (a deque: push_back keeps `cur` valid)
@@ -685,7 +686,9 @@ static ol_status build_items(ol_ctx *c, uint64_t chunk) {
         }
         s.chunk_end = (uint32_t)items.size();
     }
-    ol_ctx::ItemTable t{chunk, items, nullptr, nullptr};
+    uint32_t max_lists = 0;
+    for (auto &sb : subs) max_lists = sb.chunk_end - sb.chunk_begin > max_lists ? sb.chunk_end - sb.chunk_begin : max_lists;
+    ol_ctx::ItemTable t{chunk, items, nullptr, nullptr, max_lists};
     OL_CUDA(c, cudaMalloc((void **)&t.items_d, sizeof(WorkItem) * (items.empty() ? 1 : items.size())));
     if (cudaMalloc((void **)&t.subs_d, sizeof(SubInfo) * c->n_sub) != cudaSuccess) {
         cudaFree(t.items_d);
@@ -1188,6 +1191,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
     ma.partial = c->partial_d; ma.subs = c->cur ? c->cur->subs_d : c->subs_d; ma.coords = c->coords; ma.records = c->payload_d;
     ma.nq = nq; ma.n_items = n_items; ma.n_sub = c->n_sub; ma.N = N;
     ma.cand = nullptr; ma.sub_prefix = nullptr; ma.M = M; ma.n_cand = per_q * nq;
+    ma.max_lists = c->cur ? c->cur->max_lists : (uint32_t)n_items;
     c->cand_fused = false;
     if (c->world == 1) {   // the merge also writes the candidate rows (one launch fewer)
         st = ensure_prefix(c, N);
