@@ -434,6 +434,9 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *                   sequence; not used when "tc", "chunk" or "qtile" force a path or schedule
  *   "agg_block"     0 (default) / 1: tests: Algorithm 2 by the CTA-wide kernel for bundles of
  *                   <= 32 candidates too (default: one warp, shuffles only); same results
+ *   "merge_scan"    0 (default) / 1: tests: the per-rank merge takes its fallback (N rounds of
+ *                   a CTA-wide minimum over every work-item list) instead of gathering the keys
+ *                   <= min over lists of list[N-1]; same results
  *   "poison"        0 (default) / 1: tests (an initcheck stand-in): the next uploads fill padding
  *                   rows and coords with NaN bytes instead of zeros, and every query first
  *                   fills its scratch and output buffers with garbage; results must not change

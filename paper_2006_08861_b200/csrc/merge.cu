@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_chunks_kernel(MergeArgs a
     }
     __syncthreads();
     const uint32_t nb = nbuf;
-    if (nb <= a.buf_cap) {
+    if (nb <= a.buf_cap && !a.force_scan) {
         if (N <= 32) block_select32(buf, nb, N, sel, scratch);
         else if (warp == 0) {
             u64 lo = 0;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_chunks_kernel(MergeArgs a
 cudaError_t launch_merge_chunks(const MergeArgs &a_in, cudaStream_t s) {
     MergeArgs a = a_in;
     const uint64_t keys = (uint64_t)a.max_lists * a.N;
-    a.buf_cap = (uint32_t)(keys < kMergeBuf ? (keys ? keys : 1) : kMergeBuf);
+    a.buf_cap = a.force_scan ? 0u : (uint32_t)(keys < kMergeBuf ? (keys ? keys : 1) : kMergeBuf);
     const uint32_t threads = a.max_lists <= 8 ? 32u : a.max_lists <= 64 ? 128u : (uint32_t)kMergeThreads;
     const size_t smem = sizeof(u64) * ((size_t)a.buf_cap + a.N + threads + threads / 32);
     merge_chunks_kernel<<<(unsigned)((uint64_t)a.nq * a.n_sub), threads, smem, s>>>(a);

@@ -118,6 +118,7 @@ struct MergeArgs {
     uint64_t n_cand;             // candidate rows (bounds checks)
     uint32_t max_lists;          // the most work items of one subspace (launch shape)
     uint32_t buf_cap;            // (set by launch_merge_chunks)
+    uint32_t force_scan;         // tests: always the N-round scan over all keys (the fallback)
 };
 
 struct RankMergeArgs {

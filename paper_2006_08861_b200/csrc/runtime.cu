@@ -170,6 +170,7 @@ struct ol_ctx {
     uint32_t *bcount_d = nullptr; size_t bcount_cap = 0;   // NK10 per-bundle job counters (kept zero)
     bool used_micro = false;
     int64_t opt_micro = 1;
+    int64_t opt_merge_scan = 0;  // 1: the merge's N-round scan over every key (tests: the fallback)
     int64_t opt_agg_block = 0;   // 1: Algorithm 2 by the CTA-wide kernel for bundles <= 32 too (tests)
     int32_t *agg_xy_d = nullptr; size_t agg_xy_cap = 0;
     int *flags_d = nullptr;                // [0] nonfinite frames, [1] aggregation error
@@ -1192,6 +1193,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
     ma.nq = nq; ma.n_items = n_items; ma.n_sub = c->n_sub; ma.N = N;
     ma.cand = nullptr; ma.sub_prefix = nullptr; ma.M = M; ma.n_cand = per_q * nq;
     ma.max_lists = c->cur ? c->cur->max_lists : (uint32_t)n_items;
+    ma.force_scan = (uint32_t)c->opt_merge_scan;
     c->cand_fused = false;
     if (c->world == 1) {   // the merge also writes the candidate rows (one launch fewer)
         st = ensure_prefix(c, N);
@@ -1740,6 +1742,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "tau_share")) { if (v != 0 && v != 1) goto bad; c->opt_tau_share = v; }
     else if (!strcmp(key, "micro")) { if (v != 0 && v != 1) goto bad; c->opt_micro = v; }
     else if (!strcmp(key, "agg_block")) { if (v != 0 && v != 1) goto bad; c->opt_agg_block = v; }
+    else if (!strcmp(key, "merge_scan")) { if (v != 0 && v != 1) goto bad; c->opt_merge_scan = v; }
     else if (!strcmp(key, "poison")) { if (v != 0 && v != 1) goto bad; c->opt_poison = v; }
     else return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown option '%s'", key);
     ++c->gen;   // every option can change the launch sequence: retire a captured graph

@@ -281,6 +281,35 @@ def test_micro_kernel_split_shares_vs_oracle():
             e.close()
 
 
+@pytest.mark.parametrize("tc", [0, 1])
+def test_merge_gather_and_fallback_vs_oracle(tc):
+    """The per-rank merge gathers only the keys <= min over work-item lists of list[N-1] (the
+    lists are ascending); option merge_scan = 1 takes its fallback, N rounds of a CTA-wide
+    minimum over every key.  Both equal the oracle with many lists per subspace (small
+    chunks), ragged subspaces, N above and below 32, and ties from duplicated rows."""
+    rng = np.random.default_rng(960 + tc)
+    sizes = [9000, 6001, 40]
+    F = np.abs(rng.standard_normal((sum(sizes), 64))).astype(np.float32)
+    F /= np.linalg.norm(F, axis=1, keepdims=True)
+    F[rng.integers(0, len(F), 50)] = F[rng.integers(0, len(F), 50)]
+    C = rng.integers(0, 60, (sum(sizes), 2)).astype(np.int32)
+    Q = (F[rng.integers(0, len(F), 60)] + 1e-3 * rng.standard_normal((60, 64))).astype(np.float32)
+    Q = np.ascontiguousarray(Q.reshape(20, 3, 64))
+    for N in (15, 40):
+        ref = oracle.retrieve(sizes, F, C, Q, N)
+        outs = []
+        for scan in (0, 1):
+            e = _engine(16, tc=tc, chunk=512, merge_scan=scan)
+            e.upload(F, C, sizes, (64, 64))
+            e.query(Q, N=N, aggregate=True)
+            assert e.stat("used_tc") == tc and e.stat("items") >= 30
+            assert_candidates_equal(e.topk(), ref, f"merge tc {tc} N {N} scan {scan}")
+            assert_estimates_equal(e.estimates(), ref, ctx=f"merge tc {tc} N {N} scan {scan}")
+            outs.append(e.topk().tobytes())
+            e.close()
+        assert outs[0] == outs[1]
+
+
 def test_aggregate_negative_tiles_and_grid_range():
     """Standalone Alg. 2 ranks tiles by count, then signed (y, x) ascending (R7) for
     any tile, negative ones included (ADVICE r01: the unbiased sort key put them last);

@@ -110,11 +110,31 @@ def main(n_fuzz: int):
     for es in engines:
         assert_candidates_equal(es.topk(), ref, "p2p")
     done.append("shards+p2p")
+    # NK10 split over a cluster (N > 32: the rounds select), and the merge's gather / fallback
+    rng = np.random.default_rng(5)
+    Fm = np.abs(rng.standard_normal((5000, 64))).astype(np.float32)
+    Fm /= np.linalg.norm(Fm, axis=1, keepdims=True)
+    Cm = rng.integers(0, 60, (5000, 2)).astype(np.int32)
+    Qm = np.ascontiguousarray((Fm[[7, 4000, 123]] + 1e-3).astype(np.float32).reshape(3, 1, 64))
+    for N in (5, 40):
+        e = ol.Engine(0)
+        e.upload(Fm, Cm, [4990, 10], (64, 64))
+        e.query(Qm, N=N, aggregate=True)
+        assert e.stat("used_micro") == 1
+        ref = oracle.retrieve([4990, 10], Fm, Cm, Qm, N)
+        assert_candidates_equal(e.topk(), ref, f"micro N {N}"); assert_estimates_equal(e.estimates(), ref, ctx=f"micro N {N}")
+        for scan in (0, 1):
+            e = ol.Engine(0)
+            e.set_option("micro", 0); e.set_option("chunk", 512); e.set_option("merge_scan", scan)
+            e.upload(Fm, Cm, [4990, 10], (64, 64))
+            e.query(Qm, N=N, aggregate=True)
+            assert_candidates_equal(e.topk(), ref, f"merge N {N} scan {scan}")
+    done.append("micro+merge")
     # standalone Alg. 2 with negative tiles
     rng = np.random.default_rng(4)
-    xy = rng.integers(-30, 30, (300, 2)).astype(np.int32)
-    est = ol.Engine(0).aggregate(xy, np.array([0, 100, 300], np.uint32))
-    for b, (lo, hi) in enumerate(((0, 100), (100, 300))):
+    xy = rng.integers(-30, 30, (320, 2)).astype(np.int32)
+    est = ol.Engine(0).aggregate(xy, np.array([0, 100, 300, 320], np.uint32))   # (the last: one warp)
+    for b, (lo, hi) in enumerate(((0, 100), (100, 300), (300, 320))):
         r = oracle.aggregate(xy[lo:hi])
         assert (est[b]["x"], est[b]["y"]) == (r.x, r.y)
     done.append("aggregate")
