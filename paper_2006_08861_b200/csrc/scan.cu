@@ -675,7 +675,27 @@ __global__ void __launch_bounds__(256) seed_acc_kernel(SeedArgs a) {
     for (int k4 = 0; k4 < kK / 4; ++k4)
         f[k4] = 4 * k4 < KC ? __ldg(reinterpret_cast<const float4 *>(a.coarse + coarse_off(row, 4 * k4, KC)))
                             : __ldg(reinterpret_cast<const float4 *>(a.fine + row * (kK - KC) + (4 * k4 - KC)));
-    for (uint32_t j = 0; j < nf; ++j) {
+    // two frames at a time: two independent fixed-order chains in flight per thread (a single
+    // chain issues one FFMA per 4-cycle latency)
+    const size_t fstride = (size_t)a.n_sub * a.splits * a.samples;
+    uint32_t *out = a.scratch + ((size_t)f0 * a.n_sub + i) * a.splits * a.samples + (size_t)split * a.samples + smp;
+    uint32_t j = 0;
+    for (; j + 1 < nf; j += 2) {
+        const float4 *qa = reinterpret_cast<const float4 *>(qs[j]);
+        const float4 *qb = reinterpret_cast<const float4 *>(qs[j + 1]);
+        float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+        for (int k4 = 0; k4 < kK / 4; ++k4) {
+            const float4 x = qa[k4], y = qb[k4];
+            acc0 = chain_step(acc0, x.x, f[k4].x); acc1 = chain_step(acc1, y.x, f[k4].x);
+            acc0 = chain_step(acc0, x.y, f[k4].y); acc1 = chain_step(acc1, y.y, f[k4].y);
+            acc0 = chain_step(acc0, x.z, f[k4].z); acc1 = chain_step(acc1, y.z, f[k4].z);
+            acc0 = chain_step(acc0, x.w, f[k4].w); acc1 = chain_step(acc1, y.w, f[k4].w);
+        }
+        out[j * fstride] = __float_as_uint(acc0);
+        out[(j + 1) * fstride] = __float_as_uint(acc1);
+    }
+    if (j < nf) {
         const float4 *q4 = reinterpret_cast<const float4 *>(qs[j]);
         float acc = 0.f;
 #pragma unroll
@@ -684,7 +704,7 @@ __global__ void __launch_bounds__(256) seed_acc_kernel(SeedArgs a) {
             acc = chain_step(acc, x.x, f[k4].x); acc = chain_step(acc, x.y, f[k4].y);
             acc = chain_step(acc, x.z, f[k4].z); acc = chain_step(acc, x.w, f[k4].w);
         }
-        a.scratch[(((size_t)(f0 + j) * a.n_sub + i) * a.splits + split) * a.samples + smp] = __float_as_uint(acc);
+        out[j * fstride] = __float_as_uint(acc);
     }
 }
 
@@ -743,6 +763,64 @@ __global__ void __launch_bounds__(256) seed_select_kernel(SeedArgs a) {
     }
     // every split's N-th smallest is an upper bound of the true N-th: keep the least
     if (tid == 0) atomicMin(&a.tau0[(size_t)q * a.n_sub + i], prefix);
+}
+
+// N <= 32 (about one pass over the job's values instead of four): T = the N-th smallest of
+// 512 evenly strided values (an upper bound of the N-th smallest of all S), then every value
+// <= T -- about N x S / 512 of them -- is gathered into shared memory and the N-th smallest
+// of those is the answer (keys acc bits << 32 | sample index are unique; ties in acc resolve
+// to the same value).  If more than kSelBuf values are <= T, the N-th smallest of the
+// gathered ones is a tighter bound: gather again below it (at most 3 rounds; the last bound
+// found is valid in any case).
+constexpr uint32_t kSelBuf = 2048;
+__global__ void __launch_bounds__(256) seed_select_small_kernel(SeedArgs a) {
+    __shared__ u64 buf[kSelBuf];
+    __shared__ u64 sel[32];
+    __shared__ u64 scratch[256];
+    __shared__ uint32_t nbuf;
+    const uint32_t job = blockIdx.x;   // (frame, subspace, split)
+    const uint32_t i = (job / a.splits) % a.n_sub, q = (job / a.splits) / a.n_sub;
+    const uint32_t S = (uint32_t)min((uint64_t)a.samples, a.subs[i].count);
+    if (S < a.N) return;   // (uniform over the CTA)
+    const uint32_t *v = a.scratch + (size_t)job * a.samples;
+    const uint32_t S0 = min(S, 512u);
+    for (uint32_t t = threadIdx.x; t < S0; t += blockDim.x) {
+        const uint32_t idx = (uint32_t)(((uint64_t)t * S) / S0);
+        buf[t] = ((u64)__ldcg(v + idx) << 32) | idx;
+    }
+    __syncthreads();
+    block_select32(buf, S0, a.N, sel, scratch);
+    __syncthreads();
+    uint32_t T = (uint32_t)(sel[a.N - 1] >> 32);
+    for (int round = 0; round < 3; ++round) {
+        if (threadIdx.x == 0) nbuf = 0;
+        __syncthreads();
+        for (uint32_t t0 = 0; t0 < S; t0 += 8 * 256) {
+            uint32_t x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t t = t0 + j * 256 + threadIdx.x;
+                x[j] = t < S ? __ldcg(v + t) : 0xFFFFFFFFu;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t t = t0 + j * 256 + threadIdx.x;
+                if (t < S && x[j] <= T) {
+                    const uint32_t pos = atomicAdd(&nbuf, 1u);
+                    if (pos < kSelBuf) buf[pos] = ((u64)x[j] << 32) | t;
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t nb = nbuf;
+        block_select32(buf, min(nb, kSelBuf), a.N, sel, scratch);
+        __syncthreads();
+        T = (uint32_t)(sel[a.N - 1] >> 32);   // (N values <= it: a valid bound either way)
+        __syncthreads();
+        if (nb <= kSelBuf) break;              // exact: every value <= the old T was gathered
+    }
+    // every split's N-th smallest is an upper bound of the true N-th: keep the least
+    if (threadIdx.x == 0) atomicMin(&a.tau0[(size_t)q * a.n_sub + i], T);
 }
 
 // Warp per job (small samples, many jobs: a CTA per job would mostly wait at barriers).
@@ -814,7 +892,8 @@ cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         // one CTA per job streams large samples with its loads in flight (C4: 170 -> 28 us);
         // a warp per job is faster for small ones (C2, 500 samples x 25,000 jobs: 0.18 vs 0.32 ms)
-        if (a.samples >= 2048) seed_select_kernel<<<a.nq * a.n_sub * a.splits, 256, 0, s>>>(a);
+        if (a.samples >= 2048 && a.N <= 32) seed_select_small_kernel<<<a.nq * a.n_sub * a.splits, 256, 0, s>>>(a);
+        else if (a.samples >= 2048) seed_select_kernel<<<a.nq * a.n_sub * a.splits, 256, 0, s>>>(a);
         else seed_select_warp_kernel<<<(a.nq * a.n_sub * a.splits + 7) / 8, 256, 0, s>>>(a);
         return cudaGetLastError();
     }
