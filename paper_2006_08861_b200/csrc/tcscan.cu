@@ -62,6 +62,7 @@ constexpr int kEv = 8;                  // survivor event ring entries per exact
                                         // 20M 2.82 / 2.70 / 2.66 / 2.67, 1M 0.68 / - / 0.58 / 0.57)
 constexpr int kTrackMax = 16;
 constexpr int kBndRing = 16;
+constexpr uint32_t kTlTiles = 120;      // profiling timeline (tc_debug 32 | 2048): tiles of CTA 0 recorded
 constexpr uint32_t kL2Ahead = 24;       // row tiles prefetched into L2 ahead of the TMA stage loads            // >= kMaxStages + kTBufs: see TcSmem::bnd           // largest N of the bound pre-pass (register list)
 constexpr float kTauInflate = 1.0f + 1.0f / 131072.0f;   // 1 + 2^-17
 constexpr uint32_t kStageBytesMax = kTileRows * kK * 2;   // 32 KB (pw = 64; 16 KB at pw = 32)
@@ -310,6 +311,8 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 if (t >= kTBufs) mbar_wait_sleep(&s.tempty[buf], ((t / kTBufs) - 1) & 1);
                 long long c2 = prof ? clock64() : 0;
                 if (prof) { pw_full += c1 - c0; pw_tempty += c2 - c1; pw_lat += c1 - *(volatile long long *)&s.tma_t0[st]; }
+                const bool tl = prof && (a.dbg & 2048) && blockIdx.x == 0 && t < kTlTiles && leader;   // (timeline)
+                if (tl) a.prof[64 + t * 8 + 0] = (unsigned long long)c2;
                 tc_fence_after();
                 const uint32_t rm = smem_u32(stage0 + (size_t)st * stage_bytes);
                 const uint32_t d = tmem + buf * kTileRows;
@@ -333,6 +336,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 }
                 __syncwarp();
                 if (prof) { pw_issue += c3 - c2; pw_commit += clock64() - c3; }
+                if (tl) a.prof[64 + t * 8 + 1] = (unsigned long long)clock64();
             }
             if (prof && leader) {
                 atomicAdd(&a.prof[0], (unsigned long long)pw_full); atomicAdd(&a.prof[1], (unsigned long long)pw_tempty);
@@ -397,6 +401,8 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             mbar_wait_sleep(&s.tfull[buf], (t / kTBufs) & 1);
             const long long w1 = prof ? clock64() : 0;
             if (prof && lane == 0) ew_tfull += w1 - w0;
+            const bool tl = prof && (a.dbg & 2048) && blockIdx.x == 0 && t < kTlTiles && lane == 0;   // (timeline)
+            if (tl) atomicMax(&a.prof[64 + t * 8 + 2], (unsigned long long)w1);
             tc_fence_after();
             if (quarter * 32 >= qn) {   // no frame in this warp's TMEM lanes (few frames, a pair's padding CTA)
                 tc_fence_before();
@@ -412,6 +418,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 mbar_wait(&s.bfull[sl], (t / kBndRing) & 1);   // (long complete: loaded with the rows)
                 const float4 *bp = reinterpret_cast<const float4 *>(&s.bnd[sl][half * 4]);
                 const float4 b01 = bp[0], b23 = bp[1];   // (g, e) of blocks 0, 1 | 2, 3
+                if (tl) atomicMax(&a.prof[64 + t * 8 + 6], (unsigned long long)clock64());
                 th0 = __fadd_rd(h, __fsub_rd(b01.x, __fmul_ru(nqm, b01.y)));
                 th1 = __fadd_rd(h, __fsub_rd(b01.z, __fmul_ru(nqm, b01.w)));
                 th2 = __fadd_rd(h, __fsub_rd(b23.x, __fmul_ru(nqm, b23.y)));
@@ -435,6 +442,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             tmem_ld32(taddr + 32, v1);
             tmem_ld_wait_regs(v0);   // orders every use of v0, v1 after the wait
             reg_fence(v1);
+            if (tl) atomicMax(&a.prof[64 + t * 8 + 7], (unsigned long long)clock64());
             if (kBound) {
                 float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
                 max32(v0, m0, m1);
@@ -461,6 +469,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             if (lane == 0) { if (kPair) mbar_arrive_leader(&s.tempty[buf]); else mbar_arrive(&s.tempty[buf]); }
             const long long w2 = prof ? clock64() : 0;
             if (prof && lane == 0) ew_ld += w2 - w1;
+            if (tl) atomicMax(&a.prof[64 + t * 8 + 3], (unsigned long long)w2);
             if (kBound) {
                 float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
                 max32(v0, m0, m1);
@@ -483,6 +492,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                     const long long e0 = clock64();
                     const uint32_t cnt = __popc(mk0) + __popc(mk1) + __popc(mk2) + __popc(mk3);
                     if (cnt) tc_enqueue_event(s, mk0, mk1, mk2, mk3, rb, ql, prof ? a.prof : nullptr);
+                    if (prof && (a.dbg & 2048) && blockIdx.x == 0 && t < kTlTiles) atomicAdd(&a.prof[64 + t * 8 + 5], 1ull);
                     if (a.stat_flagged) atomicAdd(a.stat_flagged, 1ull);
                     if (prof) {
                         const unsigned long long d = clock64() - e0;
@@ -497,6 +507,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
             // 10.08 ms (box-normalised), 20M rows 2.72 / 2.69 / 2.69, 1M 0.583 / 0.554 / 0.543
             if (refresher && ql < qn && gt < s.tau[ql]) atomicMin(&s.tau[ql], gt);
             if (prof && lane == 0) ew_tile += clock64() - ts;
+            if (tl) atomicMax(&a.prof[64 + t * 8 + 4], (unsigned long long)clock64());
         };
         float2 gA = load_g(grp), gC = load_g(grp + 2);
         const long long l0 = clock64();
