@@ -612,22 +612,35 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                     const uint64_t row = it.row_begin + rl;
                     if (OL_DCHECK(rl < it.count && col < qn && q0 + col < a.nq)) {
                         const float4 *qv = reinterpret_cast<const float4 *>(a.queries + (size_t)(q0 + col) * kK);
+                        // The chain is monotone (each step adds a square, RN is monotone), so once
+                        // its first 32 steps exceed the frame's threshold the pair cannot reach the
+                        // top-N: the second half of the row is read only for the rest (~1/3 of the
+                        // survivors; this halves their random DRAM reads, which crowd the row
+                        // stream's TMA loads during every CTA's start-up burst)
+                        const float tcur = __uint_as_float(lds_u32(&s.tau[col]));
                         float acc = 0.f;
-                        float4 f[kK / 4];   // all 16 row loads in flight (one selected address each)
+                        float4 f[kK / 8];
 #pragma unroll
-                        for (int k4 = 0; k4 < kK / 4; ++k4) {
-                            const float *src = 4 * k4 < (int)a.kc ? a.coarse + coarse_off(row, 4 * k4, a.kc)
-                                                                  : a.fine + row * (kK - a.kc) + (4 * k4 - a.kc);
-                            f[k4] = __ldg(reinterpret_cast<const float4 *>(src));
-                        }
+                        for (int h = 0; h < 2; ++h) {
+                            if (h == 1 && acc > tcur) break;
 #pragma unroll
-                        for (int k4 = 0; k4 < kK / 4; ++k4) {
-                            const float4 x = __ldg(qv + k4);
-                            acc = chain_step_tc(acc, x.x, f[k4].x); acc = chain_step_tc(acc, x.y, f[k4].y);
-                            acc = chain_step_tc(acc, x.z, f[k4].z); acc = chain_step_tc(acc, x.w, f[k4].w);
+                            for (int k = 0; k < kK / 8; ++k) {
+                                const int k4 = h * (kK / 8) + k;
+                                const float *src = 4 * k4 < (int)a.kc ? a.coarse + coarse_off(row, 4 * k4, a.kc)
+                                                                      : a.fine + row * (kK - a.kc) + (4 * k4 - a.kc);
+                                f[k] = __ldg(reinterpret_cast<const float4 *>(src));
+                            }
+#pragma unroll
+                            for (int k = 0; k < kK / 8; ++k) {
+                                const float4 x = __ldg(qv + h * (kK / 8) + k);
+                                acc = chain_step_tc(acc, x.x, f[k].x); acc = chain_step_tc(acc, x.y, f[k].y);
+                                acc = chain_step_tc(acc, x.z, f[k].z); acc = chain_step_tc(acc, x.w, f[k].w);
+                            }
                         }
                         key = ((u64)__float_as_uint(acc) << 32) | (u64)(it.frame_begin + rl);
-                        if (!(key < lists[(size_t)col * N + N - 1])) key = kPadKey;   // cannot enter the list
+                        // beyond the frame's threshold (a bound on the N-th best over all CTAs), or
+                        // not below this CTA's N-th: cannot enter the top-N
+                        if (acc > tcur || !(key < lists[(size_t)col * N + N - 1])) key = kPadKey;
                     } else col = 0xFFFFFFFFu;
                 }
                 // insert the keys into their frames' sorted lists: lanes of distinct frames in
