@@ -333,17 +333,14 @@ __global__ void __launch_bounds__(kAggThreads) micro_kernel(MicroArgs a) {
     const uint32_t per = (n + split - 1) / split;          // this job's rows per share
     const uint32_t r_lo = min(n, g * per), cnt = min(n, r_lo + per) - r_lo;
     // one row per thread per pass, its 16 float4 loads in flight together (a small query is
-    // latency-bound: one L2 round trip per pass); the coarse plane's 16-byte columns for
-    // k < kc, the fine plane's row after
+    // latency-bound: one L2 round trip per pass), from the fine plane's full row
     const float4 *q4 = reinterpret_cast<const float4 *>(qs);
     for (uint32_t r = threadIdx.x; r < cnt; r += blockDim.x) {
         const uint64_t row = si.row_begin + r_lo + r;
         float4 f[kK / 4];
 #pragma unroll
         for (int k4 = 0; k4 < kK / 4; ++k4) {
-            const float *src = 4 * k4 < (int)a.kc ? a.coarse + coarse_off(row, 4 * k4, a.kc)
-                                                  : a.fine + row * (kK - a.kc) + (4 * k4 - a.kc);
-            f[k4] = __ldg(reinterpret_cast<const float4 *>(src));
+            f[k4] = __ldg(reinterpret_cast<const float4 *>(a.fine + fine_off(row, 4 * k4)));
         }
         float acc = 0.f;
 #pragma unroll

@@ -62,6 +62,10 @@ constexpr uint32_t kInfBits = 0x7F800000u;  // +inf: "no threshold yet"
 // coefficients, each column 32 rows x 16 B contiguous.  A warp whose lane i owns
 // row (32 t + i) loads 512 contiguous bytes per LDG.128.  Every subspace starts
 // on a tile boundary (rows padded to a multiple of 32).
+// The fine plane holds every row in full, row-major [rows][64] (round 2: the exact re-scoring
+// reads a survivor's first 32 coefficients as one 128-B line, the rest as a second; round 1
+// stored only coefficients kc..63 there); the scans' fine passes start at column kc.
+__host__ __device__ __forceinline__ uint64_t fine_off(uint64_t row, uint32_t k) { return row * 64ull + k; }
 __host__ __device__ __forceinline__ uint64_t coarse_off(uint64_t row, uint32_t k, uint32_t kc) {
     return (((row >> 5) * (kc >> 2) + (k >> 2)) << 7) + ((row & 31) << 2) + (k & 3);
 }
@@ -86,7 +90,7 @@ struct SubInfo {
 
 struct ScanArgs {
     const float *coarse;         // [rows][kc]
-    const float *fine;           // [rows][K - kc] (null when kc == K)
+    const float *fine;           // [rows][K] full rows (fine_off)
     const float *queries;        // [nq][K]
     const WorkItem *items;
     uint32_t *tau0;              // [nq][n_sub] acc bits (seeded; shared running minimum), or null

@@ -567,10 +567,8 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
     // padding rows = 0 (option "poison": NaN bytes, so a padding element that is ever read shows)
     const int fillb = c->opt_poison ? 0xFF : 0;
     OL_CUDA(c, cudaMemsetAsync(c->coarse, fillb, sizeof(float) * R * kc, c->stream));
-    if (kc < OL_K) {
-        OL_CUDA(c, cudaMalloc((void **)&c->fine, sizeof(float) * R * (OL_K - kc)));
-        OL_CUDA(c, cudaMemsetAsync(c->fine, fillb, sizeof(float) * R * (OL_K - kc), c->stream));
-    }
+    OL_CUDA(c, cudaMalloc((void **)&c->fine, sizeof(float) * R * OL_K));   // (full rows: fine_off)
+    OL_CUDA(c, cudaMemsetAsync(c->fine, fillb, sizeof(float) * R * OL_K, c->stream));
     OL_CUDA(c, cudaMalloc((void **)&c->coords, sizeof(int32_t) * 2 * R));
     OL_CUDA(c, cudaMemsetAsync(c->coords, fillb, sizeof(int32_t) * 2 * R, c->stream));
     OL_CUDA(c, cudaMalloc((void **)&c->subs_d, sizeof(SubInfo) * ns));

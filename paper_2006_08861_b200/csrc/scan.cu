@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kScanThreads) scan_kernel(ScanArgs a) {
                     ++survivors;
                     if (KC < kK) {  // fine pass: continue the same chain
                         const float4 *fr =
-                            reinterpret_cast<const float4 *>(a.fine + row * (kK - KC));
+                            reinterpret_cast<const float4 *>(a.fine + fine_off(row, KC));
 #pragma unroll
                         for (int k = 0; k < (kK - KC) / 4; ++k) {
                             float4 x = qv[KC / 4 + k];
@@ -199,7 +199,7 @@ __device__ __noinline__ void scan2_survivors(const ScanArgs &a, const WorkItem &
             ++survivors;
             if (KC < kK) {  // fine pass: continue the same chain
                 const uint64_t row = it.row_begin + e;
-                const float4 *fr = reinterpret_cast<const float4 *>(a.fine + row * (kK - KC));
+                const float4 *fr = reinterpret_cast<const float4 *>(a.fine + fine_off(row, KC));
                 const float4 *qv = reinterpret_cast<const float4 *>(qs + q * kK);
 #pragma unroll
                 for (int k = 0; k < (kK - KC) / 4; ++k) {
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kScanThreads + 32) scan3_kernel(ScanArgs a) {
                             ++survivors;
                             if (KC < kK) {
                                 const uint64_t row = it.row_begin + e;
-                                const float4 *fr = reinterpret_cast<const float4 *>(a.fine + row * (kK - KC));
+                                const float4 *fr = reinterpret_cast<const float4 *>(a.fine + fine_off(row, KC));
                                 const float4 *qv = reinterpret_cast<const float4 *>(qs + q * kK);
 #pragma unroll
                                 for (int k = 0; k < (kK - KC) / 4; ++k) {
@@ -590,8 +590,7 @@ __global__ void __launch_bounds__(kSeedThreads, 2) tau_seed_kernel(SeedArgs a) {
         float4 f[kK / 4];   // (KC is a compile-time constant: all 16 loads issue before the chain)
 #pragma unroll
         for (int k4 = 0; k4 < kK / 4; ++k4)
-            f[k4] = 4 * k4 < KC ? __ldg(reinterpret_cast<const float4 *>(a.coarse + coarse_off(row, 4 * k4, KC)))
-                                : __ldg(reinterpret_cast<const float4 *>(a.fine + row * (kK - KC) + (4 * k4 - KC)));
+            f[k4] = __ldg(reinterpret_cast<const float4 *>(a.fine + fine_off(row, 4 * k4)));
         float acc = 0.f;
 #pragma unroll
         for (int k4 = 0; k4 < kK / 4; ++k4) {
@@ -673,8 +672,7 @@ __global__ void __launch_bounds__(256) seed_acc_kernel(SeedArgs a) {
     float4 f[kK / 4];
 #pragma unroll
     for (int k4 = 0; k4 < kK / 4; ++k4)
-        f[k4] = 4 * k4 < KC ? __ldg(reinterpret_cast<const float4 *>(a.coarse + coarse_off(row, 4 * k4, KC)))
-                            : __ldg(reinterpret_cast<const float4 *>(a.fine + row * (kK - KC) + (4 * k4 - KC)));
+        f[k4] = __ldg(reinterpret_cast<const float4 *>(a.fine + fine_off(row, 4 * k4)));
     // two frames at a time: two independent fixed-order chains in flight per thread (a single
     // chain issues one FFMA per 4-cycle latency)
     const size_t fstride = (size_t)a.n_sub * a.splits * a.samples;
@@ -909,7 +907,7 @@ cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ upload helpers
-// [rows][64] source rows -> tiled coarse plane (rows dst_row0 ..) + row-major fine plane
+// [rows][64] source rows -> tiled coarse plane (rows dst_row0 ..) + row-major fine plane (full rows)
 __global__ void relayout_kernel(const float *src, uint64_t rows, uint64_t dst_row0, int kc, float *coarse,
                                 float *fine) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < rows * kK;
@@ -918,7 +916,7 @@ __global__ void relayout_kernel(const float *src, uint64_t rows, uint64_t dst_ro
         const int k = (int)(i % kK);
         const float v = src[i];
         if (k < kc) coarse[coarse_off(d, k, kc)] = v;
-        else fine[d * (kK - kc) + (k - kc)] = v;
+        fine[fine_off(d, k)] = v;
     }
 }
 
@@ -942,7 +940,7 @@ __global__ void pad_rows_kernel(const SubInfo *subs, uint32_t n_sub, int kc, flo
         const uint64_t dst = si.row_begin + p;
         const int k = threadIdx.x % kK;
         if (k < kc) coarse[coarse_off(dst, k, kc)] = coarse[coarse_off(src, k, kc)];
-        else fine[dst * (kK - kc) + (k - kc)] = fine[src * (kK - kc) + (k - kc)];
+        fine[fine_off(dst, k)] = fine[fine_off(src, k)];
     }
 }
 

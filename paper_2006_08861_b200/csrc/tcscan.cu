@@ -626,9 +626,7 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
 #pragma unroll
                             for (int k = 0; k < kK / 8; ++k) {
                                 const int k4 = h * (kK / 8) + k;
-                                const float *src = 4 * k4 < (int)a.kc ? a.coarse + coarse_off(row, 4 * k4, a.kc)
-                                                                      : a.fine + row * (kK - a.kc) + (4 * k4 - a.kc);
-                                f[k] = __ldg(reinterpret_cast<const float4 *>(src));
+                                f[k] = __ldg(reinterpret_cast<const float4 *>(a.fine + fine_off(row, 4 * k4)));
                             }
 #pragma unroll
                             for (int k = 0; k < kK / 8; ++k) {
@@ -719,8 +717,8 @@ __global__ void tc_prep_rows_kernel(const float *coarse, const float *fine, int 
         float amax = 0.f;
         __half2 *dst = reinterpret_cast<__half2 *>(plane + r * pw);
         for (int k = 0; k < kK; k += 2) {
-            const float f0 = k < kc ? coarse[coarse_off(r, k, kc)] : fine[r * (kK - kc) + (k - kc)];
-            const float f1 = k + 1 < kc ? coarse[coarse_off(r, k + 1, kc)] : fine[r * (kK - kc) + (k + 1 - kc)];
+            const float f0 = fine[fine_off(r, k)];
+            const float f1 = fine[fine_off(r, k + 1)];
             const __half h0 = __float2half_rn(f0), h1 = __float2half_rn(f1);
             if (k < pw) dst[k / 2] = __halves2half2(h0, h1);
             amax = fmaxf(amax, fmaxf(fabsf(f0), fabsf(f1)));
