@@ -415,7 +415,9 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *                   pairs (tcgen05 cta_group::2) for the tensor-core scan
  *   "cluster"       1 (default) / 2 / 4 / 8: thread-block clusters over a work item's query
  *                   blocks when pairs are off
- *   "scan2"         1 (default) / 0 / 2: small-batch CUDA-core kernel choice
+ *   "scan2"         1 (default: the TMA-fed kernel for 1-2 frames per tile, the row-pair
+ *                   streaming kernel up to 16) / 2 (TMA-fed up to 16) / 0 (the general kernel):
+ *                   small-batch CUDA-core kernel choice
  *   "ctas"          cap on resident CTAs (0 = automatic)
  *   "time_kernels"  1 / 0: per-stage CUDA-event timing (stats "time_{seed,scan,merge,final}_ns")
  *   "tc_debug"      profiling only (results invalid when nonzero; host-side bits 64 = keep

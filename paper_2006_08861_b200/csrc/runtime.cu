@@ -197,7 +197,7 @@ struct ol_ctx {
     int64_t opt_tc_seed = 0;     // tensor-core path: 1 = seed thresholds with the bound pre-pass (off: the exact sampled seed is as fast at C4 and tighter at C3)
     int64_t opt_cluster = 1;     // tensor-core path: CTAs per cluster (query blocks sharing rows)
     int64_t opt_pair = 1;        // tensor-core path: CTA pairs (cta_group::2, M = 256): 0 off, 1 auto, 2 on
-    int64_t opt_scan2 = 1;       // small batches (<= 16 frames per tile) use scan2_kernel    // profiling experiments only (results invalid when nonzero)
+    int64_t opt_scan2 = 1;       // small batches (<= 16 frames per tile): 1 auto (scan3 for <= 2, else scan2), 2 scan3, 0 scan_kernel    // profiling experiments only (results invalid when nonzero)
     // per-kernel-class CUDA-event timing (option "time_kernels"): pairs recorded on
     // the context stream around each launch; summed and released by ol_get_stat
     enum { T_SEED, T_SCAN, T_MERGE, T_FINAL, T_COUNT };
@@ -1179,9 +1179,13 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         a.nq = nq; a.n_items = n_items; a.n_qtiles = n_qtiles; a.qt = qt; a.n_sub = c->n_sub; a.N = N;
         a.rows_pad = c->rows_pad;
         TimeScope ts(c, ol_ctx::T_SCAN);
-        if (qt <= 16 && c->opt_scan2 == 2 && c->kc < OL_K)   // few frames: TMA-fed row-pair kernel
+        // few frames: the TMA-fed row-pair kernel for 1-2 frames per tile (it streams the coarse
+        // plane faster: tools/scan3_sweep.py, 10M rows 0.121 vs 0.140 ms at 1 frame, 100M 0.916
+        // vs 0.937), the row-pair f32x2 streaming kernel for more (4 frames: 1.10 vs 0.98 ms)
+        const bool kc3 = c->kc == 8 || c->kc == 16 || c->kc == 32, kc2 = kc3 || c->kc == 64;
+        if (qt <= 16 && kc3 && (c->opt_scan2 == 2 || (c->opt_scan2 == 1 && qt <= 2)))
             OL_LAUNCH(c, launch_scan3(c->kc, a, scan3_smem_bytes(qt, N, c->kc), (int)(n_items * n_qtiles), c->stream));
-        else if (qt <= 16 && c->opt_scan2)   // few frames: row-pair f32x2 streaming kernel
+        else if (qt <= 16 && kc2 && c->opt_scan2)
             OL_LAUNCH(c, launch_scan2(c->kc, a, scan2_smem_bytes(qt, N, c->kc), (int)(n_items * n_qtiles), c->stream));
         else
             OL_LAUNCH(c, launch_scan(c->kc, a, scan_smem_bytes(qt, N), (int)(n_items * n_qtiles), c->stream));

@@ -310,6 +310,31 @@ def test_merge_gather_and_fallback_vs_oracle(tc):
         assert outs[0] == outs[1]
 
 
+@pytest.mark.parametrize("kc", [0, 8, 16, 32, 64])
+def test_small_batch_cuda_core_kernels_vs_oracle(kc):
+    """The CUDA-core scans for few frames -- scan3 (TMA-fed; automatic for 1-2 frames per tile),
+    scan2 (row-pair streaming; automatic up to 16) and the general scan_kernel (option
+    scan2 = 0) -- equal the oracle for every coarse width, 1 to 16 frames, ragged subspaces."""
+    rng = np.random.default_rng(970 + kc)
+    sizes = [12001, 9000, 37]
+    F = np.abs(rng.standard_normal((sum(sizes), 64))).astype(np.float32)
+    F /= np.linalg.norm(F, axis=1, keepdims=True)
+    F[rng.integers(0, len(F), 40)] = F[rng.integers(0, len(F), 40)]
+    C = rng.integers(0, 60, (sum(sizes), 2)).astype(np.int32)
+    e = _engine(kc, tc=0, micro=0)
+    e.upload(F, C, sizes, (64, 64))
+    for nq in (1, 2, 5, 16):
+        Q = (F[rng.integers(0, len(F), nq)] + 1e-3 * rng.standard_normal((nq, 64))).astype(np.float32)
+        Q = np.ascontiguousarray(Q.reshape(nq, 1, 64))
+        ref = oracle.retrieve(sizes, F, C, Q, 15)
+        for v in (1, 2, 0):
+            e.set_option("scan2", v)
+            e.query(Q, N=15, aggregate=True)
+            assert e.stat("used_tc") == 0
+            assert_candidates_equal(e.topk(), ref, f"kc {kc} nq {nq} scan2 {v}")
+            assert_estimates_equal(e.estimates(), ref, ctx=f"kc {kc} nq {nq} scan2 {v}")
+
+
 def test_aggregate_negative_tiles_and_grid_range():
     """Standalone Alg. 2 ranks tiles by count, then signed (y, x) ascending (R7) for
     any tile, negative ones included (ADVICE r01: the unbiased sort key put them last);
