@@ -1182,7 +1182,8 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         // few frames: the TMA-fed row-pair kernel for 1-2 frames per tile (it streams the coarse
         // plane faster: tools/scan3_sweep.py, 10M rows 0.121 vs 0.140 ms at 1 frame, 100M 0.916
         // vs 0.937), the row-pair f32x2 streaming kernel for more (4 frames: 1.10 vs 0.98 ms)
-        const bool kc3 = c->kc == 8 || c->kc == 16 || c->kc == 32, kc2 = kc3 || c->kc == 64;
+        // (scan3 bulk-copies whole 32-row tiles of the coarse plane: work items must start on one)
+        const bool kc3 = (c->kc == 8 || c->kc == 16 || c->kc == 32) && chunk % 32 == 0, kc2 = c->kc == 8 || c->kc == 16 || c->kc == 32 || c->kc == 64;
         if (qt <= 16 && kc3 && (c->opt_scan2 == 2 || (c->opt_scan2 == 1 && qt <= 2)))
             OL_LAUNCH(c, launch_scan3(c->kc, a, scan3_smem_bytes(qt, N, c->kc), (int)(n_items * n_qtiles), c->stream));
         else if (qt <= 16 && kc2 && c->opt_scan2)

@@ -321,18 +321,20 @@ def test_small_batch_cuda_core_kernels_vs_oracle(kc):
     F /= np.linalg.norm(F, axis=1, keepdims=True)
     F[rng.integers(0, len(F), 40)] = F[rng.integers(0, len(F), 40)]
     C = rng.integers(0, 60, (sum(sizes), 2)).astype(np.int32)
-    e = _engine(kc, tc=0, micro=0)
-    e.upload(F, C, sizes, (64, 64))
-    for nq in (1, 2, 5, 16):
-        Q = (F[rng.integers(0, len(F), nq)] + 1e-3 * rng.standard_normal((nq, 64))).astype(np.float32)
-        Q = np.ascontiguousarray(Q.reshape(nq, 1, 64))
-        ref = oracle.retrieve(sizes, F, C, Q, 15)
-        for v in (1, 2, 0):
-            e.set_option("scan2", v)
-            e.query(Q, N=15, aggregate=True)
-            assert e.stat("used_tc") == 0
-            assert_candidates_equal(e.topk(), ref, f"kc {kc} nq {nq} scan2 {v}")
-            assert_estimates_equal(e.estimates(), ref, ctx=f"kc {kc} nq {nq} scan2 {v}")
+    for chunk in (0, 100):   # (100: work items off the 32-row tiles -- scan3 then stands aside)
+        e = _engine(kc, tc=0, micro=0, chunk=chunk)
+        e.upload(F, C, sizes, (64, 64))
+        for nq in (1, 2, 5, 16):
+            Q = (F[rng.integers(0, len(F), nq)] + 1e-3 * rng.standard_normal((nq, 64))).astype(np.float32)
+            Q = np.ascontiguousarray(Q.reshape(nq, 1, 64))
+            ref = oracle.retrieve(sizes, F, C, Q, 15)
+            for v in (1, 2, 0):
+                e.set_option("scan2", v)
+                e.query(Q, N=15, aggregate=True)
+                assert e.stat("used_tc") == 0
+                ctx = f"kc {kc} chunk {chunk} nq {nq} scan2 {v}"
+                assert_candidates_equal(e.topk(), ref, ctx)
+                assert_estimates_equal(e.estimates(), ref, ctx=ctx)
 
 
 def test_aggregate_negative_tiles_and_grid_range():
