@@ -56,6 +56,24 @@ def one_case(rng, idx):
         opts["tau_seed"] = 0
     if rng.random() < 0.15:
         opts["tc"] = 0
+    # schedule / kernel-choice options (results never depend on them)
+    if rng.random() < 0.25:
+        opts["seed_kernel"] = int(rng.choice([0, 1]))
+    if rng.random() < 0.25:
+        opts["seed_samples"] = int(rng.choice([16, 300, 4096, 20000]))
+    if rng.random() < 0.2:
+        opts["cluster"] = int(rng.choice([2, 4]))
+    if rng.random() < 0.15:
+        opts["ctas"] = int(rng.choice([1, 37]))
+    if rng.random() < 0.2:
+        opts["scan2"] = int(rng.choice([0, 1, 2]))
+    if rng.random() < 0.15:
+        opts["tc_min_frames"] = int(rng.choice([1, 64, 100000]))
+        opts["tc"] = -1
+    if rng.random() < 0.15:
+        opts["merge_scan"] = 1
+    if rng.random() < 0.15:
+        opts["agg_block"] = 1
     e = ol.Engine(0, coarse_k=16)
     if os.environ.get("OL_POISON") == "1":
         e.set_option("poison", 1)
