@@ -180,6 +180,7 @@ struct MicroArgs {
     AggArgs agg;                            // cand / per_bundle / out / params of Algorithm 2
     unsigned long long *prof;               // profiling only (tc_debug & 32): phase cycles, or null
 };
+constexpr uint64_t kInlineMaxChunk = 8192;    // tensor-core scan: inline re-scoring for work items up to this many rows (C2: 4,096; C3: 13,568)
 constexpr uint64_t kMicroMaxRows = 8192;    // per subspace (64 KB of keys in shared memory)
 constexpr uint64_t kMicroMaxPairs = 1u << 16;   // frames x rows of the whole query
 size_t micro_smem_bytes(uint64_t max_rows, uint32_t split, uint32_t N, uint32_t agg_cap);
@@ -203,6 +204,7 @@ struct TcScanArgs {
     unsigned long long *stat_survivors;
     unsigned long long *stat_flagged;   // (frame, row tile) pairs that took the cold path
     uint32_t nq, n_items, n_qblocks, qb, n_sub, N, kc, stages;
+    uint32_t inline_rescore;      // 1: the epilogue warps re-score their own survivors (short items: C2-like)
     uint32_t dbg;                 // profiling only: 1 skip epilogue math, 2 skip MMA, 4 skip cold path, 8 drop
                                   // survivors, 16 / 32 counters, 64 keep the last thresholds, 128 stale rows,
                                   // 256 no threshold refresh

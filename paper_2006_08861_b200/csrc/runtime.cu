@@ -170,6 +170,7 @@ struct ol_ctx {
     uint32_t *bcount_d = nullptr; size_t bcount_cap = 0;   // NK10 per-bundle job counters (kept zero)
     bool used_micro = false;
     int64_t opt_micro = 1;
+    int64_t opt_inline = -1;     // tensor-core scan: epilogue warps re-score their own survivors (-1 auto: short items)
     int64_t opt_merge_scan = 0;  // 1: the merge's N-round scan over every key (tests: the fallback)
     int64_t opt_agg_block = 0;   // 1: Algorithm 2 by the CTA-wide kernel for bundles <= 32 too (tests)
     int32_t *agg_xy_d = nullptr; size_t agg_xy_cap = 0;
@@ -1147,7 +1148,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         a.partial = c->partial_d; a.stat_survivors = c->stat_d; a.stat_flagged = c->stat_d + 1;
         a.nq = nq; a.n_items = n_items; a.n_qblocks = n_qblocks; a.qb = qb; a.n_sub = c->n_sub;
         a.kf = c->tc_kf; a.pw = c->tc_pw;
-        a.N = N; a.kc = (uint32_t)c->kc; a.stages = tc_stages; a.dbg = (uint32_t)c->opt_tc_debug; a.prof = c->prof_d;
+        a.N = N; a.kc = (uint32_t)c->kc; a.stages = tc_stages; a.inline_rescore = c->opt_inline == 1 || (c->opt_inline == -1 && chunk <= kInlineMaxChunk); a.dbg = (uint32_t)c->opt_tc_debug; a.prof = c->prof_d;
         if (a.dbg & 32) OL_CUDA(c, cudaMemsetAsync(c->prof_d, 0, ((a.dbg & 2048) ? 1024 : 64) * sizeof(unsigned long long), c->stream));
         if (tc_seed && !(a.dbg & 64)) {
             // bound pre-pass: tensor-core scores of every S-th row give each (frame,
@@ -1746,6 +1747,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     else if (!strcmp(key, "micro")) { if (v != 0 && v != 1) goto bad; c->opt_micro = v; }
     else if (!strcmp(key, "agg_block")) { if (v != 0 && v != 1) goto bad; c->opt_agg_block = v; }
     else if (!strcmp(key, "merge_scan")) { if (v != 0 && v != 1) goto bad; c->opt_merge_scan = v; }
+    else if (!strcmp(key, "inline_rescore")) { if (v < -1 || v > 1) goto bad; c->opt_inline = v; }
     else if (!strcmp(key, "poison")) { if (v != 0 && v != 1) goto bad; c->opt_poison = v; }
     else return fail(c, OL_ERR_INVALID_ARGUMENT, "unknown option '%s'", key);
     ++c->gen;   // every option can change the launch sequence: retire a captured graph

@@ -175,6 +175,97 @@ __device__ __noinline__ void tc_warp_merge(u64 *L, uint32_t N, u64 key, int lane
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// Inline exact re-scoring (a.inline_rescore, short work items): one epilogue warp re-scores
+// its own survivors.  Lane l contributes the passing rows of its frame (masks mk0..3 over the
+// warp's 128 rows from rb); the warp re-scores them 32 at a time, one lane per (frame, row),
+// with the exact fp32 chain (R3; the second half of a row only while the chain is within the
+// frame's threshold), merges each frame's keys into its list under the frame's lock (the 4
+// epilogue warps of a frame share its list) and publishes the tightened threshold.  With
+// short items (C2: 16 tiles per CTA, 3 % of pairs surviving) the two exact warps were the
+// bottleneck; on long items the round trips on the epilogue's path cost more than they save.
+__device__ __noinline__ void tc_rescore_warp(const TcScanArgs &a, TcSmem &s, u64 *lists, const WorkItem &it,
+                                             uint32_t q0, uint32_t qbase, uint32_t mk0, uint32_t mk1, uint32_t mk2,
+                                             uint32_t mk3, uint32_t rb) {
+    constexpr uint32_t kAll = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const uint32_t N = a.N;
+    const uint32_t cnt = __popc(mk0) + __popc(mk1) + __popc(mk2) + __popc(mk3);
+    uint32_t incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(kAll, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const uint32_t total = __shfl_sync(kAll, incl, 31);
+    for (uint32_t base = 0; base < total; base += 32) {
+        const uint32_t sidx = base + lane;
+        uint32_t e = 0;   // owner lane: the first with incl > sidx
+        for (int j = 0; j < 32; ++j) e += __shfl_sync(kAll, incl, j) <= sidx;
+        const uint32_t es = min(e, 31u);
+        const uint32_t e_incl = __shfl_sync(kAll, incl, es), e_cnt = __shfl_sync(kAll, cnt, es);
+        const uint32_t w0 = __shfl_sync(kAll, mk0, es), w1 = __shfl_sync(kAll, mk1, es);
+        const uint32_t w2 = __shfl_sync(kAll, mk2, es), w3 = __shfl_sync(kAll, mk3, es);
+        const uint32_t col = qbase + es;   // frame within the CTA
+        u64 key = kPadKey;
+        if (sidx < total) {
+            uint32_t k = sidx - (e_incl - e_cnt), wsel = 0, w = w0;
+            if (k >= (uint32_t)__popc(w)) { k -= __popc(w); w = w1; wsel = 1;
+                if (k >= (uint32_t)__popc(w)) { k -= __popc(w); w = w2; wsel = 2;
+                    if (k >= (uint32_t)__popc(w)) { k -= __popc(w); w = w3; wsel = 3; } } }
+            const uint32_t bit = __fns(w, 0, (int)k + 1);
+            const uint32_t rl = rb + 32 * wsel + bit;
+            const uint64_t row = it.row_begin + rl;
+            if (OL_DCHECK(rl < it.count && col < kQB && q0 + col < a.nq)) {
+                const float4 *qv = reinterpret_cast<const float4 *>(a.queries + (size_t)(q0 + col) * kK);
+                const float tcur = __uint_as_float(lds_u32(&s.tau[col]));
+                float acc = 0.f;
+                float4 f[kK / 8];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (h == 1 && acc > tcur) break;
+#pragma unroll
+                    for (int kk = 0; kk < kK / 8; ++kk)
+                        f[kk] = __ldg(reinterpret_cast<const float4 *>(a.fine + fine_off(row, 4 * (h * (kK / 8) + kk))));
+#pragma unroll
+                    for (int kk = 0; kk < kK / 8; ++kk) {
+                        const float4 x = __ldg(qv + h * (kK / 8) + kk);
+                        acc = chain_step_tc(acc, x.x, f[kk].x); acc = chain_step_tc(acc, x.y, f[kk].y);
+                        acc = chain_step_tc(acc, x.z, f[kk].z); acc = chain_step_tc(acc, x.w, f[kk].w);
+                    }
+                }
+                key = ((u64)__float_as_uint(acc) << 32) | (u64)(it.frame_begin + rl);
+                if (acc > tcur || !(key < lists[(size_t)col * N + N - 1])) key = kPadKey;   // cannot enter the top-N
+            }
+        }
+        // (bit e: some lane holds a key of owner e's frame) one warp-wide merge per frame, locked
+        const uint32_t frames = __reduce_or_sync(kAll, key != kPadKey ? (1u << es) : 0u);
+        for (uint32_t fb = frames; fb; fb &= fb - 1) {
+            const uint32_t eo = (uint32_t)(__ffs(fb) - 1), f = qbase + eo;
+            if (lane == 0) {
+                while (atomicCAS(&s.lock[f], 0, 1) != 0) __nanosleep(32);
+                __threadfence_block();
+            }
+            __syncwarp();
+            u64 *L = lists + (size_t)f * N;
+            tc_warp_merge(L, N, es == eo ? key : kPadKey, lane);
+            if (lane == 0) {
+                const u64 last = L[N - 1];
+                __threadfence_block();
+                atomicExch(&s.lock[f], 0);
+                if (last != kPadKey) {   // publish this frame's tightened threshold
+                    const uint32_t tb = (uint32_t)(last >> 32);
+                    atomicMin(&s.tau[f], tb);
+                    const size_t ti = (size_t)(q0 + f) * a.n_sub + it.sub;
+                    atomicMin(&a.g_tau[ti], tb);
+                    for (uint32_t pr = 0; pr < a.n_peer; ++pr) atomicMin(&a.peer_tau[pr][ti], tb);   // (RED over NVLink)
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (lane == 0 && a.stat_survivors) atomicAdd(a.stat_survivors, (unsigned long long)total);
+}
+
+
 // max over 32 accumulator columns into two running maxima
 __device__ __forceinline__ void max32(const uint32_t (&v)[32], float &m0, float &m1) {
 #pragma unroll
@@ -191,7 +282,7 @@ __device__ __forceinline__ uint32_t mask32(const uint32_t (&v)[32], float h, int
     return m;
 }
 
-template <bool kProf, bool kBound, bool kPair>
+template <bool kProf, bool kBound, bool kPair, bool kInline = false>
 __global__ void __launch_bounds__(kTcThreads, 1)
 tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constant__ CUtensorMap map_q, TcScanArgs a) {
     extern __shared__ __align__(1024) unsigned char raw[];
@@ -488,7 +579,12 @@ tcscan_kernel(const __grid_constant__ CUtensorMap map_rows, const __grid_constan
                 if (prof && lane == 0) ew_math += clock64() - w2;
                 // cold path (rare): enqueue exactly the passing columns; columns past the
                 // item's last row (last tile only) are excluded by the masks
-                if (any) {
+                if constexpr (kInline) {   // (a separate instantiation: the call's ABI costs the others registers)
+                    if (__any_sync(0xffffffffu, any)) {
+                        if (a.stat_flagged && any) atomicAdd(a.stat_flagged, 1ull);
+                        tc_rescore_warp(a, s, lists, it, q0, quarter * 32, mk0, mk1, mk2, mk3, rb);
+                    }
+                } else if (any) {
                     const long long e0 = clock64();
                     const uint32_t cnt = __popc(mk0) + __popc(mk1) + __popc(mk2) + __popc(mk3);
                     if (cnt) tc_enqueue_event(s, mk0, mk1, mk2, mk3, rb, ql, prof ? a.prof : nullptr);
@@ -856,6 +952,7 @@ cudaError_t launch_tcscan(const CUtensorMap &map_rows, const CUtensorMap &map_q,
     const bool pair = a.pair && !a.bound;
     auto kern = a.bound ? (prof ? tcscan_kernel<true, true, false> : tcscan_kernel<false, true, false>)
               : pair    ? (prof ? tcscan_kernel<true, false, true> : tcscan_kernel<false, false, true>)
+              : a.inline_rescore ? (prof ? tcscan_kernel<true, false, false, true> : tcscan_kernel<false, false, false, true>)
                         : (prof ? tcscan_kernel<true, false, false> : tcscan_kernel<false, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -192,3 +192,27 @@ def test_tc_narrow_plane_large_and_small_N(N, nq):
         e = _run(F, C, sizes, Q, N, 1, agg=False, pair=pair, tc_k=32)
         assert e.stat("used_tc") == 1 and e.stat("tc_k") == 32
         assert_candidates_equal(e.topk(), ref, f"N={N} nq={nq} pair={pair}")
+
+
+@pytest.mark.parametrize("N", [5, 15, 40, 128])
+def test_tc_inline_rescore(N):
+    """Short work items (C2-like: a small database, many frames) re-score survivors in the
+    epilogue warps themselves (per-frame list locks; option inline_rescore, automatic for work
+    items of <= 8,192 rows); forced on and off, on paper-shaped and adversarial (flat-spectrum,
+    duplicated) data, the results equal the oracle."""
+    spec = synthgen.Spec(seed=77, n_floors=1, paths=5, frames_per_path=900)
+    F, C = synthgen.db_host(spec)
+    sizes = [900] * 5
+    V = synthgen.render_host(spec, synthgen.query_points(spec, 13, 700))["desc"]
+    Q = np.ascontiguousarray(V[:695].reshape(139, 5, 64))
+    G = synthgen.gflat(3000, seed=5, dup_frac=0.1)
+    Cg = np.random.default_rng(6).integers(0, 500, (3000, 2)).astype(np.int32)
+    Qg = np.ascontiguousarray((G[np.random.default_rng(7).integers(0, 3000, 300)] + 1e-3).astype(np.float32).reshape(300, 1, 64))
+    for (FF, CC, ss, QQ, grid) in ((F, C, sizes, Q, spec.grid()), (G, Cg, [1000, 2000], Qg, (4096, 4096))):
+        ref = oracle.retrieve(ss, FF, CC, QQ, N)
+        for v in (1, 0, -1):
+            e = _run(FF, CC, ss, QQ, N, 1, grid, inline_rescore=v)
+            assert e.stat("used_tc") == 1 or N == 128
+            assert_candidates_equal(e.topk(), ref, f"N={N} inline={v}")
+            assert_estimates_equal(e.estimates(), ref, ctx=f"N={N} inline={v}")
+            e.close()
