@@ -86,6 +86,16 @@ def main(n_fuzz: int):
         assert e.stat("used_tc") == 1 and e.stat("used_pair") == (1 if pair else 0)
         assert_candidates_equal(e.topk(), oracle.retrieve([1500, 1500], F, C, Qt, 9), f"tc k{tck} pair{pair}")
         done.append(f"tcscan k{tck} pair{pair}")
+    # inline exact re-scoring in the epilogue (short work items; per-frame list locks)
+    e = ol.Engine(0)
+    e.set_option("tc", 1); e.set_option("inline_rescore", 1)
+    e.upload(F, C, [1500, 1500], spec.grid())
+    Qt = np.ascontiguousarray(V[:70][:, None, :])
+    e.query(Qt, N=9, aggregate=True)
+    assert e.stat("used_tc") == 1
+    ref = oracle.retrieve([1500, 1500], F, C, Qt, 9)
+    assert_candidates_equal(e.topk(), ref, "tc inline"); assert_estimates_equal(e.estimates(), ref, ctx="tc inline")
+    done.append("tcscan inline")
     # world-2 logical shards: payload + merge_ranks + candidates; and the emulated p2p kernel
     Qs = np.ascontiguousarray(V[:20][:, None, :])
     ref = oracle.retrieve([1500, 1500], F, C, Qs, 7)
