@@ -854,8 +854,11 @@ if __name__ == "__main__":
     if args.impl != "reference" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(_spawn_ranks(args.gpus))
     if os.environ.get("OL_BENCH_RANK_PROBE"):   # tests: the launch plumbing only, no GPU work
-        print(json.dumps({"rank": int(os.environ.get("RANK", "0")), "world": int(os.environ.get("WORLD_SIZE", "1")),
-                          "gpus": args.gpus}), flush=True)
+        # (one write per line: the ranks share the pipe, and print's separate newline write
+        # could interleave with another rank's line)
+        sys.stdout.write(json.dumps({"rank": int(os.environ.get("RANK", "0")),
+                                     "world": int(os.environ.get("WORLD_SIZE", "1")), "gpus": args.gpus}) + "\n")
+        sys.stdout.flush()
         sys.exit(0 if int(os.environ.get("WORLD_SIZE", "1")) == args.gpus else 3)
     if args.impl == "reference":
         run_reference(args)
