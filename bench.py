@@ -172,6 +172,13 @@ def _spawn_ranks(n_gpus: int) -> int:
     return subprocess.call(cmd)
 
 
+def _emit(out: dict) -> None:
+    """The bench's one JSON line, written with a single write (other ranks' output may share
+    the stream)."""
+    sys.stdout.write(json.dumps(out) + "\n")
+    sys.stdout.flush()
+
+
 def _dist_init(n_gpus):
     import torch
     import torch.distributed as dist
@@ -536,7 +543,7 @@ def run_omniloc(a):
     if rank == 0 and world == 1 and not a.no_cpu:
         out["cpu_baseline"] = cpu_baseline(F, C, Qd, cfg, n_total)
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        _emit(out)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
@@ -750,7 +757,7 @@ def run_streaming(a):
     if cap is not None:
         out["capacity"] = cap
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        _emit(out)
 
 
 def _capacity(eng, spec, params, M, fps, secs=2.0, budget_ms=33.0):
@@ -846,7 +853,7 @@ def run_reference(a):
                             "sample": f"1 query frame per step x first {S:,} of {n_total:,} DB rows "
                                       f"(rate scaled by {S:,}/{n_total:,})"},
            "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    _emit(out)
 
 
 if __name__ == "__main__":
