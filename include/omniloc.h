@@ -436,11 +436,11 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *                   sequence; not used when "tc", "chunk" or "qtile" force a path or schedule
  *   "agg_block"     0 (default) / 1: tests: Algorithm 2 by the CTA-wide kernel for bundles of
  *                   <= 32 candidates too (default: one warp, shuffles only); same results
- *   "inline_rescore" -1 (default: for work items of <= 8,192 rows) / 1 / 0: the tensor-core
+ *   "inline_rescore" -1 (default: when the subspaces average <= 65,536 rows) / 1 / 0: the tensor-core
  *                   scan's epilogue warps re-score their own survivors (per-frame list locks)
  *                   instead of queueing them to the two exact warps -- for small databases
- *                   with many frames (C2: 1.61 -> 1.00 ms), not for long items (C3: 0.39 ->
- *                   0.70 ms); single CTAs only (CTA pairs keep the exact warps)
+ *                   (many small subspaces: C2 1.61 -> 1.00 ms), not for large ones (C3:
+ *                   0.39 -> 0.70 ms); single CTAs only (CTA pairs keep the exact warps)
  *   "merge_scan"    0 (default) / 1: tests: the per-rank merge takes its fallback (N rounds of
  *                   a CTA-wide minimum over every work-item list) instead of gathering the keys
  *                   <= min over lists of list[N-1]; same results

@@ -180,7 +180,11 @@ struct MicroArgs {
     AggArgs agg;                            // cand / per_bundle / out / params of Algorithm 2
     unsigned long long *prof;               // profiling only (tc_debug & 32): phase cycles, or null
 };
-constexpr uint64_t kInlineMaxChunk = 8192;    // tensor-core scan: inline re-scoring for work items up to this many rows (C2: 4,096; C3: 13,568)
+// tensor-core scan: inline re-scoring when the subspaces average at most this many rows -- many
+// small subspaces (per-subspace top-N) leave 0.5-3 % of pairs to the exact path, which the two
+// exact warps cannot absorb (C2, 4,000 rows: 1.61 -> 1.00 ms; C3 split 50 ways, 20,000: 3.07 ->
+// 2.51 ms); with 200,000 (C3 in 5) or more rows per subspace the queue wins (0.82 vs 1.33 ms)
+constexpr uint64_t kInlineMaxRowsPerSub = 65536;
 constexpr uint64_t kMicroMaxRows = 8192;    // per subspace (64 KB of keys in shared memory)
 constexpr uint64_t kMicroMaxPairs = 1u << 16;   // frames x rows of the whole query
 size_t micro_smem_bytes(uint64_t max_rows, uint32_t split, uint32_t N, uint32_t agg_cap);

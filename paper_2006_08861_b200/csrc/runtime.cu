@@ -1148,7 +1148,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         a.partial = c->partial_d; a.stat_survivors = c->stat_d; a.stat_flagged = c->stat_d + 1;
         a.nq = nq; a.n_items = n_items; a.n_qblocks = n_qblocks; a.qb = qb; a.n_sub = c->n_sub;
         a.kf = c->tc_kf; a.pw = c->tc_pw;
-        a.N = N; a.kc = (uint32_t)c->kc; a.stages = tc_stages; a.inline_rescore = c->opt_inline == 1 || (c->opt_inline == -1 && chunk <= kInlineMaxChunk); a.dbg = (uint32_t)c->opt_tc_debug; a.prof = c->prof_d;
+        a.N = N; a.kc = (uint32_t)c->kc; a.stages = tc_stages; a.inline_rescore = c->opt_inline == 1 || (c->opt_inline == -1 && c->rows <= (uint64_t)c->n_sub * kInlineMaxRowsPerSub); a.dbg = (uint32_t)c->opt_tc_debug; a.prof = c->prof_d;
         if (a.dbg & 32) OL_CUDA(c, cudaMemsetAsync(c->prof_d, 0, ((a.dbg & 2048) ? 1024 : 64) * sizeof(unsigned long long), c->stream));
         if (tc_seed && !(a.dbg & 64)) {
             // bound pre-pass: tensor-core scores of every S-th row give each (frame,

@@ -64,6 +64,7 @@ def test_tc_adversarial(seed):
     N = int(rng.choice([5, 15, 33]))
     ref = oracle.retrieve(sizes, F, C, Q, N)
     opts = {"tau_seed": 0} if seed % 3 == 0 else {}
+    opts["inline_rescore"] = [-1, 0][seed % 2]   # (small databases default to inline re-scoring)
     e = _run(F, C, sizes, Q, N, 1, **opts)
     assert e.stat("used_tc") == 1
     assert_candidates_equal(e.topk(), ref, f"seed {seed}")
@@ -198,7 +199,7 @@ def test_tc_narrow_plane_large_and_small_N(N, nq):
 def test_tc_inline_rescore(N):
     """Short work items (C2-like: a small database, many frames) re-score survivors in the
     epilogue warps themselves (per-frame list locks; option inline_rescore, automatic for work
-    items of <= 8,192 rows); forced on and off, on paper-shaped and adversarial (flat-spectrum,
+    subspaces averaging <= 65,536 rows); forced on and off, on paper-shaped and adversarial (flat-spectrum,
     duplicated) data, the results equal the oracle."""
     spec = synthgen.Spec(seed=77, n_floors=1, paths=5, frames_per_path=900)
     F, C = synthgen.db_host(spec)

@@ -74,7 +74,7 @@ def one_case(rng, idx):
         opts["merge_scan"] = 1
     if rng.random() < 0.15:
         opts["agg_block"] = 1
-    if rng.random() < 0.2:
+    if rng.random() < 0.5:
         opts["inline_rescore"] = int(rng.choice([0, 1]))
     e = ol.Engine(0, coarse_k=16)
     if os.environ.get("OL_POISON") == "1":
