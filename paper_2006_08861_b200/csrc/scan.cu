@@ -656,12 +656,19 @@ constexpr int kSeedFrames = 32;
 
 template <int KC>
 __global__ void __launch_bounds__(256) seed_acc_kernel(SeedArgs a) {
-    __shared__ alignas(16) float qs[kSeedFrames][kK];
+    // frames as interleaved pairs: qd[p][k] = (q_{2p}[k], q_{2p+1}[k]), so one f32x2 FADD2 + FFMA2
+    // advances two frames' chains (each lane of the pair the exact RN fp32 step of R3)
+    __shared__ alignas(16) uint64_t qd[kSeedFrames / 2][kK];
     const uint32_t isp = blockIdx.x;                     // (subspace, split)
     const uint32_t i = isp / a.splits, split = isp % a.splits;
     const uint32_t f0 = blockIdx.z * kSeedFrames;
     const uint32_t nf = min((uint32_t)kSeedFrames, a.nq - f0);
-    for (uint32_t t = threadIdx.x; t < nf * kK; t += blockDim.x) qs[t / kK][t % kK] = a.queries[(size_t)f0 * kK + t];
+    for (uint32_t t = threadIdx.x; t < (kSeedFrames / 2) * kK; t += blockDim.x) {
+        const uint32_t p = t / kK, k = t % kK;
+        const float lo = 2 * p < nf ? a.queries[(size_t)(f0 + 2 * p) * kK + k] : 0.f;
+        const float hi = 2 * p + 1 < nf ? a.queries[(size_t)(f0 + 2 * p + 1) * kK + k] : 0.f;
+        qd[p][k] = f2pack(lo, hi);
+    }
     __syncthreads();
     const SubInfo si = a.subs[i];
     const uint32_t S = (uint32_t)min((uint64_t)a.samples, si.count);
@@ -673,36 +680,31 @@ __global__ void __launch_bounds__(256) seed_acc_kernel(SeedArgs a) {
 #pragma unroll
     for (int k4 = 0; k4 < kK / 4; ++k4)
         f[k4] = __ldg(reinterpret_cast<const float4 *>(a.fine + fine_off(row, 4 * k4)));
-    // two frames at a time: two independent fixed-order chains in flight per thread (a single
-    // chain issues one FFMA per 4-cycle latency)
     const size_t fstride = (size_t)a.n_sub * a.splits * a.samples;
     uint32_t *out = a.scratch + ((size_t)f0 * a.n_sub + i) * a.splits * a.samples + (size_t)split * a.samples + smp;
-    uint32_t j = 0;
-    for (; j + 1 < nf; j += 2) {
-        const float4 *qa = reinterpret_cast<const float4 *>(qs[j]);
-        const float4 *qb = reinterpret_cast<const float4 *>(qs[j + 1]);
-        float acc0 = 0.f, acc1 = 0.f;
+    // four frames at a time: two f32x2 chains in flight
+    for (uint32_t p = 0; 2 * p < nf; p += 2) {
+        const ulonglong2 *qa = reinterpret_cast<const ulonglong2 *>(qd[p]);
+        const ulonglong2 *qb = reinterpret_cast<const ulonglong2 *>(qd[p + 1 < kSeedFrames / 2 ? p + 1 : p]);
+        uint64_t acc0 = 0, acc1 = 0;
 #pragma unroll
         for (int k4 = 0; k4 < kK / 4; ++k4) {
-            const float4 x = qa[k4], y = qb[k4];
-            acc0 = chain_step(acc0, x.x, f[k4].x); acc1 = chain_step(acc1, y.x, f[k4].x);
-            acc0 = chain_step(acc0, x.y, f[k4].y); acc1 = chain_step(acc1, y.y, f[k4].y);
-            acc0 = chain_step(acc0, x.z, f[k4].z); acc1 = chain_step(acc1, y.z, f[k4].z);
-            acc0 = chain_step(acc0, x.w, f[k4].w); acc1 = chain_step(acc1, y.w, f[k4].w);
-        }
-        out[j * fstride] = __float_as_uint(acc0);
-        out[(j + 1) * fstride] = __float_as_uint(acc1);
-    }
-    if (j < nf) {
-        const float4 *q4 = reinterpret_cast<const float4 *>(qs[j]);
-        float acc = 0.f;
+            const float fv[4] = {f[k4].x, f[k4].y, f[k4].z, f[k4].w};
 #pragma unroll
-        for (int k4 = 0; k4 < kK / 4; ++k4) {
-            const float4 x = q4[k4];
-            acc = chain_step(acc, x.x, f[k4].x); acc = chain_step(acc, x.y, f[k4].y);
-            acc = chain_step(acc, x.z, f[k4].z); acc = chain_step(acc, x.w, f[k4].w);
+            for (int c = 0; c < 2; ++c) {
+                const ulonglong2 x = qa[2 * k4 + c], y = qb[2 * k4 + c];
+                const uint64_t fa = f2pack(fv[2 * c], fv[2 * c]), fb = f2pack(fv[2 * c + 1], fv[2 * c + 1]);
+                uint64_t d = f2sub(x.x, fa); acc0 = f2fma(d, d, acc0);
+                d = f2sub(y.x, fa); acc1 = f2fma(d, d, acc1);
+                d = f2sub(x.y, fb); acc0 = f2fma(d, d, acc0);
+                d = f2sub(y.y, fb); acc1 = f2fma(d, d, acc1);
+            }
         }
-        out[j * fstride] = __float_as_uint(acc);
+        const uint32_t j = 2 * p;
+        out[j * fstride] = (uint32_t)acc0;
+        if (j + 1 < nf) out[(j + 1) * fstride] = (uint32_t)(acc0 >> 32);
+        if (j + 2 < nf) out[(j + 2) * fstride] = (uint32_t)acc1;
+        if (j + 3 < nf) out[(j + 3) * fstride] = (uint32_t)(acc1 >> 32);
     }
 }
 
