@@ -1,3 +1,4 @@
+"""C2 (20k rows in 5 path subspaces, 1,000 bundles of M = 5, Alg. 2): scan paths and coarse widths (tc auto vs CUDA-core kc 0 / 8 / 32, qtile 32)."""
 import sys, torch
 sys.path.insert(0, '.')
 import synthgen, paper_2006_08861_b200 as ol
