@@ -508,8 +508,7 @@ def run_omniloc(a):
         e0.record(stream)
         for _ in range(a.steps):
             eng.query(Q3h.numpy(), params=params, aggregate=True)   # H2D inside (pinned host)
-            eng.topk_into(res)                                        # D2H of the candidates ...
-            eng.estimates_into(est)                                   # ... and of the Alg. 2 estimates
+            eng.results_into(res, est)   # D2H of the candidates and the Alg. 2 estimates, one sync
         e1.record(stream)
         torch.cuda.synchronize()
         wall = (time.perf_counter() - t0) / a.steps * 1e3

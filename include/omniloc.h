@@ -295,6 +295,15 @@ OL_API ol_status ol_topk_device(ol_ctx *ctx, const ol_candidate **dev_ptr, uint6
  * NOT_READY, CUDA. */
 OL_API ol_status ol_get_estimates(ol_ctx *ctx, ol_estimate *out, uint32_t capacity);
 
+/* Both at once with ONE stream synchronisation (the latency configurations: a second
+ * D2H + sync costs ~15 us on a 20 us query): the candidates as ol_get_topk into
+ * cand_out (cand_capacity) and, when the query aggregated and est_out is non-NULL,
+ * the n_bundles estimates as ol_get_estimates into est_out (est_capacity).
+ * *written = the candidate count.  Errors: those of ol_get_topk / ol_get_estimates
+ * (EMPTY only if est_out is non-NULL and aggregation was not requested). */
+OL_API ol_status ol_get_results(ol_ctx *ctx, ol_candidate *cand_out, uint64_t cand_capacity, uint64_t *written,
+                                ol_estimate *est_out, uint32_t est_capacity);
+
 /* ---- standalone pieces --------------------------------------------------- */
 
 /* Algorithm 2 alone on caller-provided candidate tiles: bundle b owns

@@ -116,6 +116,7 @@ def lib():
             "ol_get_topk": ([P, P, u64, ctypes.POINTER(u64)], i32),
             "ol_topk_device": ([P, ctypes.POINTER(P), ctypes.POINTER(u64)], i32),
             "ol_get_estimates": ([P, P, u32], i32),
+            "ol_get_results": ([P, P, u64, ctypes.POINTER(u64), P, u32], i32),
             "ol_aggregate": ([P, u32, P, P, i32, ctypes.POINTER(ol_params), P], i32),
             "ol_select_window": ([u32, u32, u32, ctypes.POINTER(u32), ctypes.POINTER(u32)], i32),
             "ol_set_option": ([P, ctypes.c_char_p, i64], i32),
@@ -411,6 +412,16 @@ class Engine:
         self._ck(lib().ol_get_estimates(self._h, ctypes.c_void_p(pinned.data_ptr()),
                                         pinned.numel() // ESTIMATE_DTYPE.itemsize))
         return B * ESTIMATE_DTYPE.itemsize
+
+    def results_into(self, cand_pinned, est_pinned=None) -> tuple:
+        """D2H of the candidates and (if given) the estimates into (pinned) torch uint8 host
+        tensors with one synchronisation (ol_get_results); returns (candidate, estimate) bytes."""
+        w = ctypes.c_uint64()
+        est_p = ctypes.c_void_p(est_pinned.data_ptr()) if est_pinned is not None else None
+        est_cap = est_pinned.numel() // ESTIMATE_DTYPE.itemsize if est_pinned is not None else 0
+        self._ck(lib().ol_get_results(self._h, ctypes.c_void_p(cand_pinned.data_ptr()),
+                                      cand_pinned.numel() // CANDIDATE_DTYPE.itemsize, ctypes.byref(w), est_p, est_cap))
+        return w.value * CANDIDATE_DTYPE.itemsize, (self._last[0] * ESTIMATE_DTYPE.itemsize if est_pinned is not None else 0)
 
     def topk_device(self):
         """(device pointer, count) of the candidate array (owned by the engine)."""

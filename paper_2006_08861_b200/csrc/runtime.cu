@@ -1488,6 +1488,28 @@ ol_status ol_get_estimates(ol_ctx *c, ol_estimate *out, uint32_t capacity) {
     return check_flags(c);
 }
 
+ol_status ol_get_results(ol_ctx *c, ol_candidate *cand_out, uint64_t cand_capacity, uint64_t *written,
+                         ol_estimate *est_out, uint32_t est_capacity) {
+    if (!c) return fail(nullptr, OL_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!c->finalized) return fail(c, OL_ERR_NOT_READY, "no finalized query");
+    if (!cand_out || cand_capacity < c->n_cand)
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "capacity %llu < %llu candidates",
+                    (unsigned long long)cand_capacity, (unsigned long long)c->n_cand);
+    if (est_out && !c->aggregate) return fail(c, OL_ERR_EMPTY, "aggregation was not requested");
+    if (est_out && est_capacity < c->nb)
+        return fail(c, OL_ERR_INVALID_ARGUMENT, "capacity %u < %u bundles", est_capacity, c->nb);
+    OL_CUDA(c, cudaSetDevice(c->device));
+    OL_CUDA(c, cudaMemcpyAsync(cand_out, c->cand_d, sizeof(ol_candidate) * c->n_cand, cudaMemcpyDeviceToHost,
+                               c->stream));
+    if (est_out)
+        OL_CUDA(c, cudaMemcpyAsync(est_out, c->est_d, sizeof(ol_estimate) * c->nb, cudaMemcpyDeviceToHost,
+                                   c->stream));
+    ol_status st = check_flags(c);   // (one synchronisation for both copies)
+    if (st) return st;
+    if (written) *written = c->n_cand;
+    return OL_OK;
+}
+
 ol_status ol_aggregate(ol_ctx *c, uint32_t nb, const uint32_t *offsets, const int32_t *xy,
                        int32_t on_device, const ol_params *p, ol_estimate *out) {
     NvtxRange nv("ol_aggregate");

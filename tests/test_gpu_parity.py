@@ -560,3 +560,28 @@ def test_micro_kernel_small_queries_vs_oracle(seed):            # NK10, the late
     e.query(Q, N=N, aggregate=True)
     assert e.stat("used_micro") == 0
     assert e.topk().tobytes() == got.tobytes() and e.estimates().tobytes() == est.tobytes()
+
+
+def test_get_results_one_fetch():
+    """ol_get_results copies the candidates and the estimates with one synchronisation: the
+    same bytes as ol_get_topk + ol_get_estimates; EMPTY when estimates are asked of a query
+    that did not aggregate; INVALID_ARGUMENT for short buffers."""
+    import torch
+    cfg = synthgen.CONFIGS["C1"]
+    F, C = synthgen.db_host(cfg.spec)
+    Q = synthgen.render_host(cfg.spec, synthgen.query_points(cfg.spec, 11, 3))["desc"][:, None, :]
+    e = _engine(16)
+    e.upload(F, C, cfg.subspace_sizes, cfg.spec.grid())
+    e.query(Q, N=cfg.N, aggregate=True)
+    got, est = e.topk(), e.estimates()
+    res = torch.empty(len(got) * ol.CANDIDATE_DTYPE.itemsize, dtype=torch.uint8)
+    es = torch.empty(len(est) * ol.ESTIMATE_DTYPE.itemsize, dtype=torch.uint8)
+    nb, ne = e.results_into(res, es)
+    assert nb == res.numel() and ne == es.numel()
+    assert res.numpy().tobytes() == got.tobytes() and es.numpy().tobytes() == est.tobytes()
+    assert e.results_into(res)[0] == res.numel()                      # candidates only
+    with pytest.raises(ol.OmnilocError, match="INVALID_ARGUMENT"):
+        e.results_into(res[: res.numel() - 1], es)
+    e.query(Q, N=cfg.N, aggregate=False)
+    with pytest.raises(ol.OmnilocError, match="EMPTY"):
+        e.results_into(res, es)
