@@ -81,13 +81,19 @@ int main(void) {
     CHECK(ol_get_topk(ctx, got, n, &w));
     ol_estimate est[NB];
     CHECK(ol_get_estimates(ctx, est, NB));
+    /* the one-synchronisation fetch gives the same bytes */
+    ol_candidate *got2 = malloc(sizeof(ol_candidate) * n);
+    ol_estimate est2[NB];
+    uint64_t w2 = 0;
+    CHECK(ol_get_results(ctx, got2, n, &w2, est2, NB));
+    const int same = w2 == n && !memcmp(got, got2, sizeof(ol_candidate) * n) && !memcmp(est, est2, sizeof(est));
 
     /* the oracle on the same inputs */
     uint32_t *os = malloc(4 * n), *of = malloc(4 * n), *ob = malloc(4 * n), *oq = malloc(4 * n);
     float *oa = malloc(4 * n), *od = malloc(4 * n);
     int32_t *ox = malloc(4 * n), *oy = malloc(4 * n);
     const int64_t m = oracle_retrieve(2, sizes64, F, C, K, NB, M, Q, N, 0, os, of, ob, oq, oa, od, ox, oy, (int64_t)n);
-    int bad = (m != (int64_t)n) || (w != n) || nccl != 1;
+    int bad = (m != (int64_t)n) || (w != n) || nccl != 1 || !same;
     for (uint64_t i = 0; !bad && i < n; ++i) {
         uint32_t ga, ra, gd, rd;
         memcpy(&ga, &got[i].dist2, 4); memcpy(&ra, &oa[i], 4);
