@@ -72,6 +72,10 @@ def _args():
 # 2 x 256-column buffers, FMNMX3 math); round 1's probe (841) had a serial-chain epilogue
 PIPE_PROBE = {32: 456}
 
+# binary64 DADD + DMUL + DFMA thread instructions per profile of fft_extract_kernel<8> (W = 256),
+# counted by ncu on the final kernel (706M + 2,263M + 5,447M over 1,048,576 profiles)
+FFT_FP64_OPS_PER_PROFILE = 8024
+
 
 class Clocks:
     """SM clock and clock-event (throttle) reasons sampled DURING the timed region
@@ -483,14 +487,23 @@ def run_omniloc(a):
         ims = e0.elapsed_time(e1) / reps
         ib = Wp * 8 + 64 * 4 + 1    # profile in (binary64), fp32 descriptor + degenerate flag out
         igbs = n_in * ib / (ims / 1e3) / 1e9
+        # FP64 arithmetic per profile (DADD + DMUL + DFMA thread instructions; ncu on the final
+        # kernel, profiles/r02_summary.md): the binding resource -- the fp64 pipe is ~50 % busy,
+        # HBM at ~0.23.  Peak: 64 DFMA lanes per SM (ncu sm__sass_thread_inst_executed_op_dfma
+        # peak_sustained) x 148 SMs x the max SM clock
+        fp64_ops = FFT_FP64_OPS_PER_PROFILE
+        fp64_peak = 148 * 64 * sm_max * 1e6 / 1e12
+        fp64_ach = n_in * fp64_ops / (ims / 1e3) / 1e12
         out["ingest"] = {"kernel": "fft_extract_kernel<8>", "profiles": n_in, "W": Wp, "ms": ims,
                          "profiles_per_s": n_in / (ims / 1e3), "hbm_bytes_per_profile": ib,
-                         "roofline": {"bound": "hbm", "achieved": igbs, "peak": hbm_peak, "unit": "GB/s",
-                                      "frac": igbs / hbm_peak,
-                                      "peak_source": "MEASURED_PEAKS hbm_gbs (copy)",
-                                      "note": "FFT (P:121): ~12.8k binary64 operations per profile at W = 256, "
-                                              "vs 65.5k for the round-1 direct sum; the kernel is FP64-issue "
-                                              "bound: ncu fp64 pipe 50 % active (profiles/r02_summary.md)"}}
+                         "hbm_gbs": igbs, "hbm_frac": igbs / hbm_peak,
+                         "roofline": {"bound": "fp64", "achieved": fp64_ach, "peak": fp64_peak,
+                                      "unit": "T fp64 lane-instr/s", "frac": fp64_ach / fp64_peak,
+                                      "peak_source": f"148 SMs x 64 DFMA lanes x {sm_max:.0f} MHz",
+                                      "per_launch": {"fp64_lane_instr_per_profile": fp64_ops},
+                                      "note": "FFT (P:121): 8,024 binary64 DADD/DMUL/DFMA per profile at W = 256 "
+                                              "(65.5k for the round-1 direct sum); ncu: fp64 pipe 46-50 % active "
+                                              "(conversions and compares share it)"}}
         del prof
 
     # ------------------------------------------------ e2e through the public API, host buffers
