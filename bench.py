@@ -72,9 +72,10 @@ def _args():
 # 2 x 256-column buffers, FMNMX3 math); round 1's probe (841) had a serial-chain epilogue
 PIPE_PROBE = {32: 456}
 
-# binary64 DADD + DMUL + DFMA thread instructions per profile of fft_extract_kernel<8> (W = 256),
-# counted by ncu on the final kernel (706M + 2,263M + 5,447M over 1,048,576 profiles)
-FFT_FP64_OPS_PER_PROFILE = 8024
+# binary64 DADD + DMUL + DFMA thread instructions per profile of fft2_extract256_kernel (W = 256,
+# two profiles per warp), counted by ncu on the final kernel (1,109M + 1,457M + 3,132M over
+# 1,048,576 profiles; the one-profile-per-warp kernel needed 8,024)
+FFT_FP64_OPS_PER_PROFILE = 5433
 
 
 class Clocks:
@@ -494,16 +495,17 @@ def run_omniloc(a):
         fp64_ops = FFT_FP64_OPS_PER_PROFILE
         fp64_peak = 148 * 64 * sm_max * 1e6 / 1e12
         fp64_ach = n_in * fp64_ops / (ims / 1e3) / 1e12
-        out["ingest"] = {"kernel": "fft_extract_kernel<8>", "profiles": n_in, "W": Wp, "ms": ims,
+        out["ingest"] = {"kernel": "fft2_extract256_kernel", "profiles": n_in, "W": Wp, "ms": ims,
                          "profiles_per_s": n_in / (ims / 1e3), "hbm_bytes_per_profile": ib,
                          "hbm_gbs": igbs, "hbm_frac": igbs / hbm_peak,
                          "roofline": {"bound": "fp64", "achieved": fp64_ach, "peak": fp64_peak,
                                       "unit": "T fp64 lane-instr/s", "frac": fp64_ach / fp64_peak,
                                       "peak_source": f"148 SMs x 64 DFMA lanes x {sm_max:.0f} MHz",
                                       "per_launch": {"fp64_lane_instr_per_profile": fp64_ops},
-                                      "note": "FFT (P:121): 8,024 binary64 DADD/DMUL/DFMA per profile at W = 256 "
-                                              "(65.5k for the round-1 direct sum); ncu: fp64 pipe 46-50 % active "
-                                              "(conversions and compares share it)"}}
+                                      "note": "FFT (P:121), two real profiles per complex transform: 5,433 binary64 "
+                                              "DADD/DMUL/DFMA per profile at W = 256 (8,024 one per warp; 65.5k for "
+                                              "the round-1 direct sum); ncu: fp64 pipe 48 % active (conversions and "
+                                              "compares share it)"}}
         del prof
 
     # ------------------------------------------------ e2e through the public API, host buffers

@@ -207,6 +207,146 @@ fft_extract_kernel(const double *prof, uint64_t n, float *out32, double *out64, 
     }
 }
 
+// W = 256: TWO profiles per warp as one complex sequence z = a + i b (the real-input trick:
+// the FFT's twiddles and butterflies serve both), separated at the end by the symmetry of real
+// inputs: A[k] = (Z[k] + conj Z[W-k]) / 2, B[k] = (Z[k] - conj Z[W-k]) / 2i.  Lane l holds
+// z[l + 32 j]; an 8-point complex DFT per lane over j (radix-2 by hand), the twiddles, the
+// 32-point DIF across the lanes, then Z[W - k] fetched from the mirror lane (l ^ 31 for
+// k1 != 0).  About half the binary64 work per profile of fft_extract_kernel<8>.
+__global__ void __launch_bounds__(32 * kExtractWarps, 3)   // (3 CTAs per SM with ~48 B of spills: 870M vs 840M profiles/s at 2)
+fft2_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out64, uint8_t *degenerate, float *prof_out) {
+    constexpr uint32_t R = 8, W = 256;
+    __shared__ double tc[W], ts[W];   // cos / sin of 2 pi j / W
+    for (uint32_t j = threadIdx.x; j < W; j += blockDim.x) {
+        double sn, cs;
+        sincospi(2.0 * (double)j / (double)W, &sn, &cs);
+        tc[j] = cs;
+        ts[j] = sn;
+    }
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t k2 = __brev(lane) >> 27;                       // this lane's DIF output
+    const uint32_t src0 = __brev((32u - k2) & 31u) >> 27;         // the lane holding Z[W - 8 k2]
+    const uint64_t pairs = (n + 1) / 2;
+    for (uint64_t pp = (uint64_t)blockIdx.x * kExtractWarps + (threadIdx.x >> 5); pp < pairs;
+         pp += (uint64_t)gridDim.x * kExtractWarps) {
+        const uint64_t pa = 2 * pp, pb = pa + 1;
+        const bool hasb = pb < n;
+        double re[R], im[R];
+        double sa = 0.0, sb = 0.0;   // (the profiles' sums, for the stored profiles' means)
+        {   // 8-point complex DFT of z_j = xa_j + i xb_j (radix 2: even / odd outputs)
+            double xa[R], xb[R];
+#pragma unroll
+            for (int j = 0; j < (int)R; ++j) {
+                xa[j] = __ldg(&prof[pa * W + lane + 32 * j]);
+                xb[j] = hasb ? __ldg(&prof[pb * W + lane + 32 * j]) : 0.0;
+            }
+            if (prof_out) {
+#pragma unroll
+                for (int j = 0; j < (int)R; ++j) { sa += xa[j]; sb += xb[j]; }
+            }
+            constexpr double c = 0.70710678118654752440;   // cos(pi/4) = sin(pi/4), RN
+            double ar[4], ai[4], br[4], bi[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                ar[j] = xa[j] + xa[j + 4]; ai[j] = xb[j] + xb[j + 4];
+                br[j] = xa[j] - xa[j + 4]; bi[j] = xb[j] - xb[j + 4];
+            }
+            // even outputs: 4-point DFT of a
+            const double A0r = ar[0] + ar[2], A0i = ai[0] + ai[2], A2r = ar[0] - ar[2], A2i = ai[0] - ai[2];
+            const double A1r = ar[1] + ar[3], A1i = ai[1] + ai[3], A3r = ar[1] - ar[3], A3i = ai[1] - ai[3];
+            re[0] = A0r + A1r; im[0] = A0i + A1i;
+            re[4] = A0r - A1r; im[4] = A0i - A1i;
+            re[2] = A2r + A3i; im[2] = A2i - A3r;   // A2 - i A3
+            re[6] = A2r - A3i; im[6] = A2i + A3r;   // A2 + i A3
+            // odd outputs: t_j = b_j e^{-i pi j / 4}, then its 4-point DFT
+            const double t1r = c * (br[1] + bi[1]), t1i = c * (bi[1] - br[1]);
+            const double t2r = bi[2], t2i = -br[2];
+            const double t3r = c * (bi[3] - br[3]), t3i = -c * (bi[3] + br[3]);
+            const double B0r = br[0] + t2r, B0i = bi[0] + t2i, B2r = br[0] - t2r, B2i = bi[0] - t2i;
+            const double B1r = t1r + t3r, B1i = t1i + t3i, B3r = t1r - t3r, B3i = t1i - t3i;
+            re[1] = B0r + B1r; im[1] = B0i + B1i;
+            re[5] = B0r - B1r; im[5] = B0i - B1i;
+            re[3] = B2r + B3i; im[3] = B2i - B3r;   // B2 - i B3
+            re[7] = B2r - B3i; im[7] = B2i + B3r;   // B2 + i B3
+        }
+        // twiddle e^{-2 pi i l k1 / W}
+#pragma unroll
+        for (int k1 = 1; k1 < (int)R; ++k1) {
+            const uint32_t t = (lane * (uint32_t)k1) % W;
+            const double c = tc[t], sn = ts[t];
+            const double r = re[k1], i = im[k1];
+            re[k1] = fma(r, c, i * sn);
+            im[k1] = fma(i, c, -r * sn);
+        }
+        // 32-point radix-2 DIF across the lanes (branch-free, as fft_extract_kernel)
+#pragma unroll
+        for (int h = 16; h >= 1; h >>= 1) {
+            const bool lower = (lane & h) != 0;
+            const uint32_t e = (lane & (h - 1)) * (W / (2 * h));
+            const double c = lower ? tc[e] : 1.0, sn = lower ? ts[e] : 0.0;
+            const double sg = lower ? -1.0 : 1.0;
+#pragma unroll
+            for (int k1 = 0; k1 < (int)R; ++k1) {
+                const double pr = __shfl_xor_sync(0xffffffffu, re[k1], h);
+                const double pi = __shfl_xor_sync(0xffffffffu, im[k1], h);
+                const double dr = fma(sg, re[k1], pr), di = fma(sg, im[k1], pi);
+                re[k1] = lower ? fma(dr, c, di * sn) : dr;
+                im[k1] = lower ? fma(di, c, -dr * sn) : di;
+            }
+        }
+        // separate: Z[W - k] for k = k1 + 8 k2 is (8 - k1) + 8 (31 - k2) in lane l ^ 31 (k1 != 0),
+        // 8 ((32 - k2) mod 32) in lane src0 (k1 = 0); the magnitudes of bins 1..64
+        double ma[R], mb[R], n2a = 0.0, n2b = 0.0;
+#pragma unroll
+        for (int k1 = 0; k1 < (int)R; ++k1) {
+            const int m1 = k1 == 0 ? 0 : (int)R - k1;
+            const double qr = k1 == 0 ? __shfl_sync(0xffffffffu, re[0], src0) : __shfl_xor_sync(0xffffffffu, re[m1], 31);
+            const double qi = k1 == 0 ? __shfl_sync(0xffffffffu, im[0], src0) : __shfl_xor_sync(0xffffffffu, im[m1], 31);
+            const uint32_t k = (uint32_t)k1 + R * k2;
+            ma[k1] = mb[k1] = 0.0;
+            if (k >= 1 && k <= (uint32_t)kK) {
+                const double sr = re[k1] + qr, di = im[k1] - qi;   // 2 A[k]
+                const double si = im[k1] + qi, dr = re[k1] - qr;   // 2 i B[k] = (dr + i si): |.| = |2 B[k]|
+                ma[k1] = 0.5 * sqrt(sr * sr + di * di);
+                mb[k1] = 0.5 * sqrt(si * si + dr * dr);
+                n2a += ma[k1] * ma[k1];
+                n2b += mb[k1] * mb[k1];
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            n2a += __shfl_xor_sync(0xffffffffu, n2a, o);
+            n2b += __shfl_xor_sync(0xffffffffu, n2b, o);
+        }
+        const double norma = sqrt(n2a), normb = sqrt(n2b);
+        const bool dega = !(norma > 1e-12), degb = !(normb > 1e-12);
+        const double inva = dega ? 0.0 : 1.0 / norma, invb = degb ? 0.0 : 1.0 / normb;
+#pragma unroll
+        for (int k1 = 0; k1 < (int)R; ++k1) {
+            const uint32_t k = (uint32_t)k1 + R * k2;
+            if (k >= 1 && k <= (uint32_t)kK) {
+                const double ca = ma[k1] * inva, cb = mb[k1] * invb;
+                const uint64_t oa = pa * kK + (k - 1), ob = pb * kK + (k - 1);
+                if (out64) { out64[oa] = ca; if (hasb) out64[ob] = cb; }
+                if (out32) { out32[oa] = __double2float_rn(ca); if (hasb) out32[ob] = __double2float_rn(cb); }
+            }
+        }
+        if (degenerate && lane == 0) { degenerate[pa] = dega ? 1 : 0; if (hasb) degenerate[pb] = degb ? 1 : 0; }
+        if (prof_out) {   // NEXT-1 stored profiles: (x - mean) / ||m|| (the profiles re-read: L2)
+            for (int o = 16; o; o >>= 1) {
+                sa += __shfl_xor_sync(0xffffffffu, sa, o);
+                sb += __shfl_xor_sync(0xffffffffu, sb, o);
+            }
+            const double meana = sa / (double)W, meanb = sb / (double)W;
+#pragma unroll
+            for (int j = 0; j < (int)R; ++j) {
+                prof_out[pa * W + lane + 32 * j] = __double2float_rn((__ldg(&prof[pa * W + lane + 32 * j]) - meana) * inva);
+                if (hasb) prof_out[pb * W + lane + 32 * j] = __double2float_rn((__ldg(&prof[pb * W + lane + 32 * j]) - meanb) * invb);
+            }
+        }
+    }
+}
+
 size_t extract_smem_bytes(uint32_t W) { return sizeof(double) * W * (2 + kExtractWarps); }
 
 cudaError_t launch_extract(const double *prof, uint64_t n, uint32_t W, float *out32, double *out64,
@@ -216,7 +356,11 @@ cudaError_t launch_extract(const double *prof, uint64_t n, uint32_t W, float *ou
         uint64_t blocks = (n + kExtractWarps - 1) / kExtractWarps;
         if (blocks > 148 * 32) blocks = 148 * 32;
         if (W == 128) fft_extract_kernel<4><<<(unsigned)blocks, 32 * kExtractWarps, 0, s>>>(prof, n, out32, out64, degenerate, prof_out);
-        else if (W == 256) fft_extract_kernel<8><<<(unsigned)blocks, 32 * kExtractWarps, 0, s>>>(prof, n, out32, out64, degenerate, prof_out);
+        else if (W == 256) {   // two profiles per warp
+            uint64_t b2 = ((n + 1) / 2 + kExtractWarps - 1) / kExtractWarps;
+            if (b2 > 148 * 32) b2 = 148 * 32;
+            fft2_extract256_kernel<<<(unsigned)b2, 32 * kExtractWarps, 0, s>>>(prof, n, out32, out64, degenerate, prof_out);
+        }
         else fft_extract_kernel<16><<<(unsigned)blocks, 32 * kExtractWarps, 0, s>>>(prof, n, out32, out64, degenerate, prof_out);
         return cudaGetLastError();
     }
