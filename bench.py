@@ -73,9 +73,9 @@ def _args():
 PIPE_PROBE = {32: 456}
 
 # binary64 DADD + DMUL + DFMA thread instructions per profile of fft2_extract256_kernel (W = 256,
-# two profiles per warp), counted by ncu on the final kernel (1,109M + 1,457M + 3,132M over
+# two profiles per warp), counted by ncu on the final kernel (840M + 1,625M + 3,400M over
 # 1,048,576 profiles; the one-profile-per-warp kernel needed 8,024)
-FFT_FP64_OPS_PER_PROFILE = 5433
+FFT_FP64_OPS_PER_PROFILE = 5593
 
 
 class Clocks:
@@ -502,7 +502,7 @@ def run_omniloc(a):
                                       "unit": "T fp64 lane-instr/s", "frac": fp64_ach / fp64_peak,
                                       "peak_source": f"148 SMs x 64 DFMA lanes x {sm_max:.0f} MHz",
                                       "per_launch": {"fp64_lane_instr_per_profile": fp64_ops},
-                                      "note": "FFT (P:121), two real profiles per complex transform: 5,433 binary64 "
+                                      "note": "FFT (P:121), two real profiles per complex transform: 5,593 binary64 "
                                               "DADD/DMUL/DFMA per profile at W = 256 (8,024 one per warp; 65.5k for "
                                               "the round-1 direct sum); ncu: fp64 pipe 48 % active (conversions and "
                                               "compares share it)"}}

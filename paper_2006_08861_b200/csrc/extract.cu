@@ -234,6 +234,7 @@ fft2_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out
         const bool hasb = pb < n;
         double re[R], im[R];
         double sa = 0.0, sb = 0.0;   // (the profiles' sums, for the stored profiles' means)
+        int ea = 0, eb = 0;          // (the profiles' power-of-two scales)
         {   // 8-point complex DFT of z_j = xa_j + i xb_j (radix 2: even / odd outputs)
             double xa[R], xb[R];
 #pragma unroll
@@ -245,6 +246,24 @@ fft2_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out
 #pragma unroll
                 for (int j = 0; j < (int)R; ++j) { sa += xa[j]; sb += xb[j]; }
             }
+            // each profile scaled by a power of two to max |x| in [1, 2): exact (all later
+            // operations scale exactly), so the descriptor is unchanged, and a dim profile
+            // is not drowned by the rounding of a bright partner's transform
+            // (the biased exponent field of the largest |x|: an integer warp max; 0 for zeros)
+            uint32_t ga = 0, gb = 0;
+#pragma unroll
+            for (int j = 0; j < (int)R; ++j) {
+                ga = max(ga, (uint32_t)(__double_as_longlong(xa[j]) >> 52) & 0x7ffu);
+                gb = max(gb, (uint32_t)(__double_as_longlong(xb[j]) >> 52) & 0x7ffu);
+            }
+            ga = __reduce_max_sync(0xffffffffu, ga);
+            gb = __reduce_max_sync(0xffffffffu, gb);
+            ea = (ga > 1 && ga < 2046) ? (int)ga - 1023 : 0;   // (subnormal / huge ranges: unscaled)
+            eb = (gb > 1 && gb < 2046) ? (int)gb - 1023 : 0;
+            const double sca = __longlong_as_double((long long)(1023 - ea) << 52);   // 2^-ea, exact
+            const double scb = __longlong_as_double((long long)(1023 - eb) << 52);
+#pragma unroll
+            for (int j = 0; j < (int)R; ++j) { xa[j] *= sca; xb[j] *= scb; }
             constexpr double c = 0.70710678118654752440;   // cos(pi/4) = sin(pi/4), RN
             double ar[4], ai[4], br[4], bi[4];
 #pragma unroll
@@ -318,8 +337,10 @@ fft2_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out
             n2a += __shfl_xor_sync(0xffffffffu, n2a, o);
             n2b += __shfl_xor_sync(0xffffffffu, n2b, o);
         }
-        const double norma = sqrt(n2a), normb = sqrt(n2b);
-        const bool dega = !(norma > 1e-12), degb = !(normb > 1e-12);
+        const double norma = sqrt(n2a), normb = sqrt(n2b);   // (of the scaled profiles)
+        const double una = __longlong_as_double((long long)(1023 + ea) << 52);   // 2^ea
+        const double unb = __longlong_as_double((long long)(1023 + eb) << 52);
+        const bool dega = !(norma * una > 1e-12), degb = !(normb * unb > 1e-12);
         const double inva = dega ? 0.0 : 1.0 / norma, invb = degb ? 0.0 : 1.0 / normb;
 #pragma unroll
         for (int k1 = 0; k1 < (int)R; ++k1) {
@@ -338,10 +359,11 @@ fft2_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out
                 sb += __shfl_xor_sync(0xffffffffu, sb, o);
             }
             const double meana = sa / (double)W, meanb = sb / (double)W;
+            const double sca2 = __longlong_as_double((long long)(1023 - ea) << 52), scb2 = __longlong_as_double((long long)(1023 - eb) << 52);
 #pragma unroll
             for (int j = 0; j < (int)R; ++j) {
-                prof_out[pa * W + lane + 32 * j] = __double2float_rn((__ldg(&prof[pa * W + lane + 32 * j]) - meana) * inva);
-                if (hasb) prof_out[pb * W + lane + 32 * j] = __double2float_rn((__ldg(&prof[pb * W + lane + 32 * j]) - meanb) * invb);
+                prof_out[pa * W + lane + 32 * j] = __double2float_rn((__ldg(&prof[pa * W + lane + 32 * j]) - meana) * (inva * sca2));
+                if (hasb) prof_out[pb * W + lane + 32 * j] = __double2float_rn((__ldg(&prof[pb * W + lane + 32 * j]) - meanb) * (invb * scb2));
             }
         }
     }

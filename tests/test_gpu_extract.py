@@ -133,3 +133,25 @@ def test_stored_profiles_vs_oracle(W):                       # NEXT-1 stored pro
     o32d, degd, pod = e.extract_features(torch.from_numpy(P).cuda(), want_profiles=True)
     torch.cuda.synchronize()
     assert np.array_equal(pod.cpu().numpy(), po) and np.array_equal(o32d.cpu().numpy(), o32)
+
+
+@pytest.mark.parametrize("n", [1, 2, 9, 301])
+def test_extract_w256_pairs_odd_counts_and_scale_disparity(n):
+    """W = 256 runs two profiles per warp as one complex transform: odd counts leave a lone
+    profile, and a pair may mix profiles of very different brightness (scales 1e-4 and 3e5
+    apart; each is scaled by a power of two first) -- each must still match the oracle."""
+    rng = np.random.default_rng(1000 + n)
+    W = 256
+    P = rng.random((n, W)) + np.sin(np.arange(W) * 2 * np.pi * 7 / W)[None, :] * rng.random((n, 1))
+    if n >= 2:
+        P[1] *= 1e-4                                   # pair (0, 1): magnitudes 1e-4 apart
+    if n >= 9:
+        P[8] *= 3e5                                    # bright, lone when n = 9
+        P[3] = 0.0                                     # degenerate partner of profile 2
+    e = ol.Engine(0)
+    o32, deg, o64 = e.extract_features(P, want64=True)
+    _check(P, o32, deg, o64)
+    _, _, po = e.extract_features(P, want_profiles=True)
+    ref = np.stack([oracle.shift_profile(x)[1] for x in P])
+    ulp = np.abs(po.view(np.int32).astype(np.int64) - ref.view(np.int32).astype(np.int64))
+    assert ulp.max() <= 1, ulp.max()
