@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kMergeThreads) merge_chunks_kernel(MergeArgs a
         for (uint32_t r = 0; r < N; ++r) {
             const u64 v = L[r];
             if (v > T || v == kPadKey) break;
-            OL_DCHECK(r == 0 || L[r - 1] < v);   // (the lists are ascending)
+            (void)OL_DCHECK(r == 0 || L[r - 1] < v);   // (the lists are ascending)
             const uint32_t pos = atomicAdd(&nbuf, 1u);
             if (pos < a.buf_cap) buf[pos] = v;
         }

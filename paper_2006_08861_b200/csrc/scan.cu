@@ -340,7 +340,7 @@ constexpr int kRows2 = 2 * kScanThreads;   // rows per stage
 
 template <int KC>
 __global__ void __launch_bounds__(kScanThreads + 32) scan3_kernel(ScanArgs a) {
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem[];   // (bulk copies need 16 B)
     const uint32_t qt = a.qt, N = a.N;
     float *rows = reinterpret_cast<float *>(smem);                         // [kStages2][kRows2][KC]
     uint64_t *full = reinterpret_cast<uint64_t *>(rows + kStages2 * kRows2 * KC);

@@ -60,12 +60,10 @@ constexpr int kEv = 8;                  // survivor event ring entries per exact
                                         // (measured with the 32-dim filter, 1,024 frames, ring
                                         // 32 / 16 / 8 / 4: 100M rows 10.05 / 9.93 / 9.95 / 9.96 ms,
                                         // 20M 2.82 / 2.70 / 2.66 / 2.67, 1M 0.68 / - / 0.58 / 0.57)
-constexpr int kTrackMax = 16;
-constexpr int kBndRing = 16;
+constexpr int kTrackMax = 16;           // largest N of the bound pre-pass (register list)
+constexpr int kBndRing = 16;            // >= kMaxStages + kTBufs: see TcSmem::bnd
 constexpr uint32_t kTlTiles = 120;      // profiling timeline (tc_debug 32 | 2048): tiles of CTA 0 recorded
-constexpr uint32_t kL2Ahead = 24;       // row tiles prefetched into L2 ahead of the TMA stage loads            // >= kMaxStages + kTBufs: see TcSmem::bnd           // largest N of the bound pre-pass (register list)
 constexpr float kTauInflate = 1.0f + 1.0f / 131072.0f;   // 1 + 2^-17
-constexpr uint32_t kStageBytesMax = kTileRows * kK * 2;   // 32 KB (pw = 64; 16 KB at pw = 32)
 
 struct TcSmem {
     alignas(1024) __half qm[kQB * kK];      // frames, main K (SW128), resident
