@@ -1,4 +1,4 @@
-"""Timing of the NEXT-3 extraction and NEXT-1 shift kernels (1M profiles of W = 256; 15,360 candidates)."""
+"""Timing of the NEXT-3 extraction kernel (1M profiles of W = 256; the shift kernel: tools/shift_timing.py)."""
 import sys, torch
 sys.path.insert(0, '.')
 import numpy as np
