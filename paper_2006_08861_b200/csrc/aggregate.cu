@@ -101,7 +101,7 @@ __device__ __noinline__ void aggregate_warp(const AggArgs &a, uint32_t b, uint32
     // step 2: rank = #tiles before it in (count desc, (y, x) asc) order; lanes of run starts are
     // in (y, x) order already
     uint32_t rank = 0;
-    for (int j = 0; j < 32; ++j) {
+    for (int j = 0; j < (int)total; ++j) {   // (run starts lie below total; warp-uniform bound)
         const uint32_t cj = __shfl_sync(kAll, cnt, j);
         if (((starts >> j) & 1u) && (cj > cnt || (cj == cnt && j < lane))) ++rank;
     }
@@ -110,7 +110,7 @@ __device__ __noinline__ void aggregate_warp(const AggArgs &a, uint32_t b, uint32
     // step 3: the tolerance circle of every ranked tile
     const int64_t cx = key_x(k), cy = key_y(k);
     uint32_t circ = 0;
-    for (int j = 0; j < 32; ++j) {
+    for (int j = 0; j < (int)total; ++j) {
         const u64 kj = __shfl_sync(kAll, k, j);
         const uint32_t cj = __shfl_sync(kAll, cnt, j);
         if ((starts >> j) & 1u) {
