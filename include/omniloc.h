@@ -415,7 +415,7 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *                   automatic, 6 when the filter plane has 64-B rows (tc_k = 32), else 12)
  *   "tc_seed"       0 (default) / 1 / 2: tensor-core bound pre-pass as the seed (N <= 16);
  *                   2 runs it after the exact sampled seed
- *   "tc_k"          0 (default: 32 when every subspace holds >= 32M rows on this rank, else
+ *   "tc_k"          0 (default: 32 when every subspace holds >= 8M rows on this rank, else
  *                   64) / 16 / 32 / 48 / 64: dimensions (a prefix) the certified tensor-core
  *                   filter scores; fewer halve its MMA work, more pairs reach the exact
  *                   re-score.  Results are identical.  Takes effect at the next ol_upload_db

@@ -608,12 +608,13 @@ ol_status ol_upload_db(ol_ctx *c, const ol_db_desc *db) {
         OL_CUDA(c, launch_pad_rows(c->subs_d, ns, kc, c->coarse, c->fine, c->stream));
         if (c->opt_tc != 0) {
             // the filter on the first 32 dimensions halves the MMA work but passes more
-            // pairs to the exact path (1,024 frames: 20M rows 2.87 vs 2.72 ms, 35M 4.15 vs
-            // 4.39, 50M 5.57 vs 6.09, 100M 9.88 vs 12.0 ms for 32 vs 64): automatic mode takes
-            // 32 once every subspace holds >= 32M rows on this rank
+            // pairs to the exact path; automatic mode takes 32 once every subspace holds >= 8M
+            // rows on this rank.  Round 2 (survivor rows read in halves, best pair setting each,
+            // 1,024 frames, kf 32 vs 64): 6M rows 0.868 vs 0.857 ms, 10M 1.216 vs 1.271, 12.5M
+            // 1.414 vs 1.507, 25M 2.379 vs 2.716, 50M 4.289 vs 5.432 (round 1 crossed at ~32M)
             uint64_t minc = ~0ull;
             for (auto &sb : subs) minc = sb.count < minc ? sb.count : minc;
-            c->tc_kf = c->opt_tc_k ? (uint32_t)c->opt_tc_k : (minc >= 32000000ull ? 32u : 64u);
+            c->tc_kf = c->opt_tc_k ? (uint32_t)c->opt_tc_k : (minc >= 8000000ull ? 32u : 64u);
             // kf = 32: the plane holds only those dimensions (64-B rows): half the bytes
             // streamed, and what makes few-frame batches HBM-bound at half the time
             c->tc_pw = c->tc_kf == 32 ? 32u : 64u;
