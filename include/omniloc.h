@@ -412,7 +412,7 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *   "tc"            -1 (default: automatic, >= tc_min_frames frames) / 1 / 0: the certified
  *                   tensor-core filter (needs |f| < 65000 and ||f|| < 300 in the database)
  *   "tc_min_frames" frames per query below which the CUDA-core scans are used (default 0:
- *                   automatic, 6 when the filter plane has 64-B rows (tc_k = 32), else 12)
+ *                   automatic, 4 when the filter plane has 64-B rows (tc_k = 32), else 16)
  *   "tc_seed"       0 (default) / 1 / 2: tensor-core bound pre-pass as the seed (N <= 16);
  *                   2 runs it after the exact sampled seed
  *   "tc_k"          0 (default: 32 when every subspace holds >= 8M rows on this rank, else

@@ -187,7 +187,7 @@ struct ol_ctx {
     // options
     int64_t opt_chunk = 0, opt_qtile = 0, opt_tau_seed = 1, opt_ctas = 0, opt_time = 0, opt_seed_samples = 0;
     int64_t opt_tc = -1;         // tensor-core filter: -1 auto (>= tc_min_frames frames), 0 off, 1 always
-    int64_t opt_tc_min_frames = 0;    // 0 = automatic: 6 with the 64-B plane (kf = 32), else 12.  Measured C4:
+    int64_t opt_tc_min_frames = 0;    // 0 = automatic: 4 with the 64-B plane (kf = 32), else 16.  Round 1, C4:
                                       // 64-B plane: 4 frames scan2 0.94 vs tc 1.02 ms, 8: 1.28 vs 1.02;
                                       // 128-B plane: 8 frames 1.37 vs 1.77, 16: 2.42 vs 1.77
     int64_t opt_tc_debug = 0;
@@ -1011,7 +1011,10 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
     // launch shape (results never depend on it): tensor-core filter or CUDA-core
     // scan, query tile, chunk size
     uint32_t tc_qb = 0, tc_stages = 0;
-    const uint32_t min_frames = c->opt_tc_min_frames ? (uint32_t)c->opt_tc_min_frames : (c->tc_pw == 32 ? 6u : 12u);
+    // (round 2, seed + scan + merge, tensor cores vs CUDA cores: 64-B plane, 100M rows 4 frames
+    // 1.014 vs 1.010 ms, 5: 1.019 vs 1.257; 10M rows 4: 0.191 vs 0.197, 5: 0.195 vs 0.223;
+    // 128-B plane, 1M rows 12 frames 0.141 vs 0.128, 16: 0.140 vs 0.141)
+    const uint32_t min_frames = c->opt_tc_min_frames ? (uint32_t)c->opt_tc_min_frames : (c->tc_pw == 32 ? 4u : 16u);
     const bool use_tc = c->tc_ok && (c->opt_tc == 1 || (c->opt_tc == -1 && nq >= min_frames)) &&
                         tc_shape(N, nq, c->tc_pw, &tc_qb, &tc_stages);
     uint32_t qt = c->opt_qtile > 0 ? (uint32_t)c->opt_qtile : kMaxQT;
