@@ -107,6 +107,7 @@ struct SeedArgs {
     uint32_t nq, n_sub, N, samples, kc, splits;   // splits: independent samples per (frame, sub)
     uint32_t *scratch;           // [nq][n_sub][splits][samples] acc bits (seed_acc -> seed_select)
     uint64_t rows_pad;           // device rows (bounds checks)
+    uint32_t select_old = 0;     // 1: the CTA / radix selects even where the warp gather applies (tests, A/B)
 };
 
 struct MergeArgs {

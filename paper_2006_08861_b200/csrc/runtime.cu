@@ -185,7 +185,7 @@ struct ol_ctx {
     uint64_t n_cand = 0, per_bundle = 0, pairs = 0;
     int launches = 0;
     // options
-    int64_t opt_chunk = 0, opt_qtile = 0, opt_tau_seed = 1, opt_ctas = 0, opt_time = 0, opt_seed_samples = 0;
+    int64_t opt_chunk = 0, opt_qtile = 0, opt_tau_seed = 1, opt_ctas = 0, opt_time = 0, opt_seed_samples = 0, opt_seed_select = 0;
     int64_t opt_tc = -1;         // tensor-core filter: -1 auto (>= tc_min_frames frames), 0 off, 1 always
     int64_t opt_tc_min_frames = 0;    // 0 = automatic: 4 with the 64-B plane (kf = 32), else 16.  Round 1, C4:
                                       // 64-B plane: 4 frames scan2 0.94 vs tc 1.02 ms, 8: 1.28 vs 1.02;
@@ -1084,6 +1084,7 @@ static ol_status query_body(ol_ctx *c, uint32_t nb, uint32_t M, const float *q, 
         sa.coarse = c->coarse; sa.fine = c->fine; sa.queries = q; sa.subs = c->subs_d;
         sa.tau0 = c->tau0_d; sa.nq = nq; sa.n_sub = c->n_sub; sa.N = N; sa.kc = (uint32_t)c->kc;
         sa.rows_pad = c->rows_pad;
+        sa.select_old = c->opt_seed_select == 1;
         // splits x (count/8, at most 4096) rows per subspace, about 64k sampled pairs per
         // row... i.e. more splits for few frames; below N rows per split: no seed (+inf)
         // automatic: 8,192 samples for >= 1,024 (frame, subspace) jobs (1,024 frames: 1M rows
@@ -1756,6 +1757,7 @@ ol_status ol_set_option(ol_ctx *c, const char *key, int64_t v) {
     if (!strcmp(key, "chunk")) { if (v < 0) goto bad; c->opt_chunk = v; }
     else if (!strcmp(key, "qtile")) { if (v < 0 || v > kMaxQT) goto bad; c->opt_qtile = v; }
     else if (!strcmp(key, "tau_seed")) { if (v != 0 && v != 1) goto bad; c->opt_tau_seed = v; }
+    else if (!strcmp(key, "seed_select")) { if (v < 0 || v > 1) goto bad; c->opt_seed_select = v; }
     else if (!strcmp(key, "seed_samples")) { if (v != 0 && (v < 16 || v > 32768)) goto bad; c->opt_seed_samples = v; }
     else if (!strcmp(key, "ctas")) { if (v < 0) goto bad; c->opt_ctas = v; }
     else if (!strcmp(key, "time_kernels")) { if (v != 0 && v != 1) goto bad; c->opt_time = v; }

@@ -823,6 +823,74 @@ __global__ void __launch_bounds__(256) seed_select_small_kernel(SeedArgs a) {
     if (threadIdx.x == 0) atomicMin(&a.tau0[(size_t)q * a.n_sub + i], T);
 }
 
+// Warp per job, S <= 4,096 and N <= 32 (many small jobs: C3 split into 50 subspaces is
+// 51,200 jobs of 2,500 samples).  T = the N-th smallest of 256 evenly strided values (N
+// real samples: an upper bound of the N-th smallest of all S); one pass gathers every value
+// <= T, compacted by ballot into the warp's shared buffer (about N x S / 256 of them); the
+// N-th smallest of the gathered is the answer when they all fit (exact); otherwise the
+// N-th smallest of those that fit (N real samples: a valid, tighter bound) is gathered
+// below again, at most 3 rounds (or until it stops moving: ties).  Sorting networks on 32-key warp
+// lists (warp_sort32 / warp_merge32), no CTA barriers.
+constexpr uint32_t kWSelBuf = 512;
+__global__ void __launch_bounds__(256) seed_select_gather_warp_kernel(SeedArgs a) {
+    __shared__ u64 buf[8][kWSelBuf];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t job = blockIdx.x * 8 + w;   // (frame, subspace, split)
+    if (job >= a.nq * a.n_sub * a.splits) return;   // (whole warps)
+    const uint32_t i = (job / a.splits) % a.n_sub, q = (job / a.splits) / a.n_sub;
+    const uint32_t S = (uint32_t)min((uint64_t)a.samples, a.subs[i].count);
+    if (S < a.N) return;
+    const uint32_t *v = a.scratch + (size_t)job * a.samples;
+    const uint32_t S0 = min(S, 256u);
+    u64 run = kPadKey;
+    for (uint32_t b = 0; b < S0; b += 32) {
+        const uint32_t t = b + lane;
+        u64 k = kPadKey;
+        if (t < S0) {
+            const uint32_t idx = (uint32_t)(((uint64_t)t * S) / S0);
+            k = ((u64)__ldcg(v + idx) << 32) | idx;
+        }
+        run = warp_merge32(run, warp_sort32(k, lane), lane);
+    }
+    uint32_t T = (uint32_t)(__shfl_sync(0xffffffffu, run, a.N - 1) >> 32);
+    uint32_t R = T;
+    for (int round = 0; round < 3; ++round) {
+        uint32_t nb = 0;
+        for (uint32_t t0 = 0; t0 < S; t0 += 32 * 8) {
+            uint32_t x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t t = t0 + j * 32 + lane;
+                x[j] = t < S ? __ldcg(v + t) : 0xFFFFFFFFu;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t t = t0 + j * 32 + lane;
+                const bool in = t < S && x[j] <= T;
+                const unsigned m = __ballot_sync(0xffffffffu, in);
+                if (in) {
+                    const uint32_t pos = nb + __popc(m & ((1u << lane) - 1u));
+                    if (pos < kWSelBuf) buf[w][pos] = ((u64)x[j] << 32) | t;
+                }
+                nb += __popc(m);
+            }
+        }
+        __syncwarp();
+        const uint32_t ng = min(nb, kWSelBuf);   // >= N: N samples are <= T
+        run = kPadKey;
+        for (uint32_t b = 0; b < ng; b += 32) {
+            const u64 k = b + lane < ng ? buf[w][b + lane] : kPadKey;
+            run = warp_merge32(run, warp_sort32(k, lane), lane);
+        }
+        __syncwarp();
+        R = (uint32_t)(__shfl_sync(0xffffffffu, run, a.N - 1) >> 32);   // (N samples <= R: valid)
+        if (nb <= kWSelBuf || R == T) break;     // exact: every value <= T was gathered
+        T = R;                                   // (overflow: again below the tighter bound)
+    }
+    // every split's N-th smallest is an upper bound of the true N-th: keep the least
+    if (lane == 0) atomicMin(&a.tau0[(size_t)q * a.n_sub + i], R);
+}
+
 // Warp per job (small samples, many jobs: a CTA per job would mostly wait at barriers).
 __global__ void __launch_bounds__(256) seed_select_warp_kernel(SeedArgs a) {
     __shared__ uint32_t hist[8][256];
@@ -892,7 +960,9 @@ cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         // one CTA per job streams large samples with its loads in flight (C4: 170 -> 28 us);
         // a warp per job is faster for small ones (C2, 500 samples x 25,000 jobs: 0.18 vs 0.32 ms)
-        if (a.samples >= 2048 && a.N <= 32) seed_select_small_kernel<<<a.nq * a.n_sub * a.splits, 256, 0, s>>>(a);
+        const uint32_t jobs = a.nq * a.n_sub * a.splits;
+        if (a.samples <= 4096 && a.N <= 32 && !a.select_old) seed_select_gather_warp_kernel<<<(jobs + 7) / 8, 256, 0, s>>>(a);
+        else if (a.samples >= 2048 && a.N <= 32) seed_select_small_kernel<<<a.nq * a.n_sub * a.splits, 256, 0, s>>>(a);
         else if (a.samples >= 2048) seed_select_kernel<<<a.nq * a.n_sub * a.splits, 256, 0, s>>>(a);
         else seed_select_warp_kernel<<<(a.nq * a.n_sub * a.splits + 7) / 8, 256, 0, s>>>(a);
         return cudaGetLastError();

@@ -310,6 +310,37 @@ def test_merge_gather_and_fallback_vs_oracle(tc):
         assert outs[0] == outs[1]
 
 
+def test_seed_select_gather_warp_vs_other_selects_vs_oracle():
+    """The two-kernel seed's warp-per-job select (samples <= 4,096: N-th smallest of a strided
+    subset as the bound, one gathering pass, sorting networks) finds the same thresholds as
+    the CTA / radix selects (option seed_select = 1) -- the exact N-th smallest of every
+    job's samples -- including a subspace of identical rows (every sample ties, the gather
+    buffer overflows), N above and below 16; the queries then equal the oracle."""
+    rng = np.random.default_rng(990)
+    sizes = [33000, 40000, 33000, 36001, 32768]
+    F = np.abs(rng.standard_normal((sum(sizes), 64))).astype(np.float32)
+    F /= np.linalg.norm(F, axis=1, keepdims=True)
+    F[73000:106000] = F[73000]                                   # subspace 2: one row repeated
+    C = rng.integers(0, 60, (sum(sizes), 2)).astype(np.int32)
+    Q = (F[rng.integers(0, len(F), 40)] + 1e-3 * rng.standard_normal((40, 64))).astype(np.float32)
+    Q = np.ascontiguousarray(Q.reshape(40, 1, 64))
+    for N, S in ((15, 4096), (15, 2500), (31, 300), (5, 64)):
+        taus = []
+        for sel in (0, 1):
+            e = _engine(16, tc_seed=0, seed_samples=S, seed_select=sel, tc_debug=512)
+            e.upload(F, C, sizes, (64, 64))
+            e.query(Q, N=N)
+            taus.append(e.thresholds().cpu().numpy().copy())
+            e.close()
+        assert (taus[0] == taus[1]).all(), f"N {N} S {S}: thresholds differ"
+        assert (taus[0] < 0x7F800000).all()                     # every job seeded
+        e = _engine(16, tc_seed=0, seed_samples=S)
+        e.upload(F, C, sizes, (64, 64))
+        e.query(Q, N=N)
+        assert_candidates_equal(e.topk(), oracle.retrieve(sizes, F, C, Q, N), f"seed select N {N} S {S}")
+        e.close()
+
+
 @pytest.mark.parametrize("kc", [0, 8, 16, 32, 64])
 def test_small_batch_cuda_core_kernels_vs_oracle(kc):
     """The CUDA-core scans for few frames -- scan3 (TMA-fed; automatic for 1-2 frames per tile),
