@@ -407,7 +407,8 @@ OL_API ol_status ol_extract_features(ol_ctx *ctx, const double *profiles, uint64
  *                   8192 for >= 1,024 (frame, subspace) jobs, else 4096; at most 8192 when the
  *                   one-CTA-per-job seed kernel runs)
  *   "seed_select"   0 (default) / 1: the two-kernel seed's select step: a warp per job gathering
- *                   the values below a strided-subset bound when samples <= 4,096 and N <= 32 /
+ *                   the values below a strided-subset bound when 2,048 <= samples <= 4,096 and
+ *                   N <= 32 /
  *                   the CTA-per-job or radix selects everywhere
  *   "seed_kernel"   1 (default) / 0: two-kernel seed (sample rows reused across frames; one CTA
  *                   per job when its scratch would exceed 2^28 entries) / one CTA per

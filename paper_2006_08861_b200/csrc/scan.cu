@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(256) seed_select_small_kernel(SeedArgs a) {
     if (threadIdx.x == 0) atomicMin(&a.tau0[(size_t)q * a.n_sub + i], T);
 }
 
-// Warp per job, S <= 4,096 and N <= 32 (many small jobs: C3 split into 50 subspaces is
+// Warp per job, 2,048 <= S <= 4,096 and N <= 32 (many mid-sized jobs: C3 split into 50 subspaces is
 // 51,200 jobs of 2,500 samples).  T = the N-th smallest of 256 evenly strided values (N
 // real samples: an upper bound of the N-th smallest of all S); one pass gathers every value
 // <= T, compacted by ballot into the warp's shared buffer (about N x S / 256 of them); the
@@ -959,9 +959,12 @@ cudaError_t launch_tau_seed(const SeedArgs &a, cudaStream_t s) {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         // one CTA per job streams large samples with its loads in flight (C4: 170 -> 28 us);
-        // a warp per job is faster for small ones (C2, 500 samples x 25,000 jobs: 0.18 vs 0.32 ms)
+        // a warp per job is faster for small ones: gathering below a strided bound for 2,048-4,096
+        // samples (C3 / 50 subspaces, 2,500 x 51,200 jobs: 0.31 vs 0.68 ms; at 8,192 samples it
+        // loses), radix passes below 2,048 (C2, 500 samples x 25,000 jobs: 0.173 vs 0.198 ms for
+        // the gather, 0.32 ms for the CTA per job)
         const uint32_t jobs = a.nq * a.n_sub * a.splits;
-        if (a.samples <= 4096 && a.N <= 32 && !a.select_old) seed_select_gather_warp_kernel<<<(jobs + 7) / 8, 256, 0, s>>>(a);
+        if (a.samples >= 2048 && a.samples <= 4096 && a.N <= 32 && !a.select_old) seed_select_gather_warp_kernel<<<(jobs + 7) / 8, 256, 0, s>>>(a);
         else if (a.samples >= 2048 && a.N <= 32) seed_select_small_kernel<<<a.nq * a.n_sub * a.splits, 256, 0, s>>>(a);
         else if (a.samples >= 2048) seed_select_kernel<<<a.nq * a.n_sub * a.splits, 256, 0, s>>>(a);
         else seed_select_warp_kernel<<<(a.nq * a.n_sub * a.splits + 7) / 8, 256, 0, s>>>(a);
