@@ -199,6 +199,32 @@ def _dist_init(n_gpus):
     return rank, world, local
 
 
+def _make_engine(ol, local, a, group, world, coarse_k):
+    """The engine with the requested exchange; at world > 1, if creating it failed on any
+    rank (e.g. the library could not load NCCL), every rank falls back together to
+    exchange="torch" (torch's all-gather + the library's merge kernel) and a.exchange records
+    it.  A failure inside a collective init that hangs instead cannot be caught here."""
+    if world == 1:
+        return ol.Engine(local, coarse_k=coarse_k, process_group=group, exchange=a.exchange)
+    try:
+        eng, ok = ol.Engine(local, coarse_k=coarse_k, process_group=group, exchange=a.exchange), 1
+    except Exception as ex:   # noqa: BLE001 -- reported, then decided collectively
+        eng, ok = None, 0
+        sys.stderr.write(f"bench.py: Engine(exchange={a.exchange!r}) failed: {ex}\n")
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ok], dtype=torch.int32, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    if int(t.item()):
+        return eng
+    if a.exchange == "torch":
+        raise SystemExit("bench.py: could not create the engine")
+    if eng is not None:
+        eng.close()
+    a.exchange = "torch"
+    return ol.Engine(local, coarse_k=coarse_k, process_group=group, exchange="torch")
+
+
 def _barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -260,7 +286,7 @@ def run_omniloc(a):
     if world > 1:
         import torch.distributed as dist
         group = dist.group.WORLD
-    eng = ol.Engine(local, coarse_k=a.coarse_k, process_group=group, exchange=a.exchange)
+    eng = _make_engine(ol, local, a, group, world, coarse_k=a.coarse_k)
     t0 = time.time()
     eng.upload(F, C, [n_total], spec.grid())
     torch.cuda.synchronize()
@@ -753,7 +779,7 @@ def run_streaming(a):
     if world > 1:
         import torch.distributed as dist
         group = dist.group.WORLD
-    eng = ol.Engine(local, coarse_k=16, process_group=group, exchange=a.exchange)
+    eng = _make_engine(ol, local, a, group, world, coarse_k=16)
     eng.upload(F, C, [n_total], spec.grid())
     if a.graph and world == 1:
         eng.set_option("graph", 1)
