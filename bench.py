@@ -72,10 +72,11 @@ def _args():
 # 2 x 256-column buffers, FMNMX3 math); round 1's probe (841) had a serial-chain epilogue
 PIPE_PROBE = {32: 456}
 
-# binary64 DADD + DMUL + DFMA thread instructions per profile of fft2_extract256_kernel (W = 256,
-# two profiles per warp), counted by ncu on the final kernel (840M + 1,625M + 3,400M over
-# 1,048,576 profiles; the one-profile-per-warp kernel needed 8,024)
-FFT_FP64_OPS_PER_PROFILE = 5593
+# binary64 DADD + DMUL + DFMA thread instructions per profile of fft3_extract256_kernel (W = 256,
+# two profiles per warp, 8 x 8 x 4 with shared-memory transposes), counted by ncu on the final
+# kernel (2,182M + 1,248M + 1,664M over 1,048,576 profiles; the five-shuffle-stage version
+# needed 5,593, one profile per warp 8,024)
+FFT_FP64_OPS_PER_PROFILE = 4857
 
 
 class Clocks:
@@ -515,23 +516,23 @@ def run_omniloc(a):
         ib = Wp * 8 + 64 * 4 + 1    # profile in (binary64), fp32 descriptor + degenerate flag out
         igbs = n_in * ib / (ims / 1e3) / 1e9
         # FP64 arithmetic per profile (DADD + DMUL + DFMA thread instructions; ncu on the final
-        # kernel, profiles/r02_summary.md): the binding resource -- the fp64 pipe is ~50 % busy,
-        # HBM at ~0.23.  Peak: 64 DFMA lanes per SM (ncu sm__sass_thread_inst_executed_op_dfma
+        # kernel, profiles/r02_summary.md): the binding resource -- with the FP64 pipe and issue
+        # sharing it (HBM at ~0.4).  Peak: 64 DFMA lanes per SM (ncu sm__sass_thread_inst_executed_op_dfma
         # peak_sustained) x 148 SMs x the max SM clock
         fp64_ops = FFT_FP64_OPS_PER_PROFILE
         fp64_peak = 148 * 64 * sm_max * 1e6 / 1e12
         fp64_ach = n_in * fp64_ops / (ims / 1e3) / 1e12
-        out["ingest"] = {"kernel": "fft2_extract256_kernel", "profiles": n_in, "W": Wp, "ms": ims,
+        out["ingest"] = {"kernel": "fft3_extract256_kernel", "profiles": n_in, "W": Wp, "ms": ims,
                          "profiles_per_s": n_in / (ims / 1e3), "hbm_bytes_per_profile": ib,
                          "hbm_gbs": igbs, "hbm_frac": igbs / hbm_peak,
                          "roofline": {"bound": "fp64", "achieved": fp64_ach, "peak": fp64_peak,
                                       "unit": "T fp64 lane-instr/s", "frac": fp64_ach / fp64_peak,
                                       "peak_source": f"148 SMs x 64 DFMA lanes x {sm_max:.0f} MHz",
                                       "per_launch": {"fp64_lane_instr_per_profile": fp64_ops},
-                                      "note": "FFT (P:121), two real profiles per complex transform: 5,593 binary64 "
-                                              "DADD/DMUL/DFMA per profile at W = 256 (8,024 one per warp; 65.5k for "
-                                              "the round-1 direct sum); ncu: fp64 pipe 48 % active (conversions and "
-                                              "compares share it)"}}
+                                      "note": "FFT (P:121), two real profiles per complex transform, 8 x 8 x 4 with "
+                                              "shared-memory transposes: 4,857 binary64 DADD/DMUL/DFMA per profile at "
+                                              "W = 256 (5,593 with shuffle stages, 8,024 one per warp, 65.5k for the "
+                                              "round-1 direct sum)"}}
         del prof
 
     # ------------------------------------------------ e2e through the public API, host buffers

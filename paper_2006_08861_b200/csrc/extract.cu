@@ -207,16 +207,56 @@ fft_extract_kernel(const double *prof, uint64_t n, float *out32, double *out64, 
     }
 }
 
+// 8-point complex DFT (W_8 = e^{-2 pi i / 8}) of (xr, xi), radix 2 by hand: out k -> (yr, yi)[k]
+__device__ __forceinline__ void dft8(const double *xr, const double *xi, double *yr, double *yi) {
+    constexpr double c = 0.70710678118654752440;   // cos(pi/4) = sin(pi/4), RN
+    double ar[4], ai[4], br[4], bi[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        ar[j] = xr[j] + xr[j + 4]; ai[j] = xi[j] + xi[j + 4];
+        br[j] = xr[j] - xr[j + 4]; bi[j] = xi[j] - xi[j + 4];
+    }
+    const double A0r = ar[0] + ar[2], A0i = ai[0] + ai[2], A2r = ar[0] - ar[2], A2i = ai[0] - ai[2];
+    const double A1r = ar[1] + ar[3], A1i = ai[1] + ai[3], A3r = ar[1] - ar[3], A3i = ai[1] - ai[3];
+    yr[0] = A0r + A1r; yi[0] = A0i + A1i;
+    yr[4] = A0r - A1r; yi[4] = A0i - A1i;
+    yr[2] = A2r + A3i; yi[2] = A2i - A3r;
+    yr[6] = A2r - A3i; yi[6] = A2i + A3r;
+    const double t1r = c * (br[1] + bi[1]), t1i = c * (bi[1] - br[1]);
+    const double t2r = bi[2], t2i = -br[2];
+    const double t3r = c * (bi[3] - br[3]), t3i = -c * (bi[3] + br[3]);
+    const double B0r = br[0] + t2r, B0i = bi[0] + t2i, B2r = br[0] - t2r, B2i = bi[0] - t2i;
+    const double B1r = t1r + t3r, B1i = t1i + t3i, B3r = t1r - t3r, B3i = t1i - t3i;
+    yr[1] = B0r + B1r; yi[1] = B0i + B1i;
+    yr[5] = B0r - B1r; yi[5] = B0i - B1i;
+    yr[3] = B2r + B3i; yi[3] = B2i - B3r;
+    yr[7] = B2r - B3i; yi[7] = B2i + B3r;
+}
+
+// (row r of 8 doubles, element e) -> a per-warp shared-memory slot: rows padded to 9, so a
+// warp writing one element of every row, or reading rows a + 4 b, spreads over the banks, and
+// every address is a per-lane base plus an immediate
+__device__ __forceinline__ uint32_t sw8(uint32_t r, uint32_t e) { return r * 9 + e; }
+// Z[k] slot: 4 doubles of padding per 16 (the step-C writers, lanes (k1, cp), hit 16 banks)
+__device__ __forceinline__ uint32_t swz(uint32_t k) { return k + 4 * (k >> 4); }
+constexpr uint32_t kZSlots = 256 + 4 * 16;
+
 // W = 256: TWO profiles per warp as one complex sequence z = a + i b (the real-input trick:
 // the FFT's twiddles and butterflies serve both), separated at the end by the symmetry of real
-// inputs: A[k] = (Z[k] + conj Z[W-k]) / 2, B[k] = (Z[k] - conj Z[W-k]) / 2i.  Lane l holds
-// z[l + 32 j]; an 8-point complex DFT per lane over j (radix-2 by hand), the twiddles, the
-// 32-point DIF across the lanes, then Z[W - k] fetched from the mirror lane (l ^ 31 for
-// k1 != 0).  About half the binary64 work per profile of fft_extract_kernel<8>.
-__global__ void __launch_bounds__(32 * kExtractWarps, 3)   // (3 CTAs per SM with ~48 B of spills: 870M vs 840M profiles/s at 2)
-fft2_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out64, uint8_t *degenerate, float *prof_out) {
-    constexpr uint32_t R = 8, W = 256;
+// inputs: A[k] = (Z[k] + conj Z[W-k]) / 2, B[k] = (Z[k] - conj Z[W-k]) / 2i.  The 256-point
+// FFT as 8 x 8 x 4 with two shared-memory transposes (round 2; the first version, an 8-point
+// DFT per lane and a 32-point DIF across the lanes by five shuffle stages, ran 840M profiles/s,
+// this one 1,186M): n = l + 32 j, k = k1 + 8 k2 with l = a + 4 b, k2 = c + 8 d:
+//   Y[l][k1]   = DFT8_j z[l + 32 j] . W_256^{l k1}            (lane l)
+//   U[k1,a][c] = DFT8_b Y[a + 4 b][k1] . W_32^{a c}           (lane 4 k1 + a)
+//   Z[k1 + 8 c + 64 d] = DFT4_a U[k1,a][c]                     (lane 4 k1 + c / 2, two c)
+// then Z goes to shared memory, lane l separates bins l + 1 and l + 33 of both profiles from
+// Z[k], Z[256 - k], and the outputs are written contiguously.
+__global__ void __launch_bounds__(32 * kExtractWarps, 3)
+fft3_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out64, uint8_t *degenerate, float *prof_out) {
+    constexpr uint32_t W = 256;
     __shared__ double tc[W], ts[W];   // cos / sin of 2 pi j / W
+    __shared__ double zr[kExtractWarps][kZSlots], zi[kExtractWarps][kZSlots];
     for (uint32_t j = threadIdx.x; j < W; j += blockDim.x) {
         double sn, cs;
         sincospi(2.0 * (double)j / (double)W, &sn, &cs);
@@ -224,133 +264,131 @@ fft2_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out
         ts[j] = sn;
     }
     __syncthreads();
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t k2 = __brev(lane) >> 27;                       // this lane's DIF output
-    const uint32_t src0 = __brev((32u - k2) & 31u) >> 27;         // the lane holding Z[W - 8 k2]
+    const uint32_t lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    double *const br = zr[wi], *const bi = zi[wi];
+    const uint32_t k1 = lane >> 2, a = lane & 3;   // steps B and C: (k1, a) / (k1, c pair)
     const uint64_t pairs = (n + 1) / 2;
-    for (uint64_t pp = (uint64_t)blockIdx.x * kExtractWarps + (threadIdx.x >> 5); pp < pairs;
-         pp += (uint64_t)gridDim.x * kExtractWarps) {
+    for (uint64_t pp = (uint64_t)blockIdx.x * kExtractWarps + wi; pp < pairs; pp += (uint64_t)gridDim.x * kExtractWarps) {
         const uint64_t pa = 2 * pp, pb = pa + 1;
         const bool hasb = pb < n;
-        double re[R], im[R];
-        double sa = 0.0, sb = 0.0;   // (the profiles' sums, for the stored profiles' means)
-        int ea = 0, eb = 0;          // (the profiles' power-of-two scales)
-        {   // 8-point complex DFT of z_j = xa_j + i xb_j (radix 2: even / odd outputs)
-            double xa[R], xb[R];
+        double re[8], im[8];
+        double sa = 0.0, sb = 0.0;
+        int ea = 0, eb = 0;
+        {   // step A: lane l, the 8-point DFT over j of z[l + 32 j], twiddled
+            double xa[8], xb[8];
 #pragma unroll
-            for (int j = 0; j < (int)R; ++j) {
+            for (int j = 0; j < 8; ++j) {
                 xa[j] = __ldg(&prof[pa * W + lane + 32 * j]);
                 xb[j] = hasb ? __ldg(&prof[pb * W + lane + 32 * j]) : 0.0;
             }
             if (prof_out) {
 #pragma unroll
-                for (int j = 0; j < (int)R; ++j) { sa += xa[j]; sb += xb[j]; }
+                for (int j = 0; j < 8; ++j) { sa += xa[j]; sb += xb[j]; }
             }
             // each profile scaled by a power of two to max |x| in [1, 2): exact (all later
-            // operations scale exactly), so the descriptor is unchanged, and a dim profile
-            // is not drowned by the rounding of a bright partner's transform
-            // (the biased exponent field of the largest |x|: an integer warp max; 0 for zeros)
+            // operations scale exactly), so the descriptor is unchanged, and a dim profile is
+            // not drowned by the rounding of a bright partner's transform (the biased exponent
+            // field of the largest |x|: an integer warp max; 0 for zeros)
             uint32_t ga = 0, gb = 0;
 #pragma unroll
-            for (int j = 0; j < (int)R; ++j) {
+            for (int j = 0; j < 8; ++j) {
                 ga = max(ga, (uint32_t)(__double_as_longlong(xa[j]) >> 52) & 0x7ffu);
                 gb = max(gb, (uint32_t)(__double_as_longlong(xb[j]) >> 52) & 0x7ffu);
             }
             ga = __reduce_max_sync(0xffffffffu, ga);
             gb = __reduce_max_sync(0xffffffffu, gb);
-            ea = (ga > 1 && ga < 2046) ? (int)ga - 1023 : 0;   // (subnormal / huge ranges: unscaled)
+            ea = (ga > 1 && ga < 2046) ? (int)ga - 1023 : 0;
             eb = (gb > 1 && gb < 2046) ? (int)gb - 1023 : 0;
-            const double sca = __longlong_as_double((long long)(1023 - ea) << 52);   // 2^-ea, exact
+            const double sca = __longlong_as_double((long long)(1023 - ea) << 52);
             const double scb = __longlong_as_double((long long)(1023 - eb) << 52);
 #pragma unroll
-            for (int j = 0; j < (int)R; ++j) { xa[j] *= sca; xb[j] *= scb; }
-            constexpr double c = 0.70710678118654752440;   // cos(pi/4) = sin(pi/4), RN
-            double ar[4], ai[4], br[4], bi[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                ar[j] = xa[j] + xa[j + 4]; ai[j] = xb[j] + xb[j + 4];
-                br[j] = xa[j] - xa[j + 4]; bi[j] = xb[j] - xb[j + 4];
-            }
-            // even outputs: 4-point DFT of a
-            const double A0r = ar[0] + ar[2], A0i = ai[0] + ai[2], A2r = ar[0] - ar[2], A2i = ai[0] - ai[2];
-            const double A1r = ar[1] + ar[3], A1i = ai[1] + ai[3], A3r = ar[1] - ar[3], A3i = ai[1] - ai[3];
-            re[0] = A0r + A1r; im[0] = A0i + A1i;
-            re[4] = A0r - A1r; im[4] = A0i - A1i;
-            re[2] = A2r + A3i; im[2] = A2i - A3r;   // A2 - i A3
-            re[6] = A2r - A3i; im[6] = A2i + A3r;   // A2 + i A3
-            // odd outputs: t_j = b_j e^{-i pi j / 4}, then its 4-point DFT
-            const double t1r = c * (br[1] + bi[1]), t1i = c * (bi[1] - br[1]);
-            const double t2r = bi[2], t2i = -br[2];
-            const double t3r = c * (bi[3] - br[3]), t3i = -c * (bi[3] + br[3]);
-            const double B0r = br[0] + t2r, B0i = bi[0] + t2i, B2r = br[0] - t2r, B2i = bi[0] - t2i;
-            const double B1r = t1r + t3r, B1i = t1i + t3i, B3r = t1r - t3r, B3i = t1i - t3i;
-            re[1] = B0r + B1r; im[1] = B0i + B1i;
-            re[5] = B0r - B1r; im[5] = B0i - B1i;
-            re[3] = B2r + B3i; im[3] = B2i - B3r;   // B2 - i B3
-            re[7] = B2r - B3i; im[7] = B2i + B3r;   // B2 + i B3
+            for (int j = 0; j < 8; ++j) { xa[j] *= sca; xb[j] *= scb; }
+            dft8(xa, xb, re, im);
         }
-        // twiddle e^{-2 pi i l k1 / W}
 #pragma unroll
-        for (int k1 = 1; k1 < (int)R; ++k1) {
-            const uint32_t t = (lane * (uint32_t)k1) % W;
+        for (int q = 1; q < 8; ++q) {   // W_256^{l q}
+            const uint32_t t = (lane * (uint32_t)q) & (W - 1);
             const double c = tc[t], sn = ts[t];
-            const double r = re[k1], i = im[k1];
-            re[k1] = fma(r, c, i * sn);
-            im[k1] = fma(i, c, -r * sn);
+            const double r = re[q], i = im[q];
+            re[q] = fma(r, c, i * sn);
+            im[q] = fma(i, c, -r * sn);
         }
-        // 32-point radix-2 DIF across the lanes (branch-free, as fft_extract_kernel)
+        __syncwarp();   // (the previous pair's readers of the buffer are done)
 #pragma unroll
-        for (int h = 16; h >= 1; h >>= 1) {
-            const bool lower = (lane & h) != 0;
-            const uint32_t e = (lane & (h - 1)) * (W / (2 * h));
-            const double c = lower ? tc[e] : 1.0, sn = lower ? ts[e] : 0.0;
-            const double sg = lower ? -1.0 : 1.0;
+        for (int q = 0; q < 8; ++q) { br[sw8(lane, q)] = re[q]; bi[sw8(lane, q)] = im[q]; }
+        __syncwarp();
+        {   // step B: lane (k1, a), the 8-point DFT over b of Y[a + 4 b][k1], twiddled by W_32^{a c}
+            double xr[8], xi[8];
 #pragma unroll
-            for (int k1 = 0; k1 < (int)R; ++k1) {
-                const double pr = __shfl_xor_sync(0xffffffffu, re[k1], h);
-                const double pi = __shfl_xor_sync(0xffffffffu, im[k1], h);
-                const double dr = fma(sg, re[k1], pr), di = fma(sg, im[k1], pi);
-                re[k1] = lower ? fma(dr, c, di * sn) : dr;
-                im[k1] = lower ? fma(di, c, -dr * sn) : di;
+            for (int b = 0; b < 8; ++b) { xr[b] = br[sw8(a + 4 * b, k1)]; xi[b] = bi[sw8(a + 4 * b, k1)]; }
+            dft8(xr, xi, re, im);
+        }
+#pragma unroll
+        for (int c = 1; c < 8; ++c) {
+            const uint32_t t = (8u * a * (uint32_t)c) & (W - 1);
+            const double cs = tc[t], sn = ts[t];
+            const double r = re[c], i = im[c];
+            re[c] = fma(r, cs, i * sn);
+            im[c] = fma(i, cs, -r * sn);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 8; ++c) { br[sw8(lane, c)] = re[c]; bi[sw8(lane, c)] = im[c]; }
+        __syncwarp();
+        {   // step C: lane (k1, cp), the 4-point DFTs over a of U[k1, a][c], c = 2 cp, 2 cp + 1
+            const uint32_t cp = a;
+            double ur[2][4], ui[2][4];
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+#pragma unroll
+                for (int aa = 0; aa < 4; ++aa) {
+                    ur[e][aa] = br[sw8(4 * k1 + aa, 2 * cp + e)];
+                    ui[e][aa] = bi[sw8(4 * k1 + aa, 2 * cp + e)];
+                }
+            __syncwarp();
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double x0r = ur[e][0] + ur[e][2], x0i = ui[e][0] + ui[e][2];
+                const double x1r = ur[e][0] - ur[e][2], x1i = ui[e][0] - ui[e][2];
+                const double x2r = ur[e][1] + ur[e][3], x2i = ui[e][1] + ui[e][3];
+                const double x3r = ur[e][1] - ur[e][3], x3i = ui[e][1] - ui[e][3];
+                const uint32_t k = k1 + 8 * (2 * cp + e);
+                br[swz(k)] = x0r + x2r;         bi[swz(k)] = x0i + x2i;          // d = 0
+                br[swz(k + 128)] = x0r - x2r;   bi[swz(k + 128)] = x0i - x2i;    // d = 2
+                br[swz(k + 64)] = x1r + x3i;    bi[swz(k + 64)] = x1i - x3r;     // d = 1: X1 - i X3
+                br[swz(k + 192)] = x1r - x3i;   bi[swz(k + 192)] = x1i + x3r;    // d = 3: X1 + i X3
             }
         }
-        // separate: Z[W - k] for k = k1 + 8 k2 is (8 - k1) + 8 (31 - k2) in lane l ^ 31 (k1 != 0),
-        // 8 ((32 - k2) mod 32) in lane src0 (k1 = 0); the magnitudes of bins 1..64
-        double ma[R], mb[R], n2a = 0.0, n2b = 0.0;
+        __syncwarp();
+        // separate bins k = lane + 1 and lane + 33: 2 A[k] = Z[k] + conj Z[W - k],
+        // 2 i B[k] = Z[k] - conj Z[W - k]
+        double ma[2], mb[2], n2a = 0.0, n2b = 0.0;
 #pragma unroll
-        for (int k1 = 0; k1 < (int)R; ++k1) {
-            const int m1 = k1 == 0 ? 0 : (int)R - k1;
-            const double qr = k1 == 0 ? __shfl_sync(0xffffffffu, re[0], src0) : __shfl_xor_sync(0xffffffffu, re[m1], 31);
-            const double qi = k1 == 0 ? __shfl_sync(0xffffffffu, im[0], src0) : __shfl_xor_sync(0xffffffffu, im[m1], 31);
-            const uint32_t k = (uint32_t)k1 + R * k2;
-            ma[k1] = mb[k1] = 0.0;
-            if (k >= 1 && k <= (uint32_t)kK) {
-                const double sr = re[k1] + qr, di = im[k1] - qi;   // 2 A[k]
-                const double si = im[k1] + qi, dr = re[k1] - qr;   // 2 i B[k] = (dr + i si): |.| = |2 B[k]|
-                ma[k1] = 0.5 * sqrt(sr * sr + di * di);
-                mb[k1] = 0.5 * sqrt(si * si + dr * dr);
-                n2a += ma[k1] * ma[k1];
-                n2b += mb[k1] * mb[k1];
-            }
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t k = lane + 1 + 32 * h, m = W - k;
+            const double zkr = br[swz(k)], zki = bi[swz(k)], zmr = br[swz(m)], zmi = bi[swz(m)];
+            const double sr = zkr + zmr, di = zki - zmi;
+            const double si = zki + zmi, dr = zkr - zmr;
+            ma[h] = 0.5 * sqrt(sr * sr + di * di);
+            mb[h] = 0.5 * sqrt(si * si + dr * dr);
+            n2a += ma[h] * ma[h];
+            n2b += mb[h] * mb[h];
         }
         for (int o = 16; o; o >>= 1) {
             n2a += __shfl_xor_sync(0xffffffffu, n2a, o);
             n2b += __shfl_xor_sync(0xffffffffu, n2b, o);
         }
         const double norma = sqrt(n2a), normb = sqrt(n2b);   // (of the scaled profiles)
-        const double una = __longlong_as_double((long long)(1023 + ea) << 52);   // 2^ea
+        const double una = __longlong_as_double((long long)(1023 + ea) << 52);
         const double unb = __longlong_as_double((long long)(1023 + eb) << 52);
         const bool dega = !(norma * una > 1e-12), degb = !(normb * unb > 1e-12);
         const double inva = dega ? 0.0 : 1.0 / norma, invb = degb ? 0.0 : 1.0 / normb;
 #pragma unroll
-        for (int k1 = 0; k1 < (int)R; ++k1) {
-            const uint32_t k = (uint32_t)k1 + R * k2;
-            if (k >= 1 && k <= (uint32_t)kK) {
-                const double ca = ma[k1] * inva, cb = mb[k1] * invb;
-                const uint64_t oa = pa * kK + (k - 1), ob = pb * kK + (k - 1);
-                if (out64) { out64[oa] = ca; if (hasb) out64[ob] = cb; }
-                if (out32) { out32[oa] = __double2float_rn(ca); if (hasb) out32[ob] = __double2float_rn(cb); }
-            }
+        for (int h = 0; h < 2; ++h) {
+            const double ca = ma[h] * inva, cb = mb[h] * invb;
+            const uint64_t oa = pa * kK + lane + 32 * h, ob = pb * kK + lane + 32 * h;
+            if (out64) { out64[oa] = ca; if (hasb) out64[ob] = cb; }
+            if (out32) { out32[oa] = __double2float_rn(ca); if (hasb) out32[ob] = __double2float_rn(cb); }
         }
         if (degenerate && lane == 0) { degenerate[pa] = dega ? 1 : 0; if (hasb) degenerate[pb] = degb ? 1 : 0; }
         if (prof_out) {   // NEXT-1 stored profiles: (x - mean) / ||m|| (the profiles re-read: L2)
@@ -361,7 +399,7 @@ fft2_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out
             const double meana = sa / (double)W, meanb = sb / (double)W;
             const double sca2 = __longlong_as_double((long long)(1023 - ea) << 52), scb2 = __longlong_as_double((long long)(1023 - eb) << 52);
 #pragma unroll
-            for (int j = 0; j < (int)R; ++j) {
+            for (int j = 0; j < 8; ++j) {
                 prof_out[pa * W + lane + 32 * j] = __double2float_rn((__ldg(&prof[pa * W + lane + 32 * j]) - meana) * (inva * sca2));
                 if (hasb) prof_out[pb * W + lane + 32 * j] = __double2float_rn((__ldg(&prof[pb * W + lane + 32 * j]) - meanb) * (invb * scb2));
             }
@@ -381,7 +419,7 @@ cudaError_t launch_extract(const double *prof, uint64_t n, uint32_t W, float *ou
         else if (W == 256) {   // two profiles per warp
             uint64_t b2 = ((n + 1) / 2 + kExtractWarps - 1) / kExtractWarps;
             if (b2 > 148 * 32) b2 = 148 * 32;
-            fft2_extract256_kernel<<<(unsigned)b2, 32 * kExtractWarps, 0, s>>>(prof, n, out32, out64, degenerate, prof_out);
+            fft3_extract256_kernel<<<(unsigned)b2, 32 * kExtractWarps, 0, s>>>(prof, n, out32, out64, degenerate, prof_out);
         }
         else fft_extract_kernel<16><<<(unsigned)blocks, 32 * kExtractWarps, 0, s>>>(prof, n, out32, out64, degenerate, prof_out);
         return cudaGetLastError();
