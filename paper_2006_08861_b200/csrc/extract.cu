@@ -255,13 +255,19 @@ constexpr uint32_t kZSlots = 256 + 4 * 16;
 __global__ void __launch_bounds__(32 * kExtractWarps, 3)
 fft3_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out64, uint8_t *degenerate, float *prof_out) {
     constexpr uint32_t W = 256;
-    __shared__ double tc[W], ts[W];   // cos / sin of 2 pi j / W
+    // twiddles laid out in the order the lanes read them (a table indexed by l q mod 256 put
+    // lanes of even q on the same banks: up to 8-way conflicts); the same sincospi values
+    //   twA[q][l] = W_256^{l q} (step A, lane l),  twB[c][a] = W_256^{8 a c} (step B)
+    __shared__ double2 twA[8][32], twB[8][4];
     __shared__ double zr[kExtractWarps][kZSlots], zi[kExtractWarps][kZSlots];
-    for (uint32_t j = threadIdx.x; j < W; j += blockDim.x) {
+    for (uint32_t j = threadIdx.x; j < 8 * 32 + 8 * 4; j += blockDim.x) {
+        const bool isA = j < 8 * 32;
+        const uint32_t jb = j - 8 * 32;
+        const uint32_t t = isA ? ((j & 31) * (j >> 5)) & (W - 1) : (8u * (jb & 3) * (jb >> 2)) & (W - 1);
         double sn, cs;
-        sincospi(2.0 * (double)j / (double)W, &sn, &cs);
-        tc[j] = cs;
-        ts[j] = sn;
+        sincospi(2.0 * (double)t / (double)W, &sn, &cs);
+        if (isA) twA[j >> 5][j & 31] = make_double2(cs, sn);
+        else twB[jb >> 2][jb & 3] = make_double2(cs, sn);
     }
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
@@ -271,6 +277,10 @@ fft3_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out
     for (uint64_t pp = (uint64_t)blockIdx.x * kExtractWarps + wi; pp < pairs; pp += (uint64_t)gridDim.x * kExtractWarps) {
         const uint64_t pa = 2 * pp, pb = pa + 1;
         const bool hasb = pb < n;
+        {   // the warp's next pair (4 KB contiguous: 128 B per lane) towards L2 while this one computes
+            const uint64_t nx = 2 * (pp + (uint64_t)gridDim.x * kExtractWarps) * W + 16ull * lane;
+            if (nx < n * W) asm volatile("prefetch.global.L2 [%0];" ::"l"(prof + nx));
+        }
         double re[8], im[8];
         double sa = 0.0, sb = 0.0;
         int ea = 0, eb = 0;
@@ -307,8 +317,8 @@ fft3_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out
         }
 #pragma unroll
         for (int q = 1; q < 8; ++q) {   // W_256^{l q}
-            const uint32_t t = (lane * (uint32_t)q) & (W - 1);
-            const double c = tc[t], sn = ts[t];
+            const double2 w = twA[q][lane];
+            const double c = w.x, sn = w.y;
             const double r = re[q], i = im[q];
             re[q] = fma(r, c, i * sn);
             im[q] = fma(i, c, -r * sn);
@@ -325,8 +335,8 @@ fft3_extract256_kernel(const double *prof, uint64_t n, float *out32, double *out
         }
 #pragma unroll
         for (int c = 1; c < 8; ++c) {
-            const uint32_t t = (8u * a * (uint32_t)c) & (W - 1);
-            const double cs = tc[t], sn = ts[t];
+            const double2 w = twB[c][a];
+            const double cs = w.x, sn = w.y;
             const double r = re[c], i = im[c];
             re[c] = fma(r, cs, i * sn);
             im[c] = fma(i, cs, -r * sn);
